@@ -1,0 +1,189 @@
+/*
+ * klref_b200 — C-ABI of the B200-native hot path of the kl-refinement method
+ * (arXiv 2508.06049): matrix-free FMG on the hierarchical hybrid grid (HHG)
+ * plus the FMG-byproduct error estimator, as sm_100a CUDA kernels.
+ *
+ * The reference ships no C-ABI (proj/src/CMakeLists.txt:18 names a capi.cpp
+ * that is absent); its interface for this path is the C++ API of
+ * proj/include/klref/{hhg,fem,multigrid,estimator}.hpp.  Every entry point
+ * below names the reference function it replaces.  Conventions:
+ *   - plain pointers and sizes, opaque handles, no torch / CUDA types;
+ *   - every function returns a status (KLREF_OK = 0) and never throws; the
+ *     message of the last failure on the calling thread is klref_last_error()
+ *     and the codes mirror proj/include/klref/errors.hpp:10-53;
+ *   - host arrays of grid functions use the reference layout: macro-major
+ *     (slot order = ascending active element id), each macro a triangular
+ *     lattice row-major in j, index j(n+1) - j(j-1)/2 + i
+ *     (proj/include/klref/hhg.hpp:13), interface copies included;
+ *   - there is no CPU fallback: without a CUDA device every compute entry
+ *     point fails with KLREF_ERR_CUDA.
+ */
+#ifndef KLREF_B200_H
+#define KLREF_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (proj/include/klref/errors.hpp) */
+#define KLREF_OK 0
+#define KLREF_ERR_STRUCTURAL 1 /* StructuralError */
+#define KLREF_ERR_DOMAIN 2     /* DomainError */
+#define KLREF_ERR_SOLVER 3     /* SolverError: see klref_last_error_residual() */
+#define KLREF_ERR_IO 4         /* IoError */
+#define KLREF_ERR_INTERNAL 5   /* InternalError */
+#define KLREF_ERR_RESOURCE 6   /* ResourceError: see klref_last_error_level() */
+#define KLREF_ERR_CUDA 7       /* CUDA runtime failure / no device */
+
+/* problem kinds (BASELINE.json configs; proj/src/problems.cpp:36-53) */
+#define KLREF_PROBLEM_ZERO 0
+#define KLREF_PROBLEM_SIN2D 1  /* u = sin(pi x) sin(pi y), f = 2 pi^2 u     (config 1) */
+#define KLREF_PROBLEM_LSHAPE 2 /* make_lshape_spec: f = 0, g = r^2/3 sin(2t/3) (config 2) */
+
+/* operator kinds (OperatorKind, proj/include/klref/fem.hpp:13) */
+#define KLREF_STIFFNESS 0
+#define KLREF_MASS 1
+
+/* estimator kinds (EstimatorKind, proj/include/klref/estimator.hpp:10) */
+#define KLREF_UNSCALED 0
+#define KLREF_SCALED 1
+
+/* sync modes (SyncMode, proj/include/klref/hhg.hpp:16) */
+#define KLREF_SYNC_REPLACE 0
+#define KLREF_SYNC_ADDITIVE 1
+
+/* FmgState components */
+#define KLREF_STATE_U 0 /* u[l], l = 0..L */
+#define KLREF_STATE_B 1 /* b[l], l = 0..L */
+#define KLREF_STATE_W 2 /* w[l-1] = P u[l-1], lives on level l = 1..L */
+
+/* marking rules for klref_mark (proj/src/amr.cpp:41-68, BASELINE.json configs 2/4) */
+#define KLREF_MARK_TOP_FRACTION 0
+#define KLREF_MARK_HALF_MAX 1
+
+typedef struct klref_mesh_s* klref_mesh;
+typedef struct klref_hierarchy_s* klref_hierarchy;
+typedef struct klref_problem_s* klref_problem;
+typedef struct klref_solver_s* klref_solver;
+typedef struct klref_gf_s* klref_gf;
+
+/* SolverConfig, proj/include/klref/multigrid.hpp:19-29 (finest_policy: 0 = None) */
+typedef struct {
+  int nu;
+  int pre_smooth;
+  int post_smooth;
+  double coarse_rel_tol;
+  double coarse_abs_floor;
+  int coarse_max_iter;
+  int finest_policy;
+  int faithful_source; /* 1: host-tabulated f (bitwise-faithful RHS); 0: device-evaluated f */
+  int use_graph;       /* 1: replay the FMG as one CUDA graph */
+} klref_solver_config;
+
+/* EstimateReport, proj/include/klref/estimator.hpp:15-24 (eta_local returned separately) */
+typedef struct {
+  int offset;
+  int base_level;
+  int kind;
+  double norm_coarser;
+  double norm_base;
+  double conv_factor;
+  double eta;
+} klref_estimate_report;
+
+/* ---- errors ---------------------------------------------------------- */
+const char* klref_last_error(void);
+double klref_last_error_residual(void); /* SolverError::last_residual */
+int klref_last_error_level(void);       /* ResourceError::level */
+int klref_abi_version(void);
+
+/* ---- coarse mesh ------------------------------------------------------ */
+/* Conforming macro mesh in slot order (MacroMesh::create,
+ * proj/src/macro_mesh.cpp:115-204, restricted to what the hot path reads):
+ * coords[dim * num_vertices], corners[(dim + 1) * num_elements] (vertex ids);
+ * elements are oriented positively as the reference does. */
+int klref_mesh_create(int dim, int num_vertices, const double* coords, int num_elements,
+                      const int* corners, klref_mesh* out);
+void klref_mesh_destroy(klref_mesh mesh);
+
+/* ---- hierarchy -------------------------------------------------------- */
+/* GridHierarchy::build, proj/src/hhg.cpp:48-144 (+ device upload) */
+int klref_hierarchy_build(klref_mesh mesh, int max_level, klref_hierarchy* out);
+/* host-only build (no device memory touched): tables for CPU tests */
+int klref_hierarchy_build_host(klref_mesh mesh, int max_level, klref_hierarchy* out);
+void klref_hierarchy_destroy(klref_hierarchy h);
+int klref_hierarchy_num_macros(klref_hierarchy h, int* out);            /* num_macros() */
+int klref_hierarchy_max_level(klref_hierarchy h, int* out);             /* max_level() */
+int klref_hierarchy_dof_count(klref_hierarchy h, int level, int64_t* out); /* dof_count(l) */
+int klref_hierarchy_fine_element_count(klref_hierarchy h, int level, int64_t* out);
+int klref_hierarchy_lattice_size(klref_hierarchy h, int level, int* out); /* lattice_size(2^l) */
+int klref_hierarchy_dag_depth(klref_hierarchy h, int* out);
+/* Level(l).groups (proj/include/klref/hhg.hpp:19-27): ptr[num_groups + 1],
+ * members[4 * num_members] = (slot, idx, i, j).  Pass NULL to query sizes. */
+int klref_hierarchy_groups(klref_hierarchy h, int level, int* num_groups, int* num_members, int* ptr,
+                           int* members);
+/* OperatorP1::matrices/stencil (proj/include/klref/fem.hpp:30-37): mats[18 * M]
+ * (up, down per macro), stencil[7 * M] (stiffness only; may be NULL) */
+int klref_hierarchy_element_matrices(klref_hierarchy h, int level, int kind, double* mats, double* stencil);
+
+/* ---- problems --------------------------------------------------------- */
+int klref_problem_create(int kind, klref_problem* out);
+/* ProblemSpec with host callbacks (proj/include/klref/fem.hpp:55-64); f is
+ * tabulated on the host at the quadrature points (bitwise-faithful RHS). */
+int klref_problem_create_host(double (*source)(double, double, void*), double (*boundary)(double, double, void*),
+                              void* ctx, klref_problem* out);
+void klref_problem_destroy(klref_problem p);
+
+/* ---- solver ----------------------------------------------------------- */
+void klref_solver_config_default(klref_solver_config* cfg);
+/* MultigridSolver(h, p, cfg), proj/src/multigrid.cpp:113-119 */
+int klref_solver_create(klref_hierarchy h, klref_problem p, const klref_solver_config* cfg, klref_solver* out);
+void klref_solver_destroy(klref_solver s);
+/* MultigridSolver::fmg, proj/src/multigrid.cpp:248-321 (state kept device-resident in the solver) */
+int klref_solver_fmg(klref_solver s);
+/* asynchronous variant + completion (error status is checked by synchronize) */
+int klref_solver_fmg_enqueue(klref_solver s);
+int klref_solver_synchronize(klref_solver s);
+/* the cudaStream_t the solver launches on (for event timing), as void* */
+int klref_solver_stream(klref_solver s, void** stream);
+/* number of kernel launches one FMG enqueues (graph nodes that are kernels/memsets) */
+int klref_solver_launch_count(klref_solver s, int* out);
+int klref_solver_last_cg_iterations(klref_solver s, int* out);
+/* FmgState::u/b/w (proj/include/klref/multigrid.hpp:43-53), copied to the host */
+int klref_solver_state_read(klref_solver s, int which, int level, double* host_out);
+
+/* error_estimate(state, j, kind), proj/src/estimator.cpp:8-45; eta_local[M] may be NULL */
+int klref_error_estimate(klref_solver s, int offset, int kind, klref_estimate_report* out, double* eta_local);
+int klref_error_estimate_enqueue(klref_solver s, int offset);
+int klref_error_estimate_finish(klref_solver s, int offset, int kind, klref_estimate_report* out,
+                                double* eta_local);
+
+/* ---- device grid functions and single operations ---------------------- */
+int klref_gf_create(klref_hierarchy h, int level, klref_gf* out); /* create_function(l) (zeros) */
+void klref_gf_destroy(klref_gf f);
+int klref_gf_upload(klref_gf f, const double* host);
+int klref_gf_download(klref_gf f, double* host);
+int klref_apply(klref_solver s, int kind, klref_gf x, klref_gf y);            /* OperatorP1::apply   fem.cpp:95 */
+int klref_residual(klref_solver s, klref_gf u, klref_gf b, klref_gf r);       /* residual      multigrid.cpp:183 */
+int klref_gauss_seidel(klref_solver s, klref_gf u, klref_gf b, int sweeps);   /* gauss_seidel  multigrid.cpp:127 */
+int klref_restrict_transpose(klref_solver s, klref_gf fine, klref_gf coarse); /* multigrid.cpp:55 */
+int klref_prolongate(klref_solver s, klref_gf coarse, klref_gf fine);         /* multigrid.cpp:22 */
+int klref_cg_level0(klref_solver s, klref_gf u, klref_gf b);                  /* cg_level0     multigrid.cpp:198 */
+int klref_dot_unique(klref_solver s, klref_gf a, klref_gf b, double* out);    /* hhg.cpp:227 */
+int klref_interface_sync(klref_solver s, klref_gf f, int mode);               /* hhg.cpp:206 */
+
+/* ---- host marking (mark_and_refine's reversion aggregate + rule) ------ */
+/* proj/src/amr.cpp:41-66 and mark_top_fraction proj/src/macro_mesh.cpp:678-695.
+ * active_ids[num_active] with green_parent[num_active] (-1 if not a green child),
+ * indicator[num_active]; reverted_ids[num_reverted] = active ids after revert_green.
+ * marks_out[num_reverted] receives the sorted marked ids, *num_marks their count. */
+int klref_mark(int rule, double fraction, int num_active, const int* active_ids, const int* green_parent,
+               const double* indicator, int num_reverted, const int* reverted_ids, int* marks_out, int* num_marks);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KLREF_B200_H */

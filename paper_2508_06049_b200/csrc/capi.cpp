@@ -1,0 +1,512 @@
+// extern "C" boundary of libklref_b200.so (include/klref_b200.h).  Converts
+// the internal C++ exceptions (kb::Error, mirroring the reference's
+// errors.hpp) into status codes plus a thread-local message.
+#include "../../include/klref_b200.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <new>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "solver2d.hpp"
+
+struct klref_mesh_s {
+  int dim = 2;
+  kb::Mesh2D mesh;
+};
+struct klref_hierarchy_s {
+  std::shared_ptr<kb::DeviceHierarchy2D> dev;  // lev empty for host-only builds
+  bool on_device = false;
+};
+struct klref_problem_s {
+  kb::Problem2D p;
+};
+struct klref_solver_s {
+  std::unique_ptr<kb::Solver2D> s;
+  klref_hierarchy_s* h = nullptr;
+};
+struct klref_gf_s {
+  double* d = nullptr;
+  size_t count = 0;
+  int level = 0;
+  klref_hierarchy_s* h = nullptr;
+};
+
+namespace {
+
+thread_local std::string g_msg;
+thread_local double g_residual = 0.0;
+thread_local int g_level = -1;
+
+int set_error(int code, const std::string& msg, double residual = 0.0, int level = -1) {
+  g_msg = msg;
+  g_residual = residual;
+  g_level = level;
+  return code;
+}
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return KLREF_OK;
+  } catch (const kb::Error& e) {
+    return set_error(e.code, e.what(), e.residual, e.level);
+  } catch (const std::bad_alloc&) {
+    return set_error(KLREF_ERR_RESOURCE, "host allocation failed");
+  } catch (const std::exception& e) {
+    return set_error(KLREF_ERR_INTERNAL, e.what());
+  }
+}
+
+void require_device() {
+  int count = 0;
+  const cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0)
+    kb::fail(kb::KB_CUDA, std::string("no CUDA device available (the hot path has no CPU fallback): ") +
+                              (e != cudaSuccess ? cudaGetErrorString(e) : "0 devices"));
+}
+
+void need(const void* p, const char* what) {
+  if (!p) kb::fail(kb::KB_STRUCTURAL, std::string("null argument: ") + what);
+}
+
+const kb::Hierarchy2D& host_of(klref_hierarchy h) { return h->dev->host; }
+
+void check_level(klref_hierarchy h, int level) {
+  if (level < 0 || level > host_of(h).L) kb::fail(kb::KB_STRUCTURAL, "level out of range");
+}
+
+void same_hier(klref_solver s, klref_gf f) {
+  need(f, "grid function");
+  if (f->h != s->h) kb::fail(kb::KB_STRUCTURAL, "grid function belongs to another hierarchy");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* klref_last_error(void) { return g_msg.c_str(); }
+double klref_last_error_residual(void) { return g_residual; }
+int klref_last_error_level(void) { return g_level; }
+int klref_abi_version(void) { return 1; }
+
+int klref_mesh_create(int dim, int num_vertices, const double* coords, int num_elements, const int* corners,
+                      klref_mesh* out) {
+  return guarded([&] {
+    need(coords, "coords");
+    need(corners, "corners");
+    need(out, "out");
+    if (dim != 2) kb::fail(kb::KB_STRUCTURAL, "grid hierarchies are only available for 2-d macro meshes");
+    auto m = std::make_unique<klref_mesh_s>();
+    m->dim = dim;
+    m->mesh = kb::Mesh2D::create(num_vertices, coords, num_elements, corners);
+    *out = m.release();
+  });
+}
+
+void klref_mesh_destroy(klref_mesh mesh) { delete mesh; }
+
+static int build_impl(klref_mesh mesh, int max_level, klref_hierarchy* out, bool device) {
+  return guarded([&] {
+    need(mesh, "mesh");
+    need(out, "out");
+    auto h = std::make_unique<klref_hierarchy_s>();
+    if (device) {
+      require_device();
+      h->dev = kb::DeviceHierarchy2D::create(mesh->mesh, max_level);
+      h->on_device = true;
+    } else {
+      h->dev = std::make_shared<kb::DeviceHierarchy2D>();
+      h->dev->host = kb::Hierarchy2D::build(mesh->mesh, max_level);
+    }
+    *out = h.release();
+  });
+}
+
+int klref_hierarchy_build(klref_mesh mesh, int max_level, klref_hierarchy* out) {
+  return build_impl(mesh, max_level, out, true);
+}
+int klref_hierarchy_build_host(klref_mesh mesh, int max_level, klref_hierarchy* out) {
+  return build_impl(mesh, max_level, out, false);
+}
+void klref_hierarchy_destroy(klref_hierarchy h) { delete h; }
+
+int klref_hierarchy_num_macros(klref_hierarchy h, int* out) {
+  return guarded([&] {
+    need(h, "h");
+    *out = host_of(h).M;
+  });
+}
+int klref_hierarchy_max_level(klref_hierarchy h, int* out) {
+  return guarded([&] {
+    need(h, "h");
+    *out = host_of(h).L;
+  });
+}
+int klref_hierarchy_dof_count(klref_hierarchy h, int level, int64_t* out) {
+  return guarded([&] {
+    need(h, "h");
+    check_level(h, level);
+    *out = host_of(h).levels[level].dofs;
+  });
+}
+int klref_hierarchy_fine_element_count(klref_hierarchy h, int level, int64_t* out) {
+  return guarded([&] {
+    need(h, "h");
+    *out = static_cast<int64_t>(host_of(h).M) << (2 * level);
+  });
+}
+int klref_hierarchy_lattice_size(klref_hierarchy h, int level, int* out) {
+  return guarded([&] {
+    need(h, "h");
+    check_level(h, level);
+    *out = host_of(h).levels[level].S;
+  });
+}
+int klref_hierarchy_dag_depth(klref_hierarchy h, int* out) {
+  return guarded([&] {
+    need(h, "h");
+    *out = host_of(h).dag_depth;
+  });
+}
+int klref_hierarchy_groups(klref_hierarchy h, int level, int* num_groups, int* num_members, int* ptr,
+                           int* members) {
+  return guarded([&] {
+    need(h, "h");
+    check_level(h, level);
+    const kb::Level2D& lv = host_of(h).levels[level];
+    if (num_groups) *num_groups = static_cast<int>(lv.grp_ptr.size()) - 1;
+    if (num_members) *num_members = static_cast<int>(lv.mem_slot.size());
+    if (ptr) std::copy(lv.grp_ptr.begin(), lv.grp_ptr.end(), ptr);
+    if (members)
+      for (size_t k = 0; k < lv.mem_slot.size(); ++k) {
+        members[4 * k] = lv.mem_slot[k];
+        members[4 * k + 1] = lv.mem_idx[k];
+        members[4 * k + 2] = lv.mem_i[k];
+        members[4 * k + 3] = lv.mem_j[k];
+      }
+  });
+}
+int klref_hierarchy_element_matrices(klref_hierarchy h, int level, int kind, double* mats, double* stencil) {
+  return guarded([&] {
+    need(h, "h");
+    check_level(h, level);
+    const kb::Level2D& lv = host_of(h).levels[level];
+    if (mats) {
+      const auto& src = kind == KLREF_MASS ? lv.kmass : lv.kstiff;
+      std::copy(src.begin(), src.end(), mats);
+    }
+    if (stencil) std::copy(lv.stencil.begin(), lv.stencil.end(), stencil);
+  });
+}
+
+int klref_problem_create(int kind, klref_problem* out) {
+  return guarded([&] {
+    need(out, "out");
+    auto p = std::make_unique<klref_problem_s>();
+    p->p = kb::Problem2D::builtin(kind);
+    *out = p.release();
+  });
+}
+
+int klref_problem_create_host(double (*source)(double, double, void*), double (*boundary)(double, double, void*),
+                              void* ctx, klref_problem* out) {
+  return guarded([&] {
+    need(out, "out");
+    need(reinterpret_cast<const void*>(source), "source");
+    need(reinterpret_cast<const void*>(boundary), "boundary");
+    auto p = std::make_unique<klref_problem_s>();
+    p->p.kind = kb::PROB_HOST;
+    p->p.source = [source, ctx](double x, double y) { return source(x, y, ctx); };
+    p->p.boundary = [boundary, ctx](double x, double y) { return boundary(x, y, ctx); };
+    p->p.has_exact = false;
+    *out = p.release();
+  });
+}
+void klref_problem_destroy(klref_problem p) { delete p; }
+
+void klref_solver_config_default(klref_solver_config* cfg) {
+  if (!cfg) return;
+  cfg->nu = 2;
+  cfg->pre_smooth = 2;
+  cfg->post_smooth = 2;
+  cfg->coarse_rel_tol = 1e-9;
+  cfg->coarse_abs_floor = 1e-12;
+  cfg->coarse_max_iter = 100000;
+  cfg->finest_policy = 0;
+  cfg->faithful_source = 0;
+  cfg->use_graph = 1;
+}
+
+int klref_solver_create(klref_hierarchy h, klref_problem p, const klref_solver_config* cfg, klref_solver* out) {
+  return guarded([&] {
+    need(h, "h");
+    need(p, "problem");
+    need(out, "out");
+    require_device();
+    if (!h->on_device) kb::fail(kb::KB_STRUCTURAL, "hierarchy was built host-only");
+    kb::SolverConfig2D c;
+    if (cfg) {
+      c.nu = cfg->nu;
+      c.pre_smooth = cfg->pre_smooth;
+      c.post_smooth = cfg->post_smooth;
+      c.coarse_rel_tol = cfg->coarse_rel_tol;
+      c.coarse_abs_floor = cfg->coarse_abs_floor;
+      c.coarse_max_iter = cfg->coarse_max_iter;
+      c.finest_policy = cfg->finest_policy;
+      c.faithful_source = cfg->faithful_source;
+      c.use_graph = cfg->use_graph;
+    }
+    auto s = std::make_unique<klref_solver_s>();
+    s->s = std::make_unique<kb::Solver2D>(h->dev, p->p, c);
+    s->h = h;
+    *out = s.release();
+  });
+}
+void klref_solver_destroy(klref_solver s) { delete s; }
+
+int klref_solver_fmg(klref_solver s) {
+  return guarded([&] {
+    need(s, "solver");
+    s->s->fmg();
+  });
+}
+int klref_solver_fmg_enqueue(klref_solver s) {
+  return guarded([&] {
+    need(s, "solver");
+    s->s->fmg_enqueue();
+  });
+}
+int klref_solver_synchronize(klref_solver s) {
+  return guarded([&] {
+    need(s, "solver");
+    s->s->sync_and_check();
+  });
+}
+int klref_solver_stream(klref_solver s, void** stream) {
+  return guarded([&] {
+    need(s, "solver");
+    *stream = reinterpret_cast<void*>(s->s->stream());
+  });
+}
+int klref_solver_launch_count(klref_solver s, int* out) {
+  return guarded([&] {
+    need(s, "solver");
+    *out = s->s->launches_per_fmg();
+  });
+}
+int klref_solver_last_cg_iterations(klref_solver s, int* out) {
+  return guarded([&] {
+    need(s, "solver");
+    *out = s->s->last_cg_iters();
+  });
+}
+int klref_solver_state_read(klref_solver s, int which, int level, double* host_out) {
+  return guarded([&] {
+    need(s, "solver");
+    need(host_out, "host_out");
+    const double* d = s->s->state(which, level);
+    const size_t count = s->s->level_size(level);
+    KB_CUDA_CHECK(cudaMemcpyAsync(host_out, d, count * 8, cudaMemcpyDeviceToHost, s->s->stream()));
+    KB_CUDA_CHECK(cudaStreamSynchronize(s->s->stream()));
+  });
+}
+
+static void fill_report(const kb::EstimateReport2D& r, klref_estimate_report* out, double* eta_local) {
+  if (out) {
+    out->offset = r.offset;
+    out->base_level = r.base_level;
+    out->kind = r.kind;
+    out->norm_coarser = r.norm_coarser;
+    out->norm_base = r.norm_base;
+    out->conv_factor = r.conv_factor;
+    out->eta = r.eta;
+  }
+  if (eta_local) std::copy(r.eta_local.begin(), r.eta_local.end(), eta_local);
+}
+
+int klref_error_estimate(klref_solver s, int offset, int kind, klref_estimate_report* out, double* eta_local) {
+  return guarded([&] {
+    need(s, "solver");
+    fill_report(s->s->estimate(offset, kind), out, eta_local);
+  });
+}
+int klref_error_estimate_enqueue(klref_solver s, int offset) {
+  return guarded([&] {
+    need(s, "solver");
+    s->s->estimate_enqueue(offset);
+  });
+}
+int klref_error_estimate_finish(klref_solver s, int offset, int kind, klref_estimate_report* out,
+                                double* eta_local) {
+  return guarded([&] {
+    need(s, "solver");
+    fill_report(s->s->estimate_finish(offset, kind), out, eta_local);
+  });
+}
+
+int klref_gf_create(klref_hierarchy h, int level, klref_gf* out) {
+  return guarded([&] {
+    need(h, "h");
+    need(out, "out");
+    require_device();
+    check_level(h, level);
+    auto f = std::make_unique<klref_gf_s>();
+    f->count = static_cast<size_t>(host_of(h).M) * host_of(h).levels[level].S;
+    f->level = level;
+    f->h = h;
+    KB_CUDA_CHECK(cudaMalloc(&f->d, f->count * 8));
+    KB_CUDA_CHECK(cudaMemset(f->d, 0, f->count * 8));
+    *out = f.release();
+  });
+}
+void klref_gf_destroy(klref_gf f) {
+  if (!f) return;
+  if (f->d) cudaFree(f->d);
+  delete f;
+}
+int klref_gf_upload(klref_gf f, const double* host) {
+  return guarded([&] {
+    need(f, "f");
+    need(host, "host");
+    KB_CUDA_CHECK(cudaMemcpy(f->d, host, f->count * 8, cudaMemcpyHostToDevice));
+  });
+}
+int klref_gf_download(klref_gf f, double* host) {
+  return guarded([&] {
+    need(f, "f");
+    need(host, "host");
+    KB_CUDA_CHECK(cudaMemcpy(host, f->d, f->count * 8, cudaMemcpyDeviceToHost));
+  });
+}
+
+int klref_apply(klref_solver s, int kind, klref_gf x, klref_gf y) {
+  return guarded([&] {
+    need(s, "solver");
+    same_hier(s, x);
+    same_hier(s, y);
+    if (x->level != y->level) kb::fail(kb::KB_STRUCTURAL, "operator level mismatch");
+    s->s->apply(x->level, kind == KLREF_MASS, x->d, y->d);
+  });
+}
+int klref_residual(klref_solver s, klref_gf u, klref_gf b, klref_gf r) {
+  return guarded([&] {
+    need(s, "solver");
+    same_hier(s, u);
+    same_hier(s, b);
+    same_hier(s, r);
+    if (u->level != b->level || u->level != r->level) kb::fail(kb::KB_STRUCTURAL, "grid function level mismatch");
+    s->s->residual(u->level, u->d, b->d, r->d);
+  });
+}
+int klref_gauss_seidel(klref_solver s, klref_gf u, klref_gf b, int sweeps) {
+  return guarded([&] {
+    need(s, "solver");
+    same_hier(s, u);
+    same_hier(s, b);
+    if (u->level != b->level) kb::fail(kb::KB_STRUCTURAL, "grid function level mismatch");
+    s->s->gauss_seidel(u->level, u->d, b->d, sweeps);
+  });
+}
+int klref_restrict_transpose(klref_solver s, klref_gf fine, klref_gf coarse) {
+  return guarded([&] {
+    need(s, "solver");
+    same_hier(s, fine);
+    same_hier(s, coarse);
+    if (coarse->level + 1 != fine->level) kb::fail(kb::KB_STRUCTURAL, "restriction level mismatch");
+    s->s->restrict_to(fine->level, fine->d, coarse->d);
+  });
+}
+int klref_prolongate(klref_solver s, klref_gf coarse, klref_gf fine) {
+  return guarded([&] {
+    need(s, "solver");
+    same_hier(s, fine);
+    same_hier(s, coarse);
+    if (coarse->level + 1 != fine->level) kb::fail(kb::KB_STRUCTURAL, "prolongation level mismatch");
+    s->s->prolongate(coarse->level, coarse->d, fine->d);
+  });
+}
+int klref_cg_level0(klref_solver s, klref_gf u, klref_gf b) {
+  return guarded([&] {
+    need(s, "solver");
+    same_hier(s, u);
+    same_hier(s, b);
+    if (u->level != 0 || b->level != 0) kb::fail(kb::KB_STRUCTURAL, "cg_level0 works on level 0");
+    s->s->cg_level0(u->d, b->d);
+  });
+}
+int klref_dot_unique(klref_solver s, klref_gf a, klref_gf b, double* out) {
+  return guarded([&] {
+    need(s, "solver");
+    same_hier(s, a);
+    same_hier(s, b);
+    need(out, "out");
+    if (a->level != b->level) kb::fail(kb::KB_STRUCTURAL, "grid function level mismatch");
+    *out = s->s->dot_unique(a->level, a->d, b->d);
+  });
+}
+int klref_interface_sync(klref_solver s, klref_gf f, int mode) {
+  return guarded([&] {
+    need(s, "solver");
+    same_hier(s, f);
+    s->s->interface_sync(f->level, f->d, mode == KLREF_SYNC_ADDITIVE);
+  });
+}
+
+int klref_mark(int rule, double fraction, int num_active, const int* active_ids, const int* green_parent,
+               const double* indicator, int num_reverted, const int* reverted_ids, int* marks_out, int* num_marks) {
+  return guarded([&] {
+    need(active_ids, "active_ids");
+    need(indicator, "indicator");
+    need(reverted_ids, "reverted_ids");
+    need(marks_out, "marks_out");
+    need(num_marks, "num_marks");
+    // aggregation on the green-reverted set, proj/src/amr.cpp:45-65
+    std::map<int, double> by_id;
+    for (int t = 0; t < num_active; ++t) by_id[active_ids[t]] = indicator[t];
+    std::vector<double> agg(num_reverted, 0.0);
+    for (int t = 0; t < num_reverted; ++t) {
+      const int id = reverted_ids[t];
+      auto it = by_id.find(id);
+      if (it != by_id.end()) {
+        agg[t] = it->second;
+        continue;
+      }
+      double sq = 0.0;
+      for (int a = 0; a < num_active; ++a)
+        if (green_parent && green_parent[a] == id) sq += indicator[a] * indicator[a];
+      agg[t] = std::sqrt(sq);
+    }
+    std::vector<int> marks;
+    if (rule == KLREF_MARK_TOP_FRACTION) {
+      // mark_top_fraction, proj/src/macro_mesh.cpp:678-695
+      if (!(fraction > 0.0) || fraction > 1.0) kb::fail(kb::KB_STRUCTURAL, "mark fraction must be in (0, 1]");
+      const size_t count = static_cast<size_t>(std::ceil(fraction * static_cast<double>(num_reverted)));
+      std::vector<size_t> order(num_reverted);
+      std::iota(order.begin(), order.end(), 0);
+      std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) {
+        if (agg[a] != agg[b]) return agg[a] > agg[b];
+        return reverted_ids[a] < reverted_ids[b];
+      });
+      for (size_t i = 0; i < count; ++i) marks.push_back(reverted_ids[order[i]]);
+    } else if (rule == KLREF_MARK_HALF_MAX) {
+      double mx = 0.0;
+      for (double v : agg) mx = std::max(mx, v);
+      for (int t = 0; t < num_reverted; ++t)
+        if (agg[t] >= 0.5 * mx) marks.push_back(reverted_ids[t]);
+    } else {
+      kb::fail(kb::KB_STRUCTURAL, "unknown marking rule");
+    }
+    std::sort(marks.begin(), marks.end());
+    std::copy(marks.begin(), marks.end(), marks_out);
+    *num_marks = static_cast<int>(marks.size());
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,91 @@
+// Device-side views of the 2-d HHG tables and the kernel launch API
+// (implemented in kernels2d.cu).  Everything is fp64; grid functions are
+// stored macro-major with interface copies, each macro in the reference's
+// row-major lattice order (proj/include/klref/hhg.hpp:13, :33-53), so a
+// level-l function is one contiguous array of M * S_l doubles.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "hier2d.hpp"
+
+namespace kb {
+
+struct DevLevel2D {
+  int n, S, M;
+  const int* node_gid;
+  const std::uint8_t* node_flags;
+  const int* grp_ptr;
+  const int* mem_off;
+  const int* mem_ij;   // i | (j << 16)
+  const int* mem_slot;
+  const double* kstiff;
+  const double* kmass;
+  const double* stencil;
+  const double* inv_c;
+  const BNode* bnode;
+  const MemberRec* rec;
+  const int* wr;
+  const int* ghost_ptr;
+  const int* ghost_off;
+  int max_ghosts;
+  int num_groups;
+  const int* dot_order;
+  int dot_count;
+  const double* geo;   // per macro: c0x, c0y, ux, uy, wx, wy (RHS quadrature map, proj/src/fem.cpp:183-186)
+  const double* wq;    // per macro: cell_area / 3
+};
+
+struct DevHier2D {
+  int M, L;
+  const int* nb_lo_ptr;
+  const int* nb_lo;
+  const int* nb_hi_ptr;
+  const int* nb_hi;
+};
+
+enum ApplyMode : int { APPLY_PLAIN = 0, APPLY_RESIDUAL = 1, APPLY_ZERO_BND = 2 };
+enum ProlongMode : int { PROLONG_ASSIGN = 0, PROLONG_ADD = 1, PROLONG_W_NEXT = 2 };
+
+// Device problem descriptor for the source term (fast mode); faithful mode
+// passes a host-tabulated f instead (RHS).
+enum SourceKind : int { SRC_ZERO = 0, SRC_TABLE = 1, SRC_SIN2D = 2 };
+
+struct CgParams {
+  double rel_tol, abs_floor;
+  int max_iter;
+};
+
+// status word written by device code (level-0 CG failures)
+struct DevStatus {
+  int code;       // 0 ok, 1 not converged, 2 lost positive definiteness
+  int iters;
+  double residual;
+};
+
+// y = Op x (+ residual / boundary modes); K = kstiff or kmass of the level
+void launch_apply(const DevLevel2D& lv, const double* K, const double* x, double* y, const double* b,
+                  int mode, cudaStream_t st);
+void launch_restrict(const DevLevel2D& fine, const DevLevel2D& coarse, const double* r, double* rc,
+                     int zero_boundary, cudaStream_t st);
+void launch_prolong(const DevLevel2D& coarse, const DevLevel2D& fine, const double* c, double* f,
+                    double* next, const double* gbnd, int mode, cudaStream_t st);
+void launch_set_boundary(const DevLevel2D& lv, double* f, const double* gbnd, int zero_rest,
+                         cudaStream_t st);
+void launch_rhs(const DevLevel2D& lv, int src_kind, const double* ftab, double* ftab_scratch,
+                const double* gbnd, double* b, cudaStream_t st);
+void launch_cg0(const DevLevel2D& lv0, double* u, const double* b, double* scratch, CgParams prm,
+                DevStatus* status, cudaStream_t st);
+void launch_gs(const DevHier2D& hd, const DevLevel2D& lv, double* u, const double* b, int sweeps,
+               int* done, cudaStream_t st);
+void launch_estimate(const DevLevel2D& lv, const double* uL, const double* wb, const double* wc,
+                     double* sums, cudaStream_t st);
+void launch_dot(const DevLevel2D& lv, const double* a, const double* b, double* partial,
+                double* out, cudaStream_t st);
+void launch_sync(const DevLevel2D& lv, double* f, int additive, cudaStream_t st);
+void launch_axpy(double* y, const double* x, double alpha, std::int64_t count, cudaStream_t st);
+int gs_block_threads(int n);
+
+}  // namespace kb

@@ -1,0 +1,434 @@
+// Host-side construction of the 2-d HHG tables.  See hier2d.hpp.
+#include "hier2d.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <map>
+#include <new>
+
+namespace kb {
+namespace {
+
+constexpr int kLocalEdges[3][2] = {{0, 1}, {0, 2}, {1, 2}};
+
+double signed_area(double ax, double ay, double bx, double by, double cx, double cy) {
+  return 0.5 * ((bx - ax) * (cy - ay) - (by - ay) * (cx - ax));
+}
+
+// P1 stiffness on one micro triangle; D1 fix: |area| (proj/src/fem.cpp:30-41).
+std::array<double, 9> stiffness_matrix(double p0x, double p0y, double p1x, double p1y, double p2x,
+                                       double p2y) {
+  const double area2 = (p1x - p0x) * (p2y - p0y) - (p1y - p0y) * (p2x - p0x);
+  const double area = 0.5 * std::fabs(area2);
+  const double gx[3] = {-(p2y - p1y) / area2, -(p0y - p2y) / area2, -(p1y - p0y) / area2};
+  const double gy[3] = {(p2x - p1x) / area2, (p0x - p2x) / area2, (p1x - p0x) / area2};
+  std::array<double, 9> k{};
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) k[3 * i + j] = area * (gx[i] * gx[j] + gy[i] * gy[j]);
+  return k;
+}
+
+std::array<double, 9> mass_matrix(double area) {
+  const double d = area / 6.0, o = area / 12.0;
+  return {d, o, o, o, d, o, o, o, d};
+}
+
+int edge_lattice_index(int n, int le, int t) {
+  switch (le) {
+    case 0: return lattice_index(n, t, 0);
+    case 1: return lattice_index(n, 0, t);
+    default: return lattice_index(n, n - t, t);
+  }
+}
+
+int direction_code(int di, int dj) {
+  if (di == 1 && dj == 0) return 0;    // E
+  if (di == -1 && dj == 0) return 1;   // W
+  if (di == 0 && dj == 1) return 2;    // N
+  if (di == 0 && dj == -1) return 3;   // S
+  if (di == -1 && dj == 1) return 4;   // NW
+  if (di == 1 && dj == -1) return 5;   // SE
+  return -1;
+}
+
+bool on_lattice_boundary(int n, int i, int j) { return i == 0 || j == 0 || i + j == n; }
+
+}  // namespace
+
+Mesh2D Mesh2D::create(int nv, const double* xy, int ne, const int* tri3) {
+  if (nv <= 0 || ne <= 0) fail(KB_STRUCTURAL, "mesh has no vertices or no elements");
+  Mesh2D m;
+  m.x.resize(nv);
+  m.y.resize(nv);
+  for (int v = 0; v < nv; ++v) {
+    m.x[v] = xy[2 * v];
+    m.y[v] = xy[2 * v + 1];
+    if (!std::isfinite(m.x[v]) || !std::isfinite(m.y[v]))
+      fail(KB_STRUCTURAL, "vertex coordinates must be finite");
+  }
+  m.tri.resize(ne);
+  m.area.resize(ne);
+  std::map<std::pair<int, int>, int> edge_count;
+  for (int e = 0; e < ne; ++e) {
+    std::array<int, 3> v{tri3[3 * e], tri3[3 * e + 1], tri3[3 * e + 2]};
+    for (int k = 0; k < 3; ++k)
+      if (v[k] < 0 || v[k] >= nv) fail(KB_STRUCTURAL, "element references unknown vertex");
+    if (v[0] == v[1] || v[0] == v[2] || v[1] == v[2])
+      fail(KB_STRUCTURAL, "element vertices must be distinct");
+    // orient_positive, proj/src/macro_mesh.cpp:206-210
+    if (signed_area(m.x[v[0]], m.y[v[0]], m.x[v[1]], m.y[v[1]], m.x[v[2]], m.y[v[2]]) < 0.0)
+      std::swap(v[1], v[2]);
+    m.tri[e] = v;
+    m.area[e] = signed_area(m.x[v[0]], m.y[v[0]], m.x[v[1]], m.y[v[1]], m.x[v[2]], m.y[v[2]]);
+    if (!(m.area[e] > 0.0)) fail(KB_STRUCTURAL, "degenerate element in input");
+    for (const auto& le : kLocalEdges) {
+      const int a = v[le[0]], b = v[le[1]];
+      edge_count[{std::min(a, b), std::max(a, b)}]++;
+    }
+  }
+  m.boundary.assign(nv, 0);
+  for (const auto& [k, c] : edge_count) {
+    if (c > 2) fail(KB_STRUCTURAL, "edge shared by more than two elements");
+    if (c == 1) m.boundary[k.first] = m.boundary[k.second] = 1;
+  }
+  return m;
+}
+
+int Hierarchy2D::boundary_group(int slot, int l, int i, int j) const {
+  const Level2D& lvl = levels[l];
+  const int n = lvl.n;
+  const MacroLevel& ml = lvl.macros[slot];
+  const auto& ids = mesh.tri[slot];
+  if (i == 0 && j == 0) return ml.corner_group[0];
+  if (i == n && j == 0) return ml.corner_group[1];
+  if (i == 0 && j == n) return ml.corner_group[2];
+  // D2 fix: the group index counts from the edge's lower-id corner.
+  auto pos = [&](int le, int t) { return ids[kLocalEdges[le][0]] < ids[kLocalEdges[le][1]] ? t : n - t; };
+  if (j == 0) return ml.edge[0].group_start + (pos(0, i) - 1);
+  if (i == 0) return ml.edge[1].group_start + (pos(1, j) - 1);
+  if (i + j == n) return ml.edge[2].group_start + (pos(2, j) - 1);
+  fail(KB_STRUCTURAL, "node is not on the lattice boundary");
+}
+
+bool Hierarchy2D::on_domain_boundary(int slot, int l, int i, int j) const {
+  const Level2D& lvl = levels[l];
+  const int n = lvl.n;
+  const MacroLevel& ml = lvl.macros[slot];
+  if (i == 0 && j == 0) return ml.corner_boundary[0];
+  if (i == n && j == 0) return ml.corner_boundary[1];
+  if (i == 0 && j == n) return ml.corner_boundary[2];
+  if (j == 0) return ml.edge[0].domain_boundary;
+  if (i == 0) return ml.edge[1].domain_boundary;
+  if (i + j == n) return ml.edge[2].domain_boundary;
+  return false;
+}
+
+bool Hierarchy2D::owns_boundary_node(int slot, int l, int i, int j) const {
+  const Level2D& lvl = levels[l];
+  const int n = lvl.n;
+  const MacroLevel& ml = lvl.macros[slot];
+  if (i == 0 && j == 0) return ml.corner_owner[0];
+  if (i == n && j == 0) return ml.corner_owner[1];
+  if (i == 0 && j == n) return ml.corner_owner[2];
+  if (j == 0) return ml.edge[0].owner;
+  if (i == 0) return ml.edge[1].owner;
+  if (i + j == n) return ml.edge[2].owner;
+  return true;
+}
+
+void Hierarchy2D::node_coordinates(int slot, int l, int i, int j, double& x, double& y) const {
+  const int n = levels[l].n;
+  const auto& v = mesh.tri[slot];
+  const double xi = static_cast<double>(i) / n;
+  const double yj = static_cast<double>(j) / n;
+  x = mesh.x[v[0]] + xi * (mesh.x[v[1]] - mesh.x[v[0]]) + yj * (mesh.x[v[2]] - mesh.x[v[0]]);
+  y = mesh.y[v[0]] + xi * (mesh.y[v[1]] - mesh.y[v[0]]) + yj * (mesh.y[v[2]] - mesh.y[v[0]]);
+}
+
+Hierarchy2D Hierarchy2D::build(const Mesh2D& mesh, int max_level) {
+  if (max_level < 0) fail(KB_STRUCTURAL, "hierarchy level must be nonnegative");
+  if (max_level > 9) fail(KB_STRUCTURAL, "2-d wavefront smoother supports levels <= 9");
+  Hierarchy2D h;
+  h.mesh = mesh;
+  h.L = max_level;
+  h.M = static_cast<int>(mesh.tri.size());
+  const int M = h.M;
+
+  // Global vertex and edge incidence ordered by vertex id / edge key
+  // (proj/src/hhg.cpp:73-83).
+  std::map<int, std::vector<std::pair<int, int>>> vertex_use;
+  std::map<std::pair<int, int>, std::vector<std::pair<int, int>>> edge_use;
+  for (int s = 0; s < M; ++s) {
+    const auto& ids = mesh.tri[s];
+    for (int c = 0; c < 3; ++c) vertex_use[ids[c]].push_back({s, c});
+    for (int le = 0; le < 3; ++le) {
+      const int a = ids[kLocalEdges[le][0]], b = ids[kLocalEdges[le][1]];
+      edge_use[{std::min(a, b), std::max(a, b)}].push_back({s, le});
+    }
+  }
+  for (const auto& [k, uses] : edge_use)
+    if (uses.size() > 2) fail(KB_STRUCTURAL, "hierarchy requires a conforming macro mesh");
+
+  // Vertex-sharing neighbours and the Gauss-Seidel dependency depth
+  // (SURVEY.md Appendix A.3).
+  {
+    std::vector<std::vector<int>> nb(M);
+    for (const auto& [vid, uses] : vertex_use)
+      for (const auto& a : uses)
+        for (const auto& b : uses)
+          if (a.first != b.first) nb[a.first].push_back(b.first);
+    h.nb_lo_ptr.assign(1, 0);
+    h.nb_hi_ptr.assign(1, 0);
+    std::vector<int> depth(M, 0);
+    for (int s = 0; s < M; ++s) {
+      auto& v = nb[s];
+      std::sort(v.begin(), v.end());
+      v.erase(std::unique(v.begin(), v.end()), v.end());
+      int d = 0;
+      for (int o : v) {
+        if (o < s) {
+          h.nb_lo.push_back(o);
+          d = std::max(d, depth[o]);
+        } else {
+          h.nb_hi.push_back(o);
+        }
+      }
+      depth[s] = d + 1;
+      h.dag_depth = std::max(h.dag_depth, depth[s]);
+      h.nb_lo_ptr.push_back(static_cast<int>(h.nb_lo.size()));
+      h.nb_hi_ptr.push_back(static_cast<int>(h.nb_hi.size()));
+    }
+  }
+
+  try {
+    for (int l = 0; l <= max_level; ++l) {
+      Level2D lvl;
+      lvl.n = 1 << l;
+      const int n = lvl.n;
+      lvl.S = lattice_size(n);
+      const int S = lvl.S;
+      lvl.macros.resize(M);
+      lvl.grp_ptr.push_back(0);
+      const int corner_idx[3] = {lattice_index(n, 0, 0), lattice_index(n, n, 0), lattice_index(n, 0, n)};
+      const int corner_ij[3][2] = {{0, 0}, {n, 0}, {0, n}};
+      auto push_member = [&](int s, int idx, int i, int j) {
+        lvl.mem_slot.push_back(s);
+        lvl.mem_idx.push_back(idx);
+        lvl.mem_i.push_back(i);
+        lvl.mem_j.push_back(j);
+      };
+      // vertex groups (proj/src/hhg.cpp:95-109)
+      for (const auto& [vid, uses] : vertex_use) {
+        const int gid = static_cast<int>(lvl.grp_ptr.size()) - 1;
+        for (const auto& [s, c] : uses) {
+          push_member(s, corner_idx[c], corner_ij[c][0], corner_ij[c][1]);
+          lvl.macros[s].corner_group[c] = gid;
+          lvl.macros[s].corner_boundary[c] = mesh.boundary[vid] != 0;
+        }
+        lvl.macros[uses.front().first].corner_owner[uses.front().second] = true;
+        lvl.grp_ptr.push_back(static_cast<int>(lvl.mem_slot.size()));
+      }
+      // edge groups (proj/src/hhg.cpp:111-132)
+      for (const auto& [key, uses] : edge_use) {
+        const bool bnd = uses.size() == 1;
+        const int group_start = static_cast<int>(lvl.grp_ptr.size()) - 1;
+        for (int s = 1; s <= n - 1; ++s) {
+          for (const auto& [slot, le] : uses) {
+            const int first = mesh.tri[slot][kLocalEdges[le][0]];
+            const int t = (first == key.first) ? s : n - s;
+            const int ii = le == 0 ? t : (le == 1 ? 0 : n - t);
+            const int jj = le == 0 ? 0 : t;
+            push_member(slot, edge_lattice_index(n, le, t), ii, jj);
+          }
+          lvl.grp_ptr.push_back(static_cast<int>(lvl.mem_slot.size()));
+        }
+        for (const auto& [slot, le] : uses) {
+          auto& info = lvl.macros[slot].edge[le];
+          info.group_start = group_start;
+          info.owner = (slot == uses.front().first && le == uses.front().second);
+          info.domain_boundary = bnd;
+        }
+      }
+      const std::int64_t interior = static_cast<std::int64_t>(n - 1) * (n - 2) / 2;
+      lvl.dofs = static_cast<std::int64_t>(vertex_use.size()) +
+                 static_cast<std::int64_t>(edge_use.size()) * (n - 1) +
+                 static_cast<std::int64_t>(M) * interior;
+      h.levels.push_back(std::move(lvl));
+    }
+  } catch (const std::bad_alloc&) {
+    Error e(KB_RESOURCE, "out of memory while building hierarchy level");
+    e.level = static_cast<int>(h.levels.size());
+    throw e;
+  }
+
+  // Derived tables.
+  for (int l = 0; l <= max_level; ++l) {
+    Level2D& lvl = h.levels[l];
+    const int n = lvl.n, S = lvl.S;
+    lvl.node_gid.assign(static_cast<std::size_t>(M) * S, -1);
+    lvl.node_flags.assign(static_cast<std::size_t>(M) * S, 4);  // interior: owner
+    for (int s = 0; s < M; ++s) {
+      for (int j = 0; j <= n; ++j)
+        for (int i = 0; i <= n - j; ++i) {
+          if (!on_lattice_boundary(n, i, j)) continue;
+          const std::size_t k = static_cast<std::size_t>(s) * S + lattice_index(n, i, j);
+          lvl.node_gid[k] = h.boundary_group(s, l, i, j);
+          std::uint8_t f = 1;
+          if (h.on_domain_boundary(s, l, i, j)) f |= 2;
+          if (h.owns_boundary_node(s, l, i, j)) f |= 4;
+          lvl.node_flags[k] = f;
+        }
+    }
+    // element matrices and stencils (proj/src/fem.cpp:62-93)
+    lvl.kstiff.assign(static_cast<std::size_t>(M) * 18, 0.0);
+    lvl.kmass.assign(static_cast<std::size_t>(M) * 18, 0.0);
+    lvl.stencil.assign(static_cast<std::size_t>(M) * 7, 0.0);
+    lvl.inv_c.assign(M, 0.0);
+    for (int s = 0; s < M; ++s) {
+      double p[3][2];
+      const int cij[3][2] = {{0, 0}, {1, 0}, {0, 1}};
+      for (int c = 0; c < 3; ++c) h.node_coordinates(s, l, cij[c][0], cij[c][1], p[c][0], p[c][1]);
+      const auto up = stiffness_matrix(p[0][0], p[0][1], p[1][0], p[1][1], p[2][0], p[2][1]);
+      std::array<double, 9> down{};
+      if (n >= 2) {
+        double q[3][2];
+        const int dij[3][2] = {{1, 0}, {0, 1}, {1, 1}};
+        for (int c = 0; c < 3; ++c) h.node_coordinates(s, l, dij[c][0], dij[c][1], q[c][0], q[c][1]);
+        down = stiffness_matrix(q[0][0], q[0][1], q[1][0], q[1][1], q[2][0], q[2][1]);
+      }
+      const double cell_area = mesh.area[s] / (static_cast<double>(n) * n);
+      const auto mu = mass_matrix(cell_area);
+      const auto md = n >= 2 ? mass_matrix(cell_area) : std::array<double, 9>{};
+      for (int k = 0; k < 9; ++k) {
+        lvl.kstiff[18 * s + k] = up[k];
+        lvl.kstiff[18 * s + 9 + k] = down[k];
+        lvl.kmass[18 * s + k] = mu[k];
+        lvl.kmass[18 * s + 9 + k] = md[k];
+      }
+      const auto& ku = up;
+      const auto& kd = down;
+      double* st = &lvl.stencil[7 * s];
+      st[0] = ku[0] + ku[4] + ku[8] + kd[0] + kd[4] + kd[8];
+      st[1] = ku[1] + kd[5];
+      st[2] = ku[3] + kd[7];
+      st[3] = ku[2] + kd[2];
+      st[4] = ku[6] + kd[6];
+      st[5] = ku[5] + kd[1];
+      st[6] = ku[7] + kd[3];
+      lvl.inv_c[s] = 1.0 / st[0];
+    }
+    // owner dot order (proj/src/hhg.cpp:233-255)
+    for (int s = 0; s < M; ++s) {
+      const std::size_t base = static_cast<std::size_t>(s) * S;
+      for (int j = 1; j < n; ++j)
+        for (int i = 1; i < n - j; ++i) lvl.dot_order.push_back(static_cast<int>(base + lattice_index(n, i, j)));
+      const MacroLevel& ml = lvl.macros[s];
+      const int corner_idx[3] = {lattice_index(n, 0, 0), lattice_index(n, n, 0), lattice_index(n, 0, n)};
+      for (int c = 0; c < 3; ++c)
+        if (ml.corner_owner[c]) lvl.dot_order.push_back(static_cast<int>(base + corner_idx[c]));
+      for (int le = 0; le < 3; ++le) {
+        if (!ml.edge[le].owner) continue;
+        for (int t = 1; t <= n - 1; ++t) lvl.dot_order.push_back(static_cast<int>(base + edge_lattice_index(n, le, t)));
+      }
+    }
+    if (l == 0) continue;
+
+    // Wavefront Gauss-Seidel tables.
+    lvl.bnode.assign(static_cast<std::size_t>(M) * 3 * n, BNode{});
+    lvl.ghost_ptr.assign(1, 0);
+    for (int m = 0; m < M; ++m) {
+      std::map<int, int> ghost_of;
+      std::vector<int> ghosts;
+      auto visit = [&](int i, int j) {
+        BNode bn{};
+        const int gid = h.boundary_group(m, l, i, j);
+        const int own_off = m * S + lattice_index(n, i, j);
+        bn.domain = h.on_domain_boundary(m, l, i, j) ? 1 : 0;
+        bn.wr_begin = static_cast<int>(lvl.wr.size());
+        for (int k = lvl.grp_ptr[gid]; k < lvl.grp_ptr[gid + 1]; ++k) {
+          const int off = lvl.mem_slot[k] * S + lvl.mem_idx[k];
+          if (off != own_off) lvl.wr.push_back(off);
+        }
+        bn.wr_count = static_cast<int>(lvl.wr.size()) - bn.wr_begin;
+        bn.rec_begin = static_cast<int>(lvl.rec.size());
+        double diag = 0.0;
+        if (!bn.domain) {
+          for (int k = lvl.grp_ptr[gid]; k < lvl.grp_ptr[gid + 1]; ++k) {
+            const int sp = lvl.mem_slot[k], ip = lvl.mem_i[k], jp = lvl.mem_j[k];
+            const double* ku = &lvl.kstiff[18 * sp];
+            const double* kd = ku + 9;
+            MemberRec r{};
+            r.slot = sp;
+            // cells of partial_row in order (proj/src/fem.cpp:138-172)
+            const bool cell[6] = {ip + jp <= n - 1,
+                                  ip >= 1 && ip - 1 + jp <= n - 1,
+                                  jp >= 1 && ip + jp - 1 <= n - 1,
+                                  ip >= 1 && ip + jp <= n - 1,
+                                  jp >= 1 && ip + jp <= n - 1,
+                                  ip >= 1 && jp >= 1 && ip + jp <= n};
+            const double dg[6] = {ku[0], ku[4], ku[8], kd[0], kd[4], kd[8]};
+            const int rd[12][2] = {{ip + 1, jp}, {ip, jp + 1}, {ip - 1, jp}, {ip - 1, jp + 1},
+                                   {ip, jp - 1}, {ip + 1, jp - 1}, {ip - 1, jp + 1}, {ip, jp + 1},
+                                   {ip + 1, jp - 1}, {ip + 1, jp}, {ip, jp - 1}, {ip - 1, jp}};
+            double d = 0.0;
+            for (int c = 0; c < 6; ++c) {
+              r.code[2 * c] = r.code[2 * c + 1] = -1;
+              if (!cell[c]) continue;
+              r.mask |= 1 << c;
+              d += dg[c];
+              for (int q = 0; q < 2; ++q) {
+                const int xi = rd[2 * c + q][0], xj = rd[2 * c + q][1];
+                int code = -1;
+                if (sp == m) {
+                  code = direction_code(xi - i, xj - j);
+                } else {
+                  if (on_lattice_boundary(n, xi, xj)) {
+                    const int g2 = h.boundary_group(sp, l, xi, xj);
+                    for (int k2 = lvl.grp_ptr[g2]; k2 < lvl.grp_ptr[g2 + 1]; ++k2)
+                      if (lvl.mem_slot[k2] == m) code = direction_code(lvl.mem_i[k2] - i, lvl.mem_j[k2] - j);
+                    if (code < 0) {
+                      bool shared = false;
+                      for (int k2 = lvl.grp_ptr[g2]; k2 < lvl.grp_ptr[g2 + 1]; ++k2)
+                        shared = shared || lvl.mem_slot[k2] == m;
+                      if (shared) fail(KB_INTERNAL, "shared neighbour is not lattice-adjacent");
+                    }
+                  }
+                  if (code < 0) {
+                    const int goff = sp * S + lattice_index(n, xi, xj);
+                    auto it = ghost_of.find(goff);
+                    int gi;
+                    if (it == ghost_of.end()) {
+                      gi = static_cast<int>(ghosts.size());
+                      ghosts.push_back(goff);
+                      ghost_of[goff] = gi;
+                    } else {
+                      gi = it->second;
+                    }
+                    code = 6 + gi;
+                  }
+                }
+                if (code < 0) fail(KB_INTERNAL, "unresolved partial-row read");
+                if (code > 32767) fail(KB_INTERNAL, "too many ghost values");
+                r.code[2 * c + q] = static_cast<std::int16_t>(code);
+              }
+            }
+            diag += d;
+            lvl.rec.push_back(r);
+          }
+        }
+        bn.rec_count = static_cast<int>(lvl.rec.size()) - bn.rec_begin;
+        bn.diag = diag;
+        lvl.bnode[static_cast<std::size_t>(m) * 3 * n + bpos(n, i, j)] = bn;
+      };
+      for (int i = 0; i <= n; ++i) visit(i, 0);
+      for (int j = 1; j <= n; ++j) visit(0, j);
+      for (int j = 1; j <= n - 1; ++j) visit(n - j, j);
+      lvl.ghost_off.insert(lvl.ghost_off.end(), ghosts.begin(), ghosts.end());
+      lvl.ghost_ptr.push_back(static_cast<int>(lvl.ghost_off.size()));
+      lvl.max_ghosts = std::max(lvl.max_ghosts, static_cast<int>(ghosts.size()));
+    }
+  }
+  return h;
+}
+
+}  // namespace kb

@@ -1,0 +1,115 @@
+// Host-side hierarchical hybrid grid (HHG) over a conforming 2-d macro mesh:
+// shared-node groups, ownership, per-macro element matrices and the derived
+// device tables used by the sm_100a kernels (kernels2d.cu).
+//
+// Semantics follow the reference GridHierarchy (proj/src/hhg.cpp:48-144) and
+// OperatorP1 (proj/src/fem.cpp:62-93) with the two defects fixed:
+//   D1: element matrices use |area| (proj/src/fem.cpp:32);
+//   D2: edge-node groups are addressed by the position counted from the edge's
+//       lower-id corner (proj/src/hhg.cpp:170-172 vs :114-123).
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <vector>
+
+#include "common.hpp"
+
+namespace kb {
+
+// Conforming 2-d macro mesh in slot order (ascending active element id).
+// Equivalent of the parts of MacroMesh (proj/include/klref/macro_mesh.hpp:62)
+// the hot path reads: vertex coordinates, vertex boundary flags, element
+// corner ids (oriented counter-clockwise as MacroMesh::create does,
+// proj/src/macro_mesh.cpp:206-216) and element areas.
+struct Mesh2D {
+  std::vector<double> x, y;
+  std::vector<std::uint8_t> boundary;   // recomputed from edge use, proj/src/macro_mesh.cpp:306-318
+  std::vector<std::array<int, 3>> tri;  // corner vertex ids per slot
+  std::vector<double> area;             // signed_area, proj/src/macro_mesh.cpp:28-30
+
+  static Mesh2D create(int num_vertices, const double* xy, int num_elements, const int* tri3);
+};
+
+struct MacroEdgeInfo {
+  int group_start = -1;
+  bool owner = false;
+  bool domain_boundary = false;
+};
+struct MacroLevel {
+  std::array<int, 3> corner_group{-1, -1, -1};
+  std::array<bool, 3> corner_owner{false, false, false};
+  std::array<bool, 3> corner_boundary{false, false, false};
+  std::array<MacroEdgeInfo, 3> edge{};
+};
+
+// Relaxation record of one group member for the wavefront Gauss-Seidel:
+// partial_row (proj/src/fem.cpp:128-173) of member `slot` at its local node,
+// with every x-read resolved either to a neighbour of the relaxing node in the
+// relaxing macro (codes 0..5 = E, W, N, S, NW, SE) or to a ghost value of a
+// node the relaxing macro does not hold (code 6 + ghost index).
+struct MemberRec {
+  std::int32_t slot;
+  std::int32_t mask;       // existing cells, bit k in the partial_row order
+  std::int16_t code[12];   // two reads per cell, in partial_row order
+};
+struct BNode {
+  std::int32_t rec_begin, rec_count;
+  std::int32_t wr_begin, wr_count;  // other copies to write
+  std::int32_t domain;              // on the domain boundary: u = b
+  std::int32_t pad;
+  double diag;                      // sum over members of the partial diagonals
+};
+
+struct Level2D {
+  int n = 1, S = 3;
+  // shared-node groups (vertex groups first, then edge groups), members ascending slot
+  std::vector<int> grp_ptr;
+  std::vector<int> mem_slot, mem_i, mem_j, mem_idx;
+  std::vector<MacroLevel> macros;
+  std::int64_t dofs = 0;
+  // dense per-copy tables (M * S)
+  std::vector<int> node_gid;               // -1 for lattice-interior nodes
+  std::vector<std::uint8_t> node_flags;    // bit0 lattice boundary, bit1 domain boundary, bit2 owner
+  // per macro element matrices: [up(9), down(9)]
+  std::vector<double> kstiff, kmass;
+  std::vector<double> stencil;             // 7 per macro (C, E, W, N, S, NW, SE), proj/src/fem.cpp:85-91
+  std::vector<double> inv_c;               // 1 / stencil[0]
+  // wavefront Gauss-Seidel tables (levels >= 1)
+  std::vector<BNode> bnode;                // M * 3n, boundary position order (see bpos())
+  std::vector<MemberRec> rec;
+  std::vector<int> wr;                     // global copy offsets
+  std::vector<int> ghost_ptr, ghost_off;   // per macro ghost lists (global offsets)
+  int max_ghosts = 0;
+  // owner dot order (dot_unique, proj/src/hhg.cpp:227-257): offsets in summation order
+  std::vector<int> dot_order;
+};
+
+// Boundary position of lattice-boundary node (i, j): row 0 first, then the
+// i = 0 edge, then the hypotenuse.
+inline int bpos(int n, int i, int j) {
+  if (j == 0) return i;
+  if (i == 0) return n + j;
+  return 2 * n + j;
+}
+
+struct Hierarchy2D {
+  Mesh2D mesh;
+  int L = 0;
+  int M = 0;
+  std::vector<Level2D> levels;
+  // vertex-sharing neighbours per macro (level independent): lower and higher slots
+  std::vector<int> nb_lo_ptr, nb_lo, nb_hi_ptr, nb_hi;
+  int dag_depth = 0;
+
+  static Hierarchy2D build(const Mesh2D& mesh, int max_level);
+
+  // boundary_group with the D2 fix (proj/src/hhg.cpp:163-174)
+  int boundary_group(int slot, int l, int i, int j) const;
+  bool on_domain_boundary(int slot, int l, int i, int j) const;
+  bool owns_boundary_node(int slot, int l, int i, int j) const;
+  // node_coordinates, proj/src/hhg.cpp:146-154
+  void node_coordinates(int slot, int l, int i, int j, double& x, double& y) const;
+};
+
+}  // namespace kb

@@ -1,0 +1,784 @@
+// sm_100a kernels of the 2-d hot path (fp64, memory/latency bound, no tensor
+// cores).  Compiled with -fmad=false: every kernel reproduces the reference's
+// floating-point operation order so that results are
+// bitwise identical to the (patched) reference.
+//
+//   apply / residual     OperatorP1::apply + interface_sync(Additive)   proj/src/fem.cpp:95-126
+//                        MultigridSolver::residual                      proj/src/multigrid.cpp:183-190
+//   restrict             restrict_transpose                             proj/src/multigrid.cpp:55-104
+//   prolong              prolongate / u += P e / FMG w snapshot          proj/src/multigrid.cpp:22-53, 243, 265-268
+//   rhs                  assemble_rhs + set_domain_boundary_values      proj/src/fem.cpp:175-228
+//   cg0                  MultigridSolver::cg_level0                     proj/src/multigrid.cpp:198-229
+//   gs                   MultigridSolver::gauss_seidel                  proj/src/multigrid.cpp:127-181
+//   estimate             error_estimate norms                           proj/src/estimator.cpp:8-45, fem.cpp:320-356
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <map>
+#include <string>
+
+#include "dev2d.hpp"
+
+namespace kb {
+namespace {
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ int dlat(int n, int i, int j) { return j * (n + 1) - (j * (j - 1)) / 2 + i; }
+
+__device__ __forceinline__ void decode(int n, int idx, int& i, int& j) {
+  const double a = 2.0 * n + 3.0;
+  int jj = static_cast<int>((a - sqrt(a * a - 8.0 * idx)) * 0.5);
+  jj = max(0, min(jj, n));
+  while (jj < n && dlat(n, 0, jj + 1) <= idx) ++jj;
+  while (jj > 0 && dlat(n, 0, jj) > idx) --jj;
+  j = jj;
+  i = idx - dlat(n, 0, jj);
+}
+
+// Gather form of the reference element scatter: the <= 6 incident cells of
+// node (p, q) in the reference's visit order (SURVEY.md A.5 "apply").
+__device__ __forceinline__ double gather_apply(const double* __restrict__ x, int n, int p, int q,
+                                               const double* __restrict__ K) {
+  const double* ku = K;
+  const double* kd = K + 9;
+  double acc = 0.0;
+  if (q >= 1 && p + q <= n)  // up(p, q-1) as c
+    acc += (ku[6] * x[dlat(n, p, q - 1)] + ku[7] * x[dlat(n, p + 1, q - 1)]) + ku[8] * x[dlat(n, p, q)];
+  if (p >= 1 && q >= 1 && p + q <= n)  // down(p-1, q-1) as c
+    acc += (kd[6] * x[dlat(n, p, q - 1)] + kd[7] * x[dlat(n, p - 1, q)]) + kd[8] * x[dlat(n, p, q)];
+  if (q >= 1 && p + q <= n - 1)  // down(p, q-1) as b
+    acc += (kd[3] * x[dlat(n, p + 1, q - 1)] + kd[4] * x[dlat(n, p, q)]) + kd[5] * x[dlat(n, p + 1, q)];
+  if (p >= 1 && p + q <= n)  // up(p-1, q) as b
+    acc += (ku[3] * x[dlat(n, p - 1, q)] + ku[4] * x[dlat(n, p, q)]) + ku[5] * x[dlat(n, p - 1, q + 1)];
+  if (p + q <= n - 1)  // up(p, q) as a
+    acc += (ku[0] * x[dlat(n, p, q)] + ku[1] * x[dlat(n, p + 1, q)]) + ku[2] * x[dlat(n, p, q + 1)];
+  if (p >= 1 && p + q <= n - 1)  // down(p-1, q) as a
+    acc += (kd[0] * x[dlat(n, p, q)] + kd[1] * x[dlat(n, p - 1, q + 1)]) + kd[2] * x[dlat(n, p, q + 1)];
+  return acc;
+}
+
+__device__ __forceinline__ void write_out(int mode, double v, int k, double* y, const double* b,
+                                          const std::uint8_t* flags) {
+  if (mode == APPLY_RESIDUAL) {
+    // r = (-y) + 1.0 * b, then zero_domain_boundary (proj/src/multigrid.cpp:185-188)
+    y[k] = (flags[k] & 2) ? 0.0 : (b[k] - v);
+  } else if (mode == APPLY_ZERO_BND) {
+    y[k] = (flags[k] & 2) ? 0.0 : v;
+  } else {
+    y[k] = v;
+  }
+}
+
+// One copy k of the level: interior nodes directly; lattice-boundary nodes are
+// produced by the group leader (first member) as the ascending-slot sum of the
+// members' macro-local products, written to every copy (interface_sync Additive).
+__device__ __forceinline__ void apply_node(const DevLevel2D& lv, const double* __restrict__ K,
+                                           const double* __restrict__ x, double* y,
+                                           const double* b, int mode, int k) {
+  const int S = lv.S, n = lv.n;
+  const int slot = k / S;
+  const int idx = k - slot * S;
+  int i, j;
+  decode(n, idx, i, j);
+  const std::uint8_t fl = lv.node_flags[k];
+  if (!(fl & 1)) {
+    write_out(mode, gather_apply(x + static_cast<size_t>(slot) * S, n, i, j, K + 18 * slot), k, y, b,
+              lv.node_flags);
+    return;
+  }
+  const int gid = lv.node_gid[k];
+  const int beg = lv.grp_ptr[gid], end = lv.grp_ptr[gid + 1];
+  if (lv.mem_off[beg] != k) return;
+  double v;
+  if (end - beg == 1) {
+    v = gather_apply(x + static_cast<size_t>(slot) * S, n, i, j, K + 18 * slot);
+  } else {
+    v = 0.0;
+    for (int m = beg; m < end; ++m) {
+      const int ms = lv.mem_slot[m], ij = lv.mem_ij[m];
+      v += gather_apply(x + static_cast<size_t>(ms) * S, n, ij & 0xffff, ij >> 16, K + 18 * ms);
+    }
+  }
+  for (int m = beg; m < end; ++m) write_out(mode, v, lv.mem_off[m], y, b, lv.node_flags);
+}
+
+__global__ void k_apply(DevLevel2D lv, const double* __restrict__ K, const double* __restrict__ x,
+                        double* y, const double* b, int mode) {
+  const int total = lv.M * lv.S;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < total; k += gridDim.x * blockDim.x)
+    apply_node(lv, K, x, y, b, mode, k);
+}
+
+// ---------------------------------------------------------------- restrict
+__device__ __forceinline__ double gather_restrict(const double* __restrict__ f,
+                                                  const std::uint8_t* __restrict__ fl, int nf, int I,
+                                                  int J) {
+  double c = 0.0;
+  // fine visit order (SURVEY.md A.5 "restrict_transpose")
+  const int ii[7] = {2 * I, 2 * I + 1, 2 * I - 1, 2 * I, 2 * I + 1, 2 * I - 1, 2 * I};
+  const int jj[7] = {2 * J - 1, 2 * J - 1, 2 * J, 2 * J, 2 * J, 2 * J + 1, 2 * J + 1};
+#pragma unroll
+  for (int t = 0; t < 7; ++t) {
+    const int i = ii[t], j = jj[t];
+    if (i < 0 || j < 0 || i + j > nf) continue;
+    const int k = dlat(nf, i, j);
+    const double v = (fl[k] & 4) ? f[k] : 0.0;  // non-owner copies masked (multigrid.cpp:63-76)
+    if (v == 0.0) continue;
+    c += (t == 3) ? v : 0.5 * v;
+  }
+  return c;
+}
+
+__global__ void k_restrict(DevLevel2D fine, DevLevel2D coarse, const double* __restrict__ r, double* rc,
+                           int zero_boundary) {
+  const int total = coarse.M * coarse.S;
+  const int Sc = coarse.S, Sf = fine.S, nc = coarse.n, nf = fine.n;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < total; k += gridDim.x * blockDim.x) {
+    const int slot = k / Sc;
+    int I, J;
+    decode(nc, k - slot * Sc, I, J);
+    const std::uint8_t fl = coarse.node_flags[k];
+    if (!(fl & 1)) {
+      rc[k] = gather_restrict(r + static_cast<size_t>(slot) * Sf, fine.node_flags + static_cast<size_t>(slot) * Sf,
+                              nf, I, J);
+      continue;
+    }
+    const int gid = coarse.node_gid[k];
+    const int beg = coarse.grp_ptr[gid], end = coarse.grp_ptr[gid + 1];
+    if (coarse.mem_off[beg] != k) continue;
+    double v;
+    if (end - beg == 1) {
+      v = gather_restrict(r + static_cast<size_t>(slot) * Sf, fine.node_flags + static_cast<size_t>(slot) * Sf, nf,
+                          I, J);
+    } else {
+      v = 0.0;
+      for (int m = beg; m < end; ++m) {
+        const int ms = coarse.mem_slot[m], ij = coarse.mem_ij[m];
+        v += gather_restrict(r + static_cast<size_t>(ms) * Sf, fine.node_flags + static_cast<size_t>(ms) * Sf, nf,
+                             ij & 0xffff, ij >> 16);
+      }
+    }
+    for (int m = beg; m < end; ++m) {
+      const int o = coarse.mem_off[m];
+      rc[o] = (zero_boundary && (coarse.node_flags[o] & 2)) ? 0.0 : v;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- prolong
+__device__ __forceinline__ double prolong_value(const double* __restrict__ c, int nc, int i, int j) {
+  if ((i & 1) == 0 && (j & 1) == 0) return c[dlat(nc, i / 2, j / 2)];
+  if ((j & 1) == 0) return 0.5 * (c[dlat(nc, (i - 1) / 2, j / 2)] + c[dlat(nc, (i + 1) / 2, j / 2)]);
+  if ((i & 1) == 0) return 0.5 * (c[dlat(nc, i / 2, (j - 1) / 2)] + c[dlat(nc, i / 2, (j + 1) / 2)]);
+  return 0.5 * (c[dlat(nc, (i + 1) / 2, (j - 1) / 2)] + c[dlat(nc, (i - 1) / 2, (j + 1) / 2)]);
+}
+
+__device__ __forceinline__ int bpos_dev(int n, int i, int j) {
+  if (j == 0) return i;
+  if (i == 0) return n + j;
+  return 2 * n + j;
+}
+
+__global__ void k_prolong(DevLevel2D coarse, DevLevel2D fine, const double* __restrict__ c, double* f,
+                          double* next, const double* __restrict__ gbnd, int mode) {
+  const int total = fine.M * fine.S;
+  const int Sf = fine.S, Sc = coarse.S, nf = fine.n, nc = coarse.n;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < total; k += gridDim.x * blockDim.x) {
+    const int slot = k / Sf;
+    int i, j;
+    decode(nf, k - slot * Sf, i, j);
+    const double v = prolong_value(c + static_cast<size_t>(slot) * Sc, nc, i, j);
+    if (mode == PROLONG_ADD) {
+      f[k] = f[k] + v;  // u.add_scaled(ef, 1.0)
+    } else {
+      f[k] = v;
+      if (mode == PROLONG_W_NEXT) {
+        const bool dom = fine.node_flags[k] & 2;
+        next[k] = dom ? gbnd[static_cast<size_t>(slot) * 3 * nf + bpos_dev(nf, i, j)] : v;
+      }
+    }
+  }
+}
+
+// Dirichlet values: f = g (owner-evaluated, replace-synced) on domain-boundary
+// copies; optionally zero everything else (u0 initialisation).
+__global__ void k_set_boundary(DevLevel2D lv, double* f, const double* __restrict__ gbnd, int zero_rest) {
+  const int total = lv.M * lv.S;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < total; k += gridDim.x * blockDim.x) {
+    const std::uint8_t fl = lv.node_flags[k];
+    if (fl & 2) {
+      const int slot = k / lv.S;
+      int i, j;
+      decode(lv.n, k - slot * lv.S, i, j);
+      f[k] = gbnd[static_cast<size_t>(slot) * 3 * lv.n + bpos_dev(lv.n, i, j)];
+    } else if (zero_rest) {
+      f[k] = 0.0;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- rhs
+__global__ void k_ftab(DevLevel2D lv, int kind, double* ftab) {
+  const int n2 = 2 * lv.n;
+  const int SF = (n2 + 1) * (n2 + 2) / 2;
+  const int total = lv.M * SF;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < total; k += gridDim.x * blockDim.x) {
+    const int slot = k / SF;
+    int I, J;
+    decode(n2, k - slot * SF, I, J);
+    const double* g = lv.geo + 6 * slot;
+    const double hi = 0.5 * I, hj = 0.5 * J;
+    const double x = g[0] + hi * g[2] + hj * g[4];
+    const double y = g[1] + hi * g[3] + hj * g[5];
+    double f = 0.0;
+    if (kind == SRC_SIN2D) f = 2.0 * M_PI * M_PI * sin(M_PI * x) * sin(M_PI * y);
+    ftab[k] = f;
+  }
+}
+
+__device__ __forceinline__ double gather_rhs(const double* __restrict__ F, int n, int p, int q, double hw) {
+  const int n2 = 2 * n;
+  auto f = [&](int I, int J) { return F[dlat(n2, I, J)]; };
+  double acc = 0.0;
+  if (q >= 1 && p + q <= n) {  // up(p, q-1) as c
+    const int i = p, j = q - 1;
+    acc += hw * (f(2 * i, 2 * j + 1) + f(2 * i + 1, 2 * j + 1));
+  }
+  if (p >= 1 && q >= 1 && p + q <= n) {  // down(p-1, q-1) as c
+    const int i = p - 1, j = q - 1;
+    acc += hw * (f(2 * i + 2, 2 * j + 1) + f(2 * i + 1, 2 * j + 2));
+  }
+  if (q >= 1 && p + q <= n - 1) {  // down(p, q-1) as b
+    const int i = p, j = q - 1;
+    acc += hw * (f(2 * i + 1, 2 * j + 1) + f(2 * i + 1, 2 * j + 2));
+  }
+  if (p >= 1 && p + q <= n) {  // up(p-1, q) as b
+    const int i = p - 1, j = q;
+    acc += hw * (f(2 * i + 1, 2 * j) + f(2 * i + 1, 2 * j + 1));
+  }
+  if (p + q <= n - 1) {  // up(p, q) as a
+    acc += hw * (f(2 * p + 1, 2 * q) + f(2 * p, 2 * q + 1));
+  }
+  if (p >= 1 && p + q <= n - 1) {  // down(p-1, q) as a
+    const int i = p - 1, j = q;
+    acc += hw * (f(2 * i + 1, 2 * j + 1) + f(2 * i + 2, 2 * j + 1));
+  }
+  return acc;
+}
+
+__global__ void k_rhs(DevLevel2D lv, const double* __restrict__ ftab, const double* __restrict__ gbnd,
+                      double* b, int src_zero) {
+  const int total = lv.M * lv.S;
+  const int S = lv.S, n = lv.n;
+  const int SF = (2 * n + 1) * (2 * n + 2) / 2;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < total; k += gridDim.x * blockDim.x) {
+    const int slot = k / S;
+    int i, j;
+    decode(n, k - slot * S, i, j);
+    const std::uint8_t fl = lv.node_flags[k];
+    if (fl & 2) {
+      b[k] = gbnd[static_cast<size_t>(slot) * 3 * n + bpos_dev(n, i, j)];
+      continue;
+    }
+    if (src_zero) {
+      b[k] = 0.0;
+      continue;
+    }
+    if (!(fl & 1)) {
+      b[k] = gather_rhs(ftab + static_cast<size_t>(slot) * SF, n, i, j, lv.wq[slot] * 0.5);
+      continue;
+    }
+    const int gid = lv.node_gid[k];
+    const int beg = lv.grp_ptr[gid], end = lv.grp_ptr[gid + 1];
+    if (lv.mem_off[beg] != k) continue;
+    double v;
+    if (end - beg == 1) {
+      v = gather_rhs(ftab + static_cast<size_t>(slot) * SF, n, i, j, lv.wq[slot] * 0.5);
+    } else {
+      v = 0.0;
+      for (int m = beg; m < end; ++m) {
+        const int ms = lv.mem_slot[m], ij = lv.mem_ij[m];
+        v += gather_rhs(ftab + static_cast<size_t>(ms) * SF, n, ij & 0xffff, ij >> 16, lv.wq[ms] * 0.5);
+      }
+    }
+    for (int m = beg; m < end; ++m) b[lv.mem_off[m]] = v;
+  }
+}
+
+// ---------------------------------------------------------------- level-0 CG
+// One CTA runs the whole unpreconditioned CG of MultigridSolver::cg_level0;
+// dot_unique is a sequential sum in the reference's owner order.
+__device__ double seq_dot(const DevLevel2D& lv, const double* a, const double* b, bool zero_bnd) {
+  double s = 0.0;
+  for (int t = 0; t < lv.dot_count; ++t) {
+    const int k = lv.dot_order[t];
+    double x = a[k], y = b[k];
+    if (zero_bnd && (lv.node_flags[k] & 2)) x = y = 0.0;
+    s += x * y;
+  }
+  return s;
+}
+
+__global__ void k_cg0(DevLevel2D lv, double* u, const double* b, double* r, double* p, double* ap,
+                      CgParams prm, DevStatus* status) {
+  const int total = lv.M * lv.S;
+  __shared__ double sh_rr, sh_alpha, sh_beta;
+  __shared__ int sh_go;
+  for (int k = threadIdx.x; k < total; k += blockDim.x) apply_node(lv, lv.kstiff, u, r, b, APPLY_RESIDUAL, k);
+  __syncthreads();
+  for (int k = threadIdx.x; k < total; k += blockDim.x) p[k] = r[k];
+  __syncthreads();
+  double tol = 0.0;
+  int it = 0;
+  if (threadIdx.x == 0) {
+    sh_rr = seq_dot(lv, r, r, false);
+    const double bnorm = sqrt(fmax(0.0, seq_dot(lv, b, b, true)));
+    const double a = prm.rel_tol * bnorm;
+    tol = (a < prm.abs_floor) ? prm.abs_floor : a;
+    sh_go = sqrt(sh_rr) > tol;
+  }
+  __syncthreads();
+  while (sh_go) {
+    if (threadIdx.x == 0 && ++it > prm.max_iter) {
+      if (status->code == 0) {
+        status->code = 1;
+        status->residual = sqrt(sh_rr);
+      }
+      sh_go = 0;
+    }
+    __syncthreads();
+    if (!sh_go) break;
+    for (int k = threadIdx.x; k < total; k += blockDim.x) apply_node(lv, lv.kstiff, p, ap, nullptr, APPLY_ZERO_BND, k);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const double pap = seq_dot(lv, p, ap, false);
+      if (pap <= 0.0) {
+        if (status->code == 0) {
+          status->code = 2;
+          status->residual = sqrt(sh_rr);
+        }
+        sh_go = 0;
+      } else {
+        sh_alpha = sh_rr / pap;
+      }
+    }
+    __syncthreads();
+    if (!sh_go) break;
+    const double alpha = sh_alpha;
+    for (int k = threadIdx.x; k < total; k += blockDim.x) {
+      u[k] = u[k] + alpha * p[k];
+      r[k] = r[k] + (-alpha) * ap[k];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const double rr_new = seq_dot(lv, r, r, false);
+      sh_beta = rr_new / sh_rr;
+      sh_rr = rr_new;
+    }
+    __syncthreads();
+    const double beta = sh_beta;
+    for (int k = threadIdx.x; k < total; k += blockDim.x) p[k] = p[k] * beta + r[k];
+    __syncthreads();
+    if (threadIdx.x == 0) sh_go = sqrt(sh_rr) > tol;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) status->iters = it;
+}
+
+// ---------------------------------------------------------------- Gauss-Seidel
+// Exact-order forward Gauss-Seidel.  Work items are (sweep, macro) in the
+// reference's sequential order; macro m's sweep s starts once every
+// vertex-sharing macro m' < m finished sweep s and every m'' > m finished
+// sweep s-1 (bitwise identical to the sequential order).
+// Inside a macro one lane owns one lattice row j and walks the hyperplane
+// wavefront t = i + 2j (A.2): W comes from the lane's own previous result,
+// S/SE from lane j-1 by shuffle (SMEM hand-off across warps), and the
+// not-yet-updated E/N/NW/b values are prefetched kPf steps ahead from L2.
+constexpr int kPf = 8;     // prefetch distance (wavefront steps)
+constexpr int kRing = 16;  // cross-warp hand-off ring
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ double pick(int c, double E, double W, double N, double S, double NW, double SE,
+                                       const double* gh) {
+  switch (c) {
+    case 0: return E;
+    case 1: return W;
+    case 2: return N;
+    case 3: return S;
+    case 4: return NW;
+    case 5: return SE;
+    default: return gh[c - 6];
+  }
+}
+
+__device__ __noinline__ double relax_interface(const DevLevel2D& lv, const BNode& bn, double B, double E,
+                                               double W, double N, double S, double NW, double SE,
+                                               const double* gh) {
+  double off = 0.0;
+  for (int r = 0; r < bn.rec_count; ++r) {
+    const MemberRec rec = lv.rec[bn.rec_begin + r];
+    const double* ku = lv.kstiff + 18 * rec.slot;
+    const double* kd = ku + 9;
+    double o = 0.0;
+    // partial_row cell order, proj/src/fem.cpp:138-172
+    if (rec.mask & 1) o += ku[1] * pick(rec.code[0], E, W, N, S, NW, SE, gh) + ku[2] * pick(rec.code[1], E, W, N, S, NW, SE, gh);
+    if (rec.mask & 2) o += ku[3] * pick(rec.code[2], E, W, N, S, NW, SE, gh) + ku[5] * pick(rec.code[3], E, W, N, S, NW, SE, gh);
+    if (rec.mask & 4) o += ku[6] * pick(rec.code[4], E, W, N, S, NW, SE, gh) + ku[7] * pick(rec.code[5], E, W, N, S, NW, SE, gh);
+    if (rec.mask & 8) o += kd[1] * pick(rec.code[6], E, W, N, S, NW, SE, gh) + kd[2] * pick(rec.code[7], E, W, N, S, NW, SE, gh);
+    if (rec.mask & 16) o += kd[3] * pick(rec.code[8], E, W, N, S, NW, SE, gh) + kd[5] * pick(rec.code[9], E, W, N, S, NW, SE, gh);
+    if (rec.mask & 32) o += kd[6] * pick(rec.code[10], E, W, N, S, NW, SE, gh) + kd[7] * pick(rec.code[11], E, W, N, S, NW, SE, gh);
+    off += o;
+  }
+  return (B - off) / bn.diag;
+}
+
+__global__ void __launch_bounds__(576, 1) k_gs(DevHier2D hd, DevLevel2D lv, double* u, const double* __restrict__ b,
+                                             int sweeps, int* done) {
+  extern __shared__ double smem[];
+  const int n = lv.n, S = lv.S, M = lv.M;
+  const int nwarps = blockDim.x >> 5;
+  double* gh = smem;
+  double* xfer = smem + lv.max_ghosts;                                 // [nwarps][kRing]
+  volatile int* prog = reinterpret_cast<int*>(xfer + nwarps * kRing);  // [nwarps]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int j = tid;
+  const bool row_ok = j <= n;
+  const int len = n - j;
+  const int rowj = row_ok ? dlat(n, 0, j) : 0;
+  const int rowj1 = (j + 1 <= n) ? dlat(n, 0, j + 1) : 0;
+  const int nitems = sweeps * M;
+
+  for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+    const int s = item / M, m = item - s * M;
+    if (tid == 0) {
+      for (int q = hd.nb_lo_ptr[m]; q < hd.nb_lo_ptr[m + 1]; ++q)
+        while (ld_acquire(done + hd.nb_lo[q]) < s + 1) {}
+      for (int q = hd.nb_hi_ptr[m]; q < hd.nb_hi_ptr[m + 1]; ++q)
+        while (ld_acquire(done + hd.nb_hi[q]) < s) {}
+      __threadfence();
+    }
+    __syncthreads();
+    const int gbeg = lv.ghost_ptr[m], gcnt = lv.ghost_ptr[m + 1] - gbeg;
+    for (int g = tid; g < gcnt; g += blockDim.x) gh[g] = __ldcg(u + lv.ghost_off[gbeg + g]);
+    if (tid < nwarps) prog[tid] = 0;
+    __syncthreads();
+
+    double* um = u + static_cast<size_t>(m) * S;
+    const double* bm = b + static_cast<size_t>(m) * S;
+    const BNode* bnm = lv.bnode + static_cast<size_t>(m) * 3 * n;
+    const double* st = lv.stencil + 7 * m;
+    const double s1 = st[1], s2 = st[2], s3 = st[3], s4 = st[4], s5 = st[5], s6 = st[6];
+    const double inv_c = lv.inv_c[m];
+
+    double eR[kPf], nR[kPf], bR[kPf];
+    auto fetch = [&](int t, double& e, double& nn, double& bb) {
+      const int i = t - 2 * j;
+      e = nn = bb = 0.0;
+      if (row_ok && i >= 0 && i <= len) {
+        bb = __ldcg(bm + rowj + i);
+        if (i + 1 <= len) e = __ldcg(um + rowj + i + 1);
+        if (i <= len - 1) nn = __ldcg(um + rowj1 + i);
+      }
+    };
+#pragma unroll
+    for (int k = 0; k < kPf; ++k) fetch(k, eR[k], nR[k], bR[k]);
+
+    double prev = 0.0, se_prev = 0.0, n_prev = 0.0;
+    const int tmax = 2 * n;
+    for (int t0 = 0; t0 <= tmax; t0 += kPf) {
+#pragma unroll
+      for (int k = 0; k < kPf; ++k) {
+        const int t = t0 + k;
+        if (t > tmax) break;
+        const double E = eR[k], N = nR[k], B = bR[k];
+        fetch(t + kPf, eR[k], nR[k], bR[k]);
+        double se = __shfl_up_sync(0xffffffffu, prev, 1);
+        if (warp > 0) {
+          // lane 0 takes row 32w-1's result of step t-1 from the previous warp
+          while (prog[warp - 1] < t) {}
+          __threadfence_block();
+          const double hand = xfer[(warp - 1) * kRing + ((t - 1) & (kRing - 1))];
+          if (lane == 0) se = hand;
+        }
+        const double Sv = se_prev, W = prev, NW = n_prev;
+        const int i = t - 2 * j;
+        double res = 0.0;
+        if (row_ok && i >= 0 && i <= len) {
+          if (j >= 1 && i >= 1 && i <= len - 1) {
+            double acc = s1 * E + s2 * W;
+            acc = acc + s3 * N;
+            acc = acc + s4 * Sv;
+            acc = acc + s5 * NW;
+            acc = acc + s6 * se;
+            res = (B - acc) * inv_c;
+          } else {
+            const BNode bn = bnm[bpos_dev(n, i, j)];
+            res = bn.domain ? B : relax_interface(lv, bn, B, E, W, N, Sv, NW, se, gh);
+            for (int q = 0; q < bn.wr_count; ++q) u[lv.wr[bn.wr_begin + q]] = res;
+          }
+          um[rowj + i] = res;
+        }
+        prev = res;
+        se_prev = se;
+        n_prev = N;
+        if (warp + 1 < nwarps) {
+          // ring overrun guard: the next warp must have consumed step t-kRing+1
+          while (prog[warp + 1] < t - kRing + 2) {}
+          if (lane == 31) xfer[warp * kRing + (t & (kRing - 1))] = res;
+          __syncwarp();
+          __threadfence_block();
+          if (lane == 0) prog[warp] = t + 1;
+        } else if (lane == 0) {
+          prog[warp] = t + 1;
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      st_release(done + m, s + 1);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- estimator
+__device__ __forceinline__ double quad_form(const double* k, double a, double b, double c) {
+  return a * (k[0] * a + k[1] * b + k[2] * c) + b * (k[3] * a + k[4] * b + k[5] * c) +
+         c * (k[6] * a + k[7] * b + k[8] * c);
+}
+
+// One CTA per macro: e_base = u_L - wb and e_coarser = u_L - P wc (inline
+// prolongation from level L-1); per-macro sums of e^T M_T e over all cells
+// (local_l2_norms, proj/src/fem.cpp:327-356) in a fixed reduction order.
+__global__ void k_estimate(DevLevel2D lv, const double* __restrict__ uL, const double* __restrict__ wb,
+                           const double* __restrict__ wc, double* sums) {
+  const int slot = blockIdx.x;
+  const int n = lv.n, S = lv.S, nc = n / 2, Sc = (nc + 1) * (nc + 2) / 2;
+  const double* u = uL + static_cast<size_t>(slot) * S;
+  const double* w1 = wb + static_cast<size_t>(slot) * S;
+  const double* w2 = wc + static_cast<size_t>(slot) * Sc;
+  const double* K = lv.kmass + 18 * slot;  // up == down for the mass matrix
+  double qb = 0.0, qc = 0.0;
+  for (int idx = threadIdx.x; idx < S; idx += blockDim.x) {
+    int i, j;
+    decode(n, idx, i, j);
+    if (i + j > n - 1) continue;
+    const int a = dlat(n, i, j), bq = dlat(n, i + 1, j), c = dlat(n, i, j + 1);
+    const double ua = u[a], ub = u[bq], uc = u[c];
+    const double eba = ua - w1[a], ebb = ub - w1[bq], ebc = uc - w1[c];
+    const double eca = ua - prolong_value(w2, nc, i, j), ecb = ub - prolong_value(w2, nc, i + 1, j),
+                 ecc = uc - prolong_value(w2, nc, i, j + 1);
+    qb += quad_form(K, eba, ebb, ebc);
+    qc += quad_form(K, eca, ecb, ecc);
+    if (i + j <= n - 2) {
+      const int d = dlat(n, i + 1, j + 1);
+      const double ud = u[d];
+      const double ebd = ud - w1[d];
+      const double ecd = ud - prolong_value(w2, nc, i + 1, j + 1);
+      qb += quad_form(K + 9, ebb, ebc, ebd);
+      qc += quad_form(K + 9, ecb, ecc, ecd);
+    }
+  }
+  __shared__ double rb[kThreads], rcq[kThreads];
+  rb[threadIdx.x] = qb;
+  rcq[threadIdx.x] = qc;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      rb[threadIdx.x] += rb[threadIdx.x + w];
+      rcq[threadIdx.x] += rcq[threadIdx.x + w];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    sums[2 * slot] = rb[0];
+    sums[2 * slot + 1] = rcq[0];
+  }
+}
+
+// ---------------------------------------------------------------- misc
+__global__ void k_dot_partial(DevLevel2D lv, const double* a, const double* b, double* partial) {
+  double s = 0.0;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < lv.dot_count; t += gridDim.x * blockDim.x) {
+    const int k = lv.dot_order[t];
+    s += a[k] * b[k];
+  }
+  __shared__ double red[kThreads];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
+}
+
+__global__ void k_dot_final(const double* partial, int count, double* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < count; ++i) s += partial[i];
+    *out = s;
+  }
+}
+
+__global__ void k_sync(DevLevel2D lv, double* f, int additive, int ngroups) {
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < ngroups; g += gridDim.x * blockDim.x) {
+    const int beg = lv.grp_ptr[g], end = lv.grp_ptr[g + 1];
+    if (end - beg < 2) continue;
+    if (additive) {
+      double sum = 0.0;
+      for (int m = beg; m < end; ++m) sum += f[lv.mem_off[m]];
+      for (int m = beg; m < end; ++m) f[lv.mem_off[m]] = sum;
+    } else {
+      const double v = f[lv.mem_off[beg]];
+      for (int m = beg + 1; m < end; ++m) f[lv.mem_off[m]] = v;
+    }
+  }
+}
+
+__global__ void k_axpy(double* y, const double* x, double alpha, long long count) {
+  for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < count;
+       k += static_cast<long long>(gridDim.x) * blockDim.x)
+    y[k] = y[k] + alpha * x[k];
+}
+
+int grid_for(long long total) {
+  long long g = (total + kThreads - 1) / kThreads;
+  if (g < 1) g = 1;
+  if (g > 148 * 32) g = 148 * 32;
+  return static_cast<int>(g);
+}
+
+void check_launch(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) fail(KB_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+}  // namespace
+
+void launch_apply(const DevLevel2D& lv, const double* K, const double* x, double* y, const double* b,
+                  int mode, cudaStream_t st) {
+  k_apply<<<grid_for(static_cast<long long>(lv.M) * lv.S), kThreads, 0, st>>>(lv, K, x, y, b, mode);
+  check_launch("k_apply");
+}
+
+void launch_restrict(const DevLevel2D& fine, const DevLevel2D& coarse, const double* r, double* rc,
+                     int zero_boundary, cudaStream_t st) {
+  k_restrict<<<grid_for(static_cast<long long>(coarse.M) * coarse.S), kThreads, 0, st>>>(fine, coarse, r, rc,
+                                                                                         zero_boundary);
+  check_launch("k_restrict");
+}
+
+void launch_prolong(const DevLevel2D& coarse, const DevLevel2D& fine, const double* c, double* f,
+                    double* next, const double* gbnd, int mode, cudaStream_t st) {
+  k_prolong<<<grid_for(static_cast<long long>(fine.M) * fine.S), kThreads, 0, st>>>(coarse, fine, c, f, next,
+                                                                                    gbnd, mode);
+  check_launch("k_prolong");
+}
+
+void launch_set_boundary(const DevLevel2D& lv, double* f, const double* gbnd, int zero_rest, cudaStream_t st) {
+  k_set_boundary<<<grid_for(static_cast<long long>(lv.M) * lv.S), kThreads, 0, st>>>(lv, f, gbnd, zero_rest);
+  check_launch("k_set_boundary");
+}
+
+void launch_rhs(const DevLevel2D& lv, int src_kind, const double* ftab, double* ftab_scratch,
+                const double* gbnd, double* b, cudaStream_t st) {
+  const double* F = ftab;
+  if (src_kind != SRC_ZERO && src_kind != SRC_TABLE) {
+    const long long SF = static_cast<long long>(2 * lv.n + 1) * (2 * lv.n + 2) / 2;
+    k_ftab<<<grid_for(lv.M * SF), kThreads, 0, st>>>(lv, src_kind, ftab_scratch);
+    check_launch("k_ftab");
+    F = ftab_scratch;
+  }
+  k_rhs<<<grid_for(static_cast<long long>(lv.M) * lv.S), kThreads, 0, st>>>(lv, F, gbnd, b,
+                                                                            src_kind == SRC_ZERO ? 1 : 0);
+  check_launch("k_rhs");
+}
+
+void launch_cg0(const DevLevel2D& lv0, double* u, const double* b, double* scratch, CgParams prm,
+                DevStatus* status, cudaStream_t st) {
+  const size_t N = static_cast<size_t>(lv0.M) * lv0.S;
+  k_cg0<<<1, 256, 0, st>>>(lv0, u, b, scratch, scratch + N, scratch + 2 * N, prm, status);
+  check_launch("k_cg0");
+}
+
+int gs_block_threads(int n) { return 32 * ((n + 1 + 31) / 32); }
+
+void launch_gs(const DevHier2D& hd, const DevLevel2D& lv, double* u, const double* b, int sweeps, int* done,
+               cudaStream_t st) {
+  if (sweeps <= 0) return;
+  const int threads = gs_block_threads(lv.n);
+  if (threads > 576) fail(KB_STRUCTURAL, "wavefront smoother supports n <= 575");
+  const int nwarps = threads / 32;
+  const size_t smem = sizeof(double) * (lv.max_ghosts + nwarps * kRing) + sizeof(int) * nwarps + 16;
+  static std::map<std::pair<int, size_t>, int> occ_cache;
+  static int num_sms = 0;
+  if (num_sms == 0) {
+    int dev = 0;
+    KB_CUDA_CHECK(cudaGetDevice(&dev));
+    KB_CUDA_CHECK(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  if (smem > 48 * 1024)
+    KB_CUDA_CHECK(cudaFuncSetAttribute(k_gs, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  int occ;
+  auto key = std::make_pair(threads, smem);
+  auto it = occ_cache.find(key);
+  if (it == occ_cache.end()) {
+    KB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gs, threads, smem));
+    occ_cache[key] = occ;
+  } else {
+    occ = it->second;
+  }
+  if (occ < 1) fail(KB_CUDA, "k_gs cannot be resident");
+  int grid = lv.M;
+  if (grid > occ * num_sms) grid = occ * num_sms;
+  KB_CUDA_CHECK(cudaMemsetAsync(done, 0, sizeof(int) * lv.M, st));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  KB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_gs, hd, lv, u, b, sweeps, done));
+}
+
+void launch_estimate(const DevLevel2D& lv, const double* uL, const double* wb, const double* wc, double* sums,
+                     cudaStream_t st) {
+  k_estimate<<<lv.M, kThreads, 0, st>>>(lv, uL, wb, wc, sums);
+  check_launch("k_estimate");
+}
+
+void launch_dot(const DevLevel2D& lv, const double* a, const double* b, double* partial, double* out,
+                cudaStream_t st) {
+  const int blocks = 64;
+  k_dot_partial<<<blocks, kThreads, 0, st>>>(lv, a, b, partial);
+  k_dot_final<<<1, 32, 0, st>>>(partial, blocks, out);
+  check_launch("k_dot");
+}
+
+void launch_sync(const DevLevel2D& lv, double* f, int additive, cudaStream_t st) {
+  k_sync<<<grid_for(lv.num_groups), kThreads, 0, st>>>(lv, f, additive, lv.num_groups);
+  check_launch("k_sync");
+}
+
+void launch_axpy(double* y, const double* x, double alpha, std::int64_t count, cudaStream_t st) {
+  k_axpy<<<grid_for(count), kThreads, 0, st>>>(y, x, alpha, count);
+  check_launch("k_axpy");
+}
+
+}  // namespace kb

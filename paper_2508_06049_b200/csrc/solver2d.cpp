@@ -1,0 +1,493 @@
+// Host orchestration of the 2-d hot path.  See solver2d.hpp.
+#include "solver2d.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+namespace kb {
+
+// ------------------------------------------------------------------ arena
+DeviceArena::~DeviceArena() {
+  if (base_) cudaFree(base_);
+}
+
+void DeviceArena::reserve(size_t bytes) {
+  if (base_) fail(KB_INTERNAL, "arena already reserved");
+  cap_ = bytes + 256;
+  const cudaError_t e = cudaMalloc(&base_, cap_);
+  if (e != cudaSuccess) {
+    base_ = nullptr;
+    Error err(KB_RESOURCE, std::string("device allocation failed: ") + cudaGetErrorString(e));
+    throw err;
+  }
+  used_ = 0;
+}
+
+void* DeviceArena::take(size_t bytes) {
+  const size_t off = (used_ + 255) & ~static_cast<size_t>(255);
+  if (off + bytes > cap_) fail(KB_INTERNAL, "device arena exhausted");
+  used_ = off + bytes;
+  return base_ + off;
+}
+
+template <typename T>
+T* DeviceArena::upload(const std::vector<T>& v) {
+  if (v.empty()) return nullptr;
+  T* p = static_cast<T*>(take(v.size() * sizeof(T)));
+  KB_CUDA_CHECK(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return p;
+}
+
+namespace {
+size_t round256(size_t b) { return (b + 255) & ~static_cast<size_t>(255); }
+template <typename T>
+size_t vbytes(const std::vector<T>& v) {
+  return round256(v.size() * sizeof(T));
+}
+}  // namespace
+
+// ------------------------------------------------------------------ hierarchy upload
+std::unique_ptr<DeviceHierarchy2D> DeviceHierarchy2D::create(const Mesh2D& mesh, int max_level) {
+  auto d = std::make_unique<DeviceHierarchy2D>();
+  d->host = Hierarchy2D::build(mesh, max_level);
+  const Hierarchy2D& h = d->host;
+  const int M = h.M;
+  std::vector<std::vector<int>> mem_off(h.L + 1), mem_ij(h.L + 1);
+  std::vector<std::vector<double>> geo(h.L + 1), wq(h.L + 1);
+  size_t bytes = vbytes(h.nb_lo_ptr) + vbytes(h.nb_lo) + vbytes(h.nb_hi_ptr) + vbytes(h.nb_hi);
+  for (int l = 0; l <= h.L; ++l) {
+    const Level2D& lv = h.levels[l];
+    const int n = lv.n;
+    for (size_t k = 0; k < lv.mem_slot.size(); ++k) {
+      mem_off[l].push_back(lv.mem_slot[k] * lv.S + lv.mem_idx[k]);
+      mem_ij[l].push_back(lv.mem_i[k] | (lv.mem_j[k] << 16));
+    }
+    for (int s = 0; s < M; ++s) {
+      const auto& v = mesh.tri[s];
+      // RHS quadrature map, proj/src/fem.cpp:183-186
+      geo[l].push_back(mesh.x[v[0]]);
+      geo[l].push_back(mesh.y[v[0]]);
+      geo[l].push_back((mesh.x[v[1]] - mesh.x[v[0]]) / n);
+      geo[l].push_back((mesh.y[v[1]] - mesh.y[v[0]]) / n);
+      geo[l].push_back((mesh.x[v[2]] - mesh.x[v[0]]) / n);
+      geo[l].push_back((mesh.y[v[2]] - mesh.y[v[0]]) / n);
+      const double cell_area = mesh.area[s] / (static_cast<double>(n) * n);
+      wq[l].push_back(cell_area / 3.0);
+    }
+    bytes += vbytes(lv.node_gid) + vbytes(lv.node_flags) + vbytes(lv.grp_ptr) + vbytes(mem_off[l]) +
+             vbytes(mem_ij[l]) + vbytes(lv.mem_slot) + vbytes(lv.kstiff) + vbytes(lv.kmass) +
+             vbytes(lv.stencil) + vbytes(lv.inv_c) + vbytes(lv.bnode) + vbytes(lv.rec) + vbytes(lv.wr) +
+             vbytes(lv.ghost_ptr) + vbytes(lv.ghost_off) + vbytes(lv.dot_order) + vbytes(geo[l]) +
+             vbytes(wq[l]);
+  }
+  d->arena.reserve(bytes + 4096);
+  d->dh.M = M;
+  d->dh.L = h.L;
+  d->dh.nb_lo_ptr = d->arena.upload(h.nb_lo_ptr);
+  d->dh.nb_lo = d->arena.upload(h.nb_lo);
+  d->dh.nb_hi_ptr = d->arena.upload(h.nb_hi_ptr);
+  d->dh.nb_hi = d->arena.upload(h.nb_hi);
+  for (int l = 0; l <= h.L; ++l) {
+    const Level2D& lv = h.levels[l];
+    DevLevel2D dl{};
+    dl.n = lv.n;
+    dl.S = lv.S;
+    dl.M = M;
+    dl.node_gid = d->arena.upload(lv.node_gid);
+    dl.node_flags = d->arena.upload(lv.node_flags);
+    dl.grp_ptr = d->arena.upload(lv.grp_ptr);
+    dl.mem_off = d->arena.upload(mem_off[l]);
+    dl.mem_ij = d->arena.upload(mem_ij[l]);
+    dl.mem_slot = d->arena.upload(lv.mem_slot);
+    dl.kstiff = d->arena.upload(lv.kstiff);
+    dl.kmass = d->arena.upload(lv.kmass);
+    dl.stencil = d->arena.upload(lv.stencil);
+    dl.inv_c = d->arena.upload(lv.inv_c);
+    dl.bnode = d->arena.upload(lv.bnode);
+    dl.rec = d->arena.upload(lv.rec);
+    dl.wr = d->arena.upload(lv.wr);
+    dl.ghost_ptr = d->arena.upload(lv.ghost_ptr);
+    dl.ghost_off = d->arena.upload(lv.ghost_off);
+    dl.max_ghosts = lv.max_ghosts;
+    dl.num_groups = static_cast<int>(lv.grp_ptr.size()) - 1;
+    dl.dot_order = d->arena.upload(lv.dot_order);
+    dl.dot_count = static_cast<int>(lv.dot_order.size());
+    dl.geo = d->arena.upload(geo[l]);
+    dl.wq = d->arena.upload(wq[l]);
+    d->lev.push_back(dl);
+  }
+  return d;
+}
+
+// ------------------------------------------------------------------ problems
+Problem2D Problem2D::builtin(int kind) {
+  Problem2D p;
+  p.kind = kind;
+  switch (kind) {
+    case PROB_ZERO:
+      p.source = p.boundary = p.exact = [](double, double) { return 0.0; };
+      p.has_exact = true;
+      break;
+    case PROB_SIN2D:
+      // BASELINE.json config 1: u = sin(pi x) sin(pi y), f = 2 pi^2 u
+      p.exact = [](double x, double y) { return std::sin(M_PI * x) * std::sin(M_PI * y); };
+      p.source = [](double x, double y) {
+        return 2.0 * M_PI * M_PI * std::sin(M_PI * x) * std::sin(M_PI * y);
+      };
+      p.boundary = p.exact;
+      p.has_exact = true;
+      break;
+    case PROB_LSHAPE:
+      // make_lshape_spec, proj/src/problems.cpp:36-53
+      p.exact = [](double x, double y) {
+        const double r = std::hypot(x, y);
+        if (r == 0.0) return 0.0;
+        double phi = std::atan2(y, x);
+        if (phi < 0.0) phi += 2.0 * M_PI;
+        return std::pow(r, 2.0 / 3.0) * std::sin(2.0 * phi / 3.0);
+      };
+      p.source = [](double, double) { return 0.0; };
+      p.boundary = p.exact;
+      p.has_exact = true;
+      break;
+    default:
+      fail(KB_STRUCTURAL, "unknown built-in problem kind");
+  }
+  return p;
+}
+
+// ------------------------------------------------------------------ solver
+Solver2D::Solver2D(std::shared_ptr<DeviceHierarchy2D> h, Problem2D p, SolverConfig2D cfg)
+    : H_(std::move(h)), prob_(std::move(p)), cfg_(cfg) {
+  const Hierarchy2D& hh = H_->host;
+  L_ = hh.L;
+  const int M = hh.M;
+  if (cfg_.finest_policy != 0)
+    fail(KB_STRUCTURAL, "only FinestPolicy::None is available on the device path");
+  if (prob_.kind == PROB_ZERO || prob_.kind == PROB_LSHAPE)
+    src_kind_ = SRC_ZERO;
+  else if (prob_.kind == PROB_SIN2D && !cfg_.faithful_source)
+    src_kind_ = SRC_SIN2D;
+  else
+    src_kind_ = SRC_TABLE;
+
+  auto lsize = [&](int l) { return static_cast<size_t>(M) * hh.levels[l].S; };
+  auto fsize = [&](int l) {
+    const size_t n2 = 2 * static_cast<size_t>(hh.levels[l].n);
+    return static_cast<size_t>(M) * (n2 + 1) * (n2 + 2) / 2;
+  };
+  size_t bytes = 0;
+  for (int l = 0; l <= L_; ++l) {
+    bytes += 2 * round256(lsize(l) * 8);                               // u, b
+    if (l < L_) bytes += round256(lsize(l + 1) * 8) + 2 * round256(lsize(l) * 8);  // w, vu, vb
+    if (l >= 1) bytes += round256(lsize(l) * 8);                       // r
+    bytes += round256(static_cast<size_t>(M) * 3 * hh.levels[l].n * 8);  // gbnd
+    if (src_kind_ != SRC_ZERO) bytes += round256(fsize(l) * 8);
+  }
+  bytes += round256(3 * lsize(0) * 8) + round256(2 * M * 8) + round256(lsize(L_) * 8) +
+           round256(lsize(std::max(L_ - 1, 0)) * 8) + round256(64 * 8) + round256(8) +
+           round256(sizeof(DevStatus)) + round256(M * 4);
+  arena_.reserve(bytes);
+  u_.assign(L_ + 1, nullptr);
+  b_.assign(L_ + 1, nullptr);
+  w_.assign(L_ + 1, nullptr);
+  vu_.assign(L_ + 1, nullptr);
+  vb_.assign(L_ + 1, nullptr);
+  r_.assign(L_ + 1, nullptr);
+  gbnd_.assign(L_ + 1, nullptr);
+  ftab_.assign(L_ + 1, nullptr);
+  for (int l = 0; l <= L_; ++l) {
+    u_[l] = static_cast<double*>(arena_.take(lsize(l) * 8));
+    b_[l] = static_cast<double*>(arena_.take(lsize(l) * 8));
+    if (l < L_) {
+      w_[l] = static_cast<double*>(arena_.take(lsize(l + 1) * 8));
+      vu_[l] = static_cast<double*>(arena_.take(lsize(l) * 8));
+      vb_[l] = static_cast<double*>(arena_.take(lsize(l) * 8));
+    }
+    if (l >= 1) r_[l] = static_cast<double*>(arena_.take(lsize(l) * 8));
+    gbnd_[l] = static_cast<double*>(arena_.take(static_cast<size_t>(M) * 3 * hh.levels[l].n * 8));
+    if (src_kind_ != SRC_ZERO) ftab_[l] = static_cast<double*>(arena_.take(fsize(l) * 8));
+  }
+  cg_scratch_ = static_cast<double*>(arena_.take(3 * lsize(0) * 8));
+  est_sums_ = static_cast<double*>(arena_.take(2 * M * 8));
+  est_tmp_a_ = static_cast<double*>(arena_.take(lsize(L_) * 8));
+  est_tmp_b_ = static_cast<double*>(arena_.take(lsize(std::max(L_ - 1, 0)) * 8));
+  dot_partial_ = static_cast<double*>(arena_.take(64 * 8));
+  dot_out_ = static_cast<double*>(arena_.take(8));
+  status_ = static_cast<DevStatus*>(arena_.take(sizeof(DevStatus)));
+  gs_done_ = static_cast<int*>(arena_.take(M * 4));
+
+  KB_CUDA_CHECK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  KB_CUDA_CHECK(cudaMallocHost(&status_host_, sizeof(DevStatus)));
+  KB_CUDA_CHECK(cudaMallocHost(&sums_host_, 2 * M * sizeof(double)));
+
+  // Dirichlet data: g at the owner copy's node coordinates for every
+  // domain-boundary copy (set_domain_boundary_values + ReplaceFromOwner,
+  // proj/src/fem.cpp:212-228), evaluated with the host libm like the reference.
+  for (int l = 0; l <= L_; ++l) {
+    const Level2D& lv = hh.levels[l];
+    const int n = lv.n;
+    std::vector<double> g(static_cast<size_t>(M) * 3 * n, 0.0);
+    for (int s = 0; s < M; ++s) {
+      auto visit = [&](int i, int j) {
+        if (!hh.on_domain_boundary(s, l, i, j)) return;
+        const int gid = hh.boundary_group(s, l, i, j);
+        const int first = lv.grp_ptr[gid];
+        double x, y;
+        hh.node_coordinates(lv.mem_slot[first], l, lv.mem_i[first], lv.mem_j[first], x, y);
+        g[static_cast<size_t>(s) * 3 * n + bpos(n, i, j)] = prob_.boundary(x, y);
+      };
+      for (int i = 0; i <= n; ++i) visit(i, 0);
+      for (int j = 1; j <= n; ++j) visit(0, j);
+      for (int j = 1; j <= n - 1; ++j) visit(n - j, j);
+    }
+    KB_CUDA_CHECK(cudaMemcpy(gbnd_[l], g.data(), g.size() * 8, cudaMemcpyHostToDevice));
+    if (src_kind_ == SRC_TABLE) {
+      // f at the cell edge midpoints through the RHS map (proj/src/fem.cpp:183-194)
+      const int n2 = 2 * n;
+      const int SF = lattice_size(n2);
+      std::vector<double> f(static_cast<size_t>(M) * SF, 0.0);
+      for (int s = 0; s < M; ++s) {
+        const auto& v = hh.mesh.tri[s];
+        const double c0x = hh.mesh.x[v[0]], c0y = hh.mesh.y[v[0]];
+        const double ux = (hh.mesh.x[v[1]] - c0x) / n, uy = (hh.mesh.y[v[1]] - c0y) / n;
+        const double wx = (hh.mesh.x[v[2]] - c0x) / n, wy = (hh.mesh.y[v[2]] - c0y) / n;
+        for (int J = 0; J <= n2; ++J)
+          for (int I = 0; I <= n2 - J; ++I) {
+            if (((I | J) & 1) == 0) continue;  // only edge midpoints are used
+            const double hi = 0.5 * I, hj = 0.5 * J;
+            f[static_cast<size_t>(s) * SF + lattice_index(n2, I, J)] =
+                prob_.source(c0x + hi * ux + hj * wx, c0y + hi * uy + hj * wy);
+          }
+      }
+      KB_CUDA_CHECK(cudaMemcpy(ftab_[l], f.data(), f.size() * 8, cudaMemcpyHostToDevice));
+    }
+  }
+  KB_CUDA_CHECK(cudaMemset(status_, 0, sizeof(DevStatus)));
+}
+
+Solver2D::~Solver2D() {
+  if (exec_) cudaGraphExecDestroy(exec_);
+  if (stream_) cudaStreamDestroy(stream_);
+  if (status_host_) cudaFreeHost(status_host_);
+  if (sums_host_) cudaFreeHost(sums_host_);
+}
+
+size_t Solver2D::level_size(int level) const {
+  return static_cast<size_t>(H_->host.M) * H_->host.levels.at(level).S;
+}
+
+double* Solver2D::state(int which, int level) {
+  if (level < 0 || level > L_) fail(KB_STRUCTURAL, "level out of range");
+  if (which == 0) return u_[level];
+  if (which == 1) return b_[level];
+  if (which == 2) {
+    if (level < 1) fail(KB_STRUCTURAL, "w lives on levels 1..L");
+    return w_[level - 1];
+  }
+  fail(KB_STRUCTURAL, "unknown state component");
+}
+
+void Solver2D::vcycle(int l, double* u, const double* b) {
+  // v_cycle, proj/src/multigrid.cpp:231-246
+  const auto& lev = H_->lev;
+  if (l == 0) {
+    launch_cg0(lev[0], u, b, cg_scratch_, {cfg_.coarse_rel_tol, cfg_.coarse_abs_floor, cfg_.coarse_max_iter},
+               status_, stream_);
+    count_launch();
+    return;
+  }
+  launch_gs(H_->dh, lev[l], u, b, cfg_.pre_smooth, gs_done_, stream_);
+  count_launch(cfg_.pre_smooth > 0);
+  launch_apply(lev[l], lev[l].kstiff, u, r_[l], b, APPLY_RESIDUAL, stream_);
+  launch_restrict(lev[l], lev[l - 1], r_[l], vb_[l - 1], 1, stream_);
+  KB_CUDA_CHECK(cudaMemsetAsync(vu_[l - 1], 0, level_size(l - 1) * 8, stream_));
+  count_launch(2);
+  vcycle(l - 1, vu_[l - 1], vb_[l - 1]);
+  launch_prolong(lev[l - 1], lev[l], vu_[l - 1], u, nullptr, nullptr, PROLONG_ADD, stream_);
+  launch_gs(H_->dh, lev[l], u, b, cfg_.post_smooth, gs_done_, stream_);
+  count_launch(1 + (cfg_.post_smooth > 0));
+}
+
+void Solver2D::enqueue_fmg_body() {
+  // MultigridSolver::fmg, proj/src/multigrid.cpp:248-279
+  const auto& lev = H_->lev;
+  launches_ = 0;
+  KB_CUDA_CHECK(cudaMemsetAsync(status_, 0, sizeof(DevStatus), stream_));
+  for (int l = 0; l <= L_; ++l) {
+    launch_rhs(lev[l], src_kind_, ftab_[l], ftab_[l], gbnd_[l], b_[l], stream_);
+    count_launch(src_kind_ == SRC_SIN2D ? 2 : 1);
+  }
+  launch_set_boundary(lev[0], u_[0], gbnd_[0], 1, stream_);
+  count_launch();
+  launch_cg0(lev[0], u_[0], b_[0], cg_scratch_, {cfg_.coarse_rel_tol, cfg_.coarse_abs_floor, cfg_.coarse_max_iter},
+             status_, stream_);
+  count_launch();
+  for (int l = 0; l < L_; ++l) {
+    // w[l] = P u[l] (snapshot before the Dirichlet reset); next = w with g on the boundary
+    launch_prolong(lev[l], lev[l + 1], u_[l], w_[l], u_[l + 1], gbnd_[l + 1], PROLONG_W_NEXT, stream_);
+    count_launch();
+    for (int c = 0; c < cfg_.nu; ++c) vcycle(l + 1, u_[l + 1], b_[l + 1]);
+  }
+  fmg_launches_ = launches_;
+}
+
+void Solver2D::fmg_enqueue() {
+  if (L_ < 1) fail(KB_STRUCTURAL, "full multigrid requires at least one level above the coarse grid");
+  if (!cfg_.use_graph) {
+    enqueue_fmg_body();
+    return;
+  }
+  if (!exec_) {
+    cudaGraph_t graph = nullptr;
+    KB_CUDA_CHECK(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+    try {
+      enqueue_fmg_body();
+    } catch (...) {
+      cudaStreamEndCapture(stream_, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      throw;
+    }
+    KB_CUDA_CHECK(cudaStreamEndCapture(stream_, &graph));
+    KB_CUDA_CHECK(cudaGraphInstantiate(&exec_, graph, 0));
+    cudaGraphDestroy(graph);
+  }
+  KB_CUDA_CHECK(cudaGraphLaunch(exec_, stream_));
+}
+
+void Solver2D::sync_and_check() {
+  KB_CUDA_CHECK(cudaMemcpyAsync(status_host_, status_, sizeof(DevStatus), cudaMemcpyDeviceToHost, stream_));
+  KB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+  if (status_host_->code == 1) {
+    Error e(KB_SOLVER, "coarse-grid CG did not converge");
+    e.residual = status_host_->residual;
+    throw e;
+  }
+  if (status_host_->code == 2) {
+    Error e(KB_SOLVER, "coarse-grid CG lost positive definiteness");
+    e.residual = status_host_->residual;
+    throw e;
+  }
+}
+
+int Solver2D::last_cg_iters() const { return status_host_ ? status_host_->iters : 0; }
+
+void Solver2D::fmg() {
+  fmg_enqueue();
+  sync_and_check();
+}
+
+void Solver2D::estimate_enqueue(int offset) {
+  // error_estimate, proj/src/estimator.cpp:8-29
+  if (offset < 1 || offset > L_ - 1) fail(KB_STRUCTURAL, "estimate offset must satisfy 1 <= j <= L-1");
+  const auto& lev = H_->lev;
+  const int base = L_ - offset;
+  // e_base = u_L - prolongate_to(w[base], L): w[base] lives on level base+1
+  const double* wb = w_[base];
+  for (int l = base + 1; l < L_; ++l) {
+    double* dst = (l + 1 == L_) ? est_tmp_a_ : vu_[l + 1];
+    launch_prolong(lev[l], lev[l + 1], wb, dst, nullptr, nullptr, PROLONG_ASSIGN, stream_);
+    wb = dst;
+  }
+  // e_coarser = u_L - prolongate_to(w[base-1], L); the last prolongation is inline
+  const double* wc = w_[base - 1];
+  for (int l = base; l < L_ - 1; ++l) {
+    double* dst = (l + 1 == L_ - 1) ? est_tmp_b_ : vb_[l + 1];
+    launch_prolong(lev[l], lev[l + 1], wc, dst, nullptr, nullptr, PROLONG_ASSIGN, stream_);
+    wc = dst;
+  }
+  launch_estimate(lev[L_], u_[L_], wb, wc, est_sums_, stream_);
+  KB_CUDA_CHECK(cudaMemcpyAsync(sums_host_, est_sums_, 2 * H_->host.M * sizeof(double), cudaMemcpyDeviceToHost,
+                                stream_));
+}
+
+EstimateReport2D Solver2D::estimate_finish(int offset, int kind) {
+  KB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+  const int M = H_->host.M;
+  EstimateReport2D rep;
+  rep.offset = offset;
+  rep.base_level = L_ - offset;
+  rep.kind = kind;
+  double gb = 0.0, gc = 0.0;
+  for (int s = 0; s < M; ++s) {
+    gb += sums_host_[2 * s];
+    gc += sums_host_[2 * s + 1];
+  }
+  rep.norm_base = std::sqrt(std::max(0.0, gb));
+  rep.norm_coarser = std::sqrt(std::max(0.0, gc));
+  rep.conv_factor = rep.norm_coarser > 0.0 ? rep.norm_base / rep.norm_coarser : 0.0;
+  rep.eta = std::pow(rep.conv_factor, offset) * rep.norm_base;
+  rep.eta_local.resize(M);
+  const double floor = 1e-14 * rep.norm_coarser;
+  for (int s = 0; s < M; ++s) {
+    const double lb = std::sqrt(std::max(0.0, sums_host_[2 * s]));
+    if (kind == 0) {
+      rep.eta_local[s] = lb;
+    } else {
+      const double lc = std::sqrt(std::max(0.0, sums_host_[2 * s + 1]));
+      const double conv_t = lc > floor ? lb / lc : rep.conv_factor;
+      rep.eta_local[s] = std::pow(conv_t, offset) * lb;
+    }
+  }
+  return rep;
+}
+
+EstimateReport2D Solver2D::estimate(int offset, int kind) {
+  estimate_enqueue(offset);
+  return estimate_finish(offset, kind);
+}
+
+// ------------------------------------------------------------------ single operations
+void Solver2D::apply(int level, int op_mass, const double* x, double* y) {
+  const auto& lv = H_->lev.at(level);
+  launch_apply(lv, op_mass ? lv.kmass : lv.kstiff, x, y, nullptr, APPLY_PLAIN, stream_);
+  KB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+}
+
+void Solver2D::residual(int level, const double* u, const double* b, double* r) {
+  const auto& lv = H_->lev.at(level);
+  launch_apply(lv, lv.kstiff, u, r, b, APPLY_RESIDUAL, stream_);
+  KB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+}
+
+void Solver2D::gauss_seidel(int level, double* u, const double* b, int sweeps) {
+  if (level < 1) fail(KB_STRUCTURAL, "Gauss-Seidel runs on levels >= 1");
+  launch_gs(H_->dh, H_->lev.at(level), u, b, sweeps, gs_done_, stream_);
+  KB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+}
+
+void Solver2D::restrict_to(int fine_level, const double* r, double* rc) {
+  if (fine_level < 1) fail(KB_STRUCTURAL, "restriction below level 0");
+  launch_restrict(H_->lev.at(fine_level), H_->lev.at(fine_level - 1), r, rc, 0, stream_);
+  KB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+}
+
+void Solver2D::prolongate(int coarse_level, const double* c, double* f) {
+  if (coarse_level + 1 > L_) fail(KB_STRUCTURAL, "prolongation beyond the finest level");
+  launch_prolong(H_->lev.at(coarse_level), H_->lev.at(coarse_level + 1), c, f, nullptr, nullptr, PROLONG_ASSIGN,
+                 stream_);
+  KB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+}
+
+void Solver2D::cg_level0(double* u, const double* b) {
+  KB_CUDA_CHECK(cudaMemsetAsync(status_, 0, sizeof(DevStatus), stream_));
+  launch_cg0(H_->lev.at(0), u, b, cg_scratch_, {cfg_.coarse_rel_tol, cfg_.coarse_abs_floor, cfg_.coarse_max_iter},
+             status_, stream_);
+  sync_and_check();
+}
+
+double Solver2D::dot_unique(int level, const double* a, const double* b) {
+  launch_dot(H_->lev.at(level), a, b, dot_partial_, dot_out_, stream_);
+  double out = 0.0;
+  KB_CUDA_CHECK(cudaMemcpyAsync(&out, dot_out_, 8, cudaMemcpyDeviceToHost, stream_));
+  KB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+  return out;
+}
+
+void Solver2D::interface_sync(int level, double* f, int additive) {
+  launch_sync(H_->lev.at(level), f, additive, stream_);
+  KB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+}
+
+}  // namespace kb

@@ -1,0 +1,136 @@
+// Host orchestration of the 2-d hot path: device-resident hierarchy, problem
+// data, and the FMG / V-cycle / estimator drivers that enqueue the sm_100a
+// kernels of kernels2d.cu on one CUDA stream (optionally as a CUDA graph).
+//
+// Mirrors MultigridSolver (proj/include/klref/multigrid.hpp:64-99,
+// proj/src/multigrid.cpp:113-321) and error_estimate
+// (proj/src/estimator.cpp:8-45).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <functional>
+#include <memory>
+#include <vector>
+
+#include "dev2d.hpp"
+#include "hier2d.hpp"
+
+namespace kb {
+
+// Bump allocator over one cudaMalloc'd arena.
+class DeviceArena {
+ public:
+  DeviceArena() = default;
+  DeviceArena(const DeviceArena&) = delete;
+  DeviceArena& operator=(const DeviceArena&) = delete;
+  ~DeviceArena();
+  void reserve(size_t bytes);
+  void* take(size_t bytes);
+  template <typename T>
+  T* upload(const std::vector<T>& v);
+  size_t used() const { return used_; }
+
+ private:
+  char* base_ = nullptr;
+  size_t cap_ = 0, used_ = 0;
+};
+
+struct DeviceHierarchy2D {
+  Hierarchy2D host;
+  std::vector<DevLevel2D> lev;
+  DevHier2D dh{};
+  int* gs_done = nullptr;
+  DeviceArena arena;
+  static std::unique_ptr<DeviceHierarchy2D> create(const Mesh2D& mesh, int max_level);
+};
+
+enum ProblemKind : int { PROB_ZERO = 0, PROB_SIN2D = 1, PROB_LSHAPE = 2, PROB_HOST = 3 };
+
+struct Problem2D {
+  int kind = PROB_ZERO;
+  std::function<double(double, double)> source;    // host (glibc) evaluation
+  std::function<double(double, double)> boundary;
+  std::function<double(double, double)> exact;
+  bool has_exact = false;
+  static Problem2D builtin(int kind);
+};
+
+struct SolverConfig2D {
+  int nu = 2, pre_smooth = 2, post_smooth = 2;
+  double coarse_rel_tol = 1e-9, coarse_abs_floor = 1e-12;
+  int coarse_max_iter = 100000;
+  int finest_policy = 0;  // 0 = None (the only device policy so far)
+  int faithful_source = 0;  // 1: host-tabulated f (bitwise-faithful RHS)
+  int use_graph = 1;
+};
+
+struct EstimateReport2D {
+  int offset = 1, base_level = 0, kind = 0;
+  double norm_coarser = 0.0, norm_base = 0.0, conv_factor = 0.0, eta = 0.0;
+  std::vector<double> eta_local;
+};
+
+class Solver2D {
+ public:
+  Solver2D(std::shared_ptr<DeviceHierarchy2D> h, Problem2D p, SolverConfig2D cfg);
+  ~Solver2D();
+
+  const Hierarchy2D& hier() const { return H_->host; }
+  cudaStream_t stream() const { return stream_; }
+
+  // FMG (proj/src/multigrid.cpp:248-321) into the solver-owned FmgState.
+  void fmg_enqueue();
+  void fmg();
+  void sync_and_check();
+  EstimateReport2D estimate(int offset, int kind);
+  void estimate_enqueue(int offset);
+  EstimateReport2D estimate_finish(int offset, int kind);
+
+  // state access: which 0 = u, 1 = b, 2 = w (w[l] lives on level l+1)
+  double* state(int which, int level);
+  size_t level_size(int level) const;
+
+  // single operations on device arrays (API parity with the reference)
+  void apply(int level, int op_mass, const double* x, double* y);
+  void residual(int level, const double* u, const double* b, double* r);
+  void gauss_seidel(int level, double* u, const double* b, int sweeps);
+  void restrict_to(int fine_level, const double* r, double* rc);
+  void prolongate(int coarse_level, const double* c, double* f);
+  void cg_level0(double* u, const double* b);
+  double dot_unique(int level, const double* a, const double* b);
+  void interface_sync(int level, double* f, int additive);
+  int launches_per_fmg() const { return fmg_launches_; }
+  int last_cg_iters() const;
+
+ private:
+  void vcycle(int l, double* u, const double* b);
+  void enqueue_fmg_body();
+  int count_launch(int k = 1) {
+    launches_ += k;
+    return launches_;
+  }
+
+  std::shared_ptr<DeviceHierarchy2D> H_;
+  Problem2D prob_;
+  SolverConfig2D cfg_;
+  cudaStream_t stream_ = nullptr;
+  DeviceArena arena_;
+  int L_ = 0;
+  std::vector<double*> u_, b_, w_, vu_, vb_, r_, gbnd_, ftab_;
+  double* cg_scratch_ = nullptr;
+  double* est_sums_ = nullptr;
+  double* est_tmp_a_ = nullptr;
+  double* est_tmp_b_ = nullptr;
+  double* dot_partial_ = nullptr;
+  double* dot_out_ = nullptr;
+  DevStatus* status_ = nullptr;
+  int* gs_done_ = nullptr;
+  DevStatus* status_host_ = nullptr;
+  double* sums_host_ = nullptr;
+  int src_kind_ = SRC_ZERO;
+  cudaGraphExec_t exec_ = nullptr;
+  int launches_ = 0, fmg_launches_ = 0;
+};
+
+}  // namespace kb

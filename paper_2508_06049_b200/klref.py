@@ -1,0 +1,532 @@
+"""Python mirror of the reference's hot-path API over the C-ABI of libklref_b200.so.
+
+The names follow the reference's C++ interface (proj/include/klref/*.hpp):
+``GridHierarchy.build`` (hhg.hpp:78), ``MultigridSolver`` / ``fmg`` /
+``gauss_seidel`` / ``residual`` / ``cg_level0`` (multigrid.hpp:64-99),
+``OperatorP1.apply`` (fem.hpp:26-40), ``restrict_transpose`` / ``prolongate``
+(multigrid.hpp:56-60), ``dot_unique`` / ``interface_sync`` (hhg.hpp:134-137),
+``error_estimate`` (estimator.hpp:26).  Errors raise the Python counterparts of
+proj/include/klref/errors.hpp.  Every compute call runs the sm_100a kernels;
+there is no CPU fallback (a missing library or device raises).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libklref_b200.so")
+
+
+# ---------------------------------------------------------------- errors
+class KlrefError(RuntimeError):
+    code = -1
+
+
+class StructuralError(KlrefError):
+    code = 1
+
+
+class DomainError(KlrefError):
+    code = 2
+
+
+class SolverError(KlrefError):
+    code = 3
+
+    def __init__(self, msg, last_residual=0.0):
+        super().__init__(msg)
+        self.last_residual = last_residual
+
+
+class IoError(KlrefError):
+    code = 4
+
+
+class InternalError(KlrefError):
+    code = 5
+
+
+class ResourceError(KlrefError):
+    code = 6
+
+    def __init__(self, msg, level=-1):
+        super().__init__(msg)
+        self.level = level
+
+
+class CudaError(KlrefError):
+    code = 7
+
+
+_ERRORS = {1: StructuralError, 2: DomainError, 3: SolverError, 4: IoError, 5: InternalError,
+           6: ResourceError, 7: CudaError}
+
+STIFFNESS, MASS = 0, 1
+UNSCALED, SCALED = 0, 1
+SYNC_REPLACE, SYNC_ADDITIVE = 0, 1
+STATE_U, STATE_B, STATE_W = 0, 1, 2
+PROBLEM_ZERO, PROBLEM_SIN2D, PROBLEM_LSHAPE = 0, 1, 2
+MARK_TOP_FRACTION, MARK_HALF_MAX = 0, 1
+
+
+class SolverConfigC(C.Structure):
+    _fields_ = [("nu", C.c_int), ("pre_smooth", C.c_int), ("post_smooth", C.c_int),
+                ("coarse_rel_tol", C.c_double), ("coarse_abs_floor", C.c_double),
+                ("coarse_max_iter", C.c_int), ("finest_policy", C.c_int),
+                ("faithful_source", C.c_int), ("use_graph", C.c_int)]
+
+
+class EstimateReportC(C.Structure):
+    _fields_ = [("offset", C.c_int), ("base_level", C.c_int), ("kind", C.c_int),
+                ("norm_coarser", C.c_double), ("norm_base", C.c_double),
+                ("conv_factor", C.c_double), ("eta", C.c_double)]
+
+
+_lib = None
+
+# exported symbols and their ctypes signatures (include/klref_b200.h)
+_P = C.c_void_p
+_I = C.c_int
+_D = C.c_double
+_PI = C.POINTER(C.c_int)
+_PD = C.POINTER(C.c_double)
+_PP = C.POINTER(C.c_void_p)
+_PI64 = C.POINTER(C.c_int64)
+SIGNATURES = {
+    "klref_last_error": (C.c_char_p, []),
+    "klref_last_error_residual": (_D, []),
+    "klref_last_error_level": (_I, []),
+    "klref_abi_version": (_I, []),
+    "klref_mesh_create": (_I, [_I, _I, _PD, _I, _PI, _PP]),
+    "klref_mesh_destroy": (None, [_P]),
+    "klref_hierarchy_build": (_I, [_P, _I, _PP]),
+    "klref_hierarchy_build_host": (_I, [_P, _I, _PP]),
+    "klref_hierarchy_destroy": (None, [_P]),
+    "klref_hierarchy_num_macros": (_I, [_P, _PI]),
+    "klref_hierarchy_max_level": (_I, [_P, _PI]),
+    "klref_hierarchy_dof_count": (_I, [_P, _I, _PI64]),
+    "klref_hierarchy_fine_element_count": (_I, [_P, _I, _PI64]),
+    "klref_hierarchy_lattice_size": (_I, [_P, _I, _PI]),
+    "klref_hierarchy_dag_depth": (_I, [_P, _PI]),
+    "klref_hierarchy_groups": (_I, [_P, _I, _PI, _PI, _PI, _PI]),
+    "klref_hierarchy_element_matrices": (_I, [_P, _I, _I, _PD, _PD]),
+    "klref_problem_create": (_I, [_I, _PP]),
+    "klref_problem_create_host": (_I, [_P, _P, _P, _PP]),
+    "klref_problem_destroy": (None, [_P]),
+    "klref_solver_config_default": (None, [C.POINTER(SolverConfigC)]),
+    "klref_solver_create": (_I, [_P, _P, C.POINTER(SolverConfigC), _PP]),
+    "klref_solver_destroy": (None, [_P]),
+    "klref_solver_fmg": (_I, [_P]),
+    "klref_solver_fmg_enqueue": (_I, [_P]),
+    "klref_solver_synchronize": (_I, [_P]),
+    "klref_solver_stream": (_I, [_P, _PP]),
+    "klref_solver_launch_count": (_I, [_P, _PI]),
+    "klref_solver_last_cg_iterations": (_I, [_P, _PI]),
+    "klref_solver_state_read": (_I, [_P, _I, _I, _PD]),
+    "klref_error_estimate": (_I, [_P, _I, _I, C.POINTER(EstimateReportC), _PD]),
+    "klref_error_estimate_enqueue": (_I, [_P, _I]),
+    "klref_error_estimate_finish": (_I, [_P, _I, _I, C.POINTER(EstimateReportC), _PD]),
+    "klref_gf_create": (_I, [_P, _I, _PP]),
+    "klref_gf_destroy": (None, [_P]),
+    "klref_gf_upload": (_I, [_P, _PD]),
+    "klref_gf_download": (_I, [_P, _PD]),
+    "klref_apply": (_I, [_P, _I, _P, _P]),
+    "klref_residual": (_I, [_P, _P, _P, _P]),
+    "klref_gauss_seidel": (_I, [_P, _P, _P, _I]),
+    "klref_restrict_transpose": (_I, [_P, _P, _P]),
+    "klref_prolongate": (_I, [_P, _P, _P]),
+    "klref_cg_level0": (_I, [_P, _P, _P]),
+    "klref_dot_unique": (_I, [_P, _P, _P, _PD]),
+    "klref_interface_sync": (_I, [_P, _P, _I]),
+    "klref_mark": (_I, [_I, _D, _I, _PI, _PI, _PD, _I, _PI, _PI, _PI]),
+}
+
+
+def lib():
+    """Load libklref_b200.so (raises if it was not built: no fallback path)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing; run __graft_entry__.build() (make -C csrc)")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc == 0:
+        return
+    L = lib()
+    msg = L.klref_last_error().decode()
+    cls = _ERRORS.get(rc, KlrefError)
+    if cls is SolverError:
+        raise SolverError(msg, L.klref_last_error_residual())
+    if cls is ResourceError:
+        raise ResourceError(msg, L.klref_last_error_level())
+    raise cls(msg)
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(_PD)
+
+
+def _iptr(a: np.ndarray):
+    return a.ctypes.data_as(_PI)
+
+
+# ---------------------------------------------------------------- lattice helpers
+def lattice_index(n: int, i: int, j: int) -> int:
+    """proj/include/klref/hhg.hpp:13"""
+    return j * (n + 1) - (j * (j - 1)) // 2 + i
+
+
+def lattice_size(n: int) -> int:
+    return (n + 1) * (n + 2) // 2
+
+
+# ---------------------------------------------------------------- mesh
+@dataclass
+class MacroMesh:
+    """Active conforming macro mesh: coords[nv, 2], elements[ne, 3] (slot order)."""
+    coords: np.ndarray
+    elements: np.ndarray
+    dim: int = 2
+
+    @staticmethod
+    def read(path: str) -> "MacroMesh":
+        """ASCII format of proj/include/klref/mesh_io.hpp:14-22 (read_mesh, mesh_io.cpp:31-96)."""
+        lines = []
+        with open(path) as fh:
+            for ln in fh:
+                s = ln.strip()
+                if s and not s.startswith("#"):
+                    lines.append(s)
+        it = iter(lines)
+        tag, dim = next(it).split()
+        if tag != "dim":
+            raise IoError("expected 'dim d' header")
+        dim = int(dim)
+        tag, nv = next(it).split()
+        nv = int(nv)
+        ids, coords = [], []
+        for _ in range(nv):
+            parts = next(it).split()
+            ids.append(int(parts[0]))
+            coords.append([float(v) for v in parts[1:1 + dim]])
+        idmap = {v: k for k, v in enumerate(ids)}
+        tag, ne = next(it).split()
+        elements = []
+        for _ in range(int(ne)):
+            parts = next(it).split()
+            elements.append([idmap[int(v)] for v in parts[1:2 + dim]])
+        return MacroMesh(np.array(coords, dtype=np.float64), np.array(elements, dtype=np.int32), dim)
+
+
+class _Handle:
+    _destroy = None
+
+    def __init__(self, ptr):
+        self._ptr = ptr
+
+    @property
+    def ptr(self):
+        return self._ptr
+
+    def close(self):
+        if self._ptr:
+            getattr(lib(), self._destroy)(self._ptr)
+            self._ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Mesh(_Handle):
+    _destroy = "klref_mesh_destroy"
+
+    def __init__(self, mm: MacroMesh):
+        out = C.c_void_p()
+        coords = np.ascontiguousarray(mm.coords, dtype=np.float64)
+        els = np.ascontiguousarray(mm.elements, dtype=np.int32)
+        _check(lib().klref_mesh_create(mm.dim, coords.shape[0], _dptr(coords), els.shape[0], _iptr(els),
+                                       C.byref(out)))
+        super().__init__(out.value)
+        self.macro = mm
+
+
+class GridHierarchy(_Handle):
+    """GridHierarchy (proj/include/klref/hhg.hpp:56-128), device resident."""
+    _destroy = "klref_hierarchy_destroy"
+
+    @staticmethod
+    def build(mesh: MacroMesh, max_level: int, device: bool = True) -> "GridHierarchy":
+        m = Mesh(mesh)
+        out = C.c_void_p()
+        fn = lib().klref_hierarchy_build if device else lib().klref_hierarchy_build_host
+        _check(fn(m.ptr, max_level, C.byref(out)))
+        h = GridHierarchy(out.value)
+        h.mesh = m
+        return h
+
+    def _int(self, fn, *args):
+        v = C.c_int()
+        _check(fn(self.ptr, *args, C.byref(v)))
+        return v.value
+
+    def _i64(self, fn, *args):
+        v = C.c_int64()
+        _check(fn(self.ptr, *args, C.byref(v)))
+        return v.value
+
+    def num_macros(self):
+        return self._int(lib().klref_hierarchy_num_macros)
+
+    def max_level(self):
+        return self._int(lib().klref_hierarchy_max_level)
+
+    def dof_count(self, l):
+        return self._i64(lib().klref_hierarchy_dof_count, l)
+
+    def fine_element_count(self, l):
+        return self._i64(lib().klref_hierarchy_fine_element_count, l)
+
+    def lattice_size(self, l):
+        return self._int(lib().klref_hierarchy_lattice_size, l)
+
+    def level_size(self, l):
+        return self.num_macros() * self.lattice_size(l)
+
+    def dag_depth(self):
+        return self._int(lib().klref_hierarchy_dag_depth)
+
+    def groups(self, l):
+        ng, nm = C.c_int(), C.c_int()
+        _check(lib().klref_hierarchy_groups(self.ptr, l, C.byref(ng), C.byref(nm), None, None))
+        ptr = np.zeros(ng.value + 1, dtype=np.int32)
+        mem = np.zeros((nm.value, 4), dtype=np.int32)
+        _check(lib().klref_hierarchy_groups(self.ptr, l, None, None, _iptr(ptr), _iptr(mem)))
+        return ptr, mem
+
+    def element_matrices(self, l, kind=STIFFNESS):
+        M = self.num_macros()
+        mats = np.zeros((M, 18))
+        st = np.zeros((M, 7))
+        _check(lib().klref_hierarchy_element_matrices(self.ptr, l, kind, _dptr(mats), _dptr(st)))
+        return mats, st
+
+    def create_function(self, l) -> "GridFunction":
+        return GridFunction(self, l)
+
+
+class GridFunction(_Handle):
+    """Device GridFunction (proj/include/klref/hhg.hpp:33-53): M * lattice_size(2^l) doubles."""
+    _destroy = "klref_gf_destroy"
+
+    def __init__(self, h: GridHierarchy, level: int, data: Optional[np.ndarray] = None):
+        out = C.c_void_p()
+        _check(lib().klref_gf_create(h.ptr, level, C.byref(out)))
+        super().__init__(out.value)
+        self.h = h
+        self._level = level
+        self.size = h.level_size(level)
+        if data is not None:
+            self.upload(data)
+
+    def level(self):
+        return self._level
+
+    def upload(self, data: np.ndarray):
+        a = np.ascontiguousarray(data, dtype=np.float64).reshape(-1)
+        if a.size != self.size:
+            raise StructuralError("grid function size mismatch")
+        _check(lib().klref_gf_upload(self.ptr, _dptr(a)))
+
+    def numpy(self) -> np.ndarray:
+        out = np.empty(self.size, dtype=np.float64)
+        _check(lib().klref_gf_download(self.ptr, _dptr(out)))
+        return out
+
+
+class Problem(_Handle):
+    _destroy = "klref_problem_destroy"
+
+    def __init__(self, kind: int):
+        out = C.c_void_p()
+        _check(lib().klref_problem_create(kind, C.byref(out)))
+        super().__init__(out.value)
+        self.kind = kind
+
+
+@dataclass
+class SolverConfig:
+    """SolverConfig, proj/include/klref/multigrid.hpp:19-29 (finest_policy 0 = None)."""
+    nu: int = 2
+    pre_smooth: int = 2
+    post_smooth: int = 2
+    coarse_rel_tol: float = 1e-9
+    coarse_abs_floor: float = 1e-12
+    coarse_max_iter: int = 100000
+    finest_policy: int = 0
+    faithful_source: int = 0
+    use_graph: int = 1
+
+    def c(self):
+        return SolverConfigC(self.nu, self.pre_smooth, self.post_smooth, self.coarse_rel_tol,
+                             self.coarse_abs_floor, self.coarse_max_iter, self.finest_policy,
+                             self.faithful_source, self.use_graph)
+
+
+@dataclass
+class EstimateReport:
+    """EstimateReport, proj/include/klref/estimator.hpp:15-24."""
+    offset: int
+    base_level: int
+    kind: int
+    norm_coarser: float
+    norm_base: float
+    conv_factor: float
+    eta: float
+    eta_local: np.ndarray = field(default_factory=lambda: np.zeros(0))
+
+
+class MultigridSolver(_Handle):
+    """MultigridSolver (proj/include/klref/multigrid.hpp:62-99) on the device."""
+    _destroy = "klref_solver_destroy"
+
+    def __init__(self, h: GridHierarchy, problem: Problem, cfg: SolverConfig = SolverConfig()):
+        out = C.c_void_p()
+        c = cfg.c()
+        _check(lib().klref_solver_create(h.ptr, problem.ptr, C.byref(c), C.byref(out)))
+        super().__init__(out.value)
+        self.h = h
+        self.problem = problem
+        self.cfg = cfg
+
+    # -- FMG (proj/src/multigrid.cpp:248-321)
+    def fmg(self) -> "FmgState":
+        _check(lib().klref_solver_fmg(self.ptr))
+        return FmgState(self)
+
+    def fmg_enqueue(self):
+        _check(lib().klref_solver_fmg_enqueue(self.ptr))
+
+    def synchronize(self):
+        _check(lib().klref_solver_synchronize(self.ptr))
+
+    def stream(self) -> int:
+        p = C.c_void_p()
+        _check(lib().klref_solver_stream(self.ptr, C.byref(p)))
+        return p.value or 0
+
+    def launch_count(self) -> int:
+        v = C.c_int()
+        _check(lib().klref_solver_launch_count(self.ptr, C.byref(v)))
+        return v.value
+
+    def last_cg_iterations(self) -> int:
+        v = C.c_int()
+        _check(lib().klref_solver_last_cg_iterations(self.ptr, C.byref(v)))
+        return v.value
+
+    def state(self, which: int, level: int) -> np.ndarray:
+        out = np.empty(self.h.level_size(level), dtype=np.float64)
+        _check(lib().klref_solver_state_read(self.ptr, which, level, _dptr(out)))
+        return out
+
+    # -- single operations (device grid functions)
+    def apply(self, kind: int, x: GridFunction, y: GridFunction):
+        _check(lib().klref_apply(self.ptr, kind, x.ptr, y.ptr))
+
+    def residual(self, u: GridFunction, b: GridFunction, r: GridFunction):
+        _check(lib().klref_residual(self.ptr, u.ptr, b.ptr, r.ptr))
+
+    def gauss_seidel(self, u: GridFunction, b: GridFunction, sweeps: int):
+        _check(lib().klref_gauss_seidel(self.ptr, u.ptr, b.ptr, sweeps))
+
+    def restrict_transpose(self, fine: GridFunction, coarse: GridFunction):
+        _check(lib().klref_restrict_transpose(self.ptr, fine.ptr, coarse.ptr))
+
+    def prolongate(self, coarse: GridFunction, fine: GridFunction):
+        _check(lib().klref_prolongate(self.ptr, coarse.ptr, fine.ptr))
+
+    def cg_level0(self, u: GridFunction, b: GridFunction):
+        _check(lib().klref_cg_level0(self.ptr, u.ptr, b.ptr))
+
+    def dot_unique(self, a: GridFunction, b: GridFunction) -> float:
+        v = C.c_double()
+        _check(lib().klref_dot_unique(self.ptr, a.ptr, b.ptr, C.byref(v)))
+        return v.value
+
+    def interface_sync(self, f: GridFunction, mode: int):
+        _check(lib().klref_interface_sync(self.ptr, f.ptr, mode))
+
+    # -- estimator (proj/src/estimator.cpp:8-45)
+    def error_estimate(self, offset: int = 1, kind: int = UNSCALED) -> EstimateReport:
+        rep = EstimateReportC()
+        loc = np.zeros(self.h.num_macros())
+        _check(lib().klref_error_estimate(self.ptr, offset, kind, C.byref(rep), _dptr(loc)))
+        return _report(rep, loc)
+
+    def error_estimate_enqueue(self, offset: int = 1):
+        _check(lib().klref_error_estimate_enqueue(self.ptr, offset))
+
+    def error_estimate_finish(self, offset: int = 1, kind: int = UNSCALED) -> EstimateReport:
+        rep = EstimateReportC()
+        loc = np.zeros(self.h.num_macros())
+        _check(lib().klref_error_estimate_finish(self.ptr, offset, kind, C.byref(rep), _dptr(loc)))
+        return _report(rep, loc)
+
+
+def _report(rep, loc):
+    return EstimateReport(rep.offset, rep.base_level, rep.kind, rep.norm_coarser, rep.norm_base,
+                          rep.conv_factor, rep.eta, loc)
+
+
+class FmgState:
+    """FmgState (proj/include/klref/multigrid.hpp:43-53); arrays stay on the device
+    and are copied to the host only on access."""
+
+    def __init__(self, solver: MultigridSolver):
+        self.solver = solver
+        self.L = solver.h.max_level()
+
+    def u(self, l):
+        return self.solver.state(STATE_U, l)
+
+    def b(self, l):
+        return self.solver.state(STATE_B, l)
+
+    def w(self, l):
+        """w[l] = P u[l], on level l + 1."""
+        return self.solver.state(STATE_W, l + 1)
+
+
+def error_estimate(state: FmgState, offset: int = 1, kind: int = UNSCALED) -> EstimateReport:
+    """error_estimate(state, j, kind), proj/include/klref/estimator.hpp:26."""
+    return state.solver.error_estimate(offset, kind)
+
+
+def mark(rule: int, fraction: float, active_ids: Sequence[int], green_parent: Sequence[int],
+         indicator: Sequence[float], reverted_ids: Sequence[int]) -> List[int]:
+    """Marking of mark_and_refine (proj/src/amr.cpp:41-66): reverted-set aggregate + rule."""
+    a = np.ascontiguousarray(active_ids, dtype=np.int32)
+    g = np.ascontiguousarray(green_parent, dtype=np.int32)
+    ind = np.ascontiguousarray(indicator, dtype=np.float64)
+    rv = np.ascontiguousarray(reverted_ids, dtype=np.int32)
+    out = np.zeros(max(1, rv.size), dtype=np.int32)
+    cnt = C.c_int()
+    _check(lib().klref_mark(rule, fraction, a.size, _iptr(a), _iptr(g), _dptr(ind), rv.size, _iptr(rv),
+                            _iptr(out), C.byref(cnt)))
+    return [int(v) for v in out[:cnt.value]]
