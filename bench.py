@@ -1,0 +1,398 @@
+"""Benchmark of the B200 hot path: FMG + error estimator on the HHG (arXiv 2508.06049).
+
+Contract (driver): ``python bench.py --gpus N --steps K --warmup W [--impl reference]``
+prints ONE JSON line on rank 0.
+
+Workload (BASELINE.json configs[1], "config 2"): the 2-D L-shaped domain, P1
+fp64, L = 7 structured levels, FMG with nu = 2 V(2,2)-cycles per level and the
+j = 1 error estimate, over the six coarse meshes T_0^k, k = 0..5, of the 5-step
+kl AMR run (estimate -> mark >= 0.5 max -> refine -> re-solve); the meshes are
+the ones the patched reference itself produces (tests/golden/cfg2_k*.mesh).
+One step = fmg() + error_estimate(j=1) on each of the six hierarchies in AMR
+order (the hot path of run_kl, proj/src/amr.cpp:176-213); hierarchy build and
+upload happen once, outside the timed region, as SURVEY.md §8(d) specifies.
+
+value     = unique fine DoF of the step / device time of the step, GDoF/s,
+            inputs resident in HBM, L2 flushed between steps (256 MiB write).
+e2e       = the same through the public API with host buffers: per mesh
+            set_problem (host tabulation + pinned H2D), fmg(), error_estimate()
+            (eta_T to the host) and u_L read back to pinned host memory.
+roofline  = the dominant kernel (by device time) from CUDA-event probes inside
+            the timed region: algorithmic bytes / its time,
+            against MEASURED_PEAKS.json's copy bandwidth.
+cpu_baseline = the patched reference (oracle/_ref/ref_driver, compiled from
+            /root/reference sources) on one host core, a bounded sample.
+--impl reference = the same reference on all host cores (one process per core,
+            each running the full step), aggregate throughput.
+Multi-GPU: the 2-D parity path does not shard (exact Gauss-Seidel order,
+SURVEY.md §8(e)): N ranks run N independent replicas ("scaling": "weak").
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+if REPO not in sys.path:
+    sys.path.insert(0, REPO)
+
+MESH_DIR = os.path.join(REPO, "tests", "golden")
+CFG2_MESHES = [f"cfg2_k{k}.mesh" for k in range(6)]
+LEVEL = 7
+NU = 2
+METRIC = "FMG+estimator DoF throughput (cfg2 L-shape AMR meshes, l=7, V(2,2) nu=2)"
+UNIT = "GDoF/s"
+REF_DRIVER = os.path.join(REPO, "oracle", "_ref", "ref_driver")
+FLUSH_BYTES = 256 << 20
+
+
+def peaks():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------- reference arm (CPU)
+def run_reference_driver(steps, warmup, procs=1):
+    """Run `procs` concurrent single-threaded reference processes; returns their JSON records."""
+    cmd = [REF_DRIVER, "timeall", "lshape", str(LEVEL), str(NU), str(steps), str(warmup)] + CFG2_MESHES
+    ps = [subprocess.Popen(cmd, cwd=MESH_DIR, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)
+          for _ in range(procs)]
+    out = []
+    for p in ps:
+        so, se = p.communicate()
+        if p.returncode != 0:
+            raise RuntimeError(f"ref_driver failed: {se.strip()[-400:]}")
+        out.append(json.loads(so.strip().splitlines()[-1]))
+    return out
+
+
+def cpu_port_sample(steps):
+    """Fallback CPU baseline when the reference binary is absent: the C restatement oracle."""
+    from oracle import oracle as O
+    from paper_2508_06049_b200 import klref as K
+
+    meshes = [K.MacroMesh.read(os.path.join(MESH_DIR, m)) for m in CFG2_MESHES]
+    hs = [O.Hier2D(m, LEVEL) for m in meshes]
+    dofs = sum(h.dofs(LEVEL) for h in hs)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        for m, h in zip(meshes, hs):
+            st = O.fmg2d(m, LEVEL, problem="lshape", nu=NU, hier=h)
+            O.estimate2d(st, 1)
+        times.append(time.perf_counter() - t0)
+    return dofs, times
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def impl_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cores = host_cores()
+    if os.path.exists(REF_DRIVER):
+        recs = run_reference_driver(args.steps, args.warmup, procs=cores)
+        dofs = recs[0]["dofs_per_step"]
+        per_proc = [statistics.mean(r["step_s"]) for r in recs]
+        value = sum(dofs / t for t in per_proc) / 1e9
+        ms = statistics.mean(per_proc) * 1e3
+        kind = "reference"
+        sample = (f"{cores} concurrent single-threaded processes of the patched reference (oracle/_ref/ref_driver), "
+                  f"each {args.steps} full steps after {args.warmup} warm-up")
+    else:
+        dofs, times = cpu_port_sample(args.steps)
+        value = dofs / statistics.mean(times) / 1e9
+        ms = statistics.mean(times) * 1e3
+        kind, cores = "port", 1
+        sample = f"C restatement oracle, {args.steps} full steps, 1 thread (reference binary absent)"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(dofs),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(dofs):
+    return {"workload": "cfg2: L-shape (-1,1)^2\\[0,1)x(-1,0], 6 macro triangles -> 5 kl AMR steps "
+                        "(meshes k=0..5), l=7, P1 fp64, FMG V(2,2) nu=2 + estimator j=1 per mesh",
+            "meshes": CFG2_MESHES, "level": LEVEL, "nu": NU, "dofs_per_step": dofs,
+            "l2": "flushed between timed steps (256 MiB write)", "parallelism": "replicas"}
+
+
+# ----------------------------------------------------------------- our arm (GPU)
+def impl_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2508_06049_b200 import klref as K
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device (the hot path has no CPU fallback)")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    K.lib()
+
+    meshes = [K.MacroMesh.read(os.path.join(MESH_DIR, m)) for m in CFG2_MESHES]
+    hs = [K.GridHierarchy.build(m, LEVEL) for m in meshes]
+    problem = K.Problem(K.PROBLEM_LSHAPE)
+    solvers = [K.MultigridSolver(h, problem, K.SolverConfig(nu=NU, use_graph=1)) for h in hs]
+    dofs = sum(h.dof_count(LEVEL) for h in hs)
+    stream = torch.cuda.Stream()
+    for s in solvers:
+        s.set_stream(stream.cuda_stream)
+        s.set_profiling(True)
+    flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
+
+    def enqueue_step():
+        for s in solvers:
+            s.fmg_enqueue()
+            s.error_estimate_enqueue(1)
+
+    def finish_step():
+        for s in solvers:
+            s.synchronize()  # raises SolverError if a level-0 CG failed
+            s.error_estimate_finish(1, K.UNSCALED)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # warm-up (graph capture happens here)
+    for _ in range(max(args.warmup, 0)):
+        enqueue_step()
+        finish_step()
+    launches_per_step = sum(s.launch_count() + s.estimate_launch_count() for s in solvers)
+
+    nkinds = 8
+    kern_ms = [0.0] * nkinds
+    kern_bytes = [0.0] * nkinds
+    kern_n = [0] * nkinds
+    step_ms = []
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    torch.cuda.synchronize()
+    for it in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.fill_(float(it))
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        enqueue_step()
+        ev1.record(stream)
+        finish_step()
+        step_ms.append(ev0.elapsed_time(ev1))
+        for kind in range(nkinds):
+            ms = b = 0.0
+            n = 0
+            for s in solvers:
+                m_, n_, b_ = s.kernel_stats(kind)
+                ms += m_
+                n += n_
+                b += b_
+            kern_ms[kind] += ms
+            kern_bytes[kind] += b
+            kern_n[kind] += n
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    t_step = max_over_ranks(sum(step_ms) / len(step_ms))
+
+    # ---- end to end through the public API with host buffers
+    u_host = [torch.empty(h.level_size(LEVEL), dtype=torch.float64, pin_memory=True).numpy() for h in hs]
+    e2e_ms = []
+    h2d = d2h = 0
+    barrier()
+    torch.cuda.synchronize()
+    for it in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.fill_(float(it))
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        hb = db = 0
+        for s, h, uh in zip(solvers, hs, u_host):
+            hb += s.set_problem(problem)
+            s.fmg()
+            rep = s.error_estimate(1, K.UNSCALED)
+            s.state_into(K.STATE_U, LEVEL, uh)
+            db += uh.nbytes + 2 * 8 * h.num_macros() + 16
+        ev1.record(stream)
+        ev1.synchronize()
+        e2e_ms.append(ev0.elapsed_time(ev1))
+        h2d, d2h = hb, db
+    torch.cuda.synchronize()
+    barrier()
+    t_e2e = max_over_ranks(sum(e2e_ms) / len(e2e_ms))
+    _ = rep
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    # ---- roofline of the dominant kernel (largest device time in the probes)
+    peak, peak_src = peaks()
+    dom = max(range(nkinds), key=lambda k: kern_ms[k])
+    ach = kern_bytes[dom] / (kern_ms[dom] * 1e-3) / 1e9 if kern_ms[dom] > 0 else 0.0
+    traffic = None
+    tpath = os.path.join(REPO, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as fh:
+                traffic = json.load(fh).get(K.KERNEL_NAMES[dom])
+        except Exception:
+            traffic = None
+    breakdown = {}
+    probe_total = sum(kern_ms)
+    for k in range(nkinds):
+        if kern_n[k] == 0:
+            continue
+        breakdown[K.KERNEL_NAMES[k]] = {
+            "ms_per_step": kern_ms[k] / args.steps, "launches_per_step": kern_n[k] / args.steps,
+            "alg_GBps": (kern_bytes[k] / (kern_ms[k] * 1e-3) / 1e9) if kern_ms[k] > 0 else None,
+            "share": kern_ms[k] / probe_total if probe_total > 0 else None}
+    est_ms = kern_ms[K.KERNEL_ESTIMATE] / args.steps
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            if os.path.exists(REF_DRIVER):
+                rec = run_reference_driver(args.cpu_steps, 1, procs=1)[0]
+                cv = rec["dofs_per_step"] / statistics.mean(rec["step_s"]) / 1e9
+                cpu = {"value": cv, "unit": UNIT, "cores": 1, "kind": "reference",
+                       "sample": f"{args.cpu_steps} full steps (6 meshes x FMG + estimate) of the patched reference "
+                                 f"(oracle/_ref/ref_driver, g++ -O2, single-threaded), after 1 warm-up",
+                       "ms_per_step": statistics.mean(rec["step_s"]) * 1e3}
+            else:
+                cd, ct = cpu_port_sample(max(1, args.cpu_steps // 2))
+                cpu = {"value": cd / statistics.mean(ct) / 1e9, "unit": UNIT, "cores": 1, "kind": "port",
+                       "sample": f"{len(ct)} full steps of the C restatement oracle, single-threaded",
+                       "ms_per_step": statistics.mean(ct) * 1e3}
+        except Exception as exc:  # the baseline is reported, not required
+            cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference", "sample": f"failed: {exc}"}
+
+    value = world * dofs / (t_step * 1e-3) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(dofs),
+        "fmg_ms_per_step": t_step - est_ms, "estimator_ms_per_step": est_ms,
+        "roofline": {"bound": "hbm", "kernel": K.KERNEL_NAMES[dom], "achieved": ach, "peak": peak,
+                     "peak_source": peak_src, "unit": "GB/s", "frac": ach / peak, "traffic": traffic,
+                     "alg_bytes_per_launch": kern_bytes[dom] / max(kern_n[dom], 1),
+                     "ms_per_launch": kern_ms[dom] / max(kern_n[dom], 1)},
+        "kernels": breakdown,
+        "e2e": {"value": world * dofs / (t_e2e * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": t_e2e,
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clk,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--cpu-steps", type=int, default=12, help="steps of the single-core reference sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return impl_reference(args)
+    return impl_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -63,6 +63,17 @@ extern "C" {
 #define KLREF_MARK_TOP_FRACTION 0
 #define KLREF_MARK_HALF_MAX 1
 
+/* kernel kinds of the per-kernel device-time probes (klref_solver_kernel_stats) */
+#define KLREF_KERNEL_ALL (-1)
+#define KLREF_KERNEL_GS 0       /* gauss_seidel sweeps            multigrid.cpp:127 */
+#define KLREF_KERNEL_RESIDUAL 1 /* residual                       multigrid.cpp:183 */
+#define KLREF_KERNEL_RESTRICT 2 /* restrict_transpose             multigrid.cpp:55 */
+#define KLREF_KERNEL_PROLONG 3  /* prolongate (+correction, w)    multigrid.cpp:22, 243, 265 */
+#define KLREF_KERNEL_RHS 4      /* assemble_rhs + Dirichlet rows  fem.cpp:175-228 */
+#define KLREF_KERNEL_CG0 5      /* cg_level0                      multigrid.cpp:198 */
+#define KLREF_KERNEL_ESTIMATE 6 /* error_estimate norms           estimator.cpp:8-45 */
+#define KLREF_KERNEL_OTHER 7    /* boundary initialisation, memsets */
+
 typedef struct klref_mesh_s* klref_mesh;
 typedef struct klref_hierarchy_s* klref_hierarchy;
 typedef struct klref_problem_s* klref_problem;
@@ -151,6 +162,21 @@ int klref_solver_stream(klref_solver s, void** stream);
 /* number of kernel launches one FMG enqueues (graph nodes that are kernels/memsets) */
 int klref_solver_launch_count(klref_solver s, int* out);
 int klref_solver_last_cg_iterations(klref_solver s, int* out);
+/* number of kernel launches one error_estimate enqueues */
+int klref_solver_estimate_launch_count(klref_solver s, int* out);
+/* launch on a caller-owned cudaStream_t (passed as void*; NULL = the solver's own stream) */
+int klref_solver_set_stream(klref_solver s, void* stream);
+/* re-tabulate the problem's data (Dirichlet g at the boundary nodes, f at the
+ * quadrature points in faithful mode) on the host and copy it host->device
+ * from pinned staging; *h2d_bytes (may be NULL) receives the bytes copied.
+ * ProblemSpec hand-over of MultigridSolver(h, p, cfg), multigrid.cpp:113-119 */
+int klref_solver_set_problem(klref_solver s, klref_problem p, int64_t* h2d_bytes);
+/* per-kernel CUDA-event probes: with profiling on, every kernel of the FMG /
+ * estimator is bracketed by event records; kernel_stats sums, for one kernel
+ * kind (or KLREF_KERNEL_ALL), the device milliseconds, launch count and
+ * algorithmic bytes of the most recent FMG + estimate. */
+int klref_solver_set_profiling(klref_solver s, int on);
+int klref_solver_kernel_stats(klref_solver s, int kind, double* ms, int* launches, double* bytes);
 /* FmgState::u/b/w (proj/include/klref/multigrid.hpp:43-53), copied to the host */
 int klref_solver_state_read(klref_solver s, int which, int level, double* host_out);
 

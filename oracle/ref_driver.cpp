@@ -384,6 +384,53 @@ int cmd_time(int argc, char** argv) {
   return 0;
 }
 
+// timeall <sin|lshape|zero> <L> <nu> <steps> <warmup> <mesh>...: one "step" is
+// MultigridSolver::fmg() + error_estimate(j=1) on every listed mesh in turn
+// (the hot path of the AMR loop, proj/src/amr.cpp:176-213; hierarchy build
+// and solver construction happen once, outside the timed region).
+int cmd_timeall(int argc, char** argv) {
+  if (argc < 8) return 2;
+  const ProblemSpec p = make_problem(argv[2]);
+  const int L = std::atoi(argv[3]), nu = std::atoi(argv[4]);
+  const int steps = std::atoi(argv[5]), warmup = std::atoi(argv[6]);
+  SolverConfig sc;
+  sc.nu = nu;
+  sc.finest_policy = FinestPolicy::None;
+  std::vector<std::shared_ptr<const GridHierarchy>> hs;
+  std::vector<std::unique_ptr<MultigridSolver>> solvers;
+  std::int64_t dofs = 0;
+  for (int a = 7; a < argc; ++a) {
+    hs.push_back(GridHierarchy::build(read_mesh_file(argv[a]), L));
+    solvers.push_back(std::make_unique<MultigridSolver>(hs.back(), p, sc));
+    dofs += hs.back()->dof_count(L);
+  }
+  std::vector<double> times;
+  double fmg_s = 0.0, est_s = 0.0;
+  for (int it = 0; it < warmup + steps; ++it) {
+    double f = 0.0, e = 0.0;
+    for (auto& s : solvers) {
+      const auto t0 = Clock::now();
+      FmgState st = s->fmg();
+      const auto t1 = Clock::now();
+      EstimateReport er = error_estimate(st, 1, EstimatorKind::Unscaled);
+      const auto t2 = Clock::now();
+      (void)er;
+      f += secs(t0, t1);
+      e += secs(t1, t2);
+    }
+    if (it >= warmup) {
+      times.push_back(f + e);
+      fmg_s += f;
+      est_s += e;
+    }
+  }
+  std::printf("{\"dofs_per_step\": %lld, \"steps\": %d, \"fmg_s\": %.9g, \"est_s\": %.9g, \"step_s\": [",
+              static_cast<long long>(dofs), steps, fmg_s, est_s);
+  for (size_t i = 0; i < times.size(); ++i) std::printf("%s%.9g", i ? ", " : "", times[i]);
+  std::printf("]}\n");
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -404,6 +451,7 @@ int main(int argc, char** argv) {
     if (cmd == "amr") return cmd_amr(argc, argv);
     if (cmd == "ops") return cmd_ops(argc, argv);
     if (cmd == "time") return cmd_time(argc, argv);
+    if (cmd == "timeall") return cmd_timeall(argc, argv);
   } catch (const std::exception& e) {
     std::fprintf(stderr, "ref_driver: %s\n", e.what());
     return 1;

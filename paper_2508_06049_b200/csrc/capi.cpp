@@ -307,6 +307,40 @@ int klref_solver_last_cg_iterations(klref_solver s, int* out) {
     *out = s->s->last_cg_iters();
   });
 }
+int klref_solver_estimate_launch_count(klref_solver s, int* out) {
+  return guarded([&] {
+    need(s, "solver");
+    need(out, "out");
+    *out = s->s->launches_per_estimate();
+  });
+}
+int klref_solver_set_stream(klref_solver s, void* stream) {
+  return guarded([&] {
+    need(s, "solver");
+    s->s->set_stream(reinterpret_cast<cudaStream_t>(stream));
+  });
+}
+int klref_solver_set_problem(klref_solver s, klref_problem p, int64_t* h2d_bytes) {
+  return guarded([&] {
+    need(s, "solver");
+    need(p, "problem");
+    const size_t b = s->s->load_problem(p->p);
+    if (h2d_bytes) *h2d_bytes = static_cast<int64_t>(b);
+  });
+}
+int klref_solver_set_profiling(klref_solver s, int on) {
+  return guarded([&] {
+    need(s, "solver");
+    s->s->set_profiling(on != 0);
+  });
+}
+int klref_solver_kernel_stats(klref_solver s, int kind, double* ms, int* launches, double* bytes) {
+  return guarded([&] {
+    need(s, "solver");
+    if (kind < KLREF_KERNEL_ALL || kind >= kb::KK_COUNT) kb::fail(kb::KB_STRUCTURAL, "unknown kernel kind");
+    s->s->kernel_stats(kind, ms, launches, bytes);
+  });
+}
 int klref_solver_state_read(klref_solver s, int which, int level, double* host_out) {
   return guarded([&] {
     need(s, "solver");

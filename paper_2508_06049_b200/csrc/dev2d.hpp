@@ -34,6 +34,9 @@ struct DevLevel2D {
   int num_groups;
   const int* dot_order;
   int dot_count;
+  const unsigned long long* blob;  // per-macro relaxation blobs (Level2D::blob)
+  const int* blob_desc;
+  int blob_max_words;
   const double* geo;   // per macro: c0x, c0y, ux, uy, wx, wy (RHS quadrature map, proj/src/fem.cpp:183-186)
   const double* wq;    // per macro: cell_area / 3
 };
@@ -44,6 +47,22 @@ struct DevHier2D {
   const int* nb_lo;
   const int* nb_hi_ptr;
   const int* nb_hi;
+  int dag_depth, dag_width;  // number of DAG levels, most macros in one level
+  const int* dag_ptr;
+  const int* dag_list;
+};
+
+// Kernel kinds for the per-kernel probes (KLREF_KERNEL_* in include/klref_b200.h).
+enum KernelKind : int {
+  KK_GS = 0,        // Gauss-Seidel sweeps
+  KK_RESIDUAL = 1,  // r = b - A u
+  KK_RESTRICT = 2,
+  KK_PROLONG = 3,   // prolongation (+ correction / w snapshot)
+  KK_RHS = 4,       // right-hand side + Dirichlet rows
+  KK_CG0 = 5,       // level-0 CG
+  KK_ESTIMATE = 6,  // fused estimator norms (+ its prolongations)
+  KK_OTHER = 7,     // boundary init, memsets
+  KK_COUNT = 8
 };
 
 enum ApplyMode : int { APPLY_PLAIN = 0, APPLY_RESIDUAL = 1, APPLY_ZERO_BND = 2 };

@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <map>
 #include <new>
 
@@ -52,6 +53,70 @@ int direction_code(int di, int dj) {
 }
 
 bool on_lattice_boundary(int n, int i, int j) { return i == 0 || j == 0 || i + j == n; }
+
+std::uint64_t pack32(std::int32_t lo, std::int32_t hi) {
+  return static_cast<std::uint64_t>(static_cast<std::uint32_t>(lo)) |
+         (static_cast<std::uint64_t>(static_cast<std::uint32_t>(hi)) << 32);
+}
+std::uint64_t pack16(std::int16_t a, std::int16_t b, std::int16_t c, std::int16_t d) {
+  return static_cast<std::uint64_t>(static_cast<std::uint16_t>(a)) |
+         (static_cast<std::uint64_t>(static_cast<std::uint16_t>(b)) << 16) |
+         (static_cast<std::uint64_t>(static_cast<std::uint16_t>(c)) << 32) |
+         (static_cast<std::uint64_t>(static_cast<std::uint16_t>(d)) << 48);
+}
+
+// Per-macro relaxation blobs (layout in hier2d.hpp, Level2D::blob).
+void build_blobs(Level2D& lvl, int M) {
+  const int n = lvl.n;
+  lvl.blob.clear();
+  lvl.blob_desc.assign(4 * static_cast<std::size_t>(M), 0);
+  lvl.blob_max_words = 0;
+  for (int m = 0; m < M; ++m) {
+    const std::size_t begin = lvl.blob.size();
+    std::vector<std::uint64_t> nodes, recs, wrs, kmat;
+    std::vector<int> wr32;
+    std::map<int, int> kslot;
+    int nrec = 0;
+    for (int p = 0; p < 3 * n; ++p) {
+      const BNode& bn = lvl.bnode[static_cast<std::size_t>(m) * 3 * n + p];
+      std::uint64_t d;
+      std::memcpy(&d, &bn.diag, 8);
+      nodes.push_back(d);
+      nodes.push_back(pack32(nrec, (bn.rec_count & 0xffff) | (bn.domain << 16)));
+      nodes.push_back(pack32(static_cast<int>(wr32.size()), bn.wr_count));
+      for (int r = 0; r < bn.rec_count; ++r) {
+        const MemberRec& rec = lvl.rec[bn.rec_begin + r];
+        auto it = kslot.find(rec.slot);
+        int ks;
+        if (it == kslot.end()) {
+          ks = static_cast<int>(kslot.size());
+          kslot[rec.slot] = ks;
+          for (int q = 0; q < 18; ++q) {
+            std::uint64_t w;
+            std::memcpy(&w, &lvl.kstiff[18 * static_cast<std::size_t>(rec.slot) + q], 8);
+            kmat.push_back(w);
+          }
+        } else {
+          ks = it->second;
+        }
+        recs.push_back(pack16(static_cast<std::int16_t>(ks), static_cast<std::int16_t>(rec.mask), rec.loc[0], rec.loc[1]));
+        recs.push_back(pack16(rec.loc[2], rec.loc[3], rec.loc[4], rec.loc[5]));
+        recs.push_back(pack16(rec.loc[6], rec.loc[7], rec.loc[8], rec.loc[9]));
+        recs.push_back(pack16(rec.loc[10], rec.loc[11], 0, 0));
+        ++nrec;
+      }
+      for (int q = 0; q < bn.wr_count; ++q) wr32.push_back(lvl.wr[bn.wr_begin + q]);
+    }
+    if (wr32.size() & 1) wr32.push_back(0);
+    for (std::size_t q = 0; q < wr32.size(); q += 2) wrs.push_back(pack32(wr32[q], wr32[q + 1]));
+    for (auto* part : {&nodes, &recs, &wrs, &kmat}) lvl.blob.insert(lvl.blob.end(), part->begin(), part->end());
+    lvl.blob_desc[4 * m] = static_cast<int>(begin);
+    lvl.blob_desc[4 * m + 1] = nrec;
+    lvl.blob_desc[4 * m + 2] = static_cast<int>(wr32.size());
+    lvl.blob_desc[4 * m + 3] = static_cast<int>(kslot.size());
+    lvl.blob_max_words = std::max(lvl.blob_max_words, static_cast<int>(lvl.blob.size() - begin));
+  }
+}
 
 }  // namespace
 
@@ -198,6 +263,12 @@ Hierarchy2D Hierarchy2D::build(const Mesh2D& mesh, int max_level) {
       h.nb_lo_ptr.push_back(static_cast<int>(h.nb_lo.size()));
       h.nb_hi_ptr.push_back(static_cast<int>(h.nb_hi.size()));
     }
+    h.dag_ptr.assign(h.dag_depth + 1, 0);
+    for (int s = 0; s < M; ++s) ++h.dag_ptr[depth[s]];
+    for (int d = 1; d <= h.dag_depth; ++d) h.dag_ptr[d] += h.dag_ptr[d - 1];
+    h.dag_list.assign(M, 0);
+    std::vector<int> fill(h.dag_ptr.begin(), h.dag_ptr.end() - 1);
+    for (int s = 0; s < M; ++s) h.dag_list[fill[depth[s] - 1]++] = s;
   }
 
   try {
@@ -373,6 +444,7 @@ Hierarchy2D Hierarchy2D::build(const Mesh2D& mesh, int max_level) {
             double d = 0.0;
             for (int c = 0; c < 6; ++c) {
               r.code[2 * c] = r.code[2 * c + 1] = -1;
+              r.loc[2 * c] = r.loc[2 * c + 1] = -1;
               if (!cell[c]) continue;
               r.mask |= 1 << c;
               d += dg[c];
@@ -410,6 +482,15 @@ Hierarchy2D Hierarchy2D::build(const Mesh2D& mesh, int max_level) {
                 if (code < 0) fail(KB_INTERNAL, "unresolved partial-row read");
                 if (code > 32767) fail(KB_INTERNAL, "too many ghost values");
                 r.code[2 * c + q] = static_cast<std::int16_t>(code);
+                int loc;
+                if (code < 6) {
+                  static const int dij[6][2] = {{1, 0}, {-1, 0}, {0, 1}, {0, -1}, {-1, 1}, {1, -1}};
+                  loc = lattice_index(n, i + dij[code][0], j + dij[code][1]);
+                } else {
+                  loc = -1 - (code - 6);
+                }
+                // only used by the shared-memory smoother (lattices up to n = 128)
+                r.loc[2 * c + q] = (loc > 32767 || loc < -32768) ? 0 : static_cast<std::int16_t>(loc);
               }
             }
             diag += d;
@@ -427,6 +508,7 @@ Hierarchy2D Hierarchy2D::build(const Mesh2D& mesh, int max_level) {
       lvl.ghost_ptr.push_back(static_cast<int>(lvl.ghost_off.size()));
       lvl.max_ghosts = std::max(lvl.max_ghosts, static_cast<int>(ghosts.size()));
     }
+    build_blobs(lvl, M);
   }
   return h;
 }

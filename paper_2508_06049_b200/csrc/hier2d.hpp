@@ -52,6 +52,9 @@ struct MemberRec {
   std::int32_t slot;
   std::int32_t mask;       // existing cells, bit k in the partial_row order
   std::int16_t code[12];   // two reads per cell, in partial_row order
+  // the same reads as lattice indices of the relaxing macro (>= 0) or ghost
+  // values (-1 - ghost index), for the shared-memory smoother
+  std::int16_t loc[12];
 };
 struct BNode {
   std::int32_t rec_begin, rec_count;
@@ -81,6 +84,17 @@ struct Level2D {
   std::vector<int> wr;                     // global copy offsets
   std::vector<int> ghost_ptr, ghost_off;   // per macro ghost lists (global offsets)
   int max_ghosts = 0;
+  // Per-macro relaxation blob for the shared-memory smoother (staged into
+  // shared memory once per macro sweep; 8-byte words):
+  //   [0, 9n)        3n boundary nodes x 3 words: diag | rec_begin:i32 rec_count:i16 domain:i16 |
+  //                  wr_begin:i32 wr_count:i32   (boundary position order, bpos())
+  //   [9n, +4 nrec)  records: kslot:i16 mask:i16 loc[12]:i16 (kslot indexes the kmat area)
+  //   [.., +nwr/2)   copy targets (global copy offsets, i32)
+  //   [.., +18 nk)   stiffness up/down matrices of the member macros
+  // blob_desc[4m..4m+3] = word offset, nrec, nwr, nk.
+  std::vector<std::uint64_t> blob;
+  std::vector<int> blob_desc;
+  int blob_max_words = 0;
   // owner dot order (dot_unique, proj/src/hhg.cpp:227-257): offsets in summation order
   std::vector<int> dot_order;
 };
@@ -101,6 +115,8 @@ struct Hierarchy2D {
   // vertex-sharing neighbours per macro (level independent): lower and higher slots
   std::vector<int> nb_lo_ptr, nb_lo, nb_hi_ptr, nb_hi;
   int dag_depth = 0;
+  // macros grouped by DAG level: dag_list[dag_ptr[d] .. dag_ptr[d+1])
+  std::vector<int> dag_ptr, dag_list;
 
   static Hierarchy2D build(const Mesh2D& mesh, int max_level);
 

@@ -13,6 +13,7 @@
 //   estimate             error_estimate norms                           proj/src/estimator.cpp:8-45, fem.cpp:320-356
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <map>
@@ -552,6 +553,210 @@ __global__ void __launch_bounds__(576, 1) k_gs(DevHier2D hd, DevLevel2D lv, doub
   }
 }
 
+
+// ------------------------------------------------ Gauss-Seidel, shared-memory
+// One warp relaxes one macro lattice held in shared memory.  Lane l owns rows
+// j = l + 32 r (r < R) and at wavefront step t = i + 2j updates node
+// (t - 2j, j) of each of its rows; every stencil neighbour of a step-t node
+// belongs to step t +- 1 or t +- 2, so a __syncwarp between
+// steps is the only synchronisation.  Interior nodes use the 7-point form of
+// proj/src/multigrid.cpp:170-175; lattice-boundary nodes the group gather of
+// relax_boundary_node (:132-150) over partial_row records whose reads are
+// either lattice indices of this macro or ghost values staged in `gh`.
+// View of one macro's relaxation blob staged in shared memory (Level2D::blob).
+struct BlobView {
+  const unsigned long long* w;
+  const short* recs;
+  const int* wr;
+  const double* km;
+};
+
+__device__ __forceinline__ BlobView blob_view(const unsigned long long* w, int n, int nrec, int nwr) {
+  BlobView v;
+  v.w = w;
+  v.recs = reinterpret_cast<const short*>(w + 9 * n);
+  v.wr = reinterpret_cast<const int*>(w + 9 * n + 4 * nrec);
+  v.km = reinterpret_cast<const double*>(w + 9 * n + 4 * nrec + nwr / 2);
+  return v;
+}
+
+// copy one macro's blob (and ghosts) into shared memory with the whole warp
+__device__ __forceinline__ BlobView stage_blob(const DevLevel2D& lv, int m, unsigned long long* dst, int lane) {
+  const int beg = lv.blob_desc[4 * m], nrec = lv.blob_desc[4 * m + 1], nwr = lv.blob_desc[4 * m + 2],
+            nk = lv.blob_desc[4 * m + 3];
+  const int words = 9 * lv.n + 4 * nrec + nwr / 2 + 18 * nk;
+  for (int q = lane; q < words; q += 32) dst[q] = __ldg(lv.blob + beg + q);
+  return blob_view(dst, lv.n, nrec, nwr);
+}
+
+// relax_boundary_node (proj/src/multigrid.cpp:132-150) from the staged blob:
+// group members in ascending slot, partial_row cells in the order of
+// proj/src/fem.cpp:138-172, off accumulated per member then summed.
+__device__ __forceinline__ double relax_blob(const BlobView& bv, int p, double B, const double* us,
+                                             const double* gh, double* copies) {
+  const unsigned long long w1 = bv.w[3 * p + 1], w2 = bv.w[3 * p + 2];
+  const int rb = static_cast<int>(w1 & 0xffffffffull);
+  const int rc = static_cast<int>((w1 >> 32) & 0xffff);
+  const int domain = static_cast<int>(w1 >> 48);
+  double res = B;
+  if (!domain) {
+    double off = 0.0;
+    for (int r = rb; r < rb + rc; ++r) {
+      const short* rec = bv.recs + 16 * r;
+      const double* ku = bv.km + 18 * rec[0];
+      const double* kd = ku + 9;
+      const int mask = rec[1];
+      auto X = [&](int q) {
+        const int loc = rec[2 + q];
+        return loc >= 0 ? us[loc] : gh[-1 - loc];
+      };
+      double o = 0.0;
+      if (mask & 1) o += ku[1] * X(0) + ku[2] * X(1);
+      if (mask & 2) o += ku[3] * X(2) + ku[5] * X(3);
+      if (mask & 4) o += ku[6] * X(4) + ku[7] * X(5);
+      if (mask & 8) o += kd[1] * X(6) + kd[2] * X(7);
+      if (mask & 16) o += kd[3] * X(8) + kd[5] * X(9);
+      if (mask & 32) o += kd[6] * X(10) + kd[7] * X(11);
+      off += o;
+    }
+    res = (B - off) / __longlong_as_double(static_cast<long long>(bv.w[3 * p]));
+  }
+  const int wb = static_cast<int>(w2 & 0xffffffffull), wc = static_cast<int>(w2 >> 32);
+  for (int q = wb; q < wb + wc; ++q) copies[bv.wr[q]] = res;
+  return res;
+}
+
+template <int R>
+__device__ __forceinline__ void warp_sweep(const DevLevel2D& lv, int m, double* us, const double* bs,
+                                           const double* gh, const BlobView& bv, double* copies, int lane) {
+  const int n = lv.n;
+  const double* st = lv.stencil + 7 * m;
+  const double s1 = st[1], s2 = st[2], s3 = st[3], s4 = st[4], s5 = st[5], s6 = st[6];
+  const double inv_c = lv.inv_c[m];
+  int rowk[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int j = lane + 32 * r;
+    rowk[r] = j <= n ? dlat(n, 0, j) : 0;
+  }
+  for (int t = 0; t <= 2 * n; ++t) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int j = lane + 32 * r;
+      const int i = t - 2 * j;
+      if (j > n || i < 0 || i > n - j) continue;
+      const int k = rowk[r] + i;
+      const double B = bs[k];
+      double res;
+      if (j >= 1 && i >= 1 && i + j <= n - 1) {
+        const double E = us[k + 1], W = us[k - 1], N = us[k + n + 1 - j], S = us[k - (n + 2 - j)];
+        const double NW = us[k + n - j], SE = us[k - (n + 1 - j)];
+        double acc = s1 * E + s2 * W;
+        acc = acc + s3 * N;
+        acc = acc + s4 * S;
+        acc = acc + s5 * NW;
+        acc = acc + s6 * SE;
+        res = (B - acc) * inv_c;
+      } else {
+        res = relax_blob(bv, bpos_dev(n, i, j), B, us, gh, copies);
+      }
+      us[k] = res;
+    }
+    __syncwarp();
+  }
+}
+
+// Mode "level": the whole level (u and b of every macro) lives in the shared
+// memory of one CTA; warps take the macros of one DAG level at a time and a
+// __syncthreads separates DAG levels.  For small lattices.
+template <int R>
+__global__ void __launch_bounds__(512, 1) k_gs_level(DevHier2D hd, DevLevel2D lv, double* u,
+                                                       const double* __restrict__ b, int sweeps) {
+  extern __shared__ double smem[];
+  const int S = lv.S, M = lv.M;
+  const int total = M * S;
+  double* lu = smem;
+  double* lb = smem + total;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  const int per_warp = lv.max_ghosts + lv.blob_max_words;
+  double* gh = lb + total + static_cast<size_t>(warp) * per_warp;
+  unsigned long long* bw = reinterpret_cast<unsigned long long*>(gh + lv.max_ghosts);
+  for (int k = threadIdx.x; k < total; k += blockDim.x) {
+    lu[k] = __ldcg(u + k);
+    lb[k] = __ldg(b + k);
+  }
+  __syncthreads();
+  for (int s = 0; s < sweeps; ++s) {
+    for (int d = 0; d < hd.dag_depth; ++d) {
+      for (int q = hd.dag_ptr[d] + warp; q < hd.dag_ptr[d + 1]; q += nwarps) {
+        const int m = hd.dag_list[q];
+        const int gbeg = lv.ghost_ptr[m], gcnt = lv.ghost_ptr[m + 1] - gbeg;
+        for (int g = lane; g < gcnt; g += 32) gh[g] = lu[lv.ghost_off[gbeg + g]];
+        const BlobView bv = stage_blob(lv, m, bw, lane);
+        __syncwarp();
+        warp_sweep<R>(lv, m, lu + static_cast<size_t>(m) * S, lb + static_cast<size_t>(m) * S, gh, bv, lu, lane);
+      }
+      __syncthreads();
+    }
+  }
+  for (int k = threadIdx.x; k < total; k += blockDim.x) u[k] = lu[k];
+}
+
+// Mode "macro": one single-warp CTA per macro sweep with the macro's u, b and
+// ghosts in shared memory; macro m's sweep s starts once every vertex-sharing
+// macro m' < m finished sweep s and every m'' > m finished sweep s-1 (A.3).
+template <int R>
+__global__ void __launch_bounds__(32, 1) k_gs_macro(DevHier2D hd, DevLevel2D lv, double* u,
+                                                 const double* __restrict__ b, int sweeps, int* done) {
+  extern __shared__ double smem[];
+  const int S = lv.S, M = lv.M;
+  double* us = smem;
+  double* bs = smem + S;
+  double* gh = bs + S;
+  unsigned long long* bw = reinterpret_cast<unsigned long long*>(gh + lv.max_ghosts);
+  const int lane = threadIdx.x;
+  BlobView bv{};
+  const int nitems = sweeps * M;
+  int cur = -1;
+  for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+    const int s = item / M, m = item - s * M;
+    if (lane == 0) {
+      for (int q = hd.nb_lo_ptr[m]; q < hd.nb_lo_ptr[m + 1]; ++q)
+        while (ld_acquire(done + hd.nb_lo[q]) < s + 1) {}
+      for (int q = hd.nb_hi_ptr[m]; q < hd.nb_hi_ptr[m + 1]; ++q)
+        while (ld_acquire(done + hd.nb_hi[q]) < s) {}
+    }
+    __syncwarp();
+    double* um = u + static_cast<size_t>(m) * S;
+    if (m != cur) {
+      bv = stage_blob(lv, m, bw, lane);
+      const double* bm = b + static_cast<size_t>(m) * S;
+      for (int k = lane; k < S; k += 32) {
+        us[k] = __ldcg(um + k);
+        bs[k] = __ldg(bm + k);
+      }
+    } else {
+      // only the interface copies of this macro can have changed since its last sweep
+      const int n = lv.n;
+      for (int p = lane; p < 3 * n; p += 32) {
+        const int k = p <= n ? p : (p < 2 * n + 1 ? dlat(n, 0, p - n) : dlat(n, 3 * n - p, p - 2 * n));
+        us[k] = __ldcg(um + k);
+      }
+    }
+    const int gbeg = lv.ghost_ptr[m], gcnt = lv.ghost_ptr[m + 1] - gbeg;
+    for (int g = lane; g < gcnt; g += 32) gh[g] = __ldcg(u + lv.ghost_off[gbeg + g]);
+    __syncwarp();
+    warp_sweep<R>(lv, m, us, bs, gh, bv, u, lane);
+    for (int k = lane; k < S; k += 32) um[k] = us[k];
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence();
+      st_release(done + m, s + 1);
+    }
+    cur = m;
+  }
+}
+
 // ---------------------------------------------------------------- estimator
 __device__ __forceinline__ double quad_form(const double* k, double a, double b, double c) {
   return a * (k[0] * a + k[1] * b + k[2] * c) + b * (k[3] * a + k[4] * b + k[5] * c) +
@@ -715,31 +920,84 @@ void launch_cg0(const DevLevel2D& lv0, double* u, const double* b, double* scrat
 
 int gs_block_threads(int n) { return 32 * ((n + 1 + 31) / 32); }
 
+namespace {
+int device_attr(cudaDeviceAttr a) {
+  int dev = 0, v = 0;
+  KB_CUDA_CHECK(cudaGetDevice(&dev));
+  KB_CUDA_CHECK(cudaDeviceGetAttribute(&v, a, dev));
+  return v;
+}
+
+template <typename K>
+void set_smem(K kernel, size_t smem) {
+  if (smem > 48 * 1024)
+    KB_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+}
+
+template <int R>
+void launch_gs_smem(const DevHier2D& hd, const DevLevel2D& lv, double* u, const double* b, int sweeps, int* done,
+                    cudaStream_t st, size_t level_smem, int level_warps, size_t macro_smem, int num_sms) {
+  if (level_smem) {
+    set_smem(k_gs_level<R>, level_smem);
+    k_gs_level<R><<<1, 32 * level_warps, level_smem, st>>>(hd, lv, u, b, sweeps);
+    check_launch("k_gs_level");
+    return;
+  }
+  set_smem(k_gs_macro<R>, macro_smem);
+  int occ = 0;
+  KB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gs_macro<R>, 32, macro_smem));
+  if (occ < 1) fail(KB_CUDA, "k_gs_macro cannot be resident");
+  int grid = lv.M;
+  if (grid > occ * num_sms) grid = occ * num_sms;
+  KB_CUDA_CHECK(cudaMemsetAsync(done, 0, sizeof(int) * lv.M, st));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(32);
+  cfg.dynamicSmemBytes = macro_smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  KB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_gs_macro<R>, hd, lv, u, b, sweeps, done));
+}
+}  // namespace
+
+// Smoother dispatch: the whole level in one CTA's shared memory when it fits,
+// else one shared-memory CTA per macro, else (n > 128) the register-wavefront
+// kernel with the lattice in L2.
 void launch_gs(const DevHier2D& hd, const DevLevel2D& lv, double* u, const double* b, int sweeps, int* done,
                cudaStream_t st) {
   if (sweeps <= 0) return;
+  static int num_sms = 0, smem_max = 0;
+  if (num_sms == 0) {
+    num_sms = device_attr(cudaDevAttrMultiProcessorCount);
+    smem_max = device_attr(cudaDevAttrMaxSharedMemoryPerBlockOptin);
+  }
+  const int R = (lv.n + 32) / 32;
+  const size_t S = static_cast<size_t>(lv.S), M = static_cast<size_t>(lv.M);
+  const int warps = std::max(1, std::min(16, hd.dag_width));
+  size_t level_smem =
+      (2 * M * S + static_cast<size_t>(warps) * (lv.max_ghosts + lv.blob_max_words)) * sizeof(double);
+  const size_t macro_smem = (2 * S + lv.max_ghosts + lv.blob_max_words) * sizeof(double);
+  if (level_smem > static_cast<size_t>(smem_max)) level_smem = 0;
+  if (R <= 5 && (level_smem || macro_smem <= static_cast<size_t>(smem_max))) {
+    switch (R) {
+      case 1: launch_gs_smem<1>(hd, lv, u, b, sweeps, done, st, level_smem, warps, macro_smem, num_sms); return;
+      case 2: launch_gs_smem<2>(hd, lv, u, b, sweeps, done, st, level_smem, warps, macro_smem, num_sms); return;
+      case 3: launch_gs_smem<3>(hd, lv, u, b, sweeps, done, st, level_smem, warps, macro_smem, num_sms); return;
+      case 4: launch_gs_smem<4>(hd, lv, u, b, sweeps, done, st, level_smem, warps, macro_smem, num_sms); return;
+      default: launch_gs_smem<5>(hd, lv, u, b, sweeps, done, st, level_smem, warps, macro_smem, num_sms); return;
+    }
+  }
   const int threads = gs_block_threads(lv.n);
   if (threads > 576) fail(KB_STRUCTURAL, "wavefront smoother supports n <= 575");
   const int nwarps = threads / 32;
   const size_t smem = sizeof(double) * (lv.max_ghosts + nwarps * kRing) + sizeof(int) * nwarps + 16;
-  static std::map<std::pair<int, size_t>, int> occ_cache;
-  static int num_sms = 0;
-  if (num_sms == 0) {
-    int dev = 0;
-    KB_CUDA_CHECK(cudaGetDevice(&dev));
-    KB_CUDA_CHECK(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
-  }
-  if (smem > 48 * 1024)
-    KB_CUDA_CHECK(cudaFuncSetAttribute(k_gs, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  int occ;
-  auto key = std::make_pair(threads, smem);
-  auto it = occ_cache.find(key);
-  if (it == occ_cache.end()) {
-    KB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gs, threads, smem));
-    occ_cache[key] = occ;
-  } else {
-    occ = it->second;
-  }
+  set_smem(k_gs, smem);
+  int occ = 0;
+  KB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gs, threads, smem));
   if (occ < 1) fail(KB_CUDA, "k_gs cannot be resident");
   int grid = lv.M;
   if (grid > occ * num_sms) grid = occ * num_sms;

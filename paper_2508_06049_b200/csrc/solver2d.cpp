@@ -55,7 +55,8 @@ std::unique_ptr<DeviceHierarchy2D> DeviceHierarchy2D::create(const Mesh2D& mesh,
   const int M = h.M;
   std::vector<std::vector<int>> mem_off(h.L + 1), mem_ij(h.L + 1);
   std::vector<std::vector<double>> geo(h.L + 1), wq(h.L + 1);
-  size_t bytes = vbytes(h.nb_lo_ptr) + vbytes(h.nb_lo) + vbytes(h.nb_hi_ptr) + vbytes(h.nb_hi);
+  size_t bytes = vbytes(h.nb_lo_ptr) + vbytes(h.nb_lo) + vbytes(h.nb_hi_ptr) + vbytes(h.nb_hi) +
+                 vbytes(h.dag_ptr) + vbytes(h.dag_list);
   for (int l = 0; l <= h.L; ++l) {
     const Level2D& lv = h.levels[l];
     const int n = lv.n;
@@ -79,7 +80,7 @@ std::unique_ptr<DeviceHierarchy2D> DeviceHierarchy2D::create(const Mesh2D& mesh,
              vbytes(mem_ij[l]) + vbytes(lv.mem_slot) + vbytes(lv.kstiff) + vbytes(lv.kmass) +
              vbytes(lv.stencil) + vbytes(lv.inv_c) + vbytes(lv.bnode) + vbytes(lv.rec) + vbytes(lv.wr) +
              vbytes(lv.ghost_ptr) + vbytes(lv.ghost_off) + vbytes(lv.dot_order) + vbytes(geo[l]) +
-             vbytes(wq[l]);
+             vbytes(wq[l]) + vbytes(lv.blob) + vbytes(lv.blob_desc);
   }
   d->arena.reserve(bytes + 4096);
   d->dh.M = M;
@@ -88,6 +89,11 @@ std::unique_ptr<DeviceHierarchy2D> DeviceHierarchy2D::create(const Mesh2D& mesh,
   d->dh.nb_lo = d->arena.upload(h.nb_lo);
   d->dh.nb_hi_ptr = d->arena.upload(h.nb_hi_ptr);
   d->dh.nb_hi = d->arena.upload(h.nb_hi);
+  d->dh.dag_depth = h.dag_depth;
+  d->dh.dag_width = 0;
+  for (int k = 0; k < h.dag_depth; ++k) d->dh.dag_width = std::max(d->dh.dag_width, h.dag_ptr[k + 1] - h.dag_ptr[k]);
+  d->dh.dag_ptr = d->arena.upload(h.dag_ptr);
+  d->dh.dag_list = d->arena.upload(h.dag_list);
   for (int l = 0; l <= h.L; ++l) {
     const Level2D& lv = h.levels[l];
     DevLevel2D dl{};
@@ -113,6 +119,9 @@ std::unique_ptr<DeviceHierarchy2D> DeviceHierarchy2D::create(const Mesh2D& mesh,
     dl.num_groups = static_cast<int>(lv.grp_ptr.size()) - 1;
     dl.dot_order = d->arena.upload(lv.dot_order);
     dl.dot_count = static_cast<int>(lv.dot_order.size());
+    dl.blob = reinterpret_cast<const unsigned long long*>(d->arena.upload(lv.blob));
+    dl.blob_desc = d->arena.upload(lv.blob_desc);
+    dl.blob_max_words = lv.blob_max_words;
     dl.geo = d->arena.upload(geo[l]);
     dl.wq = d->arena.upload(wq[l]);
     d->lev.push_back(dl);
@@ -218,17 +227,45 @@ Solver2D::Solver2D(std::shared_ptr<DeviceHierarchy2D> h, Problem2D p, SolverConf
   status_ = static_cast<DevStatus*>(arena_.take(sizeof(DevStatus)));
   gs_done_ = static_cast<int*>(arena_.take(M * 4));
 
-  KB_CUDA_CHECK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  KB_CUDA_CHECK(cudaStreamCreateWithFlags(&own_stream_, cudaStreamNonBlocking));
+  stream_ = own_stream_;
   KB_CUDA_CHECK(cudaMallocHost(&status_host_, sizeof(DevStatus)));
   KB_CUDA_CHECK(cudaMallocHost(&sums_host_, 2 * M * sizeof(double)));
 
+  gbnd_count_.assign(L_ + 1, 0);
+  ftab_count_.assign(L_ + 1, 0);
+  for (int l = 0; l <= L_; ++l) {
+    gbnd_count_[l] = static_cast<size_t>(M) * 3 * hh.levels[l].n;
+    if (src_kind_ == SRC_TABLE) ftab_count_[l] = fsize(l);
+    stage_count_ += gbnd_count_[l] + ftab_count_[l];
+  }
+  KB_CUDA_CHECK(cudaMallocHost(&stage_, stage_count_ * sizeof(double)));
+  load_problem(prob_);
+  KB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+  KB_CUDA_CHECK(cudaMemset(status_, 0, sizeof(DevStatus)));
+}
+
+Solver2D::~Solver2D() {
+  if (exec_) cudaGraphExecDestroy(exec_);
+  for (cudaEvent_t e : events_) cudaEventDestroy(e);
+  if (own_stream_) cudaStreamDestroy(own_stream_);
+  if (status_host_) cudaFreeHost(status_host_);
+  if (sums_host_) cudaFreeHost(sums_host_);
+  if (stage_) cudaFreeHost(stage_);
+}
+
+void Solver2D::tabulate(const Problem2D& p) {
   // Dirichlet data: g at the owner copy's node coordinates for every
   // domain-boundary copy (set_domain_boundary_values + ReplaceFromOwner,
   // proj/src/fem.cpp:212-228), evaluated with the host libm like the reference.
+  const Hierarchy2D& hh = H_->host;
+  const int M = hh.M;
+  double* dst = stage_;
   for (int l = 0; l <= L_; ++l) {
     const Level2D& lv = hh.levels[l];
     const int n = lv.n;
-    std::vector<double> g(static_cast<size_t>(M) * 3 * n, 0.0);
+    double* g = dst;
+    std::fill(g, g + gbnd_count_[l], 0.0);
     for (int s = 0; s < M; ++s) {
       auto visit = [&](int i, int j) {
         if (!hh.on_domain_boundary(s, l, i, j)) return;
@@ -236,18 +273,19 @@ Solver2D::Solver2D(std::shared_ptr<DeviceHierarchy2D> h, Problem2D p, SolverConf
         const int first = lv.grp_ptr[gid];
         double x, y;
         hh.node_coordinates(lv.mem_slot[first], l, lv.mem_i[first], lv.mem_j[first], x, y);
-        g[static_cast<size_t>(s) * 3 * n + bpos(n, i, j)] = prob_.boundary(x, y);
+        g[static_cast<size_t>(s) * 3 * n + bpos(n, i, j)] = p.boundary(x, y);
       };
       for (int i = 0; i <= n; ++i) visit(i, 0);
       for (int j = 1; j <= n; ++j) visit(0, j);
       for (int j = 1; j <= n - 1; ++j) visit(n - j, j);
     }
-    KB_CUDA_CHECK(cudaMemcpy(gbnd_[l], g.data(), g.size() * 8, cudaMemcpyHostToDevice));
-    if (src_kind_ == SRC_TABLE) {
+    dst += gbnd_count_[l];
+    if (ftab_count_[l]) {
       // f at the cell edge midpoints through the RHS map (proj/src/fem.cpp:183-194)
       const int n2 = 2 * n;
       const int SF = lattice_size(n2);
-      std::vector<double> f(static_cast<size_t>(M) * SF, 0.0);
+      double* f = dst;
+      std::fill(f, f + ftab_count_[l], 0.0);
       for (int s = 0; s < M; ++s) {
         const auto& v = hh.mesh.tri[s];
         const double c0x = hh.mesh.x[v[0]], c0y = hh.mesh.y[v[0]];
@@ -258,20 +296,99 @@ Solver2D::Solver2D(std::shared_ptr<DeviceHierarchy2D> h, Problem2D p, SolverConf
             if (((I | J) & 1) == 0) continue;  // only edge midpoints are used
             const double hi = 0.5 * I, hj = 0.5 * J;
             f[static_cast<size_t>(s) * SF + lattice_index(n2, I, J)] =
-                prob_.source(c0x + hi * ux + hj * wx, c0y + hi * uy + hj * wy);
+                p.source(c0x + hi * ux + hj * wx, c0y + hi * uy + hj * wy);
           }
       }
-      KB_CUDA_CHECK(cudaMemcpy(ftab_[l], f.data(), f.size() * 8, cudaMemcpyHostToDevice));
+      dst += ftab_count_[l];
     }
   }
-  KB_CUDA_CHECK(cudaMemset(status_, 0, sizeof(DevStatus)));
 }
 
-Solver2D::~Solver2D() {
-  if (exec_) cudaGraphExecDestroy(exec_);
-  if (stream_) cudaStreamDestroy(stream_);
-  if (status_host_) cudaFreeHost(status_host_);
-  if (sums_host_) cudaFreeHost(sums_host_);
+size_t Solver2D::load_problem(const Problem2D& p) {
+  // the device source path (table / zero / device-evaluated) was fixed at construction
+  if (p.kind != prob_.kind) fail(KB_STRUCTURAL, "set_problem: the problem kind must match the solver's");
+  if (&p != &prob_) prob_ = p;
+  // the staging buffer may still feed an earlier copy
+  KB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+  tabulate(prob_);
+  size_t bytes = 0;
+  const double* src = stage_;
+  for (int l = 0; l <= L_; ++l) {
+    KB_CUDA_CHECK(cudaMemcpyAsync(gbnd_[l], src, gbnd_count_[l] * 8, cudaMemcpyHostToDevice, stream_));
+    src += gbnd_count_[l];
+    bytes += gbnd_count_[l] * 8;
+    if (ftab_count_[l]) {
+      KB_CUDA_CHECK(cudaMemcpyAsync(ftab_[l], src, ftab_count_[l] * 8, cudaMemcpyHostToDevice, stream_));
+      src += ftab_count_[l];
+      bytes += ftab_count_[l] * 8;
+    }
+  }
+  return bytes;
+}
+
+void Solver2D::set_stream(cudaStream_t st) { stream_ = st ? st : own_stream_; }
+
+void Solver2D::set_profiling(bool on) {
+  if (on == profiling_) return;
+  profiling_ = on;
+  if (exec_) {
+    cudaGraphExecDestroy(exec_);
+    exec_ = nullptr;
+  }
+  fmg_probes_.clear();
+  est_probes_.clear();
+}
+
+cudaEvent_t Solver2D::event_at(int idx) {
+  while (static_cast<int>(events_.size()) <= idx) {
+    cudaEvent_t e;
+    KB_CUDA_CHECK(cudaEventCreate(&e));
+    events_.push_back(e);
+  }
+  return events_[idx];
+}
+
+static void record_event(cudaEvent_t e, cudaStream_t st, bool capturing) {
+  if (capturing)
+    KB_CUDA_CHECK(cudaEventRecordWithFlags(e, st, cudaEventRecordExternal));
+  else
+    KB_CUDA_CHECK(cudaEventRecord(e, st));
+}
+
+void Solver2D::probe_begin(std::vector<Probe>* list) {
+  probes_ = list;
+  list->clear();
+  if (!profiling_) return;
+  // FMG probes use events [0, 1024); estimator probes start at 1024
+  next_event_ = (list == &fmg_probes_) ? 0 : 1024;
+  last_event_ = next_event_++;
+  record_event(event_at(last_event_), stream_, capturing_);
+}
+
+void Solver2D::mark(int kind, double bytes, int nlaunch) {
+  launches_ += nlaunch;
+  if (!profiling_ || !probes_) return;
+  const int e = next_event_++;
+  record_event(event_at(e), stream_, capturing_);
+  probes_->push_back({kind, bytes, last_event_, e});
+  last_event_ = e;
+}
+
+void Solver2D::kernel_stats(int kind, double* ms, int* launches, double* bytes) {
+  double t = 0.0, b = 0.0;
+  int c = 0;
+  for (const auto* list : {&fmg_probes_, &est_probes_})
+    for (const Probe& p : *list) {
+      if (p.kind != kind && kind >= 0) continue;
+      float f = 0.f;
+      KB_CUDA_CHECK(cudaEventElapsedTime(&f, events_[p.ev0], events_[p.ev1]));
+      t += f;
+      b += p.bytes;
+      ++c;
+    }
+  if (ms) *ms = t;
+  if (launches) *launches = c;
+  if (bytes) *bytes = b;
 }
 
 size_t Solver2D::level_size(int level) const {
@@ -295,42 +412,55 @@ void Solver2D::vcycle(int l, double* u, const double* b) {
   if (l == 0) {
     launch_cg0(lev[0], u, b, cg_scratch_, {cfg_.coarse_rel_tol, cfg_.coarse_abs_floor, cfg_.coarse_max_iter},
                status_, stream_);
-    count_launch();
+    mark(KK_CG0, 0.0);
     return;
   }
-  launch_gs(H_->dh, lev[l], u, b, cfg_.pre_smooth, gs_done_, stream_);
-  count_launch(cfg_.pre_smooth > 0);
+  // algorithmic bytes per unique DoF: GS 24/sweep, residual 24,
+  // restriction 8 fine + 8 coarse, prolongation+correction 16 fine + 8 coarse
+  if (cfg_.pre_smooth > 0) {
+    launch_gs(H_->dh, lev[l], u, b, cfg_.pre_smooth, gs_done_, stream_);
+    mark(KK_GS, 24.0 * cfg_.pre_smooth * dofs(l));
+  }
   launch_apply(lev[l], lev[l].kstiff, u, r_[l], b, APPLY_RESIDUAL, stream_);
+  mark(KK_RESIDUAL, 24.0 * dofs(l));
   launch_restrict(lev[l], lev[l - 1], r_[l], vb_[l - 1], 1, stream_);
+  mark(KK_RESTRICT, 8.0 * dofs(l) + 8.0 * dofs(l - 1));
   KB_CUDA_CHECK(cudaMemsetAsync(vu_[l - 1], 0, level_size(l - 1) * 8, stream_));
-  count_launch(2);
+  mark(KK_OTHER, 8.0 * dofs(l - 1), 0);  // memset, not a kernel
   vcycle(l - 1, vu_[l - 1], vb_[l - 1]);
   launch_prolong(lev[l - 1], lev[l], vu_[l - 1], u, nullptr, nullptr, PROLONG_ADD, stream_);
-  launch_gs(H_->dh, lev[l], u, b, cfg_.post_smooth, gs_done_, stream_);
-  count_launch(1 + (cfg_.post_smooth > 0));
+  mark(KK_PROLONG, 16.0 * dofs(l) + 8.0 * dofs(l - 1));
+  if (cfg_.post_smooth > 0) {
+    launch_gs(H_->dh, lev[l], u, b, cfg_.post_smooth, gs_done_, stream_);
+    mark(KK_GS, 24.0 * cfg_.post_smooth * dofs(l));
+  }
 }
 
 void Solver2D::enqueue_fmg_body() {
   // MultigridSolver::fmg, proj/src/multigrid.cpp:248-279
   const auto& lev = H_->lev;
   launches_ = 0;
+  probe_begin(&fmg_probes_);
   KB_CUDA_CHECK(cudaMemsetAsync(status_, 0, sizeof(DevStatus), stream_));
+  mark(KK_OTHER, 0.0, 0);
   for (int l = 0; l <= L_; ++l) {
     launch_rhs(lev[l], src_kind_, ftab_[l], ftab_[l], gbnd_[l], b_[l], stream_);
-    count_launch(src_kind_ == SRC_SIN2D ? 2 : 1);
+    // write b (8 B/DoF) + read the f table (4 midpoints per node) when one is used
+    mark(KK_RHS, 8.0 * dofs(l) + (src_kind_ == SRC_TABLE ? 32.0 * dofs(l) : 0.0), src_kind_ == SRC_SIN2D ? 2 : 1);
   }
   launch_set_boundary(lev[0], u_[0], gbnd_[0], 1, stream_);
-  count_launch();
+  mark(KK_OTHER, 8.0 * dofs(0));
   launch_cg0(lev[0], u_[0], b_[0], cg_scratch_, {cfg_.coarse_rel_tol, cfg_.coarse_abs_floor, cfg_.coarse_max_iter},
              status_, stream_);
-  count_launch();
+  mark(KK_CG0, 0.0);
   for (int l = 0; l < L_; ++l) {
     // w[l] = P u[l] (snapshot before the Dirichlet reset); next = w with g on the boundary
     launch_prolong(lev[l], lev[l + 1], u_[l], w_[l], u_[l + 1], gbnd_[l + 1], PROLONG_W_NEXT, stream_);
-    count_launch();
+    mark(KK_PROLONG, 16.0 * dofs(l + 1) + 8.0 * dofs(l));
     for (int c = 0; c < cfg_.nu; ++c) vcycle(l + 1, u_[l + 1], b_[l + 1]);
   }
   fmg_launches_ = launches_;
+  probes_ = nullptr;
 }
 
 void Solver2D::fmg_enqueue() {
@@ -342,13 +472,16 @@ void Solver2D::fmg_enqueue() {
   if (!exec_) {
     cudaGraph_t graph = nullptr;
     KB_CUDA_CHECK(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+    capturing_ = true;
     try {
       enqueue_fmg_body();
     } catch (...) {
+      capturing_ = false;
       cudaStreamEndCapture(stream_, &graph);
       if (graph) cudaGraphDestroy(graph);
       throw;
     }
+    capturing_ = false;
     KB_CUDA_CHECK(cudaStreamEndCapture(stream_, &graph));
     KB_CUDA_CHECK(cudaGraphInstantiate(&exec_, graph, 0));
     cudaGraphDestroy(graph);
@@ -383,11 +516,14 @@ void Solver2D::estimate_enqueue(int offset) {
   if (offset < 1 || offset > L_ - 1) fail(KB_STRUCTURAL, "estimate offset must satisfy 1 <= j <= L-1");
   const auto& lev = H_->lev;
   const int base = L_ - offset;
+  const int saved = launches_;
+  probe_begin(&est_probes_);
   // e_base = u_L - prolongate_to(w[base], L): w[base] lives on level base+1
   const double* wb = w_[base];
   for (int l = base + 1; l < L_; ++l) {
     double* dst = (l + 1 == L_) ? est_tmp_a_ : vu_[l + 1];
     launch_prolong(lev[l], lev[l + 1], wb, dst, nullptr, nullptr, PROLONG_ASSIGN, stream_);
+    mark(KK_ESTIMATE, 8.0 * dofs(l + 1) + 8.0 * dofs(l));
     wb = dst;
   }
   // e_coarser = u_L - prolongate_to(w[base-1], L); the last prolongation is inline
@@ -395,11 +531,17 @@ void Solver2D::estimate_enqueue(int offset) {
   for (int l = base; l < L_ - 1; ++l) {
     double* dst = (l + 1 == L_ - 1) ? est_tmp_b_ : vb_[l + 1];
     launch_prolong(lev[l], lev[l + 1], wc, dst, nullptr, nullptr, PROLONG_ASSIGN, stream_);
+    mark(KK_ESTIMATE, 8.0 * dofs(l + 1) + 8.0 * dofs(l));
     wc = dst;
   }
   launch_estimate(lev[L_], u_[L_], wb, wc, est_sums_, stream_);
+  // one fused pass reads u_L, w[L-1] and w[L-2] (inline prolongation): 18 B per fine DoF (2-d)
+  mark(KK_ESTIMATE, 16.0 * dofs(L_) + 8.0 * dofs(L_ - 1));
+  est_launches_ = launches_ - saved;
+  launches_ = saved;
   KB_CUDA_CHECK(cudaMemcpyAsync(sums_host_, est_sums_, 2 * H_->host.M * sizeof(double), cudaMemcpyDeviceToHost,
                                 stream_));
+  probes_ = nullptr;
 }
 
 EstimateReport2D Solver2D::estimate_finish(int offset, int kind) {

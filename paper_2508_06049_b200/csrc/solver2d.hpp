@@ -9,6 +9,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cstddef>
 #include <functional>
 #include <memory>
 #include <vector>
@@ -78,6 +79,18 @@ class Solver2D {
 
   const Hierarchy2D& hier() const { return H_->host; }
   cudaStream_t stream() const { return stream_; }
+  // launch on a caller-owned stream from now on (nullptr: back to the solver's own)
+  void set_stream(cudaStream_t st);
+  // (re)tabulate the problem's f and g on the host and copy them to the device
+  // through pinned staging buffers; returns the bytes copied host->device
+  std::size_t load_problem(const Problem2D& p);
+
+  // Per-kernel CUDA-event probes (roofline evidence): when enabled, every
+  // kernel of the FMG graph / estimator is bracketed by event records, and
+  // kernel_stats() sums the device time and algorithmic bytes per kernel kind
+  // over the most recent FMG + estimate.
+  void set_profiling(bool on);
+  void kernel_stats(int kind, double* ms, int* launches, double* bytes);
 
   // FMG (proj/src/multigrid.cpp:248-321) into the solver-owned FmgState.
   void fmg_enqueue();
@@ -101,15 +114,23 @@ class Solver2D {
   double dot_unique(int level, const double* a, const double* b);
   void interface_sync(int level, double* f, int additive);
   int launches_per_fmg() const { return fmg_launches_; }
+  int launches_per_estimate() const { return est_launches_; }
   int last_cg_iters() const;
 
  private:
   void vcycle(int l, double* u, const double* b);
   void enqueue_fmg_body();
-  int count_launch(int k = 1) {
-    launches_ += k;
-    return launches_;
-  }
+  struct Probe {
+    int kind;
+    double bytes;
+    int ev0, ev1;
+  };
+  // after a kernel launch: count it and, when profiling, close its probe
+  void mark(int kind, double bytes, int nlaunch = 1);
+  void probe_begin(std::vector<Probe>* list);
+  cudaEvent_t event_at(int idx);
+  void tabulate(const Problem2D& p);
+  double dofs(int l) const { return static_cast<double>(H_->host.levels[l].dofs); }
 
   std::shared_ptr<DeviceHierarchy2D> H_;
   Problem2D prob_;
@@ -130,7 +151,19 @@ class Solver2D {
   double* sums_host_ = nullptr;
   int src_kind_ = SRC_ZERO;
   cudaGraphExec_t exec_ = nullptr;
-  int launches_ = 0, fmg_launches_ = 0;
+  int launches_ = 0, fmg_launches_ = 0, est_launches_ = 0;
+  cudaStream_t own_stream_ = nullptr;
+  // pinned staging of the problem tables (Dirichlet g per level, f table per level)
+  double* stage_ = nullptr;
+  std::size_t stage_count_ = 0;
+  std::vector<std::size_t> gbnd_count_, ftab_count_;
+  // profiling probes
+  bool profiling_ = false;
+  bool capturing_ = false;
+  std::vector<cudaEvent_t> events_;
+  int next_event_ = 0, last_event_ = -1;
+  std::vector<Probe>* probes_ = nullptr;
+  std::vector<Probe> fmg_probes_, est_probes_;
 };
 
 }  // namespace kb

@@ -72,6 +72,10 @@ SYNC_REPLACE, SYNC_ADDITIVE = 0, 1
 STATE_U, STATE_B, STATE_W = 0, 1, 2
 PROBLEM_ZERO, PROBLEM_SIN2D, PROBLEM_LSHAPE = 0, 1, 2
 MARK_TOP_FRACTION, MARK_HALF_MAX = 0, 1
+KERNEL_ALL, KERNEL_GS, KERNEL_RESIDUAL, KERNEL_RESTRICT, KERNEL_PROLONG = -1, 0, 1, 2, 3
+KERNEL_RHS, KERNEL_CG0, KERNEL_ESTIMATE, KERNEL_OTHER = 4, 5, 6, 7
+KERNEL_NAMES = {0: "gauss_seidel", 1: "residual", 2: "restrict", 3: "prolongate", 4: "rhs", 5: "cg_level0",
+                6: "estimate", 7: "other"}
 
 
 class SolverConfigC(C.Structure):
@@ -128,6 +132,11 @@ SIGNATURES = {
     "klref_solver_launch_count": (_I, [_P, _PI]),
     "klref_solver_last_cg_iterations": (_I, [_P, _PI]),
     "klref_solver_state_read": (_I, [_P, _I, _I, _PD]),
+    "klref_solver_estimate_launch_count": (_I, [_P, _PI]),
+    "klref_solver_set_stream": (_I, [_P, _P]),
+    "klref_solver_set_problem": (_I, [_P, _P, _PI64]),
+    "klref_solver_set_profiling": (_I, [_P, _I]),
+    "klref_solver_kernel_stats": (_I, [_P, _I, _PD, _PI, _PD]),
     "klref_error_estimate": (_I, [_P, _I, _I, C.POINTER(EstimateReportC), _PD]),
     "klref_error_estimate_enqueue": (_I, [_P, _I]),
     "klref_error_estimate_finish": (_I, [_P, _I, _I, C.POINTER(EstimateReportC), _PD]),
@@ -439,6 +448,41 @@ class MultigridSolver(_Handle):
         v = C.c_int()
         _check(lib().klref_solver_last_cg_iterations(self.ptr, C.byref(v)))
         return v.value
+
+    def estimate_launch_count(self) -> int:
+        v = C.c_int()
+        _check(lib().klref_solver_estimate_launch_count(self.ptr, C.byref(v)))
+        return v.value
+
+    def set_stream(self, stream: int):
+        """Launch on a caller-owned cudaStream_t (an int handle, e.g. torch's
+        ``cuda_stream``); 0 returns to the solver's own stream."""
+        _check(lib().klref_solver_set_stream(self.ptr, C.c_void_p(stream or None)))
+
+    def set_problem(self, problem: "Problem") -> int:
+        """Re-tabulate the problem data on the host and copy it to the device;
+        returns the host->device bytes."""
+        v = C.c_int64()
+        _check(lib().klref_solver_set_problem(self.ptr, problem.ptr, C.byref(v)))
+        self.problem = problem
+        return v.value
+
+    def set_profiling(self, on: bool):
+        _check(lib().klref_solver_set_profiling(self.ptr, int(bool(on))))
+
+    def kernel_stats(self, kind: int = KERNEL_ALL):
+        """(device ms, launches, algorithmic bytes) of one kernel kind over the
+        most recent FMG + estimate (needs set_profiling(True))."""
+        ms, n, b = C.c_double(), C.c_int(), C.c_double()
+        _check(lib().klref_solver_kernel_stats(self.ptr, kind, C.byref(ms), C.byref(n), C.byref(b)))
+        return ms.value, n.value, b.value
+
+    def state_into(self, which: int, level: int, out: np.ndarray) -> np.ndarray:
+        """FmgState component copied device->host into a caller buffer (e.g. pinned)."""
+        if out.size != self.h.level_size(level) or out.dtype != np.float64:
+            raise StructuralError("state_into: buffer size / dtype mismatch")
+        _check(lib().klref_solver_state_read(self.ptr, which, level, _dptr(out)))
+        return out
 
     def state(self, which: int, level: int) -> np.ndarray:
         out = np.empty(self.h.level_size(level), dtype=np.float64)
