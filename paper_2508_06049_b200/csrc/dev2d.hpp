@@ -34,9 +34,11 @@ struct DevLevel2D {
   int num_groups;
   const int* dot_order;
   int dot_count;
-  const unsigned long long* blob;  // per-macro relaxation blobs (Level2D::blob)
-  const int* blob_desc;
-  int blob_max_words;
+  const unsigned long long* prog;        // smoother step programs (Level2D::prog)
+  const long long* prog_ptr;
+  const unsigned long long* prog_extra;  // vertex-group members beyond the second
+  const int* xtra_ptr;
+  int max_extra;
   const double* geo;   // per macro: c0x, c0y, ux, uy, wx, wy (RHS quadrature map, proj/src/fem.cpp:183-186)
   const double* wq;    // per macro: cell_area / 3
 };

@@ -65,56 +65,89 @@ std::uint64_t pack16(std::int16_t a, std::int16_t b, std::int16_t c, std::int16_
          (static_cast<std::uint64_t>(static_cast<std::uint16_t>(d)) << 48);
 }
 
-// Per-macro relaxation blobs (layout in hier2d.hpp, Level2D::blob).
-void build_blobs(Level2D& lvl, int M) {
-  const int n = lvl.n;
-  lvl.blob.clear();
-  lvl.blob_desc.assign(4 * static_cast<std::size_t>(M), 0);
-  lvl.blob_max_words = 0;
-  for (int m = 0; m < M; ++m) {
-    const std::size_t begin = lvl.blob.size();
-    std::vector<std::uint64_t> nodes, recs, wrs, kmat;
-    std::vector<int> wr32;
-    std::map<int, int> kslot;
-    int nrec = 0;
-    for (int p = 0; p < 3 * n; ++p) {
-      const BNode& bn = lvl.bnode[static_cast<std::size_t>(m) * 3 * n + p];
-      std::uint64_t d;
-      std::memcpy(&d, &bn.diag, 8);
-      nodes.push_back(d);
-      nodes.push_back(pack32(nrec, (bn.rec_count & 0xffff) | (bn.domain << 16)));
-      nodes.push_back(pack32(static_cast<int>(wr32.size()), bn.wr_count));
-      for (int r = 0; r < bn.rec_count; ++r) {
-        const MemberRec& rec = lvl.rec[bn.rec_begin + r];
-        auto it = kslot.find(rec.slot);
-        int ks;
-        if (it == kslot.end()) {
-          ks = static_cast<int>(kslot.size());
-          kslot[rec.slot] = ks;
-          for (int q = 0; q < 18; ++q) {
-            std::uint64_t w;
-            std::memcpy(&w, &lvl.kstiff[18 * static_cast<std::size_t>(rec.slot) + q], 8);
-            kmat.push_back(w);
-          }
-        } else {
-          ks = it->second;
-        }
-        recs.push_back(pack16(static_cast<std::int16_t>(ks), static_cast<std::int16_t>(rec.mask), rec.loc[0], rec.loc[1]));
-        recs.push_back(pack16(rec.loc[2], rec.loc[3], rec.loc[4], rec.loc[5]));
-        recs.push_back(pack16(rec.loc[6], rec.loc[7], rec.loc[8], rec.loc[9]));
-        recs.push_back(pack16(rec.loc[10], rec.loc[11], 0, 0));
-        ++nrec;
-      }
-      for (int q = 0; q < bn.wr_count; ++q) wr32.push_back(lvl.wr[bn.wr_begin + q]);
+std::uint64_t dbits(double d) {
+  std::uint64_t w;
+  std::memcpy(&w, &d, 8);
+  return w;
+}
+
+// one compact member record: existing cells' coefficient pairs and reads
+void put_rec(std::uint64_t* w, const MemberRec& rec, const Level2D& lvl) {
+  const double* ku = &lvl.kstiff[18 * static_cast<std::size_t>(rec.slot)];
+  static const int ci[12] = {1, 2, 3, 5, 6, 7, 10, 11, 12, 14, 15, 16};
+  double c[6] = {0, 0, 0, 0, 0, 0};
+  std::int16_t loc[6] = {0, 0, 0, 0, 0, 0};
+  int nc = 0;
+  for (int cell = 0; cell < 6; ++cell) {
+    if (!((rec.mask >> cell) & 1)) continue;
+    if (nc == 3) fail(KB_INTERNAL, "boundary node with more than three cells in one macro");
+    for (int q = 0; q < 2; ++q) {
+      c[2 * nc + q] = ku[ci[2 * cell + q]];
+      loc[2 * nc + q] = rec.loc[2 * cell + q];
     }
-    if (wr32.size() & 1) wr32.push_back(0);
-    for (std::size_t q = 0; q < wr32.size(); q += 2) wrs.push_back(pack32(wr32[q], wr32[q + 1]));
-    for (auto* part : {&nodes, &recs, &wrs, &kmat}) lvl.blob.insert(lvl.blob.end(), part->begin(), part->end());
-    lvl.blob_desc[4 * m] = static_cast<int>(begin);
-    lvl.blob_desc[4 * m + 1] = nrec;
-    lvl.blob_desc[4 * m + 2] = static_cast<int>(wr32.size());
-    lvl.blob_desc[4 * m + 3] = static_cast<int>(kslot.size());
-    lvl.blob_max_words = std::max(lvl.blob_max_words, static_cast<int>(lvl.blob.size() - begin));
+    ++nc;
+  }
+  for (int q = 0; q < 6; ++q) w[q] = dbits(c[q]);
+  w[6] = pack16(loc[0], loc[1], loc[2], loc[3]);
+  w[7] = pack16(loc[4], loc[5], static_cast<std::int16_t>(nc), 0);
+}
+
+// Step programs (layout in hier2d.hpp, Level2D::prog).
+void build_programs(Level2D& lvl, int M) {
+  const int n = lvl.n;
+  const std::size_t per_macro = static_cast<std::size_t>(2 * n + 1) * kProgStepWords;
+  lvl.prog.assign(per_macro * M, 0);
+  lvl.prog_ptr.assign(M, 0);
+  lvl.prog_extra.clear();
+  lvl.xtra_ptr.assign(M + 1, 0);
+  lvl.max_extra = 0;
+  for (int m = 0; m < M; ++m) {
+    lvl.prog_ptr[m] = static_cast<long long>(per_macro * m);
+    int nextra = 0;
+    for (int t = 0; t <= 2 * n; ++t) {
+      for (int type = 0; type < 3; ++type) {
+        std::uint64_t* w = &lvl.prog[per_macro * m + static_cast<std::size_t>(t) * kProgStepWords +
+                                     static_cast<std::size_t>(type) * kProgNodeWords];
+        int i = -1, j = -1;
+        if (type == 0 && t <= n) {
+          i = t;
+          j = 0;
+        } else if (type == 1 && !(t & 1) && t >= 2) {
+          i = 0;
+          j = t / 2;
+        } else if (type == 2 && t > n && t < 2 * n) {
+          j = t - n;
+          i = n - j;
+        }
+        if (i < 0) {
+          w[0] = pack32(-1, 0);
+          continue;
+        }
+        const BNode& bn = lvl.bnode[static_cast<std::size_t>(m) * 3 * n + bpos(n, i, j)];
+        const int k = lattice_index(n, i, j);
+        const int rc = bn.domain ? 0 : bn.rec_count;
+        // header: k | flags (domain, member count) ; wr0 | wr1 ; wr_begin | wr_count ; extra index | 0 ; diag ; 1/diag
+        w[0] = pack32(k, (bn.domain ? 1 : 0) | (rc << 8));
+        w[1] = pack32(bn.wr_count > 0 ? lvl.wr[bn.wr_begin] : 0, bn.wr_count > 1 ? lvl.wr[bn.wr_begin + 1] : 0);
+        w[2] = pack32(bn.wr_begin, bn.wr_count);
+        w[3] = pack32(nextra, 0);
+        w[4] = dbits(bn.diag);
+        w[5] = dbits(bn.diag != 0.0 ? 1.0 / bn.diag : 0.0);
+        for (int r = 0; r < rc; ++r) {
+          const MemberRec& rec = lvl.rec[bn.rec_begin + r];
+          if (r < 2) {
+            put_rec(w + 6 + r * kProgRecWords, rec, lvl);
+          } else {
+            std::uint64_t x[kProgRecWords];
+            put_rec(x, rec, lvl);
+            lvl.prog_extra.insert(lvl.prog_extra.end(), x, x + kProgRecWords);
+            ++nextra;
+          }
+        }
+      }
+    }
+    lvl.xtra_ptr[m + 1] = static_cast<int>(lvl.prog_extra.size());
+    lvl.max_extra = std::max(lvl.max_extra, nextra);
   }
 }
 
@@ -508,7 +541,7 @@ Hierarchy2D Hierarchy2D::build(const Mesh2D& mesh, int max_level) {
       lvl.ghost_ptr.push_back(static_cast<int>(lvl.ghost_off.size()));
       lvl.max_ghosts = std::max(lvl.max_ghosts, static_cast<int>(ghosts.size()));
     }
-    build_blobs(lvl, M);
+    build_programs(lvl, M);
   }
   return h;
 }

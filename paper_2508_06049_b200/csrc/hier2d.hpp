@@ -64,6 +64,10 @@ struct BNode {
   double diag;                      // sum over members of the partial diagonals
 };
 
+constexpr int kProgRecWords = 8;                          // 6 coefficients, 6 reads, cell count
+constexpr int kProgNodeWords = 6 + 2 * kProgRecWords;     // header + two member records
+constexpr int kProgStepWords = 3 * kProgNodeWords;        // three boundary-node types per step
+
 struct Level2D {
   int n = 1, S = 3;
   // shared-node groups (vertex groups first, then edge groups), members ascending slot
@@ -84,17 +88,19 @@ struct Level2D {
   std::vector<int> wr;                     // global copy offsets
   std::vector<int> ghost_ptr, ghost_off;   // per macro ghost lists (global offsets)
   int max_ghosts = 0;
-  // Per-macro relaxation blob for the shared-memory smoother (staged into
-  // shared memory once per macro sweep; 8-byte words):
-  //   [0, 9n)        3n boundary nodes x 3 words: diag | rec_begin:i32 rec_count:i16 domain:i16 |
-  //                  wr_begin:i32 wr_count:i32   (boundary position order, bpos())
-  //   [9n, +4 nrec)  records: kslot:i16 mask:i16 loc[12]:i16 (kslot indexes the kmat area)
-  //   [.., +nwr/2)   copy targets (global copy offsets, i32)
-  //   [.., +18 nk)   stiffness up/down matrices of the member macros
-  // blob_desc[4m..4m+3] = word offset, nrec, nwr, nk.
-  std::vector<std::uint64_t> blob;
-  std::vector<int> blob_desc;
-  int blob_max_words = 0;
+  // Step programs of the shared-memory smoother (kernels2d.cu, k_gs_*): for
+  // every macro, wavefront step t = 0..2n and boundary-node type (row 0, left
+  // edge, hypotenuse) one ProgNode of kProgNodeWords 8-byte words -- the
+  // node's lattice index, flags, copy targets, diag and RN(1/diag), and the
+  // compact partial_row records of its first two group members (existing
+  // cells only, in the order of proj/src/fem.cpp:138-172; reads are lattice
+  // indices of the relaxing macro or ghost slots -1-g).  Members beyond the
+  // second (vertex groups) live in prog_extra; prog_ptr[m] / xtra_ptr[m] are
+  // word offsets of macro m's program / extra records.
+  std::vector<std::uint64_t> prog, prog_extra;
+  std::vector<long long> prog_ptr;
+  std::vector<int> xtra_ptr;
+  int max_extra = 0;  // most extra records of one macro
   // owner dot order (dot_unique, proj/src/hhg.cpp:227-257): offsets in summation order
   std::vector<int> dot_order;
 };

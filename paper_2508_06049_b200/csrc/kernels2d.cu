@@ -26,6 +26,23 @@ namespace {
 
 constexpr int kThreads = 256;
 
+#ifdef KB_GS_TRACE
+__device__ long long g_gs_trace[4][1 << 12];  // debug builds only: per-step clocks of block 0
+__device__ int g_dbg_S, g_dbg_G, g_dbg_MS;
+#define KB_CHECK(cond, code, a, b)                                                        \
+  do {                                                                                    \
+    if (!(cond) && atomicCAS(reinterpret_cast<unsigned long long*>(&g_gs_trace[3][4000]), 0ull, 1ull) == 0ull) { \
+      g_gs_trace[3][4001] = (code);                                                       \
+      g_gs_trace[3][4002] = (a);                                                          \
+      g_gs_trace[3][4003] = (b);                                                          \
+    }                                                                                     \
+  } while (0)
+#else
+#define KB_CHECK(cond, code, a, b) \
+  do {                             \
+  } while (0)
+#endif
+
 __device__ __forceinline__ int dlat(int n, int i, int j) { return j * (n + 1) - (j * (j - 1)) / 2 + i; }
 
 __device__ __forceinline__ void decode(int n, int idx, int& i, int& j) {
@@ -555,201 +572,367 @@ __global__ void __launch_bounds__(576, 1) k_gs(DevHier2D hd, DevLevel2D lv, doub
 
 
 // ------------------------------------------------ Gauss-Seidel, shared-memory
-// One warp relaxes one macro lattice held in shared memory.  Lane l owns rows
-// j = l + 32 r (r < R) and at wavefront step t = i + 2j updates node
-// (t - 2j, j) of each of its rows; every stencil neighbour of a step-t node
-// belongs to step t +- 1 or t +- 2, so a __syncwarp between
-// steps is the only synchronisation.  Interior nodes use the 7-point form of
-// proj/src/multigrid.cpp:170-175; lattice-boundary nodes the group gather of
-// relax_boundary_node (:132-150) over partial_row records whose reads are
-// either lattice indices of this macro or ghost values staged in `gh`.
-// View of one macro's relaxation blob staged in shared memory (Level2D::blob).
-struct BlobView {
-  const unsigned long long* w;
-  const short* recs;
-  const int* wr;
-  const double* km;
-};
+// One group of warps relaxes one macro lattice held in shared memory, along
+// the hyperplane wavefront t = i + 2j (every stencil neighbour
+// of a step-t node belongs to step t +- 1 or t +- 2, so a named barrier per
+// step is the only synchronisation).  Warp roles:
+//   warp 0  boundary warp: the (at most three) lattice-boundary nodes of step t,
+//           lane 8 type + q evaluating the partial row of group member q;
+//   warp 1  program warp: streams the precompiled step programs
+//           (Level2D::prog) into a shared-memory ring with cp.async, kRingSteps
+//           steps ahead, so the boundary warp never waits on L2;
+//   warp 2+ interior warps, one lattice row per lane (7-point form of
+//           proj/src/multigrid.cpp:170-175).
+constexpr int kRingSteps = 8;
+constexpr int kStepBytes = kProgStepWords * 8;  // 528 = 33 x 16 B
+static_assert(kStepBytes % 16 == 0, "step programs are copied in 16-byte chunks");
 
-__device__ __forceinline__ BlobView blob_view(const unsigned long long* w, int n, int nrec, int nwr) {
-  BlobView v;
-  v.w = w;
-  v.recs = reinterpret_cast<const short*>(w + 9 * n);
-  v.wr = reinterpret_cast<const int*>(w + 9 * n + 4 * nrec);
-  v.km = reinterpret_cast<const double*>(w + 9 * n + 4 * nrec + nwr / 2);
+__device__ __forceinline__ void bar_sync(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async16(unsigned dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ double ld_s64(unsigned a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_s64(unsigned a, double v) {
+  asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_s64u(unsigned a) {
+  unsigned long long v;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a) : "memory");
   return v;
 }
 
-// copy one macro's blob (and ghosts) into shared memory with the whole warp
-__device__ __forceinline__ BlobView stage_blob(const DevLevel2D& lv, int m, unsigned long long* dst, int lane) {
-  const int beg = lv.blob_desc[4 * m], nrec = lv.blob_desc[4 * m + 1], nwr = lv.blob_desc[4 * m + 2],
-            nk = lv.blob_desc[4 * m + 3];
-  const int words = 9 * lv.n + 4 * nrec + nwr / 2 + 18 * nk;
-  for (int q = lane; q < words; q += 32) dst[q] = __ldg(lv.blob + beg + q);
-  return blob_view(dst, lv.n, nrec, nwr);
+// One member record of a step program (8 words): c[6], reads[6], cell count.
+struct PRec {
+  double c[6];
+  int loc[6];
+  int nc;
+};
+// Node header + this lane's member record.
+struct PNode {
+  int k, flags, wr0, wr1, wb, wc, xb;
+  double diag, inv, B;
+  PRec r;
+};
+
+__device__ __forceinline__ void load_prec(PRec& r, unsigned a) {
+#pragma unroll
+  for (int q = 0; q < 6; ++q) r.c[q] = __longlong_as_double(static_cast<long long>(ld_s64u(a + 8 * q)));
+  const unsigned long long w6 = ld_s64u(a + 48), w7 = ld_s64u(a + 56);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) r.loc[q] = static_cast<short>((w6 >> (16 * q)) & 0xffff);
+  r.loc[4] = static_cast<short>(w7 & 0xffff);
+  r.loc[5] = static_cast<short>((w7 >> 16) & 0xffff);
+  r.nc = static_cast<int>((w7 >> 32) & 0xffff);
 }
 
-// relax_boundary_node (proj/src/multigrid.cpp:132-150) from the staged blob:
-// group members in ascending slot, partial_row cells in the order of
-// proj/src/fem.cpp:138-172, off accumulated per member then summed.
-__device__ __forceinline__ double relax_blob(const BlobView& bv, int p, double B, const double* us,
-                                             const double* gh, double* copies) {
-  const unsigned long long w1 = bv.w[3 * p + 1], w2 = bv.w[3 * p + 2];
-  const int rb = static_cast<int>(w1 & 0xffffffffull);
-  const int rc = static_cast<int>((w1 >> 32) & 0xffff);
-  const int domain = static_cast<int>(w1 >> 48);
-  double res = B;
-  if (!domain) {
-    double off = 0.0;
-    for (int r = rb; r < rb + rc; ++r) {
-      const short* rec = bv.recs + 16 * r;
-      const double* ku = bv.km + 18 * rec[0];
-      const double* kd = ku + 9;
-      const int mask = rec[1];
-      auto X = [&](int q) {
-        const int loc = rec[2 + q];
-        return loc >= 0 ? us[loc] : gh[-1 - loc];
-      };
-      double o = 0.0;
-      if (mask & 1) o += ku[1] * X(0) + ku[2] * X(1);
-      if (mask & 2) o += ku[3] * X(2) + ku[5] * X(3);
-      if (mask & 4) o += ku[6] * X(4) + ku[7] * X(5);
-      if (mask & 8) o += kd[1] * X(6) + kd[2] * X(7);
-      if (mask & 16) o += kd[3] * X(8) + kd[5] * X(9);
-      if (mask & 32) o += kd[6] * X(10) + kd[7] * X(11);
-      off += o;
+// lane (type, mem): node header of its type and record `mem` (mem < 2 from the
+// ring slot, mem >= 2 from the staged extra records)
+__device__ __forceinline__ void load_pnode(PNode& p, unsigned slot, unsigned xs, int type, int mem) {
+  const unsigned h = slot + 8u * kProgNodeWords * static_cast<unsigned>(type);
+  const unsigned long long w0 = ld_s64u(h), w1 = ld_s64u(h + 8), w2 = ld_s64u(h + 16), w3 = ld_s64u(h + 24);
+  p.k = static_cast<int>(w0 & 0xffffffffull);
+  p.flags = static_cast<int>(w0 >> 32);
+  p.wr0 = static_cast<int>(w1 & 0xffffffffull);
+  p.wr1 = static_cast<int>(w1 >> 32);
+  p.wb = static_cast<int>(w2 & 0xffffffffull);
+  p.wc = static_cast<int>(w2 >> 32);
+  p.xb = static_cast<int>(w3 & 0xffffffffull);
+  p.diag = __longlong_as_double(static_cast<long long>(ld_s64u(h + 32)));
+  p.inv = __longlong_as_double(static_cast<long long>(ld_s64u(h + 40)));
+  const int rc = (p.k >= 0) ? (p.flags >> 8) : 0;
+  const unsigned ra = mem < 2 ? h + 48u + 64u * static_cast<unsigned>(mem)
+                              : xs + 64u * static_cast<unsigned>(mem - 2 < rc - 2 ? p.xb + mem - 2 : 0);
+  load_prec(p.r, ra);
+  if (mem >= rc) {  // no record for this lane: reads stay in bounds, no cells
+#pragma unroll
+    for (int q = 0; q < 6; ++q) p.r.loc[q] = 0;
+    p.r.nc = 0;
+  }
+}
+
+// Relax the boundary nodes of one step (relax_boundary_node,
+// proj/src/multigrid.cpp:132-150): member off-diagonal sums o (cells in the
+// order of proj/src/fem.cpp:138-172), summed over members in slot order,
+// (b - off) / diag correctly rounded, written to every copy.
+__device__ __forceinline__ void relax_nodes(const PNode& p, unsigned us_s, unsigned bs_s, unsigned gh_s,
+                                            double* copies, const int* wr_global, int lane) {
+  const int type = lane >> 3, mem = lane & 7;
+  const bool lane_ok = type < 3;
+  const int rc = (lane_ok && p.k >= 0) ? (p.flags >> 8) : 0;
+  // reads: lattice values of this macro, or ghost values (constant during the sweep)
+  double x[6];
+#pragma unroll
+  for (int q = 0; q < 6; ++q) {
+    const int l = p.r.loc[q];
+#ifdef KB_GS_TRACE
+    if (l >= g_dbg_S || -1 - l > g_dbg_G) {
+      KB_CHECK(false, 2, l, 1000 * q + lane);
+      x[q] = 0.0;
+      continue;
     }
-    res = (B - off) / __longlong_as_double(static_cast<long long>(bv.w[3 * p]));
+#endif
+    x[q] = ld_s64(l >= 0 ? us_s + 8u * l : gh_s + 8u * (-1 - l));
   }
-  const int wb = static_cast<int>(w2 & 0xffffffffull), wc = static_cast<int>(w2 >> 32);
-  for (int q = wb; q < wb + wc; ++q) copies[bv.wr[q]] = res;
-  return res;
+  const double B = ld_s64(bs_s + 8u * (p.k >= 0 ? p.k : 0));
+  double o = 0.0;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const double on = o + (p.r.c[2 * c] * x[2 * c] + p.r.c[2 * c + 1] * x[2 * c + 1]);
+    o = c < p.r.nc ? on : o;
+  }
+  o = mem < rc ? o : 0.0;
+  double off = 0.0;
+  if (__any_sync(0xffffffffu, rc > 2)) {
+    // a vertex group with more than two members: sequential sum over members
+    for (int r = 0; r < 8; ++r) {
+      const double orr = __shfl_sync(0xffffffffu, o, (lane & ~7) + r);
+      if (r < rc) off = off + orr;
+    }
+  } else {
+    const double o1 = __shfl_down_sync(0xffffffffu, o, 1);
+    if (rc >= 1) off = off + o;
+    if (rc >= 2) off = off + o1;
+  }
+  if (lane_ok && mem == 0 && p.k >= 0) {
+#ifdef KB_GS_TRACE
+    if (p.k >= g_dbg_S || (p.wc > 0 && (p.wr0 < 0 || p.wr0 >= g_dbg_MS)) || (p.wc > 1 && (p.wr1 < 0 || p.wr1 >= g_dbg_MS))) {
+      KB_CHECK(false, 1, p.k, p.wr0 * 100000ll + p.wr1);
+      return;
+    }
+#endif
+    double res = B;
+    if (!(p.flags & 1)) {
+      // (B - off) / diag correctly rounded: q = x y, r = x - q d exactly (FMA),
+      // RN(q + r y) = RN(x / d) for y = RN(1 / d) (Markstein); a zero
+      // numerator keeps its sign through x * y.
+      const double xn = B - off;
+      const double q = xn * p.inv;
+      const double r = __fma_rn(-q, p.diag, xn);
+      res = xn == 0.0 ? q : __fma_rn(r, p.inv, q);
+    }
+    st_s64(us_s + 8u * p.k, res);
+    if (p.wc > 0) copies[p.wr0] = res;
+    if (p.wc > 1) copies[p.wr1] = res;
+    for (int q = p.wb + 2; q < p.wb + p.wc; ++q) copies[wr_global[q]] = res;
+  }
 }
 
-template <int R>
-__device__ __forceinline__ void warp_sweep(const DevLevel2D& lv, int m, double* us, const double* bs,
-                                           const double* gh, const BlobView& bv, double* copies, int lane) {
-  const int n = lv.n;
-  const double* st = lv.stencil + 7 * m;
-  const double s1 = st[1], s2 = st[2], s3 = st[3], s4 = st[4], s5 = st[5], s6 = st[6];
-  const double inv_c = lv.inv_c[m];
-  int rowk[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int j = lane + 32 * r;
-    rowk[r] = j <= n ? dlat(n, 0, j) : 0;
+// Issue the cp.async copies of step program `t` (if it exists) into its ring
+// slot; always commits a group so that group counting stays uniform.
+__device__ __forceinline__ void stream_step(const unsigned long long* prog_m, unsigned ring_s, int n, int t, int lane) {
+  if (t <= 2 * n) {
+    const char* src = reinterpret_cast<const char*>(prog_m + static_cast<size_t>(t) * kProgStepWords);
+    const unsigned dst = ring_s + static_cast<unsigned>(t % kRingSteps) * kStepBytes;
+    for (int c = lane; c < kStepBytes / 16; c += 32) cp_async16(dst + 16u * c, src + 16 * c);
   }
-  for (int t = 0; t <= 2 * n; ++t) {
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int j = lane + 32 * r;
+  cp_async_commit();
+}
+
+__device__ __forceinline__ void group_sweep(const DevLevel2D& lv, int m, double* us, const double* bs,
+                                            const double* gh, const unsigned long long* xs, unsigned char* ring,
+                                            double* copies, int gw, int lane, int bar_id, int bar_threads) {
+  const int n = lv.n;
+  const unsigned ring_s = smem_addr(ring);
+#ifdef KB_GS_TRACE
+  if (threadIdx.x == 0) {
+    g_dbg_S = lv.S;
+    g_dbg_G = lv.max_ghosts;
+    g_dbg_MS = lv.M * lv.S;
+  }
+#endif
+  if (gw == 1) {
+    const unsigned long long* prog_m = lv.prog + lv.prog_ptr[m];
+    // lookahead kRingSteps - 1: during step t the slot of step t - 1 is refilled
+    // (the boundary warp read it before the barrier that ended step t - 1)
+#pragma unroll 1
+    for (int t = 0; t < kRingSteps - 1; ++t) stream_step(prog_m, ring_s, n, t, lane);
+    cp_async_wait<kRingSteps - 3>();  // steps 0 and 1 landed
+    bar_sync(bar_id, bar_threads);
+    for (int t = 0; t <= 2 * n; ++t) {
+      stream_step(prog_m, ring_s, n, t + kRingSteps - 1, lane);
+      cp_async_wait<kRingSteps - 3>();  // step t + 2 landed
+      bar_sync(bar_id, bar_threads);
+    }
+    cp_async_wait<0>();
+  } else if (gw == 0) {
+    const unsigned us_s = smem_addr(us), bs_s = smem_addr(bs), gh_s = smem_addr(gh), xs_s = smem_addr(xs);
+    const int type = lane >> 3, mem = lane & 7;
+    const int tl = type < 3 ? type : 0;
+    bar_sync(bar_id, bar_threads);
+    PNode cur;
+    load_pnode(cur, ring_s, xs_s, tl, mem);
+    for (int t = 0; t <= 2 * n; ++t) {
+#ifdef KB_GS_TRACE
+      if (blockIdx.x == 0 && lane == 0 && bar_id == 1) g_gs_trace[0][t] = clock64();
+#endif
+      PNode nxt;
+      // the slot after the last step holds stale shared memory: never decode it
+      if (t < 2 * n) load_pnode(nxt, ring_s + static_cast<unsigned>((t + 1) % kRingSteps) * kStepBytes, xs_s, tl, mem);
+#ifdef KB_GS_TRACE
+      if (blockIdx.x == 0 && lane == 0 && bar_id == 1) g_gs_trace[1][t] = clock64();
+#endif
+      relax_nodes(cur, us_s, bs_s, gh_s, copies, lv.wr, lane);
+#ifdef KB_GS_TRACE
+      if (blockIdx.x == 0 && lane == 0 && bar_id == 1) g_gs_trace[2][t] = clock64();
+#endif
+      cur = nxt;
+      bar_sync(bar_id, bar_threads);
+    }
+  } else {
+    const double* st = lv.stencil + 7 * m;
+    const double s1 = st[1], s2 = st[2], s3 = st[3], s4 = st[4], s5 = st[5], s6 = st[6];
+    const double inv_c = lv.inv_c[m];
+    const int j = 32 * (gw - 2) + lane + 1;
+    const bool row = j <= n - 1;
+    const int rowk = row ? dlat(n, 0, j) : 0;
+    const int dn = n + 1 - j, dnw = n - j, ds = n + 2 - j;
+    bar_sync(bar_id, bar_threads);
+    for (int t = 0; t <= 2 * n; ++t) {
       const int i = t - 2 * j;
-      if (j > n || i < 0 || i > n - j) continue;
-      const int k = rowk[r] + i;
-      const double B = bs[k];
-      double res;
-      if (j >= 1 && i >= 1 && i + j <= n - 1) {
-        const double E = us[k + 1], W = us[k - 1], N = us[k + n + 1 - j], S = us[k - (n + 2 - j)];
-        const double NW = us[k + n - j], SE = us[k - (n + 1 - j)];
+      if (row && i >= 1 && i <= n - j - 1) {
+        const int k = rowk + i;
+        const double B = bs[k];
+        const double E = us[k + 1], W = us[k - 1], N = us[k + dn], S = us[k - ds];
+        const double NW = us[k + dnw], SE = us[k - dn];
         double acc = s1 * E + s2 * W;
         acc = acc + s3 * N;
         acc = acc + s4 * S;
         acc = acc + s5 * NW;
         acc = acc + s6 * SE;
-        res = (B - acc) * inv_c;
-      } else {
-        res = relax_blob(bv, bpos_dev(n, i, j), B, us, gh, copies);
+        us[k] = (B - acc) * inv_c;
       }
-      us[k] = res;
+#ifdef KB_GS_TRACE
+      if (blockIdx.x == 0 && gw == 2 && lane == 0 && bar_id == 1) g_gs_trace[3][t] = clock64();
+#endif
+      bar_sync(bar_id, bar_threads);
     }
-    __syncwarp();
   }
 }
 
-// Mode "level": the whole level (u and b of every macro) lives in the shared
-// memory of one CTA; warps take the macros of one DAG level at a time and a
-// __syncthreads separates DAG levels.  For small lattices.
-template <int R>
+// warps per macro group: boundary warp, program warp, one interior warp per 32 rows
+__host__ __device__ __forceinline__ int gs_group_warps(int n) { return 2 + (n - 1 + 31) / 32; }
+constexpr int kMaxLevelGroups = 8;
+constexpr int kRingBytes = kRingSteps * kStepBytes;
+
+// per-group shared scratch: ring | extra records | ghosts (8-byte words)
+__host__ __device__ __forceinline__ size_t gs_group_words(const DevLevel2D& lv) {
+  const size_t w = kRingBytes / 8 + static_cast<size_t>(lv.max_extra) * kProgRecWords + lv.max_ghosts + 1;
+  return (w + 1) & ~static_cast<size_t>(1);  // keeps every group's ring 16-byte aligned
+}
+
+// Mode "level": the whole level (u and b of every macro) in one CTA's shared
+// memory.  Groups of W warps take the macros of one DAG level at a time
+// and a __syncthreads separates DAG levels.
 __global__ void __launch_bounds__(512, 1) k_gs_level(DevHier2D hd, DevLevel2D lv, double* u,
-                                                       const double* __restrict__ b, int sweeps) {
-  extern __shared__ double smem[];
-  const int S = lv.S, M = lv.M;
-  const int total = M * S;
+                                                      const double* __restrict__ b, int sweeps) {
+  extern __shared__ __align__(16) double smem[];
+  const int S = lv.S, M = lv.M, n = lv.n, D = hd.dag_depth;
+  const int W = gs_group_warps(n);
+  const int G = blockDim.x / (32 * W);
+  const size_t total = static_cast<size_t>(M) * S;
+  const size_t gwords = gs_group_words(lv);
   double* lu = smem;
-  double* lb = smem + total;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-  const int per_warp = lv.max_ghosts + lv.blob_max_words;
-  double* gh = lb + total + static_cast<size_t>(warp) * per_warp;
-  unsigned long long* bw = reinterpret_cast<unsigned long long*>(gh + lv.max_ghosts);
-  for (int k = threadIdx.x; k < total; k += blockDim.x) {
+  double* lb = lu + total;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = warp / W, gw = warp - g * W, gt = gw * 32 + lane;
+  // 16-byte aligned group scratch
+  unsigned char* gbase = reinterpret_cast<unsigned char*>(lb + total);  // 2 * total doubles: 16-byte aligned
+  unsigned char* ring = gbase + static_cast<size_t>(g) * gwords * 8;
+  unsigned long long* xs = reinterpret_cast<unsigned long long*>(ring + kRingBytes);
+  double* gh = reinterpret_cast<double*>(xs + static_cast<size_t>(lv.max_extra) * kProgRecWords);
+
+  for (size_t k = threadIdx.x; k < total; k += blockDim.x) {
     lu[k] = __ldcg(u + k);
     lb[k] = __ldg(b + k);
   }
   __syncthreads();
+  const int gthreads = 32 * W;
   for (int s = 0; s < sweeps; ++s) {
-    for (int d = 0; d < hd.dag_depth; ++d) {
-      for (int q = hd.dag_ptr[d] + warp; q < hd.dag_ptr[d + 1]; q += nwarps) {
-        const int m = hd.dag_list[q];
-        const int gbeg = lv.ghost_ptr[m], gcnt = lv.ghost_ptr[m + 1] - gbeg;
-        for (int g = lane; g < gcnt; g += 32) gh[g] = lu[lv.ghost_off[gbeg + g]];
-        const BlobView bv = stage_blob(lv, m, bw, lane);
-        __syncwarp();
-        warp_sweep<R>(lv, m, lu + static_cast<size_t>(m) * S, lb + static_cast<size_t>(m) * S, gh, bv, lu, lane);
+    for (int d = 0; d < D; ++d) {
+      const int q0 = hd.dag_ptr[d], q1 = hd.dag_ptr[d + 1];
+      if (g < G) {
+        for (int q = q0 + g; q < q1; q += G) {
+          const int m = hd.dag_list[q];
+          const int gbeg = lv.ghost_ptr[m], gcnt = lv.ghost_ptr[m + 1] - gbeg;
+          for (int x = gt; x < gcnt; x += gthreads) gh[x] = lu[lv.ghost_off[gbeg + x]];
+          const int xb = lv.xtra_ptr[m], xc = lv.xtra_ptr[m + 1] - xb;
+          for (int x = gt; x < xc; x += gthreads) xs[x] = lv.prog_extra[xb + x];
+          bar_sync(1 + g, gthreads);
+          group_sweep(lv, m, lu + static_cast<size_t>(m) * S, lb + static_cast<size_t>(m) * S, gh, xs, ring, lu, gw,
+                      lane, 1 + g, gthreads);
+          bar_sync(1 + g, gthreads);
+        }
       }
       __syncthreads();
     }
   }
-  for (int k = threadIdx.x; k < total; k += blockDim.x) u[k] = lu[k];
+  for (size_t k = threadIdx.x; k < total; k += blockDim.x) u[k] = lu[k];
 }
 
-// Mode "macro": one single-warp CTA per macro sweep with the macro's u, b and
-// ghosts in shared memory; macro m's sweep s starts once every vertex-sharing
-// macro m' < m finished sweep s and every m'' > m finished sweep s-1 (A.3).
-template <int R>
-__global__ void __launch_bounds__(32, 1) k_gs_macro(DevHier2D hd, DevLevel2D lv, double* u,
-                                                 const double* __restrict__ b, int sweeps, int* done) {
-  extern __shared__ double smem[];
-  const int S = lv.S, M = lv.M;
-  double* us = smem;
-  double* bs = smem + S;
-  double* gh = bs + S;
-  unsigned long long* bw = reinterpret_cast<unsigned long long*>(gh + lv.max_ghosts);
-  const int lane = threadIdx.x;
-  BlobView bv{};
+// Mode "macro": one CTA (a group of W warps) per macro sweep with the macro's
+// u, b, ghosts and step-program ring in shared memory; macro m's sweep s
+// starts once every vertex-sharing macro m' < m finished sweep s and every
+// m'' > m finished sweep s-1.
+__global__ void __launch_bounds__(192, 1) k_gs_macro(DevHier2D hd, DevLevel2D lv, double* u,
+                                                     const double* __restrict__ b, int sweeps, int* done) {
+  extern __shared__ __align__(16) double smem[];
+  const int S = lv.S, M = lv.M, n = lv.n;
+  unsigned char* ring = reinterpret_cast<unsigned char*>(smem);
+  unsigned long long* xs = reinterpret_cast<unsigned long long*>(ring + kRingBytes);
+  double* gh = reinterpret_cast<double*>(xs + static_cast<size_t>(lv.max_extra) * kProgRecWords);
+  double* us = gh + lv.max_ghosts + 1;
+  double* bs = us + S;
+  const int tid = threadIdx.x, gw = tid >> 5, lane = tid & 31;
   const int nitems = sweeps * M;
   int cur = -1;
   for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
     const int s = item / M, m = item - s * M;
-    if (lane == 0) {
+    if (tid == 0) {
       for (int q = hd.nb_lo_ptr[m]; q < hd.nb_lo_ptr[m + 1]; ++q)
         while (ld_acquire(done + hd.nb_lo[q]) < s + 1) {}
       for (int q = hd.nb_hi_ptr[m]; q < hd.nb_hi_ptr[m + 1]; ++q)
         while (ld_acquire(done + hd.nb_hi[q]) < s) {}
     }
-    __syncwarp();
+    __syncthreads();
     double* um = u + static_cast<size_t>(m) * S;
     if (m != cur) {
-      bv = stage_blob(lv, m, bw, lane);
       const double* bm = b + static_cast<size_t>(m) * S;
-      for (int k = lane; k < S; k += 32) {
+#pragma unroll 4
+      for (int k = tid; k < S; k += blockDim.x) {
         us[k] = __ldcg(um + k);
         bs[k] = __ldg(bm + k);
       }
+      const int xb = lv.xtra_ptr[m], xc = lv.xtra_ptr[m + 1] - xb;
+      for (int x = tid; x < xc; x += blockDim.x) xs[x] = lv.prog_extra[xb + x];
     } else {
       // only the interface copies of this macro can have changed since its last sweep
-      const int n = lv.n;
-      for (int p = lane; p < 3 * n; p += 32) {
-        const int k = p <= n ? p : (p < 2 * n + 1 ? dlat(n, 0, p - n) : dlat(n, 3 * n - p, p - 2 * n));
+      for (int p = tid; p < 3 * n; p += blockDim.x) {
+        const int k = p <= n ? p : (p <= 2 * n ? dlat(n, 0, p - n) : dlat(n, 3 * n - p, p - 2 * n));
         us[k] = __ldcg(um + k);
       }
     }
     const int gbeg = lv.ghost_ptr[m], gcnt = lv.ghost_ptr[m + 1] - gbeg;
-    for (int g = lane; g < gcnt; g += 32) gh[g] = __ldcg(u + lv.ghost_off[gbeg + g]);
-    __syncwarp();
-    warp_sweep<R>(lv, m, us, bs, gh, bv, u, lane);
-    for (int k = lane; k < S; k += 32) um[k] = us[k];
-    __syncwarp();
-    if (lane == 0) {
+    for (int x = tid; x < gcnt; x += blockDim.x) gh[x] = __ldcg(u + lv.ghost_off[gbeg + x]);
+    __syncthreads();
+    group_sweep(lv, m, us, bs, gh, xs, ring, u, gw, lane, 1, blockDim.x);
+#pragma unroll 4
+    for (int k = tid; k < S; k += blockDim.x) um[k] = us[k];
+    __syncthreads();
+    if (tid == 0) {
       __threadfence();
       st_release(done + m, s + 1);
     }
@@ -930,37 +1113,38 @@ int device_attr(cudaDeviceAttr a) {
 
 template <typename K>
 void set_smem(K kernel, size_t smem) {
-  if (smem > 48 * 1024)
-    KB_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  // always: static + dynamic shared memory above 48 KB needs the opt-in
+  KB_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
 }
 
-template <int R>
-void launch_gs_smem(const DevHier2D& hd, const DevLevel2D& lv, double* u, const double* b, int sweeps, int* done,
-                    cudaStream_t st, size_t level_smem, int level_warps, size_t macro_smem, int num_sms) {
-  if (level_smem) {
-    set_smem(k_gs_level<R>, level_smem);
-    k_gs_level<R><<<1, 32 * level_warps, level_smem, st>>>(hd, lv, u, b, sweeps);
-    check_launch("k_gs_level");
-    return;
-  }
-  set_smem(k_gs_macro<R>, macro_smem);
+void launch_gs_level(const DevHier2D& hd, const DevLevel2D& lv, double* u, const double* b, int sweeps,
+                     cudaStream_t st, size_t smem, int groups) {
+  set_smem(k_gs_level, smem);
+  k_gs_level<<<1, 32 * gs_group_warps(lv.n) * groups, smem, st>>>(hd, lv, u, b, sweeps);
+  check_launch("k_gs_level");
+}
+
+void launch_gs_macro(const DevHier2D& hd, const DevLevel2D& lv, double* u, const double* b, int sweeps, int* done,
+                     cudaStream_t st, size_t smem, int num_sms) {
+  const int threads = 32 * gs_group_warps(lv.n);
+  set_smem(k_gs_macro, smem);
   int occ = 0;
-  KB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gs_macro<R>, 32, macro_smem));
+  KB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gs_macro, threads, smem));
   if (occ < 1) fail(KB_CUDA, "k_gs_macro cannot be resident");
   int grid = lv.M;
   if (grid > occ * num_sms) grid = occ * num_sms;
   KB_CUDA_CHECK(cudaMemsetAsync(done, 0, sizeof(int) * lv.M, st));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(32);
-  cfg.dynamicSmemBytes = macro_smem;
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  KB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_gs_macro<R>, hd, lv, u, b, sweeps, done));
+  KB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_gs_macro, hd, lv, u, b, sweeps, done));
 }
 }  // namespace
 
@@ -975,20 +1159,21 @@ void launch_gs(const DevHier2D& hd, const DevLevel2D& lv, double* u, const doubl
     num_sms = device_attr(cudaDevAttrMultiProcessorCount);
     smem_max = device_attr(cudaDevAttrMaxSharedMemoryPerBlockOptin);
   }
-  const int R = (lv.n + 32) / 32;
   const size_t S = static_cast<size_t>(lv.S), M = static_cast<size_t>(lv.M);
-  const int warps = std::max(1, std::min(16, hd.dag_width));
-  size_t level_smem =
-      (2 * M * S + static_cast<size_t>(warps) * (lv.max_ghosts + lv.blob_max_words)) * sizeof(double);
-  const size_t macro_smem = (2 * S + lv.max_ghosts + lv.blob_max_words) * sizeof(double);
-  if (level_smem > static_cast<size_t>(smem_max)) level_smem = 0;
-  if (R <= 5 && (level_smem || macro_smem <= static_cast<size_t>(smem_max))) {
-    switch (R) {
-      case 1: launch_gs_smem<1>(hd, lv, u, b, sweeps, done, st, level_smem, warps, macro_smem, num_sms); return;
-      case 2: launch_gs_smem<2>(hd, lv, u, b, sweeps, done, st, level_smem, warps, macro_smem, num_sms); return;
-      case 3: launch_gs_smem<3>(hd, lv, u, b, sweeps, done, st, level_smem, warps, macro_smem, num_sms); return;
-      case 4: launch_gs_smem<4>(hd, lv, u, b, sweeps, done, st, level_smem, warps, macro_smem, num_sms); return;
-      default: launch_gs_smem<5>(hd, lv, u, b, sweeps, done, st, level_smem, warps, macro_smem, num_sms); return;
+  const int W = gs_group_warps(lv.n);
+  if (W <= 6) {
+    // groups per CTA: named barriers 1..kMaxLevelGroups, at most 512 threads
+    const int groups = std::max(1, std::min(std::min(kMaxLevelGroups, 16 / W), hd.dag_width));
+    const size_t gwords = gs_group_words(lv);
+    const size_t level_smem = (2 * M * S + 1) * sizeof(double) + static_cast<size_t>(groups) * gwords * 8;
+    if (level_smem <= static_cast<size_t>(smem_max)) {
+      launch_gs_level(hd, lv, u, b, sweeps, st, level_smem, groups);
+      return;
+    }
+    const size_t macro_smem = gwords * 8 + 2 * S * sizeof(double);
+    if (macro_smem <= static_cast<size_t>(smem_max)) {
+      launch_gs_macro(hd, lv, u, b, sweeps, done, st, macro_smem, num_sms);
+      return;
     }
   }
   const int threads = gs_block_threads(lv.n);
@@ -1033,6 +1218,12 @@ void launch_sync(const DevLevel2D& lv, double* f, int additive, cudaStream_t st)
   k_sync<<<grid_for(lv.num_groups), kThreads, 0, st>>>(lv, f, additive, lv.num_groups);
   check_launch("k_sync");
 }
+
+#ifdef KB_GS_TRACE
+extern "C" int klref_debug_gs_trace(long long* host, int count) {
+  return cudaMemcpyFromSymbol(host, g_gs_trace, sizeof(long long) * count) == cudaSuccess ? 0 : 1;
+}
+#endif
 
 void launch_axpy(double* y, const double* x, double alpha, std::int64_t count, cudaStream_t st) {
   k_axpy<<<grid_for(count), kThreads, 0, st>>>(y, x, alpha, count);

@@ -80,7 +80,7 @@ std::unique_ptr<DeviceHierarchy2D> DeviceHierarchy2D::create(const Mesh2D& mesh,
              vbytes(mem_ij[l]) + vbytes(lv.mem_slot) + vbytes(lv.kstiff) + vbytes(lv.kmass) +
              vbytes(lv.stencil) + vbytes(lv.inv_c) + vbytes(lv.bnode) + vbytes(lv.rec) + vbytes(lv.wr) +
              vbytes(lv.ghost_ptr) + vbytes(lv.ghost_off) + vbytes(lv.dot_order) + vbytes(geo[l]) +
-             vbytes(wq[l]) + vbytes(lv.blob) + vbytes(lv.blob_desc);
+             vbytes(wq[l]) + vbytes(lv.prog) + vbytes(lv.prog_ptr) + vbytes(lv.prog_extra) + vbytes(lv.xtra_ptr);
   }
   d->arena.reserve(bytes + 4096);
   d->dh.M = M;
@@ -119,9 +119,11 @@ std::unique_ptr<DeviceHierarchy2D> DeviceHierarchy2D::create(const Mesh2D& mesh,
     dl.num_groups = static_cast<int>(lv.grp_ptr.size()) - 1;
     dl.dot_order = d->arena.upload(lv.dot_order);
     dl.dot_count = static_cast<int>(lv.dot_order.size());
-    dl.blob = reinterpret_cast<const unsigned long long*>(d->arena.upload(lv.blob));
-    dl.blob_desc = d->arena.upload(lv.blob_desc);
-    dl.blob_max_words = lv.blob_max_words;
+    dl.prog = reinterpret_cast<const unsigned long long*>(d->arena.upload(lv.prog));
+    dl.prog_ptr = d->arena.upload(lv.prog_ptr);
+    dl.prog_extra = reinterpret_cast<const unsigned long long*>(d->arena.upload(lv.prog_extra));
+    dl.xtra_ptr = d->arena.upload(lv.xtra_ptr);
+    dl.max_extra = lv.max_extra;
     dl.geo = d->arena.upload(geo[l]);
     dl.wq = d->arena.upload(wq[l]);
     d->lev.push_back(dl);

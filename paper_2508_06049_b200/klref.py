@@ -19,7 +19,7 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libklref_b200.so")
+LIB_PATH = os.environ.get("KLREF_LIB") or os.path.join(_HERE, "libklref_b200.so")
 
 
 # ---------------------------------------------------------------- errors
