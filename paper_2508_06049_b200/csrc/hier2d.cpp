@@ -71,25 +71,37 @@ std::uint64_t dbits(double d) {
   return w;
 }
 
-// one compact member record: existing cells' coefficient pairs and reads
-void put_rec(std::uint64_t* w, const MemberRec& rec, const Level2D& lvl) {
-  const double* ku = &lvl.kstiff[18 * static_cast<std::size_t>(rec.slot)];
-  static const int ci[12] = {1, 2, 3, 5, 6, 7, 10, 11, 12, 14, 15, 16};
+// One pre-decoded lane record (layout in hier2d.hpp, kProgLaneWords): the
+// compact partial_row of member `rec` (may be null: no record) of node k.
+void put_lane(std::uint64_t* w, const MemberRec* rec, const Level2D& lvl, int k, int flags, int wr0, int wr1,
+              int wb, int wc, int xb, double diag, double inv) {
   double c[6] = {0, 0, 0, 0, 0, 0};
-  std::int16_t loc[6] = {0, 0, 0, 0, 0, 0};
+  int loc[6] = {0, 0, 0, 0, 0, 0};
   int nc = 0;
-  for (int cell = 0; cell < 6; ++cell) {
-    if (!((rec.mask >> cell) & 1)) continue;
-    if (nc == 3) fail(KB_INTERNAL, "boundary node with more than three cells in one macro");
-    for (int q = 0; q < 2; ++q) {
-      c[2 * nc + q] = ku[ci[2 * cell + q]];
-      loc[2 * nc + q] = rec.loc[2 * cell + q];
+  if (rec) {
+    const double* ku = &lvl.kstiff[18 * static_cast<std::size_t>(rec->slot)];
+    static const int ci[12] = {1, 2, 3, 5, 6, 7, 10, 11, 12, 14, 15, 16};
+    for (int cell = 0; cell < 6; ++cell) {
+      if (!((rec->mask >> cell) & 1)) continue;
+      if (nc == 3) fail(KB_INTERNAL, "boundary node with more than three cells in one macro");
+      for (int q = 0; q < 2; ++q) {
+        c[2 * nc + q] = ku[ci[2 * cell + q]];
+        loc[2 * nc + q] = rec->loc[2 * cell + q];
+      }
+      ++nc;
     }
-    ++nc;
   }
   for (int q = 0; q < 6; ++q) w[q] = dbits(c[q]);
-  w[6] = pack16(loc[0], loc[1], loc[2], loc[3]);
-  w[7] = pack16(loc[4], loc[5], static_cast<std::int16_t>(nc), 0);
+  w[6] = dbits(diag);
+  w[7] = dbits(inv);
+  w[8] = pack32(loc[0], loc[1]);
+  w[9] = pack32(loc[2], loc[3]);
+  w[10] = pack32(loc[4], loc[5]);
+  w[11] = pack32(k, flags);
+  w[12] = pack32(wr0, wr1);
+  w[13] = pack32(wb, wc);
+  w[14] = pack32(xb, nc);
+  w[15] = 0;
 }
 
 // Step programs (layout in hier2d.hpp, Level2D::prog).
@@ -105,45 +117,52 @@ void build_programs(Level2D& lvl, int M) {
     lvl.prog_ptr[m] = static_cast<long long>(per_macro * m);
     int nextra = 0;
     for (int t = 0; t <= 2 * n; ++t) {
+      int ti[3], tj[3];
+      bool big = false;
+      for (int type = 0; type < 3; ++type) {
+        ti[type] = tj[type] = -1;
+        if (type == 0 && t <= n) {
+          ti[type] = t;
+          tj[type] = 0;
+        } else if (type == 1 && !(t & 1) && t >= 2) {
+          ti[type] = 0;
+          tj[type] = t / 2;
+        } else if (type == 2 && t > n && t < 2 * n) {
+          tj[type] = t - n;
+          ti[type] = n - tj[type];
+        }
+        if (ti[type] >= 0) {
+          const BNode& bn = lvl.bnode[static_cast<std::size_t>(m) * 3 * n + bpos(n, ti[type], tj[type])];
+          big = big || (!bn.domain && bn.rec_count > 2);
+        }
+      }
       for (int type = 0; type < 3; ++type) {
         std::uint64_t* w = &lvl.prog[per_macro * m + static_cast<std::size_t>(t) * kProgStepWords +
-                                     static_cast<std::size_t>(type) * kProgNodeWords];
-        int i = -1, j = -1;
-        if (type == 0 && t <= n) {
-          i = t;
-          j = 0;
-        } else if (type == 1 && !(t & 1) && t >= 2) {
-          i = 0;
-          j = t / 2;
-        } else if (type == 2 && t > n && t < 2 * n) {
-          j = t - n;
-          i = n - j;
-        }
+                                     static_cast<std::size_t>(2 * type) * kProgLaneWords];
+        const int i = ti[type], j = tj[type];
         if (i < 0) {
-          w[0] = pack32(-1, 0);
+          for (int mem = 0; mem < 2; ++mem)
+            put_lane(w + mem * kProgLaneWords, nullptr, lvl, -1, big ? 1 << 16 : 0, 0, 0, 0, 0, 0, 1.0, 1.0);
           continue;
         }
         const BNode& bn = lvl.bnode[static_cast<std::size_t>(m) * 3 * n + bpos(n, i, j)];
         const int k = lattice_index(n, i, j);
         const int rc = bn.domain ? 0 : bn.rec_count;
-        // header: k | flags (domain, member count) ; wr0 | wr1 ; wr_begin | wr_count ; extra index | 0 ; diag ; 1/diag
-        w[0] = pack32(k, (bn.domain ? 1 : 0) | (rc << 8));
-        w[1] = pack32(bn.wr_count > 0 ? lvl.wr[bn.wr_begin] : 0, bn.wr_count > 1 ? lvl.wr[bn.wr_begin + 1] : 0);
-        w[2] = pack32(bn.wr_begin, bn.wr_count);
-        w[3] = pack32(nextra, 0);
-        w[4] = dbits(bn.diag);
-        w[5] = dbits(bn.diag != 0.0 ? 1.0 / bn.diag : 0.0);
-        for (int r = 0; r < rc; ++r) {
-          const MemberRec& rec = lvl.rec[bn.rec_begin + r];
-          if (r < 2) {
-            put_rec(w + 6 + r * kProgRecWords, rec, lvl);
-          } else {
-            std::uint64_t x[kProgRecWords];
-            put_rec(x, rec, lvl);
-            lvl.prog_extra.insert(lvl.prog_extra.end(), x, x + kProgRecWords);
-            ++nextra;
-          }
+        // flags: bit 0 domain boundary, bits 8..15 member count, bit 16 a vertex group of > 2 members this step
+        const int flags = (bn.domain ? 1 : 0) | (rc << 8) | (big ? 1 << 16 : 0);
+        const int wr0 = bn.wr_count > 0 ? lvl.wr[bn.wr_begin] : 0;
+        const int wr1 = bn.wr_count > 1 ? lvl.wr[bn.wr_begin + 1] : 0;
+        const double inv = bn.diag != 0.0 ? 1.0 / bn.diag : 0.0;
+        for (int mem = 0; mem < 2; ++mem)
+          put_lane(w + mem * kProgLaneWords, mem < rc ? &lvl.rec[bn.rec_begin + mem] : nullptr, lvl, k, flags, wr0,
+                   wr1, bn.wr_begin, bn.wr_count, nextra, bn.diag, inv);
+        for (int r = 2; r < rc; ++r) {
+          std::uint64_t x[kProgLaneWords];
+          put_lane(x, &lvl.rec[bn.rec_begin + r], lvl, k, flags, wr0, wr1, bn.wr_begin, bn.wr_count, nextra, bn.diag,
+                   inv);
+          lvl.prog_extra.insert(lvl.prog_extra.end(), x, x + kProgLaneWords);
         }
+        nextra += std::max(0, rc - 2);
       }
     }
     lvl.xtra_ptr[m + 1] = static_cast<int>(lvl.prog_extra.size());

@@ -64,9 +64,9 @@ struct BNode {
   double diag;                      // sum over members of the partial diagonals
 };
 
-constexpr int kProgRecWords = 8;                          // 6 coefficients, 6 reads, cell count
-constexpr int kProgNodeWords = 6 + 2 * kProgRecWords;     // header + two member records
-constexpr int kProgStepWords = 3 * kProgNodeWords;        // three boundary-node types per step
+// lane record: c[6] diag inv (8 doubles) | loc[6] k flags wr0 wr1 wb wc xb nc (16 int32)
+constexpr int kProgLaneWords = 16;                        // 128 bytes
+constexpr int kProgStepWords = 6 * kProgLaneWords;        // 3 node types x 2 members
 
 struct Level2D {
   int n = 1, S = 3;
@@ -89,14 +89,13 @@ struct Level2D {
   std::vector<int> ghost_ptr, ghost_off;   // per macro ghost lists (global offsets)
   int max_ghosts = 0;
   // Step programs of the shared-memory smoother (kernels2d.cu, k_gs_*): for
-  // every macro, wavefront step t = 0..2n and boundary-node type (row 0, left
-  // edge, hypotenuse) one ProgNode of kProgNodeWords 8-byte words -- the
-  // node's lattice index, flags, copy targets, diag and RN(1/diag), and the
-  // compact partial_row records of its first two group members (existing
-  // cells only, in the order of proj/src/fem.cpp:138-172; reads are lattice
-  // indices of the relaxing macro or ghost slots -1-g).  Members beyond the
-  // second (vertex groups) live in prog_extra; prog_ptr[m] / xtra_ptr[m] are
-  // word offsets of macro m's program / extra records.
+  // every macro and wavefront step t = 0..2n, six pre-decoded lane records
+  // (boundary-node type x group member 0/1) of kProgLaneBytes: the compact
+  // partial_row of that member (existing cells only, in the order of
+  // proj/src/fem.cpp:138-172; reads are lattice indices of the relaxing macro
+  // or ghost slots -1-g) plus the node's lattice index, flags, copy targets,
+  // diag and RN(1/diag).  Members beyond the second (vertex groups) are lane
+  // records in prog_extra; prog_ptr[m] / xtra_ptr[m] are 8-byte-word offsets.
   std::vector<std::uint64_t> prog, prog_extra;
   std::vector<long long> prog_ptr;
   std::vector<int> xtra_ptr;

@@ -584,8 +584,11 @@ __global__ void __launch_bounds__(576, 1) k_gs(DevHier2D hd, DevLevel2D lv, doub
 //   warp 2+ interior warps, one lattice row per lane (7-point form of
 //           proj/src/multigrid.cpp:170-175).
 constexpr int kRingSteps = 8;
-constexpr int kStepBytes = kProgStepWords * 8;  // 528 = 33 x 16 B
-static_assert(kStepBytes % 16 == 0, "step programs are copied in 16-byte chunks");
+// in shared memory the six 128-byte lane records of a step are padded to 144
+// bytes so that the six boundary lanes' vector loads hit distinct banks
+constexpr int kLaneStride = 144;
+constexpr int kStepBytes = 6 * kLaneStride;  // 864 per ring slot
+static_assert(kProgLaneWords * 8 == 128, "lane records are eight 16-byte chunks");
 
 __device__ __forceinline__ void bar_sync(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
@@ -615,53 +618,41 @@ __device__ __forceinline__ unsigned long long ld_s64u(unsigned a) {
   return v;
 }
 
-// One member record of a step program (8 words): c[6], reads[6], cell count.
-struct PRec {
-  double c[6];
-  int loc[6];
-  int nc;
-};
-// Node header + this lane's member record.
+// One pre-decoded lane record of a step program (Level2D::prog, 128 bytes).
 struct PNode {
-  int k, flags, wr0, wr1, wb, wc, xb;
-  double diag, inv, B;
-  PRec r;
+  double c[6], diag, inv;
+  int loc[6], k, flags, wr0, wr1, wb, wc, xb, nc;
 };
 
-__device__ __forceinline__ void load_prec(PRec& r, unsigned a) {
-#pragma unroll
-  for (int q = 0; q < 6; ++q) r.c[q] = __longlong_as_double(static_cast<long long>(ld_s64u(a + 8 * q)));
-  const unsigned long long w6 = ld_s64u(a + 48), w7 = ld_s64u(a + 56);
-#pragma unroll
-  for (int q = 0; q < 4; ++q) r.loc[q] = static_cast<short>((w6 >> (16 * q)) & 0xffff);
-  r.loc[4] = static_cast<short>(w7 & 0xffff);
-  r.loc[5] = static_cast<short>((w7 >> 16) & 0xffff);
-  r.nc = static_cast<int>((w7 >> 32) & 0xffff);
+__device__ __forceinline__ void ld_s_v2f64(unsigned a, double& x, double& y) {
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(a) : "memory");
+}
+__device__ __forceinline__ void ld_s_v4s32(unsigned a, int& x, int& y, int& z, int& w) {
+  asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(x), "=r"(y), "=r"(z), "=r"(w) : "r"(a) : "memory");
 }
 
-// lane (type, mem): node header of its type and record `mem` (mem < 2 from the
-// ring slot, mem >= 2 from the staged extra records)
+__device__ __forceinline__ void load_lane(PNode& p, unsigned a) {
+  ld_s_v2f64(a, p.c[0], p.c[1]);
+  ld_s_v2f64(a + 16, p.c[2], p.c[3]);
+  ld_s_v2f64(a + 32, p.c[4], p.c[5]);
+  ld_s_v2f64(a + 48, p.diag, p.inv);
+  ld_s_v4s32(a + 64, p.loc[0], p.loc[1], p.loc[2], p.loc[3]);
+  ld_s_v4s32(a + 80, p.loc[4], p.loc[5], p.k, p.flags);
+  ld_s_v4s32(a + 96, p.wr0, p.wr1, p.wb, p.wc);
+  int pad0, pad1;
+  ld_s_v4s32(a + 112, p.xb, p.nc, pad0, pad1);
+}
+
+// lane (type, mem): member `mem` of the step's node of this type.  Members 0/1
+// come from the ring slot; members >= 2 (vertex groups, flag bit 16 set on
+// every record of such a step) from the staged extra records.
 __device__ __forceinline__ void load_pnode(PNode& p, unsigned slot, unsigned xs, int type, int mem) {
-  const unsigned h = slot + 8u * kProgNodeWords * static_cast<unsigned>(type);
-  const unsigned long long w0 = ld_s64u(h), w1 = ld_s64u(h + 8), w2 = ld_s64u(h + 16), w3 = ld_s64u(h + 24);
-  p.k = static_cast<int>(w0 & 0xffffffffull);
-  p.flags = static_cast<int>(w0 >> 32);
-  p.wr0 = static_cast<int>(w1 & 0xffffffffull);
-  p.wr1 = static_cast<int>(w1 >> 32);
-  p.wb = static_cast<int>(w2 & 0xffffffffull);
-  p.wc = static_cast<int>(w2 >> 32);
-  p.xb = static_cast<int>(w3 & 0xffffffffull);
-  p.diag = __longlong_as_double(static_cast<long long>(ld_s64u(h + 32)));
-  p.inv = __longlong_as_double(static_cast<long long>(ld_s64u(h + 40)));
-  const int rc = (p.k >= 0) ? (p.flags >> 8) : 0;
-  const unsigned ra = mem < 2 ? h + 48u + 64u * static_cast<unsigned>(mem)
-                              : xs + 64u * static_cast<unsigned>(mem - 2 < rc - 2 ? p.xb + mem - 2 : 0);
-  load_prec(p.r, ra);
-  if (mem >= rc) {  // no record for this lane: reads stay in bounds, no cells
-#pragma unroll
-    for (int q = 0; q < 6; ++q) p.r.loc[q] = 0;
-    p.r.nc = 0;
+  load_lane(p, slot + static_cast<unsigned>(kLaneStride) * static_cast<unsigned>(2 * type + (mem < 2 ? mem : 0)));
+  if (p.flags & (1 << 16)) {
+    const int rc = p.k >= 0 ? ((p.flags >> 8) & 0xff) : 0;
+    if (mem >= 2 && mem < rc) load_lane(p, xs + 128u * static_cast<unsigned>(p.xb + mem - 2));
   }
+  if (mem >= 2 && !(p.flags & (1 << 16))) p.nc = 0;
 }
 
 // Relax the boundary nodes of one step (relax_boundary_node,
@@ -672,31 +663,24 @@ __device__ __forceinline__ void relax_nodes(const PNode& p, unsigned us_s, unsig
                                             double* copies, const int* wr_global, int lane) {
   const int type = lane >> 3, mem = lane & 7;
   const bool lane_ok = type < 3;
-  const int rc = (lane_ok && p.k >= 0) ? (p.flags >> 8) : 0;
+  const int rc = (lane_ok && p.k >= 0) ? ((p.flags >> 8) & 0xff) : 0;
   // reads: lattice values of this macro, or ghost values (constant during the sweep)
   double x[6];
 #pragma unroll
   for (int q = 0; q < 6; ++q) {
-    const int l = p.r.loc[q];
-#ifdef KB_GS_TRACE
-    if (l >= g_dbg_S || -1 - l > g_dbg_G) {
-      KB_CHECK(false, 2, l, 1000 * q + lane);
-      x[q] = 0.0;
-      continue;
-    }
-#endif
+    const int l = p.loc[q];
     x[q] = ld_s64(l >= 0 ? us_s + 8u * l : gh_s + 8u * (-1 - l));
   }
   const double B = ld_s64(bs_s + 8u * (p.k >= 0 ? p.k : 0));
   double o = 0.0;
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
-    const double on = o + (p.r.c[2 * c] * x[2 * c] + p.r.c[2 * c + 1] * x[2 * c + 1]);
-    o = c < p.r.nc ? on : o;
+    const double on = o + (p.c[2 * c] * x[2 * c] + p.c[2 * c + 1] * x[2 * c + 1]);
+    o = c < p.nc ? on : o;
   }
   o = mem < rc ? o : 0.0;
   double off = 0.0;
-  if (__any_sync(0xffffffffu, rc > 2)) {
+  if (p.flags & (1 << 16)) {
     // a vertex group with more than two members: sequential sum over members
     for (int r = 0; r < 8; ++r) {
       const double orr = __shfl_sync(0xffffffffu, o, (lane & ~7) + r);
@@ -708,12 +692,6 @@ __device__ __forceinline__ void relax_nodes(const PNode& p, unsigned us_s, unsig
     if (rc >= 2) off = off + o1;
   }
   if (lane_ok && mem == 0 && p.k >= 0) {
-#ifdef KB_GS_TRACE
-    if (p.k >= g_dbg_S || (p.wc > 0 && (p.wr0 < 0 || p.wr0 >= g_dbg_MS)) || (p.wc > 1 && (p.wr1 < 0 || p.wr1 >= g_dbg_MS))) {
-      KB_CHECK(false, 1, p.k, p.wr0 * 100000ll + p.wr1);
-      return;
-    }
-#endif
     double res = B;
     if (!(p.flags & 1)) {
       // (B - off) / diag correctly rounded: q = x y, r = x - q d exactly (FMA),
@@ -737,7 +715,8 @@ __device__ __forceinline__ void stream_step(const unsigned long long* prog_m, un
   if (t <= 2 * n) {
     const char* src = reinterpret_cast<const char*>(prog_m + static_cast<size_t>(t) * kProgStepWords);
     const unsigned dst = ring_s + static_cast<unsigned>(t % kRingSteps) * kStepBytes;
-    for (int c = lane; c < kStepBytes / 16; c += 32) cp_async16(dst + 16u * c, src + 16 * c);
+    for (int c = lane; c < 48; c += 32)  // 6 records x 8 chunks
+      cp_async16(dst + static_cast<unsigned>(kLaneStride) * (c >> 3) + 16u * (c & 7), src + 16 * c);
   }
   cp_async_commit();
 }
@@ -747,7 +726,7 @@ __device__ __forceinline__ void group_sweep(const DevLevel2D& lv, int m, double*
                                             double* copies, int gw, int lane, int bar_id, int bar_threads) {
   const int n = lv.n;
   const unsigned ring_s = smem_addr(ring);
-#ifdef KB_GS_TRACE
+#ifdef KB_GS_CHECK
   if (threadIdx.x == 0) {
     g_dbg_S = lv.S;
     g_dbg_G = lv.max_ghosts;
@@ -830,7 +809,7 @@ constexpr int kRingBytes = kRingSteps * kStepBytes;
 
 // per-group shared scratch: ring | extra records | ghosts (8-byte words)
 __host__ __device__ __forceinline__ size_t gs_group_words(const DevLevel2D& lv) {
-  const size_t w = kRingBytes / 8 + static_cast<size_t>(lv.max_extra) * kProgRecWords + lv.max_ghosts + 1;
+  const size_t w = kRingBytes / 8 + static_cast<size_t>(lv.max_extra) * kProgLaneWords + lv.max_ghosts + 1;
   return (w + 1) & ~static_cast<size_t>(1);  // keeps every group's ring 16-byte aligned
 }
 
@@ -853,7 +832,7 @@ __global__ void __launch_bounds__(512, 1) k_gs_level(DevHier2D hd, DevLevel2D lv
   unsigned char* gbase = reinterpret_cast<unsigned char*>(lb + total);  // 2 * total doubles: 16-byte aligned
   unsigned char* ring = gbase + static_cast<size_t>(g) * gwords * 8;
   unsigned long long* xs = reinterpret_cast<unsigned long long*>(ring + kRingBytes);
-  double* gh = reinterpret_cast<double*>(xs + static_cast<size_t>(lv.max_extra) * kProgRecWords);
+  double* gh = reinterpret_cast<double*>(xs + static_cast<size_t>(lv.max_extra) * kProgLaneWords);
 
   for (size_t k = threadIdx.x; k < total; k += blockDim.x) {
     lu[k] = __ldcg(u + k);
@@ -893,7 +872,7 @@ __global__ void __launch_bounds__(192, 1) k_gs_macro(DevHier2D hd, DevLevel2D lv
   const int S = lv.S, M = lv.M, n = lv.n;
   unsigned char* ring = reinterpret_cast<unsigned char*>(smem);
   unsigned long long* xs = reinterpret_cast<unsigned long long*>(ring + kRingBytes);
-  double* gh = reinterpret_cast<double*>(xs + static_cast<size_t>(lv.max_extra) * kProgRecWords);
+  double* gh = reinterpret_cast<double*>(xs + static_cast<size_t>(lv.max_extra) * kProgLaneWords);
   double* us = gh + lv.max_ghosts + 1;
   double* bs = us + S;
   const int tid = threadIdx.x, gw = tid >> 5, lane = tid & 31;
