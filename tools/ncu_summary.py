@@ -1,0 +1,67 @@
+"""Summarise ncu outputs into markdown for profiles/ (development tool).
+
+usage: ncu_summary.py launches <launches.csv> <title>
+       ncu_summary.py full <report.ncu-rep> <title>
+"""
+import collections
+import csv
+import io
+import math
+import subprocess
+import sys
+
+
+def launches(path, title):
+    lines = open(path).read().splitlines()
+    start = [i for i, l in enumerate(lines) if l.startswith('"ID"')][0]
+    rows = list(csv.reader(lines[start:]))
+    hdr = rows[0]
+    i_name, i_val = hdr.index("Kernel Name"), hdr.index("Metric Value")
+    agg = collections.defaultdict(lambda: [0, 0.0])
+    for r in rows[1:]:
+        try:
+            v = float(r[i_val].replace(",", ""))
+        except ValueError:
+            continue
+        if not math.isfinite(v):
+            continue
+        nm = r[i_name].split("(")[0].replace("kb::<unnamed>::", "").replace("kb::", "")
+        agg[nm][0] += 1
+        agg[nm][1] += v
+    tot = sum(v[1] for v in agg.values())
+    out = [f"# {title}", "", "ncu `--metrics gpu__time_duration.sum --clock-control none` launch list "
+           "(cold-cache, serialised replay: compare shares, not absolutes).", "",
+           "| kernel | launches | total ms | share |", "|---|---:|---:|---:|"]
+    for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+        out.append(f"| `{k}` | {v[0]} | {v[1] / 1e6:.3f} | {100 * v[1] / tot:.1f}% |")
+    out.append(f"| total | {sum(v[0] for v in agg.values())} | {tot / 1e6:.3f} | 100% |")
+    return "\n".join(out)
+
+
+WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_bytes.sum",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "launch__registers_per_thread",
+        "launch__grid_size", "launch__block_size", "launch__shared_mem_per_block_dynamic",
+        "sm__warps_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
+        "sm__throughput.avg.pct_of_peak_sustained_elapsed", "smsp__average_warp_latency_issue_stalled_barrier",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
+
+
+def full(path, title):
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units = rows[0], rows[1]
+    out = [f"# {title}", "", f"`ncu --set full --clock-control none` capture `{path.split('/')[-1]}`.", ""]
+    for r in rows[2:]:
+        name = r[hdr.index("Kernel Name")]
+        out += [f"## `{name.split('(')[0]}`", "", "| metric | value | unit |", "|---|---:|---|"]
+        for w in WANT:
+            if w in hdr:
+                i = hdr.index(w)
+                out.append(f"| {w} | {r[i]} | {units[i]} |")
+        out.append("")
+    return "\n".join(out)
+
+
+if __name__ == "__main__":
+    mode, path, title = sys.argv[1], sys.argv[2], sys.argv[3]
+    print(launches(path, title) if mode == "launches" else full(path, title))
