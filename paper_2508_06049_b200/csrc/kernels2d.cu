@@ -129,6 +129,76 @@ __global__ void k_apply(DevLevel2D lv, const double* __restrict__ K, const doubl
     apply_node(lv, K, x, y, b, mode, k);
 }
 
+// Level-wide apply / residual, split by node kind in one launch:
+//  * blocks [0, interior_blocks): 256 consecutive lattice indices of one macro
+//    each; lattice-interior nodes evaluate the reference's six-cell gather with
+//    all cells present (no branches, 7 loads, the same operation order as
+//    gather_apply), lattice-boundary nodes are skipped;
+//  * the remaining blocks: one shared-node group per thread -- members'
+//    partial gathers summed in ascending slot (interface_sync Additive),
+//    written to every copy.
+__device__ __forceinline__ void decode_fast(int n, int idx, int& i, int& j) {
+  const float a = 2.0f * n + 3.0f;
+  int jj = static_cast<int>((a - sqrtf(a * a - 8.0f * idx)) * 0.5f);
+  jj = max(0, min(jj, n));
+  while (jj < n && dlat(n, 0, jj + 1) <= idx) ++jj;
+  while (jj > 0 && dlat(n, 0, jj) > idx) --jj;
+  j = jj;
+  i = idx - dlat(n, 0, jj);
+}
+
+__global__ void __launch_bounds__(256) k_apply2(DevLevel2D lv, const double* __restrict__ K,
+                                                const double* __restrict__ x, double* y,
+                                                const double* __restrict__ b, int mode, int chunks_per_macro,
+                                                int interior_blocks) {
+  const int n = lv.n, S = lv.S;
+  if (static_cast<int>(blockIdx.x) < interior_blocks) {
+    const int m = blockIdx.x / chunks_per_macro;
+    const int idx = (blockIdx.x - m * chunks_per_macro) * 256 + threadIdx.x;
+    if (idx >= S) return;
+    int p, q;
+    decode_fast(n, idx, p, q);
+    if (p == 0 || q == 0 || p + q == n) return;
+    const double* ku = K + 18 * m;
+    const double* kd = ku + 9;
+    const double* xm = x + static_cast<size_t>(m) * S;
+    const int k = idx;
+    const double C = xm[k], E = xm[k + 1], W = xm[k - 1];
+    const double N = xm[k + n + 1 - q], NW = xm[k + n - q];
+    const double Sv = xm[k - (n + 2 - q)], SE = xm[k - (n + 1 - q)];
+    // gather_apply order: up(p,q-1) c, down(p-1,q-1) c, down(p,q-1) b,
+    // up(p-1,q) b, up(p,q) a, down(p-1,q) a
+    double acc = 0.0;
+    acc += (__ldg(ku + 6) * Sv + __ldg(ku + 7) * SE) + __ldg(ku + 8) * C;
+    acc += (__ldg(kd + 6) * Sv + __ldg(kd + 7) * W) + __ldg(kd + 8) * C;
+    acc += (__ldg(kd + 3) * SE + __ldg(kd + 4) * C) + __ldg(kd + 5) * E;
+    acc += (__ldg(ku + 3) * W + __ldg(ku + 4) * C) + __ldg(ku + 5) * NW;
+    acc += (__ldg(ku + 0) * C + __ldg(ku + 1) * E) + __ldg(ku + 2) * N;
+    acc += (__ldg(kd + 0) * C + __ldg(kd + 1) * NW) + __ldg(kd + 2) * N;
+    const size_t off = static_cast<size_t>(m) * S + k;
+    if (mode == APPLY_RESIDUAL)
+      y[off] = b[off] - acc;  // interior nodes are never on the domain boundary
+    else
+      y[off] = acc;
+    return;
+  }
+  const int g = (blockIdx.x - interior_blocks) * 256 + threadIdx.x;
+  if (g >= lv.num_groups) return;
+  const int beg = lv.grp_ptr[g], end = lv.grp_ptr[g + 1];
+  double v;
+  if (end - beg == 1) {
+    const int ms = lv.mem_slot[beg], ij = lv.mem_ij[beg];
+    v = gather_apply(x + static_cast<size_t>(ms) * S, n, ij & 0xffff, ij >> 16, K + 18 * ms);
+  } else {
+    v = 0.0;
+    for (int q = beg; q < end; ++q) {
+      const int ms = lv.mem_slot[q], ij = lv.mem_ij[q];
+      v += gather_apply(x + static_cast<size_t>(ms) * S, n, ij & 0xffff, ij >> 16, K + 18 * ms);
+    }
+  }
+  for (int q = beg; q < end; ++q) write_out(mode, v, lv.mem_off[q], y, b, lv.node_flags);
+}
+
 // ---------------------------------------------------------------- restrict
 __device__ __forceinline__ double gather_restrict(const double* __restrict__ f,
                                                   const std::uint8_t* __restrict__ fl, int nf, int I,
@@ -1036,7 +1106,10 @@ void check_launch(const char* what) {
 
 void launch_apply(const DevLevel2D& lv, const double* K, const double* x, double* y, const double* b,
                   int mode, cudaStream_t st) {
-  k_apply<<<grid_for(static_cast<long long>(lv.M) * lv.S), kThreads, 0, st>>>(lv, K, x, y, b, mode);
+  const int chunks = (lv.S + 255) / 256;
+  const int interior_blocks = lv.M * chunks;
+  const int group_blocks = (lv.num_groups + 255) / 256;
+  k_apply2<<<interior_blocks + group_blocks, 256, 0, st>>>(lv, K, x, y, b, mode, chunks, interior_blocks);
   check_launch("k_apply");
 }
 
