@@ -27,6 +27,7 @@ namespace {
 constexpr int kThreads = 256;
 
 #ifdef KB_GS_TRACE
+__device__ int g_lvl_item;
 __device__ long long g_gs_trace[4][1 << 12];  // debug builds only: per-step clocks of block 0
 __device__ int g_dbg_S, g_dbg_G, g_dbg_MS;
 #define KB_CHECK(cond, code, a, b)                                                        \
@@ -690,7 +691,7 @@ __device__ __forceinline__ unsigned long long ld_s64u(unsigned a) {
 
 // One pre-decoded lane record of a step program (Level2D::prog, 128 bytes).
 struct PNode {
-  double c[6], diag, inv;
+  double c[6], diag, inv, B;
   int loc[6], k, flags, wr0, wr1, wb, wc, xb, nc;
 };
 
@@ -716,8 +717,9 @@ __device__ __forceinline__ void load_lane(PNode& p, unsigned a) {
 // lane (type, mem): member `mem` of the step's node of this type.  Members 0/1
 // come from the ring slot; members >= 2 (vertex groups, flag bit 16 set on
 // every record of such a step) from the staged extra records.
-__device__ __forceinline__ void load_pnode(PNode& p, unsigned slot, unsigned xs, int type, int mem) {
+__device__ __forceinline__ void load_pnode(PNode& p, unsigned slot, unsigned xs, unsigned bs_s, int type, int mem) {
   load_lane(p, slot + static_cast<unsigned>(kLaneStride) * static_cast<unsigned>(2 * type + (mem < 2 ? mem : 0)));
+  p.B = ld_s64(bs_s + 8u * (p.k >= 0 ? p.k : 0));  // b is constant during the sweep
   if (p.flags & (1 << 16)) {
     const int rc = p.k >= 0 ? ((p.flags >> 8) & 0xff) : 0;
     if (mem >= 2 && mem < rc) load_lane(p, xs + 128u * static_cast<unsigned>(p.xb + mem - 2));
@@ -741,7 +743,7 @@ __device__ __forceinline__ void relax_nodes(const PNode& p, unsigned us_s, unsig
     const int l = p.loc[q];
     x[q] = ld_s64(l >= 0 ? us_s + 8u * l : gh_s + 8u * (-1 - l));
   }
-  const double B = ld_s64(bs_s + 8u * (p.k >= 0 ? p.k : 0));
+  const double B = p.B;
   double o = 0.0;
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
@@ -779,19 +781,59 @@ __device__ __forceinline__ void relax_nodes(const PNode& p, unsigned us_s, unsig
   }
 }
 
-// Issue the cp.async copies of step program `t` (if it exists) into its ring
-// slot; always commits a group so that group counting stays uniform.
-__device__ __forceinline__ void stream_step(const unsigned long long* prog_m, unsigned ring_s, int n, int t, int lane) {
+// Issue the cp.async copies of step program `t` (if it exists) into its ring slot.
+__device__ __forceinline__ void issue_step(const unsigned long long* prog_m, unsigned ring_s, int n, int t, int lane) {
   if (t <= 2 * n) {
     const char* src = reinterpret_cast<const char*>(prog_m + static_cast<size_t>(t) * kProgStepWords);
     const unsigned dst = ring_s + static_cast<unsigned>(t % kRingSteps) * kStepBytes;
     for (int c = lane; c < 48; c += 32)  // 6 records x 8 chunks
       cp_async16(dst + static_cast<unsigned>(kLaneStride) * (c >> 3) + 16u * (c & 7), src + 16 * c);
   }
+}
+// ... and commit it as one group (group counting stays uniform)
+__device__ __forceinline__ void stream_step(const unsigned long long* prog_m, unsigned ring_s, int n, int t, int lane) {
+  issue_step(prog_m, ring_s, n, t, lane);
   cp_async_commit();
 }
 
-__device__ __forceinline__ void group_sweep(const DevLevel2D& lv, int m, double* us, const double* bs,
+// Static inputs of the group's next macro (level mode): its first step
+// programs, ghost offsets and extra records, streamed while this one sweeps.
+struct NextPrefetch {
+  const unsigned long long* prog_m;  // null: no next macro
+  unsigned ring_s;
+  const int* go_src;
+  int* go_dst;
+  int go_count;
+  const unsigned long long* xs_src;
+  unsigned long long* xs_dst;
+  int xs_words;
+};
+
+__device__ __forceinline__ void issue_next(const NextPrefetch& nx, int n, int t, int lane) {
+  if (!nx.prog_m || t >= kRingSteps - 1) return;
+  if (t == 0) {
+    for (int x = lane; x < nx.go_count; x += 32)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(nx.go_dst + x)), "l"(nx.go_src + x)
+                   : "memory");
+    for (int x = lane; x < nx.xs_words; x += 32)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(nx.xs_dst + x)), "l"(nx.xs_src + x)
+                   : "memory");
+  }
+  issue_step(nx.prog_m, nx.ring_s, n, t, lane);
+}
+
+// Per-macro inputs of one sweep.  `head_ready`: the first kRingSteps - 1 step
+// programs are already in the ring (streamed ahead during the previous sweep).
+struct SweepArgs {
+  int m;
+  const unsigned long long* prog_m;  // this macro's step programs (global)
+  const double* st;                  // 7-point stencil (C, E, W, N, S, NW, SE)
+  double inv_c;
+  bool head_ready;
+  NextPrefetch next;
+};
+
+__device__ __forceinline__ void group_sweep(const DevLevel2D& lv, const SweepArgs& a, double* us, const double* bs,
                                             const double* gh, const unsigned long long* xs, unsigned char* ring,
                                             double* copies, int gw, int lane, int bar_id, int bar_threads) {
   const int n = lv.n;
@@ -804,47 +846,49 @@ __device__ __forceinline__ void group_sweep(const DevLevel2D& lv, int m, double*
   }
 #endif
   if (gw == 1) {
-    const unsigned long long* prog_m = lv.prog + lv.prog_ptr[m];
+    const unsigned long long* prog_m = a.prog_m;
     // lookahead kRingSteps - 1: during step t the slot of step t - 1 is refilled
     // (the boundary warp read it before the barrier that ended step t - 1)
+    if (!a.head_ready) {
 #pragma unroll 1
-    for (int t = 0; t < kRingSteps - 1; ++t) stream_step(prog_m, ring_s, n, t, lane);
+      for (int t = 0; t < kRingSteps - 1; ++t) stream_step(prog_m, ring_s, n, t, lane);
+    }
     cp_async_wait<kRingSteps - 3>();  // steps 0 and 1 landed
     bar_sync(bar_id, bar_threads);
     for (int t = 0; t <= 2 * n; ++t) {
-      stream_step(prog_m, ring_s, n, t + kRingSteps - 1, lane);
+      issue_step(prog_m, ring_s, n, t + kRingSteps - 1, lane);
+      issue_next(a.next, n, t, lane);  // same commit group: counting unchanged
+      cp_async_commit();
       cp_async_wait<kRingSteps - 3>();  // step t + 2 landed
       bar_sync(bar_id, bar_threads);
     }
+    for (int t = 2 * n + 1; t < kRingSteps - 1; ++t) issue_next(a.next, n, t, lane);  // short sweeps
+    cp_async_commit();
     cp_async_wait<0>();
   } else if (gw == 0) {
     const unsigned us_s = smem_addr(us), bs_s = smem_addr(bs), gh_s = smem_addr(gh), xs_s = smem_addr(xs);
     const int type = lane >> 3, mem = lane & 7;
     const int tl = type < 3 ? type : 0;
     bar_sync(bar_id, bar_threads);
-    PNode cur;
-    load_pnode(cur, ring_s, xs_s, tl, mem);
-    for (int t = 0; t <= 2 * n; ++t) {
-#ifdef KB_GS_TRACE
-      if (blockIdx.x == 0 && lane == 0 && bar_id == 1) g_gs_trace[0][t] = clock64();
-#endif
-      PNode nxt;
-      // the slot after the last step holds stale shared memory: never decode it
-      if (t < 2 * n) load_pnode(nxt, ring_s + static_cast<unsigned>((t + 1) % kRingSteps) * kStepBytes, xs_s, tl, mem);
-#ifdef KB_GS_TRACE
-      if (blockIdx.x == 0 && lane == 0 && bar_id == 1) g_gs_trace[1][t] = clock64();
-#endif
-      relax_nodes(cur, us_s, bs_s, gh_s, copies, lv.wr, lane);
-#ifdef KB_GS_TRACE
-      if (blockIdx.x == 0 && lane == 0 && bar_id == 1) g_gs_trace[2][t] = clock64();
-#endif
-      cur = nxt;
+    // two register sets, ping-pong (no copies); the slot after the last step
+    // holds stale shared memory and is never decoded
+    PNode p0, p1;
+    load_pnode(p0, ring_s, xs_s, bs_s, tl, mem);
+    for (int t = 0; t <= 2 * n; t += 2) {
+      if (t + 1 <= 2 * n)
+        load_pnode(p1, ring_s + static_cast<unsigned>((t + 1) % kRingSteps) * kStepBytes, xs_s, bs_s, tl, mem);
+      relax_nodes(p0, us_s, bs_s, gh_s, copies, lv.wr, lane);
+      bar_sync(bar_id, bar_threads);
+      if (t + 1 > 2 * n) break;
+      if (t + 2 <= 2 * n)
+        load_pnode(p0, ring_s + static_cast<unsigned>((t + 2) % kRingSteps) * kStepBytes, xs_s, bs_s, tl, mem);
+      relax_nodes(p1, us_s, bs_s, gh_s, copies, lv.wr, lane);
       bar_sync(bar_id, bar_threads);
     }
   } else {
-    const double* st = lv.stencil + 7 * m;
+    const double* st = a.st;
     const double s1 = st[1], s2 = st[2], s3 = st[3], s4 = st[4], s5 = st[5], s6 = st[6];
-    const double inv_c = lv.inv_c[m];
+    const double inv_c = a.inv_c;
     const int j = 32 * (gw - 2) + lane + 1;
     const bool row = j <= n - 1;
     const int rowk = row ? dlat(n, 0, j) : 0;
@@ -885,7 +929,29 @@ __host__ __device__ __forceinline__ size_t gs_group_words(const DevLevel2D& lv) 
 
 // Mode "level": the whole level (u and b of every macro) in one CTA's shared
 // memory.  Groups of W warps take the macros of one DAG level at a time
-// and a __syncthreads separates DAG levels.
+// and a __syncthreads separates DAG levels.  The small
+// per-level tables are staged once; while a group sweeps one macro, its
+// program warp already streams the next macro's static inputs (ghost offsets,
+// extra records, first step programs) into the group's second buffer set.
+struct LevelTables {  // shared-memory copies of the per-macro tables
+  int *dag_ptr, *dag_list, *ghost_ptr, *xtra_ptr, *prog_off;
+  double *stencil, *inv_c;
+};
+
+__host__ __device__ __forceinline__ size_t gs_level_table_bytes(int M, int D) {
+  // ints: dag_ptr D+1, dag_list M, ghost_ptr M+1, xtra_ptr M+1, prog_off M (padded to 8 bytes) + doubles 8 M
+  const size_t ints = (D + 1) + M + (M + 1) + (M + 1) + M;
+  return ((ints * 4 + 7) & ~static_cast<size_t>(7)) + static_cast<size_t>(8) * M * 8;
+}
+// per-group buffers: 2 rings | 2 extra-record sets | 2 ghost-offset lists | ghost values
+__host__ __device__ __forceinline__ size_t gs_level_group_bytes(const DevLevel2D& lv) {
+  const size_t ring = kRingBytes;
+  const size_t xs = static_cast<size_t>(lv.max_extra) * kProgLaneWords * 8;
+  const size_t go = ((static_cast<size_t>(lv.max_ghosts) * 4 + 15) & ~static_cast<size_t>(15));
+  const size_t gv = static_cast<size_t>(lv.max_ghosts + 1) * 8;
+  return (2 * (ring + xs + go) + gv + 15) & ~static_cast<size_t>(15);
+}
+
 __global__ void __launch_bounds__(512, 1) k_gs_level(DevHier2D hd, DevLevel2D lv, double* u,
                                                       const double* __restrict__ b, int sweeps) {
   extern __shared__ __align__(16) double smem[];
@@ -893,42 +959,109 @@ __global__ void __launch_bounds__(512, 1) k_gs_level(DevHier2D hd, DevLevel2D lv
   const int W = gs_group_warps(n);
   const int G = blockDim.x / (32 * W);
   const size_t total = static_cast<size_t>(M) * S;
-  const size_t gwords = gs_group_words(lv);
   double* lu = smem;
   double* lb = lu + total;
+  unsigned char* tb = reinterpret_cast<unsigned char*>(lb + total);  // 16-byte aligned (2 total doubles)
+  LevelTables T;
+  {
+    int* ip = reinterpret_cast<int*>(tb);
+    T.dag_ptr = ip;
+    T.dag_list = T.dag_ptr + (D + 1);
+    T.ghost_ptr = T.dag_list + M;
+    T.xtra_ptr = T.ghost_ptr + (M + 1);
+    T.prog_off = T.xtra_ptr + (M + 1);
+    const size_t ints = (D + 1) + M + (M + 1) + (M + 1) + M;
+    T.stencil = reinterpret_cast<double*>(tb + ((ints * 4 + 7) & ~static_cast<size_t>(7)));
+    T.inv_c = T.stencil + 7 * M;
+  }
+  unsigned char* gbase = tb + ((gs_level_table_bytes(M, D) + 15) & ~static_cast<size_t>(15));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = warp / W, gw = warp - g * W, gt = gw * 32 + lane;
-  // 16-byte aligned group scratch
-  unsigned char* gbase = reinterpret_cast<unsigned char*>(lb + total);  // 2 * total doubles: 16-byte aligned
-  unsigned char* ring = gbase + static_cast<size_t>(g) * gwords * 8;
-  unsigned long long* xs = reinterpret_cast<unsigned long long*>(ring + kRingBytes);
-  double* gh = reinterpret_cast<double*>(xs + static_cast<size_t>(lv.max_extra) * kProgLaneWords);
+  const size_t gbytes = gs_level_group_bytes(lv);
+  const size_t xs_bytes = static_cast<size_t>(lv.max_extra) * kProgLaneWords * 8;
+  const size_t go_bytes = ((static_cast<size_t>(lv.max_ghosts) * 4 + 15) & ~static_cast<size_t>(15));
+  unsigned char* gb = gbase + static_cast<size_t>(g) * gbytes;
+  // buffer set `c` (0/1): ring, extra records, ghost offsets
+  auto ringb = [&](int c) { return gb + c * kRingBytes; };
+  auto xsb = [&](int c) { return reinterpret_cast<unsigned long long*>(gb + 2 * kRingBytes + c * xs_bytes); };
+  auto gob = [&](int c) { return reinterpret_cast<int*>(gb + 2 * kRingBytes + 2 * xs_bytes + c * go_bytes); };
+  double* gh = reinterpret_cast<double*>(gb + 2 * kRingBytes + 2 * xs_bytes + 2 * go_bytes);
 
   for (size_t k = threadIdx.x; k < total; k += blockDim.x) {
     lu[k] = __ldcg(u + k);
     lb[k] = __ldg(b + k);
   }
+  for (int k = threadIdx.x; k <= D; k += blockDim.x) T.dag_ptr[k] = hd.dag_ptr[k];
+  for (int k = threadIdx.x; k < M; k += blockDim.x) {
+    T.dag_list[k] = hd.dag_list[k];
+    T.prog_off[k] = static_cast<int>(lv.prog_ptr[k]);
+    T.inv_c[k] = lv.inv_c[k];
+  }
+  for (int k = threadIdx.x; k <= M; k += blockDim.x) {
+    T.ghost_ptr[k] = lv.ghost_ptr[k];
+    T.xtra_ptr[k] = lv.xtra_ptr[k];
+  }
+  for (int k = threadIdx.x; k < 7 * M; k += blockDim.x) T.stencil[k] = lv.stencil[k];
   __syncthreads();
+
   const int gthreads = 32 * W;
+  // the group's macros in schedule order: (s, d, q = dag_ptr[d] + g + G i)
+  auto next_item = [&](int& s, int& d, int& q) -> bool {
+    q += G;
+    while (q >= T.dag_ptr[d + 1]) {
+      if (++d == D) {
+        d = 0;
+        if (++s == sweeps) return false;
+      }
+      q = T.dag_ptr[d] + g;
+    }
+    return true;
+  };
+  auto next_args = [&](int m, int buf) {
+    NextPrefetch nx;
+    nx.prog_m = lv.prog + T.prog_off[m];
+    nx.ring_s = smem_addr(ringb(buf));
+    nx.go_src = lv.ghost_off + T.ghost_ptr[m];
+    nx.go_dst = gob(buf);
+    nx.go_count = T.ghost_ptr[m + 1] - T.ghost_ptr[m];
+    nx.xs_src = lv.prog_extra + T.xtra_ptr[m];
+    nx.xs_dst = xsb(buf);
+    nx.xs_words = T.xtra_ptr[m + 1] - T.xtra_ptr[m];
+    return nx;
+  };
+  if (g < G && gw == 1) {
+    int s0 = 0, d0 = 0, q0 = g - G;
+    if (next_item(s0, d0, q0)) {
+      const NextPrefetch nx = next_args(T.dag_list[q0], 0);
+      for (int t = 0; t < kRingSteps - 1; ++t) issue_next(nx, n, t, lane);
+      cp_async_commit();
+    }
+  }
+  int cur = 0;
   for (int s = 0; s < sweeps; ++s) {
     for (int d = 0; d < D; ++d) {
-      const int q0 = hd.dag_ptr[d], q1 = hd.dag_ptr[d + 1];
       if (g < G) {
-        for (int q = q0 + g; q < q1; q += G) {
-          const int m = hd.dag_list[q];
-          const int gbeg = lv.ghost_ptr[m], gcnt = lv.ghost_ptr[m + 1] - gbeg;
-          for (int x = gt; x < gcnt; x += gthreads) gh[x] = lu[lv.ghost_off[gbeg + x]];
-          const int xb = lv.xtra_ptr[m], xc = lv.xtra_ptr[m + 1] - xb;
-          for (int x = gt; x < xc; x += gthreads) xs[x] = lv.prog_extra[xb + x];
+        for (int q = T.dag_ptr[d] + g; q < T.dag_ptr[d + 1]; q += G) {
+          const int m = T.dag_list[q];
+          if (gw == 1) cp_async_wait<0>();  // this macro's inputs landed
           bar_sync(1 + g, gthreads);
-          group_sweep(lv, m, lu + static_cast<size_t>(m) * S, lb + static_cast<size_t>(m) * S, gh, xs, ring, lu, gw,
-                      lane, 1 + g, gthreads);
+          const int gc = T.ghost_ptr[m + 1] - T.ghost_ptr[m];
+          for (int x = gt; x < gc; x += gthreads) gh[x] = lu[gob(cur)[x]];
           bar_sync(1 + g, gthreads);
+          SweepArgs args{m, lv.prog + T.prog_off[m], T.stencil + 7 * m, T.inv_c[m], true, NextPrefetch{}};
+          int ns = s, nd = d, nq = q;
+          if (next_item(ns, nd, nq)) args.next = next_args(T.dag_list[nq], cur ^ 1);
+          group_sweep(lv, args, lu + static_cast<size_t>(m) * S, lb + static_cast<size_t>(m) * S, gh, xsb(cur),
+                      ringb(cur), lu, gw, lane, 1 + g, gthreads);
+          bar_sync(1 + g, gthreads);
+          cur ^= 1;
         }
       }
       __syncthreads();
     }
   }
+  cp_async_wait<0>();
+  __syncthreads();
   for (size_t k = threadIdx.x; k < total; k += blockDim.x) u[k] = lu[k];
 }
 
@@ -977,7 +1110,8 @@ __global__ void __launch_bounds__(192, 1) k_gs_macro(DevHier2D hd, DevLevel2D lv
     const int gbeg = lv.ghost_ptr[m], gcnt = lv.ghost_ptr[m + 1] - gbeg;
     for (int x = tid; x < gcnt; x += blockDim.x) gh[x] = __ldcg(u + lv.ghost_off[gbeg + x]);
     __syncthreads();
-    group_sweep(lv, m, us, bs, gh, xs, ring, u, gw, lane, 1, blockDim.x);
+    const SweepArgs args{m, lv.prog + lv.prog_ptr[m], lv.stencil + 7 * m, lv.inv_c[m], false, NextPrefetch{}};
+    group_sweep(lv, args, us, bs, gh, xs, ring, u, gw, lane, 1, blockDim.x);
 #pragma unroll 4
     for (int k = tid; k < S; k += blockDim.x) um[k] = us[k];
     __syncthreads();
@@ -1217,7 +1351,8 @@ void launch_gs(const DevHier2D& hd, const DevLevel2D& lv, double* u, const doubl
     // groups per CTA: named barriers 1..kMaxLevelGroups, at most 512 threads
     const int groups = std::max(1, std::min(std::min(kMaxLevelGroups, 16 / W), hd.dag_width));
     const size_t gwords = gs_group_words(lv);
-    const size_t level_smem = (2 * M * S + 1) * sizeof(double) + static_cast<size_t>(groups) * gwords * 8;
+    const size_t level_smem = 2 * M * S * sizeof(double) + ((gs_level_table_bytes(lv.M, hd.dag_depth) + 15) & ~15ull) +
+                              static_cast<size_t>(groups) * gs_level_group_bytes(lv);
     if (level_smem <= static_cast<size_t>(smem_max)) {
       launch_gs_level(hd, lv, u, b, sweeps, st, level_smem, groups);
       return;
