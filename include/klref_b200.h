@@ -41,6 +41,10 @@ extern "C" {
 #define KLREF_PROBLEM_ZERO 0
 #define KLREF_PROBLEM_SIN2D 1  /* u = sin(pi x) sin(pi y), f = 2 pi^2 u     (config 1) */
 #define KLREF_PROBLEM_LSHAPE 2 /* make_lshape_spec: f = 0, g = r^2/3 sin(2t/3) (config 2) */
+/* 3-d problems (no reference solver; BASELINE.json configs 3-5) */
+#define KLREF_PROBLEM_SIN3D 3  /* u = prod sin(pi x_i), f = 3 pi^2 u                 (config 3) */
+#define KLREF_PROBLEM_GAUSS3D 4 /* u = exp(-1000 |x - c|^2), c = (1/2, 1/2, 1/2)       (config 4) */
+#define KLREF_PROBLEM_SERIES3D 5 /* f = sum C_abc sin(a pi x) sin(b pi y) sin(c pi z), g = 0 (config 5) */
 
 /* operator kinds (OperatorKind, proj/include/klref/fem.hpp:13) */
 #define KLREF_STIFFNESS 0
@@ -114,7 +118,9 @@ int klref_abi_version(void);
 /* Conforming macro mesh in slot order (MacroMesh::create,
  * proj/src/macro_mesh.cpp:115-204, restricted to what the hot path reads):
  * coords[dim * num_vertices], corners[(dim + 1) * num_elements] (vertex ids);
- * elements are oriented positively as the reference does. */
+ * elements are oriented positively as the reference does.  dim = 2
+ * (triangles) or 3 (tetrahedra; the reference has no 3-d solver, the 3-d
+ * path is the builder's design -- DESIGN.md). */
 int klref_mesh_create(int dim, int num_vertices, const double* coords, int num_elements,
                       const int* corners, klref_mesh* out);
 void klref_mesh_destroy(klref_mesh mesh);
@@ -132,11 +138,13 @@ int klref_hierarchy_fine_element_count(klref_hierarchy h, int level, int64_t* ou
 int klref_hierarchy_lattice_size(klref_hierarchy h, int level, int* out); /* lattice_size(2^l) */
 int klref_hierarchy_dag_depth(klref_hierarchy h, int* out);
 /* Level(l).groups (proj/include/klref/hhg.hpp:19-27): ptr[num_groups + 1],
- * members[4 * num_members] = (slot, idx, i, j).  Pass NULL to query sizes. */
+ * members[4 * num_members] = (slot, idx, i, j) (3-d: (slot, idx, 0, 0)).
+ * Pass NULL to query sizes. */
 int klref_hierarchy_groups(klref_hierarchy h, int level, int* num_groups, int* num_members, int* ptr,
                            int* members);
 /* OperatorP1::matrices/stencil (proj/include/klref/fem.hpp:30-37): mats[18 * M]
- * (up, down per macro), stencil[7 * M] (stiffness only; may be NULL) */
+ * (up, down per macro), stencil[7 * M] (stiffness only; may be NULL).
+ * 3-d: mats[96 * M] (six micro-tet types, 4x4 each), stencil[15 * M]. */
 int klref_hierarchy_element_matrices(klref_hierarchy h, int level, int kind, double* mats, double* stencil);
 
 /* ---- problems --------------------------------------------------------- */
@@ -145,6 +153,11 @@ int klref_problem_create(int kind, klref_problem* out);
  * tabulated on the host at the quadrature points (bitwise-faithful RHS). */
 int klref_problem_create_host(double (*source)(double, double, void*), double (*boundary)(double, double, void*),
                               void* ctx, klref_problem* out);
+/* 3-d host callbacks (f, g of x, y, z), tabulated on the host in faithful mode */
+int klref_problem_create_host3(double (*source)(double, double, double, void*),
+                               double (*boundary)(double, double, double, void*), void* ctx, klref_problem* out);
+/* parameters of KLREF_PROBLEM_SERIES3D: count = 64 coefficients C_abc, a fastest */
+int klref_problem_set_params(klref_problem p, const double* params, int count);
 void klref_problem_destroy(klref_problem p);
 
 /* ---- solver ----------------------------------------------------------- */

@@ -14,20 +14,27 @@
 #include <vector>
 
 #include "solver2d.hpp"
+#include "solver3d.hpp"
 
 struct klref_mesh_s {
   int dim = 2;
   kb::Mesh2D mesh;
+  kb::Mesh3D mesh3;
 };
 struct klref_hierarchy_s {
-  std::shared_ptr<kb::DeviceHierarchy2D> dev;  // lev empty for host-only builds
+  int dim = 2;
+  std::shared_ptr<kb::DeviceHierarchy2D> dev;   // 2-d (lev empty for host-only builds)
+  std::shared_ptr<kb::DeviceHierarchy3D> dev3;  // 3-d
   bool on_device = false;
 };
 struct klref_problem_s {
   kb::Problem2D p;
+  kb::Problem3D p3;
+  int dims = 2;  // bit mask of the dimensions this problem is defined for (1: 2-d, 2: 3-d)
 };
 struct klref_solver_s {
   std::unique_ptr<kb::Solver2D> s;
+  std::unique_ptr<kb::Solver3D> s3;
   klref_hierarchy_s* h = nullptr;
 };
 struct klref_gf_s {
@@ -76,10 +83,27 @@ void need(const void* p, const char* what) {
   if (!p) kb::fail(kb::KB_STRUCTURAL, std::string("null argument: ") + what);
 }
 
-const kb::Hierarchy2D& host_of(klref_hierarchy h) { return h->dev->host; }
+const kb::Hierarchy2D& host_of(klref_hierarchy h) {
+  if (h->dim != 2) kb::fail(kb::KB_STRUCTURAL, "this query needs a 2-d hierarchy");
+  return h->dev->host;
+}
+int max_level_of(klref_hierarchy h) { return h->dim == 3 ? h->dev3->host.L : h->dev->host.L; }
+int macros_of(klref_hierarchy h) { return h->dim == 3 ? h->dev3->host.M : h->dev->host.M; }
+int lattice_size_of(klref_hierarchy h, int l) {
+  return h->dim == 3 ? h->dev3->host.levels[l].S : h->dev->host.levels[l].S;
+}
 
 void check_level(klref_hierarchy h, int level) {
-  if (level < 0 || level > host_of(h).L) kb::fail(kb::KB_STRUCTURAL, "level out of range");
+  if (level < 0 || level > max_level_of(h)) kb::fail(kb::KB_STRUCTURAL, "level out of range");
+}
+
+// run f on the solver of either dimension (same method names)
+template <typename F>
+void on_solver(klref_solver s, F&& f) {
+  if (s->s3)
+    f(*s->s3);
+  else
+    f(*s->s);
 }
 
 void same_hier(klref_solver s, klref_gf f) {
@@ -102,10 +126,13 @@ int klref_mesh_create(int dim, int num_vertices, const double* coords, int num_e
     need(coords, "coords");
     need(corners, "corners");
     need(out, "out");
-    if (dim != 2) kb::fail(kb::KB_STRUCTURAL, "grid hierarchies are only available for 2-d macro meshes");
+    if (dim != 2 && dim != 3) kb::fail(kb::KB_STRUCTURAL, "macro meshes are 2-d (triangles) or 3-d (tetrahedra)");
     auto m = std::make_unique<klref_mesh_s>();
     m->dim = dim;
-    m->mesh = kb::Mesh2D::create(num_vertices, coords, num_elements, corners);
+    if (dim == 2)
+      m->mesh = kb::Mesh2D::create(num_vertices, coords, num_elements, corners);
+    else
+      m->mesh3 = kb::Mesh3D::create(num_vertices, coords, num_elements, corners);
     *out = m.release();
   });
 }
@@ -117,7 +144,17 @@ static int build_impl(klref_mesh mesh, int max_level, klref_hierarchy* out, bool
     need(mesh, "mesh");
     need(out, "out");
     auto h = std::make_unique<klref_hierarchy_s>();
-    if (device) {
+    h->dim = mesh->dim;
+    if (mesh->dim == 3) {
+      if (device) {
+        require_device();
+        h->dev3 = kb::DeviceHierarchy3D::create(mesh->mesh3, max_level);
+        h->on_device = true;
+      } else {
+        h->dev3 = std::make_shared<kb::DeviceHierarchy3D>();
+        h->dev3->host = kb::Hierarchy3D::build(mesh->mesh3, max_level);
+      }
+    } else if (device) {
       require_device();
       h->dev = kb::DeviceHierarchy2D::create(mesh->mesh, max_level);
       h->on_device = true;
@@ -140,39 +177,39 @@ void klref_hierarchy_destroy(klref_hierarchy h) { delete h; }
 int klref_hierarchy_num_macros(klref_hierarchy h, int* out) {
   return guarded([&] {
     need(h, "h");
-    *out = host_of(h).M;
+    *out = macros_of(h);
   });
 }
 int klref_hierarchy_max_level(klref_hierarchy h, int* out) {
   return guarded([&] {
     need(h, "h");
-    *out = host_of(h).L;
+    *out = max_level_of(h);
   });
 }
 int klref_hierarchy_dof_count(klref_hierarchy h, int level, int64_t* out) {
   return guarded([&] {
     need(h, "h");
     check_level(h, level);
-    *out = host_of(h).levels[level].dofs;
+    *out = h->dim == 3 ? h->dev3->host.levels[level].dofs : host_of(h).levels[level].dofs;
   });
 }
 int klref_hierarchy_fine_element_count(klref_hierarchy h, int level, int64_t* out) {
   return guarded([&] {
     need(h, "h");
-    *out = static_cast<int64_t>(host_of(h).M) << (2 * level);
+    *out = static_cast<int64_t>(macros_of(h)) << (h->dim * level);
   });
 }
 int klref_hierarchy_lattice_size(klref_hierarchy h, int level, int* out) {
   return guarded([&] {
     need(h, "h");
     check_level(h, level);
-    *out = host_of(h).levels[level].S;
+    *out = lattice_size_of(h, level);
   });
 }
 int klref_hierarchy_dag_depth(klref_hierarchy h, int* out) {
   return guarded([&] {
     need(h, "h");
-    *out = host_of(h).dag_depth;
+    *out = h->dim == 3 ? 0 : host_of(h).dag_depth;
   });
 }
 int klref_hierarchy_groups(klref_hierarchy h, int level, int* num_groups, int* num_members, int* ptr,
@@ -180,6 +217,19 @@ int klref_hierarchy_groups(klref_hierarchy h, int level, int* num_groups, int* n
   return guarded([&] {
     need(h, "h");
     check_level(h, level);
+    if (h->dim == 3) {
+      const kb::Level3D& l3 = h->dev3->host.levels[level];
+      if (num_groups) *num_groups = static_cast<int>(l3.grp_ptr.size()) - 1;
+      if (num_members) *num_members = static_cast<int>(l3.mem_slot.size());
+      if (ptr) std::copy(l3.grp_ptr.begin(), l3.grp_ptr.end(), ptr);
+      if (members)
+        for (size_t k = 0; k < l3.mem_slot.size(); ++k) {
+          members[4 * k] = l3.mem_slot[k];
+          members[4 * k + 1] = l3.mem_idx[k];
+          members[4 * k + 2] = members[4 * k + 3] = 0;
+        }
+      return;
+    }
     const kb::Level2D& lv = host_of(h).levels[level];
     if (num_groups) *num_groups = static_cast<int>(lv.grp_ptr.size()) - 1;
     if (num_members) *num_members = static_cast<int>(lv.mem_slot.size());
@@ -197,6 +247,15 @@ int klref_hierarchy_element_matrices(klref_hierarchy h, int level, int kind, dou
   return guarded([&] {
     need(h, "h");
     check_level(h, level);
+    if (h->dim == 3) {  // mats[96 M] (six micro-tet types, 4x4), stencil[15 M]
+      const kb::Level3D& l3 = h->dev3->host.levels[level];
+      if (mats) {
+        const auto& src = kind == KLREF_MASS ? l3.kmass : l3.kstiff;
+        std::copy(src.begin(), src.end(), mats);
+      }
+      if (stencil) std::copy(l3.stencil.begin(), l3.stencil.end(), stencil);
+      return;
+    }
     const kb::Level2D& lv = host_of(h).levels[level];
     if (mats) {
       const auto& src = kind == KLREF_MASS ? lv.kmass : lv.kstiff;
@@ -210,7 +269,17 @@ int klref_problem_create(int kind, klref_problem* out) {
   return guarded([&] {
     need(out, "out");
     auto p = std::make_unique<klref_problem_s>();
-    p->p = kb::Problem2D::builtin(kind);
+    if (kind == KLREF_PROBLEM_ZERO) {
+      p->p = kb::Problem2D::builtin(kind);
+      p->p3 = kb::Problem3D::builtin(kb::P3_ZERO);
+      p->dims = 3;
+    } else if (kind >= KLREF_PROBLEM_SIN3D) {
+      p->p3 = kb::Problem3D::builtin(kind);
+      p->dims = 2;
+    } else {
+      p->p = kb::Problem2D::builtin(kind);
+      p->dims = 1;
+    }
     *out = p.release();
   });
 }
@@ -227,6 +296,28 @@ int klref_problem_create_host(double (*source)(double, double, void*), double (*
     p->p.boundary = [boundary, ctx](double x, double y) { return boundary(x, y, ctx); };
     p->p.has_exact = false;
     *out = p.release();
+  });
+}
+int klref_problem_create_host3(double (*source)(double, double, double, void*),
+                               double (*boundary)(double, double, double, void*), void* ctx, klref_problem* out) {
+  return guarded([&] {
+    need(out, "out");
+    need(reinterpret_cast<const void*>(source), "source");
+    need(reinterpret_cast<const void*>(boundary), "boundary");
+    auto p = std::make_unique<klref_problem_s>();
+    p->p3.kind = kb::P3_HOST;
+    p->p3.source = [source, ctx](double x, double y, double z) { return source(x, y, z, ctx); };
+    p->p3.boundary = [boundary, ctx](double x, double y, double z) { return boundary(x, y, z, ctx); };
+    p->dims = 2;
+    *out = p.release();
+  });
+}
+int klref_problem_set_params(klref_problem p, const double* params, int count) {
+  return guarded([&] {
+    need(p, "problem");
+    need(params, "params");
+    if (!(p->dims & 2)) kb::fail(kb::KB_STRUCTURAL, "parameters belong to 3-d series problems");
+    p->p3.set_params(params, count);
   });
 }
 void klref_problem_destroy(klref_problem p) { delete p; }
@@ -264,7 +355,13 @@ int klref_solver_create(klref_hierarchy h, klref_problem p, const klref_solver_c
       c.use_graph = cfg->use_graph;
     }
     auto s = std::make_unique<klref_solver_s>();
-    s->s = std::make_unique<kb::Solver2D>(h->dev, p->p, c);
+    if (h->dim == 3) {
+      if (!(p->dims & 2)) kb::fail(kb::KB_STRUCTURAL, "a 2-d problem cannot drive a 3-d hierarchy");
+      s->s3 = std::make_unique<kb::Solver3D>(h->dev3, p->p3, c);
+    } else {
+      if (!(p->dims & 1)) kb::fail(kb::KB_STRUCTURAL, "a 3-d problem cannot drive a 2-d hierarchy");
+      s->s = std::make_unique<kb::Solver2D>(h->dev, p->p, c);
+    }
     s->h = h;
     *out = s.release();
   });
@@ -274,81 +371,87 @@ void klref_solver_destroy(klref_solver s) { delete s; }
 int klref_solver_fmg(klref_solver s) {
   return guarded([&] {
     need(s, "solver");
-    s->s->fmg();
+    on_solver(s, [&](auto& v) { v.fmg(); });
   });
 }
 int klref_solver_fmg_enqueue(klref_solver s) {
   return guarded([&] {
     need(s, "solver");
-    s->s->fmg_enqueue();
+    on_solver(s, [&](auto& v) { v.fmg_enqueue(); });
   });
 }
 int klref_solver_synchronize(klref_solver s) {
   return guarded([&] {
     need(s, "solver");
-    s->s->sync_and_check();
+    on_solver(s, [&](auto& v) { v.sync_and_check(); });
   });
 }
 int klref_solver_stream(klref_solver s, void** stream) {
   return guarded([&] {
     need(s, "solver");
-    *stream = reinterpret_cast<void*>(s->s->stream());
+    on_solver(s, [&](auto& v) { *stream = reinterpret_cast<void*>(v.stream()); });
   });
 }
 int klref_solver_launch_count(klref_solver s, int* out) {
   return guarded([&] {
     need(s, "solver");
-    *out = s->s->launches_per_fmg();
+    on_solver(s, [&](auto& v) { *out = v.launches_per_fmg(); });
   });
 }
 int klref_solver_last_cg_iterations(klref_solver s, int* out) {
   return guarded([&] {
     need(s, "solver");
-    *out = s->s->last_cg_iters();
+    on_solver(s, [&](auto& v) { *out = v.last_cg_iters(); });
   });
 }
 int klref_solver_estimate_launch_count(klref_solver s, int* out) {
   return guarded([&] {
     need(s, "solver");
     need(out, "out");
-    *out = s->s->launches_per_estimate();
+    on_solver(s, [&](auto& v) { *out = v.launches_per_estimate(); });
   });
 }
 int klref_solver_set_stream(klref_solver s, void* stream) {
   return guarded([&] {
     need(s, "solver");
-    s->s->set_stream(reinterpret_cast<cudaStream_t>(stream));
+    on_solver(s, [&](auto& v) { v.set_stream(reinterpret_cast<cudaStream_t>(stream)); });
   });
 }
 int klref_solver_set_problem(klref_solver s, klref_problem p, int64_t* h2d_bytes) {
   return guarded([&] {
     need(s, "solver");
     need(p, "problem");
-    const size_t b = s->s->load_problem(p->p);
+    size_t b;
+    if (s->s3)
+      b = s->s3->load_problem(p->p3);
+    else
+      b = s->s->load_problem(p->p);
     if (h2d_bytes) *h2d_bytes = static_cast<int64_t>(b);
   });
 }
 int klref_solver_set_profiling(klref_solver s, int on) {
   return guarded([&] {
     need(s, "solver");
-    s->s->set_profiling(on != 0);
+    on_solver(s, [&](auto& v) { v.set_profiling(on != 0); });
   });
 }
 int klref_solver_kernel_stats(klref_solver s, int kind, double* ms, int* launches, double* bytes) {
   return guarded([&] {
     need(s, "solver");
     if (kind < KLREF_KERNEL_ALL || kind >= kb::KK_COUNT) kb::fail(kb::KB_STRUCTURAL, "unknown kernel kind");
-    s->s->kernel_stats(kind, ms, launches, bytes);
+    on_solver(s, [&](auto& v) { v.kernel_stats(kind, ms, launches, bytes); });
   });
 }
 int klref_solver_state_read(klref_solver s, int which, int level, double* host_out) {
   return guarded([&] {
     need(s, "solver");
     need(host_out, "host_out");
-    const double* d = s->s->state(which, level);
-    const size_t count = s->s->level_size(level);
-    KB_CUDA_CHECK(cudaMemcpyAsync(host_out, d, count * 8, cudaMemcpyDeviceToHost, s->s->stream()));
-    KB_CUDA_CHECK(cudaStreamSynchronize(s->s->stream()));
+    on_solver(s, [&](auto& v) {
+      const double* d = v.state(which, level);
+      const size_t count = v.level_size(level);
+      KB_CUDA_CHECK(cudaMemcpyAsync(host_out, d, count * 8, cudaMemcpyDeviceToHost, v.stream()));
+      KB_CUDA_CHECK(cudaStreamSynchronize(v.stream()));
+    });
   });
 }
 
@@ -368,20 +471,20 @@ static void fill_report(const kb::EstimateReport2D& r, klref_estimate_report* ou
 int klref_error_estimate(klref_solver s, int offset, int kind, klref_estimate_report* out, double* eta_local) {
   return guarded([&] {
     need(s, "solver");
-    fill_report(s->s->estimate(offset, kind), out, eta_local);
+    on_solver(s, [&](auto& v) { fill_report(v.estimate(offset, kind), out, eta_local); });
   });
 }
 int klref_error_estimate_enqueue(klref_solver s, int offset) {
   return guarded([&] {
     need(s, "solver");
-    s->s->estimate_enqueue(offset);
+    on_solver(s, [&](auto& v) { v.estimate_enqueue(offset); });
   });
 }
 int klref_error_estimate_finish(klref_solver s, int offset, int kind, klref_estimate_report* out,
                                 double* eta_local) {
   return guarded([&] {
     need(s, "solver");
-    fill_report(s->s->estimate_finish(offset, kind), out, eta_local);
+    on_solver(s, [&](auto& v) { fill_report(v.estimate_finish(offset, kind), out, eta_local); });
   });
 }
 
@@ -392,7 +495,7 @@ int klref_gf_create(klref_hierarchy h, int level, klref_gf* out) {
     require_device();
     check_level(h, level);
     auto f = std::make_unique<klref_gf_s>();
-    f->count = static_cast<size_t>(host_of(h).M) * host_of(h).levels[level].S;
+    f->count = static_cast<size_t>(macros_of(h)) * lattice_size_of(h, level);
     f->level = level;
     f->h = h;
     KB_CUDA_CHECK(cudaMalloc(&f->d, f->count * 8));
@@ -426,7 +529,7 @@ int klref_apply(klref_solver s, int kind, klref_gf x, klref_gf y) {
     same_hier(s, x);
     same_hier(s, y);
     if (x->level != y->level) kb::fail(kb::KB_STRUCTURAL, "operator level mismatch");
-    s->s->apply(x->level, kind == KLREF_MASS, x->d, y->d);
+    on_solver(s, [&](auto& v) { v.apply(x->level, kind == KLREF_MASS, x->d, y->d); });
   });
 }
 int klref_residual(klref_solver s, klref_gf u, klref_gf b, klref_gf r) {
@@ -436,7 +539,7 @@ int klref_residual(klref_solver s, klref_gf u, klref_gf b, klref_gf r) {
     same_hier(s, b);
     same_hier(s, r);
     if (u->level != b->level || u->level != r->level) kb::fail(kb::KB_STRUCTURAL, "grid function level mismatch");
-    s->s->residual(u->level, u->d, b->d, r->d);
+    on_solver(s, [&](auto& v) { v.residual(u->level, u->d, b->d, r->d); });
   });
 }
 int klref_gauss_seidel(klref_solver s, klref_gf u, klref_gf b, int sweeps) {
@@ -445,7 +548,7 @@ int klref_gauss_seidel(klref_solver s, klref_gf u, klref_gf b, int sweeps) {
     same_hier(s, u);
     same_hier(s, b);
     if (u->level != b->level) kb::fail(kb::KB_STRUCTURAL, "grid function level mismatch");
-    s->s->gauss_seidel(u->level, u->d, b->d, sweeps);
+    on_solver(s, [&](auto& v) { v.gauss_seidel(u->level, u->d, b->d, sweeps); });
   });
 }
 int klref_restrict_transpose(klref_solver s, klref_gf fine, klref_gf coarse) {
@@ -454,7 +557,7 @@ int klref_restrict_transpose(klref_solver s, klref_gf fine, klref_gf coarse) {
     same_hier(s, fine);
     same_hier(s, coarse);
     if (coarse->level + 1 != fine->level) kb::fail(kb::KB_STRUCTURAL, "restriction level mismatch");
-    s->s->restrict_to(fine->level, fine->d, coarse->d);
+    on_solver(s, [&](auto& v) { v.restrict_to(fine->level, fine->d, coarse->d); });
   });
 }
 int klref_prolongate(klref_solver s, klref_gf coarse, klref_gf fine) {
@@ -463,7 +566,7 @@ int klref_prolongate(klref_solver s, klref_gf coarse, klref_gf fine) {
     same_hier(s, fine);
     same_hier(s, coarse);
     if (coarse->level + 1 != fine->level) kb::fail(kb::KB_STRUCTURAL, "prolongation level mismatch");
-    s->s->prolongate(coarse->level, coarse->d, fine->d);
+    on_solver(s, [&](auto& v) { v.prolongate(coarse->level, coarse->d, fine->d); });
   });
 }
 int klref_cg_level0(klref_solver s, klref_gf u, klref_gf b) {
@@ -472,7 +575,7 @@ int klref_cg_level0(klref_solver s, klref_gf u, klref_gf b) {
     same_hier(s, u);
     same_hier(s, b);
     if (u->level != 0 || b->level != 0) kb::fail(kb::KB_STRUCTURAL, "cg_level0 works on level 0");
-    s->s->cg_level0(u->d, b->d);
+    on_solver(s, [&](auto& v) { v.cg_level0(u->d, b->d); });
   });
 }
 int klref_dot_unique(klref_solver s, klref_gf a, klref_gf b, double* out) {
@@ -482,14 +585,14 @@ int klref_dot_unique(klref_solver s, klref_gf a, klref_gf b, double* out) {
     same_hier(s, b);
     need(out, "out");
     if (a->level != b->level) kb::fail(kb::KB_STRUCTURAL, "grid function level mismatch");
-    *out = s->s->dot_unique(a->level, a->d, b->d);
+    on_solver(s, [&](auto& v) { *out = v.dot_unique(a->level, a->d, b->d); });
   });
 }
 int klref_interface_sync(klref_solver s, klref_gf f, int mode) {
   return guarded([&] {
     need(s, "solver");
     same_hier(s, f);
-    s->s->interface_sync(f->level, f->d, mode == KLREF_SYNC_ADDITIVE);
+    on_solver(s, [&](auto& v) { v.interface_sync(f->level, f->d, mode == KLREF_SYNC_ADDITIVE); });
   });
 }
 

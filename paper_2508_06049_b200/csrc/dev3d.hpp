@@ -1,0 +1,66 @@
+// Device-side views of the 3-d HHG tables and the 3-d kernel launch API
+// (kernels3d.cu).  Grid functions are fp64 arrays of M * S_l doubles,
+// macro-major, each macro a k-major tet lattice (lattice_index3) with
+// interface copies.  Unlike the 2-d path there are no dense per-copy tables:
+// lattice-interior nodes are recognised from (i, j, k), every
+// lattice-boundary copy is reached through its shared-node group.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "dev2d.hpp"
+#include "hier3d.hpp"
+
+namespace kb {
+
+struct DevLevel3D {
+  int n, S, M, ng, colors;
+  const int* grp_ptr;
+  const int* mem_slot;
+  const int* mem_ijk;          // i | j << 10 | k << 20
+  const std::uint8_t* grp_domain;
+  const double* grp_diag;
+  const int* color_grp_ptr;    // boundary groups by colour
+  const int* color_grp;
+  const double* kstiff;        // 96 per macro: [type][4][4]
+  const double* kmass;
+  const double* stK;           // 15 per macro (kDir order)
+  const double* stM;
+  const double* inv_c;
+  const int* pat_color;        // 8 per macro
+  const int* own_dot;          // group owner copy offsets (dot order)
+};
+
+enum Apply3Mode : int {
+  A3_PLAIN = 0,     // y = Op x, every copy
+  A3_RESIDUAL = 1,  // r = b - A u, domain-boundary copies 0
+  A3_RES_OWNER = 2, // residual for restriction: non-owner and domain copies 0
+};
+enum Prolong3Mode : int { P3_ASSIGN = 0, P3_ADD = 1 };
+
+void launch3_apply(const DevLevel3D& lv, bool mass, const double* x, double* y, const double* b, int mode,
+                   cudaStream_t st);
+void launch3_gs(const DevLevel3D& lv, double* u, const double* b, int sweeps, cudaStream_t st);
+void launch3_prolong(const DevLevel3D& coarse, const DevLevel3D& fine, const double* c, double* f, int mode,
+                     cudaStream_t st);
+// restriction of an owner-masked fine vector (A3_RES_OWNER residual), then
+// coarse additive sync; zero_domain: coarse domain-boundary copies 0
+void launch3_restrict(const DevLevel3D& fine, const DevLevel3D& coarse, const double* rf, double* rc,
+                      int zero_domain, cudaStream_t st);
+// zero the non-owner copies of f into out (single-operation restriction)
+void launch3_owner_mask(const DevLevel3D& lv, const double* f, double* out, cudaStream_t st);
+// set domain-boundary copies to g (per group); zero_rest: other nodes 0
+void launch3_set_boundary(const DevLevel3D& lv, double* f, const double* g_grp, int zero_rest, cudaStream_t st);
+void launch3_sync(const DevLevel3D& lv, double* f, int additive, cudaStream_t st);
+void launch3_cg0(const DevLevel3D& lv0, double* u, const double* b, double* scratch, CgParams prm,
+                 DevStatus* status, cudaStream_t st);
+// per-macro sums of e^T M e for e_base = uL - wb and e_coarser = uL - wc (all on level L)
+void launch3_estimate(const DevLevel3D& lv, const double* uL, const double* wb, const double* wc, double* sums,
+                      cudaStream_t st);
+void launch3_dot(const DevLevel3D& lv, const double* a, const double* b, double* partial, double* out,
+                 cudaStream_t st);
+void launch3_axpy(double* y, const double* x, double alpha, std::int64_t count, cudaStream_t st);
+
+}  // namespace kb

@@ -1,0 +1,721 @@
+// sm_100a kernels of the 3-d hot path (fp64, HBM-bound, no tensor cores).
+// The reference has no 3-d solver; the operation orders below are the
+// builder's specification, restated sequentially by oracle/klref_oracle3d.c
+// (tests compare bit for bit).  Compiled with -fmad=false like the 2-d path.
+//
+//   apply / residual    15-point stencil on lattice-interior nodes (plane-
+//                       parallel), member partial rows + additive sync on the
+//                       shared-node groups (like proj/src/fem.cpp:95-173)
+//   gauss_seidel        multicolour: boundary groups colour by colour, then
+//                       every macro's interior colour by colour, one 8-CTA
+//                       cluster per macro (the macro stays L2-resident)
+//   restrict / prolong  Freudenthal linear interpolation and its transpose
+//   cg0                 level-0 CG in one CTA (proj/src/multigrid.cpp:198-229 order)
+//   estimate            fused per-macro e^T M e over all micro-cells
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+
+#include "dev3d.hpp"
+
+namespace kb {
+namespace {
+
+constexpr int kT = 256;
+
+__constant__ int c_cv[6][4][3];  // vertex r of a type-t micro-cell relative to its base
+__constant__ int c_dir[15][3];
+__constant__ int c_pdir[8];      // parity pattern -> direction index (prolongation)
+
+__device__ __forceinline__ int tsz(int n) { return (n + 1) * (n + 2) * (n + 3) / 6; }
+__device__ __forceinline__ int lat2(int n, int i, int j) { return j * (n + 1) - (j * (j - 1)) / 2 + i; }
+__device__ __forceinline__ int lat3(int n, int i, int j, int k) { return tsz(n) - tsz(n - k) + lat2(n - k, i, j); }
+__device__ __forceinline__ bool inl(int n, int i, int j, int k) {
+  return i >= 0 && j >= 0 && k >= 0 && i + j + k <= n;
+}
+__device__ __forceinline__ bool interior3(int n, int i, int j, int k) {
+  return i >= 1 && j >= 1 && k >= 1 && i + j + k <= n - 1;
+}
+// (i, j) of the 2-d index q in a plane lattice of size m
+__device__ __forceinline__ void decode2(int m, int q, int& i, int& j) {
+  const float a = 2.0f * m + 3.0f;
+  int jj = static_cast<int>((a - sqrtf(a * a - 8.0f * q)) * 0.5f);
+  jj = max(0, min(jj, m));
+  while (jj < m && lat2(m, 0, jj + 1) <= q) ++jj;
+  while (jj > 0 && lat2(m, 0, jj) > q) --jj;
+  j = jj;
+  i = q - lat2(m, 0, jj);
+}
+
+// full partial row of node (i,j,k) of one macro (cells in type, role order)
+__device__ double partial_full(const double* __restrict__ K, const double* __restrict__ xm, int n, int i, int j,
+                               int k) {
+  double acc = 0.0;
+  for (int ty = 0; ty < 6; ++ty)
+    for (int r = 0; r < 4; ++r) {
+      const int bi = i - c_cv[ty][r][0], bj = j - c_cv[ty][r][1], bk = k - c_cv[ty][r][2];
+      int vi[4];
+      bool ok = true;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int a = bi + c_cv[ty][c][0], b = bj + c_cv[ty][c][1], cc = bk + c_cv[ty][c][2];
+        ok = ok && inl(n, a, b, cc);
+        vi[c] = ok ? lat3(n, a, b, cc) : 0;
+      }
+      if (!ok) continue;
+      const double* Kr = K + 16 * ty + 4 * r;
+      acc = acc + (((Kr[0] * xm[vi[0]] + Kr[1] * xm[vi[1]]) + Kr[2] * xm[vi[2]]) + Kr[3] * xm[vi[3]]);
+    }
+  return acc;
+}
+
+// off-diagonal part of the partial row (Gauss-Seidel)
+__device__ double partial_off3(const double* __restrict__ K, const double* xm, int n, int i, int j, int k) {
+  double o = 0.0;
+  for (int ty = 0; ty < 6; ++ty)
+    for (int r = 0; r < 4; ++r) {
+      const int bi = i - c_cv[ty][r][0], bj = j - c_cv[ty][r][1], bk = k - c_cv[ty][r][2];
+      int vi[4];
+      bool ok = true;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int a = bi + c_cv[ty][c][0], b = bj + c_cv[ty][c][1], cc = bk + c_cv[ty][c][2];
+        ok = ok && inl(n, a, b, cc);
+        vi[c] = ok ? lat3(n, a, b, cc) : 0;
+      }
+      if (!ok) continue;
+      const double* Kr = K + 16 * ty + 4 * r;
+      double v[3], kk[3];
+      int q = 0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (c != r) {
+          v[q] = xm[vi[c]];
+          kk[q] = Kr[c];
+          ++q;
+        }
+      o = o + ((kk[0] * v[0] + kk[1] * v[1]) + kk[2] * v[2]);
+    }
+  return o;
+}
+
+__device__ __forceinline__ void unpack_ijk(int p, int& i, int& j, int& k) {
+  i = p & 1023;
+  j = (p >> 10) & 1023;
+  k = (p >> 20) & 1023;
+}
+
+// ---------------------------------------------------------------- apply / residual
+// blocks [0, M (n+1)): one k-plane of one macro, lattice-interior nodes;
+// remaining blocks: one shared-node group per thread.
+__global__ void __launch_bounds__(kT) k3_apply(DevLevel3D lv, int mass, const double* __restrict__ x, double* y,
+                                               const double* __restrict__ b, int mode, int plane_blocks) {
+  const int n = lv.n, S = lv.S;
+  const double* __restrict__ st_all = mass ? lv.stM : lv.stK;
+  if (static_cast<int>(blockIdx.x) < plane_blocks) {
+    const int m = blockIdx.x / (n + 1), k = blockIdx.x - m * (n + 1);
+    const int m2 = n - k;
+    if (k < 1 || m2 < 3) return;
+    const double* st = st_all + 15 * m;
+    double s[15];
+#pragma unroll
+    for (int d = 0; d < 15; ++d) s[d] = __ldg(st + d);
+    const double* xm = x + static_cast<size_t>(m) * S;
+    const int base = tsz(n) - tsz(n - k);
+    const int np = (m2 + 1) * (m2 + 2) / 2;
+    for (int q = threadIdx.x; q < np; q += blockDim.x) {
+      int i, j;
+      decode2(m2, q, i, j);
+      if (!interior3(n, i, j, k)) continue;
+      double acc = s[0] * xm[base + q];
+#pragma unroll
+      for (int d = 1; d < 15; ++d) acc = acc + s[d] * xm[lat3(n, i + c_dir[d][0], j + c_dir[d][1], k + c_dir[d][2])];
+      const size_t off = static_cast<size_t>(m) * S + base + q;
+      y[off] = mode == A3_PLAIN ? acc : b[off] - acc;
+    }
+    return;
+  }
+  const int g = (blockIdx.x - plane_blocks) * blockDim.x + threadIdx.x;
+  if (g >= lv.ng) return;
+  const double* K = mass ? lv.kmass : lv.kstiff;
+  const int beg = lv.grp_ptr[g], end = lv.grp_ptr[g + 1];
+  double v;
+  auto part = [&](int q) {
+    const int s = lv.mem_slot[q];
+    int i, j, k;
+    unpack_ijk(lv.mem_ijk[q], i, j, k);
+    return partial_full(K + 96 * s, x + static_cast<size_t>(s) * S, n, i, j, k);
+  };
+  if (end - beg == 1) {
+    v = part(beg);
+  } else {
+    v = 0.0;
+    for (int q = beg; q < end; ++q) v += part(q);
+  }
+  const bool dom = lv.grp_domain[g];
+  for (int q = beg; q < end; ++q) {
+    int i, j, k;
+    unpack_ijk(lv.mem_ijk[q], i, j, k);
+    const size_t off = static_cast<size_t>(lv.mem_slot[q]) * S + lat3(n, i, j, k);
+    if (mode == A3_PLAIN)
+      y[off] = v;
+    else if (mode == A3_RESIDUAL)
+      y[off] = dom ? 0.0 : b[off] - v;
+    else
+      y[off] = (dom || q != beg) ? 0.0 : b[off] - v;
+  }
+}
+
+// ---------------------------------------------------------------- Gauss-Seidel
+// boundary phase of colour c: one group per thread
+__global__ void __launch_bounds__(kT) k3_gs_groups(DevLevel3D lv, double* u, const double* __restrict__ b, int c) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int p0 = lv.color_grp_ptr[c], p1 = lv.color_grp_ptr[c + 1];
+  if (p0 + t >= p1) return;
+  const int g = lv.color_grp[p0 + t];
+  const int n = lv.n, S = lv.S;
+  const int beg = lv.grp_ptr[g], end = lv.grp_ptr[g + 1];
+  int i0, j0, k0;
+  unpack_ijk(lv.mem_ijk[beg], i0, j0, k0);
+  const size_t own = static_cast<size_t>(lv.mem_slot[beg]) * S + lat3(n, i0, j0, k0);
+  double val;
+  if (lv.grp_domain[g]) {
+    val = b[own];
+  } else {
+    double off = 0.0;
+    for (int q = beg; q < end; ++q) {
+      const int s = lv.mem_slot[q];
+      int i, j, k;
+      unpack_ijk(lv.mem_ijk[q], i, j, k);
+      off = off + partial_off3(lv.kstiff + 96 * s, u + static_cast<size_t>(s) * S, n, i, j, k);
+    }
+    val = (b[own] - off) / lv.grp_diag[g];
+  }
+  for (int q = beg; q < end; ++q) {
+    int i, j, k;
+    unpack_ijk(lv.mem_ijk[q], i, j, k);
+    u[static_cast<size_t>(lv.mem_slot[q]) * S + lat3(n, i, j, k)] = val;
+  }
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned cluster_id_x() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+constexpr int kCluster = 8;
+
+// interior phase: one cluster of kCluster CTAs per macro, colours in order,
+// a cluster barrier between colours; nodes of colour c are the parity
+// patterns p with pat_color[m][p] == c (enumerated over their bounding box)
+__global__ void __launch_bounds__(kT) k3_gs_interior(DevLevel3D lv, double* u, const double* __restrict__ b) {
+  const int m = cluster_id_x();
+  const int r = cluster_rank();
+  const int n = lv.n, S = lv.S;
+  const double* st = lv.stK + 15 * m;
+  double s[15];
+#pragma unroll
+  for (int d = 0; d < 15; ++d) s[d] = __ldg(st + d);
+  const double inv_c = __ldg(lv.inv_c + m);
+  double* um = u + static_cast<size_t>(m) * S;
+  const double* bm = b + static_cast<size_t>(m) * S;
+  const int A = n / 2 + 1;  // box extent per parity class
+  const int box = A * A * A;
+  for (int c = 0; c < lv.colors; ++c) {
+    for (int p = 0; p < 8; ++p) {
+      if (__ldg(lv.pat_color + 8 * m + p) != c) continue;
+      const int pi = p & 1, pj = (p >> 1) & 1, pk = (p >> 2) & 1;
+      for (int v = threadIdx.x + kT * r; v < box; v += kT * kCluster) {
+        const int a = v % A, bb = (v / A) % A, cc = v / (A * A);
+        const int i = 2 * a + pi, j = 2 * bb + pj, k = 2 * cc + pk;
+        if (!interior3(n, i, j, k)) continue;
+        const int idx = lat3(n, i, j, k);
+        double acc = s[1] * __ldcg(um + lat3(n, i + c_dir[1][0], j + c_dir[1][1], k + c_dir[1][2]));
+#pragma unroll
+        for (int d = 2; d < 15; ++d)
+          acc = acc + s[d] * __ldcg(um + lat3(n, i + c_dir[d][0], j + c_dir[d][1], k + c_dir[d][2]));
+        __stcg(um + idx, (__ldg(bm + idx) - acc) * inv_c);
+      }
+    }
+    cluster_sync_all();
+  }
+}
+
+// ---------------------------------------------------------------- transfers
+__global__ void __launch_bounds__(kT) k3_prolong(DevLevel3D cv, DevLevel3D fv, const double* __restrict__ c, double* f,
+                                                 int mode) {
+  const int nf = fv.n, nc = cv.n;
+  const int m = blockIdx.x / (nf + 1), k = blockIdx.x - m * (nf + 1);
+  const int m2 = nf - k;
+  const int np = (m2 + 1) * (m2 + 2) / 2;
+  const int base = tsz(nf) - tsz(nf - k);
+  const double* cm = c + static_cast<size_t>(m) * cv.S;
+  for (int q = threadIdx.x; q < np; q += blockDim.x) {
+    int i, j;
+    decode2(m2, q, i, j);
+    const int p = (i & 1) | ((j & 1) << 1) | ((k & 1) << 2);
+    double v;
+    if (p == 0) {
+      v = cm[lat3(nc, i >> 1, j >> 1, k >> 1)];
+    } else {
+      const int d = c_pdir[p];
+      const int di = c_dir[d][0], dj = c_dir[d][1], dk = c_dir[d][2];
+      v = 0.5 * (cm[lat3(nc, (i - di) / 2, (j - dj) / 2, (k - dk) / 2)] +
+                 cm[lat3(nc, (i + di) / 2, (j + dj) / 2, (k + dk) / 2)]);
+    }
+    const size_t off = static_cast<size_t>(m) * fv.S + base + q;
+    f[off] = mode == P3_ADD ? f[off] + v : v;
+  }
+}
+
+__global__ void __launch_bounds__(kT) k3_restrict(DevLevel3D fv, DevLevel3D cv, const double* __restrict__ rf,
+                                                  double* rc) {
+  const int nf = fv.n, nc = cv.n;
+  const int m = blockIdx.x / (nc + 1), k = blockIdx.x - m * (nc + 1);
+  const int m2 = nc - k;
+  const int np = (m2 + 1) * (m2 + 2) / 2;
+  const int base = tsz(nc) - tsz(nc - k);
+  const double* fm = rf + static_cast<size_t>(m) * fv.S;
+  for (int q = threadIdx.x; q < np; q += blockDim.x) {
+    int i, j;
+    decode2(m2, q, i, j);
+    double acc = 0.0;
+#pragma unroll
+    for (int d = 0; d < 15; ++d) {
+      const int a = 2 * i + c_dir[d][0], bb = 2 * j + c_dir[d][1], cc = 2 * k + c_dir[d][2];
+      if (!inl(nf, a, bb, cc)) continue;
+      const double v = fm[lat3(nf, a, bb, cc)];
+      acc = acc + (d == 0 ? v : 0.5 * v);
+    }
+    rc[static_cast<size_t>(m) * cv.S + base + q] = acc;
+  }
+}
+
+// shared-node groups: additive / replace sync, optional zero of domain copies
+__global__ void __launch_bounds__(kT) k3_sync(DevLevel3D lv, double* f, int additive, int zero_domain) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= lv.ng) return;
+  const int n = lv.n, S = lv.S;
+  const int beg = lv.grp_ptr[g], end = lv.grp_ptr[g + 1];
+  auto off_of = [&](int q) {
+    int i, j, k;
+    unpack_ijk(lv.mem_ijk[q], i, j, k);
+    return static_cast<size_t>(lv.mem_slot[q]) * S + lat3(n, i, j, k);
+  };
+  if (zero_domain && lv.grp_domain[g]) {
+    for (int q = beg; q < end; ++q) f[off_of(q)] = 0.0;
+    return;
+  }
+  if (end - beg < 2) return;
+  double v;
+  if (additive) {
+    v = 0.0;
+    for (int q = beg; q < end; ++q) v += f[off_of(q)];
+  } else {
+    v = f[off_of(beg)];
+  }
+  for (int q = beg; q < end; ++q) f[off_of(q)] = v;
+}
+
+__global__ void __launch_bounds__(kT) k3_owner_mask(DevLevel3D lv, double* f) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= lv.ng) return;
+  const int n = lv.n, S = lv.S;
+  for (int q = lv.grp_ptr[g] + 1; q < lv.grp_ptr[g + 1]; ++q) {
+    int i, j, k;
+    unpack_ijk(lv.mem_ijk[q], i, j, k);
+    f[static_cast<size_t>(lv.mem_slot[q]) * S + lat3(n, i, j, k)] = 0.0;
+  }
+}
+
+__global__ void __launch_bounds__(kT) k3_set_boundary(DevLevel3D lv, double* f, const double* __restrict__ g_grp) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= lv.ng || !lv.grp_domain[g]) return;
+  const int n = lv.n, S = lv.S;
+  const double v = g_grp[g];
+  for (int q = lv.grp_ptr[g]; q < lv.grp_ptr[g + 1]; ++q) {
+    int i, j, k;
+    unpack_ijk(lv.mem_ijk[q], i, j, k);
+    f[static_cast<size_t>(lv.mem_slot[q]) * S + lat3(n, i, j, k)] = v;
+  }
+}
+
+// ---------------------------------------------------------------- level-0 CG (one CTA)
+__device__ double seq_dot3(const DevLevel3D& lv, const double* a, const double* b, bool zero_dom) {
+  double s = 0.0;
+  for (int g = 0; g < lv.ng; ++g) {
+    const int o = lv.own_dot[g];
+    double x = a[o], y = b[o];
+    if (zero_dom && lv.grp_domain[g]) x = y = 0.0;
+    s += x * y;
+  }
+  return s;
+}
+
+// y = A x on level 0 (vertex groups only); mode 0 plain with domain rows 0, 1 residual
+__device__ void cg_apply0(const DevLevel3D& lv, const double* x, double* y, const double* b, int residual) {
+  for (int g = threadIdx.x; g < lv.ng; g += blockDim.x) {
+    const int beg = lv.grp_ptr[g], end = lv.grp_ptr[g + 1];
+    double v;
+    auto part = [&](int q) {
+      const int s = lv.mem_slot[q];
+      int i, j, k;
+      unpack_ijk(lv.mem_ijk[q], i, j, k);
+      return partial_full(lv.kstiff + 96 * s, x + static_cast<size_t>(s) * lv.S, lv.n, i, j, k);
+    };
+    if (end - beg == 1) {
+      v = part(beg);
+    } else {
+      v = 0.0;
+      for (int q = beg; q < end; ++q) v += part(q);
+    }
+    const bool dom = lv.grp_domain[g];
+    for (int q = beg; q < end; ++q) {
+      int i, j, k;
+      unpack_ijk(lv.mem_ijk[q], i, j, k);
+      const size_t off = static_cast<size_t>(lv.mem_slot[q]) * lv.S + lat3(lv.n, i, j, k);
+      y[off] = dom ? 0.0 : (residual ? b[off] - v : v);
+    }
+  }
+}
+
+__global__ void k3_cg0(DevLevel3D lv, double* u, const double* b, double* r, double* p, double* ap, CgParams prm,
+                       DevStatus* status) {
+  const int total = lv.M * lv.S;
+  __shared__ double sh_rr, sh_alpha, sh_beta, sh_tol;
+  __shared__ int sh_go, sh_it;
+  cg_apply0(lv, u, r, b, 1);
+  __syncthreads();
+  for (int q = threadIdx.x; q < total; q += blockDim.x) p[q] = r[q];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    sh_rr = seq_dot3(lv, r, r, false);
+    const double bn = sqrt(fmax(0.0, seq_dot3(lv, b, b, true)));
+    const double a = prm.rel_tol * bn;
+    sh_tol = a < prm.abs_floor ? prm.abs_floor : a;
+    sh_go = sqrt(sh_rr) > sh_tol;
+    sh_it = 0;
+  }
+  __syncthreads();
+  while (sh_go) {
+    if (threadIdx.x == 0 && ++sh_it > prm.max_iter) {
+      if (status->code == 0) {
+        status->code = 1;
+        status->residual = sqrt(sh_rr);
+      }
+      sh_go = 0;
+    }
+    __syncthreads();
+    if (!sh_go) break;
+    cg_apply0(lv, p, ap, nullptr, 0);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const double pap = seq_dot3(lv, p, ap, false);
+      if (pap <= 0.0) {
+        if (status->code == 0) {
+          status->code = 2;
+          status->residual = sqrt(sh_rr);
+        }
+        sh_go = 0;
+      } else {
+        sh_alpha = sh_rr / pap;
+      }
+    }
+    __syncthreads();
+    if (!sh_go) break;
+    const double alpha = sh_alpha;
+    for (int q = threadIdx.x; q < total; q += blockDim.x) {
+      u[q] = u[q] + alpha * p[q];
+      r[q] = r[q] + (-alpha) * ap[q];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const double rn = seq_dot3(lv, r, r, false);
+      sh_beta = rn / sh_rr;
+      sh_rr = rn;
+    }
+    __syncthreads();
+    const double beta = sh_beta;
+    for (int q = threadIdx.x; q < total; q += blockDim.x) p[q] = p[q] * beta + r[q];
+    __syncthreads();
+    if (threadIdx.x == 0) sh_go = sqrt(sh_rr) > sh_tol;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) status->iters = sh_it;
+}
+
+// ---------------------------------------------------------------- estimator
+__global__ void __launch_bounds__(kT) k3_estimate(DevLevel3D lv, const double* __restrict__ uL,
+                                                  const double* __restrict__ wb, const double* __restrict__ wc,
+                                                  double* sums) {
+  const int m = blockIdx.x;
+  const int n = lv.n, S = lv.S;
+  const size_t mo = static_cast<size_t>(m) * S;
+  const double* Mt = lv.kmass + 96 * m;
+  double qb = 0.0, qc = 0.0;
+  for (int v = threadIdx.x; v < S * 6; v += blockDim.x) {
+    const int ty = v % 6, idx = v / 6;
+    // decode the base node of lattice index idx
+    int k = 0;
+    while (idx >= tsz(n) - tsz(n - k - 1)) ++k;
+    int i, j;
+    decode2(n - k, idx - (tsz(n) - tsz(n - k)), i, j);
+    int vi[4];
+    bool ok = true;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int a = i + c_cv[ty][c][0], b = j + c_cv[ty][c][1], cc = k + c_cv[ty][c][2];
+      ok = ok && inl(n, a, b, cc);
+      vi[c] = ok ? lat3(n, a, b, cc) : 0;
+    }
+    if (!ok) continue;
+    double eb[4], ec[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const double uu = uL[mo + vi[c]];
+      eb[c] = uu - wb[mo + vi[c]];
+      ec[c] = uu - wc[mo + vi[c]];
+    }
+    const double* T = Mt + 16 * ty;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const double rb = ((T[4 * a] * eb[0] + T[4 * a + 1] * eb[1]) + T[4 * a + 2] * eb[2]) + T[4 * a + 3] * eb[3];
+      const double rc = ((T[4 * a] * ec[0] + T[4 * a + 1] * ec[1]) + T[4 * a + 2] * ec[2]) + T[4 * a + 3] * ec[3];
+      qb = qb + eb[a] * rb;
+      qc = qc + ec[a] * rc;
+    }
+  }
+  __shared__ double rb[kT], rcs[kT];
+  rb[threadIdx.x] = qb;
+  rcs[threadIdx.x] = qc;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      rb[threadIdx.x] += rb[threadIdx.x + w];
+      rcs[threadIdx.x] += rcs[threadIdx.x + w];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    sums[2 * m] = rb[0];
+    sums[2 * m + 1] = rcs[0];
+  }
+}
+
+// ---------------------------------------------------------------- dot (owner copies + interiors)
+__global__ void __launch_bounds__(kT) k3_dot_partial(DevLevel3D lv, const double* a, const double* b, double* part) {
+  const int n = lv.n, S = lv.S;
+  double s = 0.0;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < lv.ng; t += stride) {
+    const int o = lv.own_dot[t];
+    s += a[o] * b[o];
+  }
+  const long long total = static_cast<long long>(lv.M) * S;
+  for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < total; t += stride) {
+    const int m = static_cast<int>(t / S), idx = static_cast<int>(t - static_cast<long long>(m) * S);
+    int k = 0;
+    while (idx >= tsz(n) - tsz(n - k - 1)) ++k;
+    int i, j;
+    decode2(n - k, idx - (tsz(n) - tsz(n - k)), i, j);
+    if (interior3(n, i, j, k)) s += a[t] * b[t];
+  }
+  __shared__ double red[kT];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+
+__global__ void k3_dot_final(const double* part, int count, double* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < count; ++i) s += part[i];
+    *out = s;
+  }
+}
+
+__global__ void k3_axpy(double* y, const double* x, double alpha, long long count) {
+  for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < count;
+       q += static_cast<long long>(gridDim.x) * blockDim.x)
+    y[q] = y[q] + alpha * x[q];
+}
+
+// source table f at every copy's own node coordinates (device libm; fast mode)
+__global__ void __launch_bounds__(kT) k3_ftab(DevLevel3D lv, const double* __restrict__ corners, int kind,
+                                              const double* __restrict__ par, double* f) {
+  const int n = lv.n;
+  const int m = blockIdx.x / (n + 1), k = blockIdx.x - m * (n + 1);
+  const int m2 = n - k;
+  const int np = (m2 + 1) * (m2 + 2) / 2;
+  const int base = tsz(n) - tsz(n - k);
+  const double* P = corners + 12 * m;
+  for (int q = threadIdx.x; q < np; q += blockDim.x) {
+    int i, j;
+    decode2(m2, q, i, j);
+    double X[3];
+    for (int a = 0; a < 3; ++a)
+      X[a] = P[a] + (static_cast<double>(i) / n) * (P[3 + a] - P[a]) + (static_cast<double>(j) / n) * (P[6 + a] - P[a]) +
+             (static_cast<double>(k) / n) * (P[9 + a] - P[a]);
+    double v = 0.0;
+    if (kind == 3) {
+      v = 3.0 * M_PI * M_PI * (sin(M_PI * X[0]) * sin(M_PI * X[1]) * sin(M_PI * X[2]));
+    } else if (kind == 4) {
+      const double dx = X[0] - 0.5, dy = X[1] - 0.5, dz = X[2] - 0.5, r2 = dx * dx + dy * dy + dz * dz;
+      v = (6.0 * 1000.0 - 4.0 * 1000.0 * 1000.0 * r2) * exp(-1000.0 * r2);
+    } else if (kind == 5) {
+      double sx[4], sy[4], sz[4];
+      for (int a = 0; a < 4; ++a) {
+        sx[a] = sin((a + 1) * M_PI * X[0]);
+        sy[a] = sin((a + 1) * M_PI * X[1]);
+        sz[a] = sin((a + 1) * M_PI * X[2]);
+      }
+      for (int c = 0; c < 4; ++c)
+        for (int b = 0; b < 4; ++b)
+          for (int a = 0; a < 4; ++a) v += par[a + 4 * b + 16 * c] * (sx[a] * sy[b] * sz[c]);
+    }
+    f[static_cast<size_t>(m) * lv.S + base + q] = v;
+  }
+}
+
+void check3(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) fail(KB_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void init_constants() {
+  static bool done = false;
+  if (done) return;
+  int cv[6][4][3];
+  for (int ty = 0; ty < 6; ++ty)
+    for (int r = 0; r < 4; ++r) cell_vertex(ty, r, cv[ty][r][0], cv[ty][r][1], cv[ty][r][2]);
+  KB_CUDA_CHECK(cudaMemcpyToSymbol(c_cv, cv, sizeof(cv)));
+  KB_CUDA_CHECK(cudaMemcpyToSymbol(c_dir, kDir, sizeof(kDir)));
+  int pdir[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int p = 1; p < 8; ++p)
+    for (int d = 1; d < 15; ++d) {
+      const int* v = kDir[d];
+      // the positive direction whose parities are p
+      if (((v[0] & 1) | ((v[1] & 1) << 1) | ((v[2] & 1) << 2)) == p && (d & 1)) pdir[p] = d;
+    }
+  KB_CUDA_CHECK(cudaMemcpyToSymbol(c_pdir, pdir, sizeof(pdir)));
+  done = true;
+}
+
+int blocks_for(long long count) { return static_cast<int>(std::max(1ll, (count + kT - 1) / kT)); }
+
+}  // namespace
+
+void launch3_apply(const DevLevel3D& lv, bool mass, const double* x, double* y, const double* b, int mode,
+                   cudaStream_t st) {
+  init_constants();
+  const int planes = lv.M * (lv.n + 1);
+  k3_apply<<<planes + blocks_for(lv.ng), kT, 0, st>>>(lv, mass ? 1 : 0, x, y, b, mode, planes);
+  check3("k3_apply");
+}
+
+void launch3_gs(const DevLevel3D& lv, double* u, const double* b, int sweeps, cudaStream_t st) {
+  init_constants();
+  for (int s = 0; s < sweeps; ++s) {
+    for (int c = 0; c < lv.colors; ++c) {
+      k3_gs_groups<<<blocks_for(lv.ng), kT, 0, st>>>(lv, u, b, c);
+      check3("k3_gs_groups");
+    }
+    if (lv.n < 4) continue;  // no lattice-interior nodes
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(kCluster * lv.M);
+    cfg.blockDim = dim3(kT);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kCluster;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    KB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k3_gs_interior, lv, u, b));
+  }
+}
+
+void launch3_prolong(const DevLevel3D& coarse, const DevLevel3D& fine, const double* c, double* f, int mode,
+                     cudaStream_t st) {
+  init_constants();
+  k3_prolong<<<fine.M * (fine.n + 1), kT, 0, st>>>(coarse, fine, c, f, mode);
+  check3("k3_prolong");
+}
+
+void launch3_restrict(const DevLevel3D& fine, const DevLevel3D& coarse, const double* rf, double* rc,
+                      int zero_domain, cudaStream_t st) {
+  init_constants();
+  k3_restrict<<<coarse.M * (coarse.n + 1), kT, 0, st>>>(fine, coarse, rf, rc);
+  check3("k3_restrict");
+  k3_sync<<<blocks_for(coarse.ng), kT, 0, st>>>(coarse, rc, 1, zero_domain);
+  check3("k3_sync");
+}
+
+void launch3_owner_mask(const DevLevel3D& lv, const double* f, double* out, cudaStream_t st) {
+  KB_CUDA_CHECK(cudaMemcpyAsync(out, f, sizeof(double) * static_cast<size_t>(lv.M) * lv.S, cudaMemcpyDeviceToDevice,
+                                st));
+  k3_owner_mask<<<blocks_for(lv.ng), kT, 0, st>>>(lv, out);
+  check3("k3_owner_mask");
+}
+
+void launch3_set_boundary(const DevLevel3D& lv, double* f, const double* g_grp, int zero_rest, cudaStream_t st) {
+  if (zero_rest) KB_CUDA_CHECK(cudaMemsetAsync(f, 0, sizeof(double) * static_cast<size_t>(lv.M) * lv.S, st));
+  k3_set_boundary<<<blocks_for(lv.ng), kT, 0, st>>>(lv, f, g_grp);
+  check3("k3_set_boundary");
+}
+
+void launch3_sync(const DevLevel3D& lv, double* f, int additive, cudaStream_t st) {
+  k3_sync<<<blocks_for(lv.ng), kT, 0, st>>>(lv, f, additive, 0);
+  check3("k3_sync");
+}
+
+void launch3_cg0(const DevLevel3D& lv0, double* u, const double* b, double* scratch, CgParams prm,
+                 DevStatus* status, cudaStream_t st) {
+  init_constants();
+  const size_t N = static_cast<size_t>(lv0.M) * lv0.S;
+  k3_cg0<<<1, kT, 0, st>>>(lv0, u, b, scratch, scratch + N, scratch + 2 * N, prm, status);
+  check3("k3_cg0");
+}
+
+void launch3_estimate(const DevLevel3D& lv, const double* uL, const double* wb, const double* wc, double* sums,
+                      cudaStream_t st) {
+  init_constants();
+  k3_estimate<<<lv.M, kT, 0, st>>>(lv, uL, wb, wc, sums);
+  check3("k3_estimate");
+}
+
+void launch3_dot(const DevLevel3D& lv, const double* a, const double* b, double* partial, double* out,
+                 cudaStream_t st) {
+  k3_dot_partial<<<64, kT, 0, st>>>(lv, a, b, partial);
+  k3_dot_final<<<1, 32, 0, st>>>(partial, 64, out);
+  check3("k3_dot");
+}
+
+void launch3_ftab(const DevLevel3D& lv, const double* corners, int kind, const double* params, double* f,
+                  cudaStream_t st) {
+  init_constants();
+  k3_ftab<<<lv.M * (lv.n + 1), kT, 0, st>>>(lv, corners, kind, params, f);
+  check3("k3_ftab");
+}
+
+void launch3_axpy(double* y, const double* x, double alpha, std::int64_t count, cudaStream_t st) {
+  k3_axpy<<<blocks_for(std::min<long long>(count, 148ll * 32 * kT)), kT, 0, st>>>(y, x, alpha, count);
+  check3("k3_axpy");
+}
+
+}  // namespace kb

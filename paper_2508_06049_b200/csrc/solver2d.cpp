@@ -31,13 +31,6 @@ void* DeviceArena::take(size_t bytes) {
   return base_ + off;
 }
 
-template <typename T>
-T* DeviceArena::upload(const std::vector<T>& v) {
-  if (v.empty()) return nullptr;
-  T* p = static_cast<T*>(take(v.size() * sizeof(T)));
-  KB_CUDA_CHECK(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
-  return p;
-}
 
 namespace {
 size_t round256(size_t b) { return (b + 255) & ~static_cast<size_t>(255); }

@@ -29,7 +29,12 @@ class DeviceArena {
   void reserve(size_t bytes);
   void* take(size_t bytes);
   template <typename T>
-  T* upload(const std::vector<T>& v);
+  T* upload(const std::vector<T>& v) {
+    if (v.empty()) return nullptr;
+    T* p = static_cast<T*>(take(v.size() * sizeof(T)));
+    KB_CUDA_CHECK(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return p;
+  }
   size_t used() const { return used_; }
 
  private:

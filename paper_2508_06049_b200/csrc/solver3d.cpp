@@ -1,0 +1,574 @@
+// Host orchestration of the 3-d hot path.  See solver3d.hpp.
+#include "solver3d.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+namespace kb {
+
+void launch3_ftab(const DevLevel3D& lv, const double* corners, int kind, const double* params, double* f,
+                  cudaStream_t st);  // kernels3d.cu
+
+namespace {
+size_t r256(size_t b) { return (b + 255) & ~static_cast<size_t>(255); }
+
+double sin3(double x, double y, double z) { return std::sin(M_PI * x) * std::sin(M_PI * y) * std::sin(M_PI * z); }
+double gauss3(double x, double y, double z) {
+  const double dx = x - 0.5, dy = y - 0.5, dz = z - 0.5;
+  return std::exp(-1000.0 * (dx * dx + dy * dy + dz * dz));
+}
+}  // namespace
+
+// ------------------------------------------------------------------ hierarchy upload
+std::unique_ptr<DeviceHierarchy3D> DeviceHierarchy3D::create(const Mesh3D& mesh, int max_level) {
+  auto d = std::make_unique<DeviceHierarchy3D>();
+  d->host = Hierarchy3D::build(mesh, max_level);
+  const Hierarchy3D& h = d->host;
+  std::vector<std::vector<int>> ijk(h.L + 1), own(h.L + 1);
+  size_t bytes = 0;
+  for (int l = 0; l <= h.L; ++l) {
+    const Level3D& lv = h.levels[l];
+    const int n = lv.n;
+    ijk[l].resize(lv.mem_slot.size());
+    // member (i, j, k) from the lattice index
+    std::vector<int> ii(lv.S), jj(lv.S), kk(lv.S);
+    for (int k = 0; k <= n; ++k)
+      for (int j = 0; j <= n - k; ++j)
+        for (int i = 0; i <= n - k - j; ++i) {
+          const int idx = lattice_index3(n, i, j, k);
+          ii[idx] = i, jj[idx] = j, kk[idx] = k;
+        }
+    for (size_t q = 0; q < lv.mem_slot.size(); ++q) {
+      const int idx = lv.mem_idx[q];
+      ijk[l][q] = ii[idx] | (jj[idx] << 10) | (kk[idx] << 20);
+    }
+    const int ng = static_cast<int>(lv.grp_ptr.size()) - 1;
+    own[l].resize(ng);
+    for (int g = 0; g < ng; ++g) {
+      const int q = lv.grp_ptr[g];
+      own[l][g] = lv.mem_slot[q] * lv.S + lv.mem_idx[q];
+    }
+    auto vb = [](auto& v) { return r256(v.size() * sizeof(v[0])); };
+    bytes += vb(lv.grp_ptr) + vb(lv.mem_slot) + vb(ijk[l]) + vb(lv.grp_domain) + vb(lv.grp_diag) +
+             vb(lv.color_grp_ptr) + vb(lv.color_grp) + vb(lv.kstiff) + vb(lv.kmass) + 2 * vb(lv.stencil) +
+             vb(lv.inv_c) + vb(lv.pat_color) + vb(own[l]);
+  }
+  d->arena.reserve(bytes + 4096);
+  for (int l = 0; l <= h.L; ++l) {
+    const Level3D& lv = h.levels[l];
+    DevLevel3D dl{};
+    dl.n = lv.n;
+    dl.S = lv.S;
+    dl.M = h.M;
+    dl.ng = static_cast<int>(lv.grp_ptr.size()) - 1;
+    dl.colors = h.colors;
+    dl.grp_ptr = d->arena.upload(lv.grp_ptr);
+    dl.mem_slot = d->arena.upload(lv.mem_slot);
+    dl.mem_ijk = d->arena.upload(ijk[l]);
+    dl.grp_domain = d->arena.upload(lv.grp_domain);
+    dl.grp_diag = d->arena.upload(lv.grp_diag);
+    dl.color_grp_ptr = d->arena.upload(lv.color_grp_ptr);
+    dl.color_grp = d->arena.upload(lv.color_grp);
+    dl.kstiff = d->arena.upload(lv.kstiff);
+    dl.kmass = d->arena.upload(lv.kmass);
+    // interior stencils: stiffness from the host tables, mass summed the same way
+    std::vector<double> stM(15 * static_cast<size_t>(h.M), 0.0);
+    for (int s = 0; s < h.M; ++s)
+      for (int ty = 0; ty < 6; ++ty)
+        for (int r = 0; r < 4; ++r)
+          for (int c = 0; c < 4; ++c) {
+            int ri, rj, rk, ci, cj, ck;
+            cell_vertex(ty, r, ri, rj, rk);
+            cell_vertex(ty, c, ci, cj, ck);
+            stM[15 * s + dir_index(ci - ri, cj - rj, ck - rk)] += lv.kmass[96 * s + 16 * ty + 4 * r + c];
+          }
+    dl.stK = d->arena.upload(lv.stencil);
+    dl.stM = d->arena.upload(stM);
+    dl.inv_c = d->arena.upload(lv.inv_c);
+    dl.pat_color = d->arena.upload(lv.pat_color);
+    dl.own_dot = d->arena.upload(own[l]);
+    d->lev.push_back(dl);
+  }
+  return d;
+}
+
+// ------------------------------------------------------------------ problems
+Problem3D Problem3D::builtin(int kind) {
+  Problem3D p;
+  p.kind = kind;
+  switch (kind) {
+    case P3_ZERO:
+      p.source = p.boundary = [](double, double, double) { return 0.0; };
+      break;
+    case P3_SIN:  // BASELINE.json config 3: u = prod sin(pi x_i), f = 3 pi^2 u
+      p.boundary = sin3;
+      p.source = [](double x, double y, double z) { return 3.0 * M_PI * M_PI * sin3(x, y, z); };
+      break;
+    case P3_GAUSS:  // config 4: u = exp(-1000 |x - c|^2), f = (6a - 4a^2 r^2) u
+      p.boundary = gauss3;
+      p.source = [](double x, double y, double z) {
+        const double dx = x - 0.5, dy = y - 0.5, dz = z - 0.5, r2 = dx * dx + dy * dy + dz * dz;
+        return (6.0 * 1000.0 - 4.0 * 1000.0 * 1000.0 * r2) * gauss3(x, y, z);
+      };
+      break;
+    case P3_SERIES:  // config 5: f = sum C_abc sin(a pi x) sin(b pi y) sin(c pi z), g = 0
+      p.params.assign(64, 0.0);
+      p.boundary = [](double, double, double) { return 0.0; };
+      break;
+    default:
+      fail(KB_STRUCTURAL, "unknown built-in 3-d problem kind");
+  }
+  return p;
+}
+
+void Problem3D::set_params(const double* v, int count) {
+  if (kind != P3_SERIES || count != 64) fail(KB_STRUCTURAL, "series problems take 64 coefficients");
+  params.assign(v, v + count);
+}
+
+static double series_value(const std::vector<double>& C, double x, double y, double z) {
+  double acc = 0.0;
+  for (int c = 1; c <= 4; ++c)
+    for (int b = 1; b <= 4; ++b)
+      for (int a = 1; a <= 4; ++a)
+        acc += C[(a - 1) + 4 * (b - 1) + 16 * (c - 1)] *
+               (std::sin(a * M_PI * x) * std::sin(b * M_PI * y) * std::sin(c * M_PI * z));
+  return acc;
+}
+
+// ------------------------------------------------------------------ solver
+Solver3D::Solver3D(std::shared_ptr<DeviceHierarchy3D> h, Problem3D p, SolverConfig2D cfg)
+    : H_(std::move(h)), prob_(std::move(p)), cfg_(cfg) {
+  const Hierarchy3D& hh = H_->host;
+  L_ = hh.L;
+  const int M = hh.M;
+  if (cfg_.finest_policy != 0) fail(KB_STRUCTURAL, "only FinestPolicy::None is available on the device path");
+  has_source_ = prob_.kind != P3_ZERO;
+  auto lsize = [&](int l) { return static_cast<size_t>(M) * hh.levels[l].S; };
+  size_t bytes = 0;
+  for (int l = 0; l <= L_; ++l) {
+    bytes += 2 * r256(lsize(l) * 8);
+    if (l < L_) bytes += r256(lsize(l + 1) * 8) + 2 * r256(lsize(l) * 8);
+    if (l >= 1) bytes += r256(lsize(l) * 8);
+    bytes += r256((hh.levels[l].grp_ptr.size()) * 8);
+    if (has_source_) bytes += r256(lsize(l) * 8);
+  }
+  bytes += r256(3 * lsize(0) * 8) + r256(2 * M * 8) + 3 * r256(lsize(L_) * 8) + r256(64 * 8) + r256(8) +
+           r256(sizeof(DevStatus)) + r256(12 * M * 8) + r256(64 * 8);
+  arena_.reserve(bytes);
+  u_.assign(L_ + 1, nullptr);
+  b_ = w_ = vu_ = vb_ = r_ = gbnd_ = ftab_ = u_;
+  for (int l = 0; l <= L_; ++l) {
+    u_[l] = static_cast<double*>(arena_.take(lsize(l) * 8));
+    b_[l] = static_cast<double*>(arena_.take(lsize(l) * 8));
+    if (l < L_) {
+      w_[l] = static_cast<double*>(arena_.take(lsize(l + 1) * 8));
+      vu_[l] = static_cast<double*>(arena_.take(lsize(l) * 8));
+      vb_[l] = static_cast<double*>(arena_.take(lsize(l) * 8));
+    }
+    if (l >= 1) r_[l] = static_cast<double*>(arena_.take(lsize(l) * 8));
+    gbnd_[l] = static_cast<double*>(arena_.take(hh.levels[l].grp_ptr.size() * 8));
+    if (has_source_) ftab_[l] = static_cast<double*>(arena_.take(lsize(l) * 8));
+  }
+  cg_scratch_ = static_cast<double*>(arena_.take(3 * lsize(0) * 8));
+  est_sums_ = static_cast<double*>(arena_.take(2 * M * 8));
+  est_a_ = static_cast<double*>(arena_.take(lsize(L_) * 8));
+  est_b_ = static_cast<double*>(arena_.take(lsize(L_) * 8));
+  est_c_ = static_cast<double*>(arena_.take(lsize(L_) * 8));
+  dot_partial_ = static_cast<double*>(arena_.take(64 * 8));
+  dot_out_ = static_cast<double*>(arena_.take(8));
+  status_ = static_cast<DevStatus*>(arena_.take(sizeof(DevStatus)));
+  double* corners = static_cast<double*>(arena_.take(12 * M * 8));
+  double* params = static_cast<double*>(arena_.take(64 * 8));
+  KB_CUDA_CHECK(cudaStreamCreateWithFlags(&own_stream_, cudaStreamNonBlocking));
+  stream_ = own_stream_;
+  KB_CUDA_CHECK(cudaMallocHost(&status_host_, sizeof(DevStatus)));
+  KB_CUDA_CHECK(cudaMallocHost(&sums_host_, 2 * M * sizeof(double)));
+  KB_CUDA_CHECK(cudaMemset(status_, 0, sizeof(DevStatus)));
+  // macro corners + series coefficients for the device source tables (fast mode)
+  std::vector<double> cv(12 * static_cast<size_t>(M));
+  for (int s = 0; s < M; ++s)
+    for (int c = 0; c < 4; ++c) {
+      const int v = hh.mesh.tet[s][c];
+      cv[12 * s + 3 * c] = hh.mesh.x[v];
+      cv[12 * s + 3 * c + 1] = hh.mesh.y[v];
+      cv[12 * s + 3 * c + 2] = hh.mesh.z[v];
+    }
+  KB_CUDA_CHECK(cudaMemcpy(corners, cv.data(), cv.size() * 8, cudaMemcpyHostToDevice));
+  std::vector<double> par(64, 0.0);
+  if (!prob_.params.empty()) std::copy(prob_.params.begin(), prob_.params.end(), par.begin());
+  KB_CUDA_CHECK(cudaMemcpy(params, par.data(), 64 * 8, cudaMemcpyHostToDevice));
+  for (int l = 0; l <= L_; ++l) stage_count_ = std::max(stage_count_, std::max(lsize(l), hh.levels[l].grp_ptr.size()));
+  KB_CUDA_CHECK(cudaMallocHost(&stage_, stage_count_ * sizeof(double)));
+  load_problem(prob_);
+  if (has_source_ && !cfg_.faithful_source) {
+    for (int l = 0; l <= L_; ++l) launch3_ftab(H_->lev[l], corners, prob_.kind, params, ftab_[l], stream_);
+  }
+  KB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+}
+
+Solver3D::~Solver3D() {
+  if (exec_) cudaGraphExecDestroy(exec_);
+  for (cudaEvent_t e : events_) cudaEventDestroy(e);
+  if (own_stream_) cudaStreamDestroy(own_stream_);
+  if (status_host_) cudaFreeHost(status_host_);
+  if (sums_host_) cudaFreeHost(sums_host_);
+  if (stage_) cudaFreeHost(stage_);
+}
+
+size_t Solver3D::level_size(int level) const {
+  return static_cast<size_t>(H_->host.M) * H_->host.levels.at(level).S;
+}
+
+// Dirichlet values g per group and (faithful mode) f per copy, both at the
+// owner copy's node coordinates, host libm (like proj/src/fem.cpp:212-228).
+size_t Solver3D::load_problem(const Problem3D& p) {
+  if (p.kind != prob_.kind) fail(KB_STRUCTURAL, "set_problem: the problem kind must match the solver's");
+  if (&p != &prob_) prob_ = p;
+  const Hierarchy3D& hh = H_->host;
+  const int M = hh.M;
+  auto src = [&](double x, double y, double z) {
+    return prob_.kind == P3_SERIES ? series_value(prob_.params, x, y, z) : prob_.source(x, y, z);
+  };
+  size_t bytes = 0;
+  for (int l = 0; l <= L_; ++l) {
+    const Level3D& lv = hh.levels[l];
+    const int n = lv.n, S = lv.S;
+    auto coords = [&](int s, int i, int j, int k, double* out) {
+      const auto& t = hh.mesh.tet[s];
+      const double P[4][3] = {{hh.mesh.x[t[0]], hh.mesh.y[t[0]], hh.mesh.z[t[0]]},
+                              {hh.mesh.x[t[1]], hh.mesh.y[t[1]], hh.mesh.z[t[1]]},
+                              {hh.mesh.x[t[2]], hh.mesh.y[t[2]], hh.mesh.z[t[2]]},
+                              {hh.mesh.x[t[3]], hh.mesh.y[t[3]], hh.mesh.z[t[3]]}};
+      for (int a = 0; a < 3; ++a)
+        out[a] = P[0][a] + (static_cast<double>(i) / n) * (P[1][a] - P[0][a]) +
+                 (static_cast<double>(j) / n) * (P[2][a] - P[0][a]) + (static_cast<double>(k) / n) * (P[3][a] - P[0][a]);
+    };
+    std::vector<int> ii(S), jj(S), kk(S);
+    for (int k = 0; k <= n; ++k)
+      for (int j = 0; j <= n - k; ++j)
+        for (int i = 0; i <= n - k - j; ++i) {
+          const int idx = lattice_index3(n, i, j, k);
+          ii[idx] = i, jj[idx] = j, kk[idx] = k;
+        }
+    const int ng = static_cast<int>(lv.grp_ptr.size()) - 1;
+    KB_CUDA_CHECK(cudaStreamSynchronize(stream_));  // the staging buffer may feed an earlier copy
+    for (int g = 0; g < ng; ++g) {
+      double v = 0.0;
+      if (lv.grp_domain[g]) {
+        const int q = lv.grp_ptr[g], s = lv.mem_slot[q], idx = lv.mem_idx[q];
+        double x[3];
+        coords(s, ii[idx], jj[idx], kk[idx], x);
+        v = prob_.boundary(x[0], x[1], x[2]);
+      }
+      stage_[g] = v;
+    }
+    KB_CUDA_CHECK(cudaMemcpyAsync(gbnd_[l], stage_, ng * 8, cudaMemcpyHostToDevice, stream_));
+    bytes += ng * 8;
+    if (has_source_ && cfg_.faithful_source) {
+      KB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+      const size_t N = level_size(l);
+      for (int s = 0; s < M; ++s)
+        for (int idx = 0; idx < S; ++idx) {
+          const size_t off = static_cast<size_t>(s) * S + idx;
+          int os = s, oidx = idx;
+          const int g = lv.node_gid[off];
+          if (g >= 0) {
+            os = lv.mem_slot[lv.grp_ptr[g]];
+            oidx = lv.mem_idx[lv.grp_ptr[g]];
+          }
+          double x[3];
+          coords(os, ii[oidx], jj[oidx], kk[oidx], x);
+          stage_[off] = src(x[0], x[1], x[2]);
+        }
+      KB_CUDA_CHECK(cudaMemcpyAsync(ftab_[l], stage_, N * 8, cudaMemcpyHostToDevice, stream_));
+      bytes += N * 8;
+    }
+  }
+  KB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+  return bytes;
+}
+
+double* Solver3D::state(int which, int level) {
+  if (level < 0 || level > L_) fail(KB_STRUCTURAL, "level out of range");
+  if (which == 0) return u_[level];
+  if (which == 1) return b_[level];
+  if (which == 2) {
+    if (level < 1) fail(KB_STRUCTURAL, "w lives on levels 1..L");
+    return w_[level - 1];
+  }
+  fail(KB_STRUCTURAL, "unknown state component");
+}
+
+// ------------------------------------------------------------------ probes (as Solver2D)
+void Solver3D::set_profiling(bool on) {
+  if (on == profiling_) return;
+  profiling_ = on;
+  if (exec_) {
+    cudaGraphExecDestroy(exec_);
+    exec_ = nullptr;
+  }
+  fmg_probes_.clear();
+  est_probes_.clear();
+}
+cudaEvent_t Solver3D::event_at(int idx) {
+  while (static_cast<int>(events_.size()) <= idx) {
+    cudaEvent_t e;
+    KB_CUDA_CHECK(cudaEventCreate(&e));
+    events_.push_back(e);
+  }
+  return events_[idx];
+}
+void Solver3D::probe_begin(std::vector<Probe>* list) {
+  probes_ = list;
+  list->clear();
+  if (!profiling_) return;
+  next_event_ = (list == &fmg_probes_) ? 0 : 4096;
+  last_event_ = next_event_++;
+  cudaEvent_t e = event_at(last_event_);
+  if (capturing_)
+    KB_CUDA_CHECK(cudaEventRecordWithFlags(e, stream_, cudaEventRecordExternal));
+  else
+    KB_CUDA_CHECK(cudaEventRecord(e, stream_));
+}
+void Solver3D::mark(int kind, double bytes, int nlaunch) {
+  launches_ += nlaunch;
+  if (!profiling_ || !probes_) return;
+  const int e = next_event_++;
+  if (capturing_)
+    KB_CUDA_CHECK(cudaEventRecordWithFlags(event_at(e), stream_, cudaEventRecordExternal));
+  else
+    KB_CUDA_CHECK(cudaEventRecord(event_at(e), stream_));
+  probes_->push_back({kind, bytes, last_event_, e});
+  last_event_ = e;
+}
+void Solver3D::kernel_stats(int kind, double* ms, int* launches, double* bytes) {
+  double t = 0.0, b = 0.0;
+  int c = 0;
+  for (const auto* list : {&fmg_probes_, &est_probes_})
+    for (const Probe& p : *list) {
+      if (p.kind != kind && kind >= 0) continue;
+      float f = 0.f;
+      KB_CUDA_CHECK(cudaEventElapsedTime(&f, events_[p.ev0], events_[p.ev1]));
+      t += f;
+      b += p.bytes;
+      ++c;
+    }
+  if (ms) *ms = t;
+  if (launches) *launches = c;
+  if (bytes) *bytes = b;
+}
+
+// ------------------------------------------------------------------ FMG
+void Solver3D::vcycle(int l, double* u, const double* b) {
+  const auto& lev = H_->lev;
+  if (l == 0) {
+    launch3_cg0(lev[0], u, b, cg_scratch_, {cfg_.coarse_rel_tol, cfg_.coarse_abs_floor, cfg_.coarse_max_iter},
+                status_, stream_);
+    mark(KK_CG0, 0.0);
+    return;
+  }
+  const int colors = lev[l].colors;
+  const int gs_launches = colors + (lev[l].n >= 4 ? 1 : 0);
+  // algorithmic bytes per unique DoF: GS 24/sweep, residual 24,
+  // restriction 8 fine + 8 coarse, prolongation+correction 16 fine + 8 coarse
+  if (cfg_.pre_smooth > 0) {
+    launch3_gs(lev[l], u, b, cfg_.pre_smooth, stream_);
+    mark(KK_GS, 24.0 * cfg_.pre_smooth * dofs(l), gs_launches * cfg_.pre_smooth);
+  }
+  launch3_apply(lev[l], false, u, r_[l], b, A3_RES_OWNER, stream_);
+  mark(KK_RESIDUAL, 24.0 * dofs(l));
+  launch3_restrict(lev[l], lev[l - 1], r_[l], vb_[l - 1], 1, stream_);
+  mark(KK_RESTRICT, 8.0 * dofs(l) + 8.0 * dofs(l - 1), 2);
+  KB_CUDA_CHECK(cudaMemsetAsync(vu_[l - 1], 0, level_size(l - 1) * 8, stream_));
+  mark(KK_OTHER, 8.0 * dofs(l - 1), 0);
+  vcycle(l - 1, vu_[l - 1], vb_[l - 1]);
+  launch3_prolong(lev[l - 1], lev[l], vu_[l - 1], u, P3_ADD, stream_);
+  mark(KK_PROLONG, 16.0 * dofs(l) + 8.0 * dofs(l - 1));
+  if (cfg_.post_smooth > 0) {
+    launch3_gs(lev[l], u, b, cfg_.post_smooth, stream_);
+    mark(KK_GS, 24.0 * cfg_.post_smooth * dofs(l), gs_launches * cfg_.post_smooth);
+  }
+}
+
+void Solver3D::enqueue_fmg_body() {
+  const auto& lev = H_->lev;
+  launches_ = 0;
+  probe_begin(&fmg_probes_);
+  KB_CUDA_CHECK(cudaMemsetAsync(status_, 0, sizeof(DevStatus), stream_));
+  mark(KK_OTHER, 0.0, 0);
+  for (int l = 0; l <= L_; ++l) {
+    // b = M f_I, then the Dirichlet rows g
+    if (has_source_) {
+      launch3_apply(lev[l], true, ftab_[l], b_[l], nullptr, A3_PLAIN, stream_);
+      launch3_set_boundary(lev[l], b_[l], gbnd_[l], 0, stream_);
+      mark(KK_RHS, 16.0 * dofs(l), 2);
+    } else {
+      launch3_set_boundary(lev[l], b_[l], gbnd_[l], 1, stream_);
+      mark(KK_RHS, 8.0 * dofs(l), 1);
+    }
+  }
+  launch3_set_boundary(lev[0], u_[0], gbnd_[0], 1, stream_);
+  mark(KK_OTHER, 8.0 * dofs(0));
+  launch3_cg0(lev[0], u_[0], b_[0], cg_scratch_, {cfg_.coarse_rel_tol, cfg_.coarse_abs_floor, cfg_.coarse_max_iter},
+              status_, stream_);
+  mark(KK_CG0, 0.0);
+  for (int l = 0; l < L_; ++l) {
+    // w[l] = P u[l] (snapshot before the Dirichlet reset); next = w with g on the boundary
+    launch3_prolong(lev[l], lev[l + 1], u_[l], w_[l], P3_ASSIGN, stream_);
+    KB_CUDA_CHECK(cudaMemcpyAsync(u_[l + 1], w_[l], level_size(l + 1) * 8, cudaMemcpyDeviceToDevice, stream_));
+    launch3_set_boundary(lev[l + 1], u_[l + 1], gbnd_[l + 1], 0, stream_);
+    mark(KK_PROLONG, 24.0 * dofs(l + 1) + 8.0 * dofs(l), 2);
+    for (int c = 0; c < cfg_.nu; ++c) vcycle(l + 1, u_[l + 1], b_[l + 1]);
+  }
+  fmg_launches_ = launches_;
+  probes_ = nullptr;
+}
+
+void Solver3D::fmg_enqueue() {
+  if (L_ < 1) fail(KB_STRUCTURAL, "full multigrid requires at least one level above the coarse grid");
+  if (!cfg_.use_graph) {
+    enqueue_fmg_body();
+    return;
+  }
+  if (!exec_) {
+    cudaGraph_t graph = nullptr;
+    KB_CUDA_CHECK(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+    capturing_ = true;
+    try {
+      enqueue_fmg_body();
+    } catch (...) {
+      capturing_ = false;
+      cudaStreamEndCapture(stream_, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      throw;
+    }
+    capturing_ = false;
+    KB_CUDA_CHECK(cudaStreamEndCapture(stream_, &graph));
+    KB_CUDA_CHECK(cudaGraphInstantiate(&exec_, graph, 0));
+    cudaGraphDestroy(graph);
+  }
+  KB_CUDA_CHECK(cudaGraphLaunch(exec_, stream_));
+}
+
+void Solver3D::sync_and_check() {
+  KB_CUDA_CHECK(cudaMemcpyAsync(status_host_, status_, sizeof(DevStatus), cudaMemcpyDeviceToHost, stream_));
+  KB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+  if (status_host_->code) {
+    Error e(KB_SOLVER, status_host_->code == 1 ? "coarse-grid CG did not converge"
+                                               : "coarse-grid CG lost positive definiteness");
+    e.residual = status_host_->residual;
+    throw e;
+  }
+}
+
+void Solver3D::fmg() {
+  fmg_enqueue();
+  sync_and_check();
+}
+
+// error_estimate (proj/src/estimator.cpp:8-45): e_base = u_L - P^(j-1) w[L-j],
+// e_coarser = u_L - P^j w[L-j-1]
+void Solver3D::estimate_enqueue(int offset) {
+  if (offset < 1 || offset > L_ - 1) fail(KB_STRUCTURAL, "estimate offset must satisfy 1 <= j <= L-1");
+  const auto& lev = H_->lev;
+  const int base = L_ - offset;
+  const int saved = launches_;
+  probe_begin(&est_probes_);
+  auto lift = [&](const double* src, int from_level, double* out) -> const double* {
+    // prolongate from `from_level` to L through the scratch vectors
+    const double* cur = src;
+    for (int l = from_level; l < L_; ++l) {
+      double* dst = (l + 1 == L_) ? out : (l % 2 ? vu_[l + 1] : vb_[l + 1]);
+      launch3_prolong(lev[l], lev[l + 1], cur, dst, P3_ASSIGN, stream_);
+      mark(KK_ESTIMATE, 8.0 * dofs(l + 1) + 8.0 * dofs(l));
+      cur = dst;
+    }
+    return cur;
+  };
+  const double* wb = lift(w_[base], base + 1, est_a_);
+  const double* wc = lift(w_[base - 1], base, est_b_);
+  launch3_estimate(lev[L_], u_[L_], wb, wc, est_sums_, stream_);
+  mark(KK_ESTIMATE, 24.0 * dofs(L_));
+  KB_CUDA_CHECK(cudaMemcpyAsync(sums_host_, est_sums_, 2 * H_->host.M * sizeof(double), cudaMemcpyDeviceToHost,
+                                stream_));
+  probes_ = nullptr;
+  est_launches_ = launches_ - saved;
+  launches_ = saved;
+}
+
+EstimateReport2D Solver3D::estimate_finish(int offset, int kind) {
+  KB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+  const int M = H_->host.M;
+  EstimateReport2D rep;
+  rep.offset = offset;
+  rep.base_level = L_ - offset;
+  rep.kind = kind;
+  double gb = 0.0, gc = 0.0;
+  for (int s = 0; s < M; ++s) {
+    gb += sums_host_[2 * s];
+    gc += sums_host_[2 * s + 1];
+  }
+  rep.norm_base = std::sqrt(std::max(0.0, gb));
+  rep.norm_coarser = std::sqrt(std::max(0.0, gc));
+  rep.conv_factor = rep.norm_coarser > 0.0 ? rep.norm_base / rep.norm_coarser : 0.0;
+  rep.eta = std::pow(rep.conv_factor, offset) * rep.norm_base;
+  rep.eta_local.resize(M);
+  const double floor = 1e-14 * rep.norm_coarser;
+  for (int s = 0; s < M; ++s) {
+    const double lb = std::sqrt(std::max(0.0, sums_host_[2 * s]));
+    if (kind == 0) {
+      rep.eta_local[s] = lb;
+    } else {
+      const double lc = std::sqrt(std::max(0.0, sums_host_[2 * s + 1]));
+      rep.eta_local[s] = std::pow(lc > floor ? lb / lc : rep.conv_factor, offset) * lb;
+    }
+  }
+  return rep;
+}
+
+// ------------------------------------------------------------------ single operations
+void Solver3D::apply(int level, int op_mass, const double* x, double* y) {
+  launch3_apply(H_->lev.at(level), op_mass != 0, x, y, nullptr, A3_PLAIN, stream_);
+  KB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+}
+void Solver3D::residual(int level, const double* u, const double* b, double* r) {
+  launch3_apply(H_->lev.at(level), false, u, r, b, A3_RESIDUAL, stream_);
+  KB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+}
+void Solver3D::gauss_seidel(int level, double* u, const double* b, int sweeps) {
+  if (level < 1) fail(KB_STRUCTURAL, "Gauss-Seidel runs on levels >= 1");
+  launch3_gs(H_->lev.at(level), u, b, sweeps, stream_);
+  KB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+}
+void Solver3D::restrict_to(int fine_level, const double* r, double* rc) {
+  if (fine_level < 1) fail(KB_STRUCTURAL, "restriction below level 0");
+  launch3_owner_mask(H_->lev.at(fine_level), r, est_c_, stream_);
+  launch3_restrict(H_->lev.at(fine_level), H_->lev.at(fine_level - 1), est_c_, rc, 0, stream_);
+  KB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+}
+void Solver3D::prolongate(int coarse_level, const double* c, double* f) {
+  if (coarse_level + 1 > L_) fail(KB_STRUCTURAL, "prolongation beyond the finest level");
+  launch3_prolong(H_->lev.at(coarse_level), H_->lev.at(coarse_level + 1), c, f, P3_ASSIGN, stream_);
+  KB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+}
+void Solver3D::cg_level0(double* u, const double* b) {
+  KB_CUDA_CHECK(cudaMemsetAsync(status_, 0, sizeof(DevStatus), stream_));
+  launch3_cg0(H_->lev.at(0), u, b, cg_scratch_, {cfg_.coarse_rel_tol, cfg_.coarse_abs_floor, cfg_.coarse_max_iter},
+              status_, stream_);
+  sync_and_check();
+}
+double Solver3D::dot_unique(int level, const double* a, const double* b) {
+  launch3_dot(H_->lev.at(level), a, b, dot_partial_, dot_out_, stream_);
+  double out = 0.0;
+  KB_CUDA_CHECK(cudaMemcpyAsync(&out, dot_out_, 8, cudaMemcpyDeviceToHost, stream_));
+  KB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+  return out;
+}
+void Solver3D::interface_sync(int level, double* f, int additive) {
+  launch3_sync(H_->lev.at(level), f, additive, stream_);
+  KB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+}
+
+}  // namespace kb

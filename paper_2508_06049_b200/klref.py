@@ -71,6 +71,7 @@ UNSCALED, SCALED = 0, 1
 SYNC_REPLACE, SYNC_ADDITIVE = 0, 1
 STATE_U, STATE_B, STATE_W = 0, 1, 2
 PROBLEM_ZERO, PROBLEM_SIN2D, PROBLEM_LSHAPE = 0, 1, 2
+PROBLEM_SIN3D, PROBLEM_GAUSS3D, PROBLEM_SERIES3D = 3, 4, 5
 MARK_TOP_FRACTION, MARK_HALF_MAX = 0, 1
 KERNEL_ALL, KERNEL_GS, KERNEL_RESIDUAL, KERNEL_RESTRICT, KERNEL_PROLONG = -1, 0, 1, 2, 3
 KERNEL_RHS, KERNEL_CG0, KERNEL_ESTIMATE, KERNEL_OTHER = 4, 5, 6, 7
@@ -121,6 +122,8 @@ SIGNATURES = {
     "klref_hierarchy_element_matrices": (_I, [_P, _I, _I, _PD, _PD]),
     "klref_problem_create": (_I, [_I, _PP]),
     "klref_problem_create_host": (_I, [_P, _P, _P, _PP]),
+    "klref_problem_create_host3": (_I, [_P, _P, _P, _PP]),
+    "klref_problem_set_params": (_I, [_P, _PD, _I]),
     "klref_problem_destroy": (None, [_P]),
     "klref_solver_config_default": (None, [C.POINTER(SolverConfigC)]),
     "klref_solver_create": (_I, [_P, _P, C.POINTER(SolverConfigC), _PP]),
@@ -371,11 +374,14 @@ class GridFunction(_Handle):
 class Problem(_Handle):
     _destroy = "klref_problem_destroy"
 
-    def __init__(self, kind: int):
+    def __init__(self, kind: int, params: Optional[Sequence[float]] = None):
         out = C.c_void_p()
         _check(lib().klref_problem_create(kind, C.byref(out)))
         super().__init__(out.value)
         self.kind = kind
+        if params is not None:
+            p = np.ascontiguousarray(params, dtype=np.float64)
+            _check(lib().klref_problem_set_params(self.ptr, _dptr(p), p.size))
 
 
 @dataclass
