@@ -38,6 +38,10 @@ static void cvert(int ty, int r, int* d) {
   for (int q = 0; q < r; ++q)
     for (int a = 0; a < 3; ++a) d[a] += STEP[KUHN[ty][q]][a];
 }
+/* boundary signature of a lattice node: which of the faces i = 0, j = 0, k = 0, w0 = 0 it lies on */
+static int sig_of(int n, int i, int j, int k) {
+  return (i == 0) | ((j == 0) << 1) | ((k == 0) << 2) | ((i + j + k == n) << 3);
+}
 static int dirix(int a, int b, int c) {
   for (int d = 0; d < 15; ++d)
     if (DIR[d][0] == a && DIR[d][1] == b && DIR[d][2] == c) return d;
@@ -57,6 +61,7 @@ typedef struct {
   unsigned char *flag; /* bit0 boundary, bit1 domain, bit2 owner */
   double *K, *Mm;  /* 96 per macro */
   double *stK, *stM; /* 15 per macro */
+  double *psK, *psM; /* partial stencils of lattice-boundary nodes: 16 signatures x 15 per macro */
   double *gx, *gy, *gz; /* per copy: node coordinates (owner's for shared nodes) */
 } o3lev;
 
@@ -117,6 +122,7 @@ void o3_free(o3h* h) {
     free(v->gptr); free(v->mslot); free(v->midx); free(v->mi); free(v->mj); free(v->mk);
     free(v->gdom); free(v->gcol); free(v->gdiag); free(v->ncol); free(v->gid); free(v->flag);
     free(v->K); free(v->Mm); free(v->stK); free(v->stM); free(v->gx); free(v->gy); free(v->gz);
+    free(v->psK); free(v->psM);
   }
   free(h->tet); free(h->xyz); free(h);
 }
@@ -354,26 +360,46 @@ o3h* o3_build(int nv, const double* xyz, int ne, const int* tet_in, int L) {
             lv->stM[15 * s + d] += lv->Mm[96 * s + 16 * ty + 4 * r + c];
           }
     }
+    /* partial stencils: for every signature, from the first node (lattice order)
+     * carrying it, the sum over its existing cells (type, role, column order) */
+    lv->psK = calloc(240 * (size_t)ne, sizeof(double));
+    lv->psM = calloc(240 * (size_t)ne, sizeof(double));
+    for (int s = 0; s < ne; ++s) {
+      int done = 0;
+      for (int k = 0; k <= n; ++k)
+        for (int j = 0; j <= n - k; ++j)
+          for (int i = 0; i <= n - k - j; ++i) {
+            const int sg = sig_of(n, i, j, k);
+            if (sg == 0 || ((done >> sg) & 1)) continue;
+            done |= 1 << sg;
+            double* pk = lv->psK + 240 * (size_t)s + 15 * sg;
+            double* pm = lv->psM + 240 * (size_t)s + 15 * sg;
+            for (int ty = 0; ty < 6; ++ty)
+              for (int r = 0; r < 4; ++r) {
+                int dr[3], ok = 1;
+                cvert(ty, r, dr);
+                for (int c = 0; c < 4 && ok; ++c) {
+                  int dc[3];
+                  cvert(ty, c, dc);
+                  ok = inl(n, i - dr[0] + dc[0], j - dr[1] + dc[1], k - dr[2] + dc[2]);
+                }
+                if (!ok) continue;
+                for (int c = 0; c < 4; ++c) {
+                  int dc[3];
+                  cvert(ty, c, dc);
+                  const int d = dirix(dc[0] - dr[0], dc[1] - dr[1], dc[2] - dr[2]);
+                  pk[d] += lv->K[96 * s + 16 * ty + 4 * r + c];
+                  pm[d] += lv->Mm[96 * s + 16 * ty + 4 * r + c];
+                }
+              }
+          }
+    }
     /* group diagonals */
     lv->gdiag = calloc(ng, sizeof(double));
     for (int g = 0; g < ng; ++g) {
       double diag = 0.0;
-      for (int q = lv->gptr[g]; q < lv->gptr[g + 1]; ++q) {
-        const int s = lv->mslot[q], i = lv->mi[q], j = lv->mj[q], k = lv->mk[q];
-        double d = 0.0;
-        for (int ty = 0; ty < 6; ++ty)
-          for (int r = 0; r < 4; ++r) {
-            int dr[3], ok = 1;
-            cvert(ty, r, dr);
-            for (int c = 0; c < 4 && ok; ++c) {
-              int dc[3];
-              cvert(ty, c, dc);
-              ok = inl(n, i - dr[0] + dc[0], j - dr[1] + dc[1], k - dr[2] + dc[2]);
-            }
-            if (ok) d += lv->K[96 * s + 16 * ty + 5 * r];
-          }
-        diag += d;
-      }
+      for (int q = lv->gptr[g]; q < lv->gptr[g + 1]; ++q)
+        diag += lv->psK[240 * (size_t)lv->mslot[q] + 15 * sig_of(n, lv->mi[q], lv->mj[q], lv->mk[q])];
       lv->gdiag[g] = diag;
     }
     /* node coordinates, shared nodes from their owner */
@@ -405,52 +431,29 @@ o3h* o3_build(int nv, const double* xyz, int ne, const int* tet_in, int L) {
 }
 
 /* ---------------- operators */
-/* partial row of node (i,j,k) of macro s: all cells (type, role r) present in the macro */
-static double partial_full(const o3lev* lv, const double* Kt, int s, int i, int j, int k, const double* x) {
-  const int n = lv->n, S = lv->S;
-  const double* xm = x + (size_t)s * S;
-  double acc = 0.0;
-  for (int ty = 0; ty < 6; ++ty)
-    for (int r = 0; r < 4; ++r) {
-      int dr[3], vi[4], ok = 1;
-      cvert(ty, r, dr);
-      for (int c = 0; c < 4 && ok; ++c) {
-        int dc[3];
-        cvert(ty, c, dc);
-        const int a = i - dr[0] + dc[0], b = j - dr[1] + dc[1], cc = k - dr[2] + dc[2];
-        ok = inl(n, a, b, cc);
-        if (ok) vi[c] = lat3(n, a, b, cc);
-      }
-      if (!ok) continue;
-      const double* Kr = Kt + 96 * s + 16 * ty + 4 * r;
-      acc = acc + (((Kr[0] * xm[vi[0]] + Kr[1] * xm[vi[1]]) + Kr[2] * xm[vi[2]]) + Kr[3] * xm[vi[3]]);
-    }
+/* partial row of lattice-boundary node (i,j,k) of macro s: its signature's
+ * partial stencil over the neighbours inside the macro, centre first */
+static double partial_full(const o3lev* lv, const double* ps_all, int s, int i, int j, int k, const double* x) {
+  const int n = lv->n;
+  const double* xm = x + (size_t)s * lv->S;
+  const double* ps = ps_all + 240 * (size_t)s + 15 * sig_of(n, i, j, k);
+  double acc = ps[0] * xm[lat3(n, i, j, k)];
+  for (int d = 1; d < 15; ++d) {
+    const int a = i + DIR[d][0], b = j + DIR[d][1], c = k + DIR[d][2];
+    if (inl(n, a, b, c)) acc = acc + ps[d] * xm[lat3(n, a, b, c)];
+  }
   return acc;
 }
 /* off-diagonal part (Gauss-Seidel) */
 static double partial_off(const o3lev* lv, int s, int i, int j, int k, const double* x) {
-  const int n = lv->n, S = lv->S;
-  const double* xm = x + (size_t)s * S;
+  const int n = lv->n;
+  const double* xm = x + (size_t)s * lv->S;
+  const double* ps = lv->psK + 240 * (size_t)s + 15 * sig_of(n, i, j, k);
   double o = 0.0;
-  for (int ty = 0; ty < 6; ++ty)
-    for (int r = 0; r < 4; ++r) {
-      int dr[3], vi[4], ok = 1;
-      cvert(ty, r, dr);
-      for (int c = 0; c < 4 && ok; ++c) {
-        int dc[3];
-        cvert(ty, c, dc);
-        const int a = i - dr[0] + dc[0], b = j - dr[1] + dc[1], cc = k - dr[2] + dc[2];
-        ok = inl(n, a, b, cc);
-        if (ok) vi[c] = lat3(n, a, b, cc);
-      }
-      if (!ok) continue;
-      const double* Kr = lv->K + 96 * s + 16 * ty + 4 * r;
-      double v[3], kk[3];
-      int q = 0;
-      for (int c = 0; c < 4; ++c)
-        if (c != r) { v[q] = xm[vi[c]]; kk[q] = Kr[c]; ++q; }
-      o = o + ((kk[0] * v[0] + kk[1] * v[1]) + kk[2] * v[2]);
-    }
+  for (int d = 1; d < 15; ++d) {
+    const int a = i + DIR[d][0], b = j + DIR[d][1], c = k + DIR[d][2];
+    if (inl(n, a, b, c)) o = o + ps[d] * xm[lat3(n, a, b, c)];
+  }
   return o;
 }
 static double stencil_apply(const o3lev* lv, const double* st, int s, int i, int j, int k, const double* x,
@@ -474,7 +477,7 @@ static double stencil_apply(const o3lev* lv, const double* st, int s, int i, int
 void o3_apply(const o3h* h, int l, int mass, const double* x, double* y) {
   const o3lev* lv = &h->lv[l];
   const int n = lv->n, S = lv->S;
-  const double* Kt = mass ? lv->Mm : lv->K;
+  const double* Kt = mass ? lv->psM : lv->psK;
   const double* stt = mass ? lv->stM : lv->stK;
   for (int s = 0; s < h->M; ++s)
     for (int k = 1; k <= n; ++k)
@@ -593,14 +596,21 @@ void o3_restrict(const o3h* h, int lf, const double* f, double* c) {
   }
 }
 
-/* owner inner product: groups in order (owner copy), then interior nodes per macro */
+/* owner inner product: the terms -- groups in order (owner copy), then the
+ * interior nodes per macro in lattice order -- summed in chunks of 32
+ * consecutive terms (sequentially), then the chunk sums sequentially */
+typedef struct { double total, chunk; int count; } o3acc;
+static void acc_add(o3acc* a, double t) {
+  a->chunk += t;
+  if (++a->count == 32) { a->total += a->chunk; a->chunk = 0.0; a->count = 0; }
+}
 double o3_dot(const o3h* h, int l, const double* a, const double* b) {
   const o3lev* lv = &h->lv[l];
   const int n = lv->n, S = lv->S;
-  double s = 0.0;
+  o3acc acc = {0.0, 0.0, 0};
   for (int g = 0; g < lv->ng; ++g) {
     const size_t o = (size_t)lv->mslot[lv->gptr[g]] * S + lv->midx[lv->gptr[g]];
-    s += a[o] * b[o];
+    acc_add(&acc, a[o] * b[o]);
   }
   for (int m = 0; m < h->M; ++m)
     for (int k = 1; k <= n; ++k)
@@ -608,9 +618,10 @@ double o3_dot(const o3h* h, int l, const double* a, const double* b) {
         for (int i = 1; i <= n - k - j; ++i)
           if (n - i - j - k > 0) {
             const size_t o = (size_t)m * S + lat3(n, i, j, k);
-            s += a[o] * b[o];
+            acc_add(&acc, a[o] * b[o]);
           }
-  return s;
+  if (acc.count) acc.total += acc.chunk;
+  return acc.total;
 }
 
 /* ---------------- problems (host glibc), RHS */

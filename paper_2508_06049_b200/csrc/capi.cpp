@@ -30,7 +30,7 @@ struct klref_hierarchy_s {
 struct klref_problem_s {
   kb::Problem2D p;
   kb::Problem3D p3;
-  int dims = 2;  // bit mask of the dimensions this problem is defined for (1: 2-d, 2: 3-d)
+  int dims = 1;  // bit mask of the dimensions this problem is defined for (1: 2-d, 2: 3-d)
 };
 struct klref_solver_s {
   std::unique_ptr<kb::Solver2D> s;

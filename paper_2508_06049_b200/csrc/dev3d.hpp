@@ -31,6 +31,14 @@ struct DevLevel3D {
   const double* inv_c;
   const int* pat_color;        // 8 per macro
   const int* own_dot;          // group owner copy offsets (dot order)
+  const double* psK;           // boundary partial stencils: 16 signatures x 15 per macro
+  const double* psM;
+  // level-0 CG on the unique macro-vertex values (level 0 only): per group a
+  // member range, per member a term range of (coefficient, vertex) pairs
+  const int* cg_gmem;          // ng + 1
+  const int* cg_mterm;         // members + 1
+  const double* cg_coef;
+  const int* cg_vid;
 };
 
 enum Apply3Mode : int {

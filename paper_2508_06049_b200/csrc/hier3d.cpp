@@ -355,40 +355,75 @@ Hierarchy3D Hierarchy3D::build(const Mesh3D& mesh, int max_level) {
             }
         lv.inv_c[s] = 1.0 / st[0];
       }
-      // group diagonals: per member sum of the diagonal entries of its existing cells
-      lv.grp_diag.assign(nG, 0.0);
-      for (long long g = 0; g < nG; ++g) {
-        double diag = 0.0;
-        for (int q = lv.grp_ptr[g]; q < lv.grp_ptr[g + 1]; ++q) {
-          const int s = lv.mem_slot[q];
-          int i = 0, j = 0, k = 0;
-          {  // decode the lattice index
-            int idx = lv.mem_idx[q];
-            k = 0;
-            while (idx >= tet_size(n) - tet_size(n - k - 1)) ++k;
-            const int rem = idx - (tet_size(n) - tet_size(n - k));
-            const int m2 = n - k;
-            j = 0;
-            while (rem >= lattice_index(m2, 0, j + 1) && j < m2) ++j;
-            i = rem - lattice_index(m2, 0, j);
-          }
-          double d = 0.0;
-          for (int ty = 0; ty < 6; ++ty)
-            for (int r = 0; r < 4; ++r) {
-              int di, dj, dk;
-              cell_vertex(ty, r, di, dj, dk);
-              const int bi = i - di, bj = j - dj, bk = k - dk;
-              bool ok = true;
-              for (int c = 0; c < 4 && ok; ++c) {
-                int ci, cj, ck;
-                cell_vertex(ty, c, ci, cj, ck);
-                ok = in_lattice(n, bi + ci, bj + cj, bk + ck);
-              }
-              if (ok) d += lv.kstiff[96 * s + 16 * ty + 5 * r];
+      // partial stencils per boundary signature: from the first node (lattice
+      // order) carrying it, the sum over its existing cells in (type, role,
+      // column) order; every other node of that signature is checked on small
+      // levels to have the same cells
+      lv.psK.assign(240 * static_cast<size_t>(M), 0.0);
+      lv.psM.assign(240 * static_cast<size_t>(M), 0.0);
+      auto cells_of = [&](int i, int j, int k, auto&& visit) {
+        for (int ty = 0; ty < 6; ++ty)
+          for (int r = 0; r < 4; ++r) {
+            int ri, rj, rk;
+            cell_vertex(ty, r, ri, rj, rk);
+            bool ok = true;
+            for (int c = 0; c < 4 && ok; ++c) {
+              int ci, cj, ck;
+              cell_vertex(ty, c, ci, cj, ck);
+              ok = in_lattice(n, i - ri + ci, j - rj + cj, k - rk + ck);
             }
-          diag += d;
+            if (ok) visit(ty, r);
+          }
+      };
+      for (int s = 0; s < M; ++s) {
+        int done = 0;
+        std::vector<int> cellmask(16, 0);
+        for (int k = 0; k <= n; ++k)
+          for (int j = 0; j <= n - k; ++j)
+            for (int i = 0; i <= n - k - j; ++i) {
+              const int sg = boundary_signature(n, i, j, k);
+              if (sg == 0) continue;
+              int mask = 0;
+              if (!((done >> sg) & 1) || n <= 16) cells_of(i, j, k, [&](int ty, int r) { mask |= 1 << (4 * ty + r); });
+              if ((done >> sg) & 1) {
+                if (n <= 16 && mask != cellmask[sg]) fail(KB_INTERNAL, "boundary signature does not fix the cells");
+                continue;
+              }
+              done |= 1 << sg;
+              cellmask[sg] = mask;
+              double* pk = &lv.psK[240 * static_cast<size_t>(s) + 15 * sg];
+              double* pm = &lv.psM[240 * static_cast<size_t>(s) + 15 * sg];
+              cells_of(i, j, k, [&](int ty, int r) {
+                int ri, rj, rk;
+                cell_vertex(ty, r, ri, rj, rk);
+                for (int c = 0; c < 4; ++c) {
+                  int ci, cj, ck;
+                  cell_vertex(ty, c, ci, cj, ck);
+                  const int d = dir_index(ci - ri, cj - rj, ck - rk);
+                  pk[d] += lv.kstiff[96 * s + 16 * ty + 4 * r + c];
+                  pm[d] += lv.kmass[96 * s + 16 * ty + 4 * r + c];
+                }
+              });
+            }
+      }
+      // group diagonals: sum over members of the partial-stencil centres
+      lv.grp_diag.assign(nG, 0.0);
+      {
+        std::vector<int> ii(S), jj(S), kk(S);
+        for (int k = 0; k <= n; ++k)
+          for (int j = 0; j <= n - k; ++j)
+            for (int i = 0; i <= n - k - j; ++i) {
+              const int idx = lattice_index3(n, i, j, k);
+              ii[idx] = i, jj[idx] = j, kk[idx] = k;
+            }
+        for (long long g = 0; g < nG; ++g) {
+          double diag = 0.0;
+          for (int q = lv.grp_ptr[g]; q < lv.grp_ptr[g + 1]; ++q) {
+            const int idx = lv.mem_idx[q];
+            diag += lv.psK[240 * static_cast<size_t>(lv.mem_slot[q]) + 15 * boundary_signature(n, ii[idx], jj[idx], kk[idx])];
+          }
+          lv.grp_diag[g] = diag;
         }
-        lv.grp_diag[g] = diag;
       }
       // boundary groups by colour
       lv.color_grp_ptr.assign(ncol + 1, 0);

@@ -74,6 +74,9 @@ struct Level3D {
   // per macro: element matrices [type][4][4] (stiffness, mass), interior stencil, 1/s0
   std::vector<double> kstiff, kmass;     // 96 per macro each
   std::vector<double> stencil;           // 15 per macro (kDir order)
+  // partial stencils of lattice-boundary nodes, by boundary signature
+  // (i == 0 | j == 0 << 1 | k == 0 << 2 | w0 == 0 << 3): 16 x 15 per macro
+  std::vector<double> psK, psM;
   std::vector<double> inv_c;
   std::vector<int> pat_color;            // 8 per macro: colour of the parity pattern (i&1 | (j&1)<<1 | (k&1)<<2)
   std::vector<int> color_grp_ptr, color_grp;  // boundary groups by colour
@@ -86,6 +89,10 @@ struct Hierarchy3D {
   std::vector<Level3D> levels;
   static Hierarchy3D build(const Mesh3D& mesh, int max_level);
 };
+
+inline int boundary_signature(int n, int i, int j, int k) {
+  return (i == 0) | ((j == 0) << 1) | ((k == 0) << 2) | ((i + j + k == n) << 3);
+}
 
 // element matrices of one micro-tet with physical vertices p[4][3]
 void tet_matrices(const double p[4][3], double* K16, double* M16);

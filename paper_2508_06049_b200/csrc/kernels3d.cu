@@ -49,55 +49,33 @@ __device__ __forceinline__ void decode2(int m, int q, int& i, int& j) {
   i = q - lat2(m, 0, jj);
 }
 
-// full partial row of node (i,j,k) of one macro (cells in type, role order)
-__device__ double partial_full(const double* __restrict__ K, const double* __restrict__ xm, int n, int i, int j,
+__device__ __forceinline__ int sig3(int n, int i, int j, int k) {
+  return (i == 0) | ((j == 0) << 1) | ((k == 0) << 2) | ((i + j + k == n) << 3);
+}
+
+// partial row of a lattice-boundary node of one macro: its signature's partial
+// stencil over the neighbours inside the macro, centre first
+__device__ double partial_full(const double* __restrict__ ps_m, const double* __restrict__ xm, int n, int i, int j,
                                int k) {
-  double acc = 0.0;
-  for (int ty = 0; ty < 6; ++ty)
-    for (int r = 0; r < 4; ++r) {
-      const int bi = i - c_cv[ty][r][0], bj = j - c_cv[ty][r][1], bk = k - c_cv[ty][r][2];
-      int vi[4];
-      bool ok = true;
+  const double* ps = ps_m + 15 * sig3(n, i, j, k);
+  double acc = ps[0] * xm[lat3(n, i, j, k)];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int a = bi + c_cv[ty][c][0], b = bj + c_cv[ty][c][1], cc = bk + c_cv[ty][c][2];
-        ok = ok && inl(n, a, b, cc);
-        vi[c] = ok ? lat3(n, a, b, cc) : 0;
-      }
-      if (!ok) continue;
-      const double* Kr = K + 16 * ty + 4 * r;
-      acc = acc + (((Kr[0] * xm[vi[0]] + Kr[1] * xm[vi[1]]) + Kr[2] * xm[vi[2]]) + Kr[3] * xm[vi[3]]);
-    }
+  for (int d = 1; d < 15; ++d) {
+    const int a = i + c_dir[d][0], b = j + c_dir[d][1], c = k + c_dir[d][2];
+    if (inl(n, a, b, c)) acc = acc + ps[d] * xm[lat3(n, a, b, c)];
+  }
   return acc;
 }
 
-// off-diagonal part of the partial row (Gauss-Seidel)
-__device__ double partial_off3(const double* __restrict__ K, const double* xm, int n, int i, int j, int k) {
+// off-diagonal part (Gauss-Seidel)
+__device__ double partial_off3(const double* __restrict__ ps_m, const double* xm, int n, int i, int j, int k) {
+  const double* ps = ps_m + 15 * sig3(n, i, j, k);
   double o = 0.0;
-  for (int ty = 0; ty < 6; ++ty)
-    for (int r = 0; r < 4; ++r) {
-      const int bi = i - c_cv[ty][r][0], bj = j - c_cv[ty][r][1], bk = k - c_cv[ty][r][2];
-      int vi[4];
-      bool ok = true;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int a = bi + c_cv[ty][c][0], b = bj + c_cv[ty][c][1], cc = bk + c_cv[ty][c][2];
-        ok = ok && inl(n, a, b, cc);
-        vi[c] = ok ? lat3(n, a, b, cc) : 0;
-      }
-      if (!ok) continue;
-      const double* Kr = K + 16 * ty + 4 * r;
-      double v[3], kk[3];
-      int q = 0;
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        if (c != r) {
-          v[q] = xm[vi[c]];
-          kk[q] = Kr[c];
-          ++q;
-        }
-      o = o + ((kk[0] * v[0] + kk[1] * v[1]) + kk[2] * v[2]);
-    }
+  for (int d = 1; d < 15; ++d) {
+    const int a = i + c_dir[d][0], b = j + c_dir[d][1], c = k + c_dir[d][2];
+    if (inl(n, a, b, c)) o = o + ps[d] * xm[lat3(n, a, b, c)];
+  }
   return o;
 }
 
@@ -139,14 +117,14 @@ __global__ void __launch_bounds__(kT) k3_apply(DevLevel3D lv, int mass, const do
   }
   const int g = (blockIdx.x - plane_blocks) * blockDim.x + threadIdx.x;
   if (g >= lv.ng) return;
-  const double* K = mass ? lv.kmass : lv.kstiff;
+  const double* K = mass ? lv.psM : lv.psK;
   const int beg = lv.grp_ptr[g], end = lv.grp_ptr[g + 1];
   double v;
   auto part = [&](int q) {
     const int s = lv.mem_slot[q];
     int i, j, k;
     unpack_ijk(lv.mem_ijk[q], i, j, k);
-    return partial_full(K + 96 * s, x + static_cast<size_t>(s) * S, n, i, j, k);
+    return partial_full(K + 240 * s, x + static_cast<size_t>(s) * S, n, i, j, k);
   };
   if (end - beg == 1) {
     v = part(beg);
@@ -189,7 +167,7 @@ __global__ void __launch_bounds__(kT) k3_gs_groups(DevLevel3D lv, double* u, con
       const int s = lv.mem_slot[q];
       int i, j, k;
       unpack_ijk(lv.mem_ijk[q], i, j, k);
-      off = off + partial_off3(lv.kstiff + 96 * s, u + static_cast<size_t>(s) * S, n, i, j, k);
+      off = off + partial_off3(lv.psK + 240 * s, u + static_cast<size_t>(s) * S, n, i, j, k);
     }
     val = (b[own] - off) / lv.grp_diag[g];
   }
@@ -351,107 +329,111 @@ __global__ void __launch_bounds__(kT) k3_set_boundary(DevLevel3D lv, double* f, 
 }
 
 // ---------------------------------------------------------------- level-0 CG (one CTA)
-__device__ double seq_dot3(const DevLevel3D& lv, const double* a, const double* b, bool zero_dom) {
-  double s = 0.0;
-  for (int g = 0; g < lv.ng; ++g) {
-    const int o = lv.own_dot[g];
-    double x = a[o], y = b[o];
-    if (zero_dom && lv.grp_domain[g]) x = y = 0.0;
-    s += x * y;
-  }
-  return s;
-}
-
-// y = A x on level 0 (vertex groups only); mode 0 plain with domain rows 0, 1 residual
-__device__ void cg_apply0(const DevLevel3D& lv, const double* x, double* y, const double* b, int residual) {
+// cg_level0 (proj/src/multigrid.cpp:198-229 sequence) on the unique
+// macro-vertex values held in shared memory; operator rows from the level-0
+// program (the members' partial stencils in slot order, the same arithmetic
+// as the copy-based apply), inner products in chunks of 32 terms then over
+// the chunk sums (the 3-d dot order, oracle o3_dot).
+__device__ void cg0_apply(const DevLevel3D& lv, const double* x, double* y, const double* b,
+                          const unsigned char* dom, int residual) {
   for (int g = threadIdx.x; g < lv.ng; g += blockDim.x) {
-    const int beg = lv.grp_ptr[g], end = lv.grp_ptr[g + 1];
-    double v;
-    auto part = [&](int q) {
-      const int s = lv.mem_slot[q];
-      int i, j, k;
-      unpack_ijk(lv.mem_ijk[q], i, j, k);
-      return partial_full(lv.kstiff + 96 * s, x + static_cast<size_t>(s) * lv.S, lv.n, i, j, k);
-    };
-    if (end - beg == 1) {
-      v = part(beg);
-    } else {
-      v = 0.0;
-      for (int q = beg; q < end; ++q) v += part(q);
+    const int m0 = lv.cg_gmem[g], m1 = lv.cg_gmem[g + 1];
+    double v = 0.0;
+    for (int q = m0; q < m1; ++q) {
+      const int t0 = lv.cg_mterm[q], t1 = lv.cg_mterm[q + 1];
+      double acc = lv.cg_coef[t0] * x[lv.cg_vid[t0]];
+      for (int t = t0 + 1; t < t1; ++t) acc = acc + lv.cg_coef[t] * x[lv.cg_vid[t]];
+      v = (m1 - m0 == 1) ? acc : v + acc;
     }
-    const bool dom = lv.grp_domain[g];
-    for (int q = beg; q < end; ++q) {
-      int i, j, k;
-      unpack_ijk(lv.mem_ijk[q], i, j, k);
-      const size_t off = static_cast<size_t>(lv.mem_slot[q]) * lv.S + lat3(lv.n, i, j, k);
-      y[off] = dom ? 0.0 : (residual ? b[off] - v : v);
-    }
+    y[g] = dom[g] ? 0.0 : (residual ? b[g] - v : v);
   }
 }
 
-__global__ void k3_cg0(DevLevel3D lv, double* u, const double* b, double* r, double* p, double* ap, CgParams prm,
-                       DevStatus* status) {
-  const int total = lv.M * lv.S;
-  __shared__ double sh_rr, sh_alpha, sh_beta, sh_tol;
-  __shared__ int sh_go, sh_it;
-  cg_apply0(lv, u, r, b, 1);
+__device__ double cg0_dot(int ng, const double* a, const double* b, const unsigned char* dom, bool zero_dom,
+                          double* chunks) {
+  const int nch = (ng + 31) / 32;
   __syncthreads();
-  for (int q = threadIdx.x; q < total; q += blockDim.x) p[q] = r[q];
+  for (int c = threadIdx.x; c < nch; c += blockDim.x) {
+    double s = 0.0;
+    for (int g = 32 * c; g < min(ng, 32 * c + 32); ++g) {
+      double x = a[g], y = b[g];
+      if (zero_dom && dom[g]) x = y = 0.0;
+      s += x * y;
+    }
+    chunks[c] = s;
+  }
   __syncthreads();
+  __shared__ double total;
   if (threadIdx.x == 0) {
-    sh_rr = seq_dot3(lv, r, r, false);
-    const double bn = sqrt(fmax(0.0, seq_dot3(lv, b, b, true)));
-    const double a = prm.rel_tol * bn;
-    sh_tol = a < prm.abs_floor ? prm.abs_floor : a;
-    sh_go = sqrt(sh_rr) > sh_tol;
-    sh_it = 0;
+    double t = 0.0;
+    for (int c = 0; c < nch; ++c) t += chunks[c];
+    total = t;
   }
   __syncthreads();
-  while (sh_go) {
-    if (threadIdx.x == 0 && ++sh_it > prm.max_iter) {
-      if (status->code == 0) {
+  return total;
+}
+
+__global__ void __launch_bounds__(1024) k3_cg0(DevLevel3D lv, double* uc, const double* bc, CgParams prm,
+                                               DevStatus* status) {
+  extern __shared__ double sm[];
+  const int ng = lv.ng;
+  double* u = sm;
+  double* b = u + ng;
+  double* r = b + ng;
+  double* p = r + ng;
+  double* ap = p + ng;
+  double* chunks = ap + ng;
+  unsigned char* dom = reinterpret_cast<unsigned char*>(chunks + (ng + 31) / 32);
+  for (int g = threadIdx.x; g < ng; g += blockDim.x) {
+    u[g] = uc[lv.own_dot[g]];
+    b[g] = bc[lv.own_dot[g]];
+    dom[g] = lv.grp_domain[g];
+  }
+  __syncthreads();
+  cg0_apply(lv, u, r, b, dom, 1);
+  __syncthreads();
+  for (int g = threadIdx.x; g < ng; g += blockDim.x) p[g] = r[g];
+  double rr = cg0_dot(ng, r, r, dom, false, chunks);
+  const double bn = sqrt(fmax(0.0, cg0_dot(ng, b, b, dom, true, chunks)));
+  const double tol = prm.rel_tol * bn < prm.abs_floor ? prm.abs_floor : prm.rel_tol * bn;
+  int it = 0;
+  while (sqrt(rr) > tol) {
+    if (++it > prm.max_iter) {
+      if (threadIdx.x == 0 && status->code == 0) {
         status->code = 1;
-        status->residual = sqrt(sh_rr);
+        status->residual = sqrt(rr);
       }
-      sh_go = 0;
+      break;
     }
-    __syncthreads();
-    if (!sh_go) break;
-    cg_apply0(lv, p, ap, nullptr, 0);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const double pap = seq_dot3(lv, p, ap, false);
-      if (pap <= 0.0) {
-        if (status->code == 0) {
-          status->code = 2;
-          status->residual = sqrt(sh_rr);
-        }
-        sh_go = 0;
-      } else {
-        sh_alpha = sh_rr / pap;
+    cg0_apply(lv, p, ap, nullptr, dom, 0);
+    const double pap = cg0_dot(ng, p, ap, dom, false, chunks);
+    if (pap <= 0.0) {
+      if (threadIdx.x == 0 && status->code == 0) {
+        status->code = 2;
+        status->residual = sqrt(rr);
       }
+      break;
     }
-    __syncthreads();
-    if (!sh_go) break;
-    const double alpha = sh_alpha;
-    for (int q = threadIdx.x; q < total; q += blockDim.x) {
-      u[q] = u[q] + alpha * p[q];
-      r[q] = r[q] + (-alpha) * ap[q];
+    const double alpha = rr / pap;
+    for (int g = threadIdx.x; g < ng; g += blockDim.x) {
+      u[g] = u[g] + alpha * p[g];
+      r[g] = r[g] + (-alpha) * ap[g];
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const double rn = seq_dot3(lv, r, r, false);
-      sh_beta = rn / sh_rr;
-      sh_rr = rn;
-    }
-    __syncthreads();
-    const double beta = sh_beta;
-    for (int q = threadIdx.x; q < total; q += blockDim.x) p[q] = p[q] * beta + r[q];
-    __syncthreads();
-    if (threadIdx.x == 0) sh_go = sqrt(sh_rr) > sh_tol;
+    const double rn = cg0_dot(ng, r, r, dom, false, chunks);
+    const double beta = rn / rr;
+    rr = rn;
+    for (int g = threadIdx.x; g < ng; g += blockDim.x) p[g] = p[g] * beta + r[g];
     __syncthreads();
   }
-  if (threadIdx.x == 0) status->iters = sh_it;
+  if (threadIdx.x == 0) status->iters = it;
+  __syncthreads();
+  // scatter to every copy
+  for (int g = threadIdx.x; g < ng; g += blockDim.x)
+    for (int q = lv.grp_ptr[g]; q < lv.grp_ptr[g + 1]; ++q) {
+      int i, j, k;
+      unpack_ijk(lv.mem_ijk[q], i, j, k);
+      uc[static_cast<size_t>(lv.mem_slot[q]) * lv.S + lat3(lv.n, i, j, k)] = u[g];
+    }
 }
 
 // ---------------------------------------------------------------- estimator
@@ -686,9 +668,12 @@ void launch3_sync(const DevLevel3D& lv, double* f, int additive, cudaStream_t st
 
 void launch3_cg0(const DevLevel3D& lv0, double* u, const double* b, double* scratch, CgParams prm,
                  DevStatus* status, cudaStream_t st) {
+  (void)scratch;
   init_constants();
-  const size_t N = static_cast<size_t>(lv0.M) * lv0.S;
-  k3_cg0<<<1, kT, 0, st>>>(lv0, u, b, scratch, scratch + N, scratch + 2 * N, prm, status);
+  const size_t smem = (5 * static_cast<size_t>(lv0.ng) + (lv0.ng + 31) / 32) * sizeof(double) + lv0.ng + 16;
+  if (smem > 200 * 1024) fail(KB_STRUCTURAL, "coarse mesh too large for the level-0 CG (more than ~4800 vertices)");
+  KB_CUDA_CHECK(cudaFuncSetAttribute(k3_cg0, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  k3_cg0<<<1, 1024, smem, st>>>(lv0, u, b, prm, status);
   check3("k3_cg0");
 }
 

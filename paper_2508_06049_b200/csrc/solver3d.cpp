@@ -54,6 +54,33 @@ std::unique_ptr<DeviceHierarchy3D> DeviceHierarchy3D::create(const Mesh3D& mesh,
              vb(lv.color_grp_ptr) + vb(lv.color_grp) + vb(lv.kstiff) + vb(lv.kmass) + 2 * vb(lv.stencil) +
              vb(lv.inv_c) + vb(lv.pat_color) + vb(own[l]);
   }
+  // level-0 CG program: for every vertex group, its members' partial stencils
+  // as (coefficient, global vertex) terms, centre first (level-0 groups are the
+  // macro vertices in id order)
+  std::vector<int> cg_gmem(1, 0), cg_mterm(1, 0), cg_vid;
+  std::vector<double> cg_coef;
+  {
+    const Level3D& lv = h.levels[0];
+    const int ng = static_cast<int>(lv.grp_ptr.size()) - 1;
+    for (int g = 0; g < ng; ++g) {
+      for (int q = lv.grp_ptr[g]; q < lv.grp_ptr[g + 1]; ++q) {
+        const int s = lv.mem_slot[q], idx = lv.mem_idx[q];
+        const int i = idx == 1, j = idx == 2, k = idx == 3;  // n = 1: lattice index = local vertex
+        const double* ps = &lv.psK[240 * static_cast<size_t>(s) + 15 * boundary_signature(1, i, j, k)];
+        for (int dd = 0; dd < 15; ++dd) {
+          const int a = i + kDir[dd][0], b = j + kDir[dd][1], c = k + kDir[dd][2];
+          if (a < 0 || b < 0 || c < 0 || a + b + c > 1) continue;
+          cg_coef.push_back(ps[dd]);
+          cg_vid.push_back(h.mesh.tet[s][lattice_index3(1, a, b, c)]);
+        }
+        cg_mterm.push_back(static_cast<int>(cg_coef.size()));
+      }
+      cg_gmem.push_back(static_cast<int>(cg_mterm.size()) - 1);
+      if (lv.grp_ptr[g + 1] == lv.grp_ptr[g]) fail(KB_STRUCTURAL, "macro vertex used by no tetrahedron");
+    }
+    bytes += r256(cg_gmem.size() * 4) + r256(cg_mterm.size() * 4) + r256(cg_vid.size() * 4) + r256(cg_coef.size() * 8);
+  }
+  for (int l = 0; l <= h.L; ++l) bytes += 2 * r256(h.levels[l].psK.size() * 8);
   d->arena.reserve(bytes + 4096);
   for (int l = 0; l <= h.L; ++l) {
     const Level3D& lv = h.levels[l];
@@ -88,6 +115,14 @@ std::unique_ptr<DeviceHierarchy3D> DeviceHierarchy3D::create(const Mesh3D& mesh,
     dl.inv_c = d->arena.upload(lv.inv_c);
     dl.pat_color = d->arena.upload(lv.pat_color);
     dl.own_dot = d->arena.upload(own[l]);
+    dl.psK = d->arena.upload(lv.psK);
+    dl.psM = d->arena.upload(lv.psM);
+    if (l == 0) {
+      dl.cg_gmem = d->arena.upload(cg_gmem);
+      dl.cg_mterm = d->arena.upload(cg_mterm);
+      dl.cg_coef = d->arena.upload(cg_coef);
+      dl.cg_vid = d->arena.upload(cg_vid);
+    }
     d->lev.push_back(dl);
   }
   return d;
