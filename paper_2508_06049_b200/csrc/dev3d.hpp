@@ -65,8 +65,9 @@ void launch3_sync(const DevLevel3D& lv, double* f, int additive, cudaStream_t st
 void launch3_cg0(const DevLevel3D& lv0, double* u, const double* b, double* scratch, CgParams prm,
                  DevStatus* status, cudaStream_t st);
 // per-macro sums of e^T M e for e_base = uL - wb and e_coarser = uL - wc (all on level L)
+// part: scratch of 2 M (n + 1) doubles
 void launch3_estimate(const DevLevel3D& lv, const double* uL, const double* wb, const double* wc, double* sums,
-                      cudaStream_t st);
+                      double* part, cudaStream_t st);
 void launch3_dot(const DevLevel3D& lv, const double* a, const double* b, double* partial, double* out,
                  cudaStream_t st);
 void launch3_axpy(double* y, const double* x, double alpha, std::int64_t count, cudaStream_t st);

@@ -57,12 +57,24 @@ __device__ __forceinline__ int sig3(int n, int i, int j, int k) {
 // stencil over the neighbours inside the macro, centre first
 __device__ double partial_full(const double* __restrict__ ps_m, const double* __restrict__ xm, int n, int i, int j,
                                int k) {
+  // all loads issued together (clamped to the node itself when the neighbour
+  // is outside the macro), the sum keeps the specification's order and terms
   const double* ps = ps_m + 15 * sig3(n, i, j, k);
-  double acc = ps[0] * xm[lat3(n, i, j, k)];
+  const int c0 = lat3(n, i, j, k);
+  double x[15], cf[15];
+  bool ok[15];
+#pragma unroll
+  for (int d = 0; d < 15; ++d) {
+    const int a = i + c_dir[d][0], b = j + c_dir[d][1], c = k + c_dir[d][2];
+    ok[d] = inl(n, a, b, c);
+    x[d] = xm[ok[d] ? lat3(n, a, b, c) : c0];
+    cf[d] = ps[d];
+  }
+  double acc = cf[0] * x[0];
 #pragma unroll
   for (int d = 1; d < 15; ++d) {
-    const int a = i + c_dir[d][0], b = j + c_dir[d][1], c = k + c_dir[d][2];
-    if (inl(n, a, b, c)) acc = acc + ps[d] * xm[lat3(n, a, b, c)];
+    const double t = acc + cf[d] * x[d];
+    acc = ok[d] ? t : acc;
   }
   return acc;
 }
@@ -70,11 +82,21 @@ __device__ double partial_full(const double* __restrict__ ps_m, const double* __
 // off-diagonal part (Gauss-Seidel)
 __device__ double partial_off3(const double* __restrict__ ps_m, const double* xm, int n, int i, int j, int k) {
   const double* ps = ps_m + 15 * sig3(n, i, j, k);
-  double o = 0.0;
+  const int c0 = lat3(n, i, j, k);
+  double x[15], cf[15];
+  bool ok[15];
 #pragma unroll
   for (int d = 1; d < 15; ++d) {
     const int a = i + c_dir[d][0], b = j + c_dir[d][1], c = k + c_dir[d][2];
-    if (inl(n, a, b, c)) o = o + ps[d] * xm[lat3(n, a, b, c)];
+    ok[d] = inl(n, a, b, c);
+    x[d] = xm[ok[d] ? lat3(n, a, b, c) : c0];
+    cf[d] = ps[d];
+  }
+  double o = 0.0;
+#pragma unroll
+  for (int d = 1; d < 15; ++d) {
+    const double t = o + cf[d] * x[d];
+    o = ok[d] ? t : o;
   }
   return o;
 }
@@ -191,14 +213,14 @@ __device__ __forceinline__ unsigned cluster_id_x() {
   asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
   return r;
 }
-constexpr int kCluster = 8;
-
-// interior phase: one cluster of kCluster CTAs per macro, colours in order,
+// interior phase: one cluster of CL CTAs per macro (CL grows with the
+// lattice: 1 for n <= 8 ... 8 for n >= 64), colours in order,
 // a cluster barrier between colours; nodes of colour c are the parity
 // patterns p with pat_color[m][p] == c (enumerated over their bounding box)
+template <int CL>
 __global__ void __launch_bounds__(kT) k3_gs_interior(DevLevel3D lv, double* u, const double* __restrict__ b) {
-  const int m = cluster_id_x();
-  const int r = cluster_rank();
+  const int m = CL == 1 ? static_cast<int>(blockIdx.x) : static_cast<int>(cluster_id_x());
+  const int r = CL == 1 ? 0 : static_cast<int>(cluster_rank());
   const int n = lv.n, S = lv.S;
   const double* st = lv.stK + 15 * m;
   double s[15];
@@ -213,7 +235,7 @@ __global__ void __launch_bounds__(kT) k3_gs_interior(DevLevel3D lv, double* u, c
     for (int p = 0; p < 8; ++p) {
       if (__ldg(lv.pat_color + 8 * m + p) != c) continue;
       const int pi = p & 1, pj = (p >> 1) & 1, pk = (p >> 2) & 1;
-      for (int v = threadIdx.x + kT * r; v < box; v += kT * kCluster) {
+      for (int v = threadIdx.x + kT * r; v < box; v += kT * CL) {
         const int a = v % A, bb = (v / A) % A, cc = v / (A * A);
         const int i = 2 * a + pi, j = 2 * bb + pj, k = 2 * cc + pk;
         if (!interior3(n, i, j, k)) continue;
@@ -225,7 +247,10 @@ __global__ void __launch_bounds__(kT) k3_gs_interior(DevLevel3D lv, double* u, c
         __stcg(um + idx, (__ldg(bm + idx) - acc) * inv_c);
       }
     }
-    cluster_sync_all();
+    if (CL == 1)
+      __syncthreads();
+    else
+      cluster_sync_all();
   }
 }
 
@@ -437,21 +462,22 @@ __global__ void __launch_bounds__(1024) k3_cg0(DevLevel3D lv, double* uc, const 
 }
 
 // ---------------------------------------------------------------- estimator
+// one block per (macro, base plane k); per-block partial sums, reduced per
+// macro in plane order by k3_estimate_reduce
 __global__ void __launch_bounds__(kT) k3_estimate(DevLevel3D lv, const double* __restrict__ uL,
                                                   const double* __restrict__ wb, const double* __restrict__ wc,
-                                                  double* sums) {
-  const int m = blockIdx.x;
+                                                  double* part) {
   const int n = lv.n, S = lv.S;
+  const int m = blockIdx.x / (n + 1), k = blockIdx.x - m * (n + 1);
+  const int m2 = n - k;
+  const int np = (m2 + 1) * (m2 + 2) / 2;
   const size_t mo = static_cast<size_t>(m) * S;
   const double* Mt = lv.kmass + 96 * m;
   double qb = 0.0, qc = 0.0;
-  for (int v = threadIdx.x; v < S * 6; v += blockDim.x) {
-    const int ty = v % 6, idx = v / 6;
-    // decode the base node of lattice index idx
-    int k = 0;
-    while (idx >= tsz(n) - tsz(n - k - 1)) ++k;
+  for (int v = threadIdx.x; v < 6 * np; v += blockDim.x) {
+    const int ty = v % 6, q = v / 6;
     int i, j;
-    decode2(n - k, idx - (tsz(n) - tsz(n - k)), i, j);
+    decode2(m2, q, i, j);
     int vi[4];
     bool ok = true;
 #pragma unroll
@@ -489,9 +515,21 @@ __global__ void __launch_bounds__(kT) k3_estimate(DevLevel3D lv, const double* _
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    sums[2 * m] = rb[0];
-    sums[2 * m + 1] = rcs[0];
+    part[2 * static_cast<size_t>(blockIdx.x)] = rb[0];
+    part[2 * static_cast<size_t>(blockIdx.x) + 1] = rcs[0];
   }
+}
+
+__global__ void k3_estimate_reduce(int M, int planes, const double* part, double* sums) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= M) return;
+  double b = 0.0, c = 0.0;
+  for (int k = 0; k < planes; ++k) {
+    b += part[2 * (static_cast<size_t>(m) * planes + k)];
+    c += part[2 * (static_cast<size_t>(m) * planes + k) + 1];
+  }
+  sums[2 * m] = b;
+  sums[2 * m + 1] = c;
 }
 
 // ---------------------------------------------------------------- dot (owner copies + interiors)
@@ -617,18 +655,29 @@ void launch3_gs(const DevLevel3D& lv, double* u, const double* b, int sweeps, cu
       check3("k3_gs_groups");
     }
     if (lv.n < 4) continue;  // no lattice-interior nodes
+    const int cl = lv.n <= 8 ? 1 : (lv.n <= 16 ? 2 : (lv.n <= 32 ? 4 : 8));
+    if (cl == 1) {
+      k3_gs_interior<1><<<lv.M, kT, 0, st>>>(lv, u, b);
+      check3("k3_gs_interior");
+      continue;
+    }
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(kCluster * lv.M);
+    cfg.gridDim = dim3(cl * lv.M);
     cfg.blockDim = dim3(kT);
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = kCluster;
+    attr[0].val.clusterDim.x = cl;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    KB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k3_gs_interior, lv, u, b));
+    if (cl == 2)
+      KB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k3_gs_interior<2>, lv, u, b));
+    else if (cl == 4)
+      KB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k3_gs_interior<4>, lv, u, b));
+    else
+      KB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k3_gs_interior<8>, lv, u, b));
   }
 }
 
@@ -678,10 +727,12 @@ void launch3_cg0(const DevLevel3D& lv0, double* u, const double* b, double* scra
 }
 
 void launch3_estimate(const DevLevel3D& lv, const double* uL, const double* wb, const double* wc, double* sums,
-                      cudaStream_t st) {
+                      double* part, cudaStream_t st) {
   init_constants();
-  k3_estimate<<<lv.M, kT, 0, st>>>(lv, uL, wb, wc, sums);
+  k3_estimate<<<lv.M * (lv.n + 1), kT, 0, st>>>(lv, uL, wb, wc, part);
   check3("k3_estimate");
+  k3_estimate_reduce<<<(lv.M + 127) / 128, 128, 0, st>>>(lv.M, lv.n + 1, part, sums);
+  check3("k3_estimate_reduce");
 }
 
 void launch3_dot(const DevLevel3D& lv, const double* a, const double* b, double* partial, double* out,

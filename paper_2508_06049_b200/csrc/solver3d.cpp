@@ -524,7 +524,7 @@ void Solver3D::estimate_enqueue(int offset) {
   };
   const double* wb = lift(w_[base], base + 1, est_a_);
   const double* wc = lift(w_[base - 1], base, est_b_);
-  launch3_estimate(lev[L_], u_[L_], wb, wc, est_sums_, stream_);
+  launch3_estimate(lev[L_], u_[L_], wb, wc, est_sums_, est_c_, stream_);  // est_c_: per-plane partials
   mark(KK_ESTIMATE, 24.0 * dofs(L_));
   KB_CUDA_CHECK(cudaMemcpyAsync(sums_host_, est_sums_, 2 * H_->host.M * sizeof(double), cudaMemcpyDeviceToHost,
                                 stream_));

@@ -14,6 +14,7 @@ from paper_2508_06049_b200.meshes import kuhn_cube, series_coefficients
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 4
 L = int(sys.argv[2]) if len(sys.argv) > 2 else 6
 prob = sys.argv[3] if len(sys.argv) > 3 else "sin3"
+reps = int(sys.argv[4]) if len(sys.argv) > 4 else 3
 t0 = time.time()
 h = K.GridHierarchy.build(kuhn_cube(N), L)
 t1 = time.time()
@@ -22,11 +23,11 @@ s = K.MultigridSolver(h, K.Problem(kind, series_coefficients() if prob == "serie
 t2 = time.time()
 print(f"N={N} L={L} macros={h.num_macros()} dofs={h.dof_count(L)} build {t1-t0:.1f}s solver {t2-t1:.1f}s", flush=True)
 s.set_profiling(True)
-for _ in range(2):
+for _ in range(1 if reps == 1 else 2):
     s.fmg_enqueue(); s.error_estimate_enqueue(1); s.synchronize(); rep = s.error_estimate_finish(1, 0)
 st = torch.cuda.ExternalStream(s.stream())
 times = []
-for _ in range(3):
+for _ in range(reps):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
     s.fmg_enqueue(); s.error_estimate_enqueue(1)
