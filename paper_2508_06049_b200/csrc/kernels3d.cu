@@ -7,8 +7,8 @@
 //                       parallel), member partial rows + additive sync on the
 //                       shared-node groups (like proj/src/fem.cpp:95-173)
 //   gauss_seidel        multicolour: boundary groups colour by colour, then
-//                       every macro's interior colour by colour, one 8-CTA
-//                       cluster per macro (the macro stays L2-resident)
+//                       every macro's interior colour by colour (one launch
+//                       per colour, rows to warps, read-only path for u)
 //   restrict / prolong  Freudenthal linear interpolation and its transpose
 //   cg0                 level-0 CG in one CTA (proj/src/multigrid.cpp:198-229 order)
 //   estimate            fused per-macro e^T M e over all micro-cells
@@ -28,6 +28,23 @@ constexpr int kT = 256;
 __constant__ int c_cv[6][4][3];  // vertex r of a type-t micro-cell relative to its base
 __constant__ int c_dir[15][3];
 __constant__ int c_pdir[8];      // parity pattern -> direction index (prolongation)
+// compile-time tables (indices resolve in unrolled loops; no local memory)
+__device__ __forceinline__ constexpr int row_dk(int t) {
+  constexpr int v[7] = {0, 0, 0, 1, -1, 1, -1};
+  return v[t];
+}
+__device__ __forceinline__ constexpr int row_dj(int t) {
+  constexpr int v[7] = {0, 1, -1, -1, 1, 0, 0};
+  return v[t];
+}
+__device__ __forceinline__ constexpr int dir_row(int d) {  // neighbour row (0..6) of direction d
+  constexpr int v[15] = {0, 0, 0, 1, 2, 3, 4, 1, 2, 5, 6, 3, 4, 5, 6};
+  return v[d];
+}
+__device__ __forceinline__ constexpr int dir_di(int d) {  // i offset of direction d (kDir[d][0])
+  constexpr int v[15] = {0, 1, -1, -1, 1, 0, 0, 0, 0, -1, 1, 1, -1, 0, 0};
+  return v[d];
+}
 
 __device__ __forceinline__ int tsz(int n) { return (n + 1) * (n + 2) * (n + 3) / 6; }
 __device__ __forceinline__ int lat2(int n, int i, int j) { return j * (n + 1) - (j * (j - 1)) / 2 + i; }
@@ -200,57 +217,47 @@ __global__ void __launch_bounds__(kT) k3_gs_groups(DevLevel3D lv, double* u, con
   }
 }
 
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ unsigned cluster_rank() {
-  unsigned r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ unsigned cluster_id_x() {
-  unsigned r;
-  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
-  return r;
-}
-// interior phase: one cluster of CL CTAs per macro (CL grows with the
-// lattice: 1 for n <= 8 ... 8 for n >= 64), colours in order,
-// a cluster barrier between colours; nodes of colour c are the parity
-// patterns p with pat_color[m][p] == c (enumerated over their bounding box)
-template <int CL>
-__global__ void __launch_bounds__(kT) k3_gs_interior(DevLevel3D lv, double* u, const double* __restrict__ b) {
-  const int m = CL == 1 ? static_cast<int>(blockIdx.x) : static_cast<int>(cluster_id_x());
-  const int r = CL == 1 ? 0 : static_cast<int>(cluster_rank());
-  const int n = lv.n, S = lv.S;
+// interior phase, one launch per colour over every macro: block = (macro,
+// k-plane); the plane's rows of the colour's parity pattern(s) are dealt to the
+// warps, a lane takes every other node of a row.  Nodes of one colour never
+// neighbour each other, so every read of a launch is of a value no thread of
+// the launch writes: the read-only (L1-cached) path is safe and neighbour rows
+// are shared through L1.
+
+__global__ void __launch_bounds__(kT) k3_gs_color(DevLevel3D lv, double* u, const double* __restrict__ b, int c) {
+  const int n = lv.n, S = lv.S, T = tsz(n);
+  const int m = blockIdx.x / (n + 1), k = blockIdx.x - m * (n + 1);
+  if (k < 1 || k > n - 3) return;
+  const int pk = k & 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
   const double* st = lv.stK + 15 * m;
-  double s[15];
-#pragma unroll
-  for (int d = 0; d < 15; ++d) s[d] = __ldg(st + d);
-  const double inv_c = __ldg(lv.inv_c + m);
   double* um = u + static_cast<size_t>(m) * S;
   const double* bm = b + static_cast<size_t>(m) * S;
-  const int A = n / 2 + 1;  // box extent per parity class
-  const int box = A * A * A;
-  for (int c = 0; c < lv.colors; ++c) {
-    for (int p = 0; p < 8; ++p) {
-      if (__ldg(lv.pat_color + 8 * m + p) != c) continue;
-      const int pi = p & 1, pj = (p >> 1) & 1, pk = (p >> 2) & 1;
-      for (int v = threadIdx.x + kT * r; v < box; v += kT * CL) {
-        const int a = v % A, bb = (v / A) % A, cc = v / (A * A);
-        const int i = 2 * a + pi, j = 2 * bb + pj, k = 2 * cc + pk;
-        if (!interior3(n, i, j, k)) continue;
-        const int idx = lat3(n, i, j, k);
-        double acc = s[1] * __ldcg(um + lat3(n, i + c_dir[1][0], j + c_dir[1][1], k + c_dir[1][2]));
+  const int m2 = n - k;
+  for (int p = pk << 2; p < (pk << 2) + 4; ++p) {
+    if (__ldg(lv.pat_color + 8 * m + p) != c) continue;
+    const int pi = p & 1, pj = (p >> 1) & 1;
+    double s[15];
 #pragma unroll
-        for (int d = 2; d < 15; ++d)
-          acc = acc + s[d] * __ldcg(um + lat3(n, i + c_dir[d][0], j + c_dir[d][1], k + c_dir[d][2]));
-        __stcg(um + idx, (__ldg(bm + idx) - acc) * inv_c);
+    for (int d = 1; d < 15; ++d) s[d] = __ldg(st + d);
+    const double inv_c = __ldg(lv.inv_c + m);
+    for (int j = (pj ? 1 : 2) + 2 * warp; j <= m2 - 2; j += 2 * nwarps) {
+      int ra[7];
+#pragma unroll
+      for (int t = 0; t < 7; ++t) {
+        const int kk = k + row_dk(t), jj = j + row_dj(t);
+        ra[t] = T - tsz(n - kk) + lat2(n - kk, 0, jj);
+      }
+      for (int i = (pi ? 1 : 2) + 2 * lane; i <= m2 - 1 - j; i += 64) {
+        double x[15];
+#pragma unroll
+        for (int d = 1; d < 15; ++d) x[d] = __ldg(um + ra[dir_row(d)] + i + dir_di(d));
+        double acc = s[1] * x[1];
+#pragma unroll
+        for (int d = 2; d < 15; ++d) acc = acc + s[d] * x[d];
+        um[ra[0] + i] = (__ldg(bm + ra[0] + i) - acc) * inv_c;
       }
     }
-    if (CL == 1)
-      __syncthreads();
-    else
-      cluster_sync_all();
   }
 }
 
@@ -462,45 +469,72 @@ __global__ void __launch_bounds__(1024) k3_cg0(DevLevel3D lv, double* uc, const 
 }
 
 // ---------------------------------------------------------------- estimator
-// one block per (macro, base plane k); per-block partial sums, reduced per
-// macro in plane order by k3_estimate_reduce
+// vertex c of a type-t micro-cell relative to its base, axis a (compile time)
+__device__ __forceinline__ constexpr int cell_off(int t, int c, int a) {
+  constexpr int v[6][4][3] = {{{0, 0, 0}, {1, 0, 0}, {0, 1, 0}, {0, 0, 1}},
+                              {{0, 0, 0}, {1, 0, 0}, {1, -1, 1}, {0, 0, 1}},
+                              {{0, 0, 0}, {-1, 1, 0}, {0, 1, 0}, {0, 0, 1}},
+                              {{0, 0, 0}, {-1, 1, 0}, {-1, 0, 1}, {0, 0, 1}},
+                              {{0, 0, 0}, {0, -1, 1}, {1, -1, 1}, {0, 0, 1}},
+                              {{0, 0, 0}, {0, -1, 1}, {-1, 0, 1}, {0, 0, 1}}};
+  return v[t][c][a];
+}
+
+// one block per (macro, base plane k): rows to warps, base nodes to lanes, the
+// six cell types per base node; per-block partial sums, reduced per macro in
+// plane order by k3_estimate_reduce
 __global__ void __launch_bounds__(kT) k3_estimate(DevLevel3D lv, const double* __restrict__ uL,
                                                   const double* __restrict__ wb, const double* __restrict__ wc,
                                                   double* part) {
-  const int n = lv.n, S = lv.S;
+  const int n = lv.n, S = lv.S, T = tsz(n);
   const int m = blockIdx.x / (n + 1), k = blockIdx.x - m * (n + 1);
   const int m2 = n - k;
-  const int np = (m2 + 1) * (m2 + 2) / 2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
   const size_t mo = static_cast<size_t>(m) * S;
-  const double* Mt = lv.kmass + 96 * m;
+  double Mt[6][16];
+#pragma unroll
+  for (int t = 0; t < 6; ++t)
+#pragma unroll
+    for (int e = 0; e < 16; ++e) Mt[t][e] = __ldg(lv.kmass + 96 * m + 16 * t + e);
   double qb = 0.0, qc = 0.0;
-  for (int v = threadIdx.x; v < 6 * np; v += blockDim.x) {
-    const int ty = v % 6, q = v / 6;
-    int i, j;
-    decode2(m2, q, i, j);
-    int vi[4];
-    bool ok = true;
+  for (int j = warp; j <= m2; j += nwarps) {
+    // starts of rows (dk, dj) for dk in {0, 1}, dj in {-1, 0, 1}
+    int rs[2][3];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int a = i + c_cv[ty][c][0], b = j + c_cv[ty][c][1], cc = k + c_cv[ty][c][2];
-      ok = ok && inl(n, a, b, cc);
-      vi[c] = ok ? lat3(n, a, b, cc) : 0;
-    }
-    if (!ok) continue;
-    double eb[4], ec[4];
+    for (int dk = 0; dk < 2; ++dk)
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const double uu = uL[mo + vi[c]];
-      eb[c] = uu - wb[mo + vi[c]];
-      ec[c] = uu - wc[mo + vi[c]];
-    }
-    const double* T = Mt + 16 * ty;
+      for (int dj = -1; dj <= 1; ++dj) {
+        const int kk = k + dk, jj = j + dj;
+        rs[dk][dj + 1] = (kk <= n && jj >= 0) ? T - tsz(n - kk) + lat2(n - kk, 0, jj) : 0;
+      }
+    for (int i = lane; i <= m2 - j; i += 32) {
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      const double rb = ((T[4 * a] * eb[0] + T[4 * a + 1] * eb[1]) + T[4 * a + 2] * eb[2]) + T[4 * a + 3] * eb[3];
-      const double rc = ((T[4 * a] * ec[0] + T[4 * a + 1] * ec[1]) + T[4 * a + 2] * ec[2]) + T[4 * a + 3] * ec[3];
-      qb = qb + eb[a] * rb;
-      qc = qc + ec[a] * rc;
+      for (int t = 0; t < 6; ++t) {
+        bool ok = true;
+        int vi[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int a = i + cell_off(t, c, 0), bb = j + cell_off(t, c, 1), cc = k + cell_off(t, c, 2);
+          ok = ok && a >= 0 && bb >= 0 && a + bb + cc <= n;
+          vi[c] = rs[cell_off(t, c, 2)][cell_off(t, c, 1) + 1] + a;
+        }
+        if (!ok) continue;
+        double eb[4], ec[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const double uu = uL[mo + vi[c]];
+          eb[c] = uu - wb[mo + vi[c]];
+          ec[c] = uu - wc[mo + vi[c]];
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          const double* Tm = Mt[t];
+          const double rb = ((Tm[4 * a] * eb[0] + Tm[4 * a + 1] * eb[1]) + Tm[4 * a + 2] * eb[2]) + Tm[4 * a + 3] * eb[3];
+          const double rc = ((Tm[4 * a] * ec[0] + Tm[4 * a + 1] * ec[1]) + Tm[4 * a + 2] * ec[2]) + Tm[4 * a + 3] * ec[3];
+          qb = qb + eb[a] * rb;
+          qc = qc + ec[a] * rc;
+        }
+      }
     }
   }
   __shared__ double rb[kT], rcs[kT];
@@ -655,29 +689,10 @@ void launch3_gs(const DevLevel3D& lv, double* u, const double* b, int sweeps, cu
       check3("k3_gs_groups");
     }
     if (lv.n < 4) continue;  // no lattice-interior nodes
-    const int cl = lv.n <= 8 ? 1 : (lv.n <= 16 ? 2 : (lv.n <= 32 ? 4 : 8));
-    if (cl == 1) {
-      k3_gs_interior<1><<<lv.M, kT, 0, st>>>(lv, u, b);
-      check3("k3_gs_interior");
-      continue;
+    for (int c = 0; c < lv.colors; ++c) {
+      k3_gs_color<<<lv.M * (lv.n + 1), kT, 0, st>>>(lv, u, b, c);
+      check3("k3_gs_color");
     }
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(cl * lv.M);
-    cfg.blockDim = dim3(kT);
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = cl;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    if (cl == 2)
-      KB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k3_gs_interior<2>, lv, u, b));
-    else if (cl == 4)
-      KB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k3_gs_interior<4>, lv, u, b));
-    else
-      KB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k3_gs_interior<8>, lv, u, b));
   }
 }
 

@@ -405,7 +405,7 @@ void Solver3D::vcycle(int l, double* u, const double* b) {
     return;
   }
   const int colors = lev[l].colors;
-  const int gs_launches = colors + (lev[l].n >= 4 ? 1 : 0);
+  const int gs_launches = colors * (lev[l].n >= 4 ? 2 : 1);
   // algorithmic bytes per unique DoF: GS 24/sweep, residual 24,
   // restriction 8 fine + 8 coarse, prolongation+correction 16 fine + 8 coarse
   if (cfg_.pre_smooth > 0) {
