@@ -207,6 +207,76 @@ def workload_config(dofs):
             "l2": "flushed between timed steps (256 MiB write)", "parallelism": "replicas"}
 
 
+# ----------------------------------------------------------------- 3-d workloads (secondary)
+# BASELINE.json configs 3 and 5 (the reference has no 3-d solver: the path is
+# the builder's design, pinned to the 3-d C oracle).  Reported in
+# the same JSON line, not as the headline.
+def fmg_bytes_3d(dofs_L, nu):
+    """Algorithmic FMG bytes: (190.7 nu + 28.6) N_L (3-d)."""
+    return (190.7 * nu + 28.6) * dofs_L
+
+
+def run_3d(K, torch, name, N, L, prob, reps, peak):
+    from paper_2508_06049_b200.meshes import kuhn_cube, series_coefficients
+
+    t0 = time.perf_counter()
+    h = K.GridHierarchy.build(kuhn_cube(N), L)
+    kind = {"sin3": K.PROBLEM_SIN3D, "series": K.PROBLEM_SERIES3D}[prob]
+    s = K.MultigridSolver(h, K.Problem(kind, series_coefficients() if prob == "series" else None),
+                          K.SolverConfig(nu=2))
+    build_s = time.perf_counter() - t0
+    stream = torch.cuda.ExternalStream(s.stream())
+    s.set_profiling(True)
+    s.fmg_enqueue()
+    s.error_estimate_enqueue(1)
+    s.synchronize()
+    s.error_estimate_finish(1, K.UNSCALED)
+    flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
+    times, kms, kb = [], [0.0] * 8, [0.0] * 8
+    for it in range(reps):
+        with torch.cuda.stream(stream):
+            flush.fill_(float(it))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        s.fmg_enqueue()
+        s.error_estimate_enqueue(1)
+        e1.record(stream)
+        s.synchronize()
+        rep = s.error_estimate_finish(1, K.UNSCALED)
+        times.append(e0.elapsed_time(e1))
+        for kk in range(8):
+            m_, _, b_ = s.kernel_stats(kk)
+            kms[kk] += m_
+            kb[kk] += b_
+    ms = sum(times) / len(times)
+    dofs = h.dof_count(L)
+    est_ms = kms[K.KERNEL_ESTIMATE] / reps
+    gs_gbs = kb[K.KERNEL_GS] / (kms[K.KERNEL_GS] * 1e-3) / 1e9 if kms[K.KERNEL_GS] > 0 else None
+    fmg_ms = ms - est_ms
+    return {"config": name, "mesh": f"Kuhn {N}^3 cubes x 6 tets ({h.num_macros()} macros)", "level": L,
+            "dofs": dofs, "ms_fmg_plus_estimate": ms, "estimator_ms": est_ms, "value": dofs / (ms * 1e-3) / 1e9,
+            "unit": "GDoF/s", "fmg_roofline": {"alg_bytes": fmg_bytes_3d(dofs, 2),
+                                               "frac": fmg_bytes_3d(dofs, 2) / (fmg_ms * 1e-3) / 1e9 / peak},
+            "smoother_alg_GBps": gs_gbs, "eta": rep.eta, "theta": rep.conv_factor,
+            "kernel_ms": {K.KERNEL_NAMES[k]: kms[k] / reps for k in range(8) if kms[k] > 0},
+            "build_s": build_s, "parity": "builder 3-d oracle (oracle/klref_oracle3d.c), bitwise on small cases"}
+
+
+def cpu_3d_port_sample():
+    """Single-threaded 3-d C oracle on a bounded sample (config 3 mesh, l = 4)."""
+    from oracle import oracle as O
+    from paper_2508_06049_b200.meshes import kuhn_cube
+
+    m = kuhn_cube(4)
+    h = O.Hier3D(m.coords, m.elements, 4)
+    t0 = time.perf_counter()
+    st = O.fmg3d(h, "sin3", nu=2)
+    O.estimate3d(st)
+    dt = time.perf_counter() - t0
+    return {"value": h.dofs(4) / dt / 1e9, "unit": "GDoF/s", "cores": 1, "kind": "port",
+            "sample": f"3-d C oracle, config-3 mesh at l=4 ({h.dofs(4)} DoF), one FMG + estimate, 1 thread"}
+
+
 # ----------------------------------------------------------------- our arm (GPU)
 def impl_ours(args):
     import numpy as np
@@ -372,6 +442,18 @@ def impl_ours(args):
         except Exception as exc:  # the baseline is reported, not required
             cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference", "sample": f"failed: {exc}"}
 
+    extra3d = None
+    if not args.no_3d:
+        try:
+            peak3, _ = peaks()
+            extra3d = {"cfg3": run_3d(K, torch, "cfg3: unit cube, 4^3 Kuhn cubes, l=6, sin3", 4, 6, "sin3", 3, peak3),
+                       "cfg5_one_gpu": run_3d(K, torch, "cfg5: unit cube, 8^3 Kuhn cubes, l=6, sine series (g=0)",
+                                              8, 6, "series", 2, peak3)}
+            if world == 1 and not args.no_cpu_baseline:
+                extra3d["cpu_baseline_3d"] = cpu_3d_port_sample()
+        except Exception as exc:  # secondary numbers never sink the headline line
+            extra3d = {"error": str(exc)[:300]}
+
     value = world * dofs / (t_step * 1e-3) / 1e9
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -389,6 +471,7 @@ def impl_ours(args):
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk,
         "cpu_baseline": cpu,
+        "workloads_3d": extra3d,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
@@ -404,6 +487,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--cpu-steps", type=int, default=12, help="steps of the single-core reference sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-3d", action="store_true", help="skip the secondary 3-d workloads (configs 3 and 5)")
     ap.add_argument("--no-replicas", action="store_true", help="reference arm: skip the all-cores replica context run")
     args = ap.parse_args()
     if args.impl == "reference":
