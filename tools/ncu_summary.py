@@ -17,15 +17,19 @@ def launches(path, title):
     rows = list(csv.reader(lines[start:]))
     hdr = rows[0]
     i_name, i_val = hdr.index("Kernel Name"), hdr.index("Metric Value")
+    i_met, i_unit = hdr.index("Metric Name"), hdr.index("Metric Unit")
+    scale = {"ns": 1.0, "nsecond": 1.0, "us": 1e3, "usecond": 1e3, "ms": 1e6, "msecond": 1e6}
     agg = collections.defaultdict(lambda: [0, 0.0])
     for r in rows[1:]:
+        if r[i_met] != "gpu__time_duration.sum":
+            continue
         try:
-            v = float(r[i_val].replace(",", ""))
+            v = float(r[i_val].replace(",", "")) * scale.get(r[i_unit], 1.0)
         except ValueError:
             continue
         if not math.isfinite(v):
             continue
-        nm = r[i_name].split("(")[0].replace("kb::<unnamed>::", "").replace("kb::", "")
+        nm = r[i_name].split("(")[0].split("::")[-1]
         agg[nm][0] += 1
         agg[nm][1] += v
     tot = sum(v[1] for v in agg.values())
