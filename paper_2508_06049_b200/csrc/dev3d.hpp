@@ -23,13 +23,20 @@ struct DevLevel3D {
   const std::uint8_t* grp_domain;
   const double* grp_diag;
   const int* color_grp_ptr;    // boundary groups by colour
-  const int* color_grp;
+  const int* color_grp;         // per colour: wide groups (> 4 members) first
+  const int* color_wide_end;    // per colour: end of its wide groups in color_grp
   const double* kstiff;        // 96 per macro: [type][4][4]
   const double* kmass;
   const double* stK;           // 15 per macro (kDir order)
   const double* stM;
   const double* inv_c;
   const int* pat_color;        // 8 per macro
+  const int* col_pat;          // colors per macro: the parity pattern of that colour, -1 none
+  // small levels (n <= 16): lattice-interior nodes of each parity pattern
+  // (i | j << 10 | k << 20), pattern p at [pat_ptr[p], pat_ptr[p + 1]); else null
+  const int* pat_ptr;
+  const int* pat_node;
+  int pat_max;
   const int* own_dot;          // group owner copy offsets (dot order)
   const double* psK;           // boundary partial stencils: 16 signatures x 15 per macro
   const double* psM;
@@ -50,7 +57,10 @@ enum Prolong3Mode : int { P3_ASSIGN = 0, P3_ADD = 1 };
 
 void launch3_apply(const DevLevel3D& lv, bool mass, const double* x, double* y, const double* b, int mode,
                    cudaStream_t st);
+// smoother: one cooperative launch (boundary colours, then per-macro interior
+// colours; KB_GS3_SPLIT=1 selects the per-colour launches)
 void launch3_gs(const DevLevel3D& lv, double* u, const double* b, int sweeps, cudaStream_t st);
+int launch3_gs_count(const DevLevel3D& lv, int sweeps);
 void launch3_prolong(const DevLevel3D& coarse, const DevLevel3D& fine, const double* c, double* f, int mode,
                      cudaStream_t st);
 // restriction of an owner-masked fine vector (A3_RES_OWNER residual), then

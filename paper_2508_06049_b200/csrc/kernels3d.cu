@@ -12,10 +12,13 @@
 //   restrict / prolong  Freudenthal linear interpolation and its transpose
 //   cg0                 level-0 CG in one CTA (proj/src/multigrid.cpp:198-229 order)
 //   estimate            fused per-macro e^T M e over all micro-cells
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <string>
 
 #include "dev3d.hpp"
@@ -28,6 +31,7 @@ constexpr int kT = 256;
 __constant__ int c_cv[6][4][3];  // vertex r of a type-t micro-cell relative to its base
 __constant__ int c_dir[15][3];
 __constant__ int c_pdir[8];      // parity pattern -> direction index (prolongation)
+__device__ unsigned long long g_gs3_trace[64];  // measurement trace of k3_gs_sweeps (globaltimer ns)
 // compile-time tables (indices resolve in unrolled loops; no local memory)
 __device__ __forceinline__ constexpr int row_dk(int t) {
   constexpr int v[7] = {0, 0, 0, 1, -1, 1, -1};
@@ -70,24 +74,96 @@ __device__ __forceinline__ int sig3(int n, int i, int j, int k) {
   return (i == 0) | ((j == 0) << 1) | ((k == 0) << 2) | ((i + j + k == n) << 3);
 }
 
+// 15 independent fp64 loads issued back to back (see partial_row)
+__device__ __forceinline__ void load15(double (&v)[15], const double* const (&a)[15]) {
+  asm volatile(
+      "ld.global.f64 %0, [%15];\n\t"
+      "ld.global.f64 %1, [%16];\n\t"
+      "ld.global.f64 %2, [%17];\n\t"
+      "ld.global.f64 %3, [%18];\n\t"
+      "ld.global.f64 %4, [%19];\n\t"
+      "ld.global.f64 %5, [%20];\n\t"
+      "ld.global.f64 %6, [%21];\n\t"
+      "ld.global.f64 %7, [%22];\n\t"
+      "ld.global.f64 %8, [%23];\n\t"
+      "ld.global.f64 %9, [%24];\n\t"
+      "ld.global.f64 %10, [%25];\n\t"
+      "ld.global.f64 %11, [%26];\n\t"
+      "ld.global.f64 %12, [%27];\n\t"
+      "ld.global.f64 %13, [%28];\n\t"
+      "ld.global.f64 %14, [%29];"
+      : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]), "=d"(v[4]), "=d"(v[5]), "=d"(v[6]), "=d"(v[7]), "=d"(v[8]),
+        "=d"(v[9]), "=d"(v[10]), "=d"(v[11]), "=d"(v[12]), "=d"(v[13]), "=d"(v[14])
+      : "l"(a[0]), "l"(a[1]), "l"(a[2]), "l"(a[3]), "l"(a[4]), "l"(a[5]), "l"(a[6]), "l"(a[7]), "l"(a[8]), "l"(a[9]),
+        "l"(a[10]), "l"(a[11]), "l"(a[12]), "l"(a[13]), "l"(a[14])
+      : "memory");
+}
+// 15 consecutive fp64 values
+__device__ __forceinline__ void load15_seq(double (&v)[15], const double* p) {
+  asm volatile(
+      "ld.global.f64 %0, [%15];\n\t"
+      "ld.global.f64 %1, [%15+8];\n\t"
+      "ld.global.f64 %2, [%15+16];\n\t"
+      "ld.global.f64 %3, [%15+24];\n\t"
+      "ld.global.f64 %4, [%15+32];\n\t"
+      "ld.global.f64 %5, [%15+40];\n\t"
+      "ld.global.f64 %6, [%15+48];\n\t"
+      "ld.global.f64 %7, [%15+56];\n\t"
+      "ld.global.f64 %8, [%15+64];\n\t"
+      "ld.global.f64 %9, [%15+72];\n\t"
+      "ld.global.f64 %10, [%15+80];\n\t"
+      "ld.global.f64 %11, [%15+88];\n\t"
+      "ld.global.f64 %12, [%15+96];\n\t"
+      "ld.global.f64 %13, [%15+104];\n\t"
+      "ld.global.f64 %14, [%15+112];"
+      : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]), "=d"(v[4]), "=d"(v[5]), "=d"(v[6]), "=d"(v[7]), "=d"(v[8]),
+        "=d"(v[9]), "=d"(v[10]), "=d"(v[11]), "=d"(v[12]), "=d"(v[13]), "=d"(v[14])
+      : "l"(p)
+      : "memory");
+}
+
+// Offsets of the 7 lattice rows around node (., j, k) — rows (k + row_dk(t),
+// j + row_dj(t)) — and their last i (-1 when the row is outside the macro).
+__device__ __forceinline__ void node_rows(int n, int j, int k, int (&ra)[7], int (&len)[7]) {
+  const int T = tsz(n);
+  const int pb0 = T - tsz(n - k);                              // plane k
+  const int pbp = pb0 + (n - k + 1) * (n - k + 2) / 2;         // plane k + 1
+  const int pbm = pb0 - (n - k + 2) * (n - k + 3) / 2;         // plane k - 1
+#pragma unroll
+  for (int t = 0; t < 7; ++t) {
+    const int dk = row_dk(t), kk = k + dk, jj = j + row_dj(t), m2 = n - kk;
+    const int pb = dk == 0 ? pb0 : (dk > 0 ? pbp : pbm);
+    const bool valid = kk >= 0 && kk <= n && jj >= 0 && jj <= m2;
+    ra[t] = valid ? pb + jj * (m2 + 1) - (jj * (jj - 1)) / 2 : pb0;
+    len[t] = valid ? m2 - jj : -1;
+  }
+}
+
 // partial row of a lattice-boundary node of one macro: its signature's partial
-// stencil over the neighbours inside the macro, centre first
-__device__ double partial_full(const double* __restrict__ ps_m, const double* __restrict__ xm, int n, int i, int j,
-                               int k) {
-  // all loads issued together (clamped to the node itself when the neighbour
-  // is outside the macro), the sum keeps the specification's order and terms
+// stencil over the neighbours inside the macro, centre first.  All loads are
+// issued together (clamped to the node itself when the neighbour is outside
+// the macro); the sum keeps the specification's order and terms.
+template <bool kOff>
+__device__ __forceinline__ double partial_row(const double* __restrict__ ps_m, const double* xm, int n, int i, int j,
+                                              int k) {
   const double* ps = ps_m + 15 * sig3(n, i, j, k);
-  const int c0 = lat3(n, i, j, k);
+  int ra[7], len[7];
+  node_rows(n, j, k, ra, len);
+  const int c0 = ra[0] + i;
   double x[15], cf[15];
   bool ok[15];
+  const double* ad[15];
 #pragma unroll
   for (int d = 0; d < 15; ++d) {
-    const int a = i + c_dir[d][0], b = j + c_dir[d][1], c = k + c_dir[d][2];
-    ok[d] = inl(n, a, b, c);
-    x[d] = xm[ok[d] ? lat3(n, a, b, c) : c0];
-    cf[d] = ps[d];
+    const int r = dir_row(d), ii = i + dir_di(d);
+    ok[d] = ii >= 0 && ii <= len[r];
+    ad[d] = xm + (ok[d] ? ra[r] + ii : c0);
   }
-  double acc = cf[0] * x[0];
+  // ptxas sinks plain loads to just before their use, serialising the L2 round
+  // trips of the 15 terms; issued from one asm block they are all in flight
+  load15(x, ad);
+  load15_seq(cf, ps);
+  double acc = kOff ? 0.0 : cf[0] * x[0];
 #pragma unroll
   for (int d = 1; d < 15; ++d) {
     const double t = acc + cf[d] * x[d];
@@ -95,27 +171,12 @@ __device__ double partial_full(const double* __restrict__ ps_m, const double* __
   }
   return acc;
 }
-
+__device__ double partial_full(const double* __restrict__ ps_m, const double* xm, int n, int i, int j, int k) {
+  return partial_row<false>(ps_m, xm, n, i, j, k);
+}
 // off-diagonal part (Gauss-Seidel)
 __device__ double partial_off3(const double* __restrict__ ps_m, const double* xm, int n, int i, int j, int k) {
-  const double* ps = ps_m + 15 * sig3(n, i, j, k);
-  const int c0 = lat3(n, i, j, k);
-  double x[15], cf[15];
-  bool ok[15];
-#pragma unroll
-  for (int d = 1; d < 15; ++d) {
-    const int a = i + c_dir[d][0], b = j + c_dir[d][1], c = k + c_dir[d][2];
-    ok[d] = inl(n, a, b, c);
-    x[d] = xm[ok[d] ? lat3(n, a, b, c) : c0];
-    cf[d] = ps[d];
-  }
-  double o = 0.0;
-#pragma unroll
-  for (int d = 1; d < 15; ++d) {
-    const double t = o + cf[d] * x[d];
-    o = ok[d] ? t : o;
-  }
-  return o;
+  return partial_row<true>(ps_m, xm, n, i, j, k);
 }
 
 __device__ __forceinline__ void unpack_ijk(int p, int& i, int& j, int& k) {
@@ -186,13 +247,14 @@ __global__ void __launch_bounds__(kT) k3_apply(DevLevel3D lv, int mass, const do
 }
 
 // ---------------------------------------------------------------- Gauss-Seidel
-// boundary phase of colour c: one group per thread
-__global__ void __launch_bounds__(kT) k3_gs_groups(DevLevel3D lv, double* u, const double* __restrict__ b, int c) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  const int p0 = lv.color_grp_ptr[c], p1 = lv.color_grp_ptr[c + 1];
-  if (p0 + t >= p1) return;
-  const int g = lv.color_grp[p0 + t];
+// relaxation of one shared-node group (all copies get the same value)
+__device__ __forceinline__ void stamp(long long* tr, int slot) {
+  if (tr) tr[slot] = clock64();
+}
+__device__ void gs_group(const DevLevel3D& lv, double* u, const double* __restrict__ b, int g,
+                         long long* tr = nullptr) {
   const int n = lv.n, S = lv.S;
+  stamp(tr, 0);
   const int beg = lv.grp_ptr[g], end = lv.grp_ptr[g + 1];
   int i0, j0, k0;
   unpack_ijk(lv.mem_ijk[beg], i0, j0, k0);
@@ -206,14 +268,219 @@ __global__ void __launch_bounds__(kT) k3_gs_groups(DevLevel3D lv, double* u, con
       const int s = lv.mem_slot[q];
       int i, j, k;
       unpack_ijk(lv.mem_ijk[q], i, j, k);
+      stamp(tr, 1 + 2 * (q - beg));
       off = off + partial_off3(lv.psK + 240 * s, u + static_cast<size_t>(s) * S, n, i, j, k);
+      if (tr) tr[2 + 2 * (q - beg)] = clock64() + (off == 12345.0 ? 1 : 0);
     }
     val = (b[own] - off) / lv.grp_diag[g];
   }
+  if (tr) tr[8] = clock64() + (val == 12345.0 ? 1 : 0);
   for (int q = beg; q < end; ++q) {
     int i, j, k;
     unpack_ijk(lv.mem_ijk[q], i, j, k);
     u[static_cast<size_t>(lv.mem_slot[q]) * S + lat3(n, i, j, k)] = val;
+  }
+  stamp(tr, 9);
+}
+
+// boundary phase of colour c: one group per thread
+__global__ void __launch_bounds__(kT) k3_gs_groups(DevLevel3D lv, double* u, const double* __restrict__ b, int c) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int p0 = lv.color_grp_ptr[c], p1 = lv.color_grp_ptr[c + 1];
+  if (p0 + t >= p1) return;
+  gs_group(lv, u, b, lv.color_grp[p0 + t]);
+}
+
+// One interior node of macro m (row offsets ra of the 7 neighbour rows).
+__device__ __forceinline__ void gs_node(double* um, const double* __restrict__ bm, const double (&s)[15],
+                                        double inv_c, const int (&ra)[7], int i) {
+  double x[15];
+#pragma unroll
+  for (int d = 1; d < 15; ++d) x[d] = um[ra[dir_row(d)] + i + dir_di(d)];
+  double acc = s[1] * x[1];
+#pragma unroll
+  for (int d = 2; d < 15; ++d) acc = acc + s[d] * x[d];
+  um[ra[0] + i] = (__ldg(bm + ra[0] + i) - acc) * inv_c;
+}
+
+// Interior phase of one macro, all colours in order: lattice-interior nodes
+// only couple to their own macro's copies, so once the boundary phase is done
+// the macros are independent and one CTA runs a macro's whole colour sequence
+// with block barriers, the macro's lattice staying in L1/L2 between colours.
+// The rows (k, j) of a parity pattern are dealt round-robin to the warps, a
+// lane takes every other node of a row.
+__device__ void gs_interior_macro(const DevLevel3D& lv, double* u, const double* __restrict__ b, int m) {
+  const int n = lv.n, S = lv.S, T = tsz(n);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  double* um = u + static_cast<size_t>(m) * S;
+  const double* bm = b + static_cast<size_t>(m) * S;
+  double s[15];
+#pragma unroll
+  for (int d = 1; d < 15; ++d) s[d] = __ldg(lv.stK + 15 * m + d);
+  const double inv_c = __ldg(lv.inv_c + m);
+  for (int c = 0; c < lv.colors; ++c) {
+    bool any = false;
+#pragma unroll 1
+    for (int p = 0; p < 8; ++p) {
+      if (__ldg(lv.pat_color + 8 * m + p) != c) continue;
+      any = true;
+      const int pi = p & 1, pj = (p >> 1) & 1, pk = (p >> 2) & 1;
+      const int jlo = pj ? 1 : 2, ilo = (pi ? 1 : 2) + 2 * lane;
+      int k = pk ? 1 : 2, r = warp;
+      while (k <= n - 3) {
+        const int m2 = n - k;
+        const int nr = m2 - 2 >= jlo ? (m2 - 2 - jlo) / 2 + 1 : 0;
+        if (r >= nr) {
+          r -= nr;
+          k += 2;
+          continue;
+        }
+        const int j = jlo + 2 * r;
+        int ra[7];
+#pragma unroll
+        for (int t = 0; t < 7; ++t) {
+          const int kk = k + row_dk(t), jj = j + row_dj(t);
+          ra[t] = T - tsz(n - kk) + lat2(n - kk, 0, jj);
+        }
+        for (int i = ilo; i <= m2 - 1 - j; i += 64) gs_node(um, bm, s, inv_c, ra, i);
+        r += nwarps;
+      }
+    }
+    if (any) __syncthreads();
+  }
+}
+
+// Interior phase for small macros (n <= 16): the CTA's macros (every
+// active-th one) are processed together, colour by colour with block barriers;
+// the items of a colour are (macro, node of the macro's pattern of that
+// colour) from the level's pattern node lists.
+__device__ void gs_interior_batch(const DevLevel3D& lv, double* u, const double* __restrict__ b, int active,
+                                  int group) {
+  const int n = lv.n, S = lv.S, T = tsz(n), per = lv.pat_max;
+  const int mine = (lv.M - static_cast<int>(blockIdx.x) + active - 1) / active;  // macros of this CTA
+  for (int g0 = 0; g0 < mine; g0 += group)
+  for (int c = 0; c < lv.colors; ++c) {
+    const int nm = min(group, mine - g0);
+    for (int t = threadIdx.x; t < nm * per; t += blockDim.x) {
+      const int mi = t / per, idx = t - mi * per;
+      const int m = blockIdx.x + (g0 + mi) * active;
+      const int p = __ldg(lv.col_pat + lv.colors * m + c);
+      if (p < 0) continue;
+      const int q0 = __ldg(lv.pat_ptr + p);
+      if (idx >= __ldg(lv.pat_ptr + p + 1) - q0) continue;
+      int i, j, k;
+      unpack_ijk(__ldg(lv.pat_node + q0 + idx), i, j, k);
+      int ra[7];
+#pragma unroll
+      for (int r = 0; r < 7; ++r) {
+        const int kk = k + row_dk(r), jj = j + row_dj(r);
+        ra[r] = T - tsz(n - kk) + lat2(n - kk, 0, jj);
+      }
+      double st[15];
+#pragma unroll
+      for (int d = 1; d < 15; ++d) st[d] = __ldg(lv.stK + 15 * m + d);
+      gs_node(u + static_cast<size_t>(m) * S, b + static_cast<size_t>(m) * S, st, __ldg(lv.inv_c + m), ra, i);
+    }
+    __syncthreads();
+  }
+}
+
+// Relaxation of a group with many members (macro vertices, edges): one warp,
+// a lane per member partial row, the member sum in slot order by shuffles.
+__device__ void gs_group_warp(const DevLevel3D& lv, double* u, const double* __restrict__ b, int g, int lane) {
+  const int n = lv.n, S = lv.S;
+  const int beg = lv.grp_ptr[g], end = lv.grp_ptr[g + 1];
+  int i0, j0, k0;
+  unpack_ijk(lv.mem_ijk[beg], i0, j0, k0);
+  const size_t own = static_cast<size_t>(lv.mem_slot[beg]) * S + lat3(n, i0, j0, k0);
+  double val;
+  if (lv.grp_domain[g]) {
+    val = b[own];
+  } else {
+    double off = 0.0;
+    for (int q0 = beg; q0 < end; q0 += 32) {
+      double part = 0.0;
+      const int q = q0 + lane;
+      if (q < end) {
+        const int s = lv.mem_slot[q];
+        int i, j, k;
+        unpack_ijk(lv.mem_ijk[q], i, j, k);
+        part = partial_off3(lv.psK + 240 * s, u + static_cast<size_t>(s) * S, n, i, j, k);
+      }
+      const int cnt = min(32, end - q0);
+      for (int t = 0; t < cnt; ++t) off = off + __shfl_sync(0xffffffffu, part, t);
+    }
+    val = (b[own] - off) / lv.grp_diag[g];
+  }
+  for (int q = beg + lane; q < end; q += 32) {
+    int i, j, k;
+    unpack_ijk(lv.mem_ijk[q], i, j, k);
+    u[static_cast<size_t>(lv.mem_slot[q]) * S + lat3(n, i, j, k)] = val;
+  }
+}
+
+// Whole smoother (sweeps x [boundary colours, interior]) in one cooperative
+// launch: grid barriers between the boundary colours and between the phases.
+// Per colour the group list holds the wide groups (warp each) first, then the
+// narrow ones (thread each).  The interior phase runs at most `active` CTAs
+// (one macro each at a time) so that the macros being smoothed stay in L2
+// across their colours.
+template <int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k3_gs_sweeps(DevLevel3D lv, double* u, const double* __restrict__ b,
+                                                         int sweeps, int phases, int active, int group) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  const int nthreads = gridDim.x * NT;
+  const int tid = blockIdx.x * NT + threadIdx.x;
+  const int lane = threadIdx.x & 31, gw = tid >> 5, nw = nthreads >> 5;
+  if ((phases & 4) && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_gs3_trace[63]));
+  for (int sw = 0; sw < sweeps; ++sw) {
+    for (int c = 0; c < lv.colors; ++c) {
+      const int p0 = lv.color_grp_ptr[c], p1 = lv.color_grp_ptr[c + 1], pw = lv.color_wide_end[c];
+      if (phases & 1) {
+        for (int t = p0 + gw; t < pw; t += nw) gs_group_warp(lv, u, b, lv.color_grp[t], lane);
+        for (int t = pw + tid; t < p1; t += nthreads)
+          gs_group(lv, u, b, lv.color_grp[t],
+                   (phases & 8) && tid == 0 && sw == 0 ? reinterpret_cast<long long*>(g_gs3_trace + 16 + 10 * c)
+                                                        : nullptr);
+      }
+      if (phases & 4) {  // measurement trace (KB_GS3_PHASES bit 2): work end vs barrier exit
+        __syncthreads();
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (sw == 0 && threadIdx.x == 0) atomicMax(&g_gs3_trace[2 * c], t);
+      }
+      if (p1 > p0) grid.sync();
+      if ((phases & 4) && threadIdx.x == 0 && blockIdx.x == 0 && sw == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_gs3_trace[2 * c + 1] = t;
+      }
+    }
+    if (lv.n >= 4) {
+      if ((phases & 2) && static_cast<int>(blockIdx.x) < active) {
+        if (lv.pat_node)
+          gs_interior_batch(lv, u, b, active, group);
+        else
+          for (int m = blockIdx.x; m < lv.M; m += active) gs_interior_macro(lv, u, b, m);
+      }
+      if (sw + 1 < sweeps) grid.sync();
+    }
+  }
+  if (phases & 4) {
+    grid.sync();
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+      for (int c = 0; c < lv.colors; ++c)
+        printf("colour %d: groups %d wide %d, last work done %llu ns, barrier passed (blk0) %llu ns\n", c,
+               lv.color_grp_ptr[c + 1] - lv.color_grp_ptr[c], lv.color_wide_end[c] - lv.color_grp_ptr[c],
+               g_gs3_trace[2 * c] - g_gs3_trace[63], g_gs3_trace[2 * c + 1] - g_gs3_trace[63]);
+    if ((phases & 8) && blockIdx.x == 0 && threadIdx.x == 0)
+      for (int c = 0; c < 4; ++c) {
+        const unsigned long long* t = g_gs3_trace + 16 + 10 * c;
+        printf("colour %d first narrow group (cycles from start): meta %llu  m0 %llu..%llu  m1 %llu..%llu  div %llu  "
+               "store %llu\n",
+               c, t[1] - t[0], t[1] - t[0], t[2] - t[0], t[3] - t[0], t[4] - t[0], t[8] - t[0], t[9] - t[0]);
+      }
   }
 }
 
@@ -669,6 +936,34 @@ void init_constants() {
   done = true;
 }
 
+int device_attr3(cudaDeviceAttr a) {
+  int dev = 0, v = 0;
+  KB_CUDA_CHECK(cudaGetDevice(&dev));
+  KB_CUDA_CHECK(cudaDeviceGetAttribute(&v, a, dev));
+  return v;
+}
+
+// KB_GS3_SPLIT=1: the per-colour launches (k3_gs_groups + k3_gs_color), kept
+// as a same-result variant for measurement
+bool gs_split() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("KB_GS3_SPLIT");
+    v = e && e[0] == '1';
+  }
+  return v == 1;
+}
+
+// KB_GS3_PHASES (measurement only): 1 boundary phase, 2 interior phase, 3 both
+int gs_phases() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("KB_GS3_PHASES");
+    v = e ? atoi(e) : 3;
+  }
+  return v;
+}
+
 int blocks_for(long long count) { return static_cast<int>(std::max(1ll, (count + kT - 1) / kT)); }
 
 }  // namespace
@@ -683,6 +978,41 @@ void launch3_apply(const DevLevel3D& lv, bool mass, const double* x, double* y, 
 
 void launch3_gs(const DevLevel3D& lv, double* u, const double* b, int sweeps, cudaStream_t st) {
   init_constants();
+  if (sweeps <= 0) return;
+  if (!gs_split()) {
+    // 512-thread CTAs, one per SM, for large macros (the working set of the
+    // macros in flight stays in L2), 256-thread CTAs three per SM otherwise
+    static int sms = 0, occ_big = 0, occ_small = 0;
+    if (sms == 0) {
+      sms = device_attr3(cudaDevAttrMultiProcessorCount);
+      KB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_big, k3_gs_sweeps<512, 1>, 512, 0));
+      KB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_small, k3_gs_sweeps<256, 3>, 256, 0));
+      if (occ_big < 1 || occ_small < 1) fail(KB_CUDA, "k3_gs_sweeps cannot be resident");
+    }
+    bool big = false;
+    if (const char* e = getenv("KB_GS3_BIG")) big = e[0] == '1';
+    const int nt = big ? 512 : 256;
+    int grid = (big ? occ_big : occ_small) * sms;
+    if (const char* e = getenv("KB_GS3_GRID")) grid = std::max(1, std::min(grid, atoi(e)));
+    int active = grid;
+    if (const char* e = getenv("KB_GS3_ACTIVE")) active = std::max(1, std::min(grid, atoi(e)));
+    int group = lv.M;
+    if (const char* e = getenv("KB_GS3_G")) group = std::max(1, atoi(e));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(nt);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (big)
+      KB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k3_gs_sweeps<512, 1>, lv, u, b, sweeps, gs_phases(), active, group));
+    else
+      KB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k3_gs_sweeps<256, 3>, lv, u, b, sweeps, gs_phases(), active, group));
+    return;
+  }
   for (int s = 0; s < sweeps; ++s) {
     for (int c = 0; c < lv.colors; ++c) {
       k3_gs_groups<<<blocks_for(lv.ng), kT, 0, st>>>(lv, u, b, c);
@@ -694,6 +1024,11 @@ void launch3_gs(const DevLevel3D& lv, double* u, const double* b, int sweeps, cu
       check3("k3_gs_color");
     }
   }
+}
+
+int launch3_gs_count(const DevLevel3D& lv, int sweeps) {
+  if (sweeps <= 0) return 0;
+  return gs_split() ? sweeps * lv.colors * (lv.n >= 4 ? 2 : 1) : 1;
 }
 
 void launch3_prolong(const DevLevel3D& coarse, const DevLevel3D& fine, const double* c, double* f, int mode,

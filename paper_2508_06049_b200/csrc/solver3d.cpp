@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 namespace kb {
@@ -21,11 +22,24 @@ double gauss3(double x, double y, double z) {
 }  // namespace
 
 // ------------------------------------------------------------------ hierarchy upload
+namespace {
+// largest macro size whose interior smoother runs in the batched (node-list) form
+int batch_max_n() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("KB_GS3_BATCH_N");
+    v = e ? atoi(e) : 128;
+  }
+  return v;
+}
+}  // namespace
+
 std::unique_ptr<DeviceHierarchy3D> DeviceHierarchy3D::create(const Mesh3D& mesh, int max_level) {
   auto d = std::make_unique<DeviceHierarchy3D>();
   d->host = Hierarchy3D::build(mesh, max_level);
   const Hierarchy3D& h = d->host;
-  std::vector<std::vector<int>> ijk(h.L + 1), own(h.L + 1);
+  std::vector<std::vector<int>> ijk(h.L + 1), own(h.L + 1), col_pat(h.L + 1), pat_ptr(h.L + 1), pat_node(h.L + 1);
+  std::vector<int> pat_max(h.L + 1, 0);
   size_t bytes = 0;
   for (int l = 0; l <= h.L; ++l) {
     const Level3D& lv = h.levels[l];
@@ -49,10 +63,27 @@ std::unique_ptr<DeviceHierarchy3D> DeviceHierarchy3D::create(const Mesh3D& mesh,
       const int q = lv.grp_ptr[g];
       own[l][g] = lv.mem_slot[q] * lv.S + lv.mem_idx[q];
     }
+    // colour -> parity pattern per macro; small levels: interior nodes per pattern
+    col_pat[l].assign(static_cast<size_t>(h.M) * h.colors, -1);
+    for (int s = 0; s < h.M; ++s)
+      for (int p = 0; p < 8; ++p) col_pat[l][static_cast<size_t>(h.colors) * s + lv.pat_color[8 * s + p]] = p;
+    if (n <= batch_max_n()) {
+      pat_ptr[l].assign(9, 0);
+      for (int p = 0; p < 8; ++p) {
+        for (int k = 1; k <= n; ++k)
+          for (int j = 1; j <= n; ++j)
+            for (int i = 1; i + j + k <= n - 1; ++i)
+              if (((i & 1) | ((j & 1) << 1) | ((k & 1) << 2)) == p) pat_node[l].push_back(i | j << 10 | k << 20);
+        pat_ptr[l][p + 1] = static_cast<int>(pat_node[l].size());
+        pat_max[l] = std::max(pat_max[l], pat_ptr[l][p + 1] - pat_ptr[l][p]);
+      }
+      if (pat_node[l].empty()) pat_ptr[l].clear();
+    }
     auto vb = [](auto& v) { return r256(v.size() * sizeof(v[0])); };
     bytes += vb(lv.grp_ptr) + vb(lv.mem_slot) + vb(ijk[l]) + vb(lv.grp_domain) + vb(lv.grp_diag) +
              vb(lv.color_grp_ptr) + vb(lv.color_grp) + vb(lv.kstiff) + vb(lv.kmass) + 2 * vb(lv.stencil) +
-             vb(lv.inv_c) + vb(lv.pat_color) + vb(own[l]);
+             vb(lv.inv_c) + vb(lv.pat_color) + vb(own[l]) + r256(4 * h.colors) + vb(col_pat[l]) +
+             vb(pat_ptr[l]) + vb(pat_node[l]);
   }
   // level-0 CG program: for every vertex group, its members' partial stencils
   // as (coefficient, global vertex) terms, centre first (level-0 groups are the
@@ -96,7 +127,25 @@ std::unique_ptr<DeviceHierarchy3D> DeviceHierarchy3D::create(const Mesh3D& mesh,
     dl.grp_domain = d->arena.upload(lv.grp_domain);
     dl.grp_diag = d->arena.upload(lv.grp_diag);
     dl.color_grp_ptr = d->arena.upload(lv.color_grp_ptr);
-    dl.color_grp = d->arena.upload(lv.color_grp);
+    {
+      // within a colour the groups are independent: wide ones first (warp
+      // relaxation), then the narrow ones, each part ascending
+      std::vector<int> cg(lv.color_grp.size()), wide_end(h.colors);
+      for (int c = 0; c < h.colors; ++c) {
+        int w = lv.color_grp_ptr[c];
+        for (int t = lv.color_grp_ptr[c]; t < lv.color_grp_ptr[c + 1]; ++t) {
+          const int g = lv.color_grp[t];
+          if (lv.grp_ptr[g + 1] - lv.grp_ptr[g] > 4) cg[w++] = g;
+        }
+        wide_end[c] = w;
+        for (int t = lv.color_grp_ptr[c]; t < lv.color_grp_ptr[c + 1]; ++t) {
+          const int g = lv.color_grp[t];
+          if (lv.grp_ptr[g + 1] - lv.grp_ptr[g] <= 4) cg[w++] = g;
+        }
+      }
+      dl.color_grp = d->arena.upload(cg);
+      dl.color_wide_end = d->arena.upload(wide_end);
+    }
     dl.kstiff = d->arena.upload(lv.kstiff);
     dl.kmass = d->arena.upload(lv.kmass);
     // interior stencils: stiffness from the host tables, mass summed the same way
@@ -114,6 +163,12 @@ std::unique_ptr<DeviceHierarchy3D> DeviceHierarchy3D::create(const Mesh3D& mesh,
     dl.stM = d->arena.upload(stM);
     dl.inv_c = d->arena.upload(lv.inv_c);
     dl.pat_color = d->arena.upload(lv.pat_color);
+    dl.col_pat = d->arena.upload(col_pat[l]);
+    if (!pat_node[l].empty()) {
+      dl.pat_ptr = d->arena.upload(pat_ptr[l]);
+      dl.pat_node = d->arena.upload(pat_node[l]);
+      dl.pat_max = pat_max[l];
+    }
     dl.own_dot = d->arena.upload(own[l]);
     dl.psK = d->arena.upload(lv.psK);
     dl.psM = d->arena.upload(lv.psM);
@@ -404,13 +459,11 @@ void Solver3D::vcycle(int l, double* u, const double* b) {
     mark(KK_CG0, 0.0);
     return;
   }
-  const int colors = lev[l].colors;
-  const int gs_launches = colors * (lev[l].n >= 4 ? 2 : 1);
   // algorithmic bytes per unique DoF: GS 24/sweep, residual 24,
   // restriction 8 fine + 8 coarse, prolongation+correction 16 fine + 8 coarse
   if (cfg_.pre_smooth > 0) {
     launch3_gs(lev[l], u, b, cfg_.pre_smooth, stream_);
-    mark(KK_GS, 24.0 * cfg_.pre_smooth * dofs(l), gs_launches * cfg_.pre_smooth);
+    mark(KK_GS, 24.0 * cfg_.pre_smooth * dofs(l), launch3_gs_count(lev[l], cfg_.pre_smooth));
   }
   launch3_apply(lev[l], false, u, r_[l], b, A3_RES_OWNER, stream_);
   mark(KK_RESIDUAL, 24.0 * dofs(l));
@@ -423,7 +476,7 @@ void Solver3D::vcycle(int l, double* u, const double* b) {
   mark(KK_PROLONG, 16.0 * dofs(l) + 8.0 * dofs(l - 1));
   if (cfg_.post_smooth > 0) {
     launch3_gs(lev[l], u, b, cfg_.post_smooth, stream_);
-    mark(KK_GS, 24.0 * cfg_.post_smooth * dofs(l), gs_launches * cfg_.post_smooth);
+    mark(KK_GS, 24.0 * cfg_.post_smooth * dofs(l), launch3_gs_count(lev[l], cfg_.post_smooth));
   }
 }
 

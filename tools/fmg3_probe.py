@@ -42,3 +42,4 @@ for kk in range(8):
     m_, n_, b_ = s.kernel_stats(kk)
     if n_:
         print(f"  {names[kk]:12s} {m_:9.3f} ms  {n_:5d} launches  alg {b_/(m_*1e-3)/1e9 if m_>0 else 0:8.1f} GB/s")
+print("level-0 CG iterations (last call):", s.last_cg_iterations())
