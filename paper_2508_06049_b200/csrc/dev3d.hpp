@@ -46,6 +46,7 @@ struct DevLevel3D {
   const int* cg_mterm;         // members + 1
   const double* cg_coef;
   const int* cg_vid;
+  int cg_members4;             // member count when every member has exactly 4 terms, else 0
 };
 
 enum Apply3Mode : int {

@@ -648,6 +648,43 @@ __device__ void cg0_apply(const DevLevel3D& lv, const double* x, double* y, cons
   }
 }
 
+// Same operator, member-parallel (every level-0 member has exactly 4 terms):
+// the members' partial rows into mp[] (the loads of 4 members in flight per
+// thread), then per group the member sum in slot order from shared memory.
+__device__ void cg0_apply4(const DevLevel3D& lv, const double* x, double* y, const double* b,
+                           const unsigned char* dom, int residual, double* mp, int nmem) {
+  const double2* cf = reinterpret_cast<const double2*>(lv.cg_coef);
+  const int4* vi = reinterpret_cast<const int4*>(lv.cg_vid);
+  constexpr int U = 4;
+  for (int q0 = threadIdx.x; q0 < nmem; q0 += U * blockDim.x) {
+    double2 c[U][2];
+    int4 v[U];
+#pragma unroll
+    for (int a = 0; a < U; ++a) {
+      const int q = min(q0 + a * static_cast<int>(blockDim.x), nmem - 1);
+      c[a][0] = __ldg(cf + 2 * q);
+      c[a][1] = __ldg(cf + 2 * q + 1);
+      v[a] = __ldg(vi + q);
+    }
+#pragma unroll
+    for (int a = 0; a < U; ++a) {
+      const int q = q0 + a * static_cast<int>(blockDim.x);
+      double acc = c[a][0].x * x[v[a].x];
+      acc = acc + c[a][0].y * x[v[a].y];
+      acc = acc + c[a][1].x * x[v[a].z];
+      acc = acc + c[a][1].y * x[v[a].w];
+      if (q < nmem) mp[q] = acc;
+    }
+  }
+  __syncthreads();
+  for (int g = threadIdx.x; g < lv.ng; g += blockDim.x) {
+    const int m0 = lv.cg_gmem[g], m1 = lv.cg_gmem[g + 1];
+    double v = 0.0;
+    for (int q = m0; q < m1; ++q) v = (m1 - m0 == 1) ? mp[q] : v + mp[q];
+    y[g] = dom[g] ? 0.0 : (residual ? b[g] - v : v);
+  }
+}
+
 __device__ double cg0_dot(int ng, const double* a, const double* b, const unsigned char* dom, bool zero_dom,
                           double* chunks) {
   const int nch = (ng + 31) / 32;
@@ -673,7 +710,7 @@ __device__ double cg0_dot(int ng, const double* a, const double* b, const unsign
 }
 
 __global__ void __launch_bounds__(1024) k3_cg0(DevLevel3D lv, double* uc, const double* bc, CgParams prm,
-                                               DevStatus* status) {
+                                               DevStatus* status, int nmem4) {
   extern __shared__ double sm[];
   const int ng = lv.ng;
   double* u = sm;
@@ -682,14 +719,21 @@ __global__ void __launch_bounds__(1024) k3_cg0(DevLevel3D lv, double* uc, const 
   double* p = r + ng;
   double* ap = p + ng;
   double* chunks = ap + ng;
-  unsigned char* dom = reinterpret_cast<unsigned char*>(chunks + (ng + 31) / 32);
+  double* mp = chunks + (ng + 31) / 32;  // nmem4 member partials (member-parallel operator)
+  unsigned char* dom = reinterpret_cast<unsigned char*>(mp + nmem4);
+  auto cg0_op = [&](const double* x, double* y, const double* bb, int residual) {
+    if (nmem4 > 0)
+      cg0_apply4(lv, x, y, bb, dom, residual, mp, nmem4);
+    else
+      cg0_apply(lv, x, y, bb, dom, residual);
+  };
   for (int g = threadIdx.x; g < ng; g += blockDim.x) {
     u[g] = uc[lv.own_dot[g]];
     b[g] = bc[lv.own_dot[g]];
     dom[g] = lv.grp_domain[g];
   }
   __syncthreads();
-  cg0_apply(lv, u, r, b, dom, 1);
+  cg0_op(u, r, b, 1);
   __syncthreads();
   for (int g = threadIdx.x; g < ng; g += blockDim.x) p[g] = r[g];
   double rr = cg0_dot(ng, r, r, dom, false, chunks);
@@ -704,7 +748,7 @@ __global__ void __launch_bounds__(1024) k3_cg0(DevLevel3D lv, double* uc, const 
       }
       break;
     }
-    cg0_apply(lv, p, ap, nullptr, dom, 0);
+    cg0_op(p, ap, nullptr, 0);
     const double pap = cg0_dot(ng, p, ap, dom, false, chunks);
     if (pap <= 0.0) {
       if (threadIdx.x == 0 && status->code == 0) {
@@ -818,6 +862,82 @@ __global__ void __launch_bounds__(kT) k3_estimate(DevLevel3D lv, const double* _
   if (threadIdx.x == 0) {
     part[2 * static_cast<size_t>(blockIdx.x)] = rb[0];
     part[2 * static_cast<size_t>(blockIdx.x) + 1] = rcs[0];
+  }
+}
+
+// Node-centric form of the same sums: over a macro, sum_cells e_c^T M_c e_c
+// = sum_nodes e_i (M_m e)_i with M_m the macro's assembled mass matrix (the
+// interior stencil stM, the signature partial stencils psM on the lattice
+// boundary).  One block per (macro, plane k), rows to warps, nodes to lanes
+// (coalesced); e = uL - w formed at each load.  Same sums as the cell form up
+// to rounding (the tests bound the difference).
+__global__ void __launch_bounds__(kT) k3_estimate_nodes(DevLevel3D lv, const double* __restrict__ uL,
+                                                        const double* __restrict__ wb,
+                                                        const double* __restrict__ wc, double* part) {
+  const int n = lv.n, S = lv.S;
+  const int m = blockIdx.x / (n + 1), k = blockIdx.x - m * (n + 1);
+  const int m2 = n - k;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  const size_t mo = static_cast<size_t>(m) * S;
+  const double* um = uL + mo;
+  const double* bm = wb + mo;
+  const double* cm = wc + mo;
+  double qb = 0.0, qc = 0.0;
+  for (int j = warp; j <= m2; j += nwarps) {
+    int ra[7], len[7];
+    node_rows(n, j, k, ra, len);
+    for (int i = lane; i <= m2 - j; i += 32) {
+      const int sig = sig3(n, i, j, k);
+      const double* cf = sig ? lv.psM + 240 * static_cast<size_t>(m) + 15 * sig : lv.stM + 15 * static_cast<size_t>(m);
+      const int c0 = ra[0] + i;
+      bool ok[15];
+      const double *au[15], *ab[15], *ac[15];
+#pragma unroll
+      for (int d = 0; d < 15; ++d) {
+        const int r = dir_row(d), ii = i + dir_di(d);
+        ok[d] = ii >= 0 && ii <= len[r];
+        const int o = ok[d] ? ra[r] + ii : c0;
+        au[d] = um + o;
+        ab[d] = bm + o;
+        ac[d] = cm + o;
+      }
+      double xu[15], xb[15], xc[15], c[15];
+      load15(xu, au);
+      load15(xb, ab);
+      load15(xc, ac);
+      load15_seq(c, cf);
+      const double eb0 = xu[0] - xb[0], ec0 = xu[0] - xc[0];
+      double mb = c[0] * eb0, mc = c[0] * ec0;
+#pragma unroll
+      for (int d = 1; d < 15; ++d) {
+        const double tb = mb + c[d] * (xu[d] - xb[d]);
+        const double tc = mc + c[d] * (xu[d] - xc[d]);
+        mb = ok[d] ? tb : mb;
+        mc = ok[d] ? tc : mc;
+      }
+      qb = qb + eb0 * mb;
+      qc = qc + ec0 * mc;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    qb += __shfl_xor_sync(0xffffffffu, qb, o);
+    qc += __shfl_xor_sync(0xffffffffu, qc, o);
+  }
+  __shared__ double rb[kT / 32], rcs[kT / 32];
+  if (lane == 0) {
+    rb[warp] = qb;
+    rcs[warp] = qc;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double sb = 0.0, sc = 0.0;
+    for (int w = 0; w < nwarps; ++w) {
+      sb += rb[w];
+      sc += rcs[w];
+    }
+    part[2 * static_cast<size_t>(blockIdx.x)] = sb;
+    part[2 * static_cast<size_t>(blockIdx.x) + 1] = sc;
   }
 }
 
@@ -1069,17 +1189,28 @@ void launch3_cg0(const DevLevel3D& lv0, double* u, const double* b, double* scra
                  DevStatus* status, cudaStream_t st) {
   (void)scratch;
   init_constants();
-  const size_t smem = (5 * static_cast<size_t>(lv0.ng) + (lv0.ng + 31) / 32) * sizeof(double) + lv0.ng + 16;
-  if (smem > 200 * 1024) fail(KB_STRUCTURAL, "coarse mesh too large for the level-0 CG (more than ~4800 vertices)");
+  const size_t base = (5 * static_cast<size_t>(lv0.ng) + (lv0.ng + 31) / 32) * sizeof(double) + lv0.ng + 16;
+  if (base > 200 * 1024) fail(KB_STRUCTURAL, "coarse mesh too large for the level-0 CG (more than ~4800 vertices)");
+  // member-parallel operator when the member partials fit next to the vectors
+  const int nmem4 = lv0.cg_members4 > 0 && base + lv0.cg_members4 * 8.0 <= 200 * 1024 ? lv0.cg_members4 : 0;
+  const size_t smem = base + static_cast<size_t>(nmem4) * 8;
   KB_CUDA_CHECK(cudaFuncSetAttribute(k3_cg0, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  k3_cg0<<<1, 1024, smem, st>>>(lv0, u, b, prm, status);
+  k3_cg0<<<1, 1024, smem, st>>>(lv0, u, b, prm, status, nmem4);
   check3("k3_cg0");
 }
 
 void launch3_estimate(const DevLevel3D& lv, const double* uL, const double* wb, const double* wc, double* sums,
                       double* part, cudaStream_t st) {
   init_constants();
-  k3_estimate<<<lv.M * (lv.n + 1), kT, 0, st>>>(lv, uL, wb, wc, part);
+  static int cells = -1;
+  if (cells < 0) {
+    const char* e = getenv("KB_EST3_CELLS");  // measurement: the cell-by-cell form
+    cells = e && e[0] == '1';
+  }
+  if (cells)
+    k3_estimate<<<lv.M * (lv.n + 1), kT, 0, st>>>(lv, uL, wb, wc, part);
+  else
+    k3_estimate_nodes<<<lv.M * (lv.n + 1), kT, 0, st>>>(lv, uL, wb, wc, part);
   check3("k3_estimate");
   k3_estimate_reduce<<<(lv.M + 127) / 128, 128, 0, st>>>(lv.M, lv.n + 1, part, sums);
   check3("k3_estimate_reduce");

@@ -177,6 +177,9 @@ std::unique_ptr<DeviceHierarchy3D> DeviceHierarchy3D::create(const Mesh3D& mesh,
       dl.cg_mterm = d->arena.upload(cg_mterm);
       dl.cg_coef = d->arena.upload(cg_coef);
       dl.cg_vid = d->arena.upload(cg_vid);
+      bool four = true;
+      for (size_t q = 0; q + 1 < cg_mterm.size(); ++q) four = four && cg_mterm[q + 1] - cg_mterm[q] == 4;
+      dl.cg_members4 = four ? static_cast<int>(cg_mterm.size()) - 1 : 0;
     }
     d->lev.push_back(dl);
   }
