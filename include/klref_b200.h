@@ -221,6 +221,44 @@ int klref_interface_sync(klref_solver s, klref_gf f, int mode);               /*
 int klref_mark(int rule, double fraction, int num_active, const int* active_ids, const int* green_parent,
                const double* indicator, int num_reverted, const int* reverted_ids, int* marks_out, int* num_marks);
 
+/* ---- sharded 3-d solve (no reference counterpart) ------
+ * The reference is single-process.  Its paper partitions macro
+ * elements with ghost layers on the interface primitives;
+ * these entry points run MultigridSolver::fmg / error_estimate
+ * (proj/src/multigrid.cpp:248-321, proj/src/estimator.cpp:8-45) over
+ * contiguous macro slot ranges, one shard per GPU over NCCL (comm != NULL)
+ * or `local_shards` shards in this process on one device (comm == NULL, the
+ * parity harness).  Levels <= rep_level are replicated on every shard.
+ * Results are bit-identical to klref_solver_* on the same hierarchy. */
+typedef struct klref_comm_s* klref_comm;
+typedef struct klref_sharded_s* klref_sharded;
+int klref_comm_unique_id(unsigned char id[128]);
+int klref_comm_create(int nranks, int rank, const unsigned char id[128], klref_comm* out);
+void klref_comm_destroy(klref_comm c);
+int klref_sharded_create(klref_hierarchy h, klref_problem p, const klref_solver_config* cfg, klref_comm comm,
+                         int local_shards, int rep_level, klref_sharded* out);
+void klref_sharded_destroy(klref_sharded s);
+int klref_sharded_fmg(klref_sharded s);
+int klref_sharded_fmg_enqueue(klref_sharded s);
+int klref_sharded_synchronize(klref_sharded s);
+int klref_sharded_stream(klref_sharded s, void** stream);
+/* kernel launches per FMG / per estimate (all local shards), bytes one FMG exchanges */
+int klref_sharded_counts(klref_sharded s, int* fmg_launches, int* estimate_launches, double* exchange_bytes);
+int klref_sharded_error_estimate_enqueue(klref_sharded s, int offset);
+int klref_sharded_error_estimate_finish(klref_sharded s, int offset, int kind, klref_estimate_report* out,
+                                        double* eta_local);
+/* full level array (M * S); over NCCL only this rank's slot range and the replicated levels are written */
+int klref_sharded_state_read(klref_sharded s, int which, int level, double* host_out);
+/* exchange plan of one shard on one level (host only; plan checks):
+ * send_counts / recv_counts[nshards * colors] (peer-major), *colors, and per
+ * buffer position the (global group, slot, lattice index) of the member whose
+ * contribution travels there: send_keys[3 * send_total], recv_keys[3 * recv_total].
+ * NULL key arrays query the counts only. */
+int klref_shard_plan(klref_hierarchy h, int nshards, int rank, int rep_level, int level, int* colors,
+                     int64_t* send_counts, int64_t* recv_counts, int* send_keys, int* recv_keys);
+/* shard slot ranges starts[nshards + 1] of the hierarchy (host only) */
+int klref_shard_starts(int num_macros, int nshards, int* starts);
+
 #ifdef __cplusplus
 }
 #endif

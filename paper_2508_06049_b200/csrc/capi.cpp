@@ -15,6 +15,7 @@
 
 #include "solver2d.hpp"
 #include "solver3d.hpp"
+#include "solver3d_shard.hpp"
 
 struct klref_mesh_s {
   int dim = 2;
@@ -36,6 +37,12 @@ struct klref_solver_s {
   std::unique_ptr<kb::Solver2D> s;
   std::unique_ptr<kb::Solver3D> s3;
   klref_hierarchy_s* h = nullptr;
+};
+struct klref_comm_s {
+  std::shared_ptr<kb::NcclComm> c;
+};
+struct klref_sharded_s {
+  std::unique_ptr<kb::ShardedSolver3D> s;
 };
 struct klref_gf_s {
   double* d = nullptr;
@@ -643,6 +650,156 @@ int klref_mark(int rule, double fraction, int num_active, const int* active_ids,
     std::sort(marks.begin(), marks.end());
     std::copy(marks.begin(), marks.end(), marks_out);
     *num_marks = static_cast<int>(marks.size());
+  });
+}
+
+int klref_comm_unique_id(unsigned char id[128]) {
+  return guarded([&] {
+    need(id, "id");
+    kb::NcclComm::unique_id(id);
+  });
+}
+int klref_comm_create(int nranks, int rank, const unsigned char id[128], klref_comm* out) {
+  return guarded([&] {
+    need(id, "id");
+    need(out, "out");
+    require_device();
+    auto c = std::make_unique<klref_comm_s>();
+    c->c = std::make_shared<kb::NcclComm>(nranks, rank, id);
+    *out = c.release();
+  });
+}
+void klref_comm_destroy(klref_comm c) { delete c; }
+
+int klref_sharded_create(klref_hierarchy h, klref_problem p, const klref_solver_config* cfg, klref_comm comm,
+                         int local_shards, int rep_level, klref_sharded* out) {
+  return guarded([&] {
+    need(h, "h");
+    need(p, "problem");
+    need(out, "out");
+    require_device();
+    if (!h->on_device) kb::fail(kb::KB_STRUCTURAL, "hierarchy was built host-only");
+    if (h->dim != 3) kb::fail(kb::KB_STRUCTURAL, "sharding is defined for 3-d hierarchies (the 2-d path is exact-order)");
+    if (!(p->dims & 2)) kb::fail(kb::KB_STRUCTURAL, "a 2-d problem cannot drive a 3-d hierarchy");
+    kb::SolverConfig2D c;
+    if (cfg) {
+      c.nu = cfg->nu;
+      c.pre_smooth = cfg->pre_smooth;
+      c.post_smooth = cfg->post_smooth;
+      c.coarse_rel_tol = cfg->coarse_rel_tol;
+      c.coarse_abs_floor = cfg->coarse_abs_floor;
+      c.coarse_max_iter = cfg->coarse_max_iter;
+      c.finest_policy = cfg->finest_policy;
+      c.faithful_source = cfg->faithful_source;
+      c.use_graph = cfg->use_graph;
+    }
+    auto s = std::make_unique<klref_sharded_s>();
+    s->s = std::make_unique<kb::ShardedSolver3D>(h->dev3, p->p3, c, local_shards, rep_level,
+                                                 comm ? comm->c : nullptr);
+    *out = s.release();
+  });
+}
+void klref_sharded_destroy(klref_sharded s) { delete s; }
+int klref_sharded_fmg(klref_sharded s) {
+  return guarded([&] {
+    need(s, "solver");
+    s->s->fmg();
+  });
+}
+int klref_sharded_fmg_enqueue(klref_sharded s) {
+  return guarded([&] {
+    need(s, "solver");
+    s->s->fmg_enqueue();
+  });
+}
+int klref_sharded_synchronize(klref_sharded s) {
+  return guarded([&] {
+    need(s, "solver");
+    s->s->sync_and_check();
+  });
+}
+int klref_sharded_stream(klref_sharded s, void** stream) {
+  return guarded([&] {
+    need(s, "solver");
+    need(stream, "stream");
+    *stream = reinterpret_cast<void*>(s->s->stream());
+  });
+}
+int klref_sharded_counts(klref_sharded s, int* fmg_launches, int* estimate_launches, double* exchange_bytes) {
+  return guarded([&] {
+    need(s, "solver");
+    if (fmg_launches) *fmg_launches = s->s->launches_per_fmg();
+    if (estimate_launches) *estimate_launches = s->s->launches_per_estimate();
+    if (exchange_bytes) *exchange_bytes = s->s->exchange_bytes_per_fmg();
+  });
+}
+int klref_sharded_error_estimate_enqueue(klref_sharded s, int offset) {
+  return guarded([&] {
+    need(s, "solver");
+    s->s->estimate_enqueue(offset);
+  });
+}
+int klref_sharded_error_estimate_finish(klref_sharded s, int offset, int kind, klref_estimate_report* out,
+                                        double* eta_local) {
+  return guarded([&] {
+    need(s, "solver");
+    fill_report(s->s->estimate_finish(offset, kind), out, eta_local);
+  });
+}
+int klref_sharded_state_read(klref_sharded s, int which, int level, double* host_out) {
+  return guarded([&] {
+    need(s, "solver");
+    need(host_out, "host_out");
+    s->s->state_read(which, level, host_out);
+  });
+}
+int klref_shard_plan(klref_hierarchy h, int nshards, int rank, int rep_level, int level, int* colors,
+                     int64_t* send_counts, int64_t* recv_counts, int* send_keys, int* recv_keys) {
+  return guarded([&] {
+    need(h, "h");
+    if (h->dim != 3) kb::fail(kb::KB_STRUCTURAL, "sharding is defined for 3-d hierarchies");
+    check_level(h, level);
+    const kb::Hierarchy3D& hh = h->dev3->host;
+    const kb::ShardPlan3D plan = kb::build_shard_plan(hh, nshards, rank, rep_level);
+    if (colors) *colors = hh.colors;
+    const int C = hh.colors;
+    const kb::ShardLevel3D& sl = plan.lev[level];
+    for (int p = 0; p < nshards; ++p)
+      for (int c = 0; c < C; ++c) {
+        const size_t o = static_cast<size_t>(p) * (C + 1) + c;
+        if (send_counts) send_counts[p * C + c] = plan.sharded(level) ? sl.send_off[o + 1] - sl.send_off[o] : 0;
+        if (recv_counts) recv_counts[p * C + c] = plan.sharded(level) ? sl.recv_off[o + 1] - sl.recv_off[o] : 0;
+      }
+    if (!plan.sharded(level)) return;
+    if (send_keys)
+      for (size_t e = 0; e < sl.pack_pos.size(); ++e) {
+        int* k = send_keys + 3 * static_cast<size_t>(sl.pack_pos[e]);
+        k[0] = sl.pack_gid[e];
+        k[1] = sl.pack_slot[e] + plan.s0;
+        k[2] = sl.pack_idx[e];
+      }
+    if (recv_keys) {
+      const kb::Level3D& lv = hh.levels[level];
+      for (int g = 0; g < sl.ng; ++g) {
+        const int gg = sl.gid[g];
+        for (int q = sl.grp_ptr[g]; q < sl.grp_ptr[g + 1]; ++q) {
+          if (sl.mem_slot[q] >= 0) continue;
+          const int gq = lv.grp_ptr[gg] + (q - sl.grp_ptr[g]);
+          int* k = recv_keys + 3 * static_cast<size_t>(~sl.mem_slot[q]);
+          k[0] = gg;
+          k[1] = lv.mem_slot[gq];
+          k[2] = lv.mem_idx[gq];
+        }
+      }
+    }
+  });
+}
+int klref_shard_starts(int num_macros, int nshards, int* starts) {
+  return guarded([&] {
+    need(starts, "starts");
+    if (nshards < 1 || nshards > num_macros) kb::fail(kb::KB_STRUCTURAL, "shard count out of range");
+    const std::vector<int> st = kb::shard_starts(num_macros, nshards);
+    std::copy(st.begin(), st.end(), starts);
   });
 }
 

@@ -47,6 +47,11 @@ struct DevLevel3D {
   const double* cg_coef;
   const int* cg_vid;
   int cg_members4;             // member count when every member has exactly 4 terms, else 0
+  // sharded levels (solver3d_shard.cpp): a member with mem_slot < 0 lives on
+  // another shard; its contribution (partial row or copy value, as the
+  // operation needs) is ghost[~mem_slot], received by the exchange before the
+  // kernel runs, and its copy is written by its own shard
+  const double* ghost;
 };
 
 enum Apply3Mode : int {
@@ -68,6 +73,11 @@ void launch3_prolong(const DevLevel3D& coarse, const DevLevel3D& fine, const dou
 // coarse additive sync; zero_domain: coarse domain-boundary copies 0
 void launch3_restrict(const DevLevel3D& fine, const DevLevel3D& coarse, const double* rf, double* rc,
                       int zero_domain, cudaStream_t st);
+// the restriction alone over coarse.M macros (no sync; sharded levels)
+void launch3_restrict_only(const DevLevel3D& fine, const DevLevel3D& coarse, const double* rf, double* rc,
+                           cudaStream_t st);
+// interface sync with optional zero of the domain-boundary copies
+void launch3_sync_zero(const DevLevel3D& lv, double* f, int additive, int zero_domain, cudaStream_t st);
 // zero the non-owner copies of f into out (single-operation restriction)
 void launch3_owner_mask(const DevLevel3D& lv, const double* f, double* out, cudaStream_t st);
 // set domain-boundary copies to g (per group); zero_rest: other nodes 0
@@ -81,6 +91,16 @@ void launch3_estimate(const DevLevel3D& lv, const double* uL, const double* wb, 
                       double* part, cudaStream_t st);
 void launch3_dot(const DevLevel3D& lv, const double* a, const double* b, double* partial, double* out,
                  cudaStream_t st);
+// exchange pack: out[pos[e]] = contribution of local member e (slot, ijk) for
+// the entries [e0, e1): mode 0 copy value of x, 1 stiffness partial row of x,
+// 2 mass partial row of x, 3 off-diagonal stiffness partial row (smoother)
+enum Pack3Mode : int { PK3_VALUE = 0, PK3_FULL_K = 1, PK3_FULL_M = 2, PK3_OFF_K = 3 };
+void launch3_pack(const DevLevel3D& lv, int mode, const double* x, const int* pos, const int* slot, const int* ijk,
+                  int e0, int e1, double* out, cudaStream_t st);
+// boundary colour c of the smoother alone (one group per thread)
+void launch3_gs_color_groups(const DevLevel3D& lv, double* u, const double* b, int c, cudaStream_t st);
+// interior phase of the smoother alone (every macro, all colours, one sweep)
+void launch3_gs_interior(const DevLevel3D& lv, double* u, const double* b, cudaStream_t st);
 void launch3_axpy(double* y, const double* x, double alpha, std::int64_t count, cudaStream_t st);
 
 }  // namespace kb

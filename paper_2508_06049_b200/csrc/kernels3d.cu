@@ -222,6 +222,7 @@ __global__ void __launch_bounds__(kT) k3_apply(DevLevel3D lv, int mass, const do
   double v;
   auto part = [&](int q) {
     const int s = lv.mem_slot[q];
+    if (s < 0) return lv.ghost[~s];  // another shard's member (sharded levels)
     int i, j, k;
     unpack_ijk(lv.mem_ijk[q], i, j, k);
     return partial_full(K + 240 * s, x + static_cast<size_t>(s) * S, n, i, j, k);
@@ -234,6 +235,7 @@ __global__ void __launch_bounds__(kT) k3_apply(DevLevel3D lv, int mass, const do
   }
   const bool dom = lv.grp_domain[g];
   for (int q = beg; q < end; ++q) {
+    if (lv.mem_slot[q] < 0) continue;
     int i, j, k;
     unpack_ijk(lv.mem_ijk[q], i, j, k);
     const size_t off = static_cast<size_t>(lv.mem_slot[q]) * S + lat3(n, i, j, k);
@@ -256,9 +258,11 @@ __device__ void gs_group(const DevLevel3D& lv, double* u, const double* __restri
   const int n = lv.n, S = lv.S;
   stamp(tr, 0);
   const int beg = lv.grp_ptr[g], end = lv.grp_ptr[g + 1];
+  int ql = beg;  // first member on this shard: b's copies are interface-consistent
+  while (lv.mem_slot[ql] < 0) ++ql;
   int i0, j0, k0;
-  unpack_ijk(lv.mem_ijk[beg], i0, j0, k0);
-  const size_t own = static_cast<size_t>(lv.mem_slot[beg]) * S + lat3(n, i0, j0, k0);
+  unpack_ijk(lv.mem_ijk[ql], i0, j0, k0);
+  const size_t own = static_cast<size_t>(lv.mem_slot[ql]) * S + lat3(n, i0, j0, k0);
   double val;
   if (lv.grp_domain[g]) {
     val = b[own];
@@ -266,6 +270,10 @@ __device__ void gs_group(const DevLevel3D& lv, double* u, const double* __restri
     double off = 0.0;
     for (int q = beg; q < end; ++q) {
       const int s = lv.mem_slot[q];
+      if (s < 0) {
+        off = off + lv.ghost[~s];
+        continue;
+      }
       int i, j, k;
       unpack_ijk(lv.mem_ijk[q], i, j, k);
       stamp(tr, 1 + 2 * (q - beg));
@@ -276,6 +284,7 @@ __device__ void gs_group(const DevLevel3D& lv, double* u, const double* __restri
   }
   if (tr) tr[8] = clock64() + (val == 12345.0 ? 1 : 0);
   for (int q = beg; q < end; ++q) {
+    if (lv.mem_slot[q] < 0) continue;
     int i, j, k;
     unpack_ijk(lv.mem_ijk[q], i, j, k);
     u[static_cast<size_t>(lv.mem_slot[q]) * S + lat3(n, i, j, k)] = val;
@@ -390,9 +399,11 @@ __device__ void gs_interior_batch(const DevLevel3D& lv, double* u, const double*
 __device__ void gs_group_warp(const DevLevel3D& lv, double* u, const double* __restrict__ b, int g, int lane) {
   const int n = lv.n, S = lv.S;
   const int beg = lv.grp_ptr[g], end = lv.grp_ptr[g + 1];
+  int ql = beg;
+  while (lv.mem_slot[ql] < 0) ++ql;
   int i0, j0, k0;
-  unpack_ijk(lv.mem_ijk[beg], i0, j0, k0);
-  const size_t own = static_cast<size_t>(lv.mem_slot[beg]) * S + lat3(n, i0, j0, k0);
+  unpack_ijk(lv.mem_ijk[ql], i0, j0, k0);
+  const size_t own = static_cast<size_t>(lv.mem_slot[ql]) * S + lat3(n, i0, j0, k0);
   double val;
   if (lv.grp_domain[g]) {
     val = b[own];
@@ -403,9 +414,13 @@ __device__ void gs_group_warp(const DevLevel3D& lv, double* u, const double* __r
       const int q = q0 + lane;
       if (q < end) {
         const int s = lv.mem_slot[q];
-        int i, j, k;
-        unpack_ijk(lv.mem_ijk[q], i, j, k);
-        part = partial_off3(lv.psK + 240 * s, u + static_cast<size_t>(s) * S, n, i, j, k);
+        if (s < 0) {
+          part = lv.ghost[~s];
+        } else {
+          int i, j, k;
+          unpack_ijk(lv.mem_ijk[q], i, j, k);
+          part = partial_off3(lv.psK + 240 * s, u + static_cast<size_t>(s) * S, n, i, j, k);
+        }
       }
       const int cnt = min(32, end - q0);
       for (int t = 0; t < cnt; ++t) off = off + __shfl_sync(0xffffffffu, part, t);
@@ -413,6 +428,7 @@ __device__ void gs_group_warp(const DevLevel3D& lv, double* u, const double* __r
     val = (b[own] - off) / lv.grp_diag[g];
   }
   for (int q = beg + lane; q < end; q += 32) {
+    if (lv.mem_slot[q] < 0) continue;
     int i, j, k;
     unpack_ijk(lv.mem_ijk[q], i, j, k);
     u[static_cast<size_t>(lv.mem_slot[q]) * S + lat3(n, i, j, k)] = val;
@@ -589,19 +605,22 @@ __global__ void __launch_bounds__(kT) k3_sync(DevLevel3D lv, double* f, int addi
     unpack_ijk(lv.mem_ijk[q], i, j, k);
     return static_cast<size_t>(lv.mem_slot[q]) * S + lat3(n, i, j, k);
   };
+  auto val_of = [&](int q) { return lv.mem_slot[q] < 0 ? lv.ghost[~lv.mem_slot[q]] : f[off_of(q)]; };
   if (zero_domain && lv.grp_domain[g]) {
-    for (int q = beg; q < end; ++q) f[off_of(q)] = 0.0;
+    for (int q = beg; q < end; ++q)
+      if (lv.mem_slot[q] >= 0) f[off_of(q)] = 0.0;
     return;
   }
   if (end - beg < 2) return;
   double v;
   if (additive) {
     v = 0.0;
-    for (int q = beg; q < end; ++q) v += f[off_of(q)];
+    for (int q = beg; q < end; ++q) v += val_of(q);
   } else {
-    v = f[off_of(beg)];
+    v = val_of(beg);
   }
-  for (int q = beg; q < end; ++q) f[off_of(q)] = v;
+  for (int q = beg; q < end; ++q)
+    if (lv.mem_slot[q] >= 0) f[off_of(q)] = v;
 }
 
 __global__ void __launch_bounds__(kT) k3_owner_mask(DevLevel3D lv, double* f) {
@@ -609,6 +628,7 @@ __global__ void __launch_bounds__(kT) k3_owner_mask(DevLevel3D lv, double* f) {
   if (g >= lv.ng) return;
   const int n = lv.n, S = lv.S;
   for (int q = lv.grp_ptr[g] + 1; q < lv.grp_ptr[g + 1]; ++q) {
+    if (lv.mem_slot[q] < 0) continue;
     int i, j, k;
     unpack_ijk(lv.mem_ijk[q], i, j, k);
     f[static_cast<size_t>(lv.mem_slot[q]) * S + lat3(n, i, j, k)] = 0.0;
@@ -621,10 +641,33 @@ __global__ void __launch_bounds__(kT) k3_set_boundary(DevLevel3D lv, double* f, 
   const int n = lv.n, S = lv.S;
   const double v = g_grp[g];
   for (int q = lv.grp_ptr[g]; q < lv.grp_ptr[g + 1]; ++q) {
+    if (lv.mem_slot[q] < 0) continue;
     int i, j, k;
     unpack_ijk(lv.mem_ijk[q], i, j, k);
     f[static_cast<size_t>(lv.mem_slot[q]) * S + lat3(n, i, j, k)] = v;
   }
+}
+
+// exchange pack of a sharded level: the contribution of each local member of a
+// group that spans shards, computed by the same functions the group kernels
+// use, so that every shard sums bit-identical member terms in slot order
+__global__ void __launch_bounds__(kT) k3_pack(DevLevel3D lv, int mode, const double* __restrict__ x,
+                                              const int* __restrict__ pos, const int* __restrict__ slot,
+                                              const int* __restrict__ ijk, int e0, int e1, double* out) {
+  const int e = e0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= e1) return;
+  const int n = lv.n, s = slot[e];
+  int i, j, k;
+  unpack_ijk(ijk[e], i, j, k);
+  const double* xm = x + static_cast<size_t>(s) * lv.S;
+  double v;
+  if (mode == PK3_VALUE)
+    v = xm[lat3(n, i, j, k)];
+  else if (mode == PK3_OFF_K)
+    v = partial_off3(lv.psK + 240 * s, xm, n, i, j, k);
+  else
+    v = partial_full((mode == PK3_FULL_M ? lv.psM : lv.psK) + 240 * s, xm, n, i, j, k);
+  out[pos[e]] = v;
 }
 
 // ---------------------------------------------------------------- level-0 CG (one CTA)
@@ -1167,6 +1210,18 @@ void launch3_restrict(const DevLevel3D& fine, const DevLevel3D& coarse, const do
   check3("k3_sync");
 }
 
+void launch3_restrict_only(const DevLevel3D& fine, const DevLevel3D& coarse, const double* rf, double* rc,
+                           cudaStream_t st) {
+  init_constants();
+  k3_restrict<<<coarse.M * (coarse.n + 1), kT, 0, st>>>(fine, coarse, rf, rc);
+  check3("k3_restrict");
+}
+
+void launch3_sync_zero(const DevLevel3D& lv, double* f, int additive, int zero_domain, cudaStream_t st) {
+  k3_sync<<<blocks_for(lv.ng), kT, 0, st>>>(lv, f, additive, zero_domain);
+  check3("k3_sync");
+}
+
 void launch3_owner_mask(const DevLevel3D& lv, const double* f, double* out, cudaStream_t st) {
   KB_CUDA_CHECK(cudaMemcpyAsync(out, f, sizeof(double) * static_cast<size_t>(lv.M) * lv.S, cudaMemcpyDeviceToDevice,
                                 st));
@@ -1228,6 +1283,28 @@ void launch3_ftab(const DevLevel3D& lv, const double* corners, int kind, const d
   init_constants();
   k3_ftab<<<lv.M * (lv.n + 1), kT, 0, st>>>(lv, corners, kind, params, f);
   check3("k3_ftab");
+}
+
+void launch3_pack(const DevLevel3D& lv, int mode, const double* x, const int* pos, const int* slot, const int* ijk,
+                  int e0, int e1, double* out, cudaStream_t st) {
+  if (e1 <= e0) return;
+  k3_pack<<<blocks_for(e1 - e0), kT, 0, st>>>(lv, mode, x, pos, slot, ijk, e0, e1, out);
+  check3("k3_pack");
+}
+
+void launch3_gs_color_groups(const DevLevel3D& lv, double* u, const double* b, int c, cudaStream_t st) {
+  init_constants();
+  k3_gs_groups<<<blocks_for(lv.ng), kT, 0, st>>>(lv, u, b, c);
+  check3("k3_gs_groups");
+}
+
+void launch3_gs_interior(const DevLevel3D& lv, double* u, const double* b, cudaStream_t st) {
+  init_constants();
+  if (lv.n < 4) return;  // no lattice-interior nodes
+  for (int c = 0; c < lv.colors; ++c) {
+    k3_gs_color<<<lv.M * (lv.n + 1), kT, 0, st>>>(lv, u, b, c);
+    check3("k3_gs_color");
+  }
 }
 
 void launch3_axpy(double* y, const double* x, double alpha, std::int64_t count, cudaStream_t st) {

@@ -156,6 +156,21 @@ SIGNATURES = {
     "klref_dot_unique": (_I, [_P, _P, _P, _PD]),
     "klref_interface_sync": (_I, [_P, _P, _I]),
     "klref_mark": (_I, [_I, _D, _I, _PI, _PI, _PD, _I, _PI, _PI, _PI]),
+    "klref_comm_unique_id": (_I, [C.c_char_p]),
+    "klref_comm_create": (_I, [_I, _I, C.c_char_p, _PP]),
+    "klref_comm_destroy": (None, [_P]),
+    "klref_sharded_create": (_I, [_P, _P, C.POINTER(SolverConfigC), _P, _I, _I, _PP]),
+    "klref_sharded_destroy": (None, [_P]),
+    "klref_sharded_fmg": (_I, [_P]),
+    "klref_sharded_fmg_enqueue": (_I, [_P]),
+    "klref_sharded_synchronize": (_I, [_P]),
+    "klref_sharded_stream": (_I, [_P, _PP]),
+    "klref_sharded_counts": (_I, [_P, _PI, _PI, _PD]),
+    "klref_sharded_error_estimate_enqueue": (_I, [_P, _I]),
+    "klref_sharded_error_estimate_finish": (_I, [_P, _I, _I, C.POINTER(EstimateReportC), _PD]),
+    "klref_sharded_state_read": (_I, [_P, _I, _I, _PD]),
+    "klref_shard_starts": (_I, [_I, _I, _PI]),
+    "klref_shard_plan": (_I, [_P, _I, _I, _I, _I, _PI, _PI64, _PI64, _PI, _PI]),
 }
 
 
@@ -537,6 +552,106 @@ class MultigridSolver(_Handle):
         loc = np.zeros(self.h.num_macros())
         _check(lib().klref_error_estimate_finish(self.ptr, offset, kind, C.byref(rep), _dptr(loc)))
         return _report(rep, loc)
+
+
+def shard_starts(num_macros: int, nshards: int) -> np.ndarray:
+    """Contiguous macro slot ranges of the shards (starts[nshards + 1])."""
+    out = np.zeros(nshards + 1, dtype=np.int32)
+    _check(lib().klref_shard_starts(num_macros, nshards, _iptr(out)))
+    return out
+
+
+def shard_plan(h: "GridHierarchy", nshards: int, rank: int, rep_level: int, level: int):
+    """Exchange plan of one shard on one level (host only): send/recv segment
+    counts [nshards, colours] and the (group, slot, idx) key of every buffer
+    position, for plan-consistency checks."""
+    colors = C.c_int()
+    _check(lib().klref_shard_plan(h.ptr, nshards, rank, rep_level, level, C.byref(colors), None, None, None, None))
+    nc = colors.value
+    sc = np.zeros(nshards * nc, dtype=np.int64)
+    rc = np.zeros(nshards * nc, dtype=np.int64)
+    _check(lib().klref_shard_plan(h.ptr, nshards, rank, rep_level, level, C.byref(colors),
+                                  sc.ctypes.data_as(_PI64), rc.ctypes.data_as(_PI64), None, None))
+    sk = np.full((int(sc.sum()), 3), -1, dtype=np.int32)
+    rk = np.full((int(rc.sum()), 3), -1, dtype=np.int32)
+    _check(lib().klref_shard_plan(h.ptr, nshards, rank, rep_level, level, C.byref(colors),
+                                  sc.ctypes.data_as(_PI64), rc.ctypes.data_as(_PI64), _iptr(sk), _iptr(rk)))
+    return sc.reshape(nshards, nc), rc.reshape(nshards, nc), sk, rk
+
+
+class Comm(_Handle):
+    """NCCL communicator of the sharded solver (one rank per GPU).  The unique
+    id travels between ranks by whatever the caller uses (torch.distributed)."""
+    _destroy = "klref_comm_destroy"
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _check(lib().klref_comm_unique_id(buf))
+        return buf.raw
+
+    def __init__(self, nranks: int, rank: int, uid: bytes):
+        if len(uid) != 128:
+            raise StructuralError("NCCL unique id must be 128 bytes")
+        out = C.c_void_p()
+        _check(lib().klref_comm_create(nranks, rank, uid, C.byref(out)))
+        super().__init__(out.value)
+        self.nranks, self.rank = nranks, rank
+
+
+class ShardedSolver(_Handle):
+    """MultigridSolver::fmg + error_estimate over macro shards (3-d; SURVEY.md
+    §8(e)).  comm=None runs `local_shards` shards in this process on one
+    device (bit-identical to MultigridSolver; the parity harness); with a Comm
+    this process is one shard of comm.nranks."""
+    _destroy = "klref_sharded_destroy"
+
+    def __init__(self, h: GridHierarchy, problem: Problem, cfg: SolverConfig = SolverConfig(),
+                 comm: Optional[Comm] = None, local_shards: int = 1, rep_level: int = 3):
+        out = C.c_void_p()
+        c = cfg.c()
+        _check(lib().klref_sharded_create(h.ptr, problem.ptr, C.byref(c), comm.ptr if comm else None,
+                                          local_shards, rep_level, C.byref(out)))
+        super().__init__(out.value)
+        self.h, self.problem, self.cfg, self.comm = h, problem, cfg, comm
+
+    def fmg(self):
+        _check(lib().klref_sharded_fmg(self.ptr))
+
+    def fmg_enqueue(self):
+        _check(lib().klref_sharded_fmg_enqueue(self.ptr))
+
+    def synchronize(self):
+        _check(lib().klref_sharded_synchronize(self.ptr))
+
+    def stream(self) -> int:
+        p = C.c_void_p()
+        _check(lib().klref_sharded_stream(self.ptr, C.byref(p)))
+        return p.value or 0
+
+    def counts(self):
+        """(kernel launches per FMG, per estimate, bytes exchanged per FMG)."""
+        a, b, x = C.c_int(), C.c_int(), C.c_double()
+        _check(lib().klref_sharded_counts(self.ptr, C.byref(a), C.byref(b), C.byref(x)))
+        return a.value, b.value, x.value
+
+    def error_estimate_enqueue(self, offset: int = 1):
+        _check(lib().klref_sharded_error_estimate_enqueue(self.ptr, offset))
+
+    def error_estimate_finish(self, offset: int = 1, kind: int = UNSCALED) -> EstimateReport:
+        rep = EstimateReportC()
+        loc = np.zeros(self.h.num_macros())
+        _check(lib().klref_sharded_error_estimate_finish(self.ptr, offset, kind, C.byref(rep), _dptr(loc)))
+        return _report(rep, loc)
+
+    def error_estimate(self, offset: int = 1, kind: int = UNSCALED) -> EstimateReport:
+        self.error_estimate_enqueue(offset)
+        return self.error_estimate_finish(offset, kind)
+
+    def state(self, which: int, level: int) -> np.ndarray:
+        out = np.zeros(self.h.level_size(level), dtype=np.float64)
+        _check(lib().klref_sharded_state_read(self.ptr, which, level, _dptr(out)))
+        return out
 
 
 def _report(rep, loc):
