@@ -27,6 +27,8 @@ cpu_baseline = the patched reference (oracle/_ref/ref_driver, compiled from
             reported beside it for context.
 Multi-GPU: the 2-D parity path does not shard (exact Gauss-Seidel order,
 SURVEY.md §8(e)): N ranks run N independent replicas ("scaling": "weak").
+The 3-d configuration 5 does shard: at N > 1 its macros are split over the
+ranks (NCCL interface exchange; workloads_3d.cfg5_sharded, strong scaling).
 """
 import argparse
 import json
@@ -262,6 +264,57 @@ def run_3d(K, torch, name, N, L, prob, reps, peak):
             "build_s": build_s, "parity": "builder 3-d oracle (oracle/klref_oracle3d.c), bitwise on small cases"}
 
 
+def run_3d_sharded(K, torch, dist, world, rank, reps, peak, barrier, max_over_ranks):
+    """Config 5 strong scaling: the 3072 macro tets sharded over the `world`
+    GPUs (contiguous slot ranges = z-slabs), interface exchange over NCCL,
+    levels <= 3 replicated.  All ranks call this; rank 0 reports."""
+    from paper_2508_06049_b200.meshes import kuhn_cube, series_coefficients
+
+    L = 6
+    t0 = time.perf_counter()
+    h = K.GridHierarchy.build(kuhn_cube(8), L)
+    uid = [K.Comm.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    comm = K.Comm(world, rank, uid[0])
+    prob = K.Problem(K.PROBLEM_SERIES3D, series_coefficients())
+    s = K.ShardedSolver(h, prob, K.SolverConfig(nu=2), comm=comm, rep_level=3)
+    build_s = time.perf_counter() - t0
+    stream = torch.cuda.ExternalStream(s.stream())
+    flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
+    for _ in range(2):
+        s.fmg_enqueue()
+        s.error_estimate_enqueue(1)
+        s.synchronize()
+        rep = s.error_estimate_finish(1, K.UNSCALED)
+    times = []
+    for it in range(reps):
+        with torch.cuda.stream(stream):
+            flush.fill_(float(it))
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        s.fmg_enqueue()
+        s.error_estimate_enqueue(1)
+        e1.record(stream)
+        s.synchronize()
+        rep = s.error_estimate_finish(1, K.UNSCALED)
+        times.append(e0.elapsed_time(e1))
+    ms = max_over_ranks(sum(times) / len(times))
+    fl, el, xb = s.counts()
+    dofs = h.dof_count(L)
+    s.close()
+    comm.close()
+    return {"config": "cfg5: unit cube, 8^3 Kuhn cubes, l=6, sine series (g=0), macros sharded over the GPUs",
+            "n_gpus": world, "scaling": "strong", "dofs": dofs, "ms_fmg_plus_estimate": ms,
+            "value": dofs / (ms * 1e-3) / 1e9, "unit": "GDoF/s",
+            "fmg_roofline_aggregate": {"alg_bytes": fmg_bytes_3d(dofs, 2),
+                                       "frac": fmg_bytes_3d(dofs, 2) / (ms * 1e-3) / 1e9 / (peak * world)},
+            "exchange_bytes_per_fmg_rank0": xb, "launches_per_fmg_rank0": fl, "eta": rep.eta,
+            "theta": rep.conv_factor, "build_s": build_s, "rep_level": 3,
+            "parity": "bitwise equal to the one-device solver (tests/test_shard_3d.py, in-process shards)"}
+
+
 def cpu_3d_port_sample():
     """Single-threaded 3-d C oracle on a bounded sample (config 3 mesh, l = 4)."""
     from oracle import oracle as O
@@ -291,7 +344,12 @@ def impl_ours(args):
     if not torch.cuda.is_available():
         raise SystemExit("bench.py: no CUDA device (the hot path has no CPU fallback)")
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 or args.force_sharded_3d:
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     K.lib()
 
@@ -396,6 +454,13 @@ def impl_ours(args):
     t_e2e = max_over_ranks(sum(e2e_ms) / len(e2e_ms))
     _ = rep
 
+    sharded3d = None
+    if (world > 1 or args.force_sharded_3d) and not args.no_3d:
+        try:
+            sharded3d = run_3d_sharded(K, torch, dist, world, rank, 3, peaks()[0], barrier, max_over_ranks)
+        except Exception as exc:  # secondary numbers never sink the headline line
+            sharded3d = {"error": str(exc)[:300]}
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -443,7 +508,9 @@ def impl_ours(args):
             cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference", "sample": f"failed: {exc}"}
 
     extra3d = None
-    if not args.no_3d:
+    if (world > 1 or args.force_sharded_3d) and not args.no_3d:
+        extra3d = {"cfg5_sharded": sharded3d}
+    elif not args.no_3d:
         try:
             peak3, _ = peaks()
             extra3d = {"cfg3": run_3d(K, torch, "cfg3: unit cube, 4^3 Kuhn cubes, l=6, sin3", 4, 6, "sin3", 3, peak3),
@@ -474,7 +541,7 @@ def impl_ours(args):
         "workloads_3d": extra3d,
     }
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
     return 0
 
@@ -488,6 +555,8 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=12, help="steps of the single-core reference sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-3d", action="store_true", help="skip the secondary 3-d workloads (configs 3 and 5)")
+    ap.add_argument("--force-sharded-3d", action="store_true",
+                    help="run the NCCL-sharded config-5 path even at N = 1 (plumbing check)")
     ap.add_argument("--no-replicas", action="store_true", help="reference arm: skip the all-cores replica context run")
     args = ap.parse_args()
     if args.impl == "reference":
