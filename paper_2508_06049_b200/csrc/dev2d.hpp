@@ -41,6 +41,15 @@ struct DevLevel2D {
   int max_extra;
   const double* geo;   // per macro: c0x, c0y, ux, uy, wx, wy (RHS quadrature map, proj/src/fem.cpp:183-186)
   const double* wq;    // per macro: cell_area / 3
+  // static Gauss-Seidel schedules (Level2D::sched; sc_blocks[s - 1] null when absent)
+  int sc_nu;
+  const int* sc_cell_copy;
+  const int* sc_copy_cell;
+  const double* sc_mtab;
+  const double* sc_gtab;
+  const int* sc_blocks[2];
+  const int* sc_lev_off[2];
+  int sc_levels[2], sc_max_width[2], sc_max_block[2], sc_max_members[2];
 };
 
 struct DevHier2D {

@@ -67,6 +67,33 @@ struct BNode {
 // lane record: c[6] diag inv (8 doubles) | loc[6] k flags wr0 wr1 wb wc xb nc (16 int32)
 constexpr int kProgLaneWords = 16;                        // 128 bytes
 constexpr int kProgStepWords = 6 * kProgLaneWords;        // 3 node types x 2 members
+// shared-memory budget of the static schedule's resident tables (u, b, macro and group tables)
+constexpr std::size_t kSchedTableBytes = 160 * 1024;
+constexpr int kSchedMemberWords = 20;
+
+// Exact-order Gauss-Seidel of a small level as a static schedule
+// (gs_sched2d.cpp, kernels2d.cu k_gs_sched).  The reference's sequential
+// relaxations (sweep, slot, row j, node i; an interface node is
+// re-relaxed by every member macro) are levelled by their true data
+// dependences on the unique node values (read-after-write, write-after-read,
+// write-after-write), so every dependence-level is a set of independent
+// relaxations and executing the levels in order with a barrier between them
+// reproduces the sequential result bit for bit -- with far fewer barrier
+// steps than the macro DAG x wavefront schedule (cfg2 k=5, 2 sweeps: 152
+// levels at l = 1, 372 at l = 3).
+//
+// Block of one level (int32 words, 16-byte aligned): [count, 0 x 7], then
+// `count` 8-word headers, then the member records of its group relaxations:
+//   interior  {cell, macro, E, W, N, S, NW, SE}        (cells of the neighbours)
+//   group     {cell, -1 - group, member word offset in the block, members (-1: domain
+//              boundary, u = b), diag (double), RN(1/diag) (double)}
+//   member    {c0 .. c5 (doubles), r0 .. r5, cells, 0}  (partial_row terms in order:
+//              coefficient, read; 20 words)
+struct GsSched2D {
+  int sweeps = 0, levels = 0, max_width = 0, max_block_words = 0, max_members = 0;
+  std::vector<std::int32_t> blocks;
+  std::vector<std::int32_t> lev_off;  // word offset of each level block (levels + 1)
+};
 
 struct Level2D {
   int n = 1, S = 3;
@@ -102,6 +129,15 @@ struct Level2D {
   int max_extra = 0;  // most extra records of one macro
   // owner dot order (dot_unique, proj/src/hhg.cpp:227-257): offsets in summation order
   std::vector<int> dot_order;
+  // static Gauss-Seidel schedules (sched[s - 1]: s sweeps; empty when the level
+  // does not fit one CTA's shared memory).  Unique node values: groups first,
+  // then lattice-interior nodes in copy order.
+  int sc_nu = 0;
+  std::vector<int> sc_cell_copy;   // per unique node: the owner copy (gather)
+  std::vector<int> sc_copy_cell;   // per copy: its unique node (scatter)
+  std::vector<double> sc_mtab;     // per macro: s1..s6, 1/s0, 0, K_up(9), K_down(9)
+  std::vector<double> sc_gtab;     // per group: diag, RN(1/diag)
+  GsSched2D sched[2];
 };
 
 // Boundary position of lattice-boundary node (i, j): row 0 first, then the
@@ -124,6 +160,8 @@ struct Hierarchy2D {
   std::vector<int> dag_ptr, dag_list;
 
   static Hierarchy2D build(const Mesh2D& mesh, int max_level);
+  // static Gauss-Seidel schedules of the levels that fit (gs_sched2d.cpp)
+  void build_gs_schedules();
 
   // boundary_group with the D2 fix (proj/src/hhg.cpp:163-174)
   int boundary_group(int slot, int l, int i, int j) const;

@@ -1123,6 +1123,194 @@ __global__ void __launch_bounds__(192, 1) k_gs_macro(DevHier2D hd, DevLevel2D lv
   }
 }
 
+// ------------------------------------------------ Gauss-Seidel, static schedule
+// Small levels (GsSched2D, gs_sched2d.cpp): the unique node values u, b, the
+// per-macro stencils / element matrices and the per-group diagonals live in
+// shared memory; the dependence-levels of the reference's sequential
+// relaxation order are executed in order, one relaxation per thread, one
+// __syncthreads per level.  The level blocks stream from L2 into a ring of
+// shared-memory slots by TMA bulk copies (thread 0 issues block g + K once
+// every thread is past level g), completion tracked by one mbarrier per slot.
+constexpr int kSchedMaxThreads = 1024;
+
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+  unsigned done = 0;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void tma_load_block(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+
+__device__ __forceinline__ int4 ld_s_int4(unsigned a) {
+  int4 v;
+  asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+
+__device__ long long g_sched_trace[8][512];
+
+// One relaxation per SG-lane subgroup: lane q evaluates member q's partial
+// row (group relaxations), lane 0 sums the members in slot order and writes
+// the value.  The producer (last thread) issues the TMA copy of block g + K
+// after the barrier that ends level g.
+template <int SG>
+__global__ void __launch_bounds__(kSchedMaxThreads, 1) k_gs_sched(DevLevel2D lv, double* u,
+                                                                 const double* __restrict__ b, int si, int reps, int K,
+                                                                 int slot_bytes, int trace) {
+  extern __shared__ __align__(16) double smem[];
+  const int nu = lv.sc_nu, M = lv.M, NG = lv.num_groups, levels = lv.sc_levels[si];
+  double* su = smem;
+  double* sb = su + nu;
+  double* mt = sb + nu;
+  double* gt = mt + 26 * static_cast<size_t>(M);
+  int* loff = reinterpret_cast<int*>(gt + 2 * static_cast<size_t>(NG));
+  unsigned long long* mbar =
+      reinterpret_cast<unsigned long long*>((reinterpret_cast<uintptr_t>(loff + levels + 1) + 15) & ~uintptr_t(15));
+  unsigned char* ring = reinterpret_cast<unsigned char*>(mbar + 2 * ((K + 1) / 2));
+  const unsigned ring_s = smem_addr(ring), mbar_s = smem_addr(mbar);
+  const unsigned su_s = smem_addr(su), sb_s = smem_addr(sb), mt_s = smem_addr(mt);
+  const int* blocks = lv.sc_blocks[si];
+  const int tid = threadIdx.x, nthreads = blockDim.x, producer = nthreads - 1;
+  const int total = reps * levels;
+  const int q = tid & (SG - 1), sg = tid / SG, R = nthreads / SG;
+  const unsigned submask = SG == 32 ? 0xffffffffu : (((1u << SG) - 1u) << ((tid & 31) & ~(SG - 1)));
+
+  for (int k = tid; k <= levels; k += nthreads) loff[k] = lv.sc_lev_off[si][k];
+  if (tid == producer) {
+    for (int k = 0; k < K; ++k) mbar_init(mbar_s + 8u * k, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == producer)
+    for (int g = 0; g < K && g < total; ++g) {
+      const int lvl = g % levels;
+      tma_load_block(ring_s + static_cast<unsigned>(g) * slot_bytes, blocks + loff[lvl],
+                     4u * static_cast<unsigned>(loff[lvl + 1] - loff[lvl]), mbar_s + 8u * g);
+    }
+  for (int c = tid; c < nu; c += nthreads) {
+    const int o = lv.sc_cell_copy[c];
+    su[c] = __ldcg(u + o);
+    sb[c] = __ldg(b + o);
+  }
+  for (int k = tid; k < 26 * M; k += nthreads) mt[k] = lv.sc_mtab[k];
+  for (int k = tid; k < 2 * NG; k += nthreads) gt[k] = lv.sc_gtab[k];
+  __syncthreads();
+
+  for (int g = 0; g < total; ++g) {
+    const int slot = g % K;
+    if (trace && tid == 0 && g < 512) g_sched_trace[0][g] = clock64();
+    mbar_wait(mbar_s + 8u * slot, static_cast<unsigned>((g / K) & 1));
+    if (trace && tid == 0 && g < 512) g_sched_trace[1][g] = clock64();
+    const unsigned blk = ring_s + static_cast<unsigned>(slot) * slot_bytes;
+    const int count = ld_s_int4(blk).x;
+    // warp-uniform trip count: every lane reaches the member-sum shuffles
+    for (int t0 = 0; t0 < count; t0 += R) {
+      const int t = t0 + sg;
+      const bool act = t < count;
+      const unsigned hd = blk + 32u + 32u * (act ? t : 0);
+      const int4 h0 = ld_s_int4(hd), h1 = ld_s_int4(hd + 16);
+      const int cell = h0.x;
+      const bool interior = h0.y >= 0;
+      const int nm = (!act || interior) ? 0 : h0.w;  // group members (-1: domain boundary)
+      if (trace && tid == 0 && g < 512) g_sched_trace[3][g] = clock64() + (cell == -12345 ? 1 : 0);
+      double o = 0.0;
+      if (q < nm) {
+        // member q's partial_row (proj/src/fem.cpp:138-172 cell order, coefficients inline)
+        const unsigned mr = blk + 4u * static_cast<unsigned>(h0.z) + 4u * kSchedMemberWords * q;
+        double k[6];
+        ld_s_v2f64(mr, k[0], k[1]);
+        ld_s_v2f64(mr + 16, k[2], k[3]);
+        ld_s_v2f64(mr + 32, k[4], k[5]);
+        const int4 ra = ld_s_int4(mr + 48), rb = ld_s_int4(mr + 64);
+        const int nc = rb.z;
+        const int rd[6] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y};
+        double x[6];
+#pragma unroll
+        for (int c = 0; c < 6; ++c) x[c] = ld_s64(su_s + 8u * rd[c]);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const double on = o + (k[2 * c] * x[2 * c] + k[2 * c + 1] * x[2 * c + 1]);
+          o = c < nc ? on : o;
+        }
+      }
+      if (trace && tid == 0 && g < 512) g_sched_trace[4][g] = clock64() + (o == 12345.0 ? 1 : 0);
+      // members summed in ascending slot (the whole warp shuffles, converged)
+      double off = 0.0;
+#pragma unroll
+      for (int r = 0; r < SG; ++r) {
+        const double orr = __shfl_sync(0xffffffffu, o, r, SG);
+        off = r < nm ? off + orr : off;
+      }
+      if (trace && tid == 0 && g < 512) g_sched_trace[5][g] = clock64() + (off == 12345.0 ? 1 : 0) + (nm << 20);
+      if (act && q == 0) {
+        const double B = ld_s64(sb_s + 8u * cell);
+        double res;
+        if (interior) {
+          // interior node, proj/src/multigrid.cpp:170-175 (SURVEY.md A.5 order)
+          const unsigned st = mt_s + 208u * h0.y;
+          const double E = ld_s64(su_s + 8u * h0.z), W = ld_s64(su_s + 8u * h0.w);
+          const double N = ld_s64(su_s + 8u * h1.x), Sv = ld_s64(su_s + 8u * h1.y);
+          const double NW = ld_s64(su_s + 8u * h1.z), SE = ld_s64(su_s + 8u * h1.w);
+          double s1, s2, s3, s4, s5, s6, ic, pad;
+          ld_s_v2f64(st, s1, s2);
+          ld_s_v2f64(st + 16, s3, s4);
+          ld_s_v2f64(st + 32, s5, s6);
+          ld_s_v2f64(st + 48, ic, pad);
+          double acc = s1 * E + s2 * W;
+          acc = acc + s3 * N;
+          acc = acc + s4 * Sv;
+          acc = acc + s5 * NW;
+          acc = acc + s6 * SE;
+          res = (B - acc) * ic;
+        } else if (h0.w < 0) {
+          res = B;  // domain boundary: u = b
+        } else {
+          // relax_boundary_node, proj/src/multigrid.cpp:132-150
+          const double diag = __longlong_as_double(static_cast<long long>(static_cast<unsigned>(h1.x)) |
+                                                   (static_cast<long long>(h1.y) << 32));
+          const double inv = __longlong_as_double(static_cast<long long>(static_cast<unsigned>(h1.z)) |
+                                                  (static_cast<long long>(h1.w) << 32));
+          const double xn = B - off;
+          const double qq = xn * inv;
+          const double r = __fma_rn(-qq, diag, xn);
+          res = xn == 0.0 ? qq : __fma_rn(r, inv, qq);
+        }
+        st_s64(su_s + 8u * cell, res);
+      }
+    }
+    if (trace && tid == 0 && g < 512) g_sched_trace[2][g] = clock64();
+    __syncthreads();
+    if (tid == producer && g + K < total) {
+      const int lvl = (g + K) % levels;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tma_load_block(blk, blocks + loff[lvl], 4u * static_cast<unsigned>(loff[lvl + 1] - loff[lvl]),
+                     mbar_s + 8u * slot);
+    }
+  }
+  const size_t copies = static_cast<size_t>(M) * lv.S;
+  for (size_t k = tid; k < copies; k += nthreads) u[k] = su[lv.sc_copy_cell[k]];
+  if (trace && tid == 0) {
+    for (int g = 0; g < total && g < 40; ++g)
+      printf("level %d: wait %lld hdr %lld member %lld sum %lld final %lld barrier+issue %lld nm %lld\n", g,
+             g_sched_trace[1][g] - g_sched_trace[0][g], g_sched_trace[3][g] - g_sched_trace[1][g],
+             g_sched_trace[4][g] - g_sched_trace[3][g], (g_sched_trace[5][g] & 0xfffff) - (g_sched_trace[4][g] & 0xfffff),
+             g_sched_trace[2][g] - g_sched_trace[5][g], g + 1 < total ? g_sched_trace[0][g + 1] - g_sched_trace[2][g] : 0ll,
+             g_sched_trace[5][g] >> 20);
+  }
+}
+
 // ---------------------------------------------------------------- estimator
 __device__ __forceinline__ double quad_form(const double* k, double a, double b, double c) {
   return a * (k[0] * a + k[1] * b + k[2] * c) + b * (k[3] * a + k[4] * b + k[5] * c) +
@@ -1337,6 +1525,29 @@ void launch_gs_macro(const DevHier2D& hd, const DevLevel2D& lv, double* u, const
 // Smoother dispatch: the whole level in one CTA's shared memory when it fits,
 // else one shared-memory CTA per macro, else (n > 128) the register-wavefront
 // kernel with the lattice in L2.
+// shared memory of k_gs_sched for schedule si with K ring slots (0: does not fit)
+size_t gs_sched_smem(const DevLevel2D& lv, int si, int smem_max, int* K_out, int* slot_out) {
+  if (lv.sc_nu <= 0 || !lv.sc_blocks[si] || lv.sc_max_members[si] > 32) return 0;
+  const size_t tables = 16 * static_cast<size_t>(lv.sc_nu) + 8 * 26 * static_cast<size_t>(lv.M) +
+                        16 * static_cast<size_t>(lv.num_groups) + 4 * static_cast<size_t>(lv.sc_levels[si] + 1);
+  const size_t head = ((tables + 15) & ~size_t(15)) + 8 * 8;  // mbarriers (<= 8)
+  const size_t slot = (4 * static_cast<size_t>(lv.sc_max_block[si]) + 15) & ~size_t(15);
+  if (head + 2 * slot > static_cast<size_t>(smem_max)) return 0;
+  const int K = static_cast<int>(std::min<size_t>(8, (static_cast<size_t>(smem_max) - head) / slot));
+  *K_out = K;
+  *slot_out = static_cast<int>(slot);
+  return head + K * slot;
+}
+
+bool gs_sched_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("KB_GS_SCHED");
+    v = e ? (e[0] != '0') : 1;
+  }
+  return v == 1;
+}
+
 void launch_gs(const DevHier2D& hd, const DevLevel2D& lv, double* u, const double* b, int sweeps, int* done,
                cudaStream_t st) {
   if (sweeps <= 0) return;
@@ -1344,6 +1555,29 @@ void launch_gs(const DevHier2D& hd, const DevLevel2D& lv, double* u, const doubl
   if (num_sms == 0) {
     num_sms = device_attr(cudaDevAttrMultiProcessorCount);
     smem_max = device_attr(cudaDevAttrMaxSharedMemoryPerBlockOptin);
+  }
+  if (gs_sched_enabled()) {
+    // the static dependence-level schedule (small levels)
+    const int si = sweeps == 2 ? 1 : 0, reps = sweeps == 2 ? 1 : sweeps;
+    int K = 0, slot = 0;
+    const size_t smem = gs_sched_smem(lv, si, smem_max, &K, &slot);
+    if (smem > 0) {
+      static int trace = getenv("KB_SCHED_TRACE") ? 1 : 0;
+      const int SG = lv.sc_max_members[si] <= 4 ? 4 : lv.sc_max_members[si] <= 8 ? 8 : lv.sc_max_members[si] <= 16 ? 16 : 32;
+      const int threads = static_cast<int>(
+          std::min<long long>(kSchedMaxThreads, std::max<long long>(64, ((static_cast<long long>(lv.sc_max_width[si]) * SG + 31) / 32) * 32)));
+      auto go = [&](auto kern) {
+        set_smem(kern, smem);
+        kern<<<1, threads, smem, st>>>(lv, u, b, si, reps, K, slot, trace);
+      };
+      if (SG == 4) go(k_gs_sched<4>);
+      else if (SG == 8) go(k_gs_sched<8>);
+      else if (SG == 16) go(k_gs_sched<16>);
+      else go(k_gs_sched<32>);
+      trace = 0;
+      check_launch("k_gs_sched");
+      return;
+    }
   }
   const size_t S = static_cast<size_t>(lv.S), M = static_cast<size_t>(lv.M);
   const int W = gs_group_warps(lv.n);

@@ -73,7 +73,10 @@ std::unique_ptr<DeviceHierarchy2D> DeviceHierarchy2D::create(const Mesh2D& mesh,
              vbytes(mem_ij[l]) + vbytes(lv.mem_slot) + vbytes(lv.kstiff) + vbytes(lv.kmass) +
              vbytes(lv.stencil) + vbytes(lv.inv_c) + vbytes(lv.bnode) + vbytes(lv.rec) + vbytes(lv.wr) +
              vbytes(lv.ghost_ptr) + vbytes(lv.ghost_off) + vbytes(lv.dot_order) + vbytes(geo[l]) +
-             vbytes(wq[l]) + vbytes(lv.prog) + vbytes(lv.prog_ptr) + vbytes(lv.prog_extra) + vbytes(lv.xtra_ptr);
+             vbytes(wq[l]) + vbytes(lv.prog) + vbytes(lv.prog_ptr) + vbytes(lv.prog_extra) + vbytes(lv.xtra_ptr) +
+             vbytes(lv.sc_cell_copy) + vbytes(lv.sc_copy_cell) + vbytes(lv.sc_mtab) + vbytes(lv.sc_gtab) +
+             vbytes(lv.sched[0].blocks) + vbytes(lv.sched[0].lev_off) + vbytes(lv.sched[1].blocks) +
+             vbytes(lv.sched[1].lev_off);
   }
   d->arena.reserve(bytes + 4096);
   d->dh.M = M;
@@ -119,6 +122,21 @@ std::unique_ptr<DeviceHierarchy2D> DeviceHierarchy2D::create(const Mesh2D& mesh,
     dl.max_extra = lv.max_extra;
     dl.geo = d->arena.upload(geo[l]);
     dl.wq = d->arena.upload(wq[l]);
+    dl.sc_nu = lv.sc_nu;
+    if (lv.sc_nu > 0) {
+      dl.sc_cell_copy = d->arena.upload(lv.sc_cell_copy);
+      dl.sc_copy_cell = d->arena.upload(lv.sc_copy_cell);
+      dl.sc_mtab = d->arena.upload(lv.sc_mtab);
+      dl.sc_gtab = d->arena.upload(lv.sc_gtab);
+      for (int q = 0; q < 2; ++q) {
+        dl.sc_blocks[q] = d->arena.upload(lv.sched[q].blocks);
+        dl.sc_lev_off[q] = d->arena.upload(lv.sched[q].lev_off);
+        dl.sc_levels[q] = lv.sched[q].levels;
+        dl.sc_max_width[q] = lv.sched[q].max_width;
+        dl.sc_max_block[q] = lv.sched[q].max_block_words;
+        dl.sc_max_members[q] = lv.sched[q].max_members;
+      }
+    }
     d->lev.push_back(dl);
   }
   return d;
