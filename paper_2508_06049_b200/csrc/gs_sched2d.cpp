@@ -60,6 +60,7 @@ void build_one(const Hierarchy2D& h, Level2D& lv, int sweeps, GsSched2D& out) {
               for (int q = 0; q < bn.rec_count; ++q) {
                 const MemberRec& mr = lv.rec[bn.rec_begin + q];
                 std::int32_t rec[kSchedMemberWords] = {};
+                for (int z = 12; z < 18; ++z) rec[z] = lv.sc_nu;  // absent terms read the zero slot
                 double coef[6] = {0, 0, 0, 0, 0, 0};
                 int nc = 0;
                 for (int c = 0; c < 6; ++c) {
@@ -135,7 +136,7 @@ void Hierarchy2D::build_gs_schedules() {
     // unique nodes: groups, then interiors
     const std::size_t interior = copies - static_cast<std::size_t>(M) * 3 * n;
     const std::size_t nu = NG + interior;
-    const std::size_t table = 16 * nu + 8 * 26 * static_cast<std::size_t>(M) + 16 * NG;
+    const std::size_t table = 16 * (nu + 1) + 8 * 26 * static_cast<std::size_t>(M) + 16 * NG;
     if (table > kSchedTableBytes) continue;
     lv.sc_nu = static_cast<int>(nu);
     lv.sc_copy_cell.assign(copies, -1);

@@ -75,8 +75,11 @@ std::uint64_t dbits(double d) {
 // compact partial_row of member `rec` (may be null: no record) of node k.
 void put_lane(std::uint64_t* w, const MemberRec* rec, const Level2D& lvl, int k, int flags, int wr0, int wr1,
               int wb, int wc, int xb, double diag, double inv) {
+  // absent cells / members: zero coefficients reading the zero ghost slot
+  // (index max_ghosts), so the partial-row chain needs no selects
+  const int zero = -1 - lvl.max_ghosts;
   double c[6] = {0, 0, 0, 0, 0, 0};
-  int loc[6] = {0, 0, 0, 0, 0, 0};
+  int loc[6] = {zero, zero, zero, zero, zero, zero};
   int nc = 0;
   if (rec) {
     const double* ku = &lvl.kstiff[18 * static_cast<std::size_t>(rec->slot)];

@@ -744,24 +744,21 @@ __device__ __forceinline__ void relax_nodes(const PNode& p, unsigned us_s, unsig
     x[q] = ld_s64(l >= 0 ? us_s + 8u * l : gh_s + 8u * (-1 - l));
   }
   const double B = p.B;
+  // absent cells carry zero coefficients and read the zero slot: o + 0 == o
+  // bitwise, since o = 0.0 + ... is never -0.0 (no selects on the chain)
   double o = 0.0;
 #pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    const double on = o + (p.c[2 * c] * x[2 * c] + p.c[2 * c + 1] * x[2 * c + 1]);
-    o = c < p.nc ? on : o;
-  }
+  for (int c = 0; c < 3; ++c) o = o + (p.c[2 * c] * x[2 * c] + p.c[2 * c + 1] * x[2 * c + 1]);
   o = mem < rc ? o : 0.0;
   double off = 0.0;
   if (p.flags & (1 << 16)) {
     // a vertex group with more than two members: sequential sum over members
-    for (int r = 0; r < 8; ++r) {
-      const double orr = __shfl_sync(0xffffffffu, o, (lane & ~7) + r);
-      if (r < rc) off = off + orr;
-    }
+    // (members >= rc contribute +0.0)
+#pragma unroll
+    for (int r = 0; r < 8; ++r) off = off + __shfl_sync(0xffffffffu, o, (lane & ~7) + r);
   } else {
     const double o1 = __shfl_down_sync(0xffffffffu, o, 1);
-    if (rc >= 1) off = off + o;
-    if (rc >= 2) off = off + o1;
+    off = (off + o) + o1;  // rc < 2: o1 = +0.0
   }
   if (lane_ok && mem == 0 && p.k >= 0) {
     double res = B;
@@ -874,15 +871,28 @@ __device__ __forceinline__ void group_sweep(const DevLevel2D& lv, const SweepArg
     // holds stale shared memory and is never decoded
     PNode p0, p1;
     load_pnode(p0, ring_s, xs_s, bs_s, tl, mem);
+#ifdef KB_GS_TRACE
+    const bool trc = blockIdx.x == 0 && lane == 0 && bar_id == 1;
+#define KB_STAMP(row, t, dep) \
+  if (trc) g_gs_trace[row][t] = clock64() + ((dep) == 12345.0 ? 1 : 0)
+#else
+#define KB_STAMP(row, t, dep)
+#endif
     for (int t = 0; t <= 2 * n; t += 2) {
+      KB_STAMP(0, t, 0.0);
       if (t + 1 <= 2 * n)
         load_pnode(p1, ring_s + static_cast<unsigned>((t + 1) % kRingSteps) * kStepBytes, xs_s, bs_s, tl, mem);
+      KB_STAMP(1, t, p0.c[0]);
       relax_nodes(p0, us_s, bs_s, gh_s, copies, lv.wr, lane);
+      KB_STAMP(2, t, ld_s64(us_s));
       bar_sync(bar_id, bar_threads);
       if (t + 1 > 2 * n) break;
+      KB_STAMP(0, t + 1, 0.0);
       if (t + 2 <= 2 * n)
         load_pnode(p0, ring_s + static_cast<unsigned>((t + 2) % kRingSteps) * kStepBytes, xs_s, bs_s, tl, mem);
+      KB_STAMP(1, t + 1, p1.c[0]);
       relax_nodes(p1, us_s, bs_s, gh_s, copies, lv.wr, lane);
+      KB_STAMP(2, t + 1, ld_s64(us_s));
       bar_sync(bar_id, bar_threads);
     }
   } else {
@@ -986,6 +996,7 @@ __global__ void __launch_bounds__(512, 1) k_gs_level(DevHier2D hd, DevLevel2D lv
   auto xsb = [&](int c) { return reinterpret_cast<unsigned long long*>(gb + 2 * kRingBytes + c * xs_bytes); };
   auto gob = [&](int c) { return reinterpret_cast<int*>(gb + 2 * kRingBytes + 2 * xs_bytes + c * go_bytes); };
   double* gh = reinterpret_cast<double*>(gb + 2 * kRingBytes + 2 * xs_bytes + 2 * go_bytes);
+  if (gw == 0 && lane == 0) gh[lv.max_ghosts] = 0.0;  // zero slot of absent partial-row terms
 
   for (size_t k = threadIdx.x; k < total; k += blockDim.x) {
     lu[k] = __ldcg(u + k);
@@ -1081,6 +1092,7 @@ __global__ void __launch_bounds__(192, 1) k_gs_macro(DevHier2D hd, DevLevel2D lv
   const int tid = threadIdx.x, gw = tid >> 5, lane = tid & 31;
   const int nitems = sweeps * M;
   int cur = -1;
+  if (tid == 0) gh[lv.max_ghosts] = 0.0;  // zero slot of absent partial-row terms
   for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
     const int s = item / M, m = item - s * M;
     if (tid == 0) {
@@ -1171,9 +1183,9 @@ __global__ void __launch_bounds__(kSchedMaxThreads, 1) k_gs_sched(DevLevel2D lv,
                                                                  int slot_bytes, int trace) {
   extern __shared__ __align__(16) double smem[];
   const int nu = lv.sc_nu, M = lv.M, NG = lv.num_groups, levels = lv.sc_levels[si];
-  double* su = smem;
-  double* sb = su + nu;
-  double* mt = sb + nu;
+  double* su = smem;  // nu unique values + the zero slot
+  double* sb = su + nu + 1;
+  double* mt = sb + nu + 1;
   double* gt = mt + 26 * static_cast<size_t>(M);
   int* loff = reinterpret_cast<int*>(gt + 2 * static_cast<size_t>(NG));
   unsigned long long* mbar =
@@ -1204,26 +1216,33 @@ __global__ void __launch_bounds__(kSchedMaxThreads, 1) k_gs_sched(DevLevel2D lv,
     su[c] = __ldcg(u + o);
     sb[c] = __ldg(b + o);
   }
+  if (tid == 0) su[nu] = 0.0;
   for (int k = tid; k < 26 * M; k += nthreads) mt[k] = lv.sc_mtab[k];
   for (int k = tid; k < 2 * NG; k += nthreads) gt[k] = lv.sc_gtab[k];
   __syncthreads();
 
+  const int kshift = __ffs(K) - 1;
+  const int tmax = (slot_bytes - 64) / 32;  // header loads stay inside the slot
   for (int g = 0; g < total; ++g) {
-    const int slot = g % K;
+    const int slot = g & (K - 1);  // K is a power of two
     if (trace && tid == 0 && g < 512) g_sched_trace[0][g] = clock64();
-    mbar_wait(mbar_s + 8u * slot, static_cast<unsigned>((g / K) & 1));
+    mbar_wait(mbar_s + 8u * slot, static_cast<unsigned>((g >> kshift) & 1));
     if (trace && tid == 0 && g < 512) g_sched_trace[1][g] = clock64();
     const unsigned blk = ring_s + static_cast<unsigned>(slot) * slot_bytes;
-    const int count = ld_s_int4(blk).x;
-    // warp-uniform trip count: every lane reaches the member-sum shuffles
+    // warp-uniform trip count: every lane reaches the member-sum shuffles; the
+    // first header is loaded together with the count (slot 0 exists in every block)
+    int count = 1;
     for (int t0 = 0; t0 < count; t0 += R) {
       const int t = t0 + sg;
-      const bool act = t < count;
-      const unsigned hd = blk + 32u + 32u * (act ? t : 0);
+      const unsigned hd = blk + 32u + 32u * min(t, tmax);
+      const int4 c4 = ld_s_int4(blk);
       const int4 h0 = ld_s_int4(hd), h1 = ld_s_int4(hd + 16);
+      count = c4.x;
+      const bool act = t < count;
       const int cell = h0.x;
       const bool interior = h0.y >= 0;
       const int nm = (!act || interior) ? 0 : h0.w;  // group members (-1: domain boundary)
+      const double B = ld_s64(sb_s + 8u * (act ? cell : 0));
       if (trace && tid == 0 && g < 512) g_sched_trace[3][g] = clock64() + (cell == -12345 ? 1 : 0);
       double o = 0.0;
       if (q < nm) {
@@ -1239,23 +1258,22 @@ __global__ void __launch_bounds__(kSchedMaxThreads, 1) k_gs_sched(DevLevel2D lv,
         double x[6];
 #pragma unroll
         for (int c = 0; c < 6; ++c) x[c] = ld_s64(su_s + 8u * rd[c]);
+        // absent terms: zero coefficient x zero slot, o + 0 == o (o is never -0.0)
+        (void)nc;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          const double on = o + (k[2 * c] * x[2 * c] + k[2 * c + 1] * x[2 * c + 1]);
-          o = c < nc ? on : o;
-        }
+        for (int c = 0; c < 3; ++c) o = o + (k[2 * c] * x[2 * c] + k[2 * c + 1] * x[2 * c + 1]);
       }
       if (trace && tid == 0 && g < 512) g_sched_trace[4][g] = clock64() + (o == 12345.0 ? 1 : 0);
-      // members summed in ascending slot (the whole warp shuffles, converged)
+      // members summed in ascending slot; lanes beyond a group's members hold
+      // +0.0, the bound is warp-uniform (the whole warp shuffles, converged)
+      double ov[SG];
+#pragma unroll
+      for (int r = 0; r < SG; ++r) ov[r] = __shfl_sync(0xffffffffu, o, r, SG);
       double off = 0.0;
 #pragma unroll
-      for (int r = 0; r < SG; ++r) {
-        const double orr = __shfl_sync(0xffffffffu, o, r, SG);
-        off = r < nm ? off + orr : off;
-      }
+      for (int r = 0; r < SG; ++r) off = off + ov[r];
       if (trace && tid == 0 && g < 512) g_sched_trace[5][g] = clock64() + (off == 12345.0 ? 1 : 0) + (nm << 20);
       if (act && q == 0) {
-        const double B = ld_s64(sb_s + 8u * cell);
         double res;
         if (interior) {
           // interior node, proj/src/multigrid.cpp:170-175 (SURVEY.md A.5 order)
@@ -1528,12 +1546,13 @@ void launch_gs_macro(const DevHier2D& hd, const DevLevel2D& lv, double* u, const
 // shared memory of k_gs_sched for schedule si with K ring slots (0: does not fit)
 size_t gs_sched_smem(const DevLevel2D& lv, int si, int smem_max, int* K_out, int* slot_out) {
   if (lv.sc_nu <= 0 || !lv.sc_blocks[si] || lv.sc_max_members[si] > 32) return 0;
-  const size_t tables = 16 * static_cast<size_t>(lv.sc_nu) + 8 * 26 * static_cast<size_t>(lv.M) +
+  const size_t tables = 16 * static_cast<size_t>(lv.sc_nu + 1) + 8 * 26 * static_cast<size_t>(lv.M) +
                         16 * static_cast<size_t>(lv.num_groups) + 4 * static_cast<size_t>(lv.sc_levels[si] + 1);
   const size_t head = ((tables + 15) & ~size_t(15)) + 8 * 8;  // mbarriers (<= 8)
   const size_t slot = (4 * static_cast<size_t>(lv.sc_max_block[si]) + 15) & ~size_t(15);
   if (head + 2 * slot > static_cast<size_t>(smem_max)) return 0;
-  const int K = static_cast<int>(std::min<size_t>(8, (static_cast<size_t>(smem_max) - head) / slot));
+  const size_t fit = (static_cast<size_t>(smem_max) - head) / slot;
+  const int K = fit >= 8 ? 8 : fit >= 4 ? 4 : 2;  // a power of two
   *K_out = K;
   *slot_out = static_cast<int>(slot);
   return head + K * slot;
