@@ -50,6 +50,9 @@ struct DevLevel2D {
   const int* sc_blocks[2];
   const int* sc_lev_off[2];
   int sc_levels[2], sc_max_width[2], sc_max_block[2], sc_max_members[2];
+  // pipelined smoother tables (Level2D::pipe; null when absent)
+  const int* pipe_rec;
+  int pipe_rec_words, pipe_maxreq;
 };
 
 struct DevHier2D {

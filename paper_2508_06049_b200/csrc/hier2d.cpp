@@ -566,6 +566,7 @@ Hierarchy2D Hierarchy2D::build(const Mesh2D& mesh, int max_level) {
     build_programs(lvl, M);
   }
   h.build_gs_schedules();
+  h.build_pipe_tables();
   return h;
 }
 

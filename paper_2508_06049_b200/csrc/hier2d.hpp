@@ -95,6 +95,27 @@ struct GsSched2D {
   std::vector<std::int32_t> lev_off;  // word offset of each level block (levels + 1)
 };
 
+// Fine-grained pipelined smoother of larger levels (pipe2d.cpp, kernels2d.cu
+// k_gs_pipe): one CTA per macro sweeps its lattice in shared memory along the
+// wavefront while the other macros run concurrently; the
+// reference's sequential order across macros (A.1/A.3) is enforced per
+// wavefront step instead of per sweep.  For every macro m, sweep s (0, 1) and
+// step t a record lists the gate of the step -- progress[m2] >= p for the
+// other macros whose writes this step's reads need (RAW) or whose reads of
+// global values this step's writes would clobber (WAR, WAW) -- and the values
+// to re-read from global memory before the step (interface copies other
+// macros relaxed, ghost values of neighbouring lattices).  progress[m] counts
+// completed steps + 1 (published after every step); a fetch for step tau is
+// done by the end of step tau - 1 of its macro.
+//   record (int32 words, stride rec_words): nreq, nfetch, then maxreq pairs
+//   (macro, progress), then maxfetch pairs (destination: lattice index >= 0 or
+//   -1 - ghost slot, source: global offset)
+struct PipeTables2D {
+  bool ok = false;
+  int maxreq = 0, maxfetch = 0, rec_words = 0;
+  std::vector<std::int32_t> rec;  // [M][sweep 0, 1][2n + 1] records
+};
+
 struct Level2D {
   int n = 1, S = 3;
   // shared-node groups (vertex groups first, then edge groups), members ascending slot
@@ -138,6 +159,7 @@ struct Level2D {
   std::vector<double> sc_mtab;     // per macro: s1..s6, 1/s0, 0, K_up(9), K_down(9)
   std::vector<double> sc_gtab;     // per group: diag, RN(1/diag)
   GsSched2D sched[2];
+  PipeTables2D pipe;
 };
 
 // Boundary position of lattice-boundary node (i, j): row 0 first, then the
@@ -162,6 +184,8 @@ struct Hierarchy2D {
   static Hierarchy2D build(const Mesh2D& mesh, int max_level);
   // static Gauss-Seidel schedules of the levels that fit (gs_sched2d.cpp)
   void build_gs_schedules();
+  // pipelined-smoother tables of the levels the schedule does not cover (pipe2d.cpp)
+  void build_pipe_tables();
 
   // boundary_group with the D2 fix (proj/src/hhg.cpp:163-174)
   int boundary_group(int slot, int l, int i, int j) const;

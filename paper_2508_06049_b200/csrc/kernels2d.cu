@@ -732,7 +732,8 @@ __device__ __forceinline__ void load_pnode(PNode& p, unsigned slot, unsigned xs,
 // order of proj/src/fem.cpp:138-172), summed over members in slot order,
 // (b - off) / diag correctly rounded, written to every copy.
 __device__ __forceinline__ void relax_nodes(const PNode& p, unsigned us_s, unsigned bs_s, unsigned gh_s,
-                                            double* copies, const int* wr_global, int lane) {
+                                            double* copies, const int* wr_global, int lane,
+                                            double* own_copy = nullptr) {
   const int type = lane >> 3, mem = lane & 7;
   const bool lane_ok = type < 3;
   const int rc = (lane_ok && p.k >= 0) ? ((p.flags >> 8) & 0xff) : 0;
@@ -772,6 +773,7 @@ __device__ __forceinline__ void relax_nodes(const PNode& p, unsigned us_s, unsig
       res = xn == 0.0 ? q : __fma_rn(r, p.inv, q);
     }
     st_s64(us_s + 8u * p.k, res);
+    if (own_copy) own_copy[p.k] = res;  // pipelined smoother: global copies are the record
     if (p.wc > 0) copies[p.wr0] = res;
     if (p.wc > 1) copies[p.wr1] = res;
     for (int q = p.wb + 2; q < p.wb + p.wc; ++q) copies[wr_global[q]] = res;
@@ -1329,6 +1331,281 @@ __global__ void __launch_bounds__(kSchedMaxThreads, 1) k_gs_sched(DevLevel2D lv,
   }
 }
 
+// ------------------------------------------------ Gauss-Seidel, pipelined
+// One CTA per macro (all resident), the macro's lattice in shared memory, all
+// sweeps of the call in one pass over global steps tau = s T + t.  The warps
+// of group_sweep (boundary, program, interior) are the consumers; per step
+// they bar.arrive on barrier A (step done) and bar.sync on barrier B (gate of
+// the next step).  The sync warp owns the gates (PipeTables2D): it waits until
+// the step's requirements hold (other macros' progress), re-reads the step's
+// remote values from global memory into the lattice / ghost slots, then
+// arrives on B; after A it publishes this macro's progress (st.release.gpu).
+// Requirements of step tau + 2 are polled and its values fetched during step
+// tau, so the gate normally opens at once; when it does not, progress is
+// published first and the gate waits (no cyclic wait: every requirement names
+// an event that precedes the step in the sequential order).
+constexpr int kPipeBarB = 1, kPipeBarA0 = 2, kPipeBarAs = 12;  // gate; ring of step-done barriers
+constexpr int kPipePubs = 4;  // publisher warps
+constexpr int kPipeRing = 16;  // step programs + gate records in flight
+
+__device__ __forceinline__ void bar_arrive(int id, int threads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+__device__ __forceinline__ void issue_prog(const unsigned long long* prog_m, unsigned ring_s, const int* rec_m,
+                                           unsigned rring_s, int rec_words, int t, int slot, int lane) {
+  const char* src = reinterpret_cast<const char*>(prog_m + static_cast<size_t>(t) * kProgStepWords);
+  const unsigned dst = ring_s + static_cast<unsigned>(slot) * kStepBytes;
+  for (int c = lane; c < 48; c += 32)
+    cp_async16(dst + static_cast<unsigned>(kLaneStride) * (c >> 3) + 16u * (c & 7), src + 16 * c);
+  const char* rsrc = reinterpret_cast<const char*>(rec_m + static_cast<size_t>(t) * rec_words);
+  const unsigned rdst = rring_s + static_cast<unsigned>(slot * rec_words * 4);
+  for (int c = lane; c < rec_words / 4; c += 32) cp_async16(rdst + 16u * c, rsrc + 16 * c);
+}
+
+__global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, const double* __restrict__ b,
+                                                    int sweeps, int* progress, const int* __restrict__ rec,
+                                                    int rec_words, int maxreq, int trace) {
+  extern __shared__ __align__(16) double smem[];
+  const int S = lv.S, n = lv.n, T = 2 * n + 1, m = blockIdx.x, total = sweeps * T;
+  const int Wc = gs_group_warps(n), cthreads = 32 * Wc, bthreads = cthreads + 32;
+  unsigned char* ring = reinterpret_cast<unsigned char*>(smem);
+  int* rring = reinterpret_cast<int*>(ring + (kPipeRing * kStepBytes));
+  unsigned long long* xs = reinterpret_cast<unsigned long long*>(rring + kPipeRing * rec_words);
+  double* gh = reinterpret_cast<double*>(xs + static_cast<size_t>(lv.max_extra) * kProgLaneWords);
+  double* us = gh + lv.max_ghosts + 1;
+  double* bs = us + S;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const unsigned ring_s = smem_addr(ring), rring_s = smem_addr(rring);
+  __shared__ int pub_last[kPipePubs];  // last step-done barrier each publisher passed
+  __shared__ long long ptr_bstart[64], ptr_bend[64], ptr_sync[64], ptr_istart[64], ptr_iend[64];
+  if (tid < kPipePubs) pub_last[tid] = -1;
+  const unsigned long long* prog_m = lv.prog + lv.prog_ptr[m];
+  const int* rec_m0 = rec + static_cast<size_t>(m) * 2 * T * rec_words;  // sweep-0 records, then sweep >= 1
+  auto rec_src = [&](int tau) { return rec_m0 + (tau >= T ? static_cast<size_t>(T) * rec_words : 0); };
+  double* um = u + static_cast<size_t>(m) * S;
+
+  // initial state: lattice, b, extra records, ghosts; the head of the step stream
+  {
+    const double* bm = b + static_cast<size_t>(m) * S;
+    for (int k = tid; k < S; k += blockDim.x) {
+      us[k] = __ldcg(um + k);
+      bs[k] = __ldg(bm + k);
+    }
+    const int xb = lv.xtra_ptr[m], xc = lv.xtra_ptr[m + 1] - xb;
+    for (int x = tid; x < xc; x += blockDim.x) xs[x] = lv.prog_extra[xb + x];
+    const int gbeg = lv.ghost_ptr[m], gcnt = lv.ghost_ptr[m + 1] - gbeg;
+    for (int x = tid; x < gcnt; x += blockDim.x) gh[x] = __ldcg(u + lv.ghost_off[gbeg + x]);
+    if (tid == 0) gh[lv.max_ghosts] = 0.0;
+    if (warp == 1) {
+      for (int tau = 0; tau < kPipeRing - 1 && tau < total; ++tau) {
+        issue_prog(prog_m, ring_s, rec_src(tau), rring_s, rec_words, tau % T, tau % kPipeRing, lane);
+        cp_async_commit();
+      }
+      cp_async_wait<0>();
+    }
+  }
+  __syncthreads();
+
+  if (warp > Wc) {
+    // ------------------------------------------------ publisher warps (off the gate barrier B): warp
+    // Wc + 1 + w takes the step-done barriers A of steps tau = w mod kPipePubs and raises
+    // progress[m] to tau + 2 (red.release.gpu.max: the release may finish out of order)
+    const int w = warp - Wc - 1;
+    for (int tau = w; tau < total; tau += kPipePubs) {
+      bar_sync(kPipeBarA0 + tau % kPipeBarAs, bthreads);
+      if (lane == 0) {
+        *reinterpret_cast<volatile int*>(&pub_last[w]) = tau;
+        asm volatile("red.release.gpu.global.max.s32 [%0], %1;" ::"l"(progress + m), "r"(tau + 2) : "memory");
+      }
+    }
+  } else if (warp == Wc) {
+    // ------------------------------------------------ sync warp
+    // per iteration tau (between gate tau + 1 and the end of step tau + 1):
+    //   gate tau + 1: store the values fetched two iterations ago, arrive on B
+    //   step tau + 3: if the requirements polled two iterations ago hold, fetch
+    //   step tau + 5: poll the requirements (relaxed loads; the data loads are
+    //                 issued only after the flags were observed, from L2, where
+    //                 the producer's st.release.gpu made them visible first)
+    auto recp = [&](int tau) { return rring + (tau % kPipeRing) * rec_words; };
+    // sweeps >= 1 reuse table 1 (tables exist for sweeps <= 2: the shift is 0)
+    auto shift = [&](int tau) { return 0 * tau; };
+    auto poll = [&](const int* pm) {
+      int v;
+      asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(pm) : "memory");
+      return v;
+    };
+    double f1 = 0.0, f2 = 0.0, f3 = 0.0;
+    bool f1ok = false, f2ok = false, f3ok = false;
+    int p3 = 0, p4 = 0, p5 = 0;
+    bool p3ok = false, p4ok = false, p5ok = false;
+    long long t_slow = 0, t_start = clock64();
+    int n_slow = 0, n_req = 0;
+    // prologue: poll steps 0 .. 4 (their records are in the ring)
+    for (int st = 0; st < 5 && st < total; ++st) {
+      const int* r = recp(st);
+      const int pv = lane < r[0] ? poll(progress + r[2 + 2 * lane]) : 0;
+      if (st == 2) p3 = pv, p3ok = true;
+      if (st == 3) p4 = pv, p4ok = true;
+      if (st == 4) p5 = pv, p5ok = true;
+    }
+    for (int tau = -1; tau < total; ++tau) {
+      const int g = tau + 1;
+      if (g < total) {
+        const int* r = recp(g);
+        const int nreq = r[0], nfetch = r[1];
+        n_req += nreq > 0;
+        if (!f1ok && (nreq > 0 || nfetch > 0)) {
+          // slow path: wait for the requirements (the publisher reports this
+          // macro's completed steps meanwhile)
+          ++n_slow;
+          t_slow -= clock64();
+          if (lane < nreq) {
+            const int* pm = progress + r[2 + 2 * lane];
+            const int need = r[3 + 2 * lane] + shift(g);
+            long long spins = 0;
+            while (ld_acquire(pm) < need) {
+              if (++spins == (1ll << 24)) {  // a broken table would deadlock: fail loudly instead
+                printf("k_gs_pipe: macro %d step %d waits for macro %d progress %d (has %d)\n", m, g,
+                       r[2 + 2 * lane], need, ld_acquire(pm));
+                __trap();
+              }
+            }
+          }
+          __syncwarp();
+          if (lane < nfetch) f1 = __ldcg(u + r[3 + 2 * maxreq + 2 * lane]);
+          t_slow += clock64() + (f1 == 12345.0 ? 1 : 0);
+        }
+        if (lane < nfetch) {
+          const int dst = r[2 + 2 * maxreq + 2 * lane];
+          if (dst >= 0)
+            us[dst] = f1;
+          else
+            gh[-1 - dst] = f1;
+        }
+        // the step-done barrier of step g reuses the one of step g - kPipeBarAs: its
+        // publisher must have passed it (flow control only)
+        if (g >= kPipeBarAs) {
+          const int gp = g - kPipeBarAs;
+          while (*reinterpret_cast<volatile int*>(&pub_last[gp % kPipePubs]) < gp) {
+          }
+        }
+        __syncwarp();
+        if (trace && lane == 0 && g >= 64 && g < 128) ptr_sync[g - 64] = clock64();
+        bar_sync(kPipeBarB, bthreads);  // gate of step g opens
+      }
+      // step tau + 3: fetch when the polled requirements hold
+      const int s3 = tau + 3;
+      f3ok = false;
+      if (s3 < total && p3ok) {
+        const int* r = recp(s3);
+        const bool ok = lane >= r[0] || p3 >= r[3 + 2 * lane] + shift(s3);
+        if (__all_sync(0xffffffffu, ok)) {
+          if (lane < r[1]) f3 = __ldcg(u + r[3 + 2 * maxreq + 2 * lane]);
+          f3ok = true;
+        }
+      }
+      // step tau + 5: poll
+      const int s5 = tau + 5;
+      p5ok = false;
+      if (s5 < total) {
+        const int* r = recp(s5);
+        if (lane < r[0]) p5 = poll(progress + r[2 + 2 * lane]);
+        p5ok = true;
+      }
+      // rotate the stages
+      f1 = f2, f1ok = f2ok;
+      f2 = f3, f2ok = f3ok;
+      p3 = p4, p3ok = p4ok;
+      p4 = p5, p4ok = p5ok;
+    }
+    if (trace && lane == 0 && (m % 20 == 0 || m == gridDim.x - 1))
+      printf("pipe macro %d: steps %d, gated %d, slow gates %d, cycles in slow gates %lld of %lld\n", m, total, n_req,
+             n_slow, t_slow, clock64() - t_start);
+  } else {
+    // ------------------------------------------------ consumers (group_sweep roles)
+    const int gw = warp;
+    const unsigned us_s = smem_addr(us), bs_s = smem_addr(bs), gh_s = smem_addr(gh), xs_s = smem_addr(xs);
+    bar_sync(kPipeBarB, bthreads);  // gate of step 0
+    if (gw == 1) {
+      for (int tau = 0; tau < total; ++tau) {
+        const int nx = tau + kPipeRing - 1;
+        if (nx < total) issue_prog(prog_m, ring_s, rec_src(nx), rring_s, rec_words, nx % T, nx % kPipeRing, lane);
+        cp_async_commit();
+        cp_async_wait<kPipeRing - 7>();  // steps and records <= tau + 6 landed (read by the sync warp after A)
+        bar_arrive(kPipeBarA0 + tau % kPipeBarAs, bthreads);
+        if (tau + 1 < total) bar_sync(kPipeBarB, bthreads);
+      }
+      cp_async_wait<0>();
+    } else if (gw == 0) {
+      const int type = lane >> 3, mem = lane & 7;
+      const int tl = type < 3 ? type : 0;
+      PNode p0, p1;
+      load_pnode(p0, ring_s, xs_s, bs_s, tl, mem);
+      for (int tau = 0; tau < total; tau += 2) {
+        if (tau + 1 < total)
+          load_pnode(p1, ring_s + static_cast<unsigned>((tau + 1) % kPipeRing) * kStepBytes, xs_s, bs_s, tl, mem);
+        if (trace && lane == 0 && tau >= 64 && tau < 128) ptr_bstart[tau - 64] = clock64();
+        relax_nodes(p0, us_s, bs_s, gh_s, u, lv.wr, lane, um);
+        if (trace && lane == 0 && tau >= 64 && tau < 128) ptr_bend[tau - 64] = clock64() + (ld_s64(us_s) == 12345.0);
+        bar_arrive(kPipeBarA0 + tau % kPipeBarAs, bthreads);
+        if (tau + 1 >= total) break;
+        bar_sync(kPipeBarB, bthreads);
+        if (tau + 2 < total)
+          load_pnode(p0, ring_s + static_cast<unsigned>((tau + 2) % kPipeRing) * kStepBytes, xs_s, bs_s, tl, mem);
+        if (trace && lane == 0 && tau + 1 >= 64 && tau + 1 < 128) ptr_bstart[tau + 1 - 64] = clock64();
+        relax_nodes(p1, us_s, bs_s, gh_s, u, lv.wr, lane, um);
+        if (trace && lane == 0 && tau + 1 >= 64 && tau + 1 < 128) ptr_bend[tau + 1 - 64] = clock64() + (ld_s64(us_s) == 12345.0);
+        bar_arrive(kPipeBarA0 + (tau + 1) % kPipeBarAs, bthreads);
+        if (tau + 2 < total) bar_sync(kPipeBarB, bthreads);
+      }
+    } else {
+      const double* st = lv.stencil + 7 * m;
+      const double s1 = st[1], s2 = st[2], s3 = st[3], s4 = st[4], s5 = st[5], s6 = st[6];
+      const double inv_c = lv.inv_c[m];
+      const int j = 32 * (gw - 2) + lane + 1;
+      const bool row = j <= n - 1;
+      const int rowk = row ? dlat(n, 0, j) : 0;
+      const int dn = n + 1 - j, dnw = n - j, ds = n + 2 - j;
+      int t = 0;  // tau mod T, kept incrementally (no division on the step path)
+      for (int tau = 0; tau < total; ++tau, t = (t + 1 == T ? 0 : t + 1)) {
+        if (trace && gw == 2 && lane == 0 && tau >= 64 && tau < 128) ptr_istart[tau - 64] = clock64();
+        const int i = t - 2 * j;
+        if (row && i >= 1 && i <= n - j - 1) {
+          const int k = rowk + i;
+          const double B = bs[k];
+          const double E = us[k + 1], W = us[k - 1], N = us[k + dn], Sv = us[k - ds];
+          const double NW = us[k + dnw], SE = us[k - dn];
+          double acc = s1 * E + s2 * W;
+          acc = acc + s3 * N;
+          acc = acc + s4 * Sv;
+          acc = acc + s5 * NW;
+          acc = acc + s6 * SE;
+          const double v = (B - acc) * inv_c;
+          us[k] = v;
+          if (j == 1 || i == 1 || i + j == n - 1) um[k] = v;  // exported: ghost of a neighbour
+        }
+        if (trace && gw == 2 && lane == 0 && tau >= 64 && tau < 128) ptr_iend[tau - 64] = clock64() + (us[0] == 12345.0);
+        bar_arrive(kPipeBarA0 + tau % kPipeBarAs, bthreads);
+        if (tau + 1 < total) bar_sync(kPipeBarB, bthreads);
+      }
+    }
+  }
+  __syncthreads();
+  if (trace && m == 0 && tid == 0)
+    for (int q = 0; q < 12; ++q)
+      printf("step %d: boundary relax %lld, boundary end->next start %lld, interior %lld, sync arrives at B %lld before boundary start\n",
+             64 + q, ptr_bend[q] - ptr_bstart[q], ptr_bstart[q + 1] - ptr_bend[q], ptr_iend[q] - ptr_istart[q],
+             ptr_bstart[q + 1] - ptr_sync[q + 1]);
+  // lattice-interior nodes back to global memory (interface copies are kept
+  // current by every relaxation)
+  for (int k = tid; k < S; k += blockDim.x) {
+    int i, j;
+    decode(n, k, i, j);
+    if (i >= 1 && j >= 1 && i + j <= n - 1) um[k] = us[k];
+  }
+}
+
 // ---------------------------------------------------------------- estimator
 __device__ __forceinline__ double quad_form(const double* k, double a, double b, double c) {
   return a * (k[0] * a + k[1] * b + k[2] * c) + b * (k[3] * a + k[4] * b + k[5] * c) +
@@ -1567,6 +1844,15 @@ bool gs_sched_enabled() {
   return v == 1;
 }
 
+bool gs_pipe_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("KB_GS_PIPE");
+    v = e ? (e[0] != '0') : 1;
+  }
+  return v == 1;
+}
+
 void launch_gs(const DevHier2D& hd, const DevLevel2D& lv, double* u, const double* b, int sweeps, int* done,
                cudaStream_t st) {
   if (sweeps <= 0) return;
@@ -1596,6 +1882,36 @@ void launch_gs(const DevHier2D& hd, const DevLevel2D& lv, double* u, const doubl
       trace = 0;
       check_launch("k_gs_sched");
       return;
+    }
+  }
+  if (lv.pipe_rec && sweeps <= 2 && gs_pipe_enabled()) {
+    // fine-grained pipelined smoother: one resident CTA per macro
+    const int threads = 32 * (gs_group_warps(lv.n) + 1 + kPipePubs);
+    const size_t smem = kPipeRing * kStepBytes + static_cast<size_t>(kPipeRing) * lv.pipe_rec_words * 4 +
+                        static_cast<size_t>(lv.max_extra) * kProgLaneWords * 8 + (lv.max_ghosts + 1) * 8 +
+                        2 * static_cast<size_t>(lv.S) * 8;
+    if (threads <= 384 && smem <= static_cast<size_t>(smem_max)) {
+      set_smem(k_gs_pipe, smem);
+      int occ = 0;
+      KB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gs_pipe, threads, smem));
+      if (occ * num_sms >= lv.M) {
+        KB_CUDA_CHECK(cudaMemsetAsync(done, 0, sizeof(int) * lv.M, st));
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(lv.M);
+        cfg.blockDim = dim3(threads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeCooperative;  // every macro's CTA resident at once
+        attr[0].val.cooperative = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        static int trace = getenv("KB_PIPE_TRACE") ? 1 : 0;
+        KB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_gs_pipe, lv, u, b, sweeps, done, lv.pipe_rec, lv.pipe_rec_words,
+                                         lv.pipe_maxreq, trace));
+        trace = 0;
+        return;
+      }
     }
   }
   const size_t S = static_cast<size_t>(lv.S), M = static_cast<size_t>(lv.M);

@@ -1,0 +1,199 @@
+// Tables of the fine-grained pipelined 2-d smoother.  See PipeTables2D in
+// hier2d.hpp.  The dependences are derived by replaying the reference's
+// sequential relaxation order (proj/src/multigrid.cpp:152-178)
+// over the global memory locations that cross macros: every interface copy
+// (relax_boundary_node writes all copies, :132-150) and every ghost value (a
+// neighbouring lattice's node read by a member's partial_row,
+// proj/src/fem.cpp:128-173, written through by its owner when relaxed).
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <map>
+
+#include "hier2d.hpp"
+
+namespace kb {
+
+namespace {
+constexpr int kDij2[6][2] = {{1, 0}, {-1, 0}, {0, 1}, {0, -1}, {-1, 1}, {1, -1}};  // E W N S NW SE
+
+int min_pipe_n() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("KB_GS_PIPE_MIN_N");
+    v = e ? atoi(e) : 16;
+  }
+  return v;
+}
+
+void build_level(const Hierarchy2D& h, Level2D& lv) {
+  const int n = lv.n, S = lv.S, M = h.M, T = 2 * n + 1;
+  const std::size_t copies = static_cast<std::size_t>(M) * S;
+  // global locations that cross macros: interface copies and ghosts
+  std::vector<char> tracked(copies, 0);
+  for (std::size_t q = 0; q < lv.mem_slot.size(); ++q)
+    tracked[static_cast<std::size_t>(lv.mem_slot[q]) * S + lv.mem_idx[q]] = 1;
+  for (int off : lv.ghost_off) tracked[off] = 2;
+  // per location: last write (serial, macro, step) and global readers since
+  struct Reader {
+    int m, th;
+  };
+  std::vector<long long> w_serial(copies, 0);
+  std::vector<int> w_m(copies, -1), w_t(copies, 0);
+  std::vector<std::vector<Reader>> readers(copies);
+  // initial loads: every macro reads its lattice and its ghosts before its step
+  // 0; semantically at (sweep 0, m), so only later writers wait for them
+  auto initial_loads = [&](int m) {
+    auto add = [&](std::size_t L) {
+      if (w_m[L] < 0) readers[L].push_back({m, 2});
+    };
+    for (int p = 0; p < 3 * n; ++p) {
+      int i, j;
+      if (p <= n) i = p, j = 0;
+      else if (p <= 2 * n) i = 0, j = p - n;
+      else j = p - 2 * n, i = n - j;
+      add(static_cast<std::size_t>(m) * S + lattice_index(n, i, j));
+    }
+    for (int x = lv.ghost_ptr[m]; x < lv.ghost_ptr[m + 1]; ++x) add(lv.ghost_off[x]);
+  };
+  // what each macro holds: per boundary position and per ghost slot, the write serial
+  std::vector<std::vector<long long>> know_b(M, std::vector<long long>(3 * n, 0));
+  std::vector<std::vector<long long>> know_g(M);
+  for (int m = 0; m < M; ++m) know_g[m].assign(lv.ghost_ptr[m + 1] - lv.ghost_ptr[m], 0);
+  long long serial = 0;
+
+  struct StepRec {
+    std::map<int, int> req;  // macro -> progress
+    std::vector<std::pair<int, int>> fetch;
+  };
+  std::vector<StepRec> recs(static_cast<std::size_t>(M) * 2 * T);
+  auto bpos_of = [&](int i, int j) { return bpos(n, i, j); };
+  auto is_bnd = [&](int i, int j) { return i == 0 || j == 0 || i + j == n; };
+
+  for (int s = 0; s < 2; ++s)
+    for (int m = 0; m < M; ++m) {
+      if (s == 0) initial_loads(m);
+      std::vector<char> seen_b(3 * n, 0), written_b(3 * n, 0);
+      std::vector<char> seen_g(know_g[m].size(), 0);
+      const int gb = lv.ghost_ptr[m];
+      for (int t = 0; t < T; ++t) {
+        StepRec& R = recs[(static_cast<std::size_t>(m) * 2 + s) * T + t];
+        const int tau = s * T + t;
+        auto need = [&](int m2, int p) {
+          if (m2 == m) return;
+          auto it = R.req.find(m2);
+          if (it == R.req.end() || it->second < p) R.req[m2] = p;
+        };
+        auto first_use = [&](std::size_t L, int dst, long long& know) {
+          if (w_serial[L] == know) return;
+          if (w_m[L] >= 0) need(w_m[L], w_t[L] + 2);
+          R.fetch.push_back({dst, static_cast<int>(L)});
+          readers[L].push_back({m, tau + 2});
+          know = w_serial[L];
+        };
+        auto read_lattice = [&](int i, int j) {
+          if (!is_bnd(i, j)) return;
+          const int bp = bpos_of(i, j);
+          if (written_b[bp] || seen_b[bp]) return;
+          seen_b[bp] = 1;
+          first_use(static_cast<std::size_t>(m) * S + lattice_index(n, i, j), lattice_index(n, i, j), know_b[m][bp]);
+        };
+        auto read_ghost = [&](int x) {
+          if (seen_g[x]) return;
+          seen_g[x] = 1;
+          first_use(static_cast<std::size_t>(lv.ghost_off[gb + x]), -1 - x, know_g[m][x]);
+        };
+        auto write = [&](std::size_t L) {
+          if (!tracked[L]) return;
+          for (const Reader& r : readers[L]) need(r.m, r.th);
+          if (w_m[L] >= 0) need(w_m[L], w_t[L] + 2);
+          w_serial[L] = ++serial;
+          w_m[L] = m;
+          w_t[L] = tau;
+          readers[L].clear();
+        };
+        // the relaxations of wavefront step t: reads first (no node reads a
+        // node of its own step), then writes
+        std::vector<std::pair<int, int>> nodes;
+        for (int j = 0; j <= n; ++j) {
+          const int i = t - 2 * j;
+          if (i >= 0 && i <= n - j) nodes.push_back({i, j});
+        }
+        for (auto [i, j] : nodes) {
+          if (!is_bnd(i, j)) {
+            for (int d = 0; d < 6; ++d) read_lattice(i + kDij2[d][0], j + kDij2[d][1]);
+            continue;
+          }
+          const BNode& bn = lv.bnode[static_cast<std::size_t>(m) * 3 * n + bpos_of(i, j)];
+          if (bn.domain) continue;
+          for (int q = 0; q < bn.rec_count; ++q) {
+            const MemberRec& mr = lv.rec[bn.rec_begin + q];
+            for (int c = 0; c < 6; ++c) {
+              if (!((mr.mask >> c) & 1)) continue;
+              for (int z = 0; z < 2; ++z) {
+                const int code = mr.code[2 * c + z];
+                if (code < 6)
+                  read_lattice(i + kDij2[code][0], j + kDij2[code][1]);
+                else
+                  read_ghost(code - 6);
+              }
+            }
+          }
+        }
+        for (auto [i, j] : nodes) {
+          if (is_bnd(i, j)) {
+            const int bp = bpos_of(i, j);
+            const int g = lv.node_gid[static_cast<std::size_t>(m) * S + lattice_index(n, i, j)];
+            for (int q = lv.grp_ptr[g]; q < lv.grp_ptr[g + 1]; ++q)
+              write(static_cast<std::size_t>(lv.mem_slot[q]) * S + lv.mem_idx[q]);
+            written_b[bp] = 1;
+            know_b[m][bp] = w_serial[static_cast<std::size_t>(m) * S + lattice_index(n, i, j)];  // m's own write
+          } else if (i == 1 || j == 1 || i + j == n - 1) {
+            write(static_cast<std::size_t>(m) * S + lattice_index(n, i, j));  // exported (write-through)
+          }
+        }
+      }
+    }
+  PipeTables2D& P = lv.pipe;
+  P = PipeTables2D{};
+  for (const StepRec& R : recs) {
+    P.maxreq = std::max(P.maxreq, static_cast<int>(R.req.size()));
+    P.maxfetch = std::max(P.maxfetch, static_cast<int>(R.fetch.size()));
+  }
+  if (P.maxreq > 32 || P.maxfetch > 32) return;  // not supported: the macro-DAG smoother runs
+  P.rec_words = (2 + 2 * P.maxreq + 2 * P.maxfetch + 3) & ~3;  // 16-byte records
+  P.rec.assign(recs.size() * P.rec_words, 0);
+  for (std::size_t r = 0; r < recs.size(); ++r) {
+    std::int32_t* w = &P.rec[r * P.rec_words];
+    w[0] = static_cast<std::int32_t>(recs[r].req.size());
+    w[1] = static_cast<std::int32_t>(recs[r].fetch.size());
+    int k = 0;
+    for (const auto& [m2, p] : recs[r].req) {
+      w[2 + 2 * k] = m2;
+      w[3 + 2 * k] = p;
+      ++k;
+    }
+    for (std::size_t f = 0; f < recs[r].fetch.size(); ++f) {
+      w[2 + 2 * P.maxreq + 2 * f] = recs[r].fetch[f].first;
+      w[3 + 2 * P.maxreq + 2 * f] = recs[r].fetch[f].second;
+    }
+  }
+  P.ok = true;
+  if (getenv("KB_PIPE_DEBUG")) {
+    long long nr = 0, nf = 0;
+    for (const StepRec& R : recs) nr += R.req.size(), nf += R.fetch.size();
+    std::fprintf(stderr, "pipe tables M=%d n=%d: maxreq %d maxfetch %d, total req %lld fetch %lld (%.2f / %.2f per step)\n", M, n,
+                 P.maxreq, P.maxfetch, nr, nf, double(nr) / recs.size(), double(nf) / recs.size());
+  }
+}
+}  // namespace
+
+void Hierarchy2D::build_pipe_tables() {
+  for (int l = 1; l <= L; ++l) {
+    Level2D& lv = levels[l];
+    if (lv.n < min_pipe_n() || lv.sc_nu > 0 || lv.n > 128) continue;
+    build_level(*this, lv);
+  }
+}
+
+}  // namespace kb

@@ -76,7 +76,7 @@ std::unique_ptr<DeviceHierarchy2D> DeviceHierarchy2D::create(const Mesh2D& mesh,
              vbytes(wq[l]) + vbytes(lv.prog) + vbytes(lv.prog_ptr) + vbytes(lv.prog_extra) + vbytes(lv.xtra_ptr) +
              vbytes(lv.sc_cell_copy) + vbytes(lv.sc_copy_cell) + vbytes(lv.sc_mtab) + vbytes(lv.sc_gtab) +
              vbytes(lv.sched[0].blocks) + vbytes(lv.sched[0].lev_off) + vbytes(lv.sched[1].blocks) +
-             vbytes(lv.sched[1].lev_off);
+             vbytes(lv.sched[1].lev_off) + vbytes(lv.pipe.rec);
   }
   d->arena.reserve(bytes + 4096);
   d->dh.M = M;
@@ -122,6 +122,11 @@ std::unique_ptr<DeviceHierarchy2D> DeviceHierarchy2D::create(const Mesh2D& mesh,
     dl.max_extra = lv.max_extra;
     dl.geo = d->arena.upload(geo[l]);
     dl.wq = d->arena.upload(wq[l]);
+    if (lv.pipe.ok) {
+      dl.pipe_rec = d->arena.upload(lv.pipe.rec);
+      dl.pipe_rec_words = lv.pipe.rec_words;
+      dl.pipe_maxreq = lv.pipe.maxreq;
+    }
     dl.sc_nu = lv.sc_nu;
     if (lv.sc_nu > 0) {
       dl.sc_cell_copy = d->arena.upload(lv.sc_cell_copy);
