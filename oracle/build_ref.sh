@@ -62,6 +62,9 @@ for u in $SRCS; do
 done
 $CXX $BASE_FLAGS -O2 -c "$HERE/ref_driver.cpp" -o "$OUT/obj/ref_driver.o"
 $CXX $BASE_FLAGS -O3 -march=native -ffp-contract=fast -c "$HERE/ref_driver.cpp" -o "$OUT/obj_fma/ref_driver.o"
-$CXX -o "$OUT/ref_driver" "$OUT"/obj/*.o
-$CXX -o "$OUT/ref_driver_fma" "$OUT"/obj_fma/*.o
+# the builder's 3-d C oracle (config 4 AMR meshes: eta_T for the reference's 3-d refinement)
+${CC:-gcc} -O2 -std=c11 -D_GNU_SOURCE -c "$HERE/klref_oracle3d.c" -o "$OUT/obj/oracle3d.o"
+cp "$OUT/obj/oracle3d.o" "$OUT/obj_fma/oracle3d.o"
+$CXX -o "$OUT/ref_driver" "$OUT"/obj/*.o -lm
+$CXX -o "$OUT/ref_driver_fma" "$OUT"/obj_fma/*.o -lm
 echo "built $OUT/ref_driver and $OUT/ref_driver_fma"

@@ -18,6 +18,12 @@
 //   ref_driver amr   <mesh> <sin|lshape> <L> <nu> <K> <halfmax|top10> <outdir>
 //   ref_driver ops   <mesh> <L> <seed> <outdir>
 //   ref_driver time  <mesh> <sin|lshape> <L> <nu> <reps> [budget_s]
+//   ref_driver amr3d <L> <nu> <K> <outdir>
+//       BASELINE.json config 4: the unit cube as 6 Kuhn tetrahedra, K steps of
+//       (3-d estimate -> marks >= 0.5 max on the green-reverted set ->
+//       refine_rg_3d, proj/src/macro_mesh.cpp:662-676).  The reference has no
+//       3-d solver: eta_T comes from the builder's 3-d C oracle
+//       (klref_oracle3d.c, Gaussian peak problem) on the mesh as written and re-read.
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -284,6 +290,102 @@ int cmd_amr(int argc, char** argv) {
   return 0;
 }
 
+extern "C" {
+struct o3h;
+o3h* o3_build(int nv, const double* xyz, int ne, const int* tet_in, int L);
+void o3_free(o3h* h);
+int o3_level_size(const o3h* h, int l);
+long long o3_dofs(const o3h* h, int l);
+int o3_fmg(const o3h* h, int prob, const double* par, int nu, int pre, int post, double rel, double absf, int maxit,
+           double** u, double** b, double** w);
+int o3_estimate(const o3h* h, const double* uL, double** w, double* out4, double* local_sums);
+}
+
+MacroMesh kuhn_unit_cube() {
+  std::vector<Point> verts;
+  for (int k = 0; k <= 1; ++k)
+    for (int j = 0; j <= 1; ++j)
+      for (int i = 0; i <= 1; ++i) verts.push_back({double(i), double(j), double(k)});
+  auto at = [](int i, int j, int k) { return static_cast<Index>((k * 2 + j) * 2 + i); };
+  // the Kuhn subdivision of proj/src/problems.cpp:122-133 on one cube
+  static const int perms[6][3][3] = {
+      {{1, 0, 0}, {1, 1, 0}, {1, 1, 1}}, {{1, 0, 0}, {1, 0, 1}, {1, 1, 1}},
+      {{0, 1, 0}, {1, 1, 0}, {1, 1, 1}}, {{0, 1, 0}, {0, 1, 1}, {1, 1, 1}},
+      {{0, 0, 1}, {1, 0, 1}, {1, 1, 1}}, {{0, 0, 1}, {0, 1, 1}, {1, 1, 1}}};
+  std::vector<std::array<Index, 4>> elems;
+  for (const auto& p : perms)
+    elems.push_back({at(0, 0, 0), at(p[0][0], p[0][1], p[0][2]), at(p[1][0], p[1][1], p[1][2]),
+                     at(p[2][0], p[2][1], p[2][2])});
+  return MacroMesh::create(3, std::move(verts), std::move(elems));
+}
+
+int cmd_amr3d(int argc, char** argv) {
+  if (argc < 6) return 2;
+  const int L = std::atoi(argv[2]), nu = std::atoi(argv[3]), K = std::atoi(argv[4]);
+  const std::string outdir = argv[5];
+  std::filesystem::create_directories(outdir);
+  MacroMesh mesh = kuhn_unit_cube();
+  for (int k = 0; k <= K; ++k) {
+    const std::string path = outdir + "/cfg4_k" + std::to_string(k) + ".mesh";
+    write_mesh_file(mesh, path);
+    const MacroMesh fm = read_mesh_file(path);  // the numbering the solvers see
+    std::vector<double> xyz;
+    for (Index v = 0; v < static_cast<Index>(fm.num_vertices()); ++v)
+      for (int a = 0; a < 3; ++a) xyz.push_back(fm.vertex(v).coords[a]);
+    std::vector<int> tets;
+    for (Index id : fm.active())
+      for (int a = 0; a < 4; ++a) tets.push_back(fm.element(id).v[a]);
+    o3h* h = o3_build(static_cast<int>(fm.num_vertices()), xyz.data(), static_cast<int>(fm.num_active()),
+                      tets.data(), L);
+    std::vector<std::vector<double>> U(L + 1), B(L + 1), W(L + 1);
+    std::vector<double*> up(L + 1), bp(L + 1), wp(L + 1);
+    for (int l = 0; l <= L; ++l) {
+      U[l].assign(o3_level_size(h, l), 0.0);
+      B[l].assign(o3_level_size(h, l), 0.0);
+      up[l] = U[l].data();
+      bp[l] = B[l].data();
+      if (l < L) {
+        W[l].assign(o3_level_size(h, l + 1), 0.0);
+        wp[l] = W[l].data();
+      }
+    }
+    const int st = o3_fmg(h, 2 /* gauss */, nullptr, nu, 2, 2, 1e-9, 1e-12, 100000, up.data(), bp.data(), wp.data());
+    if (st != 0) throw std::runtime_error("3-d oracle FMG failed");
+    double out4[4];
+    std::vector<double> sums(2 * fm.num_active());
+    o3_estimate(h, up[L], wp.data(), out4, sums.data());
+    std::vector<double> eta_local(fm.num_active());
+    for (std::size_t t = 0; t < eta_local.size(); ++t) eta_local[t] = std::sqrt(std::max(0.0, sums[2 * t]));
+    std::ostringstream r;
+    r << "num_macros " << fm.num_active() << "\n";
+    r << "dofs " << o3_dofs(h, L) << "\n";
+    r << "active_ids " << join_ids(mesh.active()) << "\n";
+    {
+      std::vector<Index> gp;
+      for (Index id : mesh.active()) {
+        const MacroElement& el = mesh.element(id);
+        gp.push_back(el.state == ElementState::GreenChild ? el.parent : -1);
+      }
+      r << "green_parent " << join_ids(gp) << "\n";
+    }
+    r << "eta " << fmt(out4[3]) << "\n";
+    r << "norm_base " << fmt(out4[0]) << "\n";
+    r << "norm_coarser " << fmt(out4[1]) << "\n";
+    r << "eta_local " << join(eta_local) << "\n";
+    o3_free(h);
+    if (k < K) {
+      auto [rev, agg] = reverted_indicator(mesh, eta_local);
+      const MarkSet m = mark_half_max(rev, agg);
+      r << "reverted_ids " << join_ids(rev.active()) << "\n";
+      r << "marks_halfmax_eta " << join_ids(m.ids) << "\n";
+      mesh = refine_rg_3d(rev, m);
+    }
+    write_text(outdir + "/cfg4_k" + std::to_string(k) + "_report.txt", r.str());
+    std::fprintf(stderr, "amr3d k=%d: %zu macros, eta %.6e\n", k, fm.num_active(), out4[3]);
+  }
+  return 0;
+}
+
 int cmd_ops(int argc, char** argv) {
   if (argc < 6) return 2;
   const MacroMesh mesh = read_mesh_file(argv[2]);
@@ -450,6 +552,7 @@ int main(int argc, char** argv) {
     if (cmd == "solve") return cmd_solve(argc, argv);
     if (cmd == "amr") return cmd_amr(argc, argv);
     if (cmd == "ops") return cmd_ops(argc, argv);
+    if (cmd == "amr3d") return cmd_amr3d(argc, argv);
     if (cmd == "time") return cmd_time(argc, argv);
     if (cmd == "timeall") return cmd_timeall(argc, argv);
   } catch (const std::exception& e) {
