@@ -264,6 +264,62 @@ def run_3d(K, torch, name, N, L, prob, reps, peak):
             "build_s": build_s, "parity": "builder 3-d oracle (oracle/klref_oracle3d.c), bitwise on small cases"}
 
 
+def run_cfg4(K, torch, reps, peak):
+    """Config 4: the 3-d AMR sequence (tests/golden/cfg4_k*.mesh, the reference's
+    refine_rg_3d driven by the 3-d oracle): one step = FMG + estimate + the
+    >= 0.5 max marks on each of the five meshes, device time."""
+    with open(os.path.join(MESH_DIR, "cfg4.json")) as fh:
+        meta = json.load(fh)
+    L = meta["level"]
+    hs, solvers = [], []
+    for k in range(len(meta["steps"])):
+        h = K.GridHierarchy.build(K.MacroMesh.read(os.path.join(MESH_DIR, f"cfg4_k{k}.mesh")), L)
+        hs.append(h)
+        solvers.append(K.MultigridSolver(h, K.Problem(K.PROBLEM_GAUSS3D), K.SolverConfig(nu=meta["nu"])))
+    stream = torch.cuda.Stream()
+    for s in solvers:
+        s.set_stream(stream.cuda_stream)
+    flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
+
+    def step():
+        marks_ok = True
+        for s in solvers:
+            s.fmg_enqueue()
+            s.error_estimate_enqueue(1)
+        for k, s in enumerate(solvers):
+            s.synchronize()
+            rep = s.error_estimate_finish(1, K.UNSCALED)
+            st = meta["steps"][k]
+            if "marks_halfmax_eta" in st:
+                marks_ok &= K.mark(K.MARK_HALF_MAX, 0.0, st["active_ids"], st["green_parent"], rep.eta_local,
+                                   st["reverted_ids"]) == st["marks_halfmax_eta"]
+        return marks_ok
+
+    step()
+    times, ok = [], True
+    for it in range(reps):
+        with torch.cuda.stream(stream):
+            flush.fill_(float(it))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for s in solvers:
+            s.fmg_enqueue()
+            s.error_estimate_enqueue(1)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+        ok &= step()
+    ms = sum(times) / len(times)
+    dofs = sum(h.dof_count(L) for h in hs)
+    return {"config": "cfg4: unit cube, 6 Kuhn tets -> 4 kl AMR steps (meshes k=0..4), l=6, Gaussian peak, "
+                      "FMG V(2,2) + estimator per mesh", "macros": [h.num_macros() for h in hs], "level": L,
+            "dofs": dofs, "ms_fmg_plus_estimate": ms, "value": dofs / (ms * 1e-3) / 1e9, "unit": "GDoF/s",
+            "fmg_roofline": {"alg_bytes": fmg_bytes_3d(dofs, meta["nu"]),
+                             "frac": fmg_bytes_3d(dofs, meta["nu"]) / (ms * 1e-3) / 1e9 / peak},
+            "marks_equal_fixture": bool(ok),
+            "parity": "eta_T within 1e-9 and identical marks vs the 3-d oracle fixtures (tests/test_cfg4_3d.py)"}
+
+
 def run_3d_sharded(K, torch, dist, world, rank, reps, peak, barrier, max_over_ranks):
     """Config 5 strong scaling: the 3072 macro tets sharded over the `world`
     GPUs (contiguous slot ranges = z-slabs), interface exchange over NCCL,
@@ -514,6 +570,7 @@ def impl_ours(args):
         try:
             peak3, _ = peaks()
             extra3d = {"cfg3": run_3d(K, torch, "cfg3: unit cube, 4^3 Kuhn cubes, l=6, sin3", 4, 6, "sin3", 3, peak3),
+                       "cfg4": run_cfg4(K, torch, 3, peak3),
                        "cfg5_one_gpu": run_3d(K, torch, "cfg5: unit cube, 8^3 Kuhn cubes, l=6, sine series (g=0)",
                                               8, 6, "series", 2, peak3)}
             if world == 1 and not args.no_cpu_baseline:
