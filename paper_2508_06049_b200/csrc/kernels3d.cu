@@ -1249,7 +1249,11 @@ void launch3_cg0(const DevLevel3D& lv0, double* u, const double* b, double* scra
   // member-parallel operator when the member partials fit next to the vectors
   const int nmem4 = lv0.cg_members4 > 0 && base + lv0.cg_members4 * 8.0 <= 200 * 1024 ? lv0.cg_members4 : 0;
   const size_t smem = base + static_cast<size_t>(nmem4) * 8;
-  KB_CUDA_CHECK(cudaFuncSetAttribute(k3_cg0, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  static size_t cg0_high = 0;  // only ever grows (graph nodes captured earlier stay launchable)
+  if (smem > cg0_high) {
+    KB_CUDA_CHECK(cudaFuncSetAttribute(k3_cg0, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    cg0_high = smem;
+  }
   k3_cg0<<<1, 1024, smem, st>>>(lv0, u, b, prm, status, nmem4);
   check3("k3_cg0");
 }
