@@ -84,7 +84,8 @@ typedef struct klref_problem_s* klref_problem;
 typedef struct klref_solver_s* klref_solver;
 typedef struct klref_gf_s* klref_gf;
 
-/* SolverConfig, proj/include/klref/multigrid.hpp:19-29 (finest_policy: 0 = None) */
+/* SolverConfig, proj/include/klref/multigrid.hpp:19-29 (finest_policy: 0 = None,
+ * 1 = ValidationTwoDigits on 2-d hierarchies; the reference default is 1) */
 typedef struct {
   int nu;
   int pre_smooth;
@@ -95,6 +96,7 @@ typedef struct {
   int finest_policy;
   int faithful_source; /* 1: host-tabulated f (bitwise-faithful RHS); 0: device-evaluated f */
   int use_graph;       /* 1: replay the FMG as one CUDA graph */
+  int max_extra_cycles; /* SolverConfig::max_extra_cycles (ValidationTwoDigits) */
 } klref_solver_config;
 
 /* EstimateReport, proj/include/klref/estimator.hpp:15-24 (eta_local returned separately) */
@@ -156,6 +158,8 @@ int klref_problem_create_host(double (*source)(double, double, void*), double (*
 /* 3-d host callbacks (f, g of x, y, z), tabulated on the host in faithful mode */
 int klref_problem_create_host3(double (*source)(double, double, double, void*),
                                double (*boundary)(double, double, double, void*), void* ctx, klref_problem* out);
+/* ProblemSpec::exact for a host problem (proj/include/klref/fem.hpp:57-60): has_exact = true */
+int klref_problem_set_exact(klref_problem p, double (*exact)(double, double, void*), void* ctx);
 /* parameters of KLREF_PROBLEM_SERIES3D: count = 64 coefficients C_abc, a fastest */
 int klref_problem_set_params(klref_problem p, const double* params, int count);
 void klref_problem_destroy(klref_problem p);
@@ -192,6 +196,12 @@ int klref_solver_set_profiling(klref_solver s, int on);
 int klref_solver_kernel_stats(klref_solver s, int kind, double* ms, int* launches, double* bytes);
 /* FmgState::u/b/w (proj/include/klref/multigrid.hpp:43-53), copied to the host */
 int klref_solver_state_read(klref_solver s, int which, int level, double* host_out);
+
+/* ExactErrorEvaluator(h, p, L).evaluate(u_L), proj/src/fem.cpp:358-420 (three-term
+ * moment form, pointwise fallback :422-455); per_macro[M] may be NULL (2-d) */
+int klref_solver_exact_error(klref_solver s, double* global, double* per_macro);
+/* FmgState::extra_cycles of the last fmg() (FinestPolicy::ValidationTwoDigits) */
+int klref_solver_extra_cycles(klref_solver s, int* out);
 
 /* error_estimate(state, j, kind), proj/src/estimator.cpp:8-45; eta_local[M] may be NULL */
 int klref_error_estimate(klref_solver s, int offset, int kind, klref_estimate_report* out, double* eta_local);

@@ -363,7 +363,7 @@ class FmgState {
   SolverConfig config;
   Levels u, b, w;
   int extra_cycles = 0;
-  std::shared_ptr<const void> error_eval;  // validation mode only (not on the device)
+  std::shared_ptr<const void> error_eval;  // unused: exact_error_norm(state) evaluates on the device
 
  private:
   friend class MultigridSolver;
@@ -381,10 +381,11 @@ class FmgState {
 
 namespace detail {
 struct HostProblem {
-  std::function<double(double, double)> source, boundary;
+  std::function<double(double, double)> source, boundary, exact;
 };
 inline double src_cb(double x, double y, void* p) { return static_cast<HostProblem*>(p)->source(x, y); }
 inline double bnd_cb(double x, double y, void* p) { return static_cast<HostProblem*>(p)->boundary(x, y); }
+inline double exact_cb(double x, double y, void* p) { return static_cast<HostProblem*>(p)->exact(x, y); }
 }  // namespace detail
 
 class MultigridSolver {
@@ -392,12 +393,13 @@ class MultigridSolver {
   // MultigridSolver(h, p, cfg), proj/src/multigrid.cpp:113-119.  Like the
   // reference, p is not owned; f and g are tabulated here.
   MultigridSolver(HierarchyPtr h, const ProblemSpec& p, SolverConfig cfg) : h_(std::move(h)), p_(&p), cfg_(cfg) {
-    if (cfg.finest_policy != FinestPolicy::None)
-      throw StructuralError("only FinestPolicy::None runs on the device (validation policies need ExactErrorEvaluator)");
-    hp_ = std::make_unique<detail::HostProblem>(detail::HostProblem{p.source, p.boundary});
+    if (cfg.finest_policy == FinestPolicy::ResidualVsEstimate)
+      throw StructuralError("FinestPolicy::ResidualVsEstimate does not run on the device");
+    hp_ = std::make_unique<detail::HostProblem>(detail::HostProblem{p.source, p.boundary, p.exact});
     klref_problem prob = nullptr;
     detail::check(klref_problem_create_host(detail::src_cb, detail::bnd_cb, hp_.get(), &prob));
     detail::Handle<klref_problem, klref_problem_destroy> hprob(prob);
+    if (p.has_exact && p.exact) detail::check(klref_problem_set_exact(prob, detail::exact_cb, hp_.get()));
     klref_solver_config c;
     klref_solver_config_default(&c);
     c.nu = cfg.nu;
@@ -406,6 +408,8 @@ class MultigridSolver {
     c.coarse_rel_tol = cfg.coarse_rel_tol;
     c.coarse_abs_floor = cfg.coarse_abs_floor;
     c.coarse_max_iter = cfg.coarse_max_iter;
+    c.finest_policy = cfg.finest_policy == FinestPolicy::ValidationTwoDigits ? 1 : 0;
+    c.max_extra_cycles = cfg.max_extra_cycles;
     c.faithful_source = 1;
     klref_solver s = nullptr;
     detail::check(klref_solver_create(h_->handle(), prob, &c, &s));
@@ -418,7 +422,9 @@ class MultigridSolver {
   // MultigridSolver::fmg, proj/src/multigrid.cpp:248-321
   FmgState fmg() {
     detail::check(klref_solver_fmg(s_->h));
-    return FmgState(s_, h_, cfg_);
+    FmgState st(s_, h_, cfg_);
+    detail::check(klref_solver_extra_cycles(s_->h, &st.extra_cycles));
+    return st;
   }
   // single operations, proj/src/multigrid.cpp:127-229
   void gauss_seidel(int l, GridFunction& u, const GridFunction& b, int sweeps) {
@@ -496,6 +502,22 @@ inline EstimateReport error_estimate(const FmgState& state, int offset, Estimato
   out.norm_base = r.norm_base;
   out.conv_factor = r.conv_factor;
   out.eta = r.eta;
+  return out;
+}
+
+// ---------------------------------------------------------------- fem.hpp (validation)
+struct ErrorNorms {
+  double global = 0.0;
+  std::vector<double> per_macro;
+};
+
+// exact_error_norm(p, state.u.back()), proj/src/fem.cpp:358-476: the
+// ExactErrorEvaluator of the state's finest level (the solver's problem must
+// carry `exact`; 2-d)
+inline ErrorNorms exact_error_norm(const FmgState& state) {
+  ErrorNorms out;
+  out.per_macro.assign(static_cast<std::size_t>(state.h->num_macros()), 0.0);
+  detail::check(klref_solver_exact_error(EstimateAccess::solver(state), &out.global, out.per_macro.data()));
   return out;
 }
 

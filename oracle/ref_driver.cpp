@@ -18,6 +18,7 @@
 //   ref_driver amr   <mesh> <sin|lshape> <L> <nu> <K> <halfmax|top10> <outdir>
 //   ref_driver ops   <mesh> <L> <seed> <outdir>
 //   ref_driver time  <mesh> <sin|lshape> <L> <nu> <reps> [budget_s]
+//   ref_driver solvevtd <mesh> <sin|lshape> <L> <nu> <outdir>   (FinestPolicy::ValidationTwoDigits)
 //   ref_driver amr3d <L> <nu> <K> <outdir>
 //       BASELINE.json config 4: the unit cube as 6 Kuhn tetrahedra, K steps of
 //       (3-d estimate -> marks >= 0.5 max on the green-reverted set ->
@@ -386,6 +387,30 @@ int cmd_amr3d(int argc, char** argv) {
   return 0;
 }
 
+// FinestPolicy::ValidationTwoDigits (the reference default, multigrid.cpp:282-293)
+int cmd_solvevtd(int argc, char** argv) {
+  if (argc < 7) return 2;
+  const MacroMesh mesh = read_mesh_file(argv[2]);
+  const ProblemSpec p = make_problem(argv[3]);
+  const int L = std::atoi(argv[4]), nu = std::atoi(argv[5]);
+  const std::string outdir = argv[6];
+  std::filesystem::create_directories(outdir);
+  SolverConfig sc;
+  sc.nu = nu;
+  sc.finest_policy = FinestPolicy::ValidationTwoDigits;
+  auto h = GridHierarchy::build(mesh, L);
+  MultigridSolver solver(h, p, sc);
+  FmgState st = solver.fmg();
+  dump(st.u[L], outdir + "/u_" + std::to_string(L) + ".bin");
+  const ErrorNorms ex = st.error_eval ? st.error_eval->evaluate(st.u[L]) : exact_error_norm(p, st.u[L]);
+  std::ostringstream r;
+  r << "extra_cycles " << st.extra_cycles << "\n";
+  r << "exact_global " << fmt(ex.global) << "\n";
+  r << "exact_local " << join(ex.per_macro) << "\n";
+  write_text(outdir + "/report.txt", r.str());
+  return 0;
+}
+
 int cmd_ops(int argc, char** argv) {
   if (argc < 6) return 2;
   const MacroMesh mesh = read_mesh_file(argv[2]);
@@ -553,6 +578,7 @@ int main(int argc, char** argv) {
     if (cmd == "amr") return cmd_amr(argc, argv);
     if (cmd == "ops") return cmd_ops(argc, argv);
     if (cmd == "amr3d") return cmd_amr3d(argc, argv);
+    if (cmd == "solvevtd") return cmd_solvevtd(argc, argv);
     if (cmd == "time") return cmd_time(argc, argv);
     if (cmd == "timeall") return cmd_timeall(argc, argv);
   } catch (const std::exception& e) {

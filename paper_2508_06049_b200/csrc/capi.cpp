@@ -305,6 +305,14 @@ int klref_problem_create_host(double (*source)(double, double, void*), double (*
     *out = p.release();
   });
 }
+int klref_problem_set_exact(klref_problem p, double (*exact)(double, double, void*), void* ctx) {
+  return guarded([&] {
+    need(p, "problem");
+    need(reinterpret_cast<const void*>(exact), "exact");
+    p->p.exact = [exact, ctx](double x, double y) { return exact(x, y, ctx); };
+    p->p.has_exact = true;
+  });
+}
 int klref_problem_create_host3(double (*source)(double, double, double, void*),
                                double (*boundary)(double, double, double, void*), void* ctx, klref_problem* out) {
   return guarded([&] {
@@ -340,6 +348,7 @@ void klref_solver_config_default(klref_solver_config* cfg) {
   cfg->finest_policy = 0;
   cfg->faithful_source = 0;
   cfg->use_graph = 1;
+  cfg->max_extra_cycles = 60;
 }
 
 int klref_solver_create(klref_hierarchy h, klref_problem p, const klref_solver_config* cfg, klref_solver* out) {
@@ -360,6 +369,7 @@ int klref_solver_create(klref_hierarchy h, klref_problem p, const klref_solver_c
       c.finest_policy = cfg->finest_policy;
       c.faithful_source = cfg->faithful_source;
       c.use_graph = cfg->use_graph;
+      c.max_extra_cycles = cfg->max_extra_cycles;
     }
     auto s = std::make_unique<klref_solver_s>();
     if (h->dim == 3) {
@@ -459,6 +469,23 @@ int klref_solver_state_read(klref_solver s, int which, int level, double* host_o
       KB_CUDA_CHECK(cudaMemcpyAsync(host_out, d, count * 8, cudaMemcpyDeviceToHost, v.stream()));
       KB_CUDA_CHECK(cudaStreamSynchronize(v.stream()));
     });
+  });
+}
+
+int klref_solver_exact_error(klref_solver s, double* global, double* per_macro) {
+  return guarded([&] {
+    need(s, "solver");
+    if (!s->s) kb::fail(kb::KB_STRUCTURAL, "the exact-error evaluator is defined for 2-d hierarchies");
+    const auto e = s->s->exact_error();
+    if (global) *global = e.global;
+    if (per_macro) std::copy(e.per_macro.begin(), e.per_macro.end(), per_macro);
+  });
+}
+int klref_solver_extra_cycles(klref_solver s, int* out) {
+  return guarded([&] {
+    need(s, "solver");
+    need(out, "out");
+    *out = s->s ? s->s->extra_cycles() : 0;
   });
 }
 

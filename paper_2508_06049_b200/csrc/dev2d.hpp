@@ -113,6 +113,11 @@ void launch_cg0(const DevLevel2D& lv0, double* u, const double* b, double* scrat
                 DevStatus* status, cudaStream_t st);
 void launch_gs(const DevHier2D& hd, const DevLevel2D& lv, double* u, const double* b, int sweeps,
                int* done, cudaStream_t st);
+// ExactErrorEvaluator::evaluate terms (proj/src/fem.cpp:395-420): per macro
+// cross = sum_k moments[k] u[k] and uh_sq = sum over cells of the mass form,
+// both in the reference's sequential order (one thread per macro);
+// out[2 m] = cross, out[2 m + 1] = uh_sq
+void launch_exact_eval(const DevLevel2D& lv, const double* uL, const double* moments, double* out, cudaStream_t st);
 void launch_estimate(const DevLevel2D& lv, const double* uL, const double* wb, const double* wc,
                      double* sums, cudaStream_t st);
 void launch_dot(const DevLevel2D& lv, const double* a, const double* b, double* partial,

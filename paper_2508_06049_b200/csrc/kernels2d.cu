@@ -1606,6 +1606,37 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
   }
 }
 
+// ---------------------------------------------------------------- exact error (validation)
+// ExactErrorEvaluator::evaluate, proj/src/fem.cpp:395-420: one thread per
+// macro keeps the reference's sequential sums (the three-term form cancels,
+// so the order matters at the 1e-9 level)
+__global__ void k_exact_eval(DevLevel2D lv, const double* __restrict__ uL, const double* __restrict__ mom,
+                             double* out) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= lv.M) return;
+  const int n = lv.n, S = lv.S;
+  const double* cm = uL + static_cast<size_t>(m) * S;
+  const double* mm = mom + static_cast<size_t>(m) * S;
+  double cross = 0.0;
+  for (int k = 0; k < S; ++k) cross += mm[k] * cm[k];
+  const double* ku = lv.kmass + 18 * static_cast<size_t>(m);  // the up-cell mass matrix for every cell
+  const double k0 = ku[0], k1 = ku[1], k2 = ku[2], k3 = ku[3], k4 = ku[4], k5 = ku[5], k6 = ku[6], k7 = ku[7],
+               k8 = ku[8];
+  double uh_sq = 0.0;
+  auto cell = [&](int a, int b, int c) {
+    const double xa = cm[a], xb = cm[b], xc = cm[c];
+    uh_sq += xa * (k0 * xa + k1 * xb + k2 * xc) + xb * (k3 * xa + k4 * xb + k5 * xc) +
+             xc * (k6 * xa + k7 * xb + k8 * xc);
+  };
+  for (int j = 0; j < n; ++j) {
+    const int r0 = dlat(n, 0, j), r1 = dlat(n, 0, j + 1);
+    for (int i = 0; i < n - j; ++i) cell(r0 + i, r0 + i + 1, r1 + i);
+    for (int i = 0; i + 1 < n - j; ++i) cell(r0 + i + 1, r1 + i, r1 + i + 1);
+  }
+  out[2 * m] = cross;
+  out[2 * m + 1] = uh_sq;
+}
+
 // ---------------------------------------------------------------- estimator
 __device__ __forceinline__ double quad_form(const double* k, double a, double b, double c) {
   return a * (k[0] * a + k[1] * b + k[2] * c) + b * (k[3] * a + k[4] * b + k[5] * c) +
@@ -1960,6 +1991,11 @@ void launch_gs(const DevHier2D& hd, const DevLevel2D& lv, double* u, const doubl
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   KB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_gs, hd, lv, u, b, sweeps, done));
+}
+
+void launch_exact_eval(const DevLevel2D& lv, const double* uL, const double* moments, double* out, cudaStream_t st) {
+  k_exact_eval<<<(lv.M + 63) / 64, 64, 0, st>>>(lv, uL, moments, out);
+  check_launch("k_exact_eval");
 }
 
 void launch_estimate(const DevLevel2D& lv, const double* uL, const double* wb, const double* wc, double* sums,

@@ -190,8 +190,8 @@ Solver2D::Solver2D(std::shared_ptr<DeviceHierarchy2D> h, Problem2D p, SolverConf
   const Hierarchy2D& hh = H_->host;
   L_ = hh.L;
   const int M = hh.M;
-  if (cfg_.finest_policy != 0)
-    fail(KB_STRUCTURAL, "only FinestPolicy::None is available on the device path");
+  if (cfg_.finest_policy != 0 && cfg_.finest_policy != 1)
+    fail(KB_STRUCTURAL, "FinestPolicy::ResidualVsEstimate is not available on the device path");
   if (prob_.kind == PROB_ZERO || prob_.kind == PROB_LSHAPE)
     src_kind_ = SRC_ZERO;
   else if (prob_.kind == PROB_SIN2D && !cfg_.faithful_source)
@@ -326,6 +326,8 @@ size_t Solver2D::load_problem(const Problem2D& p) {
   // the device source path (table / zero / device-evaluated) was fixed at construction
   if (p.kind != prob_.kind) fail(KB_STRUCTURAL, "set_problem: the problem kind must match the solver's");
   if (&p != &prob_) prob_ = p;
+  ex_moments_ = nullptr;  // the exact-error moments belong to the previous problem
+  ex_arena_.reset();
   // the staging buffer may still feed an earlier copy
   KB_CUDA_CHECK(cudaStreamSynchronize(stream_));
   tabulate(prob_);
@@ -527,6 +529,146 @@ int Solver2D::last_cg_iters() const { return status_host_ ? status_host_->iters 
 void Solver2D::fmg() {
   fmg_enqueue();
   sync_and_check();
+  extra_cycles_ = 0;
+  // FinestPolicy::ValidationTwoDigits, proj/src/multigrid.cpp:282-293: extra
+  // finest V-cycles until the leading two digits of ||u - u_L|| settle
+  if (cfg_.finest_policy == 1 && prob_.has_exact) {
+    auto round_two_digits = [](double x) {  // proj/src/multigrid.cpp:13-18
+      if (x == 0.0 || !std::isfinite(x)) return x;
+      const double e = std::floor(std::log10(std::abs(x)));
+      const double scale = std::pow(10.0, e - 1.0);
+      return std::round(x / scale) * scale;
+    };
+    double prev = round_two_digits(exact_error().global);
+    for (int extra = 0; extra < cfg_.max_extra_cycles; ++extra) {
+      if (prev == 0.0 || prev < 1e-14) break;
+      vcycle(L_, u_[L_], b_[L_]);
+      sync_and_check();
+      ++extra_cycles_;
+      const double cur = round_two_digits(exact_error().global);
+      if (cur == prev) break;
+      prev = cur;
+    }
+  }
+}
+
+// ExactErrorEvaluator constructor, proj/src/fem.cpp:358-392: moments of the
+// exact solution per lattice copy and the per-macro integral of its square,
+// by the 6-point degree-4 rule per fine cell (host, the reference's order)
+void Solver2D::exact_setup() {
+  if (ex_moments_) return;
+  if (!prob_.has_exact) fail(KB_STRUCTURAL, "the problem has no closed-form solution");
+  const Hierarchy2D& hh = H_->host;
+  const int M = hh.M, n = hh.levels[L_].n, S = hh.levels[L_].S;
+  constexpr double kQa = 0.445948490915965, kQwa = 0.223381589678011;
+  constexpr double kQb = 0.091576213509771, kQwb = 0.109951743655322;
+  const double quad[6][4] = {{1 - 2 * kQa, kQa, kQa, kQwa}, {kQa, 1 - 2 * kQa, kQa, kQwa},
+                             {kQa, kQa, 1 - 2 * kQa, kQwa}, {1 - 2 * kQb, kQb, kQb, kQwb},
+                             {kQb, 1 - 2 * kQb, kQb, kQwb}, {kQb, kQb, 1 - 2 * kQb, kQwb}};
+  std::vector<double> mom(static_cast<size_t>(M) * S, 0.0);
+  ex_usq_.assign(M, 0.0);
+  for (int slot = 0; slot < M; ++slot) {
+    const double cell_area = hh.mesh.area[slot] / (static_cast<double>(n) * n);
+    double* mm = &mom[static_cast<size_t>(slot) * S];
+    double& usq = ex_usq_[slot];
+    const auto& t = hh.mesh.tri[slot];
+    const double c0x = hh.mesh.x[t[0]], c0y = hh.mesh.y[t[0]];
+    const double ux = (hh.mesh.x[t[1]] - c0x) / n, uy = (hh.mesh.y[t[1]] - c0y) / n;
+    const double wx = (hh.mesh.x[t[2]] - c0x) / n, wy = (hh.mesh.y[t[2]] - c0y) / n;
+    auto cell = [&](int a, int b, int c, double i0, double j0, double i1, double j1, double i2, double j2) {
+      for (const auto& q : quad) {
+        const double ii = q[0] * i0 + q[1] * i1 + q[2] * i2;
+        const double jj = q[0] * j0 + q[1] * j1 + q[2] * j2;
+        const double x = c0x + ii * ux + jj * wx;
+        const double y = c0y + ii * uy + jj * wy;
+        const double uval = prob_.exact(x, y);
+        const double wa = q[3] * cell_area;
+        mm[a] += wa * uval * q[0];
+        mm[b] += wa * uval * q[1];
+        mm[c] += wa * uval * q[2];
+        usq += wa * uval * uval;
+      }
+    };
+    for (int j = 0; j < n; ++j) {
+      const int r0 = lattice_index(n, 0, j), r1 = lattice_index(n, 0, j + 1);
+      for (int i = 0; i < n - j; ++i) cell(r0 + i, r0 + i + 1, r1 + i, i, j, i + 1, j, i, j + 1);
+      for (int i = 0; i + 1 < n - j; ++i) cell(r0 + i + 1, r1 + i, r1 + i + 1, i + 1, j, i, j + 1, i + 1, j + 1);
+    }
+  }
+  ex_arena_ = std::make_unique<DeviceArena>();
+  ex_arena_->reserve(mom.size() * 8 + 2 * static_cast<size_t>(M) * 8 + 1024);
+  ex_moments_ = ex_arena_->upload(mom);
+  ex_out_ = static_cast<double*>(ex_arena_->take(2 * static_cast<size_t>(M) * 8));
+}
+
+// ExactErrorEvaluator::evaluate, proj/src/fem.cpp:395-420 (device per-macro
+// terms, host sums in slot order, pointwise fallback on cancellation)
+Solver2D::ExactNorms Solver2D::exact_error() {
+  exact_setup();
+  const int M = H_->host.M;
+  launch_exact_eval(H_->lev[L_], u_[L_], ex_moments_, ex_out_, stream_);
+  std::vector<double> terms(2 * static_cast<size_t>(M));
+  KB_CUDA_CHECK(cudaMemcpyAsync(terms.data(), ex_out_, terms.size() * 8, cudaMemcpyDeviceToHost, stream_));
+  KB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+  ExactNorms out;
+  out.per_macro.assign(M, 0.0);
+  double total = 0.0, scale = 0.0;
+  for (int s = 0; s < M; ++s) {
+    const double e2 = ex_usq_[s] - 2.0 * terms[2 * s] + terms[2 * s + 1];
+    out.per_macro[s] = e2;
+    total += e2;
+    scale += ex_usq_[s] + terms[2 * s + 1];
+  }
+  if (total < 1e-12 * scale) return exact_pointwise();  // proj/src/fem.cpp:416-417
+  for (double& v : out.per_macro) v = std::sqrt(std::max(0.0, v));
+  out.global = std::sqrt(std::max(0.0, total));
+  return out;
+}
+
+// ExactErrorEvaluator::evaluate_pointwise, proj/src/fem.cpp:422-455 (host,
+// the cancellation fallback)
+Solver2D::ExactNorms Solver2D::exact_pointwise() {
+  const Hierarchy2D& hh = H_->host;
+  const int M = hh.M, n = hh.levels[L_].n, S = hh.levels[L_].S;
+  std::vector<double> u(static_cast<size_t>(M) * S);
+  KB_CUDA_CHECK(cudaMemcpy(u.data(), u_[L_], u.size() * 8, cudaMemcpyDeviceToHost));
+  constexpr double kQa = 0.445948490915965, kQwa = 0.223381589678011;
+  constexpr double kQb = 0.091576213509771, kQwb = 0.109951743655322;
+  const double quad[6][4] = {{1 - 2 * kQa, kQa, kQa, kQwa}, {kQa, 1 - 2 * kQa, kQa, kQwa},
+                             {kQa, kQa, 1 - 2 * kQa, kQwa}, {1 - 2 * kQb, kQb, kQb, kQwb},
+                             {kQb, 1 - 2 * kQb, kQb, kQwb}, {kQb, kQb, 1 - 2 * kQb, kQwb}};
+  ExactNorms out;
+  out.per_macro.assign(M, 0.0);
+  double total = 0.0;
+  for (int slot = 0; slot < M; ++slot) {
+    const double* cm = &u[static_cast<size_t>(slot) * S];
+    const double cell_area = hh.mesh.area[slot] / (static_cast<double>(n) * n);
+    const auto& t = hh.mesh.tri[slot];
+    const double c0x = hh.mesh.x[t[0]], c0y = hh.mesh.y[t[0]];
+    const double ux = (hh.mesh.x[t[1]] - c0x) / n, uy = (hh.mesh.y[t[1]] - c0y) / n;
+    const double wx = (hh.mesh.x[t[2]] - c0x) / n, wy = (hh.mesh.y[t[2]] - c0y) / n;
+    double sum = 0.0;
+    auto cell = [&](int a, int b, int c, double i0, double j0, double i1, double j1, double i2, double j2) {
+      const double ca = cm[a], cb = cm[b], cc = cm[c];
+      for (const auto& q : quad) {
+        const double ii = q[0] * i0 + q[1] * i1 + q[2] * i2;
+        const double jj = q[0] * j0 + q[1] * j1 + q[2] * j2;
+        const double x = c0x + ii * ux + jj * wx;
+        const double y = c0y + ii * uy + jj * wy;
+        const double diff = prob_.exact(x, y) - (q[0] * ca + q[1] * cb + q[2] * cc);
+        sum += q[3] * cell_area * diff * diff;
+      }
+    };
+    for (int j = 0; j < n; ++j) {
+      const int r0 = lattice_index(n, 0, j), r1 = lattice_index(n, 0, j + 1);
+      for (int i = 0; i < n - j; ++i) cell(r0 + i, r0 + i + 1, r1 + i, i, j, i + 1, j, i, j + 1);
+      for (int i = 0; i + 1 < n - j; ++i) cell(r0 + i + 1, r1 + i, r1 + i + 1, i + 1, j, i, j + 1, i + 1, j + 1);
+    }
+    out.per_macro[slot] = std::sqrt(sum);
+    total += sum;
+  }
+  out.global = std::sqrt(total);
+  return out;
 }
 
 void Solver2D::estimate_enqueue(int offset) {

@@ -66,7 +66,8 @@ struct SolverConfig2D {
   int nu = 2, pre_smooth = 2, post_smooth = 2;
   double coarse_rel_tol = 1e-9, coarse_abs_floor = 1e-12;
   int coarse_max_iter = 100000;
-  int finest_policy = 0;  // 0 = None (the only device policy so far)
+  int finest_policy = 0;  // 0 = None, 1 = ValidationTwoDigits (proj/include/klref/multigrid.hpp:12-17)
+  int max_extra_cycles = 60;
   int faithful_source = 0;  // 1: host-tabulated f (bitwise-faithful RHS)
   int use_graph = 1;
 };
@@ -118,6 +119,14 @@ class Solver2D {
   void cg_level0(double* u, const double* b);
   double dot_unique(int level, const double* a, const double* b);
   void interface_sync(int level, double* f, int additive);
+  // ExactErrorEvaluator at the finest level (proj/src/fem.cpp:358-476):
+  // global / per-macro ||u - u_L||; three-term moment form, pointwise fallback
+  struct ExactNorms {
+    double global = 0.0;
+    std::vector<double> per_macro;
+  };
+  ExactNorms exact_error();
+  int extra_cycles() const { return extra_cycles_; }
   int launches_per_fmg() const { return fmg_launches_; }
   int launches_per_estimate() const { return est_launches_; }
   int last_cg_iters() const;
@@ -135,6 +144,8 @@ class Solver2D {
   void probe_begin(std::vector<Probe>* list);
   cudaEvent_t event_at(int idx);
   void tabulate(const Problem2D& p);
+  void exact_setup();
+  ExactNorms exact_pointwise();
   double dofs(int l) const { return static_cast<double>(H_->host.levels[l].dofs); }
 
   std::shared_ptr<DeviceHierarchy2D> H_;
@@ -169,6 +180,12 @@ class Solver2D {
   int next_event_ = 0, last_event_ = -1;
   std::vector<Probe>* probes_ = nullptr;
   std::vector<Probe> fmg_probes_, est_probes_;
+  // exact-error evaluator state (built on first use; host moments per copy)
+  std::unique_ptr<DeviceArena> ex_arena_;
+  double* ex_moments_ = nullptr;
+  double* ex_out_ = nullptr;
+  std::vector<double> ex_usq_;
+  int extra_cycles_ = 0;
 };
 
 }  // namespace kb

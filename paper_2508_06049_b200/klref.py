@@ -71,6 +71,7 @@ UNSCALED, SCALED = 0, 1
 SYNC_REPLACE, SYNC_ADDITIVE = 0, 1
 STATE_U, STATE_B, STATE_W = 0, 1, 2
 PROBLEM_ZERO, PROBLEM_SIN2D, PROBLEM_LSHAPE = 0, 1, 2
+POLICY_NONE, POLICY_VALIDATION_TWO_DIGITS = 0, 1
 PROBLEM_SIN3D, PROBLEM_GAUSS3D, PROBLEM_SERIES3D = 3, 4, 5
 MARK_TOP_FRACTION, MARK_HALF_MAX = 0, 1
 KERNEL_ALL, KERNEL_GS, KERNEL_RESIDUAL, KERNEL_RESTRICT, KERNEL_PROLONG = -1, 0, 1, 2, 3
@@ -83,7 +84,7 @@ class SolverConfigC(C.Structure):
     _fields_ = [("nu", C.c_int), ("pre_smooth", C.c_int), ("post_smooth", C.c_int),
                 ("coarse_rel_tol", C.c_double), ("coarse_abs_floor", C.c_double),
                 ("coarse_max_iter", C.c_int), ("finest_policy", C.c_int),
-                ("faithful_source", C.c_int), ("use_graph", C.c_int)]
+                ("faithful_source", C.c_int), ("use_graph", C.c_int), ("max_extra_cycles", C.c_int)]
 
 
 class EstimateReportC(C.Structure):
@@ -124,6 +125,9 @@ SIGNATURES = {
     "klref_problem_create_host": (_I, [_P, _P, _P, _PP]),
     "klref_problem_create_host3": (_I, [_P, _P, _P, _PP]),
     "klref_problem_set_params": (_I, [_P, _PD, _I]),
+    "klref_problem_set_exact": (_I, [_P, _P, _P]),
+    "klref_solver_exact_error": (_I, [_P, _PD, _PD]),
+    "klref_solver_extra_cycles": (_I, [_P, _PI]),
     "klref_problem_destroy": (None, [_P]),
     "klref_solver_config_default": (None, [C.POINTER(SolverConfigC)]),
     "klref_solver_create": (_I, [_P, _P, C.POINTER(SolverConfigC), _PP]),
@@ -401,7 +405,8 @@ class Problem(_Handle):
 
 @dataclass
 class SolverConfig:
-    """SolverConfig, proj/include/klref/multigrid.hpp:19-29 (finest_policy 0 = None)."""
+    """SolverConfig, proj/include/klref/multigrid.hpp:19-29 (finest_policy 0 = None,
+    1 = ValidationTwoDigits on 2-d hierarchies)."""
     nu: int = 2
     pre_smooth: int = 2
     post_smooth: int = 2
@@ -411,11 +416,12 @@ class SolverConfig:
     finest_policy: int = 0
     faithful_source: int = 0
     use_graph: int = 1
+    max_extra_cycles: int = 60
 
     def c(self):
         return SolverConfigC(self.nu, self.pre_smooth, self.post_smooth, self.coarse_rel_tol,
                              self.coarse_abs_floor, self.coarse_max_iter, self.finest_policy,
-                             self.faithful_source, self.use_graph)
+                             self.faithful_source, self.use_graph, self.max_extra_cycles)
 
 
 @dataclass
@@ -536,6 +542,20 @@ class MultigridSolver(_Handle):
 
     def interface_sync(self, f: GridFunction, mode: int):
         _check(lib().klref_interface_sync(self.ptr, f.ptr, mode))
+
+    # -- ExactErrorEvaluator (proj/src/fem.cpp:358-476), 2-d
+    def exact_error(self):
+        """ErrorNorms of ExactErrorEvaluator(h, p, L).evaluate(u_L): (global, per_macro)."""
+        g = C.c_double()
+        loc = np.zeros(self.h.num_macros())
+        _check(lib().klref_solver_exact_error(self.ptr, C.byref(g), _dptr(loc)))
+        return g.value, loc
+
+    def extra_cycles(self) -> int:
+        """FmgState::extra_cycles of the last fmg() (FinestPolicy::ValidationTwoDigits)."""
+        v = C.c_int()
+        _check(lib().klref_solver_extra_cycles(self.ptr, C.byref(v)))
+        return v.value
 
     # -- estimator (proj/src/estimator.cpp:8-45)
     def error_estimate(self, offset: int = 1, kind: int = UNSCALED) -> EstimateReport:
