@@ -410,9 +410,43 @@ __device__ double seq_dot(const DevLevel2D& lv, const double* a, const double* b
   return s;
 }
 
-__global__ void k_cg0(DevLevel2D lv, double* u, const double* b, double* r, double* p, double* ap,
-                      CgParams prm, DevStatus* status) {
+// cg_level0 (proj/src/multigrid.cpp:198-229) in one CTA with its vectors, the
+// dot order and the boundary flags staged in shared memory (level 0 has 3 M
+// copies); the arithmetic and the sequential dot order are unchanged.
+__global__ void k_cg0(DevLevel2D lv, double* ug, const double* bg, CgParams prm, DevStatus* status) {
   const int total = lv.M * lv.S;
+  extern __shared__ __align__(16) double cg_smem[];
+  double* u = cg_smem;
+  double* b = u + total;
+  double* r = b + total;
+  double* p = r + total;
+  double* ap = p + total;
+  double* prod = ap + total;  // the dot products' terms (2 x dot_count)
+  int* dord = reinterpret_cast<int*>(prod + 2 * lv.dot_count);
+  std::uint8_t* flags = reinterpret_cast<std::uint8_t*>(dord + lv.dot_count);
+  for (int k = threadIdx.x; k < total; k += blockDim.x) {
+    u[k] = ug[k];
+    b[k] = bg[k];
+    flags[k] = lv.node_flags[k];
+  }
+  for (int t = threadIdx.x; t < lv.dot_count; t += blockDim.x) dord[t] = lv.dot_order[t];
+  __syncthreads();
+  const int cnt = lv.dot_count;
+  // dot_unique terms in parallel, summed by thread 0 in the sequential order
+  // (s = s + x y exactly as proj/src/hhg.cpp:227-257)
+  auto terms = [&](const double* a, const double* bb, bool zero_bnd, double* out) {
+    for (int t = threadIdx.x; t < cnt; t += blockDim.x) {
+      const int k = dord[t];
+      double x = a[k], y = bb[k];
+      if (zero_bnd && (flags[k] & 2)) x = y = 0.0;
+      out[t] = x * y;
+    }
+  };
+  auto seq_sum = [&](const double* in) {
+    double acc = 0.0;
+    for (int t = 0; t < cnt; ++t) acc += in[t];
+    return acc;
+  };
   __shared__ double sh_rr, sh_alpha, sh_beta;
   __shared__ int sh_go;
   for (int k = threadIdx.x; k < total; k += blockDim.x) apply_node(lv, lv.kstiff, u, r, b, APPLY_RESIDUAL, k);
@@ -421,9 +455,12 @@ __global__ void k_cg0(DevLevel2D lv, double* u, const double* b, double* r, doub
   __syncthreads();
   double tol = 0.0;
   int it = 0;
+  terms(r, r, false, prod);
+  terms(b, b, true, prod + cnt);
+  __syncthreads();
   if (threadIdx.x == 0) {
-    sh_rr = seq_dot(lv, r, r, false);
-    const double bnorm = sqrt(fmax(0.0, seq_dot(lv, b, b, true)));
+    sh_rr = seq_sum(prod);
+    const double bnorm = sqrt(fmax(0.0, seq_sum(prod + cnt)));
     const double a = prm.rel_tol * bnorm;
     tol = (a < prm.abs_floor) ? prm.abs_floor : a;
     sh_go = sqrt(sh_rr) > tol;
@@ -441,8 +478,10 @@ __global__ void k_cg0(DevLevel2D lv, double* u, const double* b, double* r, doub
     if (!sh_go) break;
     for (int k = threadIdx.x; k < total; k += blockDim.x) apply_node(lv, lv.kstiff, p, ap, nullptr, APPLY_ZERO_BND, k);
     __syncthreads();
+    terms(p, ap, false, prod);
+    __syncthreads();
     if (threadIdx.x == 0) {
-      const double pap = seq_dot(lv, p, ap, false);
+      const double pap = seq_sum(prod);
       if (pap <= 0.0) {
         if (status->code == 0) {
           status->code = 2;
@@ -461,8 +500,10 @@ __global__ void k_cg0(DevLevel2D lv, double* u, const double* b, double* r, doub
       r[k] = r[k] + (-alpha) * ap[k];
     }
     __syncthreads();
+    terms(r, r, false, prod);
+    __syncthreads();
     if (threadIdx.x == 0) {
-      const double rr_new = seq_dot(lv, r, r, false);
+      const double rr_new = seq_sum(prod);
       sh_beta = rr_new / sh_rr;
       sh_rr = rr_new;
     }
@@ -474,6 +515,8 @@ __global__ void k_cg0(DevLevel2D lv, double* u, const double* b, double* r, doub
     __syncthreads();
   }
   if (threadIdx.x == 0) status->iters = it;
+  __syncthreads();
+  for (int k = threadIdx.x; k < total; k += blockDim.x) ug[k] = u[k];
 }
 
 // ---------------------------------------------------------------- Gauss-Seidel
@@ -1794,10 +1837,19 @@ void launch_rhs(const DevLevel2D& lv, int src_kind, const double* ftab, double* 
   check_launch("k_rhs");
 }
 
+namespace {
+template <typename K>
+void set_smem(K kernel, size_t smem);
+}  // namespace
+
 void launch_cg0(const DevLevel2D& lv0, double* u, const double* b, double* scratch, CgParams prm,
                 DevStatus* status, cudaStream_t st) {
+  (void)scratch;
   const size_t N = static_cast<size_t>(lv0.M) * lv0.S;
-  k_cg0<<<1, 256, 0, st>>>(lv0, u, b, scratch, scratch + N, scratch + 2 * N, prm, status);
+  const size_t smem = 5 * N * 8 + static_cast<size_t>(lv0.dot_count) * 20 + N + 16;
+  if (smem > 200 * 1024) fail(KB_STRUCTURAL, "coarse mesh too large for the level-0 CG");
+  set_smem(k_cg0, smem);
+  k_cg0<<<1, 256, smem, st>>>(lv0, u, b, prm, status);
   check_launch("k_cg0");
 }
 
