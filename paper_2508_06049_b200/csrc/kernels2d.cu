@@ -817,9 +817,11 @@ __device__ __forceinline__ void relax_nodes(const PNode& p, unsigned us_s, unsig
     }
     st_s64(us_s + 8u * p.k, res);
     if (own_copy) own_copy[p.k] = res;  // pipelined smoother: global copies are the record
-    if (p.wc > 0) copies[p.wr0] = res;
-    if (p.wc > 1) copies[p.wr1] = res;
-    for (int q = p.wb + 2; q < p.wb + p.wc; ++q) copies[wr_global[q]] = res;
+    if (copies) {
+      if (p.wc > 0) copies[p.wr0] = res;
+      if (p.wc > 1) copies[p.wr1] = res;
+      for (int q = p.wb + 2; q < p.wb + p.wc; ++q) copies[wr_global[q]] = res;
+    }
   }
 }
 
@@ -1583,24 +1585,25 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
     } else if (gw == 0) {
       const int type = lane >> 3, mem = lane & 7;
       const int tl = type < 3 ? type : 0;
+      // the next step's lane records are read while waiting for its gate, so
+      // they do not queue in front of this step's lattice reads
       PNode p0, p1;
       load_pnode(p0, ring_s, xs_s, bs_s, tl, mem);
       for (int tau = 0; tau < total; tau += 2) {
-        if (tau + 1 < total)
-          load_pnode(p1, ring_s + static_cast<unsigned>((tau + 1) % kPipeRing) * kStepBytes, xs_s, bs_s, tl, mem);
         if (trace && lane == 0 && tau >= 64 && tau < 128) ptr_bstart[tau - 64] = clock64();
         relax_nodes(p0, us_s, bs_s, gh_s, u, lv.wr, lane, um);
         if (trace && lane == 0 && tau >= 64 && tau < 128) ptr_bend[tau - 64] = clock64() + (ld_s64(us_s) == 12345.0);
         bar_arrive(kPipeBarA0 + tau % kPipeBarAs, bthreads);
         if (tau + 1 >= total) break;
+        load_pnode(p1, ring_s + static_cast<unsigned>((tau + 1) % kPipeRing) * kStepBytes, xs_s, bs_s, tl, mem);
         bar_sync(kPipeBarB, bthreads);
-        if (tau + 2 < total)
-          load_pnode(p0, ring_s + static_cast<unsigned>((tau + 2) % kPipeRing) * kStepBytes, xs_s, bs_s, tl, mem);
         if (trace && lane == 0 && tau + 1 >= 64 && tau + 1 < 128) ptr_bstart[tau + 1 - 64] = clock64();
         relax_nodes(p1, us_s, bs_s, gh_s, u, lv.wr, lane, um);
         if (trace && lane == 0 && tau + 1 >= 64 && tau + 1 < 128) ptr_bend[tau + 1 - 64] = clock64() + (ld_s64(us_s) == 12345.0);
         bar_arrive(kPipeBarA0 + (tau + 1) % kPipeBarAs, bthreads);
-        if (tau + 2 < total) bar_sync(kPipeBarB, bthreads);
+        if (tau + 2 >= total) break;
+        load_pnode(p0, ring_s + static_cast<unsigned>((tau + 2) % kPipeRing) * kStepBytes, xs_s, bs_s, tl, mem);
+        bar_sync(kPipeBarB, bthreads);
       }
     } else {
       const double* st = lv.stencil + 7 * m;
@@ -1998,7 +2001,7 @@ void launch_gs(const DevHier2D& hd, const DevLevel2D& lv, double* u, const doubl
         static int trace = getenv("KB_PIPE_TRACE") ? 1 : 0;
         KB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_gs_pipe, lv, u, b, sweeps, done, lv.pipe_rec, lv.pipe_rec_words,
                                          lv.pipe_maxreq, trace));
-        trace = 0;
+        trace &= ~1;
         return;
       }
     }
