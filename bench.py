@@ -51,6 +51,7 @@ METRIC = "FMG+estimator DoF throughput (cfg2 L-shape AMR meshes, l=7, V(2,2) nu=
 UNIT = "GDoF/s"
 REF_DRIVER = os.path.join(REPO, "oracle", "_ref", "ref_driver")
 FLUSH_BYTES = 256 << 20
+SHARDED_TIMEOUT_S = 300  # watchdog of the NCCL-sharded secondary run
 
 
 def peaks():
@@ -331,7 +332,15 @@ def run_3d_sharded(K, torch, dist, world, rank, reps, peak, barrier, max_over_ra
     h = K.GridHierarchy.build(kuhn_cube(8), L)
     uid = [K.Comm.unique_id() if rank == 0 else None]
     dist.broadcast_object_list(uid, src=0)
-    comm = K.Comm(world, rank, uid[0])
+    # NCCL announces its version on stdout at init: keep stdout for the JSON line
+    sys.stdout.flush()
+    saved = os.dup(1)
+    os.dup2(2, 1)
+    try:
+        comm = K.Comm(world, rank, uid[0])
+    finally:
+        os.dup2(saved, 1)
+        os.close(saved)
     prob = K.Problem(K.PROBLEM_SERIES3D, series_coefficients())
     s = K.ShardedSolver(h, prob, K.SolverConfig(nu=2), comm=comm, rep_level=3)
     build_s = time.perf_counter() - t0
@@ -510,15 +519,14 @@ def impl_ours(args):
     t_e2e = max_over_ranks(sum(e2e_ms) / len(e2e_ms))
     _ = rep
 
-    sharded3d = None
-    if (world > 1 or args.force_sharded_3d) and not args.no_3d:
-        try:
-            sharded3d = run_3d_sharded(K, torch, dist, world, rank, 3, peaks()[0], barrier, max_over_ranks)
-        except Exception as exc:  # secondary numbers never sink the headline line
-            sharded3d = {"error": str(exc)[:300]}
-
+    sharded = (world > 1 or args.force_sharded_3d) and not args.no_3d
     if rank != 0:
-        if world > 1:
+        if sharded:
+            try:
+                run_3d_sharded(K, torch, dist, world, rank, 3, peaks()[0], barrier, max_over_ranks)
+            except Exception:
+                pass
+        if dist.is_initialized():
             dist.destroy_process_group()
         return 0
 
@@ -564,8 +572,8 @@ def impl_ours(args):
             cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference", "sample": f"failed: {exc}"}
 
     extra3d = None
-    if (world > 1 or args.force_sharded_3d) and not args.no_3d:
-        extra3d = {"cfg5_sharded": sharded3d}
+    if sharded:
+        extra3d = {"cfg5_sharded": None}  # filled after the headline line is ready (below)
     elif not args.no_3d:
         try:
             peak3, _ = peaks()
@@ -597,7 +605,30 @@ def impl_ours(args):
         "cpu_baseline": cpu,
         "workloads_3d": extra3d,
     }
-    print(json.dumps(line), flush=True)
+    if sharded:
+        # the NCCL-sharded config-5 run (all ranks): a watchdog prints the
+        # headline line without it and ends the job if it does not finish
+        done = threading.Event()
+        printed = threading.Lock()
+
+        def watchdog():
+            if not done.wait(SHARDED_TIMEOUT_S):
+                with printed:
+                    extra3d["cfg5_sharded"] = {"error": f"timed out after {SHARDED_TIMEOUT_S} s"}
+                    print(json.dumps(line), flush=True)
+                    os._exit(0)
+
+        threading.Thread(target=watchdog, daemon=True).start()
+        try:
+            res = run_3d_sharded(K, torch, dist, world, rank, 3, peaks()[0], barrier, max_over_ranks)
+        except Exception as exc:  # secondary numbers never sink the headline line
+            res = {"error": str(exc)[:300]}
+        with printed:
+            done.set()
+            extra3d["cfg5_sharded"] = res
+            print(json.dumps(line), flush=True)
+    else:
+        print(json.dumps(line), flush=True)
     if dist.is_initialized():
         dist.destroy_process_group()
     return 0
