@@ -67,6 +67,8 @@ void launch3_apply(const DevLevel3D& lv, bool mass, const double* x, double* y, 
 // colours; KB_GS3_SPLIT=1 selects the per-colour launches)
 void launch3_gs(const DevLevel3D& lv, double* u, const double* b, int sweeps, cudaStream_t st);
 int launch3_gs_count(const DevLevel3D& lv, int sweeps);
+int launch3_apply_count(const DevLevel3D& lv);     // kernels per launch3_apply
+int launch3_estimate_count(const DevLevel3D& lv);  // kernels per launch3_estimate
 void launch3_prolong(const DevLevel3D& coarse, const DevLevel3D& fine, const double* c, double* f, int mode,
                      cudaStream_t st);
 // restriction of an owner-masked fine vector (A3_RES_OWNER residual), then

@@ -70,6 +70,16 @@ __device__ __forceinline__ void decode2(int m, int q, int& i, int& j) {
   i = q - lat2(m, 0, jj);
 }
 
+// decode2 for m <= 1024 with one correction step each way (float sqrt is within one row)
+__device__ __forceinline__ void decode2_fast(int m, int q, int& i, int& j) {
+  const float a = 2.0f * m + 3.0f;
+  int jj = static_cast<int>((a - sqrtf(fmaxf(a * a - 8.0f * q, 0.0f))) * 0.5f);
+  jj = jj + (jj < m && lat2(m, 0, jj + 1) <= q);
+  jj = jj - (jj > 0 && lat2(m, 0, jj) > q);
+  j = jj;
+  i = q - lat2(m, 0, jj);
+}
+
 __device__ __forceinline__ int sig3(int n, int i, int j, int k) {
   return (i == 0) | ((j == 0) << 1) | ((k == 0) << 2) | ((i + j + k == n) << 3);
 }
@@ -185,6 +195,25 @@ __device__ __forceinline__ void unpack_ijk(int p, int& i, int& j, int& k) {
   k = (p >> 20) & 1023;
 }
 
+// k-plane streaming helpers (TMA bulk copies into shared-memory plane slots)
+__device__ __forceinline__ void p3_mbar_init(unsigned bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void p3_mbar_wait(unsigned bar, unsigned parity) {
+  unsigned done = 0;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+__device__ __forceinline__ int plane_base(int n, int k) { return tsz(n) - tsz(n - k); }
+// doubles per plane slot: the largest plane (k = 0), +1 alignment pad, 16-byte multiple
+__host__ __device__ __forceinline__ int plane_stride(int n) { return ((n + 1) * (n + 2) / 2 + 3) & ~1; }
+
 // ---------------------------------------------------------------- apply / residual
 // blocks [0, M (n+1)): one k-plane of one macro, lattice-interior nodes;
 // remaining blocks: one shared-node group per thread.
@@ -239,6 +268,188 @@ __global__ void __launch_bounds__(kT) k3_apply(DevLevel3D lv, int mass, const do
     int i, j, k;
     unpack_ijk(lv.mem_ijk[q], i, j, k);
     const size_t off = static_cast<size_t>(lv.mem_slot[q]) * S + lat3(n, i, j, k);
+    if (mode == A3_PLAIN)
+      y[off] = v;
+    else if (mode == A3_RESIDUAL)
+      y[off] = dom ? 0.0 : b[off] - v;
+    else
+      y[off] = (dom || q != beg) ? 0.0 : b[off] - v;
+  }
+}
+
+// Streaming form of the same operator (levels n >= 8), two kernels:
+//  k3_apply_stream  one CTA per macro streams the k-planes of x through a
+//                   4-slot shared-memory ring (TMA bulk copies two planes
+//                   ahead) and writes, for every node of the macro, its full
+//                   stencil row (lattice interior; y or b - y) or its partial
+//                   row (lattice boundary copies; raw) — each x, b, y value
+//                   moves once;
+//  k3_apply_groups  per shared-node group: the member partial rows summed in
+//                   slot order (the additive sync of k3_apply) and the mode's
+//                   write to every copy.
+// Same operations and orders as k3_apply / partial_row (bit-identical).
+constexpr int kAsSlots = 4;
+constexpr int kAsThreads = 256;
+constexpr int kAsPF = 6;  // L2 prefetch distance (planes) ahead of the TMA stream
+
+__global__ void __launch_bounds__(kAsThreads) k3_apply_stream(DevLevel3D lv, int mass, const double* __restrict__ x,
+                                                              double* y, const double* __restrict__ b, int mode) {
+  extern __shared__ __align__(128) unsigned long long as_smem[];
+  const int n = lv.n, S = lv.S, m = blockIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int nwarps = kAsThreads / 32;
+  const int stride = plane_stride(n);
+  double* ps = reinterpret_cast<double*>(as_smem + kAsSlots);  // 16 signatures x 15
+  double* ring = ps + 240;
+  const unsigned bar_s = static_cast<unsigned>(__cvta_generic_to_shared(as_smem));
+  const unsigned ring_s = static_cast<unsigned>(__cvta_generic_to_shared(ring));
+  const double* xm = x + static_cast<size_t>(m) * S;
+  auto issue = [&](int k) {
+    const size_t a = reinterpret_cast<size_t>(xm + plane_base(n, k));
+    const int off = static_cast<int>((a >> 3) & 1);
+    const int len = (n - k + 1) * (n - k + 2) / 2;
+    const unsigned bytes = static_cast<unsigned>(((off + len) * 8 + 15) & ~15);
+    const int slot = k % kAsSlots;
+    const unsigned bar = bar_s + 8u * slot;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            ring_s + 8u * static_cast<unsigned>(slot * stride)),
+        "l"(a - 8 * off), "r"(bytes), "r"(bar)
+        : "memory");
+  };
+  if (tid == 0) {
+    for (int t = 0; t < kAsSlots; ++t) p3_mbar_init(bar_s + 8u * t, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int k = 0; k < 2 && k <= n; ++k) issue(k);
+  }
+  const double* psg = (mass ? lv.psM : lv.psK) + 240 * static_cast<size_t>(m);
+  for (int t = tid; t < 240; t += kAsThreads) ps[t] = __ldg(psg + t);
+  double s[15];
+  {
+    const double* st = (mass ? lv.stM : lv.stK) + 15 * m;
+#pragma unroll
+    for (int d = 0; d < 15; ++d) s[d] = __ldg(st + d);
+  }
+  __syncthreads();
+  const size_t gm = static_cast<size_t>(m) * S;
+  auto l2_prefetch = [&](const double* v, int k) {
+    const int len = (n - k + 1) * (n - k + 2) / 2;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<size_t>(v + plane_base(n, k)) &
+                                                                    ~size_t(15)),
+                 "r"(static_cast<unsigned>((len * 8 + 31) & ~15))
+                 : "memory");
+  };
+  if (tid == 32)
+    for (int k = 2; k < 2 + kAsPF && k <= n; ++k) l2_prefetch(xm, k);
+  if (tid == 64 && b)
+    for (int k = 1; k < 1 + kAsPF && k <= n; ++k) l2_prefetch(b + static_cast<size_t>(m) * S, k);
+  for (int k = 0; k <= n; ++k) {
+    if (tid == 0 && k + 2 <= n) issue(k + 2);  // its slot held plane k - 2, done last step
+    if (tid == 32 && k + 2 + kAsPF <= n) l2_prefetch(xm, k + 2 + kAsPF);
+    if (tid == 64 && b && k + 1 + kAsPF <= n) l2_prefetch(b + static_cast<size_t>(m) * S, k + 1 + kAsPF);
+    if (k + 1 <= n) p3_mbar_wait(bar_s + 8u * ((k + 1) % kAsSlots), ((k + 1) / kAsSlots) & 1);
+    if (k == 0) p3_mbar_wait(bar_s, 0);
+    const int m2 = n - k;
+    int base[3];  // slot base (+ alignment offset) of planes k-1, k, k+1 (clamped to k)
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const int kk = min(max(k - 1 + d, 0), n);
+      base[d] = (kk % kAsSlots) * stride + static_cast<int>((reinterpret_cast<size_t>(xm + plane_base(n, kk)) >> 3) & 1);
+    }
+    const size_t gp = gm + plane_base(n, k);
+    // lattice-interior nodes, flattened: the plane's interior is the triangle
+    // lattice of size m2 - 3 shifted by (1, 1); full stencil
+    if (k >= 1 && m2 >= 3) {
+      const int mi = m2 - 3, ni = (mi + 1) * (mi + 2) / 2;
+      for (int e = tid; e < ni; e += kAsThreads) {
+        int i, j;
+        decode2_fast(mi, e, i, j);
+        ++i, ++j;
+        const int r0 = lat2(m2, 0, j);
+        int ra[7];
+        ra[0] = base[1] + r0;
+        ra[1] = ra[0] + (m2 + 1 - j);
+        ra[2] = ra[0] - (m2 + 2 - j);
+        ra[5] = base[2] + r0 - j;      // plane k + 1: lat2(m2 - 1, 0, j)
+        ra[3] = ra[5] - (m2 + 1 - j);  // lat2(m2 - 1, 0, j - 1)
+        ra[6] = base[0] + r0 + j;      // plane k - 1: lat2(m2 + 1, 0, j)
+        ra[4] = ra[6] + (m2 + 2 - j);  // lat2(m2 + 1, 0, j + 1)
+        const size_t off = gp + r0 + i;
+        const double bv = mode == A3_PLAIN ? 0.0 : __ldg(b + off);
+        double acc = s[0] * ring[ra[0] + i];
+#pragma unroll
+        for (int d = 1; d < 15; ++d) acc = acc + s[d] * ring[ra[dir_row(d)] + i + dir_di(d)];
+        y[off] = mode == A3_PLAIN ? acc : bv - acc;
+      }
+    }
+    // lattice-boundary nodes of the plane: partial rows (raw)
+    const int nb = k == 0 ? (m2 + 1) * (m2 + 2) / 2 : (m2 >= 1 ? 3 * m2 : 1);
+    for (int e = tid; e < nb; e += kAsThreads) {
+      int i, j;
+      if (k == 0) {
+        decode2(m2, e, i, j);
+      } else if (m2 == 0) {
+        i = 0, j = 0;
+      } else if (e < m2 + 1) {  // row j = 0
+        i = e, j = 0;
+      } else if (e < 2 * m2) {  // i = 0, j = 1 .. m2 - 1
+        i = 0, j = e - m2;
+      } else {                  // i = m2 - j, j = 1 .. m2
+        j = e - 2 * m2 + 1, i = m2 - j;
+      }
+      const double* cf = ps + 15 * sig3(n, i, j, k);
+      int ra[7];
+      bool rv[7];
+      int len[7];
+#pragma unroll
+      for (int r = 0; r < 7; ++r) {
+        const int kk = k + row_dk(r), jj = j + row_dj(r), mm = n - kk;
+        rv[r] = kk >= 0 && kk <= n && jj >= 0 && jj <= mm;
+        ra[r] = rv[r] ? base[1 + row_dk(r)] + lat2(mm, 0, jj) : base[1];
+        len[r] = rv[r] ? mm - jj : -1;
+      }
+      const int c0 = ra[0] + i;
+      double acc = cf[0] * ring[c0];
+#pragma unroll
+      for (int d = 1; d < 15; ++d) {
+        const int r = dir_row(d), ii = i + dir_di(d);
+        const bool ok = ii >= 0 && ii <= len[r];
+        const double t = acc + cf[d] * ring[ok ? ra[r] + ii : c0];
+        acc = ok ? t : acc;
+      }
+      y[gp + lat2(m2, 0, j) + i] = acc;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kT) k3_apply_groups(DevLevel3D lv, double* y, const double* __restrict__ b,
+                                                      int mode) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= lv.ng) return;
+  const int n = lv.n, S = lv.S;
+  const int beg = lv.grp_ptr[g], end = lv.grp_ptr[g + 1];
+  auto copy = [&](int q) {
+    int i, j, k;
+    unpack_ijk(lv.mem_ijk[q], i, j, k);
+    return static_cast<size_t>(lv.mem_slot[q]) * S + lat3(n, i, j, k);
+  };
+  double v;
+  if (end - beg == 1) {
+    v = y[copy(beg)];
+  } else {
+    v = 0.0;
+    for (int q = beg; q < end; ++q) {
+      const int s = lv.mem_slot[q];
+      v += s < 0 ? lv.ghost[~s] : y[copy(q)];
+    }
+  }
+  const bool dom = lv.grp_domain[g];
+  for (int q = beg; q < end; ++q) {
+    if (lv.mem_slot[q] < 0) continue;
+    const size_t off = copy(q);
     if (mode == A3_PLAIN)
       y[off] = v;
     else if (mode == A3_RESIDUAL)
@@ -984,6 +1195,159 @@ __global__ void __launch_bounds__(kT) k3_estimate_nodes(DevLevel3D lv, const dou
   }
 }
 
+// Streaming form of k3_estimate_nodes (levels n >= 8): one CTA per macro
+// walks its k-planes once; e_b = uL - wb and e_c = uL - wc of plane k + 2 are
+// loaded (coalesced, issued before the plane-k work so their latency hides
+// behind it) and stored into 3-slot shared-memory rings; plane k's nodes take
+// their mass rows (interior stencil / boundary partial stencil) from the rings.
+// Each of uL, wb, wc is read once.  Writes the macro's two sums directly.
+constexpr int kEsThreads = 256;
+constexpr int kEsPer = 9;  // plane nodes per thread (n <= 64: <= 2145 nodes)
+
+__global__ void __launch_bounds__(kEsThreads, 2) k3_estimate_stream(DevLevel3D lv, const double* __restrict__ uL,
+                                                                    const double* __restrict__ wb,
+                                                                    const double* __restrict__ wc, double* sums) {
+  extern __shared__ __align__(128) unsigned long long es_smem[];
+  const int n = lv.n, S = lv.S, m = blockIdx.x, tid = threadIdx.x;
+  const int stride = plane_stride(n);
+  double* ps = reinterpret_cast<double*>(es_smem);  // 16 signatures x 15
+  double* rb = ps + 240;                             // e_b ring, 3 slots
+  double* rc = rb + 3 * stride;                      // e_c ring, 3 slots
+  const size_t mo = static_cast<size_t>(m) * S;
+  for (int t = tid; t < 240; t += kEsThreads) ps[t] = __ldg(lv.psM + 240 * static_cast<size_t>(m) + t);
+  double s[15];
+#pragma unroll
+  for (int d = 0; d < 15; ++d) s[d] = __ldg(lv.stM + 15 * static_cast<size_t>(m) + d);
+  double lu[kEsPer], lb[kEsPer], lc[kEsPer];
+  auto load = [&](int k) {  // plane k of uL, wb, wc into registers
+    if (k > n) return;
+    const size_t o = mo + plane_base(n, k);
+    const int len = (n - k + 1) * (n - k + 2) / 2;
+#pragma unroll
+    for (int t = 0; t < kEsPer; ++t) {
+      const int q = tid + t * kEsThreads;
+      if (q < len) {
+        lu[t] = __ldg(uL + o + q);
+        lb[t] = __ldg(wb + o + q);
+        lc[t] = __ldg(wc + o + q);
+      }
+    }
+  };
+  auto store = [&](int k) {  // e of plane k into its ring slot
+    if (k > n) return;
+    const int len = (n - k + 1) * (n - k + 2) / 2, sl = (k % 3) * stride;
+#pragma unroll
+    for (int t = 0; t < kEsPer; ++t) {
+      const int q = tid + t * kEsThreads;
+      if (q < len) {
+        rb[sl + q] = lu[t] - lb[t];
+        rc[sl + q] = lu[t] - lc[t];
+      }
+    }
+  };
+  load(0);
+  store(0);
+  load(1);
+  store(1);
+  __syncthreads();
+  double qb = 0.0, qc = 0.0;
+  for (int k = 0; k <= n; ++k) {
+    load(k + 2);
+    const int m2 = n - k;
+    int base[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) base[d] = (((k - 1 + d) % 3 + 3) % 3) * stride;
+    if (k >= 1 && m2 >= 3) {
+      const int mi = m2 - 3, ni = (mi + 1) * (mi + 2) / 2;
+      for (int e = tid; e < ni; e += kEsThreads) {
+        int i, j;
+        decode2_fast(mi, e, i, j);
+        ++i, ++j;
+        const int r0 = lat2(m2, 0, j);
+        int ra[7];
+        ra[0] = base[1] + r0;
+        ra[1] = ra[0] + (m2 + 1 - j);
+        ra[2] = ra[0] - (m2 + 2 - j);
+        ra[5] = base[2] + r0 - j;
+        ra[3] = ra[5] - (m2 + 1 - j);
+        ra[6] = base[0] + r0 + j;
+        ra[4] = ra[6] + (m2 + 2 - j);
+        const double eb0 = rb[ra[0] + i], ec0 = rc[ra[0] + i];
+        double mb = s[0] * eb0, mc = s[0] * ec0;
+#pragma unroll
+        for (int d = 1; d < 15; ++d) {
+          const int a = ra[dir_row(d)] + i + dir_di(d);
+          mb = mb + s[d] * rb[a];
+          mc = mc + s[d] * rc[a];
+        }
+        qb = qb + eb0 * mb;
+        qc = qc + ec0 * mc;
+      }
+    }
+    const int nb = k == 0 ? (m2 + 1) * (m2 + 2) / 2 : (m2 >= 1 ? 3 * m2 : 1);
+    for (int e = tid; e < nb; e += kEsThreads) {
+      int i, j;
+      if (k == 0) {
+        decode2_fast(m2, e, i, j);
+      } else if (m2 == 0) {
+        i = 0, j = 0;
+      } else if (e < m2 + 1) {
+        i = e, j = 0;
+      } else if (e < 2 * m2) {
+        i = 0, j = e - m2;
+      } else {
+        j = e - 2 * m2 + 1, i = m2 - j;
+      }
+      const double* cf = ps + 15 * sig3(n, i, j, k);
+      int ra[7], len[7];
+#pragma unroll
+      for (int r = 0; r < 7; ++r) {
+        const int kk = k + row_dk(r), jj = j + row_dj(r), mm = n - kk;
+        const bool rv = kk >= 0 && kk <= n && jj >= 0 && jj <= mm;
+        ra[r] = rv ? base[1 + row_dk(r)] + lat2(mm, 0, jj) : base[1];
+        len[r] = rv ? mm - jj : -1;
+      }
+      const int c0 = ra[0] + i;
+      const double eb0 = rb[c0], ec0 = rc[c0];
+      double mb = cf[0] * eb0, mc = cf[0] * ec0;
+#pragma unroll
+      for (int d = 1; d < 15; ++d) {
+        const int r = dir_row(d), ii = i + dir_di(d);
+        const bool ok = ii >= 0 && ii <= len[r];
+        const int a = ok ? ra[r] + ii : c0;
+        const double tb = mb + cf[d] * rb[a], tc = mc + cf[d] * rc[a];
+        mb = ok ? tb : mb;
+        mc = ok ? tc : mc;
+      }
+      qb = qb + eb0 * mb;
+      qc = qc + ec0 * mc;
+    }
+    __syncthreads();  // plane k - 1's slot is free
+    store(k + 2);
+    __syncthreads();
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    qb += __shfl_xor_sync(0xffffffffu, qb, o);
+    qc += __shfl_xor_sync(0xffffffffu, qc, o);
+  }
+  __shared__ double wsum[2][kEsThreads / 32];
+  if ((tid & 31) == 0) {
+    wsum[0][tid >> 5] = qb;
+    wsum[1][tid >> 5] = qc;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double sb = 0.0, sc = 0.0;
+    for (int w = 0; w < kEsThreads / 32; ++w) {
+      sb += wsum[0][w];
+      sc += wsum[1][w];
+    }
+    sums[2 * m] = sb;
+    sums[2 * m + 1] = sc;
+  }
+}
+
 __global__ void k3_estimate_reduce(int M, int planes, const double* part, double* sums) {
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= M) return;
@@ -1127,6 +1491,24 @@ int gs_phases() {
   return v;
 }
 
+// streaming apply / estimator for levels with 8 <= n <= 64 (KB_APPLY3_STREAM=0: plane-block kernels)
+bool apply_streams(const DevLevel3D& lv) {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("KB_APPLY3_STREAM");
+    v = e ? atoi(e) : 1;
+  }
+  return v && lv.n >= 8 && lv.n <= 64 && lv.M > 0;
+}
+bool estimate_cells() {
+  static int cells = -1;
+  if (cells < 0) {
+    const char* e = getenv("KB_EST3_CELLS");  // measurement: the cell-by-cell form
+    cells = e && e[0] == '1';
+  }
+  return cells == 1;
+}
+
 int blocks_for(long long count) { return static_cast<int>(std::max(1ll, (count + kT - 1) / kT)); }
 
 }  // namespace
@@ -1134,6 +1516,22 @@ int blocks_for(long long count) { return static_cast<int>(std::max(1ll, (count +
 void launch3_apply(const DevLevel3D& lv, bool mass, const double* x, double* y, const double* b, int mode,
                    cudaStream_t st) {
   init_constants();
+  if (apply_streams(lv)) {
+    const size_t smem = (kAsSlots + 240 + kAsSlots * static_cast<size_t>(plane_stride(lv.n))) * 8;
+    static size_t smem_set = 0;  // only ever grows (graph nodes captured earlier stay launchable)
+    if (smem > smem_set) {
+      KB_CUDA_CHECK(cudaFuncSetAttribute(k3_apply_stream, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem)));
+      smem_set = smem;
+    }
+    k3_apply_stream<<<lv.M, kAsThreads, smem, st>>>(lv, mass ? 1 : 0, x, y, b, mode);
+    check3("k3_apply_stream");
+    if (lv.ng > 0) {
+      k3_apply_groups<<<blocks_for(lv.ng), kT, 0, st>>>(lv, y, b, mode);
+      check3("k3_apply_groups");
+    }
+    return;
+  }
   const int planes = lv.M * (lv.n + 1);
   k3_apply<<<planes + blocks_for(lv.ng), kT, 0, st>>>(lv, mass ? 1 : 0, x, y, b, mode, planes);
   check3("k3_apply");
@@ -1188,6 +1586,9 @@ void launch3_gs(const DevLevel3D& lv, double* u, const double* b, int sweeps, cu
     }
   }
 }
+
+int launch3_apply_count(const DevLevel3D& lv) { return apply_streams(lv) ? 1 + (lv.ng > 0) : 1; }
+int launch3_estimate_count(const DevLevel3D& lv) { return !estimate_cells() && apply_streams(lv) ? 1 : 2; }
 
 int launch3_gs_count(const DevLevel3D& lv, int sweeps) {
   if (sweeps <= 0) return 0;
@@ -1261,10 +1662,18 @@ void launch3_cg0(const DevLevel3D& lv0, double* u, const double* b, double* scra
 void launch3_estimate(const DevLevel3D& lv, const double* uL, const double* wb, const double* wc, double* sums,
                       double* part, cudaStream_t st) {
   init_constants();
-  static int cells = -1;
-  if (cells < 0) {
-    const char* e = getenv("KB_EST3_CELLS");  // measurement: the cell-by-cell form
-    cells = e && e[0] == '1';
+  const bool cells = estimate_cells();
+  if (!cells && apply_streams(lv)) {
+    const size_t smem = (240 + 6 * static_cast<size_t>(plane_stride(lv.n))) * 8;
+    static size_t smem_set = 0;  // only ever grows (graph nodes captured earlier stay launchable)
+    if (smem > smem_set) {
+      KB_CUDA_CHECK(cudaFuncSetAttribute(k3_estimate_stream, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem)));
+      smem_set = smem;
+    }
+    k3_estimate_stream<<<lv.M, kEsThreads, smem, st>>>(lv, uL, wb, wc, sums);
+    check3("k3_estimate_stream");
+    return;
   }
   if (cells)
     k3_estimate<<<lv.M * (lv.n + 1), kT, 0, st>>>(lv, uL, wb, wc, part);

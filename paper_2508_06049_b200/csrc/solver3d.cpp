@@ -469,7 +469,7 @@ void Solver3D::vcycle(int l, double* u, const double* b) {
     mark(KK_GS, 24.0 * cfg_.pre_smooth * dofs(l), launch3_gs_count(lev[l], cfg_.pre_smooth));
   }
   launch3_apply(lev[l], false, u, r_[l], b, A3_RES_OWNER, stream_);
-  mark(KK_RESIDUAL, 24.0 * dofs(l));
+  mark(KK_RESIDUAL, 24.0 * dofs(l), launch3_apply_count(lev[l]));
   launch3_restrict(lev[l], lev[l - 1], r_[l], vb_[l - 1], 1, stream_);
   mark(KK_RESTRICT, 8.0 * dofs(l) + 8.0 * dofs(l - 1), 2);
   KB_CUDA_CHECK(cudaMemsetAsync(vu_[l - 1], 0, level_size(l - 1) * 8, stream_));
@@ -494,7 +494,7 @@ void Solver3D::enqueue_fmg_body() {
     if (has_source_) {
       launch3_apply(lev[l], true, ftab_[l], b_[l], nullptr, A3_PLAIN, stream_);
       launch3_set_boundary(lev[l], b_[l], gbnd_[l], 0, stream_);
-      mark(KK_RHS, 16.0 * dofs(l), 2);
+      mark(KK_RHS, 16.0 * dofs(l), 1 + launch3_apply_count(lev[l]));
     } else {
       launch3_set_boundary(lev[l], b_[l], gbnd_[l], 1, stream_);
       mark(KK_RHS, 8.0 * dofs(l), 1);
@@ -581,7 +581,7 @@ void Solver3D::estimate_enqueue(int offset) {
   const double* wb = lift(w_[base], base + 1, est_a_);
   const double* wc = lift(w_[base - 1], base, est_b_);
   launch3_estimate(lev[L_], u_[L_], wb, wc, est_sums_, est_c_, stream_);  // est_c_: per-plane partials
-  mark(KK_ESTIMATE, 24.0 * dofs(L_));
+  mark(KK_ESTIMATE, 24.0 * dofs(L_), launch3_estimate_count(lev[L_]));
   KB_CUDA_CHECK(cudaMemcpyAsync(sums_host_, est_sums_, 2 * H_->host.M * sizeof(double), cudaMemcpyDeviceToHost,
                                 stream_));
   probes_ = nullptr;

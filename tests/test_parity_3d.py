@@ -136,3 +136,22 @@ def test_fmg_device_source_close_to_faithful():
     a = K.MultigridSolver(h, K.Problem(K.PROBLEM_SIN3D), K.SolverConfig(nu=2, faithful_source=1)).fmg().u(4)
     b = K.MultigridSolver(h, K.Problem(K.PROBLEM_SIN3D), K.SolverConfig(nu=2, faithful_source=0)).fmg().u(4)
     assert np.max(np.abs(a - b)) <= 1e-9 * np.max(np.abs(a))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,L", [("kuhn1", 5), ("kuhn1", 6), ("perturbed", 5)])
+def test_gauss_seidel_large_levels_bitwise(name, L):
+    """The plane-pipelined interior phase (levels with 16 <= n <= 64) against the
+    oracle's colour-by-colour sweep: two calls of two sweeps, bit for bit."""
+    mesh = kuhn_cube(1) if name == "kuhn1" else _perturbed_kuhn()
+    o = O.Hier3D(mesh.coords, mesh.elements, L)
+    h = K.GridHierarchy.build(mesh, L)
+    s = K.MultigridSolver(h, K.Problem(K.PROBLEM_ZERO), K.SolverConfig(nu=2))
+    X = o.coords(L)
+    x, bb = _smooth(X, 31), _smooth(X, 32)
+    gu, gb = K.GridFunction(h, L, x), K.GridFunction(h, L, bb)
+    ref = x
+    for _ in range(2):
+        s.gauss_seidel(gu, gb, 2)
+        ref = o.gauss_seidel(L, ref, bb, 2)
+        assert np.array_equal(gu.numpy(), ref)
