@@ -386,7 +386,9 @@ __global__ void __launch_bounds__(kAsThreads) k3_apply_stream(DevLevel3D lv, int
     }
     // lattice-boundary nodes of the plane: partial rows (raw)
     const int nb = k == 0 ? (m2 + 1) * (m2 + 2) / 2 : (m2 >= 1 ? 3 * m2 : 1);
-    for (int e = tid; e < nb; e += kAsThreads) {
+    // boundary nodes continue the interior's thread rotation (balanced per plane)
+    const int ni_all = k >= 1 && m2 >= 3 ? (m2 - 2) * (m2 - 1) / 2 : 0;
+    for (int e = (tid - ni_all % kAsThreads + kAsThreads) % kAsThreads; e < nb; e += kAsThreads) {
       int i, j;
       if (k == 0) {
         decode2(m2, e, i, j);
@@ -1334,7 +1336,9 @@ __global__ void __launch_bounds__(kEsThreads, 2) k3_estimate_stream(DevLevel3D l
       }
     }
     const int nb = k == 0 ? (m2 + 1) * (m2 + 2) / 2 : (m2 >= 1 ? 3 * m2 : 1);
-    for (int e = tid; e < nb; e += kEsThreads) {
+    // boundary nodes continue the interior's thread rotation (balanced per plane)
+    const int ni_all = k >= 1 && m2 >= 3 ? (m2 - 2) * (m2 - 1) / 2 : 0;
+    for (int e = (tid - ni_all % kEsThreads + kEsThreads) % kEsThreads; e < nb; e += kEsThreads) {
       int i, j;
       if (k == 0) {
         decode2_fast(m2, e, i, j);
