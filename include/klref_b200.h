@@ -231,6 +231,21 @@ int klref_interface_sync(klref_solver s, klref_gf f, int mode);               /*
 int klref_mark(int rule, double fraction, int num_active, const int* active_ids, const int* green_parent,
                const double* indicator, int num_reverted, const int* reverted_ids, int* marks_out, int* num_marks);
 
+/* ---- effectivity constants and indices (host) -------------------------- */
+/* effectivity_constants, local_spread_bound_scaled / _unscaled and
+ * effectivity_index, proj/include/klref/estimator.hpp:27-68,
+ * proj/src/estimator.cpp:47-123.  Domain violations return KLREF_ERR_DOMAIN
+ * (the reference throws DomainError).  effectivity_index: gamma = eta /
+ * exact_global (gamma_valid = exact_global > 0), gamma_local[num_local] = NaN
+ * where the macro's exact error is <= 1e-14 of the global one, spread =
+ * max / min of the valid local indices. */
+int klref_effectivity_constants(double theta, double eps, int offset, double* lower, double* upper);
+int klref_local_spread_bound_scaled(double theta_max, double eps, int offset, double* out);
+int klref_local_spread_bound_unscaled(double theta_min, double theta_max, int offset, double* out);
+int klref_effectivity_index(double eta, int num_local, const double* eta_local, double exact_global,
+                            int num_exact, const double* exact_local, double* gamma, int* gamma_valid,
+                            double* gamma_local, double* spread, int* spread_valid);
+
 /* ---- sharded 3-d solve (no reference counterpart) ------
  * The reference is single-process.  Its paper partitions macro
  * elements with ghost layers on the interface primitives;

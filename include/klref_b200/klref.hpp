@@ -24,6 +24,7 @@
 #define KLREF_B200_KLREF_HPP
 
 #include <array>
+#include <cmath>
 #include <cstdint>
 #include <functional>
 #include <memory>
@@ -518,6 +519,78 @@ inline ErrorNorms exact_error_norm(const FmgState& state) {
   ErrorNorms out;
   out.per_macro.assign(static_cast<std::size_t>(state.h->num_macros()), 0.0);
   detail::check(klref_solver_exact_error(EstimateAccess::solver(state), &out.global, out.per_macro.data()));
+  return out;
+}
+
+// ---------------------------------------------------------------- estimator.hpp: effectivity
+// proj/include/klref/estimator.hpp:27-68 (host formulas, C-ABI klref_effectivity_*)
+struct EquivalenceConstants {
+  double lower = 0.0;  // C1
+  double upper = 0.0;  // C2
+};
+inline EquivalenceConstants effectivity_constants(double theta, double eps, int offset) {
+  EquivalenceConstants c;
+  detail::check(klref_effectivity_constants(theta, eps, offset, &c.lower, &c.upper));
+  return c;
+}
+inline double local_spread_bound_scaled(double theta_max, double eps, int offset) {
+  double v = 0.0;
+  detail::check(klref_local_spread_bound_scaled(theta_max, eps, offset, &v));
+  return v;
+}
+inline double local_spread_bound_unscaled(double theta_min, double theta_max, int offset) {
+  double v = 0.0;
+  detail::check(klref_local_spread_bound_unscaled(theta_min, theta_max, offset, &v));
+  return v;
+}
+struct BoundsConstants {
+  double theta = 0.25;
+  double eps = 0.0;
+  int offset = 1;
+  int order = 2;
+  double theta_eps = 0.25;
+  EquivalenceConstants equivalence;
+  double theta_min = 0.25;
+  double theta_max = 0.25;
+  double spread_scaled = 0.0;
+  double spread_unscaled = 0.0;
+};
+inline BoundsConstants make_bounds(double theta, double eps, int offset) {
+  BoundsConstants b;
+  b.theta = theta;
+  b.eps = eps;
+  b.offset = offset;
+  b.order = static_cast<int>(std::lround(-std::log2(theta)));
+  b.theta_eps = (1.0 + eps) * theta;
+  b.equivalence = effectivity_constants(theta, eps, offset);
+  b.theta_min = theta;
+  b.theta_max = theta;
+  b.spread_scaled = local_spread_bound_scaled(theta, eps, offset);
+  b.spread_unscaled = local_spread_bound_unscaled(theta, theta, offset);
+  return b;
+}
+inline BoundsConstants make_bounds_from_order(int order, double eps, int offset) {
+  BoundsConstants b = make_bounds(std::pow(2.0, -static_cast<double>(order)), eps, offset);
+  b.order = order;
+  return b;
+}
+struct EffectivityReport {
+  double gamma = 0.0;
+  bool gamma_valid = false;
+  std::vector<double> gamma_local;
+  double spread = 0.0;
+  bool spread_valid = false;
+};
+inline EffectivityReport effectivity_index(const EstimateReport& report, const ErrorNorms& exact) {
+  EffectivityReport out;
+  out.gamma_local.assign(report.eta_local.size(), 0.0);
+  int gv = 0, sv = 0;
+  detail::check(klref_effectivity_index(report.eta, static_cast<int>(report.eta_local.size()), report.eta_local.data(),
+                                        exact.global, static_cast<int>(exact.per_macro.size()),
+                                        exact.per_macro.data(), &out.gamma, &gv, out.gamma_local.data(),
+                                        &out.spread, &sv));
+  out.gamma_valid = gv != 0;
+  out.spread_valid = sv != 0;
   return out;
 }
 

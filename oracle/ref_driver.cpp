@@ -19,6 +19,10 @@
 //   ref_driver ops   <mesh> <L> <seed> <outdir>
 //   ref_driver time  <mesh> <sin|lshape> <L> <nu> <reps> [budget_s]
 //   ref_driver solvevtd <mesh> <sin|lshape> <L> <nu> <outdir>   (FinestPolicy::ValidationTwoDigits)
+//   ref_driver bounds      (stdin: "theta eps offset" lines -> effectivity_constants,
+//                          local spread bounds, make_bounds order; "ERR" on DomainError)
+//   ref_driver effidx <file>  (eta, n, eta_local[n], exact global, m, exact per_macro[m]
+//                          -> effectivity_index: gamma valid spread valid gamma_local...)
 //   ref_driver amr3d <L> <nu> <K> <outdir>
 //       BASELINE.json config 4: the unit cube as 6 Kuhn tetrahedra, K steps of
 //       (3-d estimate -> marks >= 0.5 max on the green-reverted set ->
@@ -558,6 +562,43 @@ int cmd_timeall(int argc, char** argv) {
   return 0;
 }
 
+// effectivity constants / spread bounds (proj/src/estimator.cpp:47-99) for
+// the (theta, eps, offset) triples on stdin
+int cmd_bounds() {
+  double theta = 0.0, eps = 0.0;
+  int offset = 0;
+  while (std::scanf("%lf %lf %d", &theta, &eps, &offset) == 3) {
+    try {
+      const BoundsConstants b = make_bounds(theta, eps, offset);
+      std::printf("%.17g %.17g %.17g %.17g %d\n", b.equivalence.lower, b.equivalence.upper, b.spread_scaled,
+                  b.spread_unscaled, b.order);
+    } catch (const DomainError&) {
+      std::printf("ERR\n");
+    }
+  }
+  return 0;
+}
+
+// effectivity_index (proj/src/estimator.cpp:100-123) of the report in <file>
+int cmd_effidx(int argc, char** argv) {
+  if (argc < 3) return 2;
+  std::ifstream in(argv[2]);
+  EstimateReport r;
+  ErrorNorms ex;
+  int n = 0, m = 0;
+  in >> r.eta >> n;
+  r.eta_local.resize(n);
+  for (auto& v : r.eta_local) in >> v;
+  in >> ex.global >> m;
+  ex.per_macro.resize(m);
+  for (auto& v : ex.per_macro) in >> v;
+  const EffectivityReport e = effectivity_index(r, ex);
+  std::printf("%.17g %d %.17g %d", e.gamma, e.gamma_valid ? 1 : 0, e.spread, e.spread_valid ? 1 : 0);
+  for (double g : e.gamma_local) std::printf(" %.17g", g);
+  std::printf("\n");
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -581,6 +622,8 @@ int main(int argc, char** argv) {
     if (cmd == "solvevtd") return cmd_solvevtd(argc, argv);
     if (cmd == "time") return cmd_time(argc, argv);
     if (cmd == "timeall") return cmd_timeall(argc, argv);
+    if (cmd == "bounds") return cmd_bounds();
+    if (cmd == "effidx") return cmd_effidx(argc, argv);
   } catch (const std::exception& e) {
     std::fprintf(stderr, "ref_driver: %s\n", e.what());
     return 1;

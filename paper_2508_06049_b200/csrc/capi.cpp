@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <limits>
 #include <map>
 #include <memory>
 #include <new>
@@ -627,6 +628,83 @@ int klref_interface_sync(klref_solver s, klref_gf f, int mode) {
     need(s, "solver");
     same_hier(s, f);
     on_solver(s, [&](auto& v) { v.interface_sync(f->level, f->d, mode == KLREF_SYNC_ADDITIVE); });
+  });
+}
+
+// ---- effectivity constants and indices (host, O(1) / O(M)) -------------
+// proj/src/estimator.cpp:47-123: the equivalence constants C1, C2 of the
+// error bound, the local spread bounds, and the validation-mode effectivity
+// indices against the exact error.
+int klref_effectivity_constants(double theta, double eps, int offset, double* lower, double* upper) {
+  return guarded([&] {
+    need(lower, "lower");
+    need(upper, "upper");
+    const double theta_eps = (1.0 + eps) * theta;
+    if (!(theta > 0.0) || eps < 0.0 || offset < 1)
+      kb::fail(kb::KB_DOMAIN, "effectivity constants need theta > 0, eps >= 0, offset >= 1");
+    if (theta_eps >= 1.0) kb::fail(kb::KB_DOMAIN, "saturation requires (1 + eps) * theta < 1");
+    const double j = static_cast<double>(offset);
+    *lower = std::pow(1.0 + eps, -j) * std::pow(1.0 - std::pow(theta_eps, j), j + 1.0) /
+             std::pow(1.0 + std::pow(theta_eps, j + 1.0), j);
+    *upper = std::pow(1.0 + eps, j) * std::pow(1.0 + std::pow(theta_eps, j), j + 1.0) /
+             std::pow(1.0 - std::pow(theta_eps, j + 1.0), j);
+  });
+}
+
+int klref_local_spread_bound_scaled(double theta_max, double eps, int offset, double* out) {
+  return guarded([&] {
+    need(out, "out");
+    if (!(theta_max > 0.0) || eps < 0.0 || offset < 1 || (1.0 + eps) * theta_max >= 1.0)
+      kb::fail(kb::KB_DOMAIN, "spread bound requires (1 + eps) * theta_max < 1");
+    const double j = static_cast<double>(offset);
+    const double tj = std::pow(theta_max, j), tj1 = std::pow(theta_max, j + 1.0);
+    *out = std::pow(1.0 + eps, 2.0 * j) * std::pow((1.0 + tj1) / (1.0 - tj1), j) *
+           std::pow((1.0 + tj) / (1.0 - tj), j + 1.0);
+  });
+}
+
+int klref_local_spread_bound_unscaled(double theta_min, double theta_max, int offset, double* out) {
+  return guarded([&] {
+    need(out, "out");
+    if (!(theta_min > 0.0) || theta_min > theta_max || offset < 1)
+      kb::fail(kb::KB_DOMAIN, "spread bound requires 0 < theta_min <= theta_max");
+    if (theta_max >= 1.0) kb::fail(kb::KB_DOMAIN, "spread bound requires theta_max < 1");
+    const double j = static_cast<double>(offset);
+    *out = (std::pow(theta_min, -j) + 1.0) / (std::pow(theta_max, -j) - 1.0);
+  });
+}
+
+int klref_effectivity_index(double eta, int num_local, const double* eta_local, double exact_global,
+                            int num_exact, const double* exact_local, double* gamma, int* gamma_valid,
+                            double* gamma_local, double* spread, int* spread_valid) {
+  return guarded([&] {
+    need(gamma, "gamma");
+    need(gamma_valid, "gamma_valid");
+    need(spread, "spread");
+    need(spread_valid, "spread_valid");
+    if (num_local > 0) {
+      need(eta_local, "eta_local");
+      need(gamma_local, "gamma_local");
+    }
+    if (num_exact > 0) need(exact_local, "exact_local");
+    const double nan = std::numeric_limits<double>::quiet_NaN();
+    *gamma_valid = exact_global > 0.0;
+    *gamma = *gamma_valid ? eta / exact_global : nan;
+    double lo = std::numeric_limits<double>::infinity(), hi = 0.0;
+    bool any = false;
+    const double cutoff = 1e-14 * exact_global;
+    for (int t = 0; t < num_local; ++t) {
+      gamma_local[t] = nan;
+      if (t >= num_exact) continue;
+      if (exact_local[t] <= cutoff || exact_local[t] == 0.0) continue;
+      const double g = eta_local[t] / exact_local[t];
+      gamma_local[t] = g;
+      lo = std::min(lo, g);
+      hi = std::max(hi, g);
+      any = true;
+    }
+    *spread_valid = any && lo > 0.0;
+    *spread = *spread_valid ? hi / lo : nan;
   });
 }
 

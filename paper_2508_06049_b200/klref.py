@@ -12,6 +12,7 @@ there is no CPU fallback (a missing library or device raises).
 from __future__ import annotations
 
 import ctypes as C
+import math
 import os
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
@@ -160,6 +161,10 @@ SIGNATURES = {
     "klref_dot_unique": (_I, [_P, _P, _P, _PD]),
     "klref_interface_sync": (_I, [_P, _P, _I]),
     "klref_mark": (_I, [_I, _D, _I, _PI, _PI, _PD, _I, _PI, _PI, _PI]),
+    "klref_effectivity_constants": (_I, [_D, _D, _I, _PD, _PD]),
+    "klref_local_spread_bound_scaled": (_I, [_D, _D, _I, _PD]),
+    "klref_local_spread_bound_unscaled": (_I, [_D, _D, _I, _PD]),
+    "klref_effectivity_index": (_I, [_D, _I, _PD, _D, _I, _PD, _PD, _PI, _PD, _PD, _PI]),
     "klref_comm_unique_id": (_I, [C.c_char_p]),
     "klref_comm_create": (_I, [_I, _I, C.c_char_p, _PP]),
     "klref_comm_destroy": (None, [_P]),
@@ -701,6 +706,95 @@ class FmgState:
 def error_estimate(state: FmgState, offset: int = 1, kind: int = UNSCALED) -> EstimateReport:
     """error_estimate(state, j, kind), proj/include/klref/estimator.hpp:26."""
     return state.solver.error_estimate(offset, kind)
+
+
+# ---------------------------------------------------------------- effectivity (estimator.hpp:27-68)
+@dataclass
+class EquivalenceConstants:
+    """EquivalenceConstants, proj/include/klref/estimator.hpp:27-31: lower * ||e|| <= eta_j <= upper * ||e||."""
+    lower: float = 0.0
+    upper: float = 0.0
+
+
+@dataclass
+class BoundsConstants:
+    """BoundsConstants, proj/include/klref/estimator.hpp:40-51."""
+    theta: float = 0.25
+    eps: float = 0.0
+    offset: int = 1
+    order: int = 2
+    theta_eps: float = 0.25
+    equivalence: EquivalenceConstants = field(default_factory=EquivalenceConstants)
+    theta_min: float = 0.25
+    theta_max: float = 0.25
+    spread_scaled: float = 0.0
+    spread_unscaled: float = 0.0
+
+
+@dataclass
+class EffectivityReport:
+    """EffectivityReport, proj/include/klref/estimator.hpp:56-62."""
+    gamma: float = 0.0
+    gamma_valid: bool = False
+    gamma_local: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    spread: float = 0.0
+    spread_valid: bool = False
+
+
+def effectivity_constants(theta: float, eps: float, offset: int) -> EquivalenceConstants:
+    """effectivity_constants, proj/src/estimator.cpp:47-60 (DomainError outside its range)."""
+    lo, up = C.c_double(), C.c_double()
+    _check(lib().klref_effectivity_constants(theta, eps, offset, C.byref(lo), C.byref(up)))
+    return EquivalenceConstants(lo.value, up.value)
+
+
+def local_spread_bound_scaled(theta_max: float, eps: float, offset: int) -> float:
+    """local_spread_bound_scaled, proj/src/estimator.cpp:62-71."""
+    v = C.c_double()
+    _check(lib().klref_local_spread_bound_scaled(theta_max, eps, offset, C.byref(v)))
+    return v.value
+
+
+def local_spread_bound_unscaled(theta_min: float, theta_max: float, offset: int) -> float:
+    """local_spread_bound_unscaled, proj/src/estimator.cpp:73-79."""
+    v = C.c_double()
+    _check(lib().klref_local_spread_bound_unscaled(theta_min, theta_max, offset, C.byref(v)))
+    return v.value
+
+
+def make_bounds(theta: float, eps: float, offset: int) -> BoundsConstants:
+    """make_bounds, proj/src/estimator.cpp:81-93."""
+    b = BoundsConstants(theta=theta, eps=eps, offset=offset)
+    x = -math.log2(theta) if theta > 0.0 else math.inf
+    # std::lround (half away from zero); a non-finite argument is left to effectivity_constants' DomainError
+    b.order = int(math.copysign(math.floor(abs(x) + 0.5), x)) if math.isfinite(x) else 0
+    b.theta_eps = (1.0 + eps) * theta
+    b.equivalence = effectivity_constants(theta, eps, offset)
+    b.theta_min = b.theta_max = theta
+    b.spread_scaled = local_spread_bound_scaled(theta, eps, offset)
+    b.spread_unscaled = local_spread_bound_unscaled(theta, theta, offset)
+    return b
+
+
+def make_bounds_from_order(order: int, eps: float, offset: int) -> BoundsConstants:
+    """make_bounds_from_order, proj/src/estimator.cpp:95-99 (theta = 2^-q)."""
+    b = make_bounds(2.0 ** (-float(order)), eps, offset)
+    b.order = order
+    return b
+
+
+def effectivity_index(report: EstimateReport, exact) -> EffectivityReport:
+    """effectivity_index(report, exact), proj/src/estimator.cpp:100-123; exact = (global, per_macro)
+    as returned by MultigridSolver.exact_error()."""
+    eg, el = exact
+    loc = np.ascontiguousarray(report.eta_local, dtype=np.float64)
+    ex = np.ascontiguousarray(el, dtype=np.float64)
+    gl = np.zeros(loc.size)
+    g, sp = C.c_double(), C.c_double()
+    gv, sv = C.c_int(), C.c_int()
+    _check(lib().klref_effectivity_index(report.eta, loc.size, _dptr(loc), float(eg), ex.size, _dptr(ex), C.byref(g),
+                                         C.byref(gv), _dptr(gl), C.byref(sp), C.byref(sv)))
+    return EffectivityReport(g.value, bool(gv.value), gl, sp.value, bool(sv.value))
 
 
 def mark(rule: int, fraction: float, active_ids: Sequence[int], green_parent: Sequence[int],

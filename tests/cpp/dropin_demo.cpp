@@ -101,6 +101,10 @@ int main(int argc, char** argv) {
     klref::MultigridSolver solver(h, p, cfg);
     klref::FmgState st = solver.fmg();
     const klref::EstimateReport er = klref::error_estimate(st, 1, klref::EstimatorKind::Unscaled);
+    // validation rows of run_kl, proj/src/amr.cpp:202-204: exact error and effectivity
+    const klref::ErrorNorms exact = klref::exact_error_norm(st);
+    const klref::EffectivityReport eff = klref::effectivity_index(er, exact);
+    const klref::BoundsConstants bounds = klref::make_bounds_from_order(2, 0.0, 1);
     const klref::GridFunction uL = st.u.back();
     const std::vector<double> flat = uL.flat();
     std::FILE* f = std::fopen(argv[5], "wb");
@@ -108,8 +112,10 @@ int main(int argc, char** argv) {
     std::fwrite(flat.data(), sizeof(double), flat.size(), f);
     std::fclose(f);
     std::printf("{\"dofs\": %lld, \"eta\": %.17g, \"norm_base\": %.17g, \"norm_coarser\": %.17g, \"conv\": %.17g, "
+                "\"exact\": %.17g, \"gamma\": %.17g, \"spread\": %.17g, \"c1\": %.17g, \"c2\": %.17g, "
                 "\"eta_local\": [",
-                static_cast<long long>(h->dof_count(L)), er.eta, er.norm_base, er.norm_coarser, er.conv_factor);
+                static_cast<long long>(h->dof_count(L)), er.eta, er.norm_base, er.norm_coarser, er.conv_factor,
+                exact.global, eff.gamma, eff.spread, bounds.equivalence.lower, bounds.equivalence.upper);
     for (std::size_t s = 0; s < er.eta_local.size(); ++s) std::printf("%s%.17g", s ? ", " : "", er.eta_local[s]);
     std::printf("]}\n");
   } catch (const klref::Error& e) {

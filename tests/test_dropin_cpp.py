@@ -45,5 +45,8 @@ def test_dropin_matches_reference(tmp_path, mesh, prob, L, nu, key):
     nb, nc, th, eta = rec["est_u1"]
     tol = 1e-12 if key == "cfg1" else 1e-9
     assert rel(d["eta"], eta) <= tol and rel(d["norm_base"], nb) <= tol and rel(d["conv"], th) <= tol
+    # effectivity_index / make_bounds through the facade (proj/src/estimator.cpp:47-123)
+    assert d["gamma"] == d["eta"] / d["exact"] and d["spread"] >= 1.0
+    assert round(d["c1"], 2) == 0.53 and round(d["c2"], 2) == 1.67
     ref_loc = np.array(rec["eta_local_u1"])
     assert np.max(np.abs(np.array(d["eta_local"]) - ref_loc) / np.abs(ref_loc)) <= tol
