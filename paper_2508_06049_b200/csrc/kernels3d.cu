@@ -505,47 +505,70 @@ __device__ void gs_group(const DevLevel3D& lv, double* u, const double* __restri
   stamp(tr, 9);
 }
 
-// Relaxation of a narrow group (<= 4 members) by a quad of lanes (levels n <= 16,
-// where the colour phases are latency-bound): lane q of the
-// quad evaluates member q's partial row, every lane forms the member sum in
-// slot order from shuffles (the sequential order of gs_group), the lanes write
-// their own members' copies.  All 32 lanes of the warp call it (valid = false
-// for quads without a group).
-__device__ __forceinline__ void gs_group_quad(const DevLevel3D& lv, double* u, const double* __restrict__ b, int g,
-                                              bool valid, int sub) {
+// Relaxation of a narrow group (<= 4 members) by W lanes (W = 4 on small
+// levels, where the colour phases are latency-bound; W = 2 on large levels,
+// where most narrow groups are 2-member face groups): lane q of the W
+// evaluates the partial rows of members q and q + W, every lane forms the
+// member sum in slot order from shuffles (the sequential order of gs_group),
+// the lanes write their own members' copies.  All 32 lanes of the warp call it
+// (valid = false for lane groups without a group).
+template <int W>
+__device__ __forceinline__ void gs_group_lanes(const DevLevel3D& lv, double* u, const double* __restrict__ b, int g,
+                                               bool valid, int sub) {
+  constexpr int R = 4 / W;  // members per lane
   const int n = lv.n, S = lv.S;
-  int beg = 0, cnt = 0, slot = -1, i = 0, j = 0, k = 0;
-  double part = 0.0;
+  int beg = 0, cnt = 0, slot[R], i[R], j[R], k[R];
+  double part[R];
+  bool dom = false;
   if (valid) {
     beg = lv.grp_ptr[g];
     cnt = lv.grp_ptr[g + 1] - beg;
-    if (sub < cnt) {
-      slot = lv.mem_slot[beg + sub];
-      if (slot < 0) {
-        part = lv.ghost[~slot];
+    dom = lv.grp_domain[g];
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int q = sub + W * r;
+    slot[r] = -1;
+    i[r] = j[r] = k[r] = 0;
+    part[r] = 0.0;
+    if (valid && q < cnt) {
+      slot[r] = lv.mem_slot[beg + q];
+      if (slot[r] < 0) {
+        part[r] = lv.ghost[~slot[r]];
       } else {
-        unpack_ijk(lv.mem_ijk[beg + sub], i, j, k);
-        if (!lv.grp_domain[g])
-          part = partial_off3(lv.psK + 240 * slot, u + static_cast<size_t>(slot) * S, n, i, j, k);
+        unpack_ijk(lv.mem_ijk[beg + q], i[r], j[r], k[r]);
+        if (!dom) part[r] = partial_off3(lv.psK + 240 * slot[r], u + static_cast<size_t>(slot[r]) * S, n, i[r], j[r], k[r]);
       }
     }
   }
-  const int qbase = (threadIdx.x & 31) & ~3;
+  const int qbase = (threadIdx.x & 31) & ~(W - 1);
   double off = 0.0;
 #pragma unroll
   for (int t = 0; t < 4; ++t) {
-    const double v = __shfl_sync(0xffffffffu, part, qbase + t);
+    const double v = __shfl_sync(0xffffffffu, part[t / W], qbase + t % W);
     if (t < cnt) off = off + v;
   }
   // the first member on this shard holds b (b's copies are interface-consistent)
-  const unsigned here = __ballot_sync(0xffffffffu, valid && sub < cnt && slot >= 0);
-  const int first = __ffs((here >> qbase) & 0xFu) - 1;
-  const int src = qbase + (first < 0 ? 0 : first);
-  const double bown = (valid && sub == first) ? b[static_cast<size_t>(slot) * S + lat3(n, i, j, k)] : 0.0;
-  const double bq = __shfl_sync(0xffffffffu, bown, src);
-  if (!valid || sub >= cnt || slot < 0) return;
-  const double val = lv.grp_domain[g] ? bq : (bq - off) / lv.grp_diag[g];
-  u[static_cast<size_t>(slot) * S + lat3(n, i, j, k)] = val;
+  unsigned mine = 0;
+#pragma unroll
+  for (int r = 0; r < R; ++r) mine |= (valid && sub + W * r < cnt && slot[r] >= 0) ? 1u << r : 0u;
+  int first = 4;
+#pragma unroll
+  for (int r = R - 1; r >= 0; --r) {
+    const unsigned here = __ballot_sync(0xffffffffu, (mine >> r) & 1u);
+    const unsigned bits = (here >> qbase) & ((1u << W) - 1u);
+    if (bits) first = min(first, W * r + __ffs(bits) - 1);
+  }
+  double bown = 0.0;
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+    if (valid && sub + W * r == first) bown = b[static_cast<size_t>(slot[r]) * S + lat3(n, i[r], j[r], k[r])];
+  const double bq = __shfl_sync(0xffffffffu, bown, qbase + (first < 4 ? first % W : 0));
+  if (!valid) return;
+  const double val = dom ? bq : (bq - off) / lv.grp_diag[g];
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+    if (sub + W * r < cnt && slot[r] >= 0) u[static_cast<size_t>(slot[r]) * S + lat3(n, i[r], j[r], k[r])] = val;
 }
 
 // boundary phase of colour c: one group per thread
@@ -711,14 +734,21 @@ __global__ void __launch_bounds__(NT, MINB) k3_gs_sweeps(DevLevel3D lv, double* 
       const int p0 = lv.color_grp_ptr[c], p1 = lv.color_grp_ptr[c + 1], pw = lv.color_wide_end[c];
       if (phases & 1) {
         for (int t = p0 + gw; t < pw; t += nw) gs_group_warp(lv, u, b, lv.color_grp[t], lane);
-        if ((phases & 8) || lv.n > 16) {  // large levels (and the trace): one thread per group
+        if (phases & 8) {  // measurement trace: one thread per group
           for (int t = pw + tid; t < p1; t += nthreads)
             gs_group(lv, u, b, lv.color_grp[t],
                      tid == 0 && sw == 0 ? reinterpret_cast<long long*>(g_gs3_trace + 16 + 10 * c) : nullptr);
         } else {
-          for (int t0 = pw + 8 * gw; t0 < p1; t0 += 8 * nw) {
-            const int t = t0 + (lane >> 2);
-            gs_group_quad(lv, u, b, t < p1 ? lv.color_grp[t] : 0, t < p1, lane & 3);
+          if (lv.n <= 16) {
+            for (int t0 = pw + 8 * gw; t0 < p1; t0 += 8 * nw) {
+              const int t = t0 + (lane >> 2);
+              gs_group_lanes<4>(lv, u, b, t < p1 ? lv.color_grp[t] : 0, t < p1, lane & 3);
+            }
+          } else {
+            for (int t0 = pw + 16 * gw; t0 < p1; t0 += 16 * nw) {
+              const int t = t0 + (lane >> 1);
+              gs_group_lanes<2>(lv, u, b, t < p1 ? lv.color_grp[t] : 0, t < p1, lane & 1);
+            }
           }
         }
       }
