@@ -837,6 +837,10 @@ __global__ void __launch_bounds__(kT) k3_gs_color(DevLevel3D lv, double* u, cons
 }
 
 // ---------------------------------------------------------------- transfers
+// Fine node (i, j, k) of parity pattern p = (i&1, j&1, k&1) != 0 lies on the
+// coarse edge along the Freudenthal direction D(p) (the c_pdir table:
+// (1,0,0) (0,1,0) (-1,1,0) (0,0,1) (-1,0,1) (0,-1,1) (1,-1,1) for p = 1..7):
+// di = pi ? (pj ^ pk ? -1 : 1) : 0, dj = pj ? (pk ? -1 : 1) : 0, dk = pk.
 __global__ void __launch_bounds__(kT) k3_prolong(DevLevel3D cv, DevLevel3D fv, const double* __restrict__ c, double* f,
                                                  int mode) {
   const int nf = fv.n, nc = cv.n;
@@ -845,24 +849,30 @@ __global__ void __launch_bounds__(kT) k3_prolong(DevLevel3D cv, DevLevel3D fv, c
   const int np = (m2 + 1) * (m2 + 2) / 2;
   const int base = tsz(nf) - tsz(nf - k);
   const double* cm = c + static_cast<size_t>(m) * cv.S;
+  const int pk = k & 1;
+  // coarse planes (k - dk) / 2 and (k + dk) / 2: starts and sizes
+  const int ka = (k - pk) >> 1, kb = (k + pk) >> 1;
+  const int ca = tsz(nc) - tsz(nc - ka), cb = tsz(nc) - tsz(nc - kb);
+  const int ma = nc - ka, mb = nc - kb;
+  double* fm = f + static_cast<size_t>(m) * fv.S + base;
   for (int q = threadIdx.x; q < np; q += blockDim.x) {
     int i, j;
-    decode2(m2, q, i, j);
-    const int p = (i & 1) | ((j & 1) << 1) | ((k & 1) << 2);
+    decode2_fast(m2, q, i, j);
+    const int pi = i & 1, pj = j & 1;
     double v;
-    if (p == 0) {
-      v = cm[lat3(nc, i >> 1, j >> 1, k >> 1)];
+    if ((pi | pj | pk) == 0) {
+      v = cm[ca + lat2(ma, i >> 1, j >> 1)];
     } else {
-      const int d = c_pdir[p];
-      const int di = c_dir[d][0], dj = c_dir[d][1], dk = c_dir[d][2];
-      v = 0.5 * (cm[lat3(nc, (i - di) / 2, (j - dj) / 2, (k - dk) / 2)] +
-                 cm[lat3(nc, (i + di) / 2, (j + dj) / 2, (k + dk) / 2)]);
+      const int di = pi ? ((pj ^ pk) ? -1 : 1) : 0, dj = pj ? (pk ? -1 : 1) : 0;
+      v = 0.5 * (cm[ca + lat2(ma, (i - di) >> 1, (j - dj) >> 1)] + cm[cb + lat2(mb, (i + di) >> 1, (j + dj) >> 1)]);
     }
-    const size_t off = static_cast<size_t>(m) * fv.S + base + q;
-    f[off] = mode == P3_ADD ? f[off] + v : v;
+    fm[q] = mode == P3_ADD ? fm[q] + v : v;
   }
 }
 
+// restriction (transpose of k3_prolong): coarse node (i, j, k) gathers the fine
+// value at (2i, 2j, 2k) and half of each fine neighbour along the 14
+// directions, in direction order (the oracle's order)
 __global__ void __launch_bounds__(kT) k3_restrict(DevLevel3D fv, DevLevel3D cv, const double* __restrict__ rf,
                                                   double* rc) {
   const int nf = fv.n, nc = cv.n;
@@ -871,15 +881,32 @@ __global__ void __launch_bounds__(kT) k3_restrict(DevLevel3D fv, DevLevel3D cv, 
   const int np = (m2 + 1) * (m2 + 2) / 2;
   const int base = tsz(nc) - tsz(nc - k);
   const double* fm = rf + static_cast<size_t>(m) * fv.S;
+  const int kf = 2 * k, T = tsz(nf);
+  // fine planes kf - 1, kf, kf + 1 (sizes mf + 1, mf, mf - 1)
+  const int mf = nf - kf;
+  const int p0 = T - tsz(nf - kf);
+  const int pp = p0 + (mf + 1) * (mf + 2) / 2, pm = kf > 0 ? p0 - (mf + 2) * (mf + 3) / 2 : 0;
   for (int q = threadIdx.x; q < np; q += blockDim.x) {
     int i, j;
-    decode2(m2, q, i, j);
+    decode2_fast(m2, q, i, j);
+    const int fi = 2 * i, fj = 2 * j;
+    // row starts of the 7 fine rows around (fj, kf)
+    const int r0 = lat2(mf, 0, fj);
+    int ra[7], len[7];
+    ra[0] = p0 + r0, len[0] = mf - fj;
+    ra[1] = ra[0] + (mf + 1 - fj), len[1] = mf - fj - 1;                         // (kf, fj + 1)
+    ra[2] = ra[0] - (mf + 2 - fj), len[2] = fj >= 1 ? mf - fj + 1 : -1;          // (kf, fj - 1)
+    const bool up = kf + 1 <= nf, dn = kf >= 1;
+    ra[5] = pp + r0 - fj, len[5] = up ? mf - 1 - fj : -1;                        // (kf + 1, fj)
+    ra[3] = ra[5] - (mf + 1 - fj), len[3] = up && fj >= 1 ? mf - fj : -1;       // (kf + 1, fj - 1)
+    ra[6] = pm + r0 + fj, len[6] = dn ? mf + 1 - fj : -1;                        // (kf - 1, fj)
+    ra[4] = ra[6] + (mf + 2 - fj), len[4] = dn ? mf - fj : -1;                  // (kf - 1, fj + 1)
     double acc = 0.0;
 #pragma unroll
     for (int d = 0; d < 15; ++d) {
-      const int a = 2 * i + c_dir[d][0], bb = 2 * j + c_dir[d][1], cc = 2 * k + c_dir[d][2];
-      if (!inl(nf, a, bb, cc)) continue;
-      const double v = fm[lat3(nf, a, bb, cc)];
+      const int r = dir_row(d), ii = fi + dir_di(d);
+      if (ii < 0 || ii > len[r]) continue;
+      const double v = fm[ra[r] + ii];
       acc = acc + (d == 0 ? v : 0.5 * v);
     }
     rc[static_cast<size_t>(m) * cv.S + base + q] = acc;
