@@ -277,6 +277,53 @@ __global__ void __launch_bounds__(kT) k3_apply(DevLevel3D lv, int mass, const do
   }
 }
 
+// Group part of k3_apply on small levels (n < 8, where it is latency-bound):
+// one warp per group, lane q evaluates member q's partial row, every lane sums
+// the members in slot order from shuffles (the sequence of k3_apply), the
+// lanes write their members' copies.
+__global__ void __launch_bounds__(kT) k3_apply_groups_warp(DevLevel3D lv, int mass, const double* __restrict__ x,
+                                                           double* y, const double* __restrict__ b, int mode) {
+  const int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (g >= lv.ng) return;  // warp-uniform
+  const int n = lv.n, S = lv.S;
+  const double* K = mass ? lv.psM : lv.psK;
+  const int beg = lv.grp_ptr[g], end = lv.grp_ptr[g + 1];
+  const bool dom = lv.grp_domain[g];
+  double v = 0.0;
+  for (int q0 = beg; q0 < end; q0 += 32) {
+    const int q = q0 + lane;
+    double part = 0.0;
+    if (q < end) {
+      const int s = lv.mem_slot[q];
+      if (s < 0) {
+        part = lv.ghost[~s];
+      } else {
+        int i, j, k;
+        unpack_ijk(lv.mem_ijk[q], i, j, k);
+        part = partial_full(K + 240 * s, x + static_cast<size_t>(s) * S, n, i, j, k);
+      }
+    }
+    const int cnt = min(32, end - q0);
+    if (end - beg == 1) {
+      v = __shfl_sync(0xffffffffu, part, 0);
+    } else {
+      for (int t = 0; t < cnt; ++t) v += __shfl_sync(0xffffffffu, part, t);
+    }
+  }
+  for (int q = beg + lane; q < end; q += 32) {
+    if (lv.mem_slot[q] < 0) continue;
+    int i, j, k;
+    unpack_ijk(lv.mem_ijk[q], i, j, k);
+    const size_t off = static_cast<size_t>(lv.mem_slot[q]) * S + lat3(n, i, j, k);
+    if (mode == A3_PLAIN)
+      y[off] = v;
+    else if (mode == A3_RESIDUAL)
+      y[off] = dom ? 0.0 : b[off] - v;
+    else
+      y[off] = (dom || q != beg) ? 0.0 : b[off] - v;
+  }
+}
+
 // Streaming form of the same operator (levels n >= 8), two kernels:
 //  k3_apply_stream  one CTA per macro streams the k-planes of x through a
 //                   4-slot shared-memory ring (TMA bulk copies two planes
@@ -1643,6 +1690,13 @@ void launch3_apply(const DevLevel3D& lv, bool mass, const double* x, double* y, 
     return;
   }
   const int planes = lv.M * (lv.n + 1);
+  if (lv.n < 8 && lv.ng > 0) {  // small levels: the groups by warps (latency-bound), planes as before
+    k3_apply<<<planes, kT, 0, st>>>(lv, mass ? 1 : 0, x, y, b, mode, planes);
+    check3("k3_apply");
+    k3_apply_groups_warp<<<blocks_for(32ll * lv.ng), kT, 0, st>>>(lv, mass ? 1 : 0, x, y, b, mode);
+    check3("k3_apply_groups_warp");
+    return;
+  }
   k3_apply<<<planes + blocks_for(lv.ng), kT, 0, st>>>(lv, mass ? 1 : 0, x, y, b, mode, planes);
   check3("k3_apply");
 }
@@ -1697,7 +1751,7 @@ void launch3_gs(const DevLevel3D& lv, double* u, const double* b, int sweeps, cu
   }
 }
 
-int launch3_apply_count(const DevLevel3D& lv) { return apply_streams(lv) ? 1 + (lv.ng > 0) : 1; }
+int launch3_apply_count(const DevLevel3D& lv) { return apply_streams(lv) || (lv.n < 8 && lv.ng > 0) ? 1 + (lv.ng > 0) : 1; }
 int launch3_estimate_count(const DevLevel3D& lv) { return !estimate_cells() && apply_streams(lv) ? 1 : 2; }
 
 int launch3_gs_count(const DevLevel3D& lv, int sweeps) {
