@@ -989,6 +989,41 @@ __global__ void __launch_bounds__(kT) k3_sync(DevLevel3D lv, double* f, int addi
     if (lv.mem_slot[q] >= 0) f[off_of(q)] = v;
 }
 
+// k3_sync on small levels (n < 8, latency-bound): one warp per group, the
+// member loads in parallel, the slot-order sum from shuffles (same sequence)
+__global__ void __launch_bounds__(kT) k3_sync_warp(DevLevel3D lv, double* f, int additive, int zero_domain) {
+  const int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (g >= lv.ng) return;  // warp-uniform
+  const int n = lv.n, S = lv.S;
+  const int beg = lv.grp_ptr[g], end = lv.grp_ptr[g + 1];
+  auto off_of = [&](int q) {
+    int i, j, k;
+    unpack_ijk(lv.mem_ijk[q], i, j, k);
+    return static_cast<size_t>(lv.mem_slot[q]) * S + lat3(n, i, j, k);
+  };
+  if (zero_domain && lv.grp_domain[g]) {
+    for (int q = beg + lane; q < end; q += 32)
+      if (lv.mem_slot[q] >= 0) f[off_of(q)] = 0.0;
+    return;
+  }
+  if (end - beg < 2) return;
+  double v = 0.0;
+  if (additive) {
+    for (int q0 = beg; q0 < end; q0 += 32) {
+      const int q = q0 + lane;
+      double x = 0.0;
+      if (q < end) x = lv.mem_slot[q] < 0 ? lv.ghost[~lv.mem_slot[q]] : f[off_of(q)];
+      const int cnt = min(32, end - q0);
+      for (int t = 0; t < cnt; ++t) v += __shfl_sync(0xffffffffu, x, t);
+    }
+  } else {
+    v = lv.mem_slot[beg] < 0 ? lv.ghost[~lv.mem_slot[beg]] : f[off_of(beg)];
+  }
+  __syncwarp();  // every lane has read before any copy is overwritten
+  for (int q = beg + lane; q < end; q += 32)
+    if (lv.mem_slot[q] >= 0) f[off_of(q)] = v;
+}
+
 __global__ void __launch_bounds__(kT) k3_owner_mask(DevLevel3D lv, double* f) {
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= lv.ng) return;
@@ -1771,8 +1806,7 @@ void launch3_restrict(const DevLevel3D& fine, const DevLevel3D& coarse, const do
   init_constants();
   k3_restrict<<<coarse.M * (coarse.n + 1), kT, 0, st>>>(fine, coarse, rf, rc);
   check3("k3_restrict");
-  k3_sync<<<blocks_for(coarse.ng), kT, 0, st>>>(coarse, rc, 1, zero_domain);
-  check3("k3_sync");
+  launch3_sync_zero(coarse, rc, 1, zero_domain, st);
 }
 
 void launch3_restrict_only(const DevLevel3D& fine, const DevLevel3D& coarse, const double* rf, double* rc,
@@ -1783,7 +1817,10 @@ void launch3_restrict_only(const DevLevel3D& fine, const DevLevel3D& coarse, con
 }
 
 void launch3_sync_zero(const DevLevel3D& lv, double* f, int additive, int zero_domain, cudaStream_t st) {
-  k3_sync<<<blocks_for(lv.ng), kT, 0, st>>>(lv, f, additive, zero_domain);
+  if (lv.n < 8)
+    k3_sync_warp<<<blocks_for(32ll * lv.ng), kT, 0, st>>>(lv, f, additive, zero_domain);
+  else
+    k3_sync<<<blocks_for(lv.ng), kT, 0, st>>>(lv, f, additive, zero_domain);
   check3("k3_sync");
 }
 
@@ -1801,8 +1838,7 @@ void launch3_set_boundary(const DevLevel3D& lv, double* f, const double* g_grp, 
 }
 
 void launch3_sync(const DevLevel3D& lv, double* f, int additive, cudaStream_t st) {
-  k3_sync<<<blocks_for(lv.ng), kT, 0, st>>>(lv, f, additive, 0);
-  check3("k3_sync");
+  launch3_sync_zero(lv, f, additive, 0, st);
 }
 
 void launch3_cg0(const DevLevel3D& lv0, double* u, const double* b, double* scratch, CgParams prm,
