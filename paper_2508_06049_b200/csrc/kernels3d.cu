@@ -1753,6 +1753,7 @@ void launch3_gs(const DevLevel3D& lv, double* u, const double* b, int sweeps, cu
     if (const char* e = getenv("KB_GS3_BIG")) big = e[0] == '1';
     const int nt = big ? 512 : 256;
     int grid = (big ? occ_big : occ_small) * sms;
+    if (lv.n <= 4) grid = std::min(grid, sms);  // tiny levels: one CTA per SM (cheaper grid barriers)
     if (const char* e = getenv("KB_GS3_GRID")) grid = std::max(1, std::min(grid, atoi(e)));
     int active = grid;
     if (const char* e = getenv("KB_GS3_ACTIVE")) active = std::max(1, std::min(grid, atoi(e)));
