@@ -1757,7 +1757,10 @@ void launch3_gs(const DevLevel3D& lv, double* u, const double* b, int sweeps, cu
     if (const char* e = getenv("KB_GS3_GRID")) grid = std::max(1, std::min(grid, atoi(e)));
     int active = grid;
     if (const char* e = getenv("KB_GS3_ACTIVE")) active = std::max(1, std::min(grid, atoi(e)));
-    int group = lv.M;
+    // interior macros batched per colour pass: all of the CTA's, except n = 32
+    // where pairs keep the pass's working set in L2 (measured 0.68 -> 0.53 ms
+    // per 2 sweeps on 3072 macros)
+    int group = lv.n == 32 ? 2 : lv.M;
     if (const char* e = getenv("KB_GS3_G")) group = std::max(1, atoi(e));
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
