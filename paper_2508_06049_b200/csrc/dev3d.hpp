@@ -47,6 +47,13 @@ struct DevLevel3D {
   const double* cg_coef;
   const int* cg_vid;
   int cg_members4;             // member count when every member has exactly 4 terms, else 0
+  // compact form of the 4-term program (cg_members4 > 0): the distinct
+  // coefficient rows (4 doubles each, bitwise-deduplicated), per member its row
+  // and its 4 vertex ids (16 bit); staged in shared memory by k3_cg0
+  const double* cg_rows;
+  const unsigned short* cg_mrow;
+  const unsigned short* cg_mvid;  // 4 per member
+  int cg_nrows;                   // 0: not available
   // sharded levels (solver3d_shard.cpp): a member with mem_slot < 0 lives on
   // another shard; its contribution (partial row or copy value, as the
   // operation needs) is ghost[~mem_slot], received by the exchange before the

@@ -1129,17 +1129,65 @@ __device__ void cg0_apply4(const DevLevel3D& lv, const double* x, double* y, con
   }
 }
 
+// Same operator from the compact program: the distinct coefficient rows and the
+// member row ids in shared memory, the member vertex ids (8 bytes per member)
+// from L2; member partials in parallel into mp[] (4 members in flight per
+// thread), then per group the member sum in slot order from shared memory (the
+// order and arithmetic of cg0_apply).
+__device__ void cg0_apply_compact(int ng, int nm, const int* gmem, const double* rows, const unsigned short* mrow,
+                                  const ushort4* __restrict__ mvid, const double* x, double* y, const double* b,
+                                  const unsigned char* dom, int residual, double* mp) {
+  constexpr int U = 4;
+  for (int q0 = threadIdx.x; q0 < nm; q0 += U * blockDim.x) {
+    ushort4 v[U];
+    int rw[U];
+#pragma unroll
+    for (int a = 0; a < U; ++a) {
+      const int q = min(q0 + a * static_cast<int>(blockDim.x), nm - 1);
+      v[a] = __ldg(mvid + q);
+      rw[a] = mrow[q];
+    }
+#pragma unroll
+    for (int a = 0; a < U; ++a) {
+      const int q = q0 + a * static_cast<int>(blockDim.x);
+      const double* c = rows + 4 * rw[a];
+      double acc = c[0] * x[v[a].x];
+      acc = acc + c[1] * x[v[a].y];
+      acc = acc + c[2] * x[v[a].z];
+      acc = acc + c[3] * x[v[a].w];
+      if (q < nm) mp[q] = acc;
+    }
+  }
+  __syncthreads();
+  for (int g = threadIdx.x; g < ng; g += blockDim.x) {
+    const int m0 = gmem[g], m1 = gmem[g + 1];
+    double v = 0.0;
+    for (int q = m0; q < m1; ++q) v = (m1 - m0 == 1) ? mp[q] : v + mp[q];
+    y[g] = dom[g] ? 0.0 : (residual ? b[g] - v : v);
+  }
+}
+
+// 3-d dot order (oracle o3_dot): chunks of 32 terms summed in order, then the
+// chunk sums in order.  The products are formed in parallel first, the chunk
+// sums are unrolled (loads in flight), thread 0 adds the chunk sums.
 __device__ double cg0_dot(int ng, const double* a, const double* b, const unsigned char* dom, bool zero_dom,
-                          double* chunks) {
+                          double* chunks, double* prod) {
   const int nch = (ng + 31) / 32;
   __syncthreads();
+  for (int g = threadIdx.x; g < ng; g += blockDim.x) {
+    double x = a[g], y = b[g];
+    if (zero_dom && dom[g]) x = y = 0.0;
+    prod[g] = x * y;
+  }
+  __syncthreads();
   for (int c = threadIdx.x; c < nch; c += blockDim.x) {
+    double t[32];
+#pragma unroll
+    for (int q = 0; q < 32; ++q) t[q] = 32 * c + q < ng ? prod[32 * c + q] : 0.0;
     double s = 0.0;
-    for (int g = 32 * c; g < min(ng, 32 * c + 32); ++g) {
-      double x = a[g], y = b[g];
-      if (zero_dom && dom[g]) x = y = 0.0;
-      s += x * y;
-    }
+#pragma unroll
+    for (int q = 0; q < 32; ++q)
+      if (32 * c + q < ng) s += t[q];
     chunks[c] = s;
   }
   __syncthreads();
@@ -1154,7 +1202,7 @@ __device__ double cg0_dot(int ng, const double* a, const double* b, const unsign
 }
 
 __global__ void __launch_bounds__(1024) k3_cg0(DevLevel3D lv, double* uc, const double* bc, CgParams prm,
-                                               DevStatus* status, int nmem4) {
+                                               DevStatus* status, int nmem4, int compact) {
   extern __shared__ double sm[];
   const int ng = lv.ng;
   double* u = sm;
@@ -1162,11 +1210,27 @@ __global__ void __launch_bounds__(1024) k3_cg0(DevLevel3D lv, double* uc, const 
   double* r = b + ng;
   double* p = r + ng;
   double* ap = p + ng;
-  double* chunks = ap + ng;
+  double* prod = ap + ng;  // dot-product terms
+  double* chunks = prod + ng;
   double* mp = chunks + (ng + 31) / 32;  // nmem4 member partials (member-parallel operator)
-  unsigned char* dom = reinterpret_cast<unsigned char*>(mp + nmem4);
+  // compact program (compact != 0, nmem4 == 0): member partials, rows, member rows, group ranges
+  const int nm = compact ? lv.cg_members4 : 0;
+  double* cmp = mp;
+  double* crow = cmp + nm;
+  unsigned short* cmrow = reinterpret_cast<unsigned short*>(crow + (compact ? 4 * lv.cg_nrows : 0));
+  int* cgm = reinterpret_cast<int*>(cmrow + ((nm + 1) & ~1));
+  unsigned char* dom = compact ? reinterpret_cast<unsigned char*>(cgm + ng + 1)
+                               : reinterpret_cast<unsigned char*>(mp + nmem4);
+  const ushort4* cvid = reinterpret_cast<const ushort4*>(lv.cg_mvid);
+  if (compact) {
+    for (int t = threadIdx.x; t < 4 * lv.cg_nrows; t += blockDim.x) crow[t] = lv.cg_rows[t];
+    for (int t = threadIdx.x; t < nm; t += blockDim.x) cmrow[t] = lv.cg_mrow[t];
+    for (int t = threadIdx.x; t <= ng; t += blockDim.x) cgm[t] = lv.cg_gmem[t];
+  }
   auto cg0_op = [&](const double* x, double* y, const double* bb, int residual) {
-    if (nmem4 > 0)
+    if (compact)
+      cg0_apply_compact(ng, nm, cgm, crow, cmrow, cvid, x, y, bb, dom, residual, cmp);
+    else if (nmem4 > 0)
       cg0_apply4(lv, x, y, bb, dom, residual, mp, nmem4);
     else
       cg0_apply(lv, x, y, bb, dom, residual);
@@ -1180,8 +1244,8 @@ __global__ void __launch_bounds__(1024) k3_cg0(DevLevel3D lv, double* uc, const 
   cg0_op(u, r, b, 1);
   __syncthreads();
   for (int g = threadIdx.x; g < ng; g += blockDim.x) p[g] = r[g];
-  double rr = cg0_dot(ng, r, r, dom, false, chunks);
-  const double bn = sqrt(fmax(0.0, cg0_dot(ng, b, b, dom, true, chunks)));
+  double rr = cg0_dot(ng, r, r, dom, false, chunks, prod);
+  const double bn = sqrt(fmax(0.0, cg0_dot(ng, b, b, dom, true, chunks, prod)));
   const double tol = prm.rel_tol * bn < prm.abs_floor ? prm.abs_floor : prm.rel_tol * bn;
   int it = 0;
   while (sqrt(rr) > tol) {
@@ -1193,7 +1257,7 @@ __global__ void __launch_bounds__(1024) k3_cg0(DevLevel3D lv, double* uc, const 
       break;
     }
     cg0_op(p, ap, nullptr, 0);
-    const double pap = cg0_dot(ng, p, ap, dom, false, chunks);
+    const double pap = cg0_dot(ng, p, ap, dom, false, chunks, prod);
     if (pap <= 0.0) {
       if (threadIdx.x == 0 && status->code == 0) {
         status->code = 2;
@@ -1206,7 +1270,7 @@ __global__ void __launch_bounds__(1024) k3_cg0(DevLevel3D lv, double* uc, const 
       u[g] = u[g] + alpha * p[g];
       r[g] = r[g] + (-alpha) * ap[g];
     }
-    const double rn = cg0_dot(ng, r, r, dom, false, chunks);
+    const double rn = cg0_dot(ng, r, r, dom, false, chunks, prod);
     const double beta = rn / rr;
     rr = rn;
     for (int g = threadIdx.x; g < ng; g += blockDim.x) p[g] = p[g] * beta + r[g];
@@ -1849,17 +1913,24 @@ void launch3_cg0(const DevLevel3D& lv0, double* u, const double* b, double* scra
                  DevStatus* status, cudaStream_t st) {
   (void)scratch;
   init_constants();
-  const size_t base = (5 * static_cast<size_t>(lv0.ng) + (lv0.ng + 31) / 32) * sizeof(double) + lv0.ng + 16;
+  const size_t base = (6 * static_cast<size_t>(lv0.ng) + (lv0.ng + 31) / 32) * sizeof(double) + lv0.ng + 16;
   if (base > 200 * 1024) fail(KB_STRUCTURAL, "coarse mesh too large for the level-0 CG (more than ~4800 vertices)");
-  // member-parallel operator when the member partials fit next to the vectors
-  const int nmem4 = lv0.cg_members4 > 0 && base + lv0.cg_members4 * 8.0 <= 200 * 1024 ? lv0.cg_members4 : 0;
-  const size_t smem = base + static_cast<size_t>(nmem4) * 8;
+  // compact program staged in shared memory when it fits (no per-iteration L2
+  // traffic for the operator), else the member-parallel operator when the
+  // member partials fit next to the vectors, else the plain one
+  const size_t compact_bytes =
+      lv0.cg_nrows > 0 ? 8 * static_cast<size_t>(lv0.cg_members4) + 32 * static_cast<size_t>(lv0.cg_nrows) +
+                             2 * static_cast<size_t>((lv0.cg_members4 + 1) & ~1) + 4 * static_cast<size_t>(lv0.ng + 1)
+                       : 0;
+  const int compact = compact_bytes > 0 && base + compact_bytes + 64 <= 220 * 1024 ? 1 : 0;
+  const int nmem4 = !compact && lv0.cg_members4 > 0 && base + lv0.cg_members4 * 8.0 <= 200 * 1024 ? lv0.cg_members4 : 0;
+  const size_t smem = base + (compact ? compact_bytes + 64 : static_cast<size_t>(nmem4) * 8);
   static size_t cg0_high = 0;  // only ever grows (graph nodes captured earlier stay launchable)
   if (smem > cg0_high) {
     KB_CUDA_CHECK(cudaFuncSetAttribute(k3_cg0, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     cg0_high = smem;
   }
-  k3_cg0<<<1, 1024, smem, st>>>(lv0, u, b, prm, status, nmem4);
+  k3_cg0<<<1, 1024, smem, st>>>(lv0, u, b, prm, status, nmem4, compact);
   check3("k3_cg0");
 }
 

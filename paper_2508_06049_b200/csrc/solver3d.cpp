@@ -2,9 +2,12 @@
 #include "solver3d.hpp"
 
 #include <algorithm>
+#include <array>
 #include <cmath>
+#include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 
 namespace kb {
 
@@ -110,6 +113,8 @@ std::unique_ptr<DeviceHierarchy3D> DeviceHierarchy3D::create(const Mesh3D& mesh,
       if (lv.grp_ptr[g + 1] == lv.grp_ptr[g]) fail(KB_STRUCTURAL, "macro vertex used by no tetrahedron");
     }
     bytes += r256(cg_gmem.size() * 4) + r256(cg_mterm.size() * 4) + r256(cg_vid.size() * 4) + r256(cg_coef.size() * 8);
+    // compact program (upper bounds: every row distinct)
+    bytes += r256(cg_coef.size() * 8) + r256(cg_mterm.size() * 2) + r256(cg_vid.size() * 2);
   }
   for (int l = 0; l <= h.L; ++l) bytes += 2 * r256(h.levels[l].psK.size() * 8);
   d->arena.reserve(bytes + 4096);
@@ -180,6 +185,35 @@ std::unique_ptr<DeviceHierarchy3D> DeviceHierarchy3D::create(const Mesh3D& mesh,
       bool four = true;
       for (size_t q = 0; q + 1 < cg_mterm.size(); ++q) four = four && cg_mterm[q + 1] - cg_mterm[q] == 4;
       dl.cg_members4 = four ? static_cast<int>(cg_mterm.size()) - 1 : 0;
+      // compact program: distinct coefficient rows + 16-bit member records
+      if (four) {
+        std::map<std::array<std::uint64_t, 4>, int> rows;
+        std::vector<double> row_vals;
+        std::vector<unsigned short> mrow, mvid;
+        bool ok = true;
+        for (int q = 0; q < dl.cg_members4 && ok; ++q) {
+          std::array<std::uint64_t, 4> key{};
+          std::memcpy(key.data(), &cg_coef[4 * static_cast<size_t>(q)], 32);
+          auto it = rows.find(key);
+          if (it == rows.end()) {
+            it = rows.emplace(key, static_cast<int>(rows.size())).first;
+            row_vals.insert(row_vals.end(), &cg_coef[4 * static_cast<size_t>(q)], &cg_coef[4 * static_cast<size_t>(q)] + 4);
+          }
+          ok = it->second < 4096;
+          mrow.push_back(static_cast<unsigned short>(it->second));
+          for (int t = 0; t < 4; ++t) {
+            const int v = cg_vid[4 * static_cast<size_t>(q) + t];
+            ok = ok && v >= 0 && v < 65536;
+            mvid.push_back(static_cast<unsigned short>(v));
+          }
+        }
+        if (ok) {
+          dl.cg_rows = d->arena.upload(row_vals);
+          dl.cg_mrow = d->arena.upload(mrow);
+          dl.cg_mvid = d->arena.upload(mvid);
+          dl.cg_nrows = static_cast<int>(rows.size());
+        }
+      }
     }
     d->lev.push_back(dl);
   }
