@@ -211,6 +211,27 @@ __device__ __forceinline__ void p3_mbar_wait(unsigned bar, unsigned parity) {
 }
 
 __device__ __forceinline__ int plane_base(int n, int k) { return tsz(n) - tsz(n - k); }
+// Lattice-boundary signature bits (sig3) that put the neighbour along
+// direction d outside the macro: i = 0 and di < 0, j = 0 and dj < 0, k = 0 and
+// dk < 0, i + j + k = n and di + dj + dk > 0 (compile time per direction).
+__device__ __forceinline__ constexpr int dir_bad(int d) {
+  constexpr int v[15] = {0, 8, 1, 1, 2, 2, 4, 8, 2, 1, 4, 10, 5, 8, 4};
+  return v[d];
+}
+// Row starts (shared-memory plane slots) of the 7 rows around (., j) of plane
+// k with m2 = n - k; base[0..2]: slot bases of planes k - 1, k, k + 1.  Rows
+// outside the lattice get an address that is never loaded.
+__device__ __forceinline__ void slot_rows(const int (&base)[3], int m2, int j, int (&ra)[7]) {
+  const int r0 = lat2(m2, 0, j);
+  ra[0] = base[1] + r0;
+  ra[1] = ra[0] + (m2 + 1 - j);
+  ra[2] = ra[0] - (m2 + 2 - j);
+  ra[5] = base[2] + r0 - j;      // plane k + 1: lat2(m2 - 1, 0, j)
+  ra[3] = ra[5] - (m2 + 1 - j);  // lat2(m2 - 1, 0, j - 1)
+  ra[6] = base[0] + r0 + j;      // plane k - 1: lat2(m2 + 1, 0, j)
+  ra[4] = ra[6] + (m2 + 2 - j);  // lat2(m2 + 1, 0, j + 1)
+}
+
 // doubles per plane slot: the largest plane (k = 0), +1 alignment pad, 16-byte multiple
 __host__ __device__ __forceinline__ int plane_stride(int n) { return ((n + 1) * (n + 2) / 2 + 3) & ~1; }
 
@@ -448,24 +469,16 @@ __global__ void __launch_bounds__(kAsThreads) k3_apply_stream(DevLevel3D lv, int
       } else {                  // i = m2 - j, j = 1 .. m2
         j = e - 2 * m2 + 1, i = m2 - j;
       }
-      const double* cf = ps + 15 * sig3(n, i, j, k);
+      const int sig = sig3(n, i, j, k);
+      const double* cf = ps + 15 * sig;
       int ra[7];
-      bool rv[7];
-      int len[7];
-#pragma unroll
-      for (int r = 0; r < 7; ++r) {
-        const int kk = k + row_dk(r), jj = j + row_dj(r), mm = n - kk;
-        rv[r] = kk >= 0 && kk <= n && jj >= 0 && jj <= mm;
-        ra[r] = rv[r] ? base[1 + row_dk(r)] + lat2(mm, 0, jj) : base[1];
-        len[r] = rv[r] ? mm - jj : -1;
-      }
+      slot_rows(base, m2, j, ra);
       const int c0 = ra[0] + i;
       double acc = cf[0] * ring[c0];
 #pragma unroll
       for (int d = 1; d < 15; ++d) {
-        const int r = dir_row(d), ii = i + dir_di(d);
-        const bool ok = ii >= 0 && ii <= len[r];
-        const double t = acc + cf[d] * ring[ok ? ra[r] + ii : c0];
+        const bool ok = (sig & dir_bad(d)) == 0;
+        const double t = acc + cf[d] * ring[ok ? ra[dir_row(d)] + i + dir_di(d) : c0];
         acc = ok ? t : acc;
       }
       y[gp + lat2(m2, 0, j) + i] = acc;
@@ -1554,23 +1567,17 @@ __global__ void __launch_bounds__(kEsThreads, 2) k3_estimate_stream(DevLevel3D l
       } else {
         j = e - 2 * m2 + 1, i = m2 - j;
       }
-      const double* cf = ps + 15 * sig3(n, i, j, k);
-      int ra[7], len[7];
-#pragma unroll
-      for (int r = 0; r < 7; ++r) {
-        const int kk = k + row_dk(r), jj = j + row_dj(r), mm = n - kk;
-        const bool rv = kk >= 0 && kk <= n && jj >= 0 && jj <= mm;
-        ra[r] = rv ? base[1 + row_dk(r)] + lat2(mm, 0, jj) : base[1];
-        len[r] = rv ? mm - jj : -1;
-      }
+      const int sig = sig3(n, i, j, k);
+      const double* cf = ps + 15 * sig;
+      int ra[7];
+      slot_rows(base, m2, j, ra);
       const int c0 = ra[0] + i;
       const double eb0 = rb[c0], ec0 = rc[c0];
       double mb = cf[0] * eb0, mc = cf[0] * ec0;
 #pragma unroll
       for (int d = 1; d < 15; ++d) {
-        const int r = dir_row(d), ii = i + dir_di(d);
-        const bool ok = ii >= 0 && ii <= len[r];
-        const int a = ok ? ra[r] + ii : c0;
+        const bool ok = (sig & dir_bad(d)) == 0;
+        const int a = ok ? ra[dir_row(d)] + i + dir_di(d) : c0;
         const double tb = mb + cf[d] * rb[a], tc = mc + cf[d] * rc[a];
         mb = ok ? tb : mb;
         mc = ok ? tc : mc;
