@@ -149,6 +149,27 @@ __device__ __forceinline__ void node_rows(int n, int j, int k, int (&ra)[7], int
   }
 }
 
+// Lattice-boundary signature bits (sig3) that put the neighbour along
+// direction d outside the macro: i = 0 and di < 0, j = 0 and dj < 0, k = 0 and
+// dk < 0, i + j + k = n and di + dj + dk > 0 (compile time per direction).
+__device__ __forceinline__ constexpr int dir_bad(int d) {
+  constexpr int v[15] = {0, 8, 1, 1, 2, 2, 4, 8, 2, 1, 4, 10, 5, 8, 4};
+  return v[d];
+}
+// Row starts (shared-memory plane slots) of the 7 rows around (., j) of plane
+// k with m2 = n - k; base[0..2]: slot bases of planes k - 1, k, k + 1.  Rows
+// outside the lattice get an address that is never loaded.
+__device__ __forceinline__ void slot_rows(const int (&base)[3], int m2, int j, int (&ra)[7]) {
+  const int r0 = lat2(m2, 0, j);
+  ra[0] = base[1] + r0;
+  ra[1] = ra[0] + (m2 + 1 - j);
+  ra[2] = ra[0] - (m2 + 2 - j);
+  ra[5] = base[2] + r0 - j;      // plane k + 1: lat2(m2 - 1, 0, j)
+  ra[3] = ra[5] - (m2 + 1 - j);  // lat2(m2 - 1, 0, j - 1)
+  ra[6] = base[0] + r0 + j;      // plane k - 1: lat2(m2 + 1, 0, j)
+  ra[4] = ra[6] + (m2 + 2 - j);  // lat2(m2 + 1, 0, j + 1)
+}
+
 // partial row of a lattice-boundary node of one macro: its signature's partial
 // stencil over the neighbours inside the macro, centre first.  All loads are
 // issued together (clamped to the node itself when the neighbour is outside
@@ -156,18 +177,22 @@ __device__ __forceinline__ void node_rows(int n, int j, int k, int (&ra)[7], int
 template <bool kOff>
 __device__ __forceinline__ double partial_row(const double* __restrict__ ps_m, const double* xm, int n, int i, int j,
                                               int k) {
-  const double* ps = ps_m + 15 * sig3(n, i, j, k);
-  int ra[7], len[7];
-  node_rows(n, j, k, ra, len);
+  const int sig = sig3(n, i, j, k);
+  const double* ps = ps_m + 15 * sig;
+  // row starts from the plane offsets; a neighbour is inside the macro unless the
+  // node's boundary signature excludes its direction (dir_bad)
+  const int m2 = n - k, pb0 = tsz(n) - tsz(m2);
+  const int base[3] = {pb0 - (m2 + 2) * (m2 + 3) / 2, pb0, pb0 + (m2 + 1) * (m2 + 2) / 2};
+  int ra[7];
+  slot_rows(base, m2, j, ra);
   const int c0 = ra[0] + i;
   double x[15], cf[15];
   bool ok[15];
   const double* ad[15];
 #pragma unroll
   for (int d = 0; d < 15; ++d) {
-    const int r = dir_row(d), ii = i + dir_di(d);
-    ok[d] = ii >= 0 && ii <= len[r];
-    ad[d] = xm + (ok[d] ? ra[r] + ii : c0);
+    ok[d] = (sig & dir_bad(d)) == 0;
+    ad[d] = xm + (ok[d] ? ra[dir_row(d)] + i + dir_di(d) : c0);
   }
   // ptxas sinks plain loads to just before their use, serialising the L2 round
   // trips of the 15 terms; issued from one asm block they are all in flight
@@ -211,27 +236,6 @@ __device__ __forceinline__ void p3_mbar_wait(unsigned bar, unsigned parity) {
 }
 
 __device__ __forceinline__ int plane_base(int n, int k) { return tsz(n) - tsz(n - k); }
-// Lattice-boundary signature bits (sig3) that put the neighbour along
-// direction d outside the macro: i = 0 and di < 0, j = 0 and dj < 0, k = 0 and
-// dk < 0, i + j + k = n and di + dj + dk > 0 (compile time per direction).
-__device__ __forceinline__ constexpr int dir_bad(int d) {
-  constexpr int v[15] = {0, 8, 1, 1, 2, 2, 4, 8, 2, 1, 4, 10, 5, 8, 4};
-  return v[d];
-}
-// Row starts (shared-memory plane slots) of the 7 rows around (., j) of plane
-// k with m2 = n - k; base[0..2]: slot bases of planes k - 1, k, k + 1.  Rows
-// outside the lattice get an address that is never loaded.
-__device__ __forceinline__ void slot_rows(const int (&base)[3], int m2, int j, int (&ra)[7]) {
-  const int r0 = lat2(m2, 0, j);
-  ra[0] = base[1] + r0;
-  ra[1] = ra[0] + (m2 + 1 - j);
-  ra[2] = ra[0] - (m2 + 2 - j);
-  ra[5] = base[2] + r0 - j;      // plane k + 1: lat2(m2 - 1, 0, j)
-  ra[3] = ra[5] - (m2 + 1 - j);  // lat2(m2 - 1, 0, j - 1)
-  ra[6] = base[0] + r0 + j;      // plane k - 1: lat2(m2 + 1, 0, j)
-  ra[4] = ra[6] + (m2 + 2 - j);  // lat2(m2 + 1, 0, j + 1)
-}
-
 // doubles per plane slot: the largest plane (k = 0), +1 alignment pad, 16-byte multiple
 __host__ __device__ __forceinline__ int plane_stride(int n) { return ((n + 1) * (n + 2) / 2 + 3) & ~1; }
 
