@@ -722,12 +722,10 @@ __device__ void gs_interior_batch(const DevLevel3D& lv, double* u, const double*
       if (idx >= __ldg(lv.pat_ptr + p + 1) - q0) continue;
       int i, j, k;
       unpack_ijk(__ldg(lv.pat_node + q0 + idx), i, j, k);
+      const int m2 = n - k, pb0 = T - tsz(m2);
+      const int base[3] = {pb0 - (m2 + 2) * (m2 + 3) / 2, pb0, pb0 + (m2 + 1) * (m2 + 2) / 2};
       int ra[7];
-#pragma unroll
-      for (int r = 0; r < 7; ++r) {
-        const int kk = k + row_dk(r), jj = j + row_dj(r);
-        ra[r] = T - tsz(n - kk) + lat2(n - kk, 0, jj);
-      }
+      slot_rows(base, m2, j, ra);
       double st[15];
 #pragma unroll
       for (int d = 1; d < 15; ++d) st[d] = __ldg(lv.stK + 15 * m + d);
