@@ -431,36 +431,49 @@ __global__ void __launch_bounds__(kAsThreads) k3_apply_stream(DevLevel3D lv, int
       base[d] = (kk % kAsSlots) * stride + static_cast<int>((reinterpret_cast<size_t>(xm + plane_base(n, kk)) >> 3) & 1);
     }
     const size_t gp = gm + plane_base(n, k);
-    // lattice-interior nodes, flattened: the plane's interior is the triangle
-    // lattice of size m2 - 3 shifted by (1, 1); full stencil
+    // lattice-interior nodes, flattened in pairs (i, i + 1) of a row: the
+    // plane's interior is the triangle lattice of size mi = m2 - 3 shifted by
+    // (1, 1); rows 2c and 2c + 1 hold mi + 1 - 2c pairs together.  The two
+    // nodes share their row starts and most neighbour loads (the compiler
+    // merges the equal shared-memory addresses); each keeps the full
+    // stencil's term order.
+    int npairs = 0;
     if (k >= 1 && m2 >= 3) {
-      const int mi = m2 - 3, ni = (mi + 1) * (mi + 2) / 2;
-      for (int e = tid; e < ni; e += kAsThreads) {
-        int i, j;
-        decode2_fast(mi, e, i, j);
-        ++i, ++j;
-        const int r0 = lat2(m2, 0, j);
+      const int mi = m2 - 3, nc = (mi + 2) / 2;  // row couples
+      npairs = nc * (mi + 1) - nc * (nc - 1);
+      const float A = static_cast<float>(mi + 2);
+      for (int e = tid; e < npairs; e += kAsThreads) {
+        // couple c: pairs before it = c (mi + 1) - c (c - 1) = c (mi + 2 - c)
+        int c = static_cast<int>((A - sqrtf(fmaxf(A * A - 4.0f * e, 0.0f))) * 0.5f);
+        c = c + (c + 1 <= nc - 1 && (c + 1) * (mi + 1 - c) <= e);
+        c = c - (c > 0 && c * (mi + 2 - c) > e);
+        const int e1 = e - c * (mi + 2 - c);
+        const int L0 = mi + 1 - 2 * c, P0 = (L0 + 1) >> 1;  // first row of the couple: L0 nodes, P0 pairs
+        const int r = e1 < P0 ? 2 * c : 2 * c + 1;
+        const int p = e1 < P0 ? e1 : e1 - P0;
+        const int L = mi + 1 - r;
+        const int j = r + 1, i = 1 + 2 * p;
+        const bool two = 2 * p + 1 < L;
         int ra[7];
-        ra[0] = base[1] + r0;
-        ra[1] = ra[0] + (m2 + 1 - j);
-        ra[2] = ra[0] - (m2 + 2 - j);
-        ra[5] = base[2] + r0 - j;      // plane k + 1: lat2(m2 - 1, 0, j)
-        ra[3] = ra[5] - (m2 + 1 - j);  // lat2(m2 - 1, 0, j - 1)
-        ra[6] = base[0] + r0 + j;      // plane k - 1: lat2(m2 + 1, 0, j)
-        ra[4] = ra[6] + (m2 + 2 - j);  // lat2(m2 + 1, 0, j + 1)
-        const size_t off = gp + r0 + i;
-        const double bv = mode == A3_PLAIN ? 0.0 : __ldg(b + off);
-        double acc = s[0] * ring[ra[0] + i];
+        slot_rows(base, m2, j, ra);
+        const size_t off = gp + (ra[0] - base[1]) + i;
+        const double bv0 = mode == A3_PLAIN ? 0.0 : __ldg(b + off);
+        const double bv1 = mode == A3_PLAIN || !two ? 0.0 : __ldg(b + off + 1);
+        double acc0 = s[0] * ring[ra[0] + i];
+        double acc1 = s[0] * ring[ra[0] + i + 1];
 #pragma unroll
-        for (int d = 1; d < 15; ++d) acc = acc + s[d] * ring[ra[dir_row(d)] + i + dir_di(d)];
-        y[off] = mode == A3_PLAIN ? acc : bv - acc;
+        for (int d = 1; d < 15; ++d) {
+          acc0 = acc0 + s[d] * ring[ra[dir_row(d)] + i + dir_di(d)];
+          acc1 = acc1 + s[d] * ring[ra[dir_row(d)] + i + 1 + dir_di(d)];
+        }
+        y[off] = mode == A3_PLAIN ? acc0 : bv0 - acc0;
+        if (two) y[off + 1] = mode == A3_PLAIN ? acc1 : bv1 - acc1;
       }
     }
     // lattice-boundary nodes of the plane: partial rows (raw)
     const int nb = k == 0 ? (m2 + 1) * (m2 + 2) / 2 : (m2 >= 1 ? 3 * m2 : 1);
     // boundary nodes continue the interior's thread rotation (balanced per plane)
-    const int ni_all = k >= 1 && m2 >= 3 ? (m2 - 2) * (m2 - 1) / 2 : 0;
-    for (int e = (tid - ni_all % kAsThreads + kAsThreads) % kAsThreads; e < nb; e += kAsThreads) {
+    for (int e = (tid - npairs % kAsThreads + kAsThreads) % kAsThreads; e < nb; e += kAsThreads) {
       int i, j;
       if (k == 0) {
         decode2(m2, e, i, j);
