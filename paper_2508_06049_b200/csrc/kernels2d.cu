@@ -413,7 +413,12 @@ __device__ double seq_dot(const DevLevel2D& lv, const double* a, const double* b
 // cg_level0 (proj/src/multigrid.cpp:198-229) in one CTA with its vectors, the
 // dot order and the boundary flags staged in shared memory (level 0 has 3 M
 // copies); the arithmetic and the sequential dot order are unchanged.
-__global__ void k_cg0(DevLevel2D lv, double* ug, const double* bg, CgParams prm, DevStatus* status) {
+// With `stage` set, the operator tables apply_node walks (element stiffness
+// per macro, group/member maps) are copied to shared memory too, so every
+// CG iteration's apply reads only shared memory; the values are the same.
+__global__ void k_cg0(DevLevel2D lv_in, double* ug, const double* bg, CgParams prm, DevStatus* status,
+                      int stage) {
+  DevLevel2D lv = lv_in;
   const int total = lv.M * lv.S;
   extern __shared__ __align__(16) double cg_smem[];
   double* u = cg_smem;
@@ -422,14 +427,42 @@ __global__ void k_cg0(DevLevel2D lv, double* ug, const double* bg, CgParams prm,
   double* p = r + total;
   double* ap = p + total;
   double* prod = ap + total;  // the dot products' terms (2 x dot_count)
-  int* dord = reinterpret_cast<int*>(prod + 2 * lv.dot_count);
-  std::uint8_t* flags = reinterpret_cast<std::uint8_t*>(dord + lv.dot_count);
+  double* kst = prod + 2 * lv.dot_count;
+  int* dord = reinterpret_cast<int*>(kst + (stage ? 18 * lv.M : 0));
+  int* tail = dord + lv.dot_count;
   for (int k = threadIdx.x; k < total; k += blockDim.x) {
     u[k] = ug[k];
     b[k] = bg[k];
-    flags[k] = lv.node_flags[k];
   }
   for (int t = threadIdx.x; t < lv.dot_count; t += blockDim.x) dord[t] = lv.dot_order[t];
+  if (stage) {
+    const int G = lv.num_groups;
+    const int nmem = lv.grp_ptr[G];
+    if (nmem > total) __trap();  // the host sized the member arrays by the copy count
+    int* gid = tail;
+    int* gptr = gid + total;
+    int* moff = gptr + G + 1;
+    int* mij = moff + total;
+    int* mslot = mij + total;
+    tail = mslot + total;
+    for (int t = threadIdx.x; t < 18 * lv.M; t += blockDim.x) kst[t] = lv.kstiff[t];
+    for (int k = threadIdx.x; k < total; k += blockDim.x) gid[k] = lv.node_gid[k];
+    for (int g = threadIdx.x; g <= G; g += blockDim.x) gptr[g] = lv.grp_ptr[g];
+    for (int m = threadIdx.x; m < nmem; m += blockDim.x) {
+      moff[m] = lv.mem_off[m];
+      mij[m] = lv.mem_ij[m];
+      mslot[m] = lv.mem_slot[m];
+    }
+    lv.kstiff = kst;
+    lv.node_gid = gid;
+    lv.grp_ptr = gptr;
+    lv.mem_off = moff;
+    lv.mem_ij = mij;
+    lv.mem_slot = mslot;
+  }
+  std::uint8_t* flags = reinterpret_cast<std::uint8_t*>(tail);
+  for (int k = threadIdx.x; k < total; k += blockDim.x) flags[k] = lv.node_flags[k];
+  lv.node_flags = flags;
   __syncthreads();
   const int cnt = lv.dot_count;
   // dot_unique terms in parallel, summed by thread 0 in the sequential order
@@ -1851,8 +1884,12 @@ void launch_cg0(const DevLevel2D& lv0, double* u, const double* b, double* scrat
   const size_t N = static_cast<size_t>(lv0.M) * lv0.S;
   const size_t smem = 5 * N * 8 + static_cast<size_t>(lv0.dot_count) * 20 + N + 16;
   if (smem > 200 * 1024) fail(KB_STRUCTURAL, "coarse mesh too large for the level-0 CG");
-  set_smem(k_cg0, smem);
-  k_cg0<<<1, 256, smem, st>>>(lv0, u, b, prm, status);
+  // staged operator tables: 18 doubles per macro, gid/member maps (<= N each), group pointers
+  const size_t staged = smem + static_cast<size_t>(lv0.M) * 18 * 8 + (4 * N + lv0.num_groups + 1) * 4;
+  static int no_stage = getenv("KB_CG0_STAGE") && getenv("KB_CG0_STAGE")[0] == '0';
+  const int stage = !no_stage && staged <= 200 * 1024;
+  set_smem(k_cg0, stage ? staged : smem);
+  k_cg0<<<1, 256, stage ? staged : smem, st>>>(lv0, u, b, prm, status, stage);
   check_launch("k_cg0");
 }
 
