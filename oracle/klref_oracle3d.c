@@ -641,12 +641,20 @@ static double gauss3_f(double x, double y, double z, const double* p) {
   return (6.0 * 1000.0 - 4.0 * 1000.0 * 1000.0 * r2) * gauss3(x, y, z, p);
 }
 /* sine series: p[0..63] = C_abc (a, b, c = 1..4, a fastest) */
+/* acc += C_abc * ((sin(a pi x) * sin(b pi y)) * sin(c pi z)) in (c, b, a) order; the
+ * twelve sines are formed once per point (the same values, so the same bits
+ * as evaluating them inside the sum) */
 static double series_f(double x, double y, double z, const double* p) {
+  double sx[5], sy[5], sz[5];
+  for (int a = 1; a <= 4; ++a) {
+    sx[a] = sin(a * M_PI * x);
+    sy[a] = sin(a * M_PI * y);
+    sz[a] = sin(a * M_PI * z);
+  }
   double acc = 0.0;
   for (int c = 1; c <= 4; ++c)
     for (int b = 1; b <= 4; ++b)
-      for (int a = 1; a <= 4; ++a)
-        acc += p[(a - 1) + 4 * (b - 1) + 16 * (c - 1)] * (sin(a * M_PI * x) * sin(b * M_PI * y) * sin(c * M_PI * z));
+      for (int a = 1; a <= 4; ++a) acc += p[(a - 1) + 4 * (b - 1) + 16 * (c - 1)] * (sx[a] * sy[b] * sz[c]);
   return acc;
 }
 static double zero3(double x, double y, double z, const double* p) {

@@ -8,6 +8,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <thread>
 
 namespace kb {
 
@@ -254,14 +255,71 @@ void Problem3D::set_params(const double* v, int count) {
   params.assign(v, v + count);
 }
 
-static double series_value(const std::vector<double>& C, double x, double y, double z) {
+// acc += C_abc * ((sin(a pi x) * sin(b pi y)) * sin(c pi z)) in (c, b, a) order;
+// the twelve sines are formed once per point (same values, same bits)
+double series_value(const std::vector<double>& C, double x, double y, double z) {
+  double sx[5], sy[5], sz[5];
+  for (int a = 1; a <= 4; ++a) {
+    sx[a] = std::sin(a * M_PI * x);
+    sy[a] = std::sin(a * M_PI * y);
+    sz[a] = std::sin(a * M_PI * z);
+  }
   double acc = 0.0;
   for (int c = 1; c <= 4; ++c)
     for (int b = 1; b <= 4; ++b)
-      for (int a = 1; a <= 4; ++a)
-        acc += C[(a - 1) + 4 * (b - 1) + 16 * (c - 1)] *
-               (std::sin(a * M_PI * x) * std::sin(b * M_PI * y) * std::sin(c * M_PI * z));
+      for (int a = 1; a <= 4; ++a) acc += C[(a - 1) + 4 * (b - 1) + 16 * (c - 1)] * (sx[a] * sy[b] * sz[c]);
   return acc;
+}
+
+void tabulate_source3(const Hierarchy3D& hh, int l, const Problem3D& p, int s0, int s1, double* out) {
+  const Level3D& lv = hh.levels[l];
+  const int n = lv.n, S = lv.S;
+  std::vector<int> ii(S), jj(S), kk(S);
+  for (int k = 0; k <= n; ++k)
+    for (int j = 0; j <= n - k; ++j)
+      for (int i = 0; i <= n - k - j; ++i) {
+        const int idx = lattice_index3(n, i, j, k);
+        ii[idx] = i, jj[idx] = j, kk[idx] = k;
+      }
+  auto work = [&](int a, int b) {
+    for (int s = a; s < b; ++s)
+      for (int idx = 0; idx < S; ++idx) {
+        const size_t off = static_cast<size_t>(s) * S + idx;
+        int os = s, oidx = idx;
+        const int g = lv.node_gid[off];
+        if (g >= 0) {
+          os = lv.mem_slot[lv.grp_ptr[g]];
+          oidx = lv.mem_idx[lv.grp_ptr[g]];
+        }
+        const auto& t = hh.mesh.tet[os];
+        double x[3];
+        const double P[4][3] = {{hh.mesh.x[t[0]], hh.mesh.y[t[0]], hh.mesh.z[t[0]]},
+                                {hh.mesh.x[t[1]], hh.mesh.y[t[1]], hh.mesh.z[t[1]]},
+                                {hh.mesh.x[t[2]], hh.mesh.y[t[2]], hh.mesh.z[t[2]]},
+                                {hh.mesh.x[t[3]], hh.mesh.y[t[3]], hh.mesh.z[t[3]]}};
+        for (int c = 0; c < 3; ++c)
+          x[c] = P[0][c] + (static_cast<double>(ii[oidx]) / n) * (P[1][c] - P[0][c]) +
+                 (static_cast<double>(jj[oidx]) / n) * (P[2][c] - P[0][c]) +
+                 (static_cast<double>(kk[oidx]) / n) * (P[3][c] - P[0][c]);
+        out[static_cast<size_t>(s - s0) * S + idx] =
+            p.kind == P3_SERIES ? series_value(p.params, x[0], x[1], x[2]) : p.source(x[0], x[1], x[2]);
+      }
+  };
+  const long long nodes = static_cast<long long>(s1 - s0) * S;
+  int nt = static_cast<int>(std::min<long long>(std::max(1u, std::thread::hardware_concurrency()), nodes / 200000 + 1));
+  // host problems wrap caller callbacks (e.g. Python through ctypes): one thread
+  if (p.kind == P3_HOST) nt = 1;
+  if (nt <= 1) {
+    work(s0, s1);
+    return;
+  }
+  std::vector<std::thread> pool;
+  for (int t = 0; t < nt; ++t) {
+    const int a = s0 + static_cast<int>(static_cast<long long>(s1 - s0) * t / nt);
+    const int b = s0 + static_cast<int>(static_cast<long long>(s1 - s0) * (t + 1) / nt);
+    pool.emplace_back(work, a, b);
+  }
+  for (auto& th : pool) th.join();
 }
 
 // ------------------------------------------------------------------ solver
@@ -271,6 +329,8 @@ Solver3D::Solver3D(std::shared_ptr<DeviceHierarchy3D> h, Problem3D p, SolverConf
   L_ = hh.L;
   const int M = hh.M;
   if (cfg_.finest_policy != 0) fail(KB_STRUCTURAL, "only FinestPolicy::None is available on the device path");
+  // host-callback problems have no device form: always tabulated on the host
+  if (prob_.kind == P3_HOST) cfg_.faithful_source = 1;
   has_source_ = prob_.kind != P3_ZERO;
   auto lsize = [&](int l) { return static_cast<size_t>(M) * hh.levels[l].S; };
   size_t bytes = 0;
@@ -306,8 +366,8 @@ Solver3D::Solver3D(std::shared_ptr<DeviceHierarchy3D> h, Problem3D p, SolverConf
   dot_partial_ = static_cast<double*>(arena_.take(64 * 8));
   dot_out_ = static_cast<double*>(arena_.take(8));
   status_ = static_cast<DevStatus*>(arena_.take(sizeof(DevStatus)));
-  double* corners = static_cast<double*>(arena_.take(12 * M * 8));
-  double* params = static_cast<double*>(arena_.take(64 * 8));
+  corners_ = static_cast<double*>(arena_.take(12 * M * 8));
+  params_ = static_cast<double*>(arena_.take(64 * 8));
   KB_CUDA_CHECK(cudaStreamCreateWithFlags(&own_stream_, cudaStreamNonBlocking));
   stream_ = own_stream_;
   KB_CUDA_CHECK(cudaMallocHost(&status_host_, sizeof(DevStatus)));
@@ -322,16 +382,10 @@ Solver3D::Solver3D(std::shared_ptr<DeviceHierarchy3D> h, Problem3D p, SolverConf
       cv[12 * s + 3 * c + 1] = hh.mesh.y[v];
       cv[12 * s + 3 * c + 2] = hh.mesh.z[v];
     }
-  KB_CUDA_CHECK(cudaMemcpy(corners, cv.data(), cv.size() * 8, cudaMemcpyHostToDevice));
-  std::vector<double> par(64, 0.0);
-  if (!prob_.params.empty()) std::copy(prob_.params.begin(), prob_.params.end(), par.begin());
-  KB_CUDA_CHECK(cudaMemcpy(params, par.data(), 64 * 8, cudaMemcpyHostToDevice));
+  KB_CUDA_CHECK(cudaMemcpy(corners_, cv.data(), cv.size() * 8, cudaMemcpyHostToDevice));
   for (int l = 0; l <= L_; ++l) stage_count_ = std::max(stage_count_, std::max(lsize(l), hh.levels[l].grp_ptr.size()));
   KB_CUDA_CHECK(cudaMallocHost(&stage_, stage_count_ * sizeof(double)));
   load_problem(prob_);
-  if (has_source_ && !cfg_.faithful_source) {
-    for (int l = 0; l <= L_; ++l) launch3_ftab(H_->lev[l], corners, prob_.kind, params, ftab_[l], stream_);
-  }
   KB_CUDA_CHECK(cudaStreamSynchronize(stream_));
 }
 
@@ -355,9 +409,6 @@ size_t Solver3D::load_problem(const Problem3D& p) {
   if (&p != &prob_) prob_ = p;
   const Hierarchy3D& hh = H_->host;
   const int M = hh.M;
-  auto src = [&](double x, double y, double z) {
-    return prob_.kind == P3_SERIES ? series_value(prob_.params, x, y, z) : prob_.source(x, y, z);
-  };
   size_t bytes = 0;
   for (int l = 0; l <= L_; ++l) {
     const Level3D& lv = hh.levels[l];
@@ -396,22 +447,19 @@ size_t Solver3D::load_problem(const Problem3D& p) {
     if (has_source_ && cfg_.faithful_source) {
       KB_CUDA_CHECK(cudaStreamSynchronize(stream_));
       const size_t N = level_size(l);
-      for (int s = 0; s < M; ++s)
-        for (int idx = 0; idx < S; ++idx) {
-          const size_t off = static_cast<size_t>(s) * S + idx;
-          int os = s, oidx = idx;
-          const int g = lv.node_gid[off];
-          if (g >= 0) {
-            os = lv.mem_slot[lv.grp_ptr[g]];
-            oidx = lv.mem_idx[lv.grp_ptr[g]];
-          }
-          double x[3];
-          coords(os, ii[oidx], jj[oidx], kk[oidx], x);
-          stage_[off] = src(x[0], x[1], x[2]);
-        }
+      tabulate_source3(hh, l, prob_, 0, M, stage_);
       KB_CUDA_CHECK(cudaMemcpyAsync(ftab_[l], stage_, N * 8, cudaMemcpyHostToDevice, stream_));
       bytes += N * 8;
     }
+  }
+  if (has_source_ && !cfg_.faithful_source) {
+    // fast mode: f from the device tables of the (possibly new) coefficients
+    KB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+    std::fill(stage_, stage_ + 64, 0.0);
+    std::copy(prob_.params.begin(), prob_.params.begin() + std::min<size_t>(64, prob_.params.size()), stage_);
+    KB_CUDA_CHECK(cudaMemcpyAsync(params_, stage_, 64 * 8, cudaMemcpyHostToDevice, stream_));
+    bytes += 64 * 8;
+    for (int l = 0; l <= L_; ++l) launch3_ftab(H_->lev[l], corners_, prob_.kind, params_, ftab_[l], stream_);
   }
   KB_CUDA_CHECK(cudaStreamSynchronize(stream_));
   return bytes;

@@ -33,6 +33,11 @@ struct Problem3D {
   void set_params(const double* p, int count);
 };
 
+// f of problem p per copy of macros [s0, s1) of level l at the owner copy's
+// node coordinates (like proj/src/fem.cpp:183-186, host libm), into out[(s - s0) * S + idx];
+// host threads split the macros (the values do not depend on the split)
+void tabulate_source3(const Hierarchy3D& hh, int l, const Problem3D& p, int s0, int s1, double* out);
+
 class Solver3D {
  public:
   Solver3D(std::shared_ptr<DeviceHierarchy3D> h, Problem3D p, SolverConfig2D cfg);
@@ -97,6 +102,7 @@ class Solver3D {
   DevStatus* status_host_ = nullptr;
   double* sums_host_ = nullptr;
   double* stage_ = nullptr;
+  double *corners_ = nullptr, *params_ = nullptr;  // device: macro corners, series coefficients (fast-mode f)
   std::size_t stage_count_ = 0;
   cudaGraphExec_t exec_ = nullptr;
   int launches_ = 0, fmg_launches_ = 0, est_launches_ = 0;

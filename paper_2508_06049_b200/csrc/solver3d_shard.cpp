@@ -17,15 +17,6 @@ size_t vb(const std::vector<T>& v) {
   return r256(v.size() * sizeof(T));
 }
 
-double series_value(const std::vector<double>& C, double x, double y, double z) {
-  double acc = 0.0;
-  for (int c = 1; c <= 4; ++c)
-    for (int b = 1; b <= 4; ++b)
-      for (int a = 1; a <= 4; ++a)
-        acc += C[(a - 1) + 4 * (b - 1) + 16 * (c - 1)] *
-               (std::sin(a * M_PI * x) * std::sin(b * M_PI * y) * std::sin(c * M_PI * z));
-  return acc;
-}
 }  // namespace
 
 size_t ShardedSolver3D::lsize(const Shard3D& sh, int l) const {
@@ -39,6 +30,8 @@ ShardedSolver3D::ShardedSolver3D(std::shared_ptr<DeviceHierarchy3D> h, Problem3D
   L_ = hh.L;
   M_ = hh.M;
   if (cfg_.finest_policy != 0) fail(KB_STRUCTURAL, "only FinestPolicy::None is available on the device path");
+  // host-callback problems have no device form: always tabulated on the host
+  if (prob_.kind == P3_HOST) cfg_.faithful_source = 1;
   P_ = comm_ ? comm_->size() : nshards;
   if (P_ < 1 || P_ > M_) fail(KB_STRUCTURAL, "shard count must be in [1, number of macro elements]");
   rep_ = std::min(std::max(rep_level, 0), L_);
@@ -179,9 +172,6 @@ ShardedSolver3D::~ShardedSolver3D() {
 // node coordinates -- the tables Solver3D::load_problem builds, sliced per shard
 void ShardedSolver3D::load_problem() {
   const Hierarchy3D& hh = H_->host;
-  auto src = [&](double x, double y, double z) {
-    return prob_.kind == P3_SERIES ? series_value(prob_.params, x, y, z) : prob_.source(x, y, z);
-  };
   for (int l = 0; l <= L_; ++l) {
     const Level3D& lv = hh.levels[l];
     const int n = lv.n, S = lv.S;
@@ -223,19 +213,7 @@ void ShardedSolver3D::load_problem() {
       if (has_source_ && cfg_.faithful_source) {
         const int s0 = off(sh, l), cnt = mloc(sh, l);
         std::vector<double> f(static_cast<size_t>(cnt) * S);
-        for (int s = s0; s < s0 + cnt; ++s)
-          for (int idx = 0; idx < S; ++idx) {
-            const size_t o = static_cast<size_t>(s) * S + idx;
-            int os = s, oidx = idx;
-            const int gq = lv.node_gid[o];
-            if (gq >= 0) {
-              os = lv.mem_slot[lv.grp_ptr[gq]];
-              oidx = lv.mem_idx[lv.grp_ptr[gq]];
-            }
-            double x[3];
-            coords(os, oidx, x);
-            f[static_cast<size_t>(s - s0) * S + idx] = src(x[0], x[1], x[2]);
-          }
+        tabulate_source3(hh, l, prob_, s0, s0 + cnt, f.data());
         KB_CUDA_CHECK(cudaMemcpy(sh.ftab[l], f.data(), f.size() * 8, cudaMemcpyHostToDevice));
       }
     }
