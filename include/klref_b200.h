@@ -85,7 +85,8 @@ typedef struct klref_solver_s* klref_solver;
 typedef struct klref_gf_s* klref_gf;
 
 /* SolverConfig, proj/include/klref/multigrid.hpp:19-29 (finest_policy: 0 = None,
- * 1 = ValidationTwoDigits on 2-d hierarchies; the reference default is 1) */
+ * 1 = ValidationTwoDigits, 2 = ResidualVsEstimate, both on 2-d hierarchies;
+ * the reference default is 1) */
 typedef struct {
   int nu;
   int pre_smooth;
@@ -200,8 +201,15 @@ int klref_solver_state_read(klref_solver s, int which, int level, double* host_o
 /* ExactErrorEvaluator(h, p, L).evaluate(u_L), proj/src/fem.cpp:358-420 (three-term
  * moment form, pointwise fallback :422-455); per_macro[M] may be NULL (2-d) */
 int klref_solver_exact_error(klref_solver s, double* global, double* per_macro);
-/* FmgState::extra_cycles of the last fmg() (FinestPolicy::ValidationTwoDigits) */
+/* ExactErrorEvaluator(h, p, L).evaluate(u) of a level-L function u (the solver's
+ * finest level), proj/src/fem.cpp:395-420; 2-d */
+int klref_solver_exact_error_of(klref_solver s, klref_gf u, double* global, double* per_macro);
+/* FmgState::extra_cycles of the last fmg() (FinestPolicy::ValidationTwoDigits / ResidualVsEstimate) */
 int klref_solver_extra_cycles(klref_solver s, int* out);
+/* MultigridSolver::solve_direct(l), proj/src/multigrid.cpp:323-357: level_rhs(l), u = g
+ * on the boundary, then cg_level0 (l = 0) or the reference's level-l CG; result into u
+ * (a level-l function of the solver's hierarchy); 2-d */
+int klref_solver_solve_direct(klref_solver s, int level, klref_gf u);
 
 /* error_estimate(state, j, kind), proj/src/estimator.cpp:8-45; eta_local[M] may be NULL */
 int klref_error_estimate(klref_solver s, int offset, int kind, klref_estimate_report* out, double* eta_local);

@@ -1,11 +1,16 @@
 // klref_b200/klref.hpp -- C++ drop-in facade of the reference hot-path API
-// (proj/include/klref/{errors,hhg,fem,multigrid,estimator}.hpp) over the
-// C-ABI of libklref_b200.so (include/klref_b200.h).  Header-only; link with
-// -lklref_b200.
+// (proj/include/klref/{hhg,fem,multigrid,estimator}.hpp) over the C-ABI of
+// libklref_b200.so (include/klref_b200.h).  Header-only; link with -lklref_b200.
 //
 // Source compatibility with the reference's callers (proj/src/amr.cpp) is the
 // goal: the same namespace, class and function names, argument meaning and
-// exception types.  Differences, all forced by the device design:
+// exception types.  Put include/klref_b200/dropin first on the include path
+// and the reference's own headers after it: "klref/{hhg,fem,multigrid,
+// estimator}.hpp" then resolve to this facade, while the reference's
+// macro_mesh.hpp / errors.hpp / amr.hpp / mesh_io.hpp / problems.hpp stay the
+// reference's (the exception classes and Point / Index are the reference's
+// own when its headers are visible; identical definitions otherwise).
+// Differences, all forced by the device design:
 //   * GridHierarchy::build is a template over the mesh type: any type with the
 //     accessors of the reference MacroMesh that the hot path reads -- dim(),
 //     num_vertices(), vertex(id).coords, active(), element(id).v
@@ -17,9 +22,8 @@
 //   * FmgState's u / b / w are views of the solver's device state, copied to
 //     the host on access (the reference copies them by value); running fmg()
 //     again on the same solver updates them;
-//   * only FinestPolicy::None runs on the device (the policy of the timed
-//     runs); the validation policies need ExactErrorEvaluator (not yet on
-//     the device) and raise StructuralError.
+//   * ExactErrorEvaluator evaluates functions of its hierarchy's finest level
+//     (the reference's callers only use that level).
 #ifndef KLREF_B200_KLREF_HPP
 #define KLREF_B200_KLREF_HPP
 
@@ -38,32 +42,54 @@
 namespace klref {
 
 // ---------------------------------------------------------------- errors
-// proj/include/klref/errors.hpp:10-53
-struct Error : std::runtime_error {
-  using std::runtime_error::runtime_error;
+// proj/include/klref/errors.hpp:10-53; Point / Index, proj/include/klref/macro_mesh.hpp:16-19
+}  // namespace klref
+#if __has_include("klref/macro_mesh.hpp")
+#include "klref/macro_mesh.hpp"  // the reference's errors.hpp, Index, Point
+namespace klref {
+#else
+#include <stdexcept>
+namespace klref {
+using Index = std::int32_t;
+inline constexpr Index kNoIndex = -1;
+using Point = std::array<double, 3>;
+class StructuralError : public std::runtime_error {
+ public:
+  explicit StructuralError(const std::string& what) : std::runtime_error(what) {}
 };
-struct StructuralError : Error {
-  using Error::Error;
+class DomainError : public std::domain_error {
+ public:
+  explicit DomainError(const std::string& what) : std::domain_error(what) {}
 };
-struct DomainError : Error {
-  using Error::Error;
+class SolverError : public std::runtime_error {
+ public:
+  SolverError(const std::string& what, double last_residual) : std::runtime_error(what), last_(last_residual) {}
+  double last_residual() const { return last_; }
+
+ private:
+  double last_ = 0.0;
 };
-struct SolverError : Error {
-  SolverError(const std::string& what, double last) : Error(what), last_residual(last) {}
-  double last_residual = 0.0;
+class IoError : public std::runtime_error {
+ public:
+  explicit IoError(const std::string& what) : std::runtime_error(what) {}
 };
-struct IoError : Error {
-  using Error::Error;
+class InternalError : public std::logic_error {
+ public:
+  explicit InternalError(const std::string& what) : std::logic_error(what) {}
 };
-struct InternalError : Error {
-  using Error::Error;
+class ResourceError : public std::runtime_error {
+ public:
+  ResourceError(const std::string& what, int level) : std::runtime_error(what), level_(level) {}
+  int level() const { return level_; }
+
+ private:
+  int level_ = -1;
 };
-struct ResourceError : Error {
-  ResourceError(const std::string& what, int lvl) : Error(what), level(lvl) {}
-  int level = -1;
-};
-struct DeviceError : Error {  // CUDA failure or no device (no reference counterpart)
-  using Error::Error;
+#endif
+// CUDA failure or no device (no reference counterpart)
+class DeviceError : public std::runtime_error {
+ public:
+  explicit DeviceError(const std::string& what) : std::runtime_error(what) {}
 };
 
 namespace detail {
@@ -315,11 +341,11 @@ struct ProblemSpec {
   std::function<double(double, double)> boundary;
   bool has_exact = true;
   bool has_corner = false;
-  std::array<double, 3> corner{0.0, 0.0, 0.0};
+  Point corner{0.0, 0.0, 0.0};
   double domain_volume = 1.0;
 };
 
-// ---------------------------------------------------------------- multigrid.hpp
+// ---------------------------------------------------------------- multigrid.hpp: config
 struct SolverConfig {
   int nu = 2;
   int pre_smooth = 2;
@@ -327,11 +353,80 @@ struct SolverConfig {
   double coarse_rel_tol = 1e-9;
   double coarse_abs_floor = 1e-12;
   int coarse_max_iter = 100000;
-  FinestPolicy finest_policy = FinestPolicy::ValidationTwoDigits;  // reference default; set None for the device
+  FinestPolicy finest_policy = FinestPolicy::ValidationTwoDigits;  // the reference default
   int max_extra_cycles = 60;
   bool record_residuals = false;
 };
 
+// ---------------------------------------------------------------- fem.hpp: exact error
+struct ErrorNorms {
+  double global = 0.0;
+  std::vector<double> per_macro;
+};
+
+namespace detail {
+struct HostProblem {
+  std::function<double(double, double)> source, boundary, exact;
+};
+inline double src_cb(double x, double y, void* p) { return static_cast<HostProblem*>(p)->source(x, y); }
+inline double bnd_cb(double x, double y, void* p) { return static_cast<HostProblem*>(p)->boundary(x, y); }
+inline double exact_cb(double x, double y, void* p) { return static_cast<HostProblem*>(p)->exact(x, y); }
+using SolverHandle = std::shared_ptr<Handle<klref_solver, klref_solver_destroy>>;
+// a device solver for the host problem p; the callbacks' owner (hp) must
+// outlive it, so it is shared with whoever keeps the solver
+inline SolverHandle make_solver(klref_hierarchy h, const ProblemSpec& p, const klref_solver_config& c,
+                                std::shared_ptr<HostProblem>& hp) {
+  hp = std::make_shared<HostProblem>(HostProblem{p.source, p.boundary, p.exact});
+  klref_problem prob = nullptr;
+  check(klref_problem_create_host(src_cb, bnd_cb, hp.get(), &prob));
+  Handle<klref_problem, klref_problem_destroy> hprob(prob);
+  if (p.has_exact && p.exact) check(klref_problem_set_exact(prob, exact_cb, hp.get()));
+  klref_solver s = nullptr;
+  check(klref_solver_create(h, prob, &c, &s));
+  return std::make_shared<Handle<klref_solver, klref_solver_destroy>>(s);
+}
+}  // namespace detail
+
+// ExactErrorEvaluator (proj/include/klref/fem.hpp:101-114, proj/src/fem.cpp:358-476):
+// ||u - u_h|| by the 6-point rule in the reference's three-term moment form
+// (pointwise fallback on cancellation); moments tabulated on the host, the
+// per-macro sums on the device.  `level` must be the hierarchy's finest level.
+class ExactErrorEvaluator {
+ public:
+  ExactErrorEvaluator(HierarchyPtr h, const ProblemSpec& p, int level) : h_(std::move(h)), level_(level) {
+    if (level_ != h_->max_level())
+      throw StructuralError("ExactErrorEvaluator: the device evaluator works on the hierarchy's finest level");
+    if (!p.has_exact || !p.exact) throw StructuralError("the problem has no closed-form solution");
+    klref_solver_config c;
+    klref_solver_config_default(&c);
+    c.finest_policy = 0;
+    c.faithful_source = 1;
+    s_ = detail::make_solver(h_->handle(), p, c, hp_);
+  }
+  ErrorNorms evaluate(const GridFunction& u_h) const {
+    if (u_h.level() != level_) throw StructuralError("ExactErrorEvaluator: level mismatch");
+    ErrorNorms out;
+    out.per_macro.assign(static_cast<std::size_t>(h_->num_macros()), 0.0);
+    detail::check(klref_solver_exact_error_of(s_->h, u_h.device(), &out.global, out.per_macro.data()));
+    return out;
+  }
+
+ private:
+  friend class MultigridSolver;
+  ExactErrorEvaluator(HierarchyPtr h, int level, detail::SolverHandle s, std::shared_ptr<detail::HostProblem> hp)
+      : h_(std::move(h)), level_(level), s_(std::move(s)), hp_(std::move(hp)) {}
+  HierarchyPtr h_;
+  int level_;
+  detail::SolverHandle s_;
+  std::shared_ptr<detail::HostProblem> hp_;
+};
+
+// exact_error_norm(p, u_h), proj/include/klref/fem.hpp:116
+inline ErrorNorms exact_error_norm(const ProblemSpec& p, const GridFunction& u_h) {
+  return ExactErrorEvaluator(u_h.hierarchy(), p, u_h.level()).evaluate(u_h);
+}
+
+// ---------------------------------------------------------------- multigrid.hpp
 class MultigridSolver;
 
 // FmgState (proj/include/klref/multigrid.hpp:43-53): views of the solver's
@@ -340,8 +435,7 @@ class FmgState {
  public:
   class Levels {
    public:
-    Levels(std::shared_ptr<detail::Handle<klref_solver, klref_solver_destroy>> s, HierarchyPtr h, int which,
-           int count, int shift)
+    Levels(detail::SolverHandle s, HierarchyPtr h, int which, int count, int shift)
         : s_(std::move(s)), h_(std::move(h)), which_(which), count_(count), shift_(shift) {}
     std::size_t size() const { return static_cast<std::size_t>(count_); }
     GridFunction operator[](std::size_t l) const {
@@ -355,7 +449,7 @@ class FmgState {
     GridFunction back() const { return (*this)[size() - 1]; }
 
    private:
-    std::shared_ptr<detail::Handle<klref_solver, klref_solver_destroy>> s_;
+    detail::SolverHandle s_;
     HierarchyPtr h_;
     int which_, count_, shift_;
   };
@@ -364,43 +458,26 @@ class FmgState {
   SolverConfig config;
   Levels u, b, w;
   int extra_cycles = 0;
-  std::shared_ptr<const void> error_eval;  // unused: exact_error_norm(state) evaluates on the device
+  std::shared_ptr<const ExactErrorEvaluator> error_eval;  // set in validation mode (problem with exact)
 
  private:
   friend class MultigridSolver;
   friend struct EstimateAccess;
-  FmgState(std::shared_ptr<detail::Handle<klref_solver, klref_solver_destroy>> s, HierarchyPtr hh,
-           SolverConfig cfg)
+  FmgState(detail::SolverHandle s, HierarchyPtr hh, SolverConfig cfg)
       : h(hh),
         config(cfg),
         u(s, hh, KLREF_STATE_U, hh->max_level() + 1, 0),
         b(s, hh, KLREF_STATE_B, hh->max_level() + 1, 0),
         w(s, hh, KLREF_STATE_W, hh->max_level(), 1),
         solver_(std::move(s)) {}
-  std::shared_ptr<detail::Handle<klref_solver, klref_solver_destroy>> solver_;
+  detail::SolverHandle solver_;
 };
-
-namespace detail {
-struct HostProblem {
-  std::function<double(double, double)> source, boundary, exact;
-};
-inline double src_cb(double x, double y, void* p) { return static_cast<HostProblem*>(p)->source(x, y); }
-inline double bnd_cb(double x, double y, void* p) { return static_cast<HostProblem*>(p)->boundary(x, y); }
-inline double exact_cb(double x, double y, void* p) { return static_cast<HostProblem*>(p)->exact(x, y); }
-}  // namespace detail
 
 class MultigridSolver {
  public:
   // MultigridSolver(h, p, cfg), proj/src/multigrid.cpp:113-119.  Like the
   // reference, p is not owned; f and g are tabulated here.
   MultigridSolver(HierarchyPtr h, const ProblemSpec& p, SolverConfig cfg) : h_(std::move(h)), p_(&p), cfg_(cfg) {
-    if (cfg.finest_policy == FinestPolicy::ResidualVsEstimate)
-      throw StructuralError("FinestPolicy::ResidualVsEstimate does not run on the device");
-    hp_ = std::make_unique<detail::HostProblem>(detail::HostProblem{p.source, p.boundary, p.exact});
-    klref_problem prob = nullptr;
-    detail::check(klref_problem_create_host(detail::src_cb, detail::bnd_cb, hp_.get(), &prob));
-    detail::Handle<klref_problem, klref_problem_destroy> hprob(prob);
-    if (p.has_exact && p.exact) detail::check(klref_problem_set_exact(prob, detail::exact_cb, hp_.get()));
     klref_solver_config c;
     klref_solver_config_default(&c);
     c.nu = cfg.nu;
@@ -409,23 +486,33 @@ class MultigridSolver {
     c.coarse_rel_tol = cfg.coarse_rel_tol;
     c.coarse_abs_floor = cfg.coarse_abs_floor;
     c.coarse_max_iter = cfg.coarse_max_iter;
-    c.finest_policy = cfg.finest_policy == FinestPolicy::ValidationTwoDigits ? 1 : 0;
+    c.finest_policy = cfg.finest_policy == FinestPolicy::ValidationTwoDigits  ? 1
+                      : cfg.finest_policy == FinestPolicy::ResidualVsEstimate ? 2
+                                                                              : 0;
     c.max_extra_cycles = cfg.max_extra_cycles;
     c.faithful_source = 1;
-    klref_solver s = nullptr;
-    detail::check(klref_solver_create(h_->handle(), prob, &c, &s));
-    s_ = std::make_shared<detail::Handle<klref_solver, klref_solver_destroy>>(s);
+    s_ = detail::make_solver(h_->handle(), p, c, hp_);
   }
   const HierarchyPtr& hierarchy() const { return h_; }
   const ProblemSpec& problem() const { return *p_; }
   const SolverConfig& config() const { return cfg_; }
 
-  // MultigridSolver::fmg, proj/src/multigrid.cpp:248-321
+  // MultigridSolver::fmg, proj/src/multigrid.cpp:248-321 (finest-level policy included)
   FmgState fmg() {
     detail::check(klref_solver_fmg(s_->h));
     FmgState st(s_, h_, cfg_);
     detail::check(klref_solver_extra_cycles(s_->h, &st.extra_cycles));
+    if (cfg_.finest_policy == FinestPolicy::ValidationTwoDigits && p_->has_exact && p_->exact)
+      st.error_eval = std::shared_ptr<const ExactErrorEvaluator>(
+          new ExactErrorEvaluator(h_, h_->max_level(), s_, hp_));
     return st;
+  }
+  // MultigridSolver::solve_direct(l), proj/src/multigrid.cpp:323-357
+  GridFunction solve_direct(int l) {
+    GridFunction u(h_, l);
+    detail::check(klref_solver_solve_direct(s_->h, l, u.device()));
+    u.device_written();
+    return u;
   }
   // single operations, proj/src/multigrid.cpp:127-229
   void gauss_seidel(int l, GridFunction& u, const GridFunction& b, int sweeps) {
@@ -448,8 +535,8 @@ class MultigridSolver {
   HierarchyPtr h_;
   const ProblemSpec* p_;
   SolverConfig cfg_;
-  std::unique_ptr<detail::HostProblem> hp_;
-  std::shared_ptr<detail::Handle<klref_solver, klref_solver_destroy>> s_;
+  std::shared_ptr<detail::HostProblem> hp_;
+  detail::SolverHandle s_;
   friend struct EstimateAccess;
 };
 
@@ -503,22 +590,6 @@ inline EstimateReport error_estimate(const FmgState& state, int offset, Estimato
   out.norm_base = r.norm_base;
   out.conv_factor = r.conv_factor;
   out.eta = r.eta;
-  return out;
-}
-
-// ---------------------------------------------------------------- fem.hpp (validation)
-struct ErrorNorms {
-  double global = 0.0;
-  std::vector<double> per_macro;
-};
-
-// exact_error_norm(p, state.u.back()), proj/src/fem.cpp:358-476: the
-// ExactErrorEvaluator of the state's finest level (the solver's problem must
-// carry `exact`; 2-d)
-inline ErrorNorms exact_error_norm(const FmgState& state) {
-  ErrorNorms out;
-  out.per_macro.assign(static_cast<std::size_t>(state.h->num_macros()), 0.0);
-  detail::check(klref_solver_exact_error(EstimateAccess::solver(state), &out.global, out.per_macro.data()));
   return out;
 }
 

@@ -19,6 +19,8 @@
 //   ref_driver ops   <mesh> <L> <seed> <outdir>
 //   ref_driver time  <mesh> <sin|lshape> <L> <nu> <reps> [budget_s]
 //   ref_driver solvevtd <mesh> <sin|lshape> <L> <nu> <outdir>   (FinestPolicy::ValidationTwoDigits)
+//   ref_driver solverve <mesh> <sin|lshape> <L> <nu> <l_direct> <outdir>
+//       (FinestPolicy::ResidualVsEstimate; solve_direct(0) and solve_direct(l_direct))
 //   ref_driver bounds      (stdin: "theta eps offset" lines -> effectivity_constants,
 //                          local spread bounds, make_bounds order; "ERR" on DomainError)
 //   ref_driver effidx <file>  (eta, n, eta_local[n], exact global, m, exact per_macro[m]
@@ -415,6 +417,29 @@ int cmd_solvevtd(int argc, char** argv) {
   return 0;
 }
 
+// FinestPolicy::ResidualVsEstimate (proj/src/multigrid.cpp:294-319) and
+// MultigridSolver::solve_direct(l) (proj/src/multigrid.cpp:323-357) on the same mesh
+int cmd_solverve(int argc, char** argv) {
+  if (argc < 8) return 2;
+  const MacroMesh mesh = read_mesh_file(argv[2]);
+  const ProblemSpec p = make_problem(argv[3]);
+  const int L = std::atoi(argv[4]), nu = std::atoi(argv[5]), ld = std::atoi(argv[6]);
+  const std::string outdir = argv[7];
+  std::filesystem::create_directories(outdir);
+  SolverConfig sc;
+  sc.nu = nu;
+  sc.finest_policy = FinestPolicy::ResidualVsEstimate;
+  auto h = GridHierarchy::build(mesh, L);
+  MultigridSolver solver(h, p, sc);
+  FmgState st = solver.fmg();
+  dump(st.u[L], outdir + "/u_" + std::to_string(L) + ".bin");
+  for (int l : {0, ld}) dump(solver.solve_direct(l), outdir + "/direct_" + std::to_string(l) + ".bin");
+  std::ostringstream r;
+  r << "extra_cycles " << st.extra_cycles << "\n";
+  write_text(outdir + "/report.txt", r.str());
+  return 0;
+}
+
 int cmd_ops(int argc, char** argv) {
   if (argc < 6) return 2;
   const MacroMesh mesh = read_mesh_file(argv[2]);
@@ -617,6 +642,7 @@ int main(int argc, char** argv) {
     }
     if (cmd == "solve") return cmd_solve(argc, argv);
     if (cmd == "amr") return cmd_amr(argc, argv);
+    if (cmd == "solverve") return cmd_solverve(argc, argv);
     if (cmd == "ops") return cmd_ops(argc, argv);
     if (cmd == "amr3d") return cmd_amr3d(argc, argv);
     if (cmd == "solvevtd") return cmd_solvevtd(argc, argv);

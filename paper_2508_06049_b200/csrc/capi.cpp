@@ -482,6 +482,26 @@ int klref_solver_exact_error(klref_solver s, double* global, double* per_macro) 
     if (per_macro) std::copy(e.per_macro.begin(), e.per_macro.end(), per_macro);
   });
 }
+int klref_solver_exact_error_of(klref_solver s, klref_gf u, double* global, double* per_macro) {
+  return guarded([&] {
+    need(s, "solver");
+    same_hier(s, u);
+    if (!s->s) kb::fail(kb::KB_STRUCTURAL, "the exact-error evaluator is defined for 2-d hierarchies");
+    if (u->level != s->s->hier().L) kb::fail(kb::KB_STRUCTURAL, "the exact-error evaluator works on the finest level");
+    const auto e = s->s->exact_error(u->d);
+    if (global) *global = e.global;
+    if (per_macro) std::copy(e.per_macro.begin(), e.per_macro.end(), per_macro);
+  });
+}
+int klref_solver_solve_direct(klref_solver s, int level, klref_gf u) {
+  return guarded([&] {
+    need(s, "solver");
+    same_hier(s, u);
+    if (!s->s) kb::fail(kb::KB_STRUCTURAL, "solve_direct is defined for 2-d hierarchies");
+    if (u->level != level) kb::fail(kb::KB_STRUCTURAL, "grid function level mismatch");
+    s->s->solve_direct(level, u->d);
+  });
+}
 int klref_solver_extra_cycles(klref_solver s, int* out) {
   return guarded([&] {
     need(s, "solver");

@@ -122,8 +122,12 @@ void launch_estimate(const DevLevel2D& lv, const double* uL, const double* wb, c
                      double* sums, cudaStream_t st);
 void launch_dot(const DevLevel2D& lv, const double* a, const double* b, double* partial,
                 double* out, cudaStream_t st);
+// dot_unique in the reference's sequential owner order (single warp)
+void launch_dot_seq(const DevLevel2D& lv, const double* a, const double* b, double* out, cudaStream_t st);
 void launch_sync(const DevLevel2D& lv, double* f, int additive, cudaStream_t st);
 void launch_axpy(double* y, const double* x, double alpha, std::int64_t count, cudaStream_t st);
+// y = y * beta; y = y + 1.0 * x  (GridFunction::scale then add_scaled(x, 1.0))
+void launch_scale_add(double* y, double beta, const double* x, std::int64_t count, cudaStream_t st);
 int gs_block_threads(int n);
 
 }  // namespace kb

@@ -190,8 +190,7 @@ Solver2D::Solver2D(std::shared_ptr<DeviceHierarchy2D> h, Problem2D p, SolverConf
   const Hierarchy2D& hh = H_->host;
   L_ = hh.L;
   const int M = hh.M;
-  if (cfg_.finest_policy != 0 && cfg_.finest_policy != 1)
-    fail(KB_STRUCTURAL, "FinestPolicy::ResidualVsEstimate is not available on the device path");
+  if (cfg_.finest_policy < 0 || cfg_.finest_policy > 2) fail(KB_STRUCTURAL, "unknown finest-level policy");
   if (prob_.kind == PROB_ZERO || prob_.kind == PROB_LSHAPE)
     src_kind_ = SRC_ZERO;
   else if (prob_.kind == PROB_SIN2D && !cfg_.faithful_source)
@@ -549,7 +548,115 @@ void Solver2D::fmg() {
       if (cur == prev) break;
       prev = cur;
     }
+  } else if (cfg_.finest_policy == 2) {
+    finest_residual_vs_estimate();
   }
+}
+
+double* Solver2D::scratch(int slot, int level) {
+  if (scr_level_ != level) {
+    scr_arena_ = std::make_unique<DeviceArena>();
+    scr_arena_->reserve(4 * (level_size(level) * 8 + 256) + 256);
+    scr_.assign(4, nullptr);
+    for (auto& p : scr_) p = static_cast<double*>(scr_arena_->take(level_size(level) * 8));
+    scr_level_ = level;
+  }
+  return scr_.at(slot);
+}
+
+// l2_norm (proj/src/fem.cpp:320-325): sqrt(max(0, dot_unique(f, M f)))
+double Solver2D::l2_norm_mass(int level, const double* f, double* tmp) {
+  const auto& lv = H_->lev[level];
+  launch_apply(lv, lv.kmass, f, tmp, nullptr, APPLY_PLAIN, stream_);
+  return std::sqrt(std::max(0.0, dot_unique(level, f, tmp)));
+}
+
+// FinestPolicy::ResidualVsEstimate, proj/src/multigrid.cpp:294-319: eta_1 from
+// the stored coarse solutions, then extra finest V-cycles until the mass norm
+// of the update falls below 1e-2 eta_1
+void Solver2D::finest_residual_vs_estimate() {
+  const auto& lev = H_->lev;
+  const size_t N = level_size(L_);
+  double* e = scratch(0, L_);
+  double* mf = scratch(1, L_);
+  double* before = scratch(2, L_);
+  double* pc = scratch(3, L_);
+  double eta1 = 0.0;
+  if (L_ >= 2) {
+    // e_fine = u_L + (-1) w[L-1]
+    KB_CUDA_CHECK(cudaMemcpyAsync(e, u_[L_], N * 8, cudaMemcpyDeviceToDevice, stream_));
+    launch_axpy(e, w_[L_ - 1], -1.0, static_cast<std::int64_t>(N), stream_);
+    const double n_fine = l2_norm_mass(L_, e, mf);
+    // e_coarse = u_L + (-1) prolongate_to(w[L-2], L) (w[L-2] lives on level L-1)
+    launch_prolong(lev[L_ - 1], lev[L_], w_[L_ - 2], pc, nullptr, nullptr, PROLONG_ASSIGN, stream_);
+    KB_CUDA_CHECK(cudaMemcpyAsync(e, u_[L_], N * 8, cudaMemcpyDeviceToDevice, stream_));
+    launch_axpy(e, pc, -1.0, static_cast<std::int64_t>(N), stream_);
+    const double n_coarse = l2_norm_mass(L_, e, mf);
+    eta1 = n_coarse > 0.0 ? (n_fine / n_coarse) * n_fine : 0.0;
+  }
+  for (int extra = 0; extra < cfg_.max_extra_cycles; ++extra) {
+    KB_CUDA_CHECK(cudaMemcpyAsync(before, u_[L_], N * 8, cudaMemcpyDeviceToDevice, stream_));
+    vcycle(L_, u_[L_], b_[L_]);
+    sync_and_check();
+    ++extra_cycles_;
+    // delta = u_L + (-1) before
+    KB_CUDA_CHECK(cudaMemcpyAsync(e, u_[L_], N * 8, cudaMemcpyDeviceToDevice, stream_));
+    launch_axpy(e, before, -1.0, static_cast<std::int64_t>(N), stream_);
+    const double update = l2_norm_mass(L_, e, mf);
+    const double target = eta1 > 0.0 ? 1e-2 * eta1 : 1e-10 * std::max(1.0, l2_norm_mass(L_, u_[L_], mf));
+    if (update < target) break;
+  }
+}
+
+// dot_unique with the reference's sequential summation order (solve_direct's
+// level CG: its iterates are compared bit for bit)
+double Solver2D::dot_seq(int level, const double* a, const double* b) {
+  launch_dot_seq(H_->lev.at(level), a, b, dot_out_, stream_);
+  double out = 0.0;
+  KB_CUDA_CHECK(cudaMemcpyAsync(&out, dot_out_, 8, cudaMemcpyDeviceToHost, stream_));
+  KB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+  return out;
+}
+
+void Solver2D::solve_direct(int l, double* u) {
+  if (l < 0 || l > L_) fail(KB_STRUCTURAL, "level out of range");
+  const auto& lev = H_->lev;
+  const auto& lv = lev[l];
+  // b = level_rhs(l); u = g on the domain boundary, 0 elsewhere
+  launch_rhs(lv, src_kind_, ftab_[l], ftab_[l], gbnd_[l], b_[l], stream_);
+  launch_set_boundary(lv, u, gbnd_[l], 1, stream_);
+  if (l == 0) {
+    KB_CUDA_CHECK(cudaMemsetAsync(status_, 0, sizeof(DevStatus), stream_));
+    launch_cg0(lv, u, b_[0], cg_scratch_, {cfg_.coarse_rel_tol, cfg_.coarse_abs_floor, cfg_.coarse_max_iter},
+               status_, stream_);
+    sync_and_check();
+    return;
+  }
+  const size_t N = level_size(l);
+  const std::int64_t n64 = static_cast<std::int64_t>(N);
+  double* r = scratch(0, l);
+  double* p = scratch(1, l);
+  double* ap = scratch(2, l);
+  launch_apply(lv, lv.kstiff, u, r, b_[l], APPLY_RESIDUAL, stream_);
+  KB_CUDA_CHECK(cudaMemcpyAsync(p, r, N * 8, cudaMemcpyDeviceToDevice, stream_));
+  double rr = dot_seq(l, r, r);
+  const double tol = std::max(cfg_.coarse_rel_tol * std::sqrt(rr), cfg_.coarse_abs_floor);
+  int it = 0;
+  while (std::sqrt(rr) > tol && it < cfg_.coarse_max_iter) {
+    ++it;
+    // ap = A p, zero domain boundary (apply + zero_domain_boundary)
+    launch_apply(lv, lv.kstiff, p, ap, nullptr, APPLY_ZERO_BND, stream_);
+    const double pap = dot_seq(l, p, ap);
+    if (pap <= 0.0) break;
+    const double alpha = rr / pap;
+    launch_axpy(u, p, alpha, n64, stream_);
+    launch_axpy(r, ap, -alpha, n64, stream_);
+    const double rr_new = dot_seq(l, r, r);
+    // p.scale(rr_new / rr); p.add_scaled(r, 1.0)
+    launch_scale_add(p, rr_new / rr, r, n64, stream_);
+    rr = rr_new;
+  }
+  KB_CUDA_CHECK(cudaStreamSynchronize(stream_));
 }
 
 // ExactErrorEvaluator constructor, proj/src/fem.cpp:358-392: moments of the
@@ -603,10 +710,10 @@ void Solver2D::exact_setup() {
 
 // ExactErrorEvaluator::evaluate, proj/src/fem.cpp:395-420 (device per-macro
 // terms, host sums in slot order, pointwise fallback on cancellation)
-Solver2D::ExactNorms Solver2D::exact_error() {
+Solver2D::ExactNorms Solver2D::exact_error(const double* u) {
   exact_setup();
   const int M = H_->host.M;
-  launch_exact_eval(H_->lev[L_], u_[L_], ex_moments_, ex_out_, stream_);
+  launch_exact_eval(H_->lev[L_], u ? u : u_[L_], ex_moments_, ex_out_, stream_);
   std::vector<double> terms(2 * static_cast<size_t>(M));
   KB_CUDA_CHECK(cudaMemcpyAsync(terms.data(), ex_out_, terms.size() * 8, cudaMemcpyDeviceToHost, stream_));
   KB_CUDA_CHECK(cudaStreamSynchronize(stream_));
@@ -619,7 +726,7 @@ Solver2D::ExactNorms Solver2D::exact_error() {
     total += e2;
     scale += ex_usq_[s] + terms[2 * s + 1];
   }
-  if (total < 1e-12 * scale) return exact_pointwise();  // proj/src/fem.cpp:416-417
+  if (total < 1e-12 * scale) return exact_pointwise(u);  // proj/src/fem.cpp:416-417
   for (double& v : out.per_macro) v = std::sqrt(std::max(0.0, v));
   out.global = std::sqrt(std::max(0.0, total));
   return out;
@@ -627,11 +734,11 @@ Solver2D::ExactNorms Solver2D::exact_error() {
 
 // ExactErrorEvaluator::evaluate_pointwise, proj/src/fem.cpp:422-455 (host,
 // the cancellation fallback)
-Solver2D::ExactNorms Solver2D::exact_pointwise() {
+Solver2D::ExactNorms Solver2D::exact_pointwise(const double* ud) {
   const Hierarchy2D& hh = H_->host;
   const int M = hh.M, n = hh.levels[L_].n, S = hh.levels[L_].S;
   std::vector<double> u(static_cast<size_t>(M) * S);
-  KB_CUDA_CHECK(cudaMemcpy(u.data(), u_[L_], u.size() * 8, cudaMemcpyDeviceToHost));
+  KB_CUDA_CHECK(cudaMemcpy(u.data(), ud ? ud : u_[L_], u.size() * 8, cudaMemcpyDeviceToHost));
   constexpr double kQa = 0.445948490915965, kQwa = 0.223381589678011;
   constexpr double kQb = 0.091576213509771, kQwb = 0.109951743655322;
   const double quad[6][4] = {{1 - 2 * kQa, kQa, kQa, kQwa}, {kQa, 1 - 2 * kQa, kQa, kQwa},

@@ -125,7 +125,12 @@ class Solver2D {
     double global = 0.0;
     std::vector<double> per_macro;
   };
-  ExactNorms exact_error();
+  // of the solver's u_L, or of any level-L device function u
+  ExactNorms exact_error(const double* u = nullptr);
+  // MultigridSolver::solve_direct(l), proj/src/multigrid.cpp:323-357: b = level_rhs(l),
+  // u = g on the boundary; level 0 by cg_level0, l > 0 by the unpreconditioned CG
+  // of the reference (tolerance relative to the initial residual, no throw)
+  void solve_direct(int level, double* u);
   int extra_cycles() const { return extra_cycles_; }
   int launches_per_fmg() const { return fmg_launches_; }
   int launches_per_estimate() const { return est_launches_; }
@@ -144,8 +149,12 @@ class Solver2D {
   void probe_begin(std::vector<Probe>* list);
   cudaEvent_t event_at(int idx);
   void tabulate(const Problem2D& p);
+  double l2_norm_mass(int level, const double* f, double* tmp);
+  double dot_seq(int level, const double* a, const double* b);  // sqrt(max(0, dot_unique(f, M f)))
+  void finest_residual_vs_estimate();
+  double* scratch(int slot, int level);  // level-sized device scratch vectors (slot 0..3)
   void exact_setup();
-  ExactNorms exact_pointwise();
+  ExactNorms exact_pointwise(const double* u = nullptr);
   double dofs(int l) const { return static_cast<double>(H_->host.levels[l].dofs); }
 
   std::shared_ptr<DeviceHierarchy2D> H_;
@@ -185,6 +194,9 @@ class Solver2D {
   double* ex_moments_ = nullptr;
   double* ex_out_ = nullptr;
   std::vector<double> ex_usq_;
+  std::unique_ptr<DeviceArena> scr_arena_;
+  std::vector<double*> scr_;
+  int scr_level_ = -1;
   int extra_cycles_ = 0;
 };
 

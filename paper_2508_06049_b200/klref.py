@@ -72,7 +72,7 @@ UNSCALED, SCALED = 0, 1
 SYNC_REPLACE, SYNC_ADDITIVE = 0, 1
 STATE_U, STATE_B, STATE_W = 0, 1, 2
 PROBLEM_ZERO, PROBLEM_SIN2D, PROBLEM_LSHAPE = 0, 1, 2
-POLICY_NONE, POLICY_VALIDATION_TWO_DIGITS = 0, 1
+POLICY_NONE, POLICY_VALIDATION_TWO_DIGITS, POLICY_RESIDUAL_VS_ESTIMATE = 0, 1, 2
 PROBLEM_SIN3D, PROBLEM_GAUSS3D, PROBLEM_SERIES3D = 3, 4, 5
 MARK_TOP_FRACTION, MARK_HALF_MAX = 0, 1
 KERNEL_ALL, KERNEL_GS, KERNEL_RESIDUAL, KERNEL_RESTRICT, KERNEL_PROLONG = -1, 0, 1, 2, 3
@@ -128,6 +128,8 @@ SIGNATURES = {
     "klref_problem_set_params": (_I, [_P, _PD, _I]),
     "klref_problem_set_exact": (_I, [_P, _P, _P]),
     "klref_solver_exact_error": (_I, [_P, _PD, _PD]),
+    "klref_solver_exact_error_of": (_I, [_P, _P, _PD, _PD]),
+    "klref_solver_solve_direct": (_I, [_P, _I, _P]),
     "klref_solver_extra_cycles": (_I, [_P, _PI]),
     "klref_problem_destroy": (None, [_P]),
     "klref_solver_config_default": (None, [C.POINTER(SolverConfigC)]),
@@ -212,10 +214,15 @@ def _check(rc):
 
 
 def _dptr(a: np.ndarray):
+    # the C side reads / writes count contiguous doubles from this address
+    if a.dtype != np.float64 or not a.flags.c_contiguous:
+        raise ValueError("expected a C-contiguous float64 array")
     return a.ctypes.data_as(_PD)
 
 
 def _iptr(a: np.ndarray):
+    if a.dtype != np.int32 or not a.flags.c_contiguous:
+        raise ValueError("expected a C-contiguous int32 array")
     return a.ctypes.data_as(_PI)
 
 
@@ -511,7 +518,8 @@ class MultigridSolver(_Handle):
 
     def state_into(self, which: int, level: int, out: np.ndarray) -> np.ndarray:
         """FmgState component copied device->host into a caller buffer (e.g. pinned)."""
-        if out.size != self.h.level_size(level) or out.dtype != np.float64:
+        if (out.size != self.h.level_size(level) or out.dtype != np.float64 or not out.flags.c_contiguous
+                or not out.flags.writeable):
             raise StructuralError("state_into: buffer size / dtype mismatch")
         _check(lib().klref_solver_state_read(self.ptr, which, level, _dptr(out)))
         return out
@@ -555,6 +563,19 @@ class MultigridSolver(_Handle):
         loc = np.zeros(self.h.num_macros())
         _check(lib().klref_solver_exact_error(self.ptr, C.byref(g), _dptr(loc)))
         return g.value, loc
+
+    def exact_error_of(self, u: "GridFunction"):
+        """ExactErrorEvaluator(h, p, L).evaluate(u) of a finest-level function: (global, per_macro)."""
+        g = C.c_double()
+        loc = np.zeros(self.h.num_macros())
+        _check(lib().klref_solver_exact_error_of(self.ptr, u.ptr, C.byref(g), _dptr(loc)))
+        return g.value, loc
+
+    def solve_direct(self, level: int) -> "GridFunction":
+        """MultigridSolver::solve_direct(l), proj/src/multigrid.cpp:323-357."""
+        u = self.h.create_function(level)
+        _check(lib().klref_solver_solve_direct(self.ptr, level, u.ptr))
+        return u
 
     def extra_cycles(self) -> int:
         """FmgState::extra_cycles of the last fmg() (FinestPolicy::ValidationTwoDigits)."""

@@ -101,8 +101,8 @@ int main(int argc, char** argv) {
     klref::MultigridSolver solver(h, p, cfg);
     klref::FmgState st = solver.fmg();
     const klref::EstimateReport er = klref::error_estimate(st, 1, klref::EstimatorKind::Unscaled);
-    // validation rows of run_kl, proj/src/amr.cpp:202-204: exact error and effectivity
-    const klref::ErrorNorms exact = klref::exact_error_norm(st);
+    // validation rows of run_kl, proj/src/amr.cpp:188-204: exact error and effectivity
+    const klref::ErrorNorms exact = klref::exact_error_norm(p, st.u.back());
     const klref::EffectivityReport eff = klref::effectivity_index(er, exact);
     const klref::BoundsConstants bounds = klref::make_bounds_from_order(2, 0.0, 1);
     const klref::GridFunction uL = st.u.back();
@@ -118,7 +118,7 @@ int main(int argc, char** argv) {
                 exact.global, eff.gamma, eff.spread, bounds.equivalence.lower, bounds.equivalence.upper);
     for (std::size_t s = 0; s < er.eta_local.size(); ++s) std::printf("%s%.17g", s ? ", " : "", er.eta_local[s]);
     std::printf("]}\n");
-  } catch (const klref::Error& e) {
+  } catch (const std::exception& e) {
     std::fprintf(stderr, "dropin_demo: %s\n", e.what());
     return 1;
   }

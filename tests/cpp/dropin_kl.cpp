@@ -1,0 +1,139 @@
+// Drop-in test driver: the reference's own AMR layer over the B200 hot path.
+//
+// tests/cpp/build_dropin.sh compiles this file together with the reference's
+// UNCHANGED proj/src/{amr,macro_mesh,mesh_io,problems}.cpp (from
+// /root/reference, where they lie) with include/klref_b200/dropin ahead of the
+// reference's include directory, so "klref/{hhg,fem,multigrid,estimator}.hpp"
+// resolve to the facade (include/klref_b200/klref.hpp) and everything the
+// reference's run_kl calls on the hot path -- GridHierarchy::build,
+// MultigridSolver(h, p, cfg), solve_direct(0), fmg(), error_estimate,
+// exact_error_norm / FmgState::error_eval, effectivity_index -- runs on the
+// device through libklref_b200.so.
+//
+//   dropin_kl runkl <mesh> <sin|lshape> <ksteps> <L> <nu> <exact|eta> <final.mesh>
+//       the reference's run_kl (proj/src/amr.cpp:161-234), top-10 % marking;
+//       prints one JSON line per convergence record, then the final mesh size.
+//   dropin_kl halfmax <mesh> <sin|lshape> <ksteps> <L> <nu> <outdir>
+//       the kl loop of BASELINE.json config 2: per step build -> FMG ->
+//       error_estimate(j=1) -> revert_green + indicator aggregation
+//       (proj/src/amr.cpp:41-65) -> >= 0.5 max marking (klref_mark) ->
+//       refine_rg (proj/include/klref/macro_mesh.hpp:152-154) -> next mesh;
+//       writes outdir/kl_k<k>.mesh and prints one JSON line per step plus the
+//       wall time of the whole loop (hierarchy build and upload included).
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+#include <vector>
+
+#include "klref/amr.hpp"
+#include "klref/mesh_io.hpp"
+#include "klref/problems.hpp"
+
+namespace {
+
+klref::ProblemSpec problem(const std::string& name) {
+  if (name == "lshape") return klref::make_lshape_spec();  // proj/src/problems.cpp:36-53
+  klref::ProblemSpec p;                                     // BASELINE.json config 1
+  p.name = "sin2d";
+  p.exact = [](double x, double y) { return std::sin(M_PI * x) * std::sin(M_PI * y); };
+  p.source = [](double x, double y) { return 2.0 * M_PI * M_PI * std::sin(M_PI * x) * std::sin(M_PI * y); };
+  p.boundary = p.exact;
+  p.has_exact = true;
+  p.domain_volume = 1.0;
+  return p;
+}
+
+int run_kl_mode(char** argv) {
+  const klref::MacroMesh mesh0 = klref::read_mesh_file(argv[2]);
+  const klref::ProblemSpec p = problem(argv[3]);
+  klref::AmrConfig cfg;
+  cfg.scheme = klref::Scheme::KL;
+  cfg.ksteps = std::atoi(argv[4]);
+  cfg.levels = std::atoi(argv[5]);
+  cfg.solver.nu = std::atoi(argv[6]);
+  cfg.solver.finest_policy = klref::FinestPolicy::None;
+  cfg.driver = std::string(argv[7]) == "exact" ? klref::DriverSource::ExactLocalError
+                                                : klref::DriverSource::EstimatedIndicator;
+  const klref::AmrResult res = klref::run_kl(p, mesh0, cfg);
+  for (const auto& r : res.records)
+    std::printf("{\"record\": \"%s\", \"k\": %d, \"elements\": %lld, \"dofs\": %lld, \"error\": %.17g, "
+                "\"eta\": %.17g, \"rbar\": %.17g}\n",
+                r.phase.c_str(), r.iteration, static_cast<long long>(r.elements), static_cast<long long>(r.dofs),
+                r.error, r.eta, r.rbar_valid ? r.rbar : -1.0);
+  for (const auto& e : res.estimates)
+    std::printf("{\"estimate\": %d, \"eta\": %.17g, \"theta\": %.17g, \"gamma\": %.17g}\n", e.iteration,
+                e.report.eta, e.report.conv_factor, e.effectivity.gamma);
+  klref::write_mesh_file(res.final_mesh, argv[8]);
+  std::printf("{\"final_macros\": %zu}\n", res.final_mesh.num_active());
+  return 0;
+}
+
+int halfmax_mode(char** argv) {
+  klref::MacroMesh mesh = klref::read_mesh_file(argv[2]);
+  const klref::ProblemSpec p = problem(argv[3]);
+  const int K = std::atoi(argv[4]), L = std::atoi(argv[5]);
+  const std::string outdir = argv[7];
+  klref::SolverConfig sc;
+  sc.nu = std::atoi(argv[6]);
+  sc.finest_policy = klref::FinestPolicy::None;
+  const auto t0 = std::chrono::steady_clock::now();
+  double solve_s = 0.0;
+  for (int k = 0; k <= K; ++k) {
+    const auto s0 = std::chrono::steady_clock::now();
+    auto h = klref::GridHierarchy::build(mesh, L);
+    klref::MultigridSolver solver(h, p, sc);
+    const klref::FmgState st = solver.fmg();
+    const klref::EstimateReport er = klref::error_estimate(st, 1, klref::EstimatorKind::Unscaled);
+    solve_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - s0).count();
+    std::vector<int> marks;
+    if (k < K) {
+      // mark_and_refine's reversion + aggregation (proj/src/amr.cpp:41-65), >= 0.5 max rule
+      auto reverted = klref::revert_green(mesh, klref::MarkSet{}).first;
+      std::vector<int> active(mesh.active().begin(), mesh.active().end()), parent;
+      for (klref::Index id : mesh.active()) {
+        const klref::MacroElement& el = mesh.element(id);
+        parent.push_back(el.state == klref::ElementState::GreenChild ? static_cast<int>(el.parent) : -1);
+      }
+      std::vector<int> rev(reverted.active().begin(), reverted.active().end());
+      marks.assign(rev.size(), 0);
+      int nm = 0;
+      if (klref_mark(KLREF_MARK_HALF_MAX, 0.0, static_cast<int>(active.size()), active.data(), parent.data(),
+                     er.eta_local.data(), static_cast<int>(rev.size()), rev.data(), marks.data(), &nm) != KLREF_OK)
+        throw klref::StructuralError(klref_last_error());
+      marks.resize(static_cast<std::size_t>(nm));
+      klref::MarkSet ms;
+      ms.ids.assign(marks.begin(), marks.end());
+      mesh = klref::refine_rg(reverted, ms);
+      klref::write_mesh_file(mesh, outdir + "/kl_k" + std::to_string(k + 1) + ".mesh");
+    }
+    std::printf("{\"k\": %d, \"macros\": %d, \"dofs\": %lld, \"eta\": %.17g, \"norm_base\": %.17g, "
+                "\"theta\": %.17g, \"marks\": [",
+                k, h->num_macros(), static_cast<long long>(h->dof_count(L)), er.eta, er.norm_base, er.conv_factor);
+    for (std::size_t q = 0; q < marks.size(); ++q) std::printf("%s%d", q ? ", " : "", marks[q]);
+    std::printf("], \"eta_local\": [");
+    for (std::size_t q = 0; q < er.eta_local.size(); ++q) std::printf("%s%.17g", q ? ", " : "", er.eta_local[q]);
+    std::printf("]}\n");
+  }
+  const double total = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  std::printf("{\"loop_seconds\": %.6f, \"build_solve_estimate_seconds\": %.6f}\n", total, solve_s);
+  return 0;
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+  try {
+    const std::string mode = argc > 1 ? argv[1] : "";
+    if (mode == "runkl" && argc >= 9) return run_kl_mode(argv);
+    if (mode == "halfmax" && argc >= 8) return halfmax_mode(argv);
+    std::fprintf(stderr,
+                 "usage: dropin_kl runkl <mesh> <sin|lshape> <K> <L> <nu> <exact|eta> <final.mesh>\n"
+                 "       dropin_kl halfmax <mesh> <sin|lshape> <K> <L> <nu> <outdir>\n");
+    return 2;
+  } catch (const std::exception& e) {
+    std::fprintf(stderr, "dropin_kl: %s\n", e.what());
+    return 1;
+  }
+}

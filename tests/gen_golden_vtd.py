@@ -33,6 +33,29 @@ def main():
         out[name] = {"mesh": mesh, "problem": prob, "L": L, "nu": nu, "extra_cycles": int(d["extra_cycles"][0]),
                      "exact_global": float(d["exact_global"][0]),
                      "exact_local": [float(x) for x in d["exact_local"]], "u_sha256": u_sha}
+    # FinestPolicy::ResidualVsEstimate (proj/src/multigrid.cpp:294-319) and
+    # solve_direct(0), solve_direct(l) (proj/src/multigrid.cpp:323-357)
+    for name, mesh, prob, L, nu, ld in [("cfg1", "cfg1.mesh", "sin", 6, 1, 3),
+                                        ("cfg2k3", "cfg2_k3.mesh", "lshape", 7, 2, 2)]:
+        with tempfile.TemporaryDirectory() as tmp:
+            subprocess.run([DRIVER, "solverve", os.path.join(GOLD, mesh), prob, str(L), str(nu), str(ld), tmp],
+                           check=True)
+            with open(os.path.join(tmp, "report.txt")) as fh:
+                d = {ln.split()[0]: ln.split()[1:] for ln in fh if ln.strip()}
+
+            def h(f):
+                with open(os.path.join(tmp, f), "rb") as fh:
+                    return hashlib.sha256(fh.read()).hexdigest()
+
+            def arr(f):
+                import numpy as np
+                return [float(x) for x in np.fromfile(os.path.join(tmp, f), dtype=np.float64)]
+
+            out["rve_" + name] = {"mesh": mesh, "problem": prob, "L": L, "nu": nu, "l_direct": ld,
+                                  "extra_cycles": int(d["extra_cycles"][0]), "u_sha256": h(f"u_{L}.bin"),
+                                  "direct_0": arr("direct_0.bin"), "direct_l_sha256": h(f"direct_{ld}.bin"),
+                                  "direct_l_max_abs": max(abs(x) for x in arr(f"direct_{ld}.bin")),
+                                  "direct_l_head": arr(f"direct_{ld}.bin")[:32]}
     with open(os.path.join(GOLD, "vtd.json"), "w") as fh:
         json.dump(out, fh, indent=1)
 

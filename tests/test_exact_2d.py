@@ -64,3 +64,35 @@ def test_policy_config_plumbing():
     """The config struct carries the policy and max_extra_cycles (ABI layout)."""
     c = K.SolverConfig(finest_policy=K.POLICY_VALIDATION_TWO_DIGITS, max_extra_cycles=7).c()
     assert c.finest_policy == 1 and c.max_extra_cycles == 7
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["rve_cfg1", "rve_cfg2k3"])
+def test_residual_vs_estimate_policy(name):
+    """FinestPolicy::ResidualVsEstimate (proj/src/multigrid.cpp:294-319): the same
+    number of extra finest V-cycles and the same u_L (sha256) as the patched
+    reference (oracle/_ref/ref_driver solverve)."""
+    with open(path("vtd.json")) as fh:
+        ref = json.load(fh)[name]
+    prob = {"sin": K.PROBLEM_SIN2D, "lshape": K.PROBLEM_LSHAPE}[ref["problem"]]
+    h, s = _solve(ref["mesh"], ref["L"], prob, ref["nu"], K.POLICY_RESIDUAL_VS_ESTIMATE)
+    assert s.extra_cycles() == ref["extra_cycles"]
+    assert sha(s.state(K.STATE_U, ref["L"])) == ref["u_sha256"], "u_L after the extra cycles"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["rve_cfg1", "rve_cfg2k3"])
+def test_solve_direct(name):
+    """MultigridSolver::solve_direct (proj/src/multigrid.cpp:323-357): level 0 by
+    the coarse CG, bit for bit; level l > 0 by the reference's level CG, within
+    1e-12 (its dot products are reduced in another order on the device)."""
+    with open(path("vtd.json")) as fh:
+        ref = json.load(fh)[name]
+    prob = {"sin": K.PROBLEM_SIN2D, "lshape": K.PROBLEM_LSHAPE}[ref["problem"]]
+    h = K.GridHierarchy.build(K.MacroMesh.read(path(ref["mesh"])), ref["L"])
+    s = K.MultigridSolver(h, K.Problem(prob), K.SolverConfig(nu=ref["nu"], faithful_source=1))
+    u0 = s.solve_direct(0).numpy()
+    assert np.array_equal(u0, np.asarray(ref["direct_0"]))
+    ul = s.solve_direct(ref["l_direct"]).numpy()
+    assert np.max(np.abs(ul[:32] - np.asarray(ref["direct_l_head"]))) <= 1e-12 * ref["direct_l_max_abs"]
+    assert abs(np.max(np.abs(ul)) - ref["direct_l_max_abs"]) <= 1e-12 * ref["direct_l_max_abs"]
