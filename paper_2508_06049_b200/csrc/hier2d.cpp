@@ -103,8 +103,18 @@ void put_lane(std::uint64_t* w, const MemberRec* rec, const Level2D& lvl, int k,
   w[11] = pack32(k, flags);
   w[12] = pack32(wr0, wr1);
   w[13] = pack32(wb, wc);
-  w[14] = pack32(xb, nc);
-  w[15] = 0;
+  // the same reads as slots of the concatenated [ghosts | lattice] shared-memory
+  // region of k_gs_pipe / k_gs_macro (ghost g -> g, lattice index l -> G + 1 + l)
+  std::uint16_t a[6];
+  for (int q = 0; q < 6; ++q) {
+    const long long v = loc[q] >= 0 ? lvl.max_ghosts + 1LL + loc[q] : -1LL - loc[q];
+    if (v < 0 || v > 0xffff) fail(KB_INTERNAL, "step-program slot does not fit 16 bits");
+    a[q] = static_cast<std::uint16_t>(v);
+  }
+  w[14] = pack32(xb, static_cast<int>(a[4] | (static_cast<unsigned>(a[5]) << 16)));
+  w[15] = static_cast<std::uint64_t>(a[0]) | (static_cast<std::uint64_t>(a[1]) << 16) |
+          (static_cast<std::uint64_t>(a[2]) << 32) | (static_cast<std::uint64_t>(a[3]) << 48);
+  (void)nc;
 }
 
 // Step programs (layout in hier2d.hpp, Level2D::prog).

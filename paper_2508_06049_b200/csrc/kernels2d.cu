@@ -769,6 +769,7 @@ __device__ __forceinline__ unsigned long long ld_s64u(unsigned a) {
 struct PNode {
   double c[6], diag, inv, B;
   int loc[6], k, flags, wr0, wr1, wb, wc, xb, nc;
+  unsigned slot01, slot23, slot45;  // [ghosts | lattice] slots of the six reads, 16 bits each
 };
 
 __device__ __forceinline__ void ld_s_v2f64(unsigned a, double& x, double& y) {
@@ -786,8 +787,12 @@ __device__ __forceinline__ void load_lane(PNode& p, unsigned a) {
   ld_s_v4s32(a + 64, p.loc[0], p.loc[1], p.loc[2], p.loc[3]);
   ld_s_v4s32(a + 80, p.loc[4], p.loc[5], p.k, p.flags);
   ld_s_v4s32(a + 96, p.wr0, p.wr1, p.wb, p.wc);
-  int pad0, pad1;
-  ld_s_v4s32(a + 112, p.xb, p.nc, pad0, pad1);
+  int s45, s01, s23;
+  ld_s_v4s32(a + 112, p.xb, s45, s01, s23);
+  p.slot01 = static_cast<unsigned>(s01);
+  p.slot23 = static_cast<unsigned>(s23);
+  p.slot45 = static_cast<unsigned>(s45);
+  p.nc = 0;
 }
 
 // lane (type, mem): member `mem` of the step's node of this type.  Members 0/1
@@ -855,6 +860,51 @@ __device__ __forceinline__ void relax_nodes(const PNode& p, unsigned us_s, unsig
       if (p.wc > 1) copies[p.wr1] = res;
       for (int q = p.wb + 2; q < p.wb + p.wc; ++q) copies[wr_global[q]] = res;
     }
+  }
+}
+
+// relax_nodes for k_gs_pipe, with the shortest dependent path after the gate:
+// the six read addresses come straight from the record (slots of the
+// [ghosts | lattice] region, gx_s = its base), no selects, absent members /
+// cells are zero coefficients on the zero slot (o = +0.0), the two-member sum
+// is one shuffle.  The own copy and up to two other copies are stored to
+// global memory; vertex groups (> 2 members, `big` steps) take the general sum
+// and the remaining copies.
+__device__ __forceinline__ void relax_pipe(const PNode& p, unsigned gx_s, unsigned us_s, double* u,
+                                           const int* wr_global, int lane, double* own_copy) {
+  const int type = lane >> 3, mem = lane & 7;
+  const unsigned a0 = gx_s + 8u * (p.slot01 & 0xffffu), a1 = gx_s + 8u * (p.slot01 >> 16);
+  const unsigned a2 = gx_s + 8u * (p.slot23 & 0xffffu), a3 = gx_s + 8u * (p.slot23 >> 16);
+  const unsigned a4 = gx_s + 8u * (p.slot45 & 0xffffu), a5 = gx_s + 8u * (p.slot45 >> 16);
+  const double x0 = ld_s64(a0), x1 = ld_s64(a1), x2 = ld_s64(a2), x3 = ld_s64(a3), x4 = ld_s64(a4), x5 = ld_s64(a5);
+  double o = 0.0;
+  o = o + (p.c[0] * x0 + p.c[1] * x1);
+  o = o + (p.c[2] * x2 + p.c[3] * x3);
+  o = o + (p.c[4] * x4 + p.c[5] * x5);
+  double off = 0.0;
+  const bool big = (p.flags >> 16) & 1;  // the same on every lane of the step
+  if (!big) {
+    const double o1 = __shfl_down_sync(0xffffffffu, o, 1);
+    off = (off + o) + o1;  // a single member: o1 = +0.0
+  } else {
+    const int rc = (type < 3 && p.k >= 0) ? ((p.flags >> 8) & 0xff) : 0;
+    o = mem < rc ? o : 0.0;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) off = off + __shfl_sync(0xffffffffu, o, (lane & ~7) + r);
+  }
+  if (type < 3 && mem == 0 && p.k >= 0) {
+    // (B - off) / diag correctly rounded (Markstein; a zero numerator keeps its sign)
+    const double xn = p.B - off;
+    const double q = xn * p.inv;
+    const double r = __fma_rn(-q, p.diag, xn);
+    const double quot = xn == 0.0 ? q : __fma_rn(r, p.inv, q);
+    const double res = (p.flags & 1) ? p.B : quot;
+    st_s64(us_s + 8u * static_cast<unsigned>(p.k), res);
+    own_copy[p.k] = res;
+    if (p.wc > 0) u[p.wr0] = res;
+    if (p.wc > 1) u[p.wr1] = res;
+    // more than two other copies: vertex groups (also domain-boundary ones, rc = 0)
+    for (int q2 = p.wb + 2; q2 < p.wb + p.wc; ++q2) u[wr_global[q2]] = res;
   }
 }
 
@@ -1255,106 +1305,8 @@ __device__ long long g_sched_trace[8][512];
 
 // One relaxation per SG-lane subgroup: lane q evaluates member q's partial
 // row (group relaxations), lane 0 sums the members in slot order and writes
-// the value.  The dependence level is the only thing on the critical path:
-// everything a relaxation needs that does not change during the sweep -- its
-// header, the member record (coefficients, operand slots), b, the interior
-// stencil -- is read into registers for level g + 1 before the barrier that
-// ends level g, so after the barrier a relaxation is: operand loads, the
-// partial-row chain, the member sum (only as many terms as the warp's widest
-// group has members: trailing +0.0 terms are identities), the quotient, one
-// store.  The last warp is the producer: it takes no relaxations and refills
-// the TMA ring slot of level g + K right after the barrier of level g.
-struct SchedItem {
-  int4 h0, h1;
-  double B, ic;
-  double k[6];
-  int rd[6];
-  int count, nm;
-  bool act, interior;
-};
-
-template <int SG>
-__device__ __forceinline__ void sched_fetch(SchedItem& it, unsigned blk, int t, int tmax, int q, unsigned sb_s,
-                                            unsigned mt_s, int zero_slot) {
-  const int4 c4 = ld_s_int4(blk);
-  const unsigned hd = blk + 32u + 32u * min(t, tmax);
-  it.h0 = ld_s_int4(hd);
-  it.h1 = ld_s_int4(hd + 16);
-  it.count = c4.x;
-  it.act = t < it.count;
-  it.interior = it.h0.y >= 0;
-  it.nm = (!it.act || it.interior) ? 0 : it.h0.w;  // group members (-1: domain boundary)
-  it.B = ld_s64(sb_s + 8u * (it.act ? it.h0.x : 0));
-  it.ic = 0.0;
-  if (it.act && it.interior) {
-    // interior node: the macro's stencil s1..s6, 1/s0 and the six neighbour slots
-    const unsigned st = mt_s + 208u * it.h0.y;
-    ld_s_v2f64(st, it.k[0], it.k[1]);
-    ld_s_v2f64(st + 16, it.k[2], it.k[3]);
-    ld_s_v2f64(st + 32, it.k[4], it.k[5]);
-    double pad;
-    ld_s_v2f64(st + 48, it.ic, pad);
-    it.rd[0] = it.h0.z, it.rd[1] = it.h0.w, it.rd[2] = it.h1.x;
-    it.rd[3] = it.h1.y, it.rd[4] = it.h1.z, it.rd[5] = it.h1.w;
-  } else if (q < it.nm) {
-    // member q's partial_row (proj/src/fem.cpp:138-172 cell order, coefficients inline)
-    const unsigned mr = blk + 4u * static_cast<unsigned>(it.h0.z) + 4u * kSchedMemberWords * q;
-    ld_s_v2f64(mr, it.k[0], it.k[1]);
-    ld_s_v2f64(mr + 16, it.k[2], it.k[3]);
-    ld_s_v2f64(mr + 32, it.k[4], it.k[5]);
-    const int4 ra = ld_s_int4(mr + 48), rb = ld_s_int4(mr + 64);
-    it.rd[0] = ra.x, it.rd[1] = ra.y, it.rd[2] = ra.z, it.rd[3] = ra.w, it.rd[4] = rb.x, it.rd[5] = rb.y;
-  } else {
-#pragma unroll
-    for (int c = 0; c < 6; ++c) it.k[c] = 0.0, it.rd[c] = zero_slot;
-  }
-}
-
-template <int SG>
-__device__ __forceinline__ void sched_relax(const SchedItem& it, int q, int nmax, unsigned su_s) {
-  double x[6];
-#pragma unroll
-  for (int c = 0; c < 6; ++c) x[c] = ld_s64(su_s + 8u * it.rd[c]);
-  double o = 0.0;
-  // absent terms: zero coefficient x zero slot, o + 0 == o (o is never -0.0)
-#pragma unroll
-  for (int c = 0; c < 3; ++c) o = o + (it.k[2 * c] * x[2 * c] + it.k[2 * c + 1] * x[2 * c + 1]);
-  // members summed in ascending slot; lanes beyond a group's members hold +0.0
-  double ov[SG];
-#pragma unroll
-  for (int r = 0; r < SG; ++r) ov[r] = __shfl_sync(0xffffffffu, o, r, SG);
-  double off = 0.0;
-#pragma unroll
-  for (int r = 0; r < SG; ++r)
-    if (r < nmax) off = off + ov[r];
-  if (it.act && q == 0) {
-    double res;
-    if (it.interior) {
-      // interior node, proj/src/multigrid.cpp:170-175 (SURVEY.md A.5 order)
-      double acc = it.k[0] * x[0] + it.k[1] * x[1];
-      acc = acc + it.k[2] * x[2];
-      acc = acc + it.k[3] * x[3];
-      acc = acc + it.k[4] * x[4];
-      acc = acc + it.k[5] * x[5];
-      res = (it.B - acc) * it.ic;
-    } else if (it.h0.w < 0) {
-      res = it.B;  // domain boundary: u = b
-    } else {
-      // relax_boundary_node, proj/src/multigrid.cpp:132-150: (b - off) / diag
-      // correctly rounded (Markstein)
-      const double diag = __longlong_as_double(static_cast<long long>(static_cast<unsigned>(it.h1.x)) |
-                                               (static_cast<long long>(it.h1.y) << 32));
-      const double inv = __longlong_as_double(static_cast<long long>(static_cast<unsigned>(it.h1.z)) |
-                                              (static_cast<long long>(it.h1.w) << 32));
-      const double xn = it.B - off;
-      const double qq = xn * inv;
-      const double r = __fma_rn(-qq, diag, xn);
-      res = xn == 0.0 ? qq : __fma_rn(r, inv, qq);
-    }
-    st_s64(su_s + 8u * it.h0.x, res);
-  }
-}
-
+// the value.  The producer (last thread) issues the TMA copy of block g + K
+// after the barrier that ends level g.
 template <int SG>
 __global__ void __launch_bounds__(kSchedMaxThreads, 1) k_gs_sched(DevLevel2D lv, double* u,
                                                                  const double* __restrict__ b, int si, int reps, int K,
@@ -1372,18 +1324,18 @@ __global__ void __launch_bounds__(kSchedMaxThreads, 1) k_gs_sched(DevLevel2D lv,
   const unsigned ring_s = smem_addr(ring), mbar_s = smem_addr(mbar);
   const unsigned su_s = smem_addr(su), sb_s = smem_addr(sb), mt_s = smem_addr(mt);
   const int* blocks = lv.sc_blocks[si];
-  const int tid = threadIdx.x, nthreads = blockDim.x, producer_warp = nthreads / 32 - 1;
-  const bool producer = tid / 32 == producer_warp;
+  const int tid = threadIdx.x, nthreads = blockDim.x, producer = nthreads - 1;
   const int total = reps * levels;
-  const int q = tid & (SG - 1), sg = tid / SG, R = (nthreads - 32) / SG;
+  const int q = tid & (SG - 1), sg = tid / SG, R = nthreads / SG;
+  const unsigned submask = SG == 32 ? 0xffffffffu : (((1u << SG) - 1u) << ((tid & 31) & ~(SG - 1)));
 
   for (int k = tid; k <= levels; k += nthreads) loff[k] = lv.sc_lev_off[si][k];
-  if (tid == nthreads - 1) {
+  if (tid == producer) {
     for (int k = 0; k < K; ++k) mbar_init(mbar_s + 8u * k, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if (tid == nthreads - 1)
+  if (tid == producer)
     for (int g = 0; g < K && g < total; ++g) {
       const int lvl = g % levels;
       tma_load_block(ring_s + static_cast<unsigned>(g) * slot_bytes, blocks + loff[lvl],
@@ -1401,56 +1353,109 @@ __global__ void __launch_bounds__(kSchedMaxThreads, 1) k_gs_sched(DevLevel2D lv,
 
   const int kshift = __ffs(K) - 1;
   const int tmax = (slot_bytes - 64) / 32;  // header loads stay inside the slot
-  if (producer) {
-    // refill slot g & (K-1) with level g + K once every relaxation of level g is done
-    for (int g = 0; g < total; ++g) {
-      __syncthreads();
-      if (tid == nthreads - 1 && g + K < total) {
-        const int lvl = (g + K) % levels;
-        const unsigned blk = ring_s + static_cast<unsigned>(g & (K - 1)) * slot_bytes;
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        tma_load_block(blk, blocks + loff[lvl], 4u * static_cast<unsigned>(loff[lvl + 1] - loff[lvl]),
-                       mbar_s + 8u * (g & (K - 1)));
+  for (int g = 0; g < total; ++g) {
+    const int slot = g & (K - 1);  // K is a power of two
+    if (trace && tid == 0 && g < 512) g_sched_trace[0][g] = clock64();
+    mbar_wait(mbar_s + 8u * slot, static_cast<unsigned>((g >> kshift) & 1));
+    if (trace && tid == 0 && g < 512) g_sched_trace[1][g] = clock64();
+    const unsigned blk = ring_s + static_cast<unsigned>(slot) * slot_bytes;
+    // warp-uniform trip count: every lane reaches the member-sum shuffles; the
+    // first header is loaded together with the count (slot 0 exists in every block)
+    int count = 1;
+    for (int t0 = 0; t0 < count; t0 += R) {
+      const int t = t0 + sg;
+      const unsigned hd = blk + 32u + 32u * min(t, tmax);
+      const int4 c4 = ld_s_int4(blk);
+      const int4 h0 = ld_s_int4(hd), h1 = ld_s_int4(hd + 16);
+      count = c4.x;
+      const bool act = t < count;
+      const int cell = h0.x;
+      const bool interior = h0.y >= 0;
+      const int nm = (!act || interior) ? 0 : h0.w;  // group members (-1: domain boundary)
+      const double B = ld_s64(sb_s + 8u * (act ? cell : 0));
+      if (trace && tid == 0 && g < 512) g_sched_trace[3][g] = clock64() + (cell == -12345 ? 1 : 0);
+      double o = 0.0;
+      if (q < nm) {
+        // member q's partial_row (proj/src/fem.cpp:138-172 cell order, coefficients inline)
+        const unsigned mr = blk + 4u * static_cast<unsigned>(h0.z) + 4u * kSchedMemberWords * q;
+        double k[6];
+        ld_s_v2f64(mr, k[0], k[1]);
+        ld_s_v2f64(mr + 16, k[2], k[3]);
+        ld_s_v2f64(mr + 32, k[4], k[5]);
+        const int4 ra = ld_s_int4(mr + 48), rb = ld_s_int4(mr + 64);
+        const int nc = rb.z;
+        const int rd[6] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y};
+        double x[6];
+#pragma unroll
+        for (int c = 0; c < 6; ++c) x[c] = ld_s64(su_s + 8u * rd[c]);
+        // absent terms: zero coefficient x zero slot, o + 0 == o (o is never -0.0)
+        (void)nc;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) o = o + (k[2 * c] * x[2 * c] + k[2 * c + 1] * x[2 * c + 1]);
+      }
+      if (trace && tid == 0 && g < 512) g_sched_trace[4][g] = clock64() + (o == 12345.0 ? 1 : 0);
+      // members summed in ascending slot; lanes beyond a group's members hold
+      // +0.0, the bound is warp-uniform (the whole warp shuffles, converged)
+      double ov[SG];
+#pragma unroll
+      for (int r = 0; r < SG; ++r) ov[r] = __shfl_sync(0xffffffffu, o, r, SG);
+      double off = 0.0;
+#pragma unroll
+      for (int r = 0; r < SG; ++r) off = off + ov[r];
+      if (trace && tid == 0 && g < 512) g_sched_trace[5][g] = clock64() + (off == 12345.0 ? 1 : 0) + (nm << 20);
+      if (act && q == 0) {
+        double res;
+        if (interior) {
+          // interior node, proj/src/multigrid.cpp:170-175 (SURVEY.md A.5 order)
+          const unsigned st = mt_s + 208u * h0.y;
+          const double E = ld_s64(su_s + 8u * h0.z), W = ld_s64(su_s + 8u * h0.w);
+          const double N = ld_s64(su_s + 8u * h1.x), Sv = ld_s64(su_s + 8u * h1.y);
+          const double NW = ld_s64(su_s + 8u * h1.z), SE = ld_s64(su_s + 8u * h1.w);
+          double s1, s2, s3, s4, s5, s6, ic, pad;
+          ld_s_v2f64(st, s1, s2);
+          ld_s_v2f64(st + 16, s3, s4);
+          ld_s_v2f64(st + 32, s5, s6);
+          ld_s_v2f64(st + 48, ic, pad);
+          double acc = s1 * E + s2 * W;
+          acc = acc + s3 * N;
+          acc = acc + s4 * Sv;
+          acc = acc + s5 * NW;
+          acc = acc + s6 * SE;
+          res = (B - acc) * ic;
+        } else if (h0.w < 0) {
+          res = B;  // domain boundary: u = b
+        } else {
+          // relax_boundary_node, proj/src/multigrid.cpp:132-150
+          const double diag = __longlong_as_double(static_cast<long long>(static_cast<unsigned>(h1.x)) |
+                                                   (static_cast<long long>(h1.y) << 32));
+          const double inv = __longlong_as_double(static_cast<long long>(static_cast<unsigned>(h1.z)) |
+                                                  (static_cast<long long>(h1.w) << 32));
+          const double xn = B - off;
+          const double qq = xn * inv;
+          const double r = __fma_rn(-qq, diag, xn);
+          res = xn == 0.0 ? qq : __fma_rn(r, inv, qq);
+        }
+        st_s64(su_s + 8u * cell, res);
       }
     }
-  } else {
-    SchedItem it;
-    int nmax = 0;
-    auto fetch = [&](int g) {
-      const int slot = g & (K - 1);  // K is a power of two
-      mbar_wait(mbar_s + 8u * slot, static_cast<unsigned>((g >> kshift) & 1));
-      sched_fetch<SG>(it, ring_s + static_cast<unsigned>(slot) * slot_bytes, sg, tmax, q, sb_s, mt_s, nu);
-      nmax = __reduce_max_sync(0xffffffffu, max(it.nm, 0));
-    };
-    fetch(0);
-    for (int g = 0; g < total; ++g) {
-      if (trace && tid == 0 && g < 512) g_sched_trace[0][g] = clock64();
-      sched_relax<SG>(it, q, nmax, su_s);
-      if (trace && tid == 0 && g < 512) g_sched_trace[1][g] = clock64();
-      // a level wider than one pass of subgroups: the remaining items unpipelined
-      const int count = it.count;
-      if (count > R) {
-        const unsigned blk = ring_s + static_cast<unsigned>(g & (K - 1)) * slot_bytes;
-        for (int t0 = R; t0 < count; t0 += R) {
-          SchedItem extra;
-          sched_fetch<SG>(extra, blk, t0 + sg, tmax, q, sb_s, mt_s, nu);
-          const int nx = __reduce_max_sync(0xffffffffu, max(extra.nm, 0));
-          sched_relax<SG>(extra, q, nx, su_s);
-        }
-      }
-      if (g + 1 < total) fetch(g + 1);
-      if (trace && tid == 0 && g < 512) g_sched_trace[2][g] = clock64();
-      __syncthreads();
+    if (trace && tid == 0 && g < 512) g_sched_trace[2][g] = clock64();
+    __syncthreads();
+    if (tid == producer && g + K < total) {
+      const int lvl = (g + K) % levels;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tma_load_block(blk, blocks + loff[lvl], 4u * static_cast<unsigned>(loff[lvl + 1] - loff[lvl]),
+                     mbar_s + 8u * slot);
     }
   }
-  __syncthreads();
   const size_t copies = static_cast<size_t>(M) * lv.S;
   for (size_t k = tid; k < copies; k += nthreads) u[k] = su[lv.sc_copy_cell[k]];
   if (trace && tid == 0) {
     for (int g = 0; g < total && g < 40; ++g)
-      printf("level %d: relax %lld, prefetch next %lld, barrier -> next start %lld\n", g,
-             g_sched_trace[1][g] - g_sched_trace[0][g], g_sched_trace[2][g] - g_sched_trace[1][g],
-             g + 1 < total ? g_sched_trace[0][g + 1] - g_sched_trace[2][g] : 0ll);
+      printf("level %d: wait %lld hdr %lld member %lld sum %lld final %lld barrier+issue %lld nm %lld\n", g,
+             g_sched_trace[1][g] - g_sched_trace[0][g], g_sched_trace[3][g] - g_sched_trace[1][g],
+             g_sched_trace[4][g] - g_sched_trace[3][g], (g_sched_trace[5][g] & 0xfffff) - (g_sched_trace[4][g] & 0xfffff),
+             g_sched_trace[2][g] - g_sched_trace[5][g], g + 1 < total ? g_sched_trace[0][g + 1] - g_sched_trace[2][g] : 0ll,
+             g_sched_trace[5][g] >> 20);
   }
 }
 
@@ -1614,7 +1619,9 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
           }
         }
         __syncwarp();
+#ifdef KB_GS_TRACE
         if (trace && lane == 0 && g >= 64 && g < 128) ptr_sync[g - 64] = clock64();
+#endif
         bar_sync(kPipeBarB, bthreads);  // gate of step g opens
       }
       // step tau + 3: fetch when the polled requirements hold
@@ -1668,16 +1675,24 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
       PNode p0, p1;
       load_pnode(p0, ring_s, xs_s, bs_s, tl, mem);
       for (int tau = 0; tau < total; tau += 2) {
+#ifdef KB_GS_TRACE
         if (trace && lane == 0 && tau >= 64 && tau < 128) ptr_bstart[tau - 64] = clock64();
-        relax_nodes(p0, us_s, bs_s, gh_s, u, lv.wr, lane, um);
+#endif
+        relax_pipe(p0, gh_s, us_s, u, lv.wr, lane, um);
+#ifdef KB_GS_TRACE
         if (trace && lane == 0 && tau >= 64 && tau < 128) ptr_bend[tau - 64] = clock64() + (ld_s64(us_s) == 12345.0);
+#endif
         bar_arrive(kPipeBarA0 + tau % kPipeBarAs, bthreads);
         if (tau + 1 >= total) break;
         load_pnode(p1, ring_s + static_cast<unsigned>((tau + 1) % kPipeRing) * kStepBytes, xs_s, bs_s, tl, mem);
         bar_sync(kPipeBarB, bthreads);
+#ifdef KB_GS_TRACE
         if (trace && lane == 0 && tau + 1 >= 64 && tau + 1 < 128) ptr_bstart[tau + 1 - 64] = clock64();
-        relax_nodes(p1, us_s, bs_s, gh_s, u, lv.wr, lane, um);
+#endif
+        relax_pipe(p1, gh_s, us_s, u, lv.wr, lane, um);
+#ifdef KB_GS_TRACE
         if (trace && lane == 0 && tau + 1 >= 64 && tau + 1 < 128) ptr_bend[tau + 1 - 64] = clock64() + (ld_s64(us_s) == 12345.0);
+#endif
         bar_arrive(kPipeBarA0 + (tau + 1) % kPipeBarAs, bthreads);
         if (tau + 2 >= total) break;
         load_pnode(p0, ring_s + static_cast<unsigned>((tau + 2) % kPipeRing) * kStepBytes, xs_s, bs_s, tl, mem);
@@ -1693,7 +1708,9 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
       const int dn = n + 1 - j, dnw = n - j, ds = n + 2 - j;
       int t = 0;  // tau mod T, kept incrementally (no division on the step path)
       for (int tau = 0; tau < total; ++tau, t = (t + 1 == T ? 0 : t + 1)) {
+#ifdef KB_GS_TRACE
         if (trace && gw == 2 && lane == 0 && tau >= 64 && tau < 128) ptr_istart[tau - 64] = clock64();
+#endif
         const int i = t - 2 * j;
         if (row && i >= 1 && i <= n - j - 1) {
           const int k = rowk + i;
@@ -1709,18 +1726,22 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
           us[k] = v;
           if (j == 1 || i == 1 || i + j == n - 1) um[k] = v;  // exported: ghost of a neighbour
         }
+#ifdef KB_GS_TRACE
         if (trace && gw == 2 && lane == 0 && tau >= 64 && tau < 128) ptr_iend[tau - 64] = clock64() + (us[0] == 12345.0);
+#endif
         bar_arrive(kPipeBarA0 + tau % kPipeBarAs, bthreads);
         if (tau + 1 < total) bar_sync(kPipeBarB, bthreads);
       }
     }
   }
   __syncthreads();
+#ifdef KB_GS_TRACE
   if (trace && m == 0 && tid == 0)
     for (int q = 0; q < 12; ++q)
       printf("step %d: boundary relax %lld, boundary end->next start %lld, interior %lld, sync arrives at B %lld before boundary start\n",
              64 + q, ptr_bend[q] - ptr_bstart[q], ptr_bstart[q + 1] - ptr_bend[q], ptr_iend[q] - ptr_istart[q],
              ptr_bstart[q + 1] - ptr_sync[q + 1]);
+#endif
   // lattice-interior nodes back to global memory (interface copies are kept
   // current by every relaxation)
   for (int k = tid; k < S; k += blockDim.x) {
@@ -2072,10 +2093,8 @@ void launch_gs(const DevHier2D& hd, const DevLevel2D& lv, double* u, const doubl
     if (smem > 0) {
       static int trace = getenv("KB_SCHED_TRACE") ? 1 : 0;
       const int SG = lv.sc_max_members[si] <= 4 ? 4 : lv.sc_max_members[si] <= 8 ? 8 : lv.sc_max_members[si] <= 16 ? 16 : 32;
-      // relaxation warps for the widest level (one SG-lane subgroup each) + the producer warp
-      const int threads = static_cast<int>(std::min<long long>(
-          kSchedMaxThreads,
-          std::max<long long>(64, ((static_cast<long long>(lv.sc_max_width[si]) * SG + 31) / 32) * 32 + 32)));
+      const int threads = static_cast<int>(
+          std::min<long long>(kSchedMaxThreads, std::max<long long>(64, ((static_cast<long long>(lv.sc_max_width[si]) * SG + 31) / 32) * 32)));
       auto go = [&](auto kern) {
         set_smem(kern, smem);
         kern<<<1, threads, smem, st>>>(lv, u, b, si, reps, K, slot, trace);
