@@ -53,6 +53,15 @@ struct DevLevel2D {
   // pipelined smoother tables (Level2D::pipe; null when absent)
   const int* pipe_rec;
   int pipe_rec_words, pipe_maxreq;
+  // level 0 only: the coarse operator over unique DoF in dot_unique order
+  // (k_cg0): per DoF the member range, per member the three (coefficient,
+  // DoF) terms of its cell row, per DoF the copy offsets to write back
+  int cg_nmem, cg_ncopy;
+  const int* cg_mem_ptr;      // dot_count + 1
+  const int* cg_mem_dof;      // 3 per member
+  const double* cg_mem_coef;  // 3 per member
+  const int* cg_copy_ptr;     // dot_count + 1
+  const int* cg_copy;         // copy offsets
 };
 
 struct DevHier2D {

@@ -410,146 +410,144 @@ __device__ double seq_dot(const DevLevel2D& lv, const double* a, const double* b
   return s;
 }
 
-// cg_level0 (proj/src/multigrid.cpp:198-229) in one CTA with its vectors, the
-// dot order and the boundary flags staged in shared memory (level 0 has 3 M
-// copies); the arithmetic and the sequential dot order are unchanged.
-// With `stage` set, the operator tables apply_node walks (element stiffness
-// per macro, group/member maps) are copied to shared memory too, so every
-// CG iteration's apply reads only shared memory; the values are the same.
-__global__ void k_cg0(DevLevel2D lv_in, double* ug, const double* bg, CgParams prm, DevStatus* status,
-                      int stage) {
-  DevLevel2D lv = lv_in;
-  const int total = lv.M * lv.S;
+// cg_level0 (proj/src/multigrid.cpp:198-229) by one CTA over the unique DoF
+// of level 0, numbered in the owner order of dot_unique (every copy of a node
+// holds the same value throughout the CG, so the copy-wise arithmetic of the
+// reference is the DoF-wise arithmetic here, bit for bit):
+//   apply   OperatorP1::apply at n = 1: member m of a node contributes
+//           acc_m = 0.0 + ((k0 x_a + k1 x_b) + k2 x_c) (row `role` of its K_up,
+//           the gather order of proj/src/fem.cpp:106-115); a single member is
+//           the row value, several are summed 0.0 + acc_0 + acc_1 ... in slot
+//           order (interface_sync Additive); domain rows zeroed;
+//   dot     the products in parallel, then s = s + x y in DoF order by one
+//           thread from 16-byte shared-memory loads issued ahead of the
+//           dependent additions (measured: the dependent chain of additions
+//           is the cost of the CG, ~ 8-9 cycles per DoF and dot).
+constexpr int kCg0Threads = 128;
+
+__device__ __forceinline__ double cg_seq_sum(const double* prod, int cnt) {
+  double acc = 0.0;
+  int t = 0;
+  for (; t + 16 <= cnt; t += 16) {
+    double v[16];
+    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(prod + t));
+#pragma unroll
+    for (int q = 0; q < 16; q += 2)
+      asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v[q]), "=d"(v[q + 1]) : "r"(a + 8u * q) : "memory");
+#pragma unroll
+    for (int q = 0; q < 16; ++q) acc = acc + v[q];
+  }
+  for (; t < cnt; ++t) acc = acc + prod[t];
+  return acc;
+}
+
+__global__ void __launch_bounds__(kCg0Threads) k_cg0(DevLevel2D lv, double* ug, const double* bg, CgParams prm,
+                                                      DevStatus* status) {
   extern __shared__ __align__(16) double cg_smem[];
+  const int cnt = lv.dot_count, nmem = lv.cg_nmem, tid = threadIdx.x;
+  const int cnt2 = (cnt + 1) & ~1;  // 16-byte aligned arrays
   double* u = cg_smem;
-  double* b = u + total;
-  double* r = b + total;
-  double* p = r + total;
-  double* ap = p + total;
-  double* prod = ap + total;  // the dot products' terms (2 x dot_count)
-  double* kst = prod + 2 * lv.dot_count;
-  int* dord = reinterpret_cast<int*>(kst + (stage ? 18 * lv.M : 0));
-  int* tail = dord + lv.dot_count;
-  for (int k = threadIdx.x; k < total; k += blockDim.x) {
-    u[k] = ug[k];
-    b[k] = bg[k];
+  double* b = u + cnt2;
+  double* r = b + cnt2;
+  double* p = r + cnt2;
+  double* ap = p + cnt2;
+  double* prod = ap + cnt2;
+  double* acc_m = prod + cnt2;                                  // nmem
+  double* coef = acc_m + nmem;                                  // 3 nmem
+  int* mdof = reinterpret_cast<int*>(coef + 3 * static_cast<size_t>(nmem));  // 3 nmem
+  int* mptr = mdof + 3 * nmem;                                  // cnt + 1
+  unsigned char* dom = reinterpret_cast<unsigned char*>(mptr + cnt + 1);
+  __shared__ double sh_s;
+  for (int d = tid; d < cnt; d += kCg0Threads) {
+    const int k = lv.dot_order[d];
+    u[d] = ug[k];
+    b[d] = bg[k];
+    dom[d] = lv.node_flags[k] & 2;
   }
-  for (int t = threadIdx.x; t < lv.dot_count; t += blockDim.x) dord[t] = lv.dot_order[t];
-  if (stage) {
-    const int G = lv.num_groups;
-    const int nmem = lv.grp_ptr[G];
-    if (nmem > total) __trap();  // the host sized the member arrays by the copy count
-    int* gid = tail;
-    int* gptr = gid + total;
-    int* moff = gptr + G + 1;
-    int* mij = moff + total;
-    int* mslot = mij + total;
-    tail = mslot + total;
-    for (int t = threadIdx.x; t < 18 * lv.M; t += blockDim.x) kst[t] = lv.kstiff[t];
-    for (int k = threadIdx.x; k < total; k += blockDim.x) gid[k] = lv.node_gid[k];
-    for (int g = threadIdx.x; g <= G; g += blockDim.x) gptr[g] = lv.grp_ptr[g];
-    for (int m = threadIdx.x; m < nmem; m += blockDim.x) {
-      moff[m] = lv.mem_off[m];
-      mij[m] = lv.mem_ij[m];
-      mslot[m] = lv.mem_slot[m];
-    }
-    lv.kstiff = kst;
-    lv.node_gid = gid;
-    lv.grp_ptr = gptr;
-    lv.mem_off = moff;
-    lv.mem_ij = mij;
-    lv.mem_slot = mslot;
+  for (int q = tid; q < 3 * nmem; q += kCg0Threads) {
+    coef[q] = lv.cg_mem_coef[q];
+    mdof[q] = lv.cg_mem_dof[q];
   }
-  std::uint8_t* flags = reinterpret_cast<std::uint8_t*>(tail);
-  for (int k = threadIdx.x; k < total; k += blockDim.x) flags[k] = lv.node_flags[k];
-  lv.node_flags = flags;
+  for (int d = tid; d <= cnt; d += kCg0Threads) mptr[d] = lv.cg_mem_ptr[d];
   __syncthreads();
-  const int cnt = lv.dot_count;
-  // dot_unique terms in parallel, summed by thread 0 in the sequential order
-  // (s = s + x y exactly as proj/src/hhg.cpp:227-257)
-  auto terms = [&](const double* a, const double* bb, bool zero_bnd, double* out) {
-    for (int t = threadIdx.x; t < cnt; t += blockDim.x) {
-      const int k = dord[t];
-      double x = a[k], y = bb[k];
-      if (zero_bnd && (flags[k] & 2)) x = y = 0.0;
-      out[t] = x * y;
-    }
-  };
-  auto seq_sum = [&](const double* in) {
-    double acc = 0.0;
-    for (int t = 0; t < cnt; ++t) acc += in[t];
-    return acc;
-  };
-  __shared__ double sh_rr, sh_alpha, sh_beta;
-  __shared__ int sh_go;
-  for (int k = threadIdx.x; k < total; k += blockDim.x) apply_node(lv, lv.kstiff, u, r, b, APPLY_RESIDUAL, k);
-  __syncthreads();
-  for (int k = threadIdx.x; k < total; k += blockDim.x) p[k] = r[k];
-  __syncthreads();
-  double tol = 0.0;
-  int it = 0;
-  terms(r, r, false, prod);
-  terms(b, b, true, prod + cnt);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    sh_rr = seq_sum(prod);
-    const double bnorm = sqrt(fmax(0.0, seq_sum(prod + cnt)));
-    const double a = prm.rel_tol * bnorm;
-    tol = (a < prm.abs_floor) ? prm.abs_floor : a;
-    sh_go = sqrt(sh_rr) > tol;
-  }
-  __syncthreads();
-  while (sh_go) {
-    if (threadIdx.x == 0 && ++it > prm.max_iter) {
-      if (status->code == 0) {
-        status->code = 1;
-        status->residual = sqrt(sh_rr);
-      }
-      sh_go = 0;
+  // y = A x (residual: y = b - A x); domain rows zeroed
+  auto apply = [&](const double* x, double* y, bool residual) {
+    for (int m = tid; m < nmem; m += kCg0Threads) {
+      const int q = 3 * m;
+      acc_m[m] = 0.0 + ((coef[q] * x[mdof[q]] + coef[q + 1] * x[mdof[q + 1]]) + coef[q + 2] * x[mdof[q + 2]]);
     }
     __syncthreads();
-    if (!sh_go) break;
-    for (int k = threadIdx.x; k < total; k += blockDim.x) apply_node(lv, lv.kstiff, p, ap, nullptr, APPLY_ZERO_BND, k);
-    __syncthreads();
-    terms(p, ap, false, prod);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const double pap = seq_sum(prod);
-      if (pap <= 0.0) {
-        if (status->code == 0) {
-          status->code = 2;
-          status->residual = sqrt(sh_rr);
-        }
-        sh_go = 0;
+    for (int d = tid; d < cnt; d += kCg0Threads) {
+      const int m0 = mptr[d], m1 = mptr[d + 1];
+      double v;
+      if (m1 - m0 == 1) {
+        v = acc_m[m0];
       } else {
-        sh_alpha = sh_rr / pap;
+        v = 0.0;
+        for (int m = m0; m < m1; ++m) v += acc_m[m];
       }
+      y[d] = dom[d] ? 0.0 : (residual ? b[d] - v : v);
     }
     __syncthreads();
-    if (!sh_go) break;
-    const double alpha = sh_alpha;
-    for (int k = threadIdx.x; k < total; k += blockDim.x) {
-      u[k] = u[k] + alpha * p[k];
-      r[k] = r[k] + (-alpha) * ap[k];
+  };
+  // dot_unique in its sequential order; `zero_dom` zeroes domain rows of both operands
+  auto dot = [&](const double* x, const double* y, bool zero_dom) {
+    for (int d = tid; d < cnt; d += kCg0Threads) {
+      double xv = x[d], yv = y[d];
+      if (zero_dom && dom[d]) xv = yv = 0.0;
+      prod[d] = xv * yv;
     }
     __syncthreads();
-    terms(r, r, false, prod);
+    if (tid == 0) sh_s = cg_seq_sum(prod, cnt);
     __syncthreads();
-    if (threadIdx.x == 0) {
-      const double rr_new = seq_sum(prod);
-      sh_beta = rr_new / sh_rr;
-      sh_rr = rr_new;
+    return sh_s;
+  };
+  apply(u, r, true);
+  for (int d = tid; d < cnt; d += kCg0Threads) p[d] = r[d];
+  double rr = dot(r, r, false);
+  const double bnorm = sqrt(fmax(0.0, dot(b, b, true)));
+  const double tl = prm.rel_tol * bnorm;
+  const double tol = (tl < prm.abs_floor) ? prm.abs_floor : tl;
+  int it = 0, code = 0;
+  while (sqrt(rr) > tol) {
+    if (++it > prm.max_iter) {
+      code = 1;
+      break;
+    }
+    apply(p, ap, false);
+    const double pap = dot(p, ap, false);
+    if (pap <= 0.0) {
+      code = 2;
+      break;
+    }
+    const double alpha = rr / pap;
+    // the products of (r + (-alpha) ap)^2 from the values the update stores
+    for (int d = tid; d < cnt; d += kCg0Threads) {
+      const double rn = r[d] + (-alpha) * ap[d];
+      u[d] = u[d] + alpha * p[d];
+      r[d] = rn;
+      prod[d] = rn * rn;
     }
     __syncthreads();
-    const double beta = sh_beta;
-    for (int k = threadIdx.x; k < total; k += blockDim.x) p[k] = p[k] * beta + r[k];
+    if (tid == 0) sh_s = cg_seq_sum(prod, cnt);
     __syncthreads();
-    if (threadIdx.x == 0) sh_go = sqrt(sh_rr) > tol;
-    __syncthreads();
+    const double rr_new = sh_s;
+    const double beta = rr_new / rr;
+    for (int d = tid; d < cnt; d += kCg0Threads) p[d] = p[d] * beta + r[d];
+    // (the next apply reads p after its own first barrier)
+    rr = rr_new;
   }
-  if (threadIdx.x == 0) status->iters = it;
+  if (tid == 0) {
+    status->iters = it;
+    if (code != 0 && status->code == 0) {
+      status->code = code;
+      status->residual = sqrt(rr);
+    }
+  }
   __syncthreads();
-  for (int k = threadIdx.x; k < total; k += blockDim.x) ug[k] = u[k];
+  // every copy of each DoF
+  for (int d = tid; d < cnt; d += kCg0Threads)
+    for (int c = lv.cg_copy_ptr[d]; c < lv.cg_copy_ptr[d + 1]; ++c) ug[lv.cg_copy[c]] = u[d];
 }
 
 // ---------------------------------------------------------------- Gauss-Seidel
@@ -1976,15 +1974,11 @@ void set_smem(K kernel, size_t smem);
 void launch_cg0(const DevLevel2D& lv0, double* u, const double* b, double* scratch, CgParams prm,
                 DevStatus* status, cudaStream_t st) {
   (void)scratch;
-  const size_t N = static_cast<size_t>(lv0.M) * lv0.S;
-  const size_t smem = 5 * N * 8 + static_cast<size_t>(lv0.dot_count) * 20 + N + 16;
+  const size_t cnt2 = (static_cast<size_t>(lv0.dot_count) + 1) & ~size_t(1), nmem = static_cast<size_t>(lv0.cg_nmem);
+  const size_t smem = 6 * cnt2 * 8 + nmem * 8 + 3 * nmem * 8 + 3 * nmem * 4 + (cnt2 + 1) * 4 + cnt2 + 16;
   if (smem > 200 * 1024) fail(KB_STRUCTURAL, "coarse mesh too large for the level-0 CG");
-  // staged operator tables: 18 doubles per macro, gid/member maps (<= N each), group pointers
-  const size_t staged = smem + static_cast<size_t>(lv0.M) * 18 * 8 + (4 * N + lv0.num_groups + 1) * 4;
-  static int no_stage = getenv("KB_CG0_STAGE") && getenv("KB_CG0_STAGE")[0] == '0';
-  const int stage = !no_stage && staged <= 200 * 1024;
-  set_smem(k_cg0, stage ? staged : smem);
-  k_cg0<<<1, 256, stage ? staged : smem, st>>>(lv0, u, b, prm, status, stage);
+  set_smem(k_cg0, smem);
+  k_cg0<<<1, kCg0Threads, smem, st>>>(lv0, u, b, prm, status);
   check_launch("k_cg0");
 }
 

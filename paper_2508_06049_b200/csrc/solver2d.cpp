@@ -78,6 +78,44 @@ std::unique_ptr<DeviceHierarchy2D> DeviceHierarchy2D::create(const Mesh2D& mesh,
              vbytes(lv.sched[0].blocks) + vbytes(lv.sched[0].lev_off) + vbytes(lv.sched[1].blocks) +
              vbytes(lv.sched[1].lev_off) + vbytes(lv.pipe.rec);
   }
+  // level-0 CG tables (k_cg0): the gather of OperatorP1::apply at n = 1 -- every
+  // node is a macro corner whose one cell up(0,0) contributes row r (its role)
+  // of K_up, proj/src/fem.cpp:106-115 -- expressed over the unique DoF in the
+  // owner order of dot_unique (proj/src/hhg.cpp:227-257)
+  std::vector<int> cg_mem_ptr, cg_mem_dof, cg_copy_ptr, cg_copy;
+  std::vector<double> cg_mem_coef;
+  {
+    const Level2D& l0 = h.levels[0];
+    const int cnt = static_cast<int>(l0.dot_order.size());
+    std::vector<int> dof_of_group(l0.grp_ptr.size(), -1);
+    for (int dd = 0; dd < cnt; ++dd) {
+      const int g = l0.node_gid[l0.dot_order[dd]];
+      if (g < 0) fail(KB_INTERNAL, "level-0 node outside a group");
+      dof_of_group[g] = dd;
+    }
+    auto dof_of_copy = [&](int k) {
+      const int g = l0.node_gid[k];
+      if (g < 0 || dof_of_group[g] < 0) fail(KB_INTERNAL, "level-0 copy without a DoF");
+      return dof_of_group[g];
+    };
+    cg_mem_ptr.push_back(0);
+    cg_copy_ptr.push_back(0);
+    for (int dd = 0; dd < cnt; ++dd) {
+      const int g = l0.node_gid[l0.dot_order[dd]];
+      for (int q = l0.grp_ptr[g]; q < l0.grp_ptr[g + 1]; ++q) {
+        const int slot = l0.mem_slot[q];
+        const int role = l0.mem_j[q] == 1 ? 2 : l0.mem_i[q];  // (0,0) a, (1,0) b, (0,1) c
+        for (int c = 0; c < 3; ++c) {
+          cg_mem_coef.push_back(l0.kstiff[18 * static_cast<size_t>(slot) + 3 * role + c]);
+          cg_mem_dof.push_back(dof_of_copy(slot * l0.S + c));  // lattice index of corner c at n = 1
+        }
+        cg_copy.push_back(slot * l0.S + l0.mem_idx[q]);
+      }
+      cg_mem_ptr.push_back(static_cast<int>(cg_mem_coef.size() / 3));
+      cg_copy_ptr.push_back(static_cast<int>(cg_copy.size()));
+    }
+    bytes += vbytes(cg_mem_ptr) + vbytes(cg_mem_dof) + vbytes(cg_copy_ptr) + vbytes(cg_copy) + vbytes(cg_mem_coef);
+  }
   d->arena.reserve(bytes + 4096);
   d->dh.M = M;
   d->dh.L = h.L;
@@ -120,6 +158,15 @@ std::unique_ptr<DeviceHierarchy2D> DeviceHierarchy2D::create(const Mesh2D& mesh,
     dl.prog_extra = reinterpret_cast<const unsigned long long*>(d->arena.upload(lv.prog_extra));
     dl.xtra_ptr = d->arena.upload(lv.xtra_ptr);
     dl.max_extra = lv.max_extra;
+    if (l == 0) {
+      dl.cg_nmem = static_cast<int>(cg_mem_coef.size() / 3);
+      dl.cg_ncopy = static_cast<int>(cg_copy.size());
+      dl.cg_mem_ptr = d->arena.upload(cg_mem_ptr);
+      dl.cg_mem_dof = d->arena.upload(cg_mem_dof);
+      dl.cg_mem_coef = d->arena.upload(cg_mem_coef);
+      dl.cg_copy_ptr = d->arena.upload(cg_copy_ptr);
+      dl.cg_copy = d->arena.upload(cg_copy);
+    }
     dl.geo = d->arena.upload(geo[l]);
     dl.wq = d->arena.upload(wq[l]);
     if (lv.pipe.ok) {
