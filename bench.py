@@ -158,6 +158,17 @@ def host_cores():
         return os.cpu_count() or 1
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
 def impl_reference(args):
     """The reference's own CPU implementation of the path (the patched reference
     compiled from /root/reference sources, oracle/_ref/ref_driver).  The
@@ -196,7 +207,7 @@ def impl_reference(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_config(dofs),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": kind, "sample": sample,
-                             "host_cores": cores},
+                             "host_cores": cores, "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "replicas_all_cores": replicas}
     print(json.dumps(line), flush=True)
@@ -256,13 +267,55 @@ def run_3d(K, torch, name, N, L, prob, reps, peak):
     est_ms = kms[K.KERNEL_ESTIMATE] / reps
     gs_gbs = kb[K.KERNEL_GS] / (kms[K.KERNEL_GS] * 1e-3) / 1e9 if kms[K.KERNEL_GS] > 0 else None
     fmg_ms = ms - est_ms
+    # headline-shaped roofline of this workload's dominant kernel (CUDA-event
+    # probes in the captured graph, algorithmic bytes of SURVEY.md §8(d))
+    dom = max(range(8), key=lambda k: kms[k])
+    n_dom = s.kernel_stats(dom)[1]
+    ach = kb[dom] / (kms[dom] * 1e-3) / 1e9 if kms[dom] > 0 else 0.0
+    traffic = None
+    try:
+        with open(os.path.join(REPO, "profiles", "ncu_traffic.json")) as fh:
+            traffic = json.load(fh).get(f"{name.split(':')[0]}_{K.KERNEL_NAMES[dom]}")
+    except Exception:
+        traffic = None
+    roof = {"bound": "hbm", "kernel": K.KERNEL_NAMES[dom], "achieved": ach, "peak": peak, "unit": "GB/s",
+            "frac": ach / peak, "traffic": traffic, "alg_bytes_per_launch": kb[dom] / reps / max(n_dom, 1),
+            "ms_per_launch": kms[dom] / reps / max(n_dom, 1), "launches_per_fmg": n_dom}
     return {"config": name, "mesh": f"Kuhn {N}^3 cubes x 6 tets ({h.num_macros()} macros)", "level": L,
             "dofs": dofs, "ms_fmg_plus_estimate": ms, "estimator_ms": est_ms, "value": dofs / (ms * 1e-3) / 1e9,
             "unit": "GDoF/s", "fmg_roofline": {"alg_bytes": fmg_bytes_3d(dofs, 2),
                                                "frac": fmg_bytes_3d(dofs, 2) / (fmg_ms * 1e-3) / 1e9 / peak},
-            "smoother_alg_GBps": gs_gbs, "eta": rep.eta, "theta": rep.conv_factor,
+            "roofline": roof, "smoother_alg_GBps": gs_gbs, "eta": rep.eta, "theta": rep.conv_factor,
             "kernel_ms": {K.KERNEL_NAMES[k]: kms[k] / reps for k in range(8) if kms[k] > 0},
             "build_s": build_s, "parity": "builder 3-d oracle (oracle/klref_oracle3d.c), bitwise on small cases"}
+
+
+def run_kl_loop():
+    """BASELINE.json config 2 end to end through the product: the 5-step kl
+    loop of build/dropin/dropin_kl (the reference's own mesh layer linked
+    against the facade; per step host hierarchy build + upload, FMG, estimate,
+    >= 0.5 max marks, refine_rg), wall clock of the whole loop."""
+    exe = os.path.join(REPO, "build", "dropin", "dropin_kl")
+    if not os.path.exists(exe):
+        return {"error": "build/dropin/dropin_kl not built (needs the reference sources at build time)"}
+    import tempfile
+    with tempfile.TemporaryDirectory() as tmp:
+        runs = []
+        for _ in range(2):  # the second run is reported (first-touch of the library and device)
+            r = subprocess.run([exe, "halfmax", os.path.join(MESH_DIR, CFG2_MESHES[0]), "lshape", "5", str(LEVEL),
+                                str(NU), tmp], capture_output=True, text=True, timeout=600)
+            if r.returncode != 0:
+                return {"error": r.stderr.strip()[-300:]}
+            lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+            runs.append(lines)
+    steps = [d for d in runs[-1] if "k" in d]
+    tail = runs[-1][-1]
+    dofs = sum(d["dofs"] for d in steps)
+    return {"workload": "cfg2 kl loop: k = 0..5, build + upload + FMG + estimate + mark + refine per step",
+            "loop_seconds": tail["loop_seconds"], "build_solve_estimate_seconds": tail["build_solve_estimate_seconds"],
+            "dofs": dofs, "value": dofs / tail["loop_seconds"] / 1e9, "unit": "GDoF/s",
+            "macros": [d["macros"] for d in steps], "marks": [d["marks"] for d in steps[:-1]],
+            "eta": [d["eta"] for d in steps]}
 
 
 def run_cfg4(K, torch, reps, peak):
@@ -380,19 +433,22 @@ def run_3d_sharded(K, torch, dist, world, rank, reps, peak, barrier, max_over_ra
             "parity": "bitwise equal to the one-device solver (tests/test_shard_3d.py, in-process shards)"}
 
 
-def cpu_3d_port_sample():
-    """Single-threaded 3-d C oracle on a bounded sample (config 3 mesh, l = 4)."""
+def cpu_3d_port_sample(level=6):
+    """Single-threaded 3-d C oracle on config 3 itself (4^3 Kuhn cubes, l = 6,
+    17 M DoF): one FMG + estimate (about 30 s of CPU work)."""
     from oracle import oracle as O
     from paper_2508_06049_b200.meshes import kuhn_cube
 
     m = kuhn_cube(4)
-    h = O.Hier3D(m.coords, m.elements, 4)
+    h = O.Hier3D(m.coords, m.elements, level)
     t0 = time.perf_counter()
     st = O.fmg3d(h, "sin3", nu=2)
     O.estimate3d(st)
     dt = time.perf_counter() - t0
-    return {"value": h.dofs(4) / dt / 1e9, "unit": "GDoF/s", "cores": 1, "kind": "port",
-            "sample": f"3-d C oracle, config-3 mesh at l=4 ({h.dofs(4)} DoF), one FMG + estimate, 1 thread"}
+    return {"value": h.dofs(level) / dt / 1e9, "unit": "GDoF/s", "cores": 1, "kind": "port",
+            "ms_fmg_plus_estimate": dt * 1e3, "host_cores": host_cores(), "cpu_model": cpu_model(),
+            "sample": f"3-d C oracle (builder restatement, not the reference: the reference has no 3-d solver), "
+                      f"config 3 at l={level} ({h.dofs(level)} DoF), one FMG + estimate, 1 thread"}
 
 
 # ----------------------------------------------------------------- our arm (GPU)
@@ -562,7 +618,8 @@ def impl_ours(args):
                 cpu = {"value": cv, "unit": UNIT, "cores": 1, "kind": "reference",
                        "sample": f"{args.cpu_steps} full steps (6 meshes x FMG + estimate) of the patched reference "
                                  f"(oracle/_ref/ref_driver, g++ -O2, single-threaded), after 1 warm-up",
-                       "ms_per_step": statistics.mean(rec["step_s"]) * 1e3}
+                       "ms_per_step": statistics.mean(rec["step_s"]) * 1e3, "host_cores": host_cores(),
+                       "cpu_model": cpu_model()}
             else:
                 cd, ct = cpu_port_sample(max(1, args.cpu_steps // 2))
                 cpu = {"value": cd / statistics.mean(ct) / 1e9, "unit": UNIT, "cores": 1, "kind": "port",
@@ -585,6 +642,12 @@ def impl_ours(args):
                 extra3d["cpu_baseline_3d"] = cpu_3d_port_sample()
         except Exception as exc:  # secondary numbers never sink the headline line
             extra3d = {"error": str(exc)[:300]}
+    kl_loop = None
+    if world == 1 and not args.no_3d:
+        try:
+            kl_loop = run_kl_loop()
+        except Exception as exc:  # secondary numbers never sink the headline line
+            kl_loop = {"error": str(exc)[:300]}
 
     value = world * dofs / (t_step * 1e-3) / 1e9
     line = {
@@ -604,6 +667,7 @@ def impl_ours(args):
         "clocks": clk,
         "cpu_baseline": cpu,
         "workloads_3d": extra3d,
+        "kl_loop_e2e": kl_loop,
     }
     if sharded:
         # the NCCL-sharded config-5 run (all ranks): a watchdog prints the
