@@ -803,17 +803,22 @@ __global__ void __launch_bounds__(NT, MINB) k3_gs_sweeps(DevLevel3D lv, double* 
   const int nthreads = gridDim.x * NT;
   const int tid = blockIdx.x * NT + threadIdx.x;
   const int lane = threadIdx.x & 31, gw = tid >> 5, nw = nthreads >> 5;
+#ifdef KB_GS_TRACE
   if ((phases & 4) && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_gs3_trace[63]));
+#endif
   for (int sw = 0; sw < sweeps; ++sw) {
     for (int c = 0; c < lv.colors; ++c) {
       const int p0 = lv.color_grp_ptr[c], p1 = lv.color_grp_ptr[c + 1], pw = lv.color_wide_end[c];
       if (phases & 1) {
         for (int t = p0 + gw; t < pw; t += nw) gs_group_warp(lv, u, b, lv.color_grp[t], lane);
+#ifdef KB_GS_TRACE
         if (phases & 8) {  // measurement trace: one thread per group
           for (int t = pw + tid; t < p1; t += nthreads)
             gs_group(lv, u, b, lv.color_grp[t],
                      tid == 0 && sw == 0 ? reinterpret_cast<long long*>(g_gs3_trace + 16 + 10 * c) : nullptr);
-        } else {
+        } else
+#endif
+        {
           if (lv.n <= 16) {
             for (int t0 = pw + 8 * gw; t0 < p1; t0 += 8 * nw) {
               const int t = t0 + (lane >> 2);
@@ -827,18 +832,22 @@ __global__ void __launch_bounds__(NT, MINB) k3_gs_sweeps(DevLevel3D lv, double* 
           }
         }
       }
+#ifdef KB_GS_TRACE
       if (phases & 4) {  // measurement trace (KB_GS3_PHASES bit 2): work end vs barrier exit
         __syncthreads();
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         if (sw == 0 && threadIdx.x == 0) atomicMax(&g_gs3_trace[2 * c], t);
       }
+#endif
       if (p1 > p0) grid.sync();
+#ifdef KB_GS_TRACE
       if ((phases & 4) && threadIdx.x == 0 && blockIdx.x == 0 && sw == 0) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         g_gs3_trace[2 * c + 1] = t;
       }
+#endif
     }
     if (lv.n >= 4) {
       if ((phases & 2) && static_cast<int>(blockIdx.x) < active) {
@@ -850,6 +859,7 @@ __global__ void __launch_bounds__(NT, MINB) k3_gs_sweeps(DevLevel3D lv, double* 
       if (sw + 1 < sweeps) grid.sync();
     }
   }
+#ifdef KB_GS_TRACE
   if (phases & 4) {
     grid.sync();
     if (blockIdx.x == 0 && threadIdx.x == 0)
@@ -865,6 +875,7 @@ __global__ void __launch_bounds__(NT, MINB) k3_gs_sweeps(DevLevel3D lv, double* 
                c, t[1] - t[0], t[1] - t[0], t[2] - t[0], t[3] - t[0], t[4] - t[0], t[8] - t[0], t[9] - t[0]);
       }
   }
+#endif
 }
 
 // interior phase, one launch per colour over every macro: block = (macro,
