@@ -44,6 +44,21 @@ __device__ int g_dbg_S, g_dbg_G, g_dbg_MS;
   } while (0)
 #endif
 
+// KB_GS_CHECK builds (verification, not product): the shared-memory slots,
+// lattice indices and global offsets the smoothers take from host tables are
+// bounds-checked on the device; a violation traps (the parity tests then fail
+// with an illegal-instruction error instead of reading or writing out of range)
+#ifdef KB_GS_CHECK
+#define KB_ASSERT(cond) \
+  do {                  \
+    if (!(cond)) __trap(); \
+  } while (0)
+#else
+#define KB_ASSERT(cond) \
+  do {                  \
+  } while (0)
+#endif
+
 __device__ __forceinline__ int dlat(int n, int i, int j) { return j * (n + 1) - (j * (j - 1)) / 2 + i; }
 
 __device__ __forceinline__ void decode(int n, int idx, int& i, int& j) {
@@ -869,11 +884,20 @@ __device__ __forceinline__ void relax_nodes(const PNode& p, unsigned us_s, unsig
 // global memory; vertex groups (> 2 members, `big` steps) take the general sum
 // and the remaining copies.
 __device__ __forceinline__ void relax_pipe(const PNode& p, unsigned gx_s, unsigned us_s, double* u,
-                                           const int* wr_global, int lane, double* own_copy) {
+                                           const int* wr_global, int lane, double* own_copy, int g_chk_slots,
+                                           int g_chk_S, int g_chk_MS) {
+  (void)g_chk_slots, (void)g_chk_S, (void)g_chk_MS;  // bounds of the KB_GS_CHECK build
   const int type = lane >> 3, mem = lane & 7;
   const unsigned a0 = gx_s + 8u * (p.slot01 & 0xffffu), a1 = gx_s + 8u * (p.slot01 >> 16);
   const unsigned a2 = gx_s + 8u * (p.slot23 & 0xffffu), a3 = gx_s + 8u * (p.slot23 >> 16);
   const unsigned a4 = gx_s + 8u * (p.slot45 & 0xffffu), a5 = gx_s + 8u * (p.slot45 >> 16);
+#ifdef KB_GS_CHECK
+  {
+    const unsigned lim = gx_s + 8u * static_cast<unsigned>(g_chk_slots);
+    KB_ASSERT(a0 < lim && a1 < lim && a2 < lim && a3 < lim && a4 < lim && a5 < lim);
+    KB_ASSERT(p.k < g_chk_S);
+  }
+#endif
   const double x0 = ld_s64(a0), x1 = ld_s64(a1), x2 = ld_s64(a2), x3 = ld_s64(a3), x4 = ld_s64(a4), x5 = ld_s64(a5);
   double o = 0.0;
   o = o + (p.c[0] * x0 + p.c[1] * x1);
@@ -897,6 +921,8 @@ __device__ __forceinline__ void relax_pipe(const PNode& p, unsigned gx_s, unsign
     const double r = __fma_rn(-q, p.diag, xn);
     const double quot = xn == 0.0 ? q : __fma_rn(r, p.inv, q);
     const double res = (p.flags & 1) ? p.B : quot;
+    KB_ASSERT(p.wc <= 0 || (p.wr0 >= 0 && p.wr0 < g_chk_MS));
+    KB_ASSERT(p.wc <= 1 || (p.wr1 >= 0 && p.wr1 < g_chk_MS));
     st_s64(us_s + 8u * static_cast<unsigned>(p.k), res);
     own_copy[p.k] = res;
     if (p.wc > 0) u[p.wr0] = res;
@@ -963,13 +989,7 @@ __device__ __forceinline__ void group_sweep(const DevLevel2D& lv, const SweepArg
                                             double* copies, int gw, int lane, int bar_id, int bar_threads) {
   const int n = lv.n;
   const unsigned ring_s = smem_addr(ring);
-#ifdef KB_GS_CHECK
-  if (threadIdx.x == 0) {
-    g_dbg_S = lv.S;
-    g_dbg_G = lv.max_ghosts;
-    g_dbg_MS = lv.M * lv.S;
-  }
-#endif
+
   if (gw == 1) {
     const unsigned long long* prog_m = a.prog_m;
     // lookahead kRingSteps - 1: during step t the slot of step t - 1 is refilled
@@ -1508,6 +1528,7 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
   if (tid < kPipePubs) pub_last[tid] = -1;
   const unsigned long long* prog_m = lv.prog + lv.prog_ptr[m];
   const int* rec_m0 = rec + static_cast<size_t>(m) * 2 * T * rec_words;  // sweep-0 records, then sweep >= 1
+
   auto rec_src = [&](int tau) { return rec_m0 + (tau >= T ? static_cast<size_t>(T) * rec_words : 0); };
   double* um = u + static_cast<size_t>(m) * S;
 
@@ -1604,6 +1625,8 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
         }
         if (lane < nfetch) {
           const int dst = r[2 + 2 * maxreq + 2 * lane];
+          KB_ASSERT(dst < S && -1 - dst <= lv.max_ghosts);
+          KB_ASSERT(r[3 + 2 * maxreq + 2 * lane] >= 0 && r[3 + 2 * maxreq + 2 * lane] < lv.M * S);
           if (dst >= 0)
             us[dst] = f1;
           else
@@ -1676,7 +1699,7 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
 #ifdef KB_GS_TRACE
         if (trace && lane == 0 && tau >= 64 && tau < 128) ptr_bstart[tau - 64] = clock64();
 #endif
-        relax_pipe(p0, gh_s, us_s, u, lv.wr, lane, um);
+        relax_pipe(p0, gh_s, us_s, u, lv.wr, lane, um, lv.max_ghosts + 1 + S, S, lv.M * S);
 #ifdef KB_GS_TRACE
         if (trace && lane == 0 && tau >= 64 && tau < 128) ptr_bend[tau - 64] = clock64() + (ld_s64(us_s) == 12345.0);
 #endif
@@ -1687,7 +1710,7 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
 #ifdef KB_GS_TRACE
         if (trace && lane == 0 && tau + 1 >= 64 && tau + 1 < 128) ptr_bstart[tau + 1 - 64] = clock64();
 #endif
-        relax_pipe(p1, gh_s, us_s, u, lv.wr, lane, um);
+        relax_pipe(p1, gh_s, us_s, u, lv.wr, lane, um, lv.max_ghosts + 1 + S, S, lv.M * S);
 #ifdef KB_GS_TRACE
         if (trace && lane == 0 && tau + 1 >= 64 && tau + 1 < 128) ptr_bend[tau + 1 - 64] = clock64() + (ld_s64(us_s) == 12345.0);
 #endif
