@@ -1513,6 +1513,12 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
                                                     int sweeps, int* progress, const int* __restrict__ rec,
                                                     int rec_words, int maxreq, int trace) {
   extern __shared__ __align__(16) double smem[];
+#ifdef KB_GS_ABLATE
+  // measurement builds only (results are wrong): drop one role's work per bit
+  const int abl = trace >> 4;
+#else
+  constexpr int abl = 0;
+#endif
   const int S = lv.S, n = lv.n, T = 2 * n + 1, m = blockIdx.x, total = sweeps * T;
   const int Wc = gs_group_warps(n), cthreads = 32 * Wc, bthreads = cthreads + 32;
   unsigned char* ring = reinterpret_cast<unsigned char*>(smem);
@@ -1563,7 +1569,10 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
       bar_sync(kPipeBarA0 + tau % kPipeBarAs, bthreads);
       if (lane == 0) {
         *reinterpret_cast<volatile int*>(&pub_last[w]) = tau;
-        asm volatile("red.release.gpu.global.max.s32 [%0], %1;" ::"l"(progress + m), "r"(tau + 2) : "memory");
+        if (abl & 32)
+          asm volatile("red.relaxed.gpu.global.max.s32 [%0], %1;" ::"l"(progress + m), "r"(tau + 2) : "memory");
+        else
+          asm volatile("red.release.gpu.global.max.s32 [%0], %1;" ::"l"(progress + m), "r"(tau + 2) : "memory");
       }
     }
   } else if (warp == Wc) {
@@ -1582,27 +1591,37 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
       asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(pm) : "memory");
       return v;
     };
-    double f1 = 0.0, f2 = 0.0, f3 = 0.0;
-    bool f1ok = false, f2ok = false, f3ok = false;
-    int p3 = 0, p4 = 0, p5 = 0;
-    bool p3ok = false, p4ok = false, p5ok = false;
+    // Per step s the fetched value and the polled progress live in slot s % 3:
+    // a fetch issued for step tau + 3 is consumed at the gate of that step two
+    // iterations later, a poll issued for step tau + 5 is checked when step
+    // tau + 5 is fetched, two iterations later -- the loop is unrolled three
+    // times so the slots are named registers and no iteration waits for its
+    // own loads (the previous rotation through register moves did, one L2
+    // round trip per step on the gate's critical path).
+    double F0 = 0.0, F1 = 0.0, F2 = 0.0;
+    bool F0ok = false, F1ok = false, F2ok = false;
+    int P0 = 0, P1 = 0, P2 = 0;
+    bool P0ok = false, P1ok = false, P2ok = false;
     long long t_slow = 0, t_start = clock64();
     int n_slow = 0, n_req = 0;
-    // prologue: poll steps 0 .. 4 (their records are in the ring)
-    for (int st = 0; st < 5 && st < total; ++st) {
+    // prologue: poll steps 2 .. 4 (their records are in the ring)
+    for (int st = 2; st < 5 && st < total; ++st) {
       const int* r = recp(st);
       const int pv = lane < r[0] ? poll(progress + r[2 + 2 * lane]) : 0;
-      if (st == 2) p3 = pv, p3ok = true;
-      if (st == 3) p4 = pv, p4ok = true;
-      if (st == 4) p5 = pv, p5ok = true;
+      if (st == 2) P2 = pv, P2ok = true;
+      if (st == 3) P0 = pv, P0ok = true;
+      if (st == 4) P1 = pv, P1ok = true;
     }
-    for (int tau = -1; tau < total; ++tau) {
+    // one iteration: gate of step tau + 1 (slot Fg), fetch for step tau + 3
+    // (uses poll Pf, writes Ff), poll for step tau + 5 (writes Pp)
+    auto iteration = [&](int tau, double& Fg, bool& Fgok, double& Ff, bool& Ffok, int& Pf, bool& Pfok, int& Pp,
+                         bool& Ppok) {
       const int g = tau + 1;
       if (g < total) {
         const int* r = recp(g);
         const int nreq = r[0], nfetch = r[1];
         n_req += nreq > 0;
-        if (!f1ok && (nreq > 0 || nfetch > 0)) {
+        if (!(abl & 8) && !Fgok && (nreq > 0 || nfetch > 0)) {
           // slow path: wait for the requirements (the publisher reports this
           // macro's completed steps meanwhile)
           ++n_slow;
@@ -1620,17 +1639,17 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
             }
           }
           __syncwarp();
-          if (lane < nfetch) f1 = __ldcg(u + r[3 + 2 * maxreq + 2 * lane]);
-          t_slow += clock64() + (f1 == 12345.0 ? 1 : 0);
+          if (lane < nfetch) Fg = __ldcg(u + r[3 + 2 * maxreq + 2 * lane]);
+          t_slow += clock64();
         }
         if (lane < nfetch) {
           const int dst = r[2 + 2 * maxreq + 2 * lane];
           KB_ASSERT(dst < S && -1 - dst <= lv.max_ghosts);
           KB_ASSERT(r[3 + 2 * maxreq + 2 * lane] >= 0 && r[3 + 2 * maxreq + 2 * lane] < lv.M * S);
           if (dst >= 0)
-            us[dst] = f1;
+            us[dst] = Fg;
           else
-            gh[-1 - dst] = f1;
+            gh[-1 - dst] = Fg;
         }
         // the step-done barrier of step g reuses the one of step g - kPipeBarAs: its
         // publisher must have passed it (flow control only)
@@ -1647,28 +1666,30 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
       }
       // step tau + 3: fetch when the polled requirements hold
       const int s3 = tau + 3;
-      f3ok = false;
-      if (s3 < total && p3ok) {
+      Ffok = false;
+      if (s3 < total && Pfok) {
         const int* r = recp(s3);
-        const bool ok = lane >= r[0] || p3 >= r[3 + 2 * lane] + shift(s3);
+        const bool ok = lane >= r[0] || Pf >= r[3 + 2 * lane] + shift(s3);
         if (__all_sync(0xffffffffu, ok)) {
-          if (lane < r[1]) f3 = __ldcg(u + r[3 + 2 * maxreq + 2 * lane]);
-          f3ok = true;
+          if (lane < r[1]) Ff = __ldcg(u + r[3 + 2 * maxreq + 2 * lane]);
+          Ffok = true;
         }
       }
       // step tau + 5: poll
       const int s5 = tau + 5;
-      p5ok = false;
+      Ppok = false;
       if (s5 < total) {
         const int* r = recp(s5);
-        if (lane < r[0]) p5 = poll(progress + r[2 + 2 * lane]);
-        p5ok = true;
+        if (lane < r[0]) Pp = poll(progress + r[2 + 2 * lane]);
+        Ppok = true;
       }
-      // rotate the stages
-      f1 = f2, f1ok = f2ok;
-      f2 = f3, f2ok = f3ok;
-      p3 = p4, p3ok = p4ok;
-      p4 = p5, p4ok = p5ok;
+    };
+    // step s lives in slot s % 3: tau = -1 + 3q gates step 3q (slot 0), fetches
+    // step 3q + 2 (slot 2, poll slot 2), polls step 3q + 4 (slot 1)
+    for (int tau = -1; tau < total; tau += 3) {
+      iteration(tau, F0, F0ok, F2, F2ok, P2, P2ok, P1, P1ok);
+      if (tau + 1 < total) iteration(tau + 1, F1, F1ok, F0, F0ok, P0, P0ok, P2, P2ok);
+      if (tau + 2 < total) iteration(tau + 2, F2, F2ok, F1, F1ok, P1, P1ok, P0, P0ok);
     }
     if (trace && lane == 0 && (m % 20 == 0 || m == gridDim.x - 1))
       printf("pipe macro %d: steps %d, gated %d, slow gates %d, cycles in slow gates %lld of %lld\n", m, total, n_req,
@@ -1681,7 +1702,8 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
     if (gw == 1) {
       for (int tau = 0; tau < total; ++tau) {
         const int nx = tau + kPipeRing - 1;
-        if (nx < total) issue_prog(prog_m, ring_s, rec_src(nx), rring_s, rec_words, nx % T, nx % kPipeRing, lane);
+        if (nx < total && !(abl & 16))
+          issue_prog(prog_m, ring_s, rec_src(nx), rring_s, rec_words, nx % T, nx % kPipeRing, lane);
         cp_async_commit();
         cp_async_wait<kPipeRing - 7>();  // steps and records <= tau + 6 landed (read by the sync warp after A)
         bar_arrive(kPipeBarA0 + tau % kPipeBarAs, bthreads);
@@ -1699,24 +1721,24 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
 #ifdef KB_GS_TRACE
         if (trace && lane == 0 && tau >= 64 && tau < 128) ptr_bstart[tau - 64] = clock64();
 #endif
-        relax_pipe(p0, gh_s, us_s, u, lv.wr, lane, um, lv.max_ghosts + 1 + S, S, lv.M * S);
+        if (!(abl & 2)) relax_pipe(p0, gh_s, us_s, u, lv.wr, lane, um, lv.max_ghosts + 1 + S, S, lv.M * S);
 #ifdef KB_GS_TRACE
         if (trace && lane == 0 && tau >= 64 && tau < 128) ptr_bend[tau - 64] = clock64() + (ld_s64(us_s) == 12345.0);
 #endif
         bar_arrive(kPipeBarA0 + tau % kPipeBarAs, bthreads);
         if (tau + 1 >= total) break;
-        load_pnode(p1, ring_s + static_cast<unsigned>((tau + 1) % kPipeRing) * kStepBytes, xs_s, bs_s, tl, mem);
+        if (!(abl & 4)) load_pnode(p1, ring_s + static_cast<unsigned>((tau + 1) % kPipeRing) * kStepBytes, xs_s, bs_s, tl, mem);
         bar_sync(kPipeBarB, bthreads);
 #ifdef KB_GS_TRACE
         if (trace && lane == 0 && tau + 1 >= 64 && tau + 1 < 128) ptr_bstart[tau + 1 - 64] = clock64();
 #endif
-        relax_pipe(p1, gh_s, us_s, u, lv.wr, lane, um, lv.max_ghosts + 1 + S, S, lv.M * S);
+        if (!(abl & 2)) relax_pipe(p1, gh_s, us_s, u, lv.wr, lane, um, lv.max_ghosts + 1 + S, S, lv.M * S);
 #ifdef KB_GS_TRACE
         if (trace && lane == 0 && tau + 1 >= 64 && tau + 1 < 128) ptr_bend[tau + 1 - 64] = clock64() + (ld_s64(us_s) == 12345.0);
 #endif
         bar_arrive(kPipeBarA0 + (tau + 1) % kPipeBarAs, bthreads);
         if (tau + 2 >= total) break;
-        load_pnode(p0, ring_s + static_cast<unsigned>((tau + 2) % kPipeRing) * kStepBytes, xs_s, bs_s, tl, mem);
+        if (!(abl & 4)) load_pnode(p0, ring_s + static_cast<unsigned>((tau + 2) % kPipeRing) * kStepBytes, xs_s, bs_s, tl, mem);
         bar_sync(kPipeBarB, bthreads);
       }
     } else {
@@ -1733,7 +1755,7 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
         if (trace && gw == 2 && lane == 0 && tau >= 64 && tau < 128) ptr_istart[tau - 64] = clock64();
 #endif
         const int i = t - 2 * j;
-        if (row && i >= 1 && i <= n - j - 1) {
+        if (!(abl & 1) && row && i >= 1 && i <= n - j - 1) {
           const int k = rowk + i;
           const double B = bs[k];
           const double E = us[k + 1], W = us[k - 1], N = us[k + dn], Sv = us[k - ds];
@@ -2148,8 +2170,9 @@ void launch_gs(const DevHier2D& hd, const DevLevel2D& lv, double* u, const doubl
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         static int trace = getenv("KB_PIPE_TRACE") ? 1 : 0;
+        static const int ablate = getenv("KB_PIPE_ABLATE") ? atoi(getenv("KB_PIPE_ABLATE")) : 0;  // KB_GS_ABLATE builds
         KB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_gs_pipe, lv, u, b, sweeps, done, lv.pipe_rec, lv.pipe_rec_words,
-                                         lv.pipe_maxreq, trace));
+                                         lv.pipe_maxreq, trace | (ablate << 4)));
         trace &= ~1;
         return;
       }
