@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cmath>
 #include <cstdio>
 #include <map>
@@ -1569,7 +1570,8 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
       bar_sync(kPipeBarA0 + tau % kPipeBarAs, bthreads);
       if (lane == 0) {
         *reinterpret_cast<volatile int*>(&pub_last[w]) = tau;
-        if (abl & 32)
+        if (abl & 128) {
+        } else if (abl & 32)
           asm volatile("red.relaxed.gpu.global.max.s32 [%0], %1;" ::"l"(progress + m), "r"(tau + 2) : "memory");
         else
           asm volatile("red.release.gpu.global.max.s32 [%0], %1;" ::"l"(progress + m), "r"(tau + 2) : "memory");
@@ -1591,36 +1593,48 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
       asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(pm) : "memory");
       return v;
     };
-    // Per step s the fetched value and the polled progress live in slot s % 3:
-    // a fetch issued for step tau + 3 is consumed at the gate of that step two
-    // iterations later, a poll issued for step tau + 5 is checked when step
-    // tau + 5 is fetched, two iterations later -- the loop is unrolled three
-    // times so the slots are named registers and no iteration waits for its
-    // own loads (the previous rotation through register moves did, one L2
-    // round trip per step on the gate's critical path).
-    double F0 = 0.0, F1 = 0.0, F2 = 0.0;
+    // Per step s the fetched value and the polled progress live in stage slot
+    // s % 3 of shared memory: a poll issued for step tau + 5 is checked when
+    // step tau + 5 is fetched, two iterations later, and a fetch issued for
+    // step tau + 3 is consumed at the gate of that step, two iterations later.
+    // Both are cp.async (16-byte, L2) copies committed as one group per
+    // iteration, so the gate waits for the group of two iterations ago only
+    // (cp.async.wait_group 1).  Register loads would not do: every global
+    // load of the warp shares one scoreboard, and consuming any of them waits
+    // for the newest (issued one iteration ago) -- one L2 round trip per step
+    // on the gate's critical path.  The loop is unrolled three times so the
+    // slots are compile-time.
+    __shared__ __align__(16) double fstage[3][32][2];
+    __shared__ __align__(16) int pstage[3][32][4];
     bool F0ok = false, F1ok = false, F2ok = false;
-    int P0 = 0, P1 = 0, P2 = 0;
     bool P0ok = false, P1ok = false, P2ok = false;
     long long t_slow = 0, t_start = clock64();
     int n_slow = 0, n_req = 0;
-    // prologue: poll steps 2 .. 4 (their records are in the ring)
-    for (int st = 2; st < 5 && st < total; ++st) {
+    auto poll16 = [&](int slot, int macro) {
+      cp_async16(smem_addr(&pstage[slot][lane][0]), progress + (macro & ~3));
+    };
+    // prologue: poll steps 2 and 3 (their records are in the ring; iteration -1 polls step 4)
+    for (int st = 2; st < 4 && st < total; ++st) {
       const int* r = recp(st);
-      const int pv = lane < r[0] ? poll(progress + r[2 + 2 * lane]) : 0;
-      if (st == 2) P2 = pv, P2ok = true;
-      if (st == 3) P0 = pv, P0ok = true;
-      if (st == 4) P1 = pv, P1ok = true;
+      if (lane < r[0]) poll16(st % 3, r[2 + 2 * lane]);
+      if (st == 2) P2ok = true;
+      if (st == 3) P0ok = true;
     }
-    // one iteration: gate of step tau + 1 (slot Fg), fetch for step tau + 3
-    // (uses poll Pf, writes Ff), poll for step tau + 5 (writes Pp)
-    auto iteration = [&](int tau, double& Fg, bool& Fgok, double& Ff, bool& Ffok, int& Pf, bool& Pfok, int& Pp,
-                         bool& Ppok) {
+    cp_async_commit();
+    cp_async_commit();  // the group of "iteration -2" (empty)
+    // one iteration: gate of step tau + 1 (slot kg), fetch for step tau + 3
+    // (poll slot kf, fetch slot kf), poll for step tau + 5 (slot kp)
+    auto iteration = [&](int tau, auto kg_c, auto kf_c, auto kp_c, bool& Fgok, bool& Ffok, bool& Pfok, bool& Ppok) {
+      constexpr int kg = decltype(kg_c)::value, kf = decltype(kf_c)::value, kp = decltype(kp_c)::value;
       const int g = tau + 1;
       if (g < total) {
         const int* r = recp(g);
-        const int nreq = r[0], nfetch = r[1];
+        const int2 hd = *reinterpret_cast<const int2*>(r);
+        const int nreq = hd.x, nfetch = hd.y;
         n_req += nreq > 0;
+        cp_async_wait<1>();  // the polls and fetches issued two iterations ago landed
+        double v = 0.0;
+        const int2 fp = lane < nfetch ? *reinterpret_cast<const int2*>(r + 2 + 2 * maxreq + 2 * lane) : make_int2(0, 0);
         if (!(abl & 8) && !Fgok && (nreq > 0 || nfetch > 0)) {
           // slow path: wait for the requirements (the publisher reports this
           // macro's completed steps meanwhile)
@@ -1639,21 +1653,23 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
             }
           }
           __syncwarp();
-          if (lane < nfetch) Fg = __ldcg(u + r[3 + 2 * maxreq + 2 * lane]);
+          if (lane < nfetch) v = __ldcg(u + fp.y);
           t_slow += clock64();
+        } else if (lane < nfetch) {
+          v = fstage[kg][lane][fp.y & 1];
         }
         if (lane < nfetch) {
-          const int dst = r[2 + 2 * maxreq + 2 * lane];
+          const int dst = fp.x;
           KB_ASSERT(dst < S && -1 - dst <= lv.max_ghosts);
-          KB_ASSERT(r[3 + 2 * maxreq + 2 * lane] >= 0 && r[3 + 2 * maxreq + 2 * lane] < lv.M * S);
+          KB_ASSERT(fp.y >= 0 && fp.y < lv.M * S);
           if (dst >= 0)
-            us[dst] = Fg;
+            us[dst] = v;
           else
-            gh[-1 - dst] = Fg;
+            gh[-1 - dst] = v;
         }
         // the step-done barrier of step g reuses the one of step g - kPipeBarAs: its
         // publisher must have passed it (flow control only)
-        if (g >= kPipeBarAs) {
+        if (g >= kPipeBarAs && !(abl & 512)) {
           const int gp = g - kPipeBarAs;
           while (*reinterpret_cast<volatile int*>(&pub_last[gp % kPipePubs]) < gp) {
           }
@@ -1663,34 +1679,46 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
         if (trace && lane == 0 && g >= 64 && g < 128) ptr_sync[g - 64] = clock64();
 #endif
         bar_sync(kPipeBarB, bthreads);  // gate of step g opens
+      } else {
+        cp_async_wait<1>();
       }
       // step tau + 3: fetch when the polled requirements hold
       const int s3 = tau + 3;
       Ffok = false;
-      if (s3 < total && Pfok) {
+      if (s3 < total && Pfok && !(abl & 64)) {
         const int* r = recp(s3);
-        const bool ok = lane >= r[0] || Pf >= r[3 + 2 * lane] + shift(s3);
+        const int2 hd = *reinterpret_cast<const int2*>(r);
+        bool ok = true;
+        if (lane < hd.x) {
+          const int2 rq = *reinterpret_cast<const int2*>(r + 2 + 2 * lane);
+          ok = pstage[kf][lane][rq.x & 3] >= rq.y + shift(s3);
+        }
         if (__all_sync(0xffffffffu, ok)) {
-          if (lane < r[1]) Ff = __ldcg(u + r[3 + 2 * maxreq + 2 * lane]);
+          if (lane < hd.y) cp_async16(smem_addr(&fstage[kf][lane][0]), u + (r[3 + 2 * maxreq + 2 * lane] & ~1));
           Ffok = true;
         }
       }
       // step tau + 5: poll
       const int s5 = tau + 5;
       Ppok = false;
-      if (s5 < total) {
+      if (s5 < total && !(abl & 64)) {
         const int* r = recp(s5);
-        if (lane < r[0]) Pp = poll(progress + r[2 + 2 * lane]);
+        if (lane < r[0]) poll16(kp, r[2 + 2 * lane]);
         Ppok = true;
       }
+      cp_async_commit();
     };
+    using I0 = std::integral_constant<int, 0>;
+    using I1 = std::integral_constant<int, 1>;
+    using I2 = std::integral_constant<int, 2>;
     // step s lives in slot s % 3: tau = -1 + 3q gates step 3q (slot 0), fetches
     // step 3q + 2 (slot 2, poll slot 2), polls step 3q + 4 (slot 1)
     for (int tau = -1; tau < total; tau += 3) {
-      iteration(tau, F0, F0ok, F2, F2ok, P2, P2ok, P1, P1ok);
-      if (tau + 1 < total) iteration(tau + 1, F1, F1ok, F0, F0ok, P0, P0ok, P2, P2ok);
-      if (tau + 2 < total) iteration(tau + 2, F2, F2ok, F1, F1ok, P1, P1ok, P0, P0ok);
+      iteration(tau, I0{}, I2{}, I1{}, F0ok, F2ok, P2ok, P1ok);
+      if (tau + 1 < total) iteration(tau + 1, I1{}, I0{}, I2{}, F1ok, F0ok, P0ok, P2ok);
+      if (tau + 2 < total) iteration(tau + 2, I2{}, I1{}, I0{}, F2ok, F1ok, P1ok, P0ok);
     }
+    cp_async_wait<0>();
     if (trace && lane == 0 && (m % 20 == 0 || m == gridDim.x - 1))
       printf("pipe macro %d: steps %d, gated %d, slow gates %d, cycles in slow gates %lld of %lld\n", m, total, n_req,
              n_slow, t_slow, clock64() - t_start);
@@ -1705,7 +1733,7 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
         if (nx < total && !(abl & 16))
           issue_prog(prog_m, ring_s, rec_src(nx), rring_s, rec_words, nx % T, nx % kPipeRing, lane);
         cp_async_commit();
-        cp_async_wait<kPipeRing - 7>();  // steps and records <= tau + 6 landed (read by the sync warp after A)
+        if (!(abl & 256)) cp_async_wait<kPipeRing - 7>();  // steps and records <= tau + 6 landed (read by the sync warp after A)
         bar_arrive(kPipeBarA0 + tau % kPipeBarAs, bthreads);
         if (tau + 1 < total) bar_sync(kPipeBarB, bthreads);
       }
@@ -2153,7 +2181,13 @@ void launch_gs(const DevHier2D& hd, const DevLevel2D& lv, double* u, const doubl
     const size_t smem = kPipeRing * kStepBytes + static_cast<size_t>(kPipeRing) * lv.pipe_rec_words * 4 +
                         static_cast<size_t>(lv.max_extra) * kProgLaneWords * 8 + (lv.max_ghosts + 1) * 8 +
                         2 * static_cast<size_t>(lv.S) * 8;
-    if (threads <= 384 && smem <= static_cast<size_t>(smem_max)) {
+    static size_t pipe_static = 0;
+    if (!pipe_static) {
+      cudaFuncAttributes fa{};
+      KB_CUDA_CHECK(cudaFuncGetAttributes(&fa, k_gs_pipe));
+      pipe_static = fa.sharedSizeBytes;
+    }
+    if (threads <= 384 && smem + pipe_static <= static_cast<size_t>(smem_max)) {
       set_smem(k_gs_pipe, smem);
       int occ = 0;
       KB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gs_pipe, threads, smem));

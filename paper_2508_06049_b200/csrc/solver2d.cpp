@@ -260,7 +260,7 @@ Solver2D::Solver2D(std::shared_ptr<DeviceHierarchy2D> h, Problem2D p, SolverConf
   }
   bytes += round256(3 * lsize(0) * 8) + round256(2 * M * 8) + round256(lsize(L_) * 8) +
            round256(lsize(std::max(L_ - 1, 0)) * 8) + round256(64 * 8) + round256(8) +
-           round256(sizeof(DevStatus)) + round256(M * 4);
+           round256(sizeof(DevStatus)) + round256((M + 3) / 4 * 16);
   arena_.reserve(bytes);
   u_.assign(L_ + 1, nullptr);
   b_.assign(L_ + 1, nullptr);
@@ -289,7 +289,7 @@ Solver2D::Solver2D(std::shared_ptr<DeviceHierarchy2D> h, Problem2D p, SolverConf
   dot_partial_ = static_cast<double*>(arena_.take(64 * 8));
   dot_out_ = static_cast<double*>(arena_.take(8));
   status_ = static_cast<DevStatus*>(arena_.take(sizeof(DevStatus)));
-  gs_done_ = static_cast<int*>(arena_.take(M * 4));
+  gs_done_ = static_cast<int*>(arena_.take((M + 3) / 4 * 16));  // k_gs_pipe polls 16-byte chunks
 
   KB_CUDA_CHECK(cudaStreamCreateWithFlags(&own_stream_, cudaStreamNonBlocking));
   stream_ = own_stream_;
