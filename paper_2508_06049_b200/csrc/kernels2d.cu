@@ -1494,6 +1494,9 @@ __global__ void __launch_bounds__(kSchedMaxThreads, 1) k_gs_sched(DevLevel2D lv,
 constexpr int kPipeBarB = 1, kPipeBarA0 = 2, kPipeBarAs = 12;  // gate; ring of step-done barriers
 constexpr int kPipePubs = 4;  // publisher warps
 constexpr int kPipeRing = 16;  // step programs + gate records in flight
+constexpr int kPipePRing = 8;  // prefetch warp's records in flight
+constexpr int kPipeStage = 8;  // prefetched steps in flight
+constexpr int kPipeKnown = 64;  // observed-progress cache entries
 
 __device__ __forceinline__ void bar_arrive(int id, int threads) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(threads) : "memory");
@@ -1524,15 +1527,44 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
   const int Wc = gs_group_warps(n), cthreads = 32 * Wc, bthreads = cthreads + 32;
   unsigned char* ring = reinterpret_cast<unsigned char*>(smem);
   int* rring = reinterpret_cast<int*>(ring + (kPipeRing * kStepBytes));
-  unsigned long long* xs = reinterpret_cast<unsigned long long*>(rring + kPipeRing * rec_words);
+  int* pring = rring + kPipeRing * rec_words;  // the prefetch warp's record ring
+  unsigned long long* xs = reinterpret_cast<unsigned long long*>(pring + kPipePRing * rec_words);
   double* gh = reinterpret_cast<double*>(xs + static_cast<size_t>(lv.max_extra) * kProgLaneWords);
   double* us = gh + lv.max_ghosts + 1;
   double* bs = us + S;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const unsigned ring_s = smem_addr(ring), rring_s = smem_addr(rring);
   __shared__ int pub_last[kPipePubs];  // last step-done barrier each publisher passed
-  __shared__ long long ptr_bstart[64], ptr_bend[64], ptr_sync[64], ptr_istart[64], ptr_iend[64];
+  __shared__ __align__(16) double fstage[kPipeStage][32][2];  // prefetched remote values (16-byte copies)
+  __shared__ __align__(8) unsigned long long fbar[kPipeStage];  // slot filled (32 async arrivals)
+  __shared__ int2 known[kPipeKnown];  // prefetch warp: last observed progress per macro (direct mapped)
+  __shared__ int gate_pos;            // last gate opened
+  const unsigned fbar_s = smem_addr(fbar);
+#ifdef KB_GS_TRACE
+  // per-step timeline of macro m for steps 64..127 (KB_PIPE_TRACE, trace builds):
+  // 0 sync ready at B, 1 sync past B, 2 boundary past B, 3 boundary done,
+  // 4 boundary ready at B, 5 interior warp 2 done, 6 last interior warp done,
+  // 7 program warp at A, 8 publisher past A.  "Past" stamps are taken after a
+  // shared load that the barrier orders (a clock read right after a deferred
+  // BAR.SYNC records its issue, not its release)
+  __shared__ long long ptr_t[12][64];
+  __shared__ int ptr_dummy;
+  if (tid == 0) ptr_dummy = 0;
+#define PTR(row, st)                                                                     \
+  do {                                                                                   \
+    if (trace && lane == 0 && (st) >= 64 && (st) < 128) {                                \
+      if (*reinterpret_cast<volatile int*>(&ptr_dummy) != 12345) ptr_t[row][(st) - 64] = clock64(); \
+    }                                                                                    \
+  } while (0)
+#else
+#define PTR(row, st) \
+  do {               \
+  } while (0)
+#endif
   if (tid < kPipePubs) pub_last[tid] = -1;
+  if (tid < kPipeStage) mbar_init(fbar_s + 8u * tid, 32);
+  if (tid < kPipeKnown) known[tid] = make_int2(-1, 0);
+  if (tid == 0) gate_pos = -1;
   const unsigned long long* prog_m = lv.prog + lv.prog_ptr[m];
   const int* rec_m0 = rec + static_cast<size_t>(m) * 2 * T * rec_words;  // sweep-0 records, then sweep >= 1
 
@@ -1561,13 +1593,14 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
   }
   __syncthreads();
 
-  if (warp > Wc) {
+  if (warp > Wc + 1) {
     // ------------------------------------------------ publisher warps (off the gate barrier B): warp
-    // Wc + 1 + w takes the step-done barriers A of steps tau = w mod kPipePubs and raises
+    // Wc + 2 + w takes the step-done barriers A of steps tau = w mod kPipePubs and raises
     // progress[m] to tau + 2 (red.release.gpu.max: the release may finish out of order)
-    const int w = warp - Wc - 1;
+    const int w = warp - Wc - 2;
     for (int tau = w; tau < total; tau += kPipePubs) {
       bar_sync(kPipeBarA0 + tau % kPipeBarAs, bthreads);
+      PTR(8, tau);
       if (lane == 0) {
         *reinterpret_cast<volatile int*>(&pub_last[w]) = tau;
         if (abl & 128) {
@@ -1577,151 +1610,108 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
           asm volatile("red.release.gpu.global.max.s32 [%0], %1;" ::"l"(progress + m), "r"(tau + 2) : "memory");
       }
     }
-  } else if (warp == Wc) {
-    // ------------------------------------------------ sync warp
-    // per iteration tau (between gate tau + 1 and the end of step tau + 1):
-    //   gate tau + 1: store the values fetched two iterations ago, arrive on B
-    //   step tau + 3: if the requirements polled two iterations ago hold, fetch
-    //   step tau + 5: poll the requirements (relaxed loads; the data loads are
-    //                 issued only after the flags were observed, from L2, where
-    //                 the producer's st.release.gpu made them visible first)
-    auto recp = [&](int tau) { return rring + (tau % kPipeRing) * rec_words; };
-    // sweeps >= 1 reuse table 1 (tables exist for sweeps <= 2: the shift is 0)
-    auto shift = [&](int tau) { return 0 * tau; };
-    auto poll = [&](const int* pm) {
-      int v;
-      asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(pm) : "memory");
-      return v;
+  } else if (warp == Wc + 1) {
+    // ------------------------------------------------ prefetch warp
+    // Runs up to kPipeStage steps ahead of the gate.  Per step s: wait until
+    // the step's requirements hold (other macros' progress; an observed
+    // progress value is remembered, so a requirement already met costs no
+    // load), copy the step's remote values from L2 into stage slot
+    // s % kPipeStage (cp.async, issued after the acquire that observed the
+    // producer's release) and arrive on the slot's mbarrier when the copies
+    // land (cp.async.mbarrier.arrive).  Its own record ring is filled by
+    // cp.async kPipePRing - 1 steps ahead.
+    const unsigned pring_s = smem_addr(pring);
+    auto issue_rec = [&](int st) {
+      const char* rsrc = reinterpret_cast<const char*>(rec_src(st) + static_cast<size_t>(st % T) * rec_words);
+      const unsigned rdst = pring_s + static_cast<unsigned>((st % kPipePRing) * rec_words * 4);
+      for (int c = lane; c < rec_words / 4; c += 32) cp_async16(rdst + 16u * c, rsrc + 16 * c);
     };
-    // Per step s the fetched value and the polled progress live in stage slot
-    // s % 3 of shared memory: a poll issued for step tau + 5 is checked when
-    // step tau + 5 is fetched, two iterations later, and a fetch issued for
-    // step tau + 3 is consumed at the gate of that step, two iterations later.
-    // Both are cp.async (16-byte, L2) copies committed as one group per
-    // iteration, so the gate waits for the group of two iterations ago only
-    // (cp.async.wait_group 1).  Register loads would not do: every global
-    // load of the warp shares one scoreboard, and consuming any of them waits
-    // for the newest (issued one iteration ago) -- one L2 round trip per step
-    // on the gate's critical path.  The loop is unrolled three times so the
-    // slots are compile-time.
-    __shared__ __align__(16) double fstage[3][32][2];
-    __shared__ __align__(16) int pstage[3][32][4];
-    bool F0ok = false, F1ok = false, F2ok = false;
-    bool P0ok = false, P1ok = false, P2ok = false;
-    long long t_slow = 0, t_start = clock64();
-    int n_slow = 0, n_req = 0;
-    auto poll16 = [&](int slot, int macro) {
-      cp_async16(smem_addr(&pstage[slot][lane][0]), progress + (macro & ~3));
-    };
-    // prologue: poll steps 2 and 3 (their records are in the ring; iteration -1 polls step 4)
-    for (int st = 2; st < 4 && st < total; ++st) {
-      const int* r = recp(st);
-      if (lane < r[0]) poll16(st % 3, r[2 + 2 * lane]);
-      if (st == 2) P2ok = true;
-      if (st == 3) P0ok = true;
+    for (int st = 0; st < kPipePRing - 1; ++st) {
+      if (st < total) issue_rec(st);
+      cp_async_commit();
     }
-    cp_async_commit();
-    cp_async_commit();  // the group of "iteration -2" (empty)
-    // one iteration: gate of step tau + 1 (slot kg), fetch for step tau + 3
-    // (poll slot kf, fetch slot kf), poll for step tau + 5 (slot kp)
-    auto iteration = [&](int tau, auto kg_c, auto kf_c, auto kp_c, bool& Fgok, bool& Ffok, bool& Pfok, bool& Ppok) {
-      constexpr int kg = decltype(kg_c)::value, kf = decltype(kf_c)::value, kp = decltype(kp_c)::value;
-      const int g = tau + 1;
-      if (g < total) {
-        const int* r = recp(g);
-        const int2 hd = *reinterpret_cast<const int2*>(r);
-        const int nreq = hd.x, nfetch = hd.y;
-        n_req += nreq > 0;
-        cp_async_wait<1>();  // the polls and fetches issued two iterations ago landed
-        double v = 0.0;
-        const int2 fp = lane < nfetch ? *reinterpret_cast<const int2*>(r + 2 + 2 * maxreq + 2 * lane) : make_int2(0, 0);
-        if (!(abl & 8) && !Fgok && (nreq > 0 || nfetch > 0)) {
-          // slow path: wait for the requirements (the publisher reports this
-          // macro's completed steps meanwhile)
-          ++n_slow;
-          t_slow -= clock64();
-          if (lane < nreq) {
-            const int* pm = progress + r[2 + 2 * lane];
-            const int need = r[3 + 2 * lane] + shift(g);
-            long long spins = 0;
-            while (ld_acquire(pm) < need) {
-              if (++spins == (1ll << 24)) {  // a broken table would deadlock: fail loudly instead
-                printf("k_gs_pipe: macro %d step %d waits for macro %d progress %d (has %d)\n", m, g,
-                       r[2 + 2 * lane], need, ld_acquire(pm));
-                __trap();
-              }
+    long long t_wait = 0, t_start = clock64();
+    int n_wait = 0;
+    for (int st = 0, slot = 0; st < total; ++st, slot = (slot + 1 == kPipeStage ? 0 : slot + 1)) {
+      cp_async_wait<kPipePRing - 2>();  // record st landed (every lane's part)
+      __syncwarp();
+      const int* r = pring + (st % kPipePRing) * rec_words;
+      const int2 hd = *reinterpret_cast<const int2*>(r);
+      // slot reuse: the gate of step st - kPipeStage has read it
+      if (st >= kPipeStage)
+        while (*reinterpret_cast<volatile int*>(&gate_pos) < st - kPipeStage) {
+        }
+      PTR(9, st);
+      if (lane < hd.x && !(abl & 8)) {
+        const int2 rq = *reinterpret_cast<const int2*>(r + 2 + 2 * lane);
+        const int2 kn = known[rq.x & (kPipeKnown - 1)];
+        if (kn.x != rq.x || kn.y < rq.y) {
+          const int* pm = progress + rq.x;
+          int v;
+          long long spins = 0;
+          if (trace) ++n_wait, t_wait -= clock64();
+          while ((v = ld_acquire(pm)) < rq.y) {
+            if (++spins == (1ll << 24)) {  // a broken table would deadlock: fail loudly instead
+              printf("k_gs_pipe: macro %d step %d waits for macro %d progress %d (has %d)\n", m, st, rq.x, rq.y, v);
+              __trap();
             }
           }
-          __syncwarp();
-          if (lane < nfetch) v = __ldcg(u + fp.y);
-          t_slow += clock64();
-        } else if (lane < nfetch) {
-          v = fstage[kg][lane][fp.y & 1];
-        }
-        if (lane < nfetch) {
-          const int dst = fp.x;
-          KB_ASSERT(dst < S && -1 - dst <= lv.max_ghosts);
-          KB_ASSERT(fp.y >= 0 && fp.y < lv.M * S);
-          if (dst >= 0)
-            us[dst] = v;
-          else
-            gh[-1 - dst] = v;
-        }
-        // the step-done barrier of step g reuses the one of step g - kPipeBarAs: its
-        // publisher must have passed it (flow control only)
-        if (g >= kPipeBarAs && !(abl & 512)) {
-          const int gp = g - kPipeBarAs;
-          while (*reinterpret_cast<volatile int*>(&pub_last[gp % kPipePubs]) < gp) {
-          }
-        }
-        __syncwarp();
-#ifdef KB_GS_TRACE
-        if (trace && lane == 0 && g >= 64 && g < 128) ptr_sync[g - 64] = clock64();
-#endif
-        bar_sync(kPipeBarB, bthreads);  // gate of step g opens
-      } else {
-        cp_async_wait<1>();
-      }
-      // step tau + 3: fetch when the polled requirements hold
-      const int s3 = tau + 3;
-      Ffok = false;
-      if (s3 < total && Pfok && !(abl & 64)) {
-        const int* r = recp(s3);
-        const int2 hd = *reinterpret_cast<const int2*>(r);
-        bool ok = true;
-        if (lane < hd.x) {
-          const int2 rq = *reinterpret_cast<const int2*>(r + 2 + 2 * lane);
-          ok = pstage[kf][lane][rq.x & 3] >= rq.y + shift(s3);
-        }
-        if (__all_sync(0xffffffffu, ok)) {
-          if (lane < hd.y) cp_async16(smem_addr(&fstage[kf][lane][0]), u + (r[3 + 2 * maxreq + 2 * lane] & ~1));
-          Ffok = true;
+          if (trace) t_wait += clock64();
+          known[rq.x & (kPipeKnown - 1)] = make_int2(rq.x, v);
         }
       }
-      // step tau + 5: poll
-      const int s5 = tau + 5;
-      Ppok = false;
-      if (s5 < total && !(abl & 64)) {
-        const int* r = recp(s5);
-        if (lane < r[0]) poll16(kp, r[2 + 2 * lane]);
-        Ppok = true;
+      __syncwarp();
+      PTR(10, st);
+      if (lane < hd.y && !(abl & 64)) {
+        const int src = r[3 + 2 * maxreq + 2 * lane];
+        KB_ASSERT(src >= 0 && src < lv.M * S);
+        cp_async16(smem_addr(&fstage[slot][lane][0]), u + (src & ~1));
       }
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(fbar_s + 8u * slot) : "memory");
+      if (st + kPipePRing - 1 < total) issue_rec(st + kPipePRing - 1);
       cp_async_commit();
-    };
-    using I0 = std::integral_constant<int, 0>;
-    using I1 = std::integral_constant<int, 1>;
-    using I2 = std::integral_constant<int, 2>;
-    // step s lives in slot s % 3: tau = -1 + 3q gates step 3q (slot 0), fetches
-    // step 3q + 2 (slot 2, poll slot 2), polls step 3q + 4 (slot 1)
-    for (int tau = -1; tau < total; tau += 3) {
-      iteration(tau, I0{}, I2{}, I1{}, F0ok, F2ok, P2ok, P1ok);
-      if (tau + 1 < total) iteration(tau + 1, I1{}, I0{}, I2{}, F1ok, F0ok, P0ok, P2ok);
-      if (tau + 2 < total) iteration(tau + 2, I2{}, I1{}, I0{}, F2ok, F1ok, P1ok, P0ok);
+      PTR(11, st);
     }
     cp_async_wait<0>();
     if (trace && lane == 0 && (m % 20 == 0 || m == gridDim.x - 1))
-      printf("pipe macro %d: steps %d, gated %d, slow gates %d, cycles in slow gates %lld of %lld\n", m, total, n_req,
-             n_slow, t_slow, clock64() - t_start);
+      printf("pipe macro %d: steps %d, prefetch waits %d, cycles waiting %lld of %lld\n", m, total, n_wait, t_wait,
+             clock64() - t_start);
+  } else if (warp == Wc) {
+    // ------------------------------------------------ gate warp
+    // gate of step g: wait for the prefetched values of step g (slot mbarrier),
+    // store them into the lattice / ghost slots, arrive on B.  Records <= g + 5
+    // are visible here: the program warp waited for them before arriving on
+    // the B of step g - 1.
+    auto recp = [&](int tau) { return rring + (tau % kPipeRing) * rec_words; };
+    for (int g = 0, slot = 0, ph = 0; g < total; ++g) {
+      const int* r = recp(g);
+      const int nfetch = r[1];
+      const int2 fp = lane < nfetch ? *reinterpret_cast<const int2*>(r + 2 + 2 * maxreq + 2 * lane) : make_int2(0, 0);
+      mbar_wait(fbar_s + 8u * slot, ph);
+      if (lane < nfetch) {
+        const double v = fstage[slot][lane][fp.y & 1];
+        const int dst = fp.x;
+        KB_ASSERT(dst < S && -1 - dst <= lv.max_ghosts);
+        if (dst >= 0)
+          us[dst] = v;
+        else
+          gh[-1 - dst] = v;
+      }
+      __syncwarp();
+      if (lane == 0) *reinterpret_cast<volatile int*>(&gate_pos) = g;
+      if (++slot == kPipeStage) slot = 0, ph ^= 1;
+      // the step-done barrier of step g reuses the one of step g - kPipeBarAs: its
+      // publisher must have passed it (flow control only)
+      if (g >= kPipeBarAs && !(abl & 512)) {
+        const int gp = g - kPipeBarAs;
+        while (*reinterpret_cast<volatile int*>(&pub_last[gp % kPipePubs]) < gp) {
+        }
+      }
+      __syncwarp();
+      PTR(0, g);
+      bar_sync(kPipeBarB, bthreads);  // gate of step g opens
+      PTR(1, g);
+    }
   } else {
     // ------------------------------------------------ consumers (group_sweep roles)
     const int gw = warp;
@@ -1734,6 +1724,7 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
           issue_prog(prog_m, ring_s, rec_src(nx), rring_s, rec_words, nx % T, nx % kPipeRing, lane);
         cp_async_commit();
         if (!(abl & 256)) cp_async_wait<kPipeRing - 7>();  // steps and records <= tau + 6 landed (read by the sync warp after A)
+        PTR(7, tau);
         bar_arrive(kPipeBarA0 + tau % kPipeBarAs, bthreads);
         if (tau + 1 < total) bar_sync(kPipeBarB, bthreads);
       }
@@ -1746,27 +1737,21 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
       PNode p0, p1;
       load_pnode(p0, ring_s, xs_s, bs_s, tl, mem);
       for (int tau = 0; tau < total; tau += 2) {
-#ifdef KB_GS_TRACE
-        if (trace && lane == 0 && tau >= 64 && tau < 128) ptr_bstart[tau - 64] = clock64();
-#endif
+        PTR(2, tau);
         if (!(abl & 2)) relax_pipe(p0, gh_s, us_s, u, lv.wr, lane, um, lv.max_ghosts + 1 + S, S, lv.M * S);
-#ifdef KB_GS_TRACE
-        if (trace && lane == 0 && tau >= 64 && tau < 128) ptr_bend[tau - 64] = clock64() + (ld_s64(us_s) == 12345.0);
-#endif
+        PTR(3, tau);
         bar_arrive(kPipeBarA0 + tau % kPipeBarAs, bthreads);
         if (tau + 1 >= total) break;
         if (!(abl & 4)) load_pnode(p1, ring_s + static_cast<unsigned>((tau + 1) % kPipeRing) * kStepBytes, xs_s, bs_s, tl, mem);
+        PTR(4, tau + 1);
         bar_sync(kPipeBarB, bthreads);
-#ifdef KB_GS_TRACE
-        if (trace && lane == 0 && tau + 1 >= 64 && tau + 1 < 128) ptr_bstart[tau + 1 - 64] = clock64();
-#endif
+        PTR(2, tau + 1);
         if (!(abl & 2)) relax_pipe(p1, gh_s, us_s, u, lv.wr, lane, um, lv.max_ghosts + 1 + S, S, lv.M * S);
-#ifdef KB_GS_TRACE
-        if (trace && lane == 0 && tau + 1 >= 64 && tau + 1 < 128) ptr_bend[tau + 1 - 64] = clock64() + (ld_s64(us_s) == 12345.0);
-#endif
+        PTR(3, tau + 1);
         bar_arrive(kPipeBarA0 + (tau + 1) % kPipeBarAs, bthreads);
         if (tau + 2 >= total) break;
         if (!(abl & 4)) load_pnode(p0, ring_s + static_cast<unsigned>((tau + 2) % kPipeRing) * kStepBytes, xs_s, bs_s, tl, mem);
+        PTR(4, tau + 2);
         bar_sync(kPipeBarB, bthreads);
       }
     } else {
@@ -1779,9 +1764,6 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
       const int dn = n + 1 - j, dnw = n - j, ds = n + 2 - j;
       int t = 0;  // tau mod T, kept incrementally (no division on the step path)
       for (int tau = 0; tau < total; ++tau, t = (t + 1 == T ? 0 : t + 1)) {
-#ifdef KB_GS_TRACE
-        if (trace && gw == 2 && lane == 0 && tau >= 64 && tau < 128) ptr_istart[tau - 64] = clock64();
-#endif
         const int i = t - 2 * j;
         if (!(abl & 1) && row && i >= 1 && i <= n - j - 1) {
           const int k = rowk + i;
@@ -1797,9 +1779,8 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
           us[k] = v;
           if (j == 1 || i == 1 || i + j == n - 1) um[k] = v;  // exported: ghost of a neighbour
         }
-#ifdef KB_GS_TRACE
-        if (trace && gw == 2 && lane == 0 && tau >= 64 && tau < 128) ptr_iend[tau - 64] = clock64() + (us[0] == 12345.0);
-#endif
+        if (gw == 2) PTR(5, tau);
+        if (gw == Wc - 1) PTR(6, tau);
         bar_arrive(kPipeBarA0 + tau % kPipeBarAs, bthreads);
         if (tau + 1 < total) bar_sync(kPipeBarB, bthreads);
       }
@@ -1807,12 +1788,16 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
   }
   __syncthreads();
 #ifdef KB_GS_TRACE
-  if (trace && m == 0 && tid == 0)
-    for (int q = 0; q < 12; ++q)
-      printf("step %d: boundary relax %lld, boundary end->next start %lld, interior %lld, sync arrives at B %lld before boundary start\n",
-             64 + q, ptr_bend[q] - ptr_bstart[q], ptr_bstart[q + 1] - ptr_bend[q], ptr_iend[q] - ptr_istart[q],
-             ptr_bstart[q + 1] - ptr_sync[q + 1]);
+  if (trace && (m == 0 || m == gridDim.x / 2) && tid == 0)
+    for (int q = 0; q < 24; ++q) {
+      const long long b0 = ptr_t[2][q];  // boundary past B of step 64 + q
+      printf("m %d step %d: %6lld %6lld %6lld %6lld %6lld %6lld %6lld %6lld %6lld | next B %6lld | prefetch %6lld %6lld %6lld\n", m, 64 + q,
+             ptr_t[0][q] - b0, ptr_t[1][q] - b0, ptr_t[2][q] - b0, ptr_t[3][q] - b0, ptr_t[4][q] - b0,
+             ptr_t[5][q] - b0, ptr_t[6][q] - b0, ptr_t[7][q] - b0, ptr_t[8][q] - b0, ptr_t[2][q + 1] - b0,
+             ptr_t[9][q] - b0, ptr_t[10][q] - b0, ptr_t[11][q] - b0);
+    }
 #endif
+#undef PTR
   // lattice-interior nodes back to global memory (interface copies are kept
   // current by every relaxation)
   for (int k = tid; k < S; k += blockDim.x) {
@@ -2177,8 +2162,8 @@ void launch_gs(const DevHier2D& hd, const DevLevel2D& lv, double* u, const doubl
   }
   if (lv.pipe_rec && sweeps <= 2 && gs_pipe_enabled()) {
     // fine-grained pipelined smoother: one resident CTA per macro
-    const int threads = 32 * (gs_group_warps(lv.n) + 1 + kPipePubs);
-    const size_t smem = kPipeRing * kStepBytes + static_cast<size_t>(kPipeRing) * lv.pipe_rec_words * 4 +
+    const int threads = 32 * (gs_group_warps(lv.n) + 2 + kPipePubs);
+    const size_t smem = kPipeRing * kStepBytes + static_cast<size_t>(kPipeRing + kPipePRing) * lv.pipe_rec_words * 4 +
                         static_cast<size_t>(lv.max_extra) * kProgLaneWords * 8 + (lv.max_ghosts + 1) * 8 +
                         2 * static_cast<size_t>(lv.S) * 8;
     static size_t pipe_static = 0;

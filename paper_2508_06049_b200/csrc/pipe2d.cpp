@@ -184,6 +184,30 @@ void build_level(const Hierarchy2D& h, Level2D& lv) {
     for (const StepRec& R : recs) nr += R.req.size(), nf += R.fetch.size();
     std::fprintf(stderr, "pipe tables M=%d n=%d: maxreq %d maxfetch %d, total req %lld fetch %lld (%.2f / %.2f per step)\n", M, n,
                  P.maxreq, P.maxfetch, nr, nf, double(nr) / recs.size(), double(nf) / recs.size());
+    // critical path of the two sweeps under a unit model: a step costs c, a
+    // cross-macro requirement adds the hand-off latency h (development aid)
+    for (double h : {0.0, 1.0, 2.0, 4.0}) {
+      std::vector<double> F(static_cast<std::size_t>(M) * 2 * T, 0.0);
+      std::vector<int> hops(F.size(), 0);
+      for (int sw = 0; sw < 2; ++sw)
+        for (int m = 0; m < M; ++m)
+          for (int t = 0; t < T; ++t) {
+            const int tau = sw * T + t;
+            const std::size_t e = static_cast<std::size_t>(m) * 2 * T + tau;
+            double start = tau > 0 ? F[e - 1] : 0.0;
+            int hp = tau > 0 ? hops[e - 1] : 0;
+            for (const auto& [m2, p] : recs[(static_cast<std::size_t>(m) * 2 + sw) * T + t].req) {
+              const std::size_t e2 = static_cast<std::size_t>(m2) * 2 * T + (p - 2);
+              if (F[e2] + h > start) start = F[e2] + h, hp = hops[e2] + 1;
+            }
+            F[e] = start + 1.0;
+            hops[e] = hp;
+          }
+      std::size_t best = 0;
+      for (std::size_t e = 0; e < F.size(); ++e)
+        if (F[e] > F[best]) best = e;
+      std::fprintf(stderr, "  critical path (h = %.0f c): %.0f c, %d hand-offs (%d steps per macro)\n", h, F[best], hops[best], 2 * T);
+    }
   }
 }
 }  // namespace
