@@ -107,9 +107,10 @@ struct GsSched2D {
 // macros relaxed, ghost values of neighbouring lattices).  progress[m] counts
 // completed steps + 1 (published after every step); a fetch for step tau is
 // done by the end of step tau - 1 of its macro.
-//   record (int32 words, stride rec_words): nreq, nfetch, then maxreq pairs
-//   (macro, progress), then maxfetch pairs (destination: lattice index >= 0 or
-//   -1 - ghost slot, source: global offset)
+//   record: kPipeLanes int4 entries (rec_words = 4 kPipeLanes), entry k =
+//   {k-th requirement: macro or -1, progress; k-th fetch: source global
+//   offset or -1, destination: lattice index >= 0 or -1 - ghost slot}
+constexpr int kPipeLanes = 16;
 struct PipeTables2D {
   bool ok = false;
   int maxreq = 0, maxfetch = 0, rec_words = 0;

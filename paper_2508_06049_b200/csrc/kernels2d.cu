@@ -1494,23 +1494,20 @@ __global__ void __launch_bounds__(kSchedMaxThreads, 1) k_gs_sched(DevLevel2D lv,
 constexpr int kPipeBarB = 1, kPipeBarA0 = 2, kPipeBarAs = 12;  // gate; ring of step-done barriers
 constexpr int kPipePubs = 4;  // publisher warps
 constexpr int kPipeRing = 16;  // step programs + gate records in flight
-constexpr int kPipePRing = 8;  // prefetch warp's records in flight
-constexpr int kPipeStage = 8;  // prefetched steps in flight
+constexpr int kPipePRing = 16;  // record ring of the prefetch / gate warps (power of two)
+constexpr int kPipePAhead = 8;  // records requested ahead of the prefetch warp
+constexpr int kPipeStage = 8;   // prefetched steps in flight (power of two, <= kPipePRing - kPipePAhead)
 constexpr int kPipeKnown = 64;  // observed-progress cache entries
 
 __device__ __forceinline__ void bar_arrive(int id, int threads) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
-__device__ __forceinline__ void issue_prog(const unsigned long long* prog_m, unsigned ring_s, const int* rec_m,
-                                           unsigned rring_s, int rec_words, int t, int slot, int lane) {
+__device__ __forceinline__ void issue_prog(const unsigned long long* prog_m, unsigned ring_s, int t, int slot, int lane) {
   const char* src = reinterpret_cast<const char*>(prog_m + static_cast<size_t>(t) * kProgStepWords);
   const unsigned dst = ring_s + static_cast<unsigned>(slot) * kStepBytes;
   for (int c = lane; c < 48; c += 32)
     cp_async16(dst + static_cast<unsigned>(kLaneStride) * (c >> 3) + 16u * (c & 7), src + 16 * c);
-  const char* rsrc = reinterpret_cast<const char*>(rec_m + static_cast<size_t>(t) * rec_words);
-  const unsigned rdst = rring_s + static_cast<unsigned>(slot * rec_words * 4);
-  for (int c = lane; c < rec_words / 4; c += 32) cp_async16(rdst + 16u * c, rsrc + 16 * c);
 }
 
 __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, const double* __restrict__ b,
@@ -1526,14 +1523,13 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
   const int S = lv.S, n = lv.n, T = 2 * n + 1, m = blockIdx.x, total = sweeps * T;
   const int Wc = gs_group_warps(n), cthreads = 32 * Wc, bthreads = cthreads + 32;
   unsigned char* ring = reinterpret_cast<unsigned char*>(smem);
-  int* rring = reinterpret_cast<int*>(ring + (kPipeRing * kStepBytes));
-  int* pring = rring + kPipeRing * rec_words;  // the prefetch warp's record ring
-  unsigned long long* xs = reinterpret_cast<unsigned long long*>(pring + kPipePRing * rec_words);
+  int* pring = reinterpret_cast<int*>(ring + (kPipeRing * kStepBytes));  // gate records (prefetch warp's ring)
+  unsigned long long* xs = reinterpret_cast<unsigned long long*>(pring + kPipePRing * 4 * kPipeLanes);
   double* gh = reinterpret_cast<double*>(xs + static_cast<size_t>(lv.max_extra) * kProgLaneWords);
   double* us = gh + lv.max_ghosts + 1;
   double* bs = us + S;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const unsigned ring_s = smem_addr(ring), rring_s = smem_addr(rring);
+  const unsigned ring_s = smem_addr(ring);
   __shared__ int pub_last[kPipePubs];  // last step-done barrier each publisher passed
   __shared__ __align__(16) double fstage[kPipeStage][32][2];  // prefetched remote values (16-byte copies)
   __shared__ __align__(8) unsigned long long fbar[kPipeStage];  // slot filled (32 async arrivals)
@@ -1566,9 +1562,8 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
   if (tid < kPipeKnown) known[tid] = make_int2(-1, 0);
   if (tid == 0) gate_pos = -1;
   const unsigned long long* prog_m = lv.prog + lv.prog_ptr[m];
-  const int* rec_m0 = rec + static_cast<size_t>(m) * 2 * T * rec_words;  // sweep-0 records, then sweep >= 1
-
-  auto rec_src = [&](int tau) { return rec_m0 + (tau >= T ? static_cast<size_t>(T) * rec_words : 0); };
+  // sweep-0 records, then sweep-1 records (sweeps <= 2): step tau's record is rec_m0[tau]
+  const int4* rec_m0 = reinterpret_cast<const int4*>(rec) + static_cast<size_t>(m) * 2 * T * kPipeLanes;
   double* um = u + static_cast<size_t>(m) * S;
 
   // initial state: lattice, b, extra records, ghosts; the head of the step stream
@@ -1585,7 +1580,7 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
     if (tid == 0) gh[lv.max_ghosts] = 0.0;
     if (warp == 1) {
       for (int tau = 0; tau < kPipeRing - 1 && tau < total; ++tau) {
-        issue_prog(prog_m, ring_s, rec_src(tau), rring_s, rec_words, tau % T, tau % kPipeRing, lane);
+        issue_prog(prog_m, ring_s, tau % T, tau % kPipeRing, lane);
         cp_async_commit();
       }
       cp_async_wait<0>();
@@ -1618,57 +1613,58 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
     // load), copy the step's remote values from L2 into stage slot
     // s % kPipeStage (cp.async, issued after the acquire that observed the
     // producer's release) and arrive on the slot's mbarrier when the copies
-    // land (cp.async.mbarrier.arrive).  Its own record ring is filled by
-    // cp.async kPipePRing - 1 steps ahead.
+    // -- and every earlier cp.async of the lane, among them the step's record
+    // the gate reads -- have landed (cp.async.mbarrier.arrive).  Records
+    // (one int4 per lane, PipeTables2D) stream into a ring kPipePAhead steps
+    // ahead.
     const unsigned pring_s = smem_addr(pring);
+    const int4* prg = reinterpret_cast<const int4*>(pring);
     auto issue_rec = [&](int st) {
-      const char* rsrc = reinterpret_cast<const char*>(rec_src(st) + static_cast<size_t>(st % T) * rec_words);
-      const unsigned rdst = pring_s + static_cast<unsigned>((st % kPipePRing) * rec_words * 4);
-      for (int c = lane; c < rec_words / 4; c += 32) cp_async16(rdst + 16u * c, rsrc + 16 * c);
+      if (lane < kPipeLanes)
+        cp_async16(pring_s + static_cast<unsigned>((st & (kPipePRing - 1)) * kPipeLanes + lane) * 16u,
+                   rec_m0 + static_cast<size_t>(st) * kPipeLanes + lane);
     };
-    for (int st = 0; st < kPipePRing - 1; ++st) {
+    for (int st = 0; st < kPipePAhead; ++st) {
       if (st < total) issue_rec(st);
       cp_async_commit();
     }
     long long t_wait = 0, t_start = clock64();
     int n_wait = 0;
-    for (int st = 0, slot = 0; st < total; ++st, slot = (slot + 1 == kPipeStage ? 0 : slot + 1)) {
-      cp_async_wait<kPipePRing - 2>();  // record st landed (every lane's part)
+    for (int st = 0, slot = 0; st < total; ++st, slot = (slot + 1) & (kPipeStage - 1)) {
+      cp_async_wait<kPipePAhead - 1>();  // record st landed (every lane's part)
       __syncwarp();
-      const int* r = pring + (st % kPipePRing) * rec_words;
-      const int2 hd = *reinterpret_cast<const int2*>(r);
-      // slot reuse: the gate of step st - kPipeStage has read it
+      // slot reuse: the gate of step st - kPipeStage has read its values and
+      // the record the ring slot of st + kPipePAhead held
       if (st >= kPipeStage)
         while (*reinterpret_cast<volatile int*>(&gate_pos) < st - kPipeStage) {
         }
       PTR(9, st);
-      if (lane < hd.x && !(abl & 8)) {
-        const int2 rq = *reinterpret_cast<const int2*>(r + 2 + 2 * lane);
-        const int2 kn = known[rq.x & (kPipeKnown - 1)];
-        if (kn.x != rq.x || kn.y < rq.y) {
-          const int* pm = progress + rq.x;
+      const int4 e = lane < kPipeLanes ? prg[(st & (kPipePRing - 1)) * kPipeLanes + lane] : make_int4(-1, 0, -1, 0);
+      if (e.x >= 0 && !(abl & 8)) {
+        const int2 kn = known[e.x & (kPipeKnown - 1)];
+        if (kn.x != e.x || kn.y < e.y) {
+          const int* pm = progress + e.x;
           int v;
           long long spins = 0;
           if (trace) ++n_wait, t_wait -= clock64();
-          while ((v = ld_acquire(pm)) < rq.y) {
+          while ((v = ld_acquire(pm)) < e.y) {
             if (++spins == (1ll << 24)) {  // a broken table would deadlock: fail loudly instead
-              printf("k_gs_pipe: macro %d step %d waits for macro %d progress %d (has %d)\n", m, st, rq.x, rq.y, v);
+              printf("k_gs_pipe: macro %d step %d waits for macro %d progress %d (has %d)\n", m, st, e.x, e.y, v);
               __trap();
             }
           }
           if (trace) t_wait += clock64();
-          known[rq.x & (kPipeKnown - 1)] = make_int2(rq.x, v);
+          known[e.x & (kPipeKnown - 1)] = make_int2(e.x, v);
         }
       }
       __syncwarp();
       PTR(10, st);
-      if (lane < hd.y && !(abl & 64)) {
-        const int src = r[3 + 2 * maxreq + 2 * lane];
-        KB_ASSERT(src >= 0 && src < lv.M * S);
-        cp_async16(smem_addr(&fstage[slot][lane][0]), u + (src & ~1));
+      if (e.z >= 0 && !(abl & 64)) {
+        KB_ASSERT(e.z < lv.M * S);
+        cp_async16(smem_addr(&fstage[slot][lane][0]), u + (e.z & ~1));
       }
       asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(fbar_s + 8u * slot) : "memory");
-      if (st + kPipePRing - 1 < total) issue_rec(st + kPipePRing - 1);
+      if (st + kPipePAhead < total) issue_rec(st + kPipePAhead);
       cp_async_commit();
       PTR(11, st);
     }
@@ -1678,24 +1674,22 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
              clock64() - t_start);
   } else if (warp == Wc) {
     // ------------------------------------------------ gate warp
-    // gate of step g: wait for the prefetched values of step g (slot mbarrier),
-    // store them into the lattice / ghost slots, arrive on B.  Records <= g + 5
-    // are visible here: the program warp waited for them before arriving on
-    // the B of step g - 1.
-    auto recp = [&](int tau) { return rring + (tau % kPipeRing) * rec_words; };
+    // gate of step g: wait for the prefetched values of step g (slot mbarrier,
+    // which also covers the step's record), store them into the lattice /
+    // ghost slots, arrive on B
+    const int2* prg = reinterpret_cast<const int2*>(pring);
     for (int g = 0, slot = 0, ph = 0; g < total; ++g) {
-      const int* r = recp(g);
-      const int nfetch = r[1];
-      const int2 fp = lane < nfetch ? *reinterpret_cast<const int2*>(r + 2 + 2 * maxreq + 2 * lane) : make_int2(0, 0);
       mbar_wait(fbar_s + 8u * slot, ph);
-      if (lane < nfetch) {
-        const double v = fstage[slot][lane][fp.y & 1];
-        const int dst = fp.x;
-        KB_ASSERT(dst < S && -1 - dst <= lv.max_ghosts);
-        if (dst >= 0)
-          us[dst] = v;
-        else
-          gh[-1 - dst] = v;
+      if (lane < kPipeLanes) {
+        const int2 e = prg[((g & (kPipePRing - 1)) * kPipeLanes + lane) * 2 + 1];  // {source, destination}
+        if (e.x >= 0) {
+          const double v = fstage[slot][lane][e.x & 1];
+          KB_ASSERT(e.y < S && -1 - e.y <= lv.max_ghosts);
+          if (e.y >= 0)
+            us[e.y] = v;
+          else
+            gh[-1 - e.y] = v;
+        }
       }
       __syncwarp();
       if (lane == 0) *reinterpret_cast<volatile int*>(&gate_pos) = g;
@@ -1721,7 +1715,7 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
       for (int tau = 0; tau < total; ++tau) {
         const int nx = tau + kPipeRing - 1;
         if (nx < total && !(abl & 16))
-          issue_prog(prog_m, ring_s, rec_src(nx), rring_s, rec_words, nx % T, nx % kPipeRing, lane);
+          issue_prog(prog_m, ring_s, nx % T, nx % kPipeRing, lane);
         cp_async_commit();
         if (!(abl & 256)) cp_async_wait<kPipeRing - 7>();  // steps and records <= tau + 6 landed (read by the sync warp after A)
         PTR(7, tau);
@@ -1791,10 +1785,11 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
   if (trace && (m == 0 || m == gridDim.x / 2) && tid == 0)
     for (int q = 0; q < 24; ++q) {
       const long long b0 = ptr_t[2][q];  // boundary past B of step 64 + q
-      printf("m %d step %d: %6lld %6lld %6lld %6lld %6lld %6lld %6lld %6lld %6lld | next B %6lld | prefetch %6lld %6lld %6lld\n", m, 64 + q,
+      printf("m %d step %d: %6lld %6lld %6lld %6lld %6lld %6lld %6lld %6lld %6lld | next B %6lld\n", m, 64 + q,
              ptr_t[0][q] - b0, ptr_t[1][q] - b0, ptr_t[2][q] - b0, ptr_t[3][q] - b0, ptr_t[4][q] - b0,
-             ptr_t[5][q] - b0, ptr_t[6][q] - b0, ptr_t[7][q] - b0, ptr_t[8][q] - b0, ptr_t[2][q + 1] - b0,
-             ptr_t[9][q] - b0, ptr_t[10][q] - b0, ptr_t[11][q] - b0);
+             ptr_t[5][q] - b0, ptr_t[6][q] - b0, ptr_t[7][q] - b0, ptr_t[8][q] - b0, ptr_t[2][q + 1] - b0);
+      printf("m %d step %d: prefetch %6lld %6lld %6lld\n", m, 64 + q, ptr_t[9][q] - b0, ptr_t[10][q] - b0,
+             ptr_t[11][q] - b0);
     }
 #endif
 #undef PTR
@@ -2163,7 +2158,7 @@ void launch_gs(const DevHier2D& hd, const DevLevel2D& lv, double* u, const doubl
   if (lv.pipe_rec && sweeps <= 2 && gs_pipe_enabled()) {
     // fine-grained pipelined smoother: one resident CTA per macro
     const int threads = 32 * (gs_group_warps(lv.n) + 2 + kPipePubs);
-    const size_t smem = kPipeRing * kStepBytes + static_cast<size_t>(kPipeRing + kPipePRing) * lv.pipe_rec_words * 4 +
+    const size_t smem = kPipeRing * kStepBytes + static_cast<size_t>(kPipePRing) * kPipeLanes * 16 +
                         static_cast<size_t>(lv.max_extra) * kProgLaneWords * 8 + (lv.max_ghosts + 1) * 8 +
                         2 * static_cast<size_t>(lv.S) * 8;
     static size_t pipe_static = 0;

@@ -160,22 +160,26 @@ void build_level(const Hierarchy2D& h, Level2D& lv) {
     P.maxreq = std::max(P.maxreq, static_cast<int>(R.req.size()));
     P.maxfetch = std::max(P.maxfetch, static_cast<int>(R.fetch.size()));
   }
-  if (P.maxreq > 32 || P.maxfetch > 32) return;  // not supported: the macro-DAG smoother runs
-  P.rec_words = (2 + 2 * P.maxreq + 2 * P.maxfetch + 3) & ~3;  // 16-byte records
+  if (P.maxreq > kPipeLanes || P.maxfetch > kPipeLanes) {  // not supported: the macro-DAG smoother runs
+    if (getenv("KB_PIPE_DEBUG"))
+      std::fprintf(stderr, "pipe tables M=%d n=%d: maxreq %d maxfetch %d exceed %d lanes\n", M, n, P.maxreq, P.maxfetch,
+                   kPipeLanes);
+    return;
+  }
+  P.rec_words = 4 * kPipeLanes;
   P.rec.assign(recs.size() * P.rec_words, 0);
   for (std::size_t r = 0; r < recs.size(); ++r) {
     std::int32_t* w = &P.rec[r * P.rec_words];
-    w[0] = static_cast<std::int32_t>(recs[r].req.size());
-    w[1] = static_cast<std::int32_t>(recs[r].fetch.size());
+    for (int k = 0; k < kPipeLanes; ++k) w[4 * k] = -1, w[4 * k + 2] = -1;
     int k = 0;
     for (const auto& [m2, p] : recs[r].req) {
-      w[2 + 2 * k] = m2;
-      w[3 + 2 * k] = p;
+      w[4 * k] = m2;
+      w[4 * k + 1] = p;
       ++k;
     }
     for (std::size_t f = 0; f < recs[r].fetch.size(); ++f) {
-      w[2 + 2 * P.maxreq + 2 * f] = recs[r].fetch[f].first;
-      w[3 + 2 * P.maxreq + 2 * f] = recs[r].fetch[f].second;
+      w[4 * f + 2] = recs[r].fetch[f].second;
+      w[4 * f + 3] = recs[r].fetch[f].first;
     }
   }
   P.ok = true;
