@@ -877,29 +877,77 @@ __device__ __forceinline__ void relax_nodes(const PNode& p, unsigned us_s, unsig
   }
 }
 
+// Lane record of the pipelined smoother (k_gs_pipe), loaded in two parts so
+// that neither sits between the gate and the relaxation: pnode_issue (the
+// record's vector loads, issued right after the current step's six lattice
+// reads) and pnode_finish (the dependent part: b, the extra record of a
+// vertex-group member, the six read addresses), done after the current
+// step's stores.
+struct PipeNode {
+  double c[6], diag, inv, B;
+  int k, flags, wr0, wr1, wb, wc, xb;
+  unsigned s01, s23, s45;  // [ghosts | lattice] slots of the six reads, 16 bits each
+  unsigned a[6];           // their shared-memory addresses
+};
+
+__device__ __forceinline__ void ld_s_v2s32(unsigned a, int& x, int& y) {
+  asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(x), "=r"(y) : "r"(a) : "memory");
+}
+
+__device__ __forceinline__ void pnode_issue(PipeNode& p, unsigned rec) {
+  ld_s_v2f64(rec, p.c[0], p.c[1]);
+  ld_s_v2f64(rec + 16, p.c[2], p.c[3]);
+  ld_s_v2f64(rec + 32, p.c[4], p.c[5]);
+  ld_s_v2f64(rec + 48, p.diag, p.inv);
+  ld_s_v2s32(rec + 88, p.k, p.flags);
+  ld_s_v4s32(rec + 96, p.wr0, p.wr1, p.wb, p.wc);
+  int s45, s01, s23;
+  ld_s_v4s32(rec + 112, p.xb, s45, s01, s23);
+  p.s01 = static_cast<unsigned>(s01);
+  p.s23 = static_cast<unsigned>(s23);
+  p.s45 = static_cast<unsigned>(s45);
+}
+// lane (type, mem): member `mem` of the step's node of this type; members 0/1
+// come from the ring slot, members >= 2 of vertex groups (flag bit 16 set on
+// every record of such a step) from the staged extra records
+__device__ __forceinline__ unsigned pnode_rec(unsigned slot, int type, int mem) {
+  return slot + static_cast<unsigned>(kLaneStride) * static_cast<unsigned>(2 * type + (mem < 2 ? mem : 0));
+}
+__device__ __forceinline__ void pnode_finish(PipeNode& p, unsigned xs, unsigned bs_s, unsigned gx_s, int mem) {
+  if (p.flags & (1 << 16)) {
+    const int rc = p.k >= 0 ? ((p.flags >> 8) & 0xff) : 0;
+    if (mem >= 2 && mem < rc) pnode_issue(p, xs + 128u * static_cast<unsigned>(p.xb + mem - 2));
+  }
+  p.B = ld_s64(bs_s + 8u * (p.k >= 0 ? p.k : 0));  // b is constant during the sweep
+  p.a[0] = gx_s + 8u * (p.s01 & 0xffffu), p.a[1] = gx_s + 8u * (p.s01 >> 16);
+  p.a[2] = gx_s + 8u * (p.s23 & 0xffffu), p.a[3] = gx_s + 8u * (p.s23 >> 16);
+  p.a[4] = gx_s + 8u * (p.s45 & 0xffffu), p.a[5] = gx_s + 8u * (p.s45 >> 16);
+}
+
 // relax_nodes for k_gs_pipe, with the shortest dependent path after the gate:
-// the six read addresses come straight from the record (slots of the
-// [ghosts | lattice] region, gx_s = its base), no selects, absent members /
-// cells are zero coefficients on the zero slot (o = +0.0), the two-member sum
-// is one shuffle.  The own copy and up to two other copies are stored to
-// global memory; vertex groups (> 2 members, `big` steps) take the general sum
-// and the remaining copies.
-__device__ __forceinline__ void relax_pipe(const PNode& p, unsigned gx_s, unsigned us_s, double* u,
-                                           const int* wr_global, int lane, double* own_copy, int g_chk_slots,
-                                           int g_chk_S, int g_chk_MS) {
-  (void)g_chk_slots, (void)g_chk_S, (void)g_chk_MS;  // bounds of the KB_GS_CHECK build
+// the six read addresses are precomputed (slots of the [ghosts | lattice]
+// region), no selects, absent members / cells are zero coefficients on the
+// zero slot (o = +0.0), the two-member sum is one shuffle.  The own copy and
+// up to two other copies are stored to global memory; vertex groups (> 2
+// members, `big` steps) take the general sum and the remaining copies.
+// `mid` runs after the six reads are issued (the next record's loads), `tail`
+// after the stores (its dependent part).
+template <class Mid, class Tail>
+__device__ __forceinline__ void relax_pipe(const PipeNode& p, unsigned us_s, double* u, const int* wr_global, int lane,
+                                           double* own_copy, int g_chk_slots, int g_chk_S, int g_chk_MS,
+                                           unsigned gx_s, Mid&& mid, Tail&& tail) {
+  (void)g_chk_slots, (void)g_chk_S, (void)g_chk_MS, (void)gx_s;  // bounds of the KB_GS_CHECK build
   const int type = lane >> 3, mem = lane & 7;
-  const unsigned a0 = gx_s + 8u * (p.slot01 & 0xffffu), a1 = gx_s + 8u * (p.slot01 >> 16);
-  const unsigned a2 = gx_s + 8u * (p.slot23 & 0xffffu), a3 = gx_s + 8u * (p.slot23 >> 16);
-  const unsigned a4 = gx_s + 8u * (p.slot45 & 0xffffu), a5 = gx_s + 8u * (p.slot45 >> 16);
 #ifdef KB_GS_CHECK
   {
     const unsigned lim = gx_s + 8u * static_cast<unsigned>(g_chk_slots);
-    KB_ASSERT(a0 < lim && a1 < lim && a2 < lim && a3 < lim && a4 < lim && a5 < lim);
+    KB_ASSERT(p.a[0] < lim && p.a[1] < lim && p.a[2] < lim && p.a[3] < lim && p.a[4] < lim && p.a[5] < lim);
     KB_ASSERT(p.k < g_chk_S);
   }
 #endif
-  const double x0 = ld_s64(a0), x1 = ld_s64(a1), x2 = ld_s64(a2), x3 = ld_s64(a3), x4 = ld_s64(a4), x5 = ld_s64(a5);
+  const double x0 = ld_s64(p.a[0]), x1 = ld_s64(p.a[1]), x2 = ld_s64(p.a[2]);
+  const double x3 = ld_s64(p.a[3]), x4 = ld_s64(p.a[4]), x5 = ld_s64(p.a[5]);
+  mid();
   double o = 0.0;
   o = o + (p.c[0] * x0 + p.c[1] * x1);
   o = o + (p.c[2] * x2 + p.c[3] * x3);
@@ -931,6 +979,7 @@ __device__ __forceinline__ void relax_pipe(const PNode& p, unsigned gx_s, unsign
     // more than two other copies: vertex groups (also domain-boundary ones, rc = 0)
     for (int q2 = p.wb + 2; q2 < p.wb + p.wc; ++q2) u[wr_global[q2]] = res;
   }
+  tail();
 }
 
 // Issue the cp.async copies of step program `t` (if it exists) into its ring slot.
@@ -1491,12 +1540,12 @@ __global__ void __launch_bounds__(kSchedMaxThreads, 1) k_gs_sched(DevLevel2D lv,
 // tau, so the gate normally opens at once; when it does not, progress is
 // published first and the gate waits (no cyclic wait: every requirement names
 // an event that precedes the step in the sequential order).
-constexpr int kPipeBarB = 1, kPipeBarA0 = 2, kPipeBarAs = 12;  // gate; ring of step-done barriers
+constexpr int kPipeBarB = 1, kPipeBarA0 = 2, kPipeBarAs = 8;  // gate; ring of step-done barriers (power of two)
 constexpr int kPipePubs = 4;  // publisher warps
 constexpr int kPipeRing = 16;  // step programs + gate records in flight
 constexpr int kPipePRing = 16;  // record ring of the prefetch / gate warps (power of two)
-constexpr int kPipePAhead = 8;  // records requested ahead of the prefetch warp
-constexpr int kPipeStage = 8;   // prefetched steps in flight (power of two, <= kPipePRing - kPipePAhead)
+constexpr int kPipePAhead = 4;  // record pairs requested ahead of the prefetch warp
+constexpr int kPipeStage = 8;   // prefetched steps in flight (power of two, <= kPipePRing - 2 kPipePAhead)
 constexpr int kPipeKnown = 64;  // observed-progress cache entries
 
 __device__ __forceinline__ void bar_arrive(int id, int threads) {
@@ -1531,7 +1580,7 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const unsigned ring_s = smem_addr(ring);
   __shared__ int pub_last[kPipePubs];  // last step-done barrier each publisher passed
-  __shared__ __align__(16) double fstage[kPipeStage][32][2];  // prefetched remote values (16-byte copies)
+  __shared__ __align__(16) double fstage[kPipeStage][kPipeLanes][2];  // prefetched remote values (16-byte copies)
   __shared__ __align__(8) unsigned long long fbar[kPipeStage];  // slot filled (32 async arrivals)
   __shared__ int2 known[kPipeKnown];  // prefetch warp: last observed progress per macro (direct mapped)
   __shared__ int gate_pos;            // last gate opened
@@ -1548,7 +1597,7 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
   if (tid == 0) ptr_dummy = 0;
 #define PTR(row, st)                                                                     \
   do {                                                                                   \
-    if (trace && lane == 0 && (st) >= 64 && (st) < 128) {                                \
+    if ((trace & 1) && lane == 0 && (st) >= 64 && (st) < 128) {                                \
       if (*reinterpret_cast<volatile int*>(&ptr_dummy) != 12345) ptr_t[row][(st) - 64] = clock64(); \
     }                                                                                    \
   } while (0)
@@ -1558,7 +1607,7 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
   } while (0)
 #endif
   if (tid < kPipePubs) pub_last[tid] = -1;
-  if (tid < kPipeStage) mbar_init(fbar_s + 8u * tid, 32);
+  if (tid < kPipeStage) mbar_init(fbar_s + 8u * tid, kPipeLanes);
   if (tid < kPipeKnown) known[tid] = make_int2(-1, 0);
   if (tid == 0) gate_pos = -1;
   const unsigned long long* prog_m = lv.prog + lv.prog_ptr[m];
@@ -1580,7 +1629,7 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
     if (tid == 0) gh[lv.max_ghosts] = 0.0;
     if (warp == 1) {
       for (int tau = 0; tau < kPipeRing - 1 && tau < total; ++tau) {
-        issue_prog(prog_m, ring_s, tau % T, tau % kPipeRing, lane);
+        issue_prog(prog_m, ring_s, tau % T, tau & (kPipeRing - 1), lane);
         cp_async_commit();
       }
       cp_async_wait<0>();
@@ -1594,7 +1643,7 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
     // progress[m] to tau + 2 (red.release.gpu.max: the release may finish out of order)
     const int w = warp - Wc - 2;
     for (int tau = w; tau < total; tau += kPipePubs) {
-      bar_sync(kPipeBarA0 + tau % kPipeBarAs, bthreads);
+      bar_sync(kPipeBarA0 + (tau & (kPipeBarAs - 1)), bthreads);
       PTR(8, tau);
       if (lane == 0) {
         *reinterpret_cast<volatile int*>(&pub_last[w]) = tau;
@@ -1617,59 +1666,67 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
     // the gate reads -- have landed (cp.async.mbarrier.arrive).  Records
     // (one int4 per lane, PipeTables2D) stream into a ring kPipePAhead steps
     // ahead.
+    // Two steps per iteration: lanes 0-15 take the entries of step st, lanes
+    // 16-31 those of step st + 1 (records of consecutive steps are adjacent).
     const unsigned pring_s = smem_addr(pring);
     const int4* prg = reinterpret_cast<const int4*>(pring);
-    auto issue_rec = [&](int st) {
-      if (lane < kPipeLanes)
+    const int half = lane >> 4, ent = lane & (kPipeLanes - 1);
+    auto issue_recs = [&](int st) {  // records st, st + 1 (st even), one 16-byte entry per lane
+      if (st + half < total)
         cp_async16(pring_s + static_cast<unsigned>((st & (kPipePRing - 1)) * kPipeLanes + lane) * 16u,
                    rec_m0 + static_cast<size_t>(st) * kPipeLanes + lane);
     };
-    for (int st = 0; st < kPipePAhead; ++st) {
-      if (st < total) issue_rec(st);
+    for (int st = 0; st < 2 * kPipePAhead; st += 2) {
+      issue_recs(st);
       cp_async_commit();
     }
     long long t_wait = 0, t_start = clock64();
     int n_wait = 0;
-    for (int st = 0, slot = 0; st < total; ++st, slot = (slot + 1) & (kPipeStage - 1)) {
-      cp_async_wait<kPipePAhead - 1>();  // record st landed (every lane's part)
+    for (int st = 0; st < total; st += 2) {
+      cp_async_wait<kPipePAhead - 1>();  // records st, st + 1 landed (every lane's part)
       __syncwarp();
-      // slot reuse: the gate of step st - kPipeStage has read its values and
-      // the record the ring slot of st + kPipePAhead held
-      if (st >= kPipeStage)
-        while (*reinterpret_cast<volatile int*>(&gate_pos) < st - kPipeStage) {
+      const int sl = st + half;  // this lane's step
+      // slot reuse: the gate of step st + 1 - kPipeStage has read its values and
+      // the records the ring slots of st + 2 kPipePAhead (+1) held
+      if (st + 1 >= kPipeStage)
+        while (*reinterpret_cast<volatile int*>(&gate_pos) < st + 1 - kPipeStage) {
         }
       PTR(9, st);
-      const int4 e = lane < kPipeLanes ? prg[(st & (kPipePRing - 1)) * kPipeLanes + lane] : make_int4(-1, 0, -1, 0);
+      const int4 e = sl < total ? prg[(st & (kPipePRing - 1)) * kPipeLanes + lane] : make_int4(-1, 0, -1, 0);
       if (e.x >= 0 && !(abl & 8)) {
         const int2 kn = known[e.x & (kPipeKnown - 1)];
         if (kn.x != e.x || kn.y < e.y) {
           const int* pm = progress + e.x;
           int v;
           long long spins = 0;
-          if (trace) ++n_wait, t_wait -= clock64();
+          if (trace & 1) ++n_wait, t_wait -= clock64();
           while ((v = ld_acquire(pm)) < e.y) {
             if (++spins == (1ll << 24)) {  // a broken table would deadlock: fail loudly instead
-              printf("k_gs_pipe: macro %d step %d waits for macro %d progress %d (has %d)\n", m, st, e.x, e.y, v);
+              printf("k_gs_pipe: macro %d step %d waits for macro %d progress %d (has %d)\n", m, sl, e.x, e.y, v);
               __trap();
             }
           }
-          if (trace) t_wait += clock64();
+          if (trace & 1) t_wait += clock64();
           known[e.x & (kPipeKnown - 1)] = make_int2(e.x, v);
         }
       }
-      __syncwarp();
+      // each half goes on as soon as its own step's requirements hold: step st
+      // must not wait for the requirements of step st + 1 (a cycle otherwise)
+      __syncwarp(half ? 0xffff0000u : 0x0000ffffu);
       PTR(10, st);
+      const int slot = sl & (kPipeStage - 1);
       if (e.z >= 0 && !(abl & 64)) {
         KB_ASSERT(e.z < lv.M * S);
-        cp_async16(smem_addr(&fstage[slot][lane][0]), u + (e.z & ~1));
+        cp_async16(smem_addr(&fstage[slot][ent][0]), u + (e.z & ~1));
       }
-      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(fbar_s + 8u * slot) : "memory");
-      if (st + kPipePAhead < total) issue_rec(st + kPipePAhead);
+      if (sl < total)
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(fbar_s + 8u * slot) : "memory");
+      issue_recs(st + 2 * kPipePAhead);
       cp_async_commit();
       PTR(11, st);
     }
     cp_async_wait<0>();
-    if (trace && lane == 0 && (m % 20 == 0 || m == gridDim.x - 1))
+    if ((trace & 1) && lane == 0 && (m % 20 == 0 || m == gridDim.x - 1))
       printf("pipe macro %d: steps %d, prefetch waits %d, cycles waiting %lld of %lld\n", m, total, n_wait, t_wait,
              clock64() - t_start);
   } else if (warp == Wc) {
@@ -1698,7 +1755,7 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
       // publisher must have passed it (flow control only)
       if (g >= kPipeBarAs && !(abl & 512)) {
         const int gp = g - kPipeBarAs;
-        while (*reinterpret_cast<volatile int*>(&pub_last[gp % kPipePubs]) < gp) {
+        while (*reinterpret_cast<volatile int*>(&pub_last[gp & (kPipePubs - 1)]) < gp) {
         }
       }
       __syncwarp();
@@ -1712,14 +1769,14 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
     const unsigned us_s = smem_addr(us), bs_s = smem_addr(bs), gh_s = smem_addr(gh), xs_s = smem_addr(xs);
     bar_sync(kPipeBarB, bthreads);  // gate of step 0
     if (gw == 1) {
-      for (int tau = 0; tau < total; ++tau) {
-        const int nx = tau + kPipeRing - 1;
+      for (int tau = 0, tn = (kPipeRing - 1) % T; tau < total; ++tau, tn = (tn + 1 == T ? 0 : tn + 1)) {
+        const int nx = tau + kPipeRing - 1;  // step nx = tn mod T
         if (nx < total && !(abl & 16))
-          issue_prog(prog_m, ring_s, nx % T, nx % kPipeRing, lane);
+          issue_prog(prog_m, ring_s, tn, nx & (kPipeRing - 1), lane);
         cp_async_commit();
         if (!(abl & 256)) cp_async_wait<kPipeRing - 7>();  // steps and records <= tau + 6 landed (read by the sync warp after A)
         PTR(7, tau);
-        bar_arrive(kPipeBarA0 + tau % kPipeBarAs, bthreads);
+        bar_arrive(kPipeBarA0 + (tau & (kPipeBarAs - 1)), bthreads);
         if (tau + 1 < total) bar_sync(kPipeBarB, bthreads);
       }
       cp_async_wait<0>();
@@ -1728,23 +1785,35 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
       const int tl = type < 3 ? type : 0;
       // the next step's lane records are read while waiting for its gate, so
       // they do not queue in front of this step's lattice reads
-      PNode p0, p1;
-      load_pnode(p0, ring_s, xs_s, bs_s, tl, mem);
+      PipeNode p0, p1;
+      const unsigned gx_s = gh_s;
+      auto slot_of = [&](int tau) { return ring_s + static_cast<unsigned>(tau & (kPipeRing - 1)) * kStepBytes; };
+      auto relax = [&](const PipeNode& p, PipeNode& nx, int tau) {
+        const bool more = tau + 1 < total && !(abl & 4);
+        relax_pipe(
+            p, us_s, u, lv.wr, lane, um, lv.max_ghosts + 1 + S, S, lv.M * S, gx_s,
+            [&] {
+              if (more) pnode_issue(nx, pnode_rec(slot_of(tau + 1), tl, mem));
+            },
+            [&] {
+              if (more) pnode_finish(nx, xs_s, bs_s, gx_s, mem);
+            });
+      };
+      pnode_issue(p0, pnode_rec(ring_s, tl, mem));
+      pnode_finish(p0, xs_s, bs_s, gx_s, mem);
       for (int tau = 0; tau < total; tau += 2) {
         PTR(2, tau);
-        if (!(abl & 2)) relax_pipe(p0, gh_s, us_s, u, lv.wr, lane, um, lv.max_ghosts + 1 + S, S, lv.M * S);
+        if (!(abl & 2)) relax(p0, p1, tau);
         PTR(3, tau);
-        bar_arrive(kPipeBarA0 + tau % kPipeBarAs, bthreads);
+        bar_arrive(kPipeBarA0 + (tau & (kPipeBarAs - 1)), bthreads);
         if (tau + 1 >= total) break;
-        if (!(abl & 4)) load_pnode(p1, ring_s + static_cast<unsigned>((tau + 1) % kPipeRing) * kStepBytes, xs_s, bs_s, tl, mem);
         PTR(4, tau + 1);
         bar_sync(kPipeBarB, bthreads);
         PTR(2, tau + 1);
-        if (!(abl & 2)) relax_pipe(p1, gh_s, us_s, u, lv.wr, lane, um, lv.max_ghosts + 1 + S, S, lv.M * S);
+        if (!(abl & 2)) relax(p1, p0, tau + 1);
         PTR(3, tau + 1);
-        bar_arrive(kPipeBarA0 + (tau + 1) % kPipeBarAs, bthreads);
+        bar_arrive(kPipeBarA0 + ((tau + 1) & (kPipeBarAs - 1)), bthreads);
         if (tau + 2 >= total) break;
-        if (!(abl & 4)) load_pnode(p0, ring_s + static_cast<unsigned>((tau + 2) % kPipeRing) * kStepBytes, xs_s, bs_s, tl, mem);
         PTR(4, tau + 2);
         bar_sync(kPipeBarB, bthreads);
       }
@@ -1775,14 +1844,15 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
         }
         if (gw == 2) PTR(5, tau);
         if (gw == Wc - 1) PTR(6, tau);
-        bar_arrive(kPipeBarA0 + tau % kPipeBarAs, bthreads);
+        bar_arrive(kPipeBarA0 + (tau & (kPipeBarAs - 1)), bthreads);
         if (tau + 1 < total) bar_sync(kPipeBarB, bthreads);
       }
     }
   }
   __syncthreads();
 #ifdef KB_GS_TRACE
-  if (trace && (m == 0 || m == gridDim.x / 2) && tid == 0)
+  if ((trace & 1) && tid == 0 && m % 20 == 0) printf("trace end m %d\n", m);
+  if ((trace & 1) && (m == 0 || m == gridDim.x / 2) && tid == 0)
     for (int q = 0; q < 24; ++q) {
       const long long b0 = ptr_t[2][q];  // boundary past B of step 64 + q
       printf("m %d step %d: %6lld %6lld %6lld %6lld %6lld %6lld %6lld %6lld %6lld | next B %6lld\n", m, 64 + q,

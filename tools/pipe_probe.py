@@ -16,3 +16,4 @@ b = K.GridFunction(h, l, np.random.rand(h.level_size(l)))
 s.interface_sync(u, K.SYNC_REPLACE)
 s.interface_sync(b, K.SYNC_REPLACE)
 s.gauss_seidel(u, b, 2)
+s.synchronize()
