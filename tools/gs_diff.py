@@ -11,7 +11,8 @@ from paper_2508_06049_b200 import klref as K
 
 k, l, sweeps = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3])
 if os.environ.get("CHILD"):
-    h = K.GridHierarchy.build(K.MacroMesh.read(os.path.join(REPO, "tests", "golden", f"cfg2_k{k}.mesh")), 7)
+    mesh = os.environ.get("MESH") or os.path.join(REPO, "tests", "golden", f"cfg2_k{k}.mesh")
+    h = K.GridHierarchy.build(K.MacroMesh.read(mesh), 7)
     s = K.MultigridSolver(h, K.Problem(K.PROBLEM_LSHAPE), K.SolverConfig(nu=2))
     rng = np.random.default_rng(1)
     u = K.GridFunction(h, l, rng.random(h.level_size(l)))
@@ -32,6 +33,17 @@ n = 2 ** l
 S = (n + 1) * (n + 2) // 2
 d = np.nonzero(a != b)[0]
 print(f"differences: {d.size} of {a.size}")
+M = a.size // S
+lat = np.zeros(S, dtype=bool)
+q = 0
+for j in range(n + 1):
+    for i in range(n + 1 - j):
+        lat[q] = i >= 1 and j >= 1 and i + j <= n - 1
+        q += 1
+bad = (a != b).reshape(M, S)
+per = [(m, int(bad[m][lat].sum()), int(bad[m][~lat].sum())) for m in range(M)]
+print("first macros with interior differences:", [x for x in per if x[1] > 0][:8])
+print("macros with boundary-only differences:", [x for x in per if x[1] == 0 and x[2] > 0][:12])
 for q in d[:40]:
     m, idx = divmod(int(q), S)
     j = 0
