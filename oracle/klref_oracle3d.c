@@ -9,7 +9,7 @@
  *   lattice / groups / ownership        like proj/src/hhg.cpp:48-144, 206-257
  *   element matrices, apply             like proj/src/fem.cpp:30-126
  *   partial rows                        like proj/src/fem.cpp:128-173
- *   multicolour Gauss-Seidel            builder's order (boundary groups by colour, then interiors by colour)
+ *   Gauss-Seidel                        builder's order (boundary groups by colour, then every macro's interior plane by plane, four parity classes per plane)
  *   residual, transfers, CG, V-cycle,
  *   FMG (FinestPolicy::None)            like proj/src/multigrid.cpp:22-279
  *   estimator                           like proj/src/estimator.cpp:8-45
@@ -504,7 +504,7 @@ void o3_residual(const o3h* h, int l, const double* u, const double* b, double* 
   for (size_t q = 0; q < N; ++q) r[q] = (lv->flag[q] & 2) ? 0.0 : b[q] - r[q];
 }
 
-/* multicolour Gauss-Seidel: boundary groups by colour, then interior nodes by colour */
+/* Gauss-Seidel: boundary groups by colour, then the macro interiors plane by plane */
 void o3_gauss_seidel(const o3h* h, int l, double* u, const double* b, int sweeps) {
   const o3lev* lv = &h->lv[l];
   const int n = lv->n, S = lv->S;
@@ -524,20 +524,27 @@ void o3_gauss_seidel(const o3h* h, int l, double* u, const double* b, int sweeps
         }
         for (int q = bq; q < e; ++q) u[(size_t)lv->mslot[q] * S + lv->midx[q]] = val;
       }
-    for (int c = 0; c < h->C; ++c)
-      for (int s = 0; s < h->M; ++s) {
-        const double* st = lv->stK + 15 * s;
-        const double inv_c = 1.0 / st[0];
-        for (int k = 1; k <= n; ++k)
-          for (int j = 1; j <= n - k; ++j)
-            for (int i = 1; i <= n - k - j; ++i) {
-              if (n - i - j - k <= 0) continue;
+    /* interiors: every macro plane by plane (k ascending); inside a plane the
+     * four (i, j) parity classes in the order (odd, odd), (even, odd),
+     * (odd, even), (even, even) — nodes of one class are never neighbours.
+     * The row is two fused chains (directions 1..7 and 8..14), added last. */
+    for (int s = 0; s < h->M; ++s) {
+      const double* st = lv->stK + 15 * s;
+      const double inv_c = 1.0 / st[0];
+      double* um = u + (size_t)s * S;
+      for (int k = 1; k <= n - 3; ++k)
+        for (int q = 0; q < 4; ++q)
+          for (int j = 1 + (q >> 1); j <= n - 2 - k; j += 2)
+            for (int i = 1 + (q & 1); i <= n - 1 - k - j; i += 2) {
+              double x[15];
+              for (int d = 1; d < 15; ++d) x[d] = um[lat3(n, i + DIR[d][0], j + DIR[d][1], k + DIR[d][2])];
+              double a0 = st[1] * x[1], a1 = st[8] * x[8];
+              for (int d = 2; d < 8; ++d) a0 = fma(st[d], x[d], a0);
+              for (int d = 9; d < 15; ++d) a1 = fma(st[d], x[d], a1);
               const size_t off = (size_t)s * S + lat3(n, i, j, k);
-              if (lv->ncol[off] != c) continue;
-              const double acc = stencil_apply(lv, st, s, i, j, k, u, 1);
-              u[off] = (b[off] - acc) * inv_c;
+              u[off] = (b[off] - (a0 + a1)) * inv_c;
             }
-      }
+    }
   }
 }
 

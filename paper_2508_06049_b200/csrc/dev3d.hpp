@@ -32,8 +32,9 @@ struct DevLevel3D {
   const double* inv_c;
   const int* pat_color;        // 8 per macro
   const int* col_pat;          // colors per macro: the parity pattern of that colour, -1 none
-  // small levels (n <= 16): lattice-interior nodes of each parity pattern
-  // (i | j << 10 | k << 20), pattern p at [pat_ptr[p], pat_ptr[p + 1]); else null
+  // 4 <= n <= 64: a macro's lattice-interior nodes (lat2(n - k, i, j) | j << 16)
+  // in the smoother's order, step (plane k, parity class q) at
+  // [pat_ptr[4 (k - 1) + q], pat_ptr[4 (k - 1) + q + 1]); pat_max nodes at most; else null
   const int* pat_ptr;
   const int* pat_node;
   int pat_max;

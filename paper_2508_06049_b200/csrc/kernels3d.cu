@@ -19,6 +19,8 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 #include <string>
 
 #include "dev3d.hpp"
@@ -656,96 +658,61 @@ __global__ void __launch_bounds__(kT) k3_gs_groups(DevLevel3D lv, double* u, con
   gs_group(lv, u, b, lv.color_grp[p0 + t]);
 }
 
-// One interior node of macro m (row offsets ra of the 7 neighbour rows).
-__device__ __forceinline__ void gs_node(double* um, const double* __restrict__ bm, const double (&s)[15],
-                                        double inv_c, const int (&ra)[7], int i) {
-  double x[15];
+// Interior relaxation (the specification's order, oracle o3_gauss_seidel):
+// every macro plane by plane (k ascending), inside a plane the four (i, j)
+// parity classes q = 0..3 — i = 1 + (q & 1) + 2 a, j = 1 + (q >> 1) + 2 r —
+// one after the other; nodes of a class are never stencil neighbours.  The row
+// is two fused chains (directions 1..7 and 8..14) added last.
+__device__ __forceinline__ double gs_row_fma(const double (&s)[15], const double (&x)[15]) {
+  double a0 = s[1] * x[1], a1 = s[8] * x[8];
 #pragma unroll
-  for (int d = 1; d < 15; ++d) x[d] = um[ra[dir_row(d)] + i + dir_di(d)];
-  double acc = s[1] * x[1];
+  for (int d = 2; d < 8; ++d) a0 = __fma_rn(s[d], x[d], a0);
 #pragma unroll
-  for (int d = 2; d < 15; ++d) acc = acc + s[d] * x[d];
-  um[ra[0] + i] = (__ldg(bm + ra[0] + i) - acc) * inv_c;
+  for (int d = 9; d < 15; ++d) a1 = __fma_rn(s[d], x[d], a1);
+  return a0 + a1;
+}
+// Neighbour offsets of lattice-interior node c = lat2(m2, i, j) of plane k
+// (m2 = n - k) relative to the starts of planes k - 1, k, k + 1: with
+// rs = c - i the row start, the pairs (d: offset) are
+//   plane k     1: c+1  2: c-1  3: c+m2-j  7: c+m2-j+1  8: c-(m2+2-j)  4: c-(m2+2-j)+1
+//   plane k+1   5: c-m2-1  11: c-m2  9: c-j-1  13: c-j       (lat2(m2 - 1, ., .))
+//   plane k-1  14: c+j  10: c+j+1  12: c+m2+1  6: c+m2+2      (lat2(m2 + 1, ., .))
+template <typename Ld>
+__device__ __forceinline__ void gs_gather(double (&x)[15], Ld ld, int bm, int b0, int bp, int c, int j, int m2) {
+  const int e0 = b0 + c, e1 = e0 + (m2 - j), e2 = e0 - (m2 + 2 - j);
+  const int p0 = bp + c - m2 - 1, p1 = bp + c - j - 1, q0 = bm + c + j, q1 = bm + c + m2 + 1;
+  x[1] = ld(e0 + 1), x[2] = ld(e0 - 1), x[3] = ld(e1), x[4] = ld(e2 + 1), x[5] = ld(p0), x[6] = ld(q1 + 1);
+  x[7] = ld(e1 + 1), x[8] = ld(e2), x[9] = ld(p1), x[10] = ld(q0 + 1), x[11] = ld(p0 + 1), x[12] = ld(q1);
+  x[13] = ld(p1 + 1), x[14] = ld(q0);
 }
 
-// Interior phase of one macro, all colours in order: lattice-interior nodes
-// only couple to their own macro's copies, so once the boundary phase is done
-// the macros are independent and one CTA runs a macro's whole colour sequence
-// with block barriers, the macro's lattice staying in L1/L2 between colours.
-// The rows (k, j) of a parity pattern are dealt round-robin to the warps, a
-// lane takes every other node of a row.
-__device__ void gs_interior_macro(const DevLevel3D& lv, double* u, const double* __restrict__ b, int m) {
-  const int n = lv.n, S = lv.S, T = tsz(n);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-  double* um = u + static_cast<size_t>(m) * S;
-  const double* bm = b + static_cast<size_t>(m) * S;
-  double s[15];
-#pragma unroll
-  for (int d = 1; d < 15; ++d) s[d] = __ldg(lv.stK + 15 * m + d);
-  const double inv_c = __ldg(lv.inv_c + m);
-  for (int c = 0; c < lv.colors; ++c) {
-    bool any = false;
-#pragma unroll 1
-    for (int p = 0; p < 8; ++p) {
-      if (__ldg(lv.pat_color + 8 * m + p) != c) continue;
-      any = true;
-      const int pi = p & 1, pj = (p >> 1) & 1, pk = (p >> 2) & 1;
-      const int jlo = pj ? 1 : 2, ilo = (pi ? 1 : 2) + 2 * lane;
-      int k = pk ? 1 : 2, r = warp;
-      while (k <= n - 3) {
-        const int m2 = n - k;
-        const int nr = m2 - 2 >= jlo ? (m2 - 2 - jlo) / 2 + 1 : 0;
-        if (r >= nr) {
-          r -= nr;
-          k += 2;
-          continue;
-        }
-        const int j = jlo + 2 * r;
-        int ra[7];
-#pragma unroll
-        for (int t = 0; t < 7; ++t) {
-          const int kk = k + row_dk(t), jj = j + row_dj(t);
-          ra[t] = T - tsz(n - kk) + lat2(n - kk, 0, jj);
-        }
-        for (int i = ilo; i <= m2 - 1 - j; i += 64) gs_node(um, bm, s, inv_c, ra, i);
-        r += nwarps;
-      }
-    }
-    if (any) __syncthreads();
-  }
-}
-
-// Interior phase for small macros (n <= 16): the CTA's macros (every
-// active-th one) are processed together, colour by colour with block barriers;
-// the items of a colour are (macro, node of the macro's pattern of that
-// colour) from the level's pattern node lists.
+// Small levels (n <= 16, inside the cooperative smoother): the CTA's macros
+// (every active-th one) together, step by step (plane k, class q) with block
+// barriers; the items of a step are (macro, node) from the level's step lists.
 __device__ void gs_interior_batch(const DevLevel3D& lv, double* u, const double* __restrict__ b, int active,
                                   int group) {
-  const int n = lv.n, S = lv.S, T = tsz(n), per = lv.pat_max;
+  const int n = lv.n, S = lv.S, T = tsz(n), per = lv.pat_max, steps = 4 * (n - 3);
   const int mine = (lv.M - static_cast<int>(blockIdx.x) + active - 1) / active;  // macros of this CTA
   for (int g0 = 0; g0 < mine; g0 += group)
-  for (int c = 0; c < lv.colors; ++c) {
-    const int nm = min(group, mine - g0);
-    for (int t = threadIdx.x; t < nm * per; t += blockDim.x) {
-      const int mi = t / per, idx = t - mi * per;
-      const int m = blockIdx.x + (g0 + mi) * active;
-      const int p = __ldg(lv.col_pat + lv.colors * m + c);
-      if (p < 0) continue;
-      const int q0 = __ldg(lv.pat_ptr + p);
-      if (idx >= __ldg(lv.pat_ptr + p + 1) - q0) continue;
-      int i, j, k;
-      unpack_ijk(__ldg(lv.pat_node + q0 + idx), i, j, k);
-      const int m2 = n - k, pb0 = T - tsz(m2);
-      const int base[3] = {pb0 - (m2 + 2) * (m2 + 3) / 2, pb0, pb0 + (m2 + 1) * (m2 + 2) / 2};
-      int ra[7];
-      slot_rows(base, m2, j, ra);
-      double st[15];
+    for (int st = 0; st < steps; ++st) {
+      const int nm = min(group, mine - g0);
+      const int q0 = __ldg(lv.pat_ptr + st), cnt = __ldg(lv.pat_ptr + st + 1) - q0;
+      for (int t = threadIdx.x; t < nm * per; t += blockDim.x) {
+        const int mi = t / per, idx = t - mi * per;
+        if (idx >= cnt) continue;
+        const int m = blockIdx.x + (g0 + mi) * active;
+        const int ent = __ldg(lv.pat_node + q0 + idx), c = ent & 0xffff, j = ent >> 16, k = (st >> 2) + 1;
+        const int m2 = n - k, pb0 = T - tsz(m2);
+        double* um = u + static_cast<size_t>(m) * S;
+        double sc[15], x[15];
 #pragma unroll
-      for (int d = 1; d < 15; ++d) st[d] = __ldg(lv.stK + 15 * m + d);
-      gs_node(u + static_cast<size_t>(m) * S, b + static_cast<size_t>(m) * S, st, __ldg(lv.inv_c + m), ra, i);
+        for (int d = 1; d < 15; ++d) sc[d] = __ldg(lv.stK + 15 * m + d);
+        gs_gather(x, [&](int o) { return um[o]; }, pb0 - (m2 + 2) * (m2 + 3) / 2, pb0, pb0 + (m2 + 1) * (m2 + 2) / 2, c,
+                  j, m2);
+        um[pb0 + c] = (__ldg(b + static_cast<size_t>(m) * S + pb0 + c) - gs_row_fma(sc, x)) * __ldg(lv.inv_c + m);
+      }
+      __syncthreads();
     }
-    __syncthreads();
-  }
 }
 
 // Relaxation of a group with many members (macro vertices, edges): one warp,
@@ -849,12 +816,9 @@ __global__ void __launch_bounds__(NT, MINB) k3_gs_sweeps(DevLevel3D lv, double* 
       }
 #endif
     }
-    if (lv.n >= 4) {
+    if (lv.n >= 4 && lv.n <= 16) {
       if ((phases & 2) && static_cast<int>(blockIdx.x) < active) {
-        if (lv.pat_node)
-          gs_interior_batch(lv, u, b, active, group);
-        else
-          for (int m = blockIdx.x; m < lv.M; m += active) gs_interior_macro(lv, u, b, m);
+        gs_interior_batch(lv, u, b, active, group);  // levels with step lists (the host launches k3_gs_planes otherwise)
       }
       if (sw + 1 < sweeps) grid.sync();
     }
@@ -878,46 +842,141 @@ __global__ void __launch_bounds__(NT, MINB) k3_gs_sweeps(DevLevel3D lv, double* 
 #endif
 }
 
-// interior phase, one launch per colour over every macro: block = (macro,
-// k-plane); the plane's rows of the colour's parity pattern(s) are dealt to the
-// warps, a lane takes every other node of a row.  Nodes of one colour never
-// neighbour each other, so every read of a launch is of a value no thread of
-// the launch writes: the read-only (L1-cached) path is safe and neighbour rows
-// are shared through L1.
-
-__global__ void __launch_bounds__(kT) k3_gs_color(DevLevel3D lv, double* u, const double* __restrict__ b, int c) {
-  const int n = lv.n, S = lv.S, T = tsz(n);
-  const int m = blockIdx.x / (n + 1), k = blockIdx.x - m * (n + 1);
-  if (k < 1 || k > n - 3) return;
-  const int pk = k & 1;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-  const double* st = lv.stK + 15 * m;
+// Interior phase as a k-plane stream (4 <= n <= 64): one CTA per macro keeps
+// planes k - 1, k, k + 1 of u and plane k of b in shared memory (TMA bulk
+// copies: u two planes ahead in a 4-slot ring, b one plane ahead in a 2-slot
+// ring), relaxes the four parity classes of plane k with a block barrier after
+// each and writes every new value to the ring and to global memory; u and b are
+// read once and u written once per sweep.  The nodes of a step come from the
+// level's step lists (entry = in-plane index | j << 16), one per thread.
+template <int NT, int US, int BS>
+__global__ void __launch_bounds__(NT) k3_gs_planes(DevLevel3D lv, double* u, const double* __restrict__ b) {
+  // US u slots (plane k in slot k % US, US - 2 planes ahead), BS b slots (plane
+  // k in slot (k - 1) % BS, BS - 1 planes ahead); one mbarrier per slot
+  extern __shared__ __align__(128) unsigned long long gp_smem[];
+  constexpr int PF = 6;  // L2 prefetch distance beyond the TMA stream (planes)
+  const int n = lv.n, S = lv.S, m = blockIdx.x, tid = threadIdx.x;
+  const int stride = plane_stride(n);
+  const int steps = 4 * (n - 3);
+  int* sp = reinterpret_cast<int*>(gp_smem + US + BS);  // step starts (steps + 1, padded to 16 bytes)
+  double* ring_u = reinterpret_cast<double*>(gp_smem + US + BS) + ((steps + 4) >> 2 << 1);
+  double* ring_b = ring_u + US * stride;
+  const unsigned bar_s = static_cast<unsigned>(__cvta_generic_to_shared(gp_smem));
+  const unsigned ringu_s = static_cast<unsigned>(__cvta_generic_to_shared(ring_u));
+  const unsigned ringb_s = static_cast<unsigned>(__cvta_generic_to_shared(ring_b));
   double* um = u + static_cast<size_t>(m) * S;
   const double* bm = b + static_cast<size_t>(m) * S;
-  const int m2 = n - k;
-  for (int p = pk << 2; p < (pk << 2) + 4; ++p) {
-    if (__ldg(lv.pat_color + 8 * m + p) != c) continue;
-    const int pi = p & 1, pj = (p >> 1) & 1;
-    double s[15];
+  auto issue = [&](const double* src, int k, unsigned dst_s, unsigned bar) {
+    const size_t a = reinterpret_cast<size_t>(src + plane_base(n, k));
+    const int off = static_cast<int>((a >> 3) & 1);
+    const int len = (n - k + 1) * (n - k + 2) / 2;
+    const unsigned bytes = static_cast<unsigned>(((off + len) * 8 + 15) & ~15);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst_s),
+                 "l"(a - 8 * off), "r"(bytes), "r"(bar)
+                 : "memory");
+  };
+  auto issue_u = [&](int k) {
+    if (k <= n - 2) issue(um, k, ringu_s + 8u * static_cast<unsigned>((k % US) * stride), bar_s + 8u * (k % US));
+  };
+  auto issue_b = [&](int k) {
+    if (k <= n - 3)
+      issue(bm, k, ringb_s + 8u * static_cast<unsigned>(((k - 1) % BS) * stride), bar_s + 8u * (US + (k - 1) % BS));
+  };
+  auto l2_prefetch = [&](const double* v, int k) {
+    if (k > n - 2) return;
+    const int len = (n - k + 1) * (n - k + 2) / 2;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<size_t>(v + plane_base(n, k)) &
+                                                                    ~size_t(15)),
+                 "r"(static_cast<unsigned>((len * 8 + 31) & ~15))
+                 : "memory");
+  };
+  auto align_u = [&](int k) { return static_cast<int>((reinterpret_cast<size_t>(um + plane_base(n, k)) >> 3) & 1); };
+  if (tid == 0) {
+    for (int t = 0; t < US + BS; ++t) p3_mbar_init(bar_s + 8u * t, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int k = 0; k <= US - 2; ++k) issue_u(k);
+    for (int k = 1; k <= BS - 1; ++k) issue_b(k);
+  }
+  if (tid == 32)
+    for (int k = US - 1; k < US - 1 + PF; ++k) l2_prefetch(um, k);
+  if (tid == 64)
+    for (int k = BS; k < BS + PF; ++k) l2_prefetch(bm, k);
+  double s[15];
 #pragma unroll
-    for (int d = 1; d < 15; ++d) s[d] = __ldg(st + d);
-    const double inv_c = __ldg(lv.inv_c + m);
-    for (int j = (pj ? 1 : 2) + 2 * warp; j <= m2 - 2; j += 2 * nwarps) {
-      int ra[7];
-#pragma unroll
-      for (int t = 0; t < 7; ++t) {
-        const int kk = k + row_dk(t), jj = j + row_dj(t);
-        ra[t] = T - tsz(n - kk) + lat2(n - kk, 0, jj);
-      }
-      for (int i = (pi ? 1 : 2) + 2 * lane; i <= m2 - 1 - j; i += 64) {
+  for (int d = 1; d < 15; ++d) s[d] = __ldg(lv.stK + 15 * m + d);
+  s[0] = 0.0;
+  const double inv_c = __ldg(lv.inv_c + m);
+  for (int t = tid; t <= steps; t += NT) sp[t] = __ldg(lv.pat_ptr + t);
+  __syncthreads();
+  // this thread's entries of the next three steps are loaded ahead (L2 latency)
+  auto entry = [&](int st) {
+    return st < steps && tid < sp[st + 1] - sp[st] ? __ldg(lv.pat_node + sp[st] + tid) : 0;
+  };
+  int e1 = entry(0), e2 = entry(1), e3 = entry(2);
+  for (int k = 1; k <= n - 3; ++k) {
+    if (tid == 0) {
+      issue_u(k + US - 2);  // its slot held plane k - 2
+      issue_b(k + BS - 1);  // its slot held plane k - 1
+    }
+    if (tid == 32) l2_prefetch(um, k + US - 2 + PF);
+    if (tid == 64) l2_prefetch(bm, k + BS - 1 + PF);
+    if (k == 1) {
+      p3_mbar_wait(bar_s, 0);
+      p3_mbar_wait(bar_s + 8u, 0);
+    }
+    p3_mbar_wait(bar_s + 8u * ((k + 1) % US), ((k + 1) / US) & 1);
+    p3_mbar_wait(bar_s + 8u * (US + (k - 1) % BS), ((k - 1) / BS) & 1);
+    const int m2 = n - k;
+    const int bm1 = ((k - 1) % US) * stride + align_u(k - 1), b0 = (k % US) * stride + align_u(k),
+              bp1 = ((k + 1) % US) * stride + align_u(k + 1);
+    const int gp = plane_base(n, k);
+    const double* bk =
+        ring_b + ((k - 1) % BS) * stride + static_cast<int>((reinterpret_cast<size_t>(bm + gp) >> 3) & 1);
+#pragma unroll 1
+    for (int q = 0; q < 4; ++q) {
+      const int st = 4 * (k - 1) + q, p0 = sp[st], cnt = sp[st + 1] - p0;
+      int ent = e1;
+      e1 = e2, e2 = e3, e3 = entry(st + 3);
+      for (int e = tid; e < cnt; e += NT) {
+        if (e != tid) ent = __ldg(lv.pat_node + p0 + e);
+        const int c = ent & 0xffff, j = ent >> 16;
         double x[15];
-#pragma unroll
-        for (int d = 1; d < 15; ++d) x[d] = __ldg(um + ra[dir_row(d)] + i + dir_di(d));
-        double acc = s[1] * x[1];
-#pragma unroll
-        for (int d = 2; d < 15; ++d) acc = acc + s[d] * x[d];
-        um[ra[0] + i] = (__ldg(bm + ra[0] + i) - acc) * inv_c;
+        gs_gather(x, [&](int o) { return ring_u[o]; }, bm1, b0, bp1, c, j, m2);
+        const double v = (bk[c] - gs_row_fma(s, x)) * inv_c;
+        ring_u[b0 + c] = v;
+        um[gp + c] = v;
       }
+      __syncthreads();
+    }
+  }
+}
+
+// The same order straight on global memory (n > 64): one CTA per macro, rows
+// to warps, block barriers between the classes.
+__global__ void __launch_bounds__(kT) k3_gs_planes_global(DevLevel3D lv, double* u, const double* __restrict__ b) {
+  const int n = lv.n, S = lv.S, m = blockIdx.x, T = tsz(n);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  double* um = u + static_cast<size_t>(m) * S;
+  const double* bm = b + static_cast<size_t>(m) * S;
+  double s[15];
+#pragma unroll
+  for (int d = 1; d < 15; ++d) s[d] = __ldg(lv.stK + 15 * m + d);
+  s[0] = 0.0;
+  const double inv_c = __ldg(lv.inv_c + m);
+  for (int k = 1; k <= n - 3; ++k) {
+    const int m2 = n - k, pb0 = T - tsz(m2);
+    const int pbm = pb0 - (m2 + 2) * (m2 + 3) / 2, pbp = pb0 + (m2 + 1) * (m2 + 2) / 2;
+    for (int q = 0; q < 4; ++q) {
+      for (int j = 1 + (q >> 1) + 2 * warp; j <= n - 2 - k; j += 2 * nwarps)
+        for (int i = 1 + (q & 1) + 2 * lane; i + j + k <= n - 1; i += 64) {
+          const int c = lat2(m2, i, j);
+          double x[15];
+          gs_gather(x, [&](int o) { return um[o]; }, pbm, pb0, pbp, c, j, m2);
+          um[pb0 + c] = (__ldg(bm + pb0 + c) - gs_row_fma(s, x)) * inv_c;
+        }
+      __syncthreads();
     }
   }
 }
@@ -1833,57 +1892,87 @@ void launch3_apply(const DevLevel3D& lv, bool mass, const double* x, double* y, 
   check3("k3_apply");
 }
 
+// interior phase of one sweep (levels without step lists, the sharded path, KB_GS3_SPLIT)
+template <int NT, int US, int BS>
+void launch_gs_planes(const DevLevel3D& lv, double* u, const double* b, cudaStream_t st) {
+  const int steps = 4 * (lv.n - 3);
+  const int smem = 8 * (US + BS) + 8 * ((steps + 4) >> 2 << 1) + (US + BS) * plane_stride(lv.n) * 8;
+  static std::mutex mu;
+  static std::map<int, int> high;  // per device: largest opt-in so far
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    int dev = 0;
+    KB_CUDA_CHECK(cudaGetDevice(&dev));
+    if (smem > 48 * 1024 && high[dev] < smem) {
+      KB_CUDA_CHECK(cudaFuncSetAttribute(k3_gs_planes<NT, US, BS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      high[dev] = smem;
+    }
+  }
+  k3_gs_planes<NT, US, BS><<<lv.M, NT, smem, st>>>(lv, u, b);
+  check3("k3_gs_planes");
+}
+
+void launch3_gs_interior(const DevLevel3D& lv, double* u, const double* b, cudaStream_t st) {
+  init_constants();
+  if (lv.n < 4 || lv.M <= 0) return;  // no lattice-interior nodes
+  if (!lv.pat_node) {  // n > 64
+    k3_gs_planes_global<<<lv.M, kT, 0, st>>>(lv, u, b);
+    check3("k3_gs_planes_global");
+  } else if (lv.n == 64) {
+    launch_gs_planes<512, 4, 2>(lv, u, b, st);
+  } else if (lv.n == 32) {
+    launch_gs_planes<128, 8, 4>(lv, u, b, st);
+  } else {
+    launch_gs_planes<32, 8, 4>(lv, u, b, st);
+  }
+}
+
 void launch3_gs(const DevLevel3D& lv, double* u, const double* b, int sweeps, cudaStream_t st) {
   init_constants();
   if (sweeps <= 0) return;
-  if (!gs_split()) {
-    // 512-thread CTAs, one per SM, for large macros (the working set of the
-    // macros in flight stays in L2), 256-thread CTAs three per SM otherwise
-    static int sms = 0, occ_big = 0, occ_small = 0;
-    if (sms == 0) {
-      sms = device_attr3(cudaDevAttrMultiProcessorCount);
-      KB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_big, k3_gs_sweeps<512, 1>, 512, 0));
-      KB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_small, k3_gs_sweeps<256, 3>, 256, 0));
-      if (occ_big < 1 || occ_small < 1) fail(KB_CUDA, "k3_gs_sweeps cannot be resident");
+  if (gs_split()) {
+    for (int s = 0; s < sweeps; ++s) {
+      for (int c = 0; c < lv.colors; ++c) {
+        k3_gs_groups<<<blocks_for(lv.ng), kT, 0, st>>>(lv, u, b, c);
+        check3("k3_gs_groups");
+      }
+      launch3_gs_interior(lv, u, b, st);
     }
-    bool big = false;
-    if (const char* e = getenv("KB_GS3_BIG")) big = e[0] == '1';
-    const int nt = big ? 512 : 256;
-    int grid = (big ? occ_big : occ_small) * sms;
-    if (lv.n <= 4) grid = std::min(grid, sms);  // tiny levels: one CTA per SM (cheaper grid barriers)
-    if (const char* e = getenv("KB_GS3_GRID")) grid = std::max(1, std::min(grid, atoi(e)));
-    int active = grid;
-    if (const char* e = getenv("KB_GS3_ACTIVE")) active = std::max(1, std::min(grid, atoi(e)));
-    // interior macros batched per colour pass: all of the CTA's, except n = 32
-    // where pairs keep the pass's working set in L2 (measured 0.68 -> 0.53 ms
-    // per 2 sweeps on 3072 macros)
-    int group = lv.n == 32 ? 2 : lv.M;
-    if (const char* e = getenv("KB_GS3_G")) group = std::max(1, atoi(e));
+    return;
+  }
+  // 256-thread CTAs, three per SM (cooperative: grid barriers between the colours)
+  static int sms = 0, occ = 0;
+  if (sms == 0) {
+    sms = device_attr3(cudaDevAttrMultiProcessorCount);
+    KB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k3_gs_sweeps<256, 3>, 256, 0));
+    if (occ < 1) fail(KB_CUDA, "k3_gs_sweeps cannot be resident");
+  }
+  int grid = occ * sms;
+  if (lv.n <= 4) grid = std::min(grid, sms);  // tiny levels: one CTA per SM (cheaper grid barriers)
+  if (const char* e = getenv("KB_GS3_GRID")) grid = std::max(1, std::min(grid, atoi(e)));
+  int active = grid;
+  if (const char* e = getenv("KB_GS3_ACTIVE")) active = std::max(1, std::min(grid, atoi(e)));
+  int group = lv.M;  // macros of a CTA taken together per interior step
+  if (const char* e = getenv("KB_GS3_G")) group = std::max(1, atoi(e));
+  // levels with step lists (n <= 16) run whole in one launch; larger levels
+  // alternate the boundary colours (cooperative) with the plane-stream interior
+  const bool whole = lv.n <= 16;
+  const int calls = whole ? 1 : sweeps;
+  for (int s = 0; s < calls; ++s) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(nt);
+    cfg.blockDim = dim3(256);
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (big)
-      KB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k3_gs_sweeps<512, 1>, lv, u, b, sweeps, gs_phases(), active, group));
-    else
-      KB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k3_gs_sweeps<256, 3>, lv, u, b, sweeps, gs_phases(), active, group));
-    return;
-  }
-  for (int s = 0; s < sweeps; ++s) {
-    for (int c = 0; c < lv.colors; ++c) {
-      k3_gs_groups<<<blocks_for(lv.ng), kT, 0, st>>>(lv, u, b, c);
-      check3("k3_gs_groups");
-    }
-    if (lv.n < 4) continue;  // no lattice-interior nodes
-    for (int c = 0; c < lv.colors; ++c) {
-      k3_gs_color<<<lv.M * (lv.n + 1), kT, 0, st>>>(lv, u, b, c);
-      check3("k3_gs_color");
-    }
+    const int ph = gs_phases();
+    if (ph & 1 || whole)
+      KB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k3_gs_sweeps<256, 3>, lv, u, b, whole ? sweeps : 1, whole ? ph : (ph & ~2),
+                                       active, group));
+    if (!whole && (ph & 2)) launch3_gs_interior(lv, u, b, st);
   }
 }
 
@@ -1892,7 +1981,9 @@ int launch3_estimate_count(const DevLevel3D& lv) { return !estimate_cells() && a
 
 int launch3_gs_count(const DevLevel3D& lv, int sweeps) {
   if (sweeps <= 0) return 0;
-  return gs_split() ? sweeps * lv.colors * (lv.n >= 4 ? 2 : 1) : 1;
+  const int interior = lv.n >= 4 ? 1 : 0;
+  if (gs_split()) return sweeps * (lv.colors + interior);
+  return lv.n <= 16 ? 1 : sweeps * (1 + interior);
 }
 
 void launch3_prolong(const DevLevel3D& coarse, const DevLevel3D& fine, const double* c, double* f, int mode,
@@ -2017,15 +2108,6 @@ void launch3_gs_color_groups(const DevLevel3D& lv, double* u, const double* b, i
   init_constants();
   k3_gs_groups<<<blocks_for(lv.ng), kT, 0, st>>>(lv, u, b, c);
   check3("k3_gs_groups");
-}
-
-void launch3_gs_interior(const DevLevel3D& lv, double* u, const double* b, cudaStream_t st) {
-  init_constants();
-  if (lv.n < 4) return;  // no lattice-interior nodes
-  for (int c = 0; c < lv.colors; ++c) {
-    k3_gs_color<<<lv.M * (lv.n + 1), kT, 0, st>>>(lv, u, b, c);
-    check3("k3_gs_color");
-  }
 }
 
 void launch3_axpy(double* y, const double* x, double alpha, std::int64_t count, cudaStream_t st) {

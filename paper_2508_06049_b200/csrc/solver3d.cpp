@@ -26,18 +26,6 @@ double gauss3(double x, double y, double z) {
 }  // namespace
 
 // ------------------------------------------------------------------ hierarchy upload
-namespace {
-// largest macro size whose interior smoother runs in the batched (node-list) form
-int batch_max_n() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("KB_GS3_BATCH_N");
-    v = e ? atoi(e) : 128;
-  }
-  return v;
-}
-}  // namespace
-
 std::unique_ptr<DeviceHierarchy3D> DeviceHierarchy3D::create(const Mesh3D& mesh, int max_level) {
   auto d = std::make_unique<DeviceHierarchy3D>();
   d->host = Hierarchy3D::build(mesh, max_level);
@@ -67,21 +55,43 @@ std::unique_ptr<DeviceHierarchy3D> DeviceHierarchy3D::create(const Mesh3D& mesh,
       const int q = lv.grp_ptr[g];
       own[l][g] = lv.mem_slot[q] * lv.S + lv.mem_idx[q];
     }
-    // colour -> parity pattern per macro; small levels: interior nodes per pattern
+    // colour -> parity pattern per macro
     col_pat[l].assign(static_cast<size_t>(h.M) * h.colors, -1);
     for (int s = 0; s < h.M; ++s)
       for (int p = 0; p < 8; ++p) col_pat[l][static_cast<size_t>(h.colors) * s + lv.pat_color[8 * s + p]] = p;
-    if (n <= batch_max_n()) {
-      pat_ptr[l].assign(9, 0);
-      for (int p = 0; p < 8; ++p) {
-        for (int k = 1; k <= n; ++k)
-          for (int j = 1; j <= n; ++j)
-            for (int i = 1; i + j + k <= n - 1; ++i)
-              if (((i & 1) | ((j & 1) << 1) | ((k & 1) << 2)) == p) pat_node[l].push_back(i | j << 10 | k << 20);
-        pat_ptr[l][p + 1] = static_cast<int>(pat_node[l].size());
-        pat_max[l] = std::max(pat_max[l], pat_ptr[l][p + 1] - pat_ptr[l][p]);
-      }
-      if (pat_node[l].empty()) pat_ptr[l].clear();
+    // the interior relaxations of a macro in the smoother's order: step (plane k,
+    // parity class q) at [pat_ptr[4 (k - 1) + q], ...), entry = lat2(n - k, i, j) | j << 16
+    if (n >= 4 && n <= 64) {
+      pat_ptr[l].assign(1, 0);
+      for (int k = 1; k <= n - 3; ++k)
+        for (int q = 0; q < 4; ++q) {
+          // The nodes of a step are independent, so their order is free: runs of
+          // 8 consecutive class nodes of a row (16-byte stride) are paired, one
+          // with an even and one with an odd in-plane index, per half-warp — the
+          // two runs then fall on disjoint shared-memory banks for every one of
+          // the 14 neighbour loads (all offsets shift both runs alike).
+          std::vector<std::vector<int>> run[2];
+          std::vector<int> rest;
+          for (int j = 1 + (q >> 1); j <= n - 2 - k; j += 2) {
+            std::vector<int> row;
+            for (int i = 1 + (q & 1); i <= n - 1 - k - j; i += 2)
+              row.push_back((j * (n - k + 1) - (j * (j - 1)) / 2 + i) | j << 16);
+            size_t t = 0;
+            for (; t + 8 <= row.size(); t += 8)
+              run[(row[t] & 0xffff) & 1].emplace_back(row.begin() + t, row.begin() + t + 8);
+            rest.insert(rest.end(), row.begin() + t, row.end());
+          }
+          const size_t pairs = std::min(run[0].size(), run[1].size());
+          for (size_t t = 0; t < pairs; ++t)
+            for (int h = 0; h < 2; ++h) pat_node[l].insert(pat_node[l].end(), run[h][t].begin(), run[h][t].end());
+          for (int h = 0; h < 2; ++h)
+            for (size_t t = pairs; t < run[h].size(); ++t)
+              pat_node[l].insert(pat_node[l].end(), run[h][t].begin(), run[h][t].end());
+          pat_node[l].insert(pat_node[l].end(), rest.begin(), rest.end());
+          const int end = static_cast<int>(pat_node[l].size());
+          pat_max[l] = std::max(pat_max[l], end - pat_ptr[l].back());
+          pat_ptr[l].push_back(end);
+        }
     }
     auto vb = [](auto& v) { return r256(v.size() * sizeof(v[0])); };
     bytes += vb(lv.grp_ptr) + vb(lv.mem_slot) + vb(ijk[l]) + vb(lv.grp_domain) + vb(lv.grp_diag) +
