@@ -592,42 +592,54 @@ __device__ void gs_group(const DevLevel3D& lv, double* u, const double* __restri
 // the lanes write their own members' copies.  All 32 lanes of the warp call it
 // (valid = false for lane groups without a group).
 template <int W>
-__device__ __forceinline__ void gs_group_lanes(const DevLevel3D& lv, double* u, const double* __restrict__ b, int g,
+__device__ __forceinline__ void gs_group_lanes(const DevLevel3D& lv, double* u, const double* __restrict__ b, int t,
                                                bool valid, int sub) {
   constexpr int R = 4 / W;  // members per lane
   const int n = lv.n, S = lv.S;
-  int beg = 0, cnt = 0, slot[R], i[R], j[R], k[R];
-  double part[R];
+  int cnt = 0, slot[R], i[R], j[R], k[R];
+  double part[R], diag = 1.0;
   bool dom = false;
-  if (valid) {
-    beg = lv.grp_ptr[g];
-    cnt = lv.grp_ptr[g + 1] - beg;
-    dom = lv.grp_domain[g];
-  }
+  // One round trip for the group's data: its flat record (header: diagonal,
+  // member count, domain flag; four member slots of (macro slot, i j k)) at
+  // the group's position in the colour list; without records (shard tables)
+  // the chain colour list -> group -> member tables.
+  if (lv.nar_hdr) {
+    int4 hd = make_int4(0, 0, 0, 0);
+    if (valid) hd = __ldg(lv.nar_hdr + t);
+    cnt = hd.z & 0xff;
+    dom = (hd.z >> 8) != 0;
+    diag = __hiloint2double(hd.y, hd.x);
 #pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int q = sub + W * r;
-    slot[r] = -1;
-    i[r] = j[r] = k[r] = 0;
-    part[r] = 0.0;
-    if (valid && q < cnt) {
-      slot[r] = lv.mem_slot[beg + q];
-      if (slot[r] < 0) {
-        part[r] = lv.ghost[~slot[r]];
-      } else {
-        unpack_ijk(lv.mem_ijk[beg + q], i[r], j[r], k[r]);
-        if (!dom) part[r] = partial_off3(lv.psK + 240 * slot[r], u + static_cast<size_t>(slot[r]) * S, n, i[r], j[r], k[r]);
+    for (int r = 0; r < R; ++r) {
+      const int q = sub + W * r;
+      int2 mm = make_int2(-1, 0);
+      if (valid && q < cnt) mm = __ldg(lv.nar_mem + 4 * static_cast<size_t>(t) + q);
+      slot[r] = q < cnt ? mm.x : -1;
+      unpack_ijk(mm.y, i[r], j[r], k[r]);
+    }
+  } else {
+    int beg = 0;
+    if (valid) {
+      const int g = lv.color_grp[t];
+      beg = lv.grp_ptr[g];
+      cnt = lv.grp_ptr[g + 1] - beg;
+      dom = lv.grp_domain[g];
+      diag = lv.grp_diag[g];
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int q = sub + W * r;
+      slot[r] = -1;
+      i[r] = j[r] = k[r] = 0;
+      if (valid && q < cnt) {
+        slot[r] = lv.mem_slot[beg + q];
+        if (slot[r] >= 0) unpack_ijk(lv.mem_ijk[beg + q], i[r], j[r], k[r]);
       }
     }
   }
   const int qbase = (threadIdx.x & 31) & ~(W - 1);
-  double off = 0.0;
-#pragma unroll
-  for (int t = 0; t < 4; ++t) {
-    const double v = __shfl_sync(0xffffffffu, part[t / W], qbase + t % W);
-    if (t < cnt) off = off + v;
-  }
-  // the first member on this shard holds b (b's copies are interface-consistent)
+  // the first member on this shard holds b (b's copies are interface-consistent);
+  // its load goes out before the partial rows
   unsigned mine = 0;
 #pragma unroll
   for (int r = 0; r < R; ++r) mine |= (valid && sub + W * r < cnt && slot[r] >= 0) ? 1u << r : 0u;
@@ -641,10 +653,27 @@ __device__ __forceinline__ void gs_group_lanes(const DevLevel3D& lv, double* u, 
   double bown = 0.0;
 #pragma unroll
   for (int r = 0; r < R; ++r)
-    if (valid && sub + W * r == first) bown = b[static_cast<size_t>(slot[r]) * S + lat3(n, i[r], j[r], k[r])];
+    if (valid && sub + W * r == first) bown = __ldg(b + static_cast<size_t>(slot[r]) * S + lat3(n, i[r], j[r], k[r]));
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int q = sub + W * r;
+    part[r] = 0.0;
+    if (valid && q < cnt) {
+      if (slot[r] < 0)
+        part[r] = lv.ghost[~slot[r]];
+      else if (!dom)
+        part[r] = partial_off3(lv.psK + 240 * slot[r], u + static_cast<size_t>(slot[r]) * S, n, i[r], j[r], k[r]);
+    }
+  }
+  double off = 0.0;
+#pragma unroll
+  for (int t4 = 0; t4 < 4; ++t4) {
+    const double v = __shfl_sync(0xffffffffu, part[t4 / W], qbase + t4 % W);
+    if (t4 < cnt) off = off + v;
+  }
   const double bq = __shfl_sync(0xffffffffu, bown, qbase + (first < 4 ? first % W : 0));
   if (!valid) return;
-  const double val = dom ? bq : (bq - off) / lv.grp_diag[g];
+  const double val = dom ? bq : (bq - off) / diag;
 #pragma unroll
   for (int r = 0; r < R; ++r)
     if (sub + W * r < cnt && slot[r] >= 0) u[static_cast<size_t>(slot[r]) * S + lat3(n, i[r], j[r], k[r])] = val;
@@ -789,12 +818,12 @@ __global__ void __launch_bounds__(NT, MINB) k3_gs_sweeps(DevLevel3D lv, double* 
           if (lv.n <= 16) {
             for (int t0 = pw + 8 * gw; t0 < p1; t0 += 8 * nw) {
               const int t = t0 + (lane >> 2);
-              gs_group_lanes<4>(lv, u, b, t < p1 ? lv.color_grp[t] : 0, t < p1, lane & 3);
+              gs_group_lanes<4>(lv, u, b, t, t < p1, lane & 3);
             }
           } else {
             for (int t0 = pw + 16 * gw; t0 < p1; t0 += 16 * nw) {
               const int t = t0 + (lane >> 1);
-              gs_group_lanes<2>(lv, u, b, t < p1 ? lv.color_grp[t] : 0, t < p1, lane & 1);
+              gs_group_lanes<2>(lv, u, b, t, t < p1, lane & 1);
             }
           }
         }
