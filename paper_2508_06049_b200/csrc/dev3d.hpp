@@ -25,11 +25,14 @@ struct DevLevel3D {
   const int* color_grp_ptr;    // boundary groups by colour
   const int* color_grp;         // per colour: wide groups (> 4 members) first
   const int* color_wide_end;    // per colour: end of its wide groups in color_grp
-  // flat records of the narrow groups (<= 4 members) at their position t in
-  // color_grp: header (diagonal lo, hi, members | domain << 8, 0) and four
-  // member slots (macro slot, i | j << 10 | k << 20); null on shard tables
+  // flat records of the groups at their position t in color_grp: header
+  // (diagonal lo, hi, members | domain << 16, first member in wide_mem) and, for
+  // narrow groups (<= 4 members), four member slots (macro slot, i | j << 10 |
+  // k << 20) at 4 t; wide groups keep theirs contiguous in wide_mem; null on
+  // shard tables
   const int4* nar_hdr;
   const int2* nar_mem;
+  const int2* wide_mem;
   const double* kstiff;        // 96 per macro: [type][4][4]
   const double* kmass;
   const double* stK;           // 15 per macro (kDir order)

@@ -606,8 +606,8 @@ __device__ __forceinline__ void gs_group_lanes(const DevLevel3D& lv, double* u, 
   if (lv.nar_hdr) {
     int4 hd = make_int4(0, 0, 0, 0);
     if (valid) hd = __ldg(lv.nar_hdr + t);
-    cnt = hd.z & 0xff;
-    dom = (hd.z >> 8) != 0;
+    cnt = hd.z & 0xffff;
+    dom = (hd.z >> 16) != 0;
     diag = __hiloint2double(hd.y, hd.x);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -746,8 +746,42 @@ __device__ void gs_interior_batch(const DevLevel3D& lv, double* u, const double*
 
 // Relaxation of a group with many members (macro vertices, edges): one warp,
 // a lane per member partial row, the member sum in slot order by shuffles.
-__device__ void gs_group_warp(const DevLevel3D& lv, double* u, const double* __restrict__ b, int g, int lane) {
+__device__ void gs_group_warp(const DevLevel3D& lv, double* u, const double* __restrict__ b, int t, int lane) {
   const int n = lv.n, S = lv.S;
+  if (lv.nar_hdr) {
+    // flat record: header at the colour-list position, members contiguous from hd.w
+    const int4 hd = __ldg(lv.nar_hdr + t);
+    const int cnt = hd.z & 0xffff;
+    const bool dom = (hd.z >> 16) != 0;
+    const int2* mem = lv.wide_mem + hd.w;
+    double off = 0.0, bown = 0.0;
+    int2 first = make_int2(0, 0);
+    for (int q0 = 0; q0 < cnt; q0 += 32) {
+      double part = 0.0;
+      int2 mm = make_int2(0, 0);
+      if (q0 + lane < cnt) {
+        mm = __ldg(mem + q0 + lane);
+        int i, j, k;
+        unpack_ijk(mm.y, i, j, k);
+        if (q0 + lane == 0) bown = __ldg(b + static_cast<size_t>(mm.x) * S + lat3(n, i, j, k));
+        if (!dom) part = partial_off3(lv.psK + 240 * mm.x, u + static_cast<size_t>(mm.x) * S, n, i, j, k);
+      }
+      if (q0 == 0) first = mm;
+      const int c32 = min(32, cnt - q0);
+      if (!dom)
+        for (int q = 0; q < c32; ++q) off = off + __shfl_sync(0xffffffffu, part, q);
+    }
+    bown = __shfl_sync(0xffffffffu, bown, 0);
+    const double val = dom ? bown : (bown - off) / __hiloint2double(hd.y, hd.x);
+    for (int q = lane; q < cnt; q += 32) {
+      const int2 mm = q < 32 ? first : __ldg(mem + q);
+      int i, j, k;
+      unpack_ijk(mm.y, i, j, k);
+      u[static_cast<size_t>(mm.x) * S + lat3(n, i, j, k)] = val;
+    }
+    return;
+  }
+  const int g = lv.color_grp[t];
   const int beg = lv.grp_ptr[g], end = lv.grp_ptr[g + 1];
   int ql = beg;
   while (lv.mem_slot[ql] < 0) ++ql;
@@ -802,11 +836,20 @@ __global__ void __launch_bounds__(NT, MINB) k3_gs_sweeps(DevLevel3D lv, double* 
 #ifdef KB_GS_TRACE
   if ((phases & 4) && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_gs3_trace[63]));
 #endif
+  // colour ranges once (not a dependent load at the head of every phase)
+  __shared__ int s_cptr[65], s_cwide[64];
+  for (int c = threadIdx.x; c <= lv.colors && c <= 64; c += NT) {
+    s_cptr[c] = lv.color_grp_ptr[c];
+    if (c < lv.colors) s_cwide[c] = lv.color_wide_end[c];
+  }
+  __syncthreads();
   for (int sw = 0; sw < sweeps; ++sw) {
     for (int c = 0; c < lv.colors; ++c) {
-      const int p0 = lv.color_grp_ptr[c], p1 = lv.color_grp_ptr[c + 1], pw = lv.color_wide_end[c];
+      const bool cached = lv.colors <= 64;
+      const int p0 = cached ? s_cptr[c] : lv.color_grp_ptr[c], p1 = cached ? s_cptr[c + 1] : lv.color_grp_ptr[c + 1],
+                pw = cached ? s_cwide[c] : lv.color_wide_end[c];
       if (phases & 1) {
-        for (int t = p0 + gw; t < pw; t += nw) gs_group_warp(lv, u, b, lv.color_grp[t], lane);
+        for (int t = p0 + gw; t < pw; t += nw) gs_group_warp(lv, u, b, t, lane);
 #ifdef KB_GS_TRACE
         if (phases & 8) {  // measurement trace: one thread per group
           for (int t = pw + tid; t < p1; t += nthreads)

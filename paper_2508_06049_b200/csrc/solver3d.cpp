@@ -97,7 +97,8 @@ std::unique_ptr<DeviceHierarchy3D> DeviceHierarchy3D::create(const Mesh3D& mesh,
     bytes += vb(lv.grp_ptr) + vb(lv.mem_slot) + vb(ijk[l]) + vb(lv.grp_domain) + vb(lv.grp_diag) +
              vb(lv.color_grp_ptr) + vb(lv.color_grp) + vb(lv.kstiff) + vb(lv.kmass) + 2 * vb(lv.stencil) +
              vb(lv.inv_c) + vb(lv.pat_color) + vb(own[l]) + r256(4 * h.colors) + vb(col_pat[l]) +
-             vb(pat_ptr[l]) + vb(pat_node[l]) + r256(lv.color_grp.size() * 16) + r256(lv.color_grp.size() * 32);
+             vb(pat_ptr[l]) + vb(pat_node[l]) + r256(lv.color_grp.size() * 16) + r256(lv.color_grp.size() * 32) +
+             r256(lv.mem_slot.size() * 8 + 8);
   }
   // level-0 CG program: for every vertex group, its members' partial stencils
   // as (coefficient, global vertex) terms, centre first (level-0 groups are the
@@ -161,19 +162,27 @@ std::unique_ptr<DeviceHierarchy3D> DeviceHierarchy3D::create(const Mesh3D& mesh,
       }
       dl.color_grp = d->arena.upload(cg);
       dl.color_wide_end = d->arena.upload(wide_end);
-      // flat records of the narrow groups at their colour-list position
+      // flat records of the groups at their colour-list position
       std::vector<int4> hdr(cg.size(), make_int4(0, 0, 0, 0));
-      std::vector<int2> mem(4 * cg.size(), make_int2(-1, 0));
+      std::vector<int2> mem(4 * cg.size(), make_int2(-1, 0)), wide;
       for (size_t t = 0; t < cg.size(); ++t) {
         const int g = cg[t], beg = lv.grp_ptr[g], cnt = lv.grp_ptr[g + 1] - beg;
-        if (cnt > 4) continue;
+        if (cnt > 0xffff) fail(KB_STRUCTURAL, "shared-node group with more than 65535 members");
         std::int32_t w[2];
         std::memcpy(w, &lv.grp_diag[g], 8);
-        hdr[t] = make_int4(w[0], w[1], cnt | (lv.grp_domain[g] ? 1 << 8 : 0), 0);
-        for (int q = 0; q < cnt; ++q) mem[4 * t + q] = make_int2(lv.mem_slot[beg + q], ijk[l][beg + q]);
+        hdr[t] = make_int4(w[0], w[1], cnt | (lv.grp_domain[g] ? 1 << 16 : 0), static_cast<int>(wide.size()));
+        for (int q = 0; q < cnt; ++q) {
+          const int2 rec = make_int2(lv.mem_slot[beg + q], ijk[l][beg + q]);
+          if (cnt <= 4)
+            mem[4 * t + q] = rec;
+          else
+            wide.push_back(rec);
+        }
       }
+      if (wide.empty()) wide.push_back(make_int2(0, 0));
       dl.nar_hdr = d->arena.upload(hdr);
       dl.nar_mem = d->arena.upload(mem);
+      dl.wide_mem = d->arena.upload(wide);
     }
     dl.kstiff = d->arena.upload(lv.kstiff);
     dl.kmass = d->arena.upload(lv.kmass);
