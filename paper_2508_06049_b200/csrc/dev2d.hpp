@@ -8,10 +8,31 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include "hier2d.hpp"
 
 namespace kb {
+
+// Dynamic shared memory above 48 KB needs the per-kernel opt-in, which is a
+// per-device attribute.  The high-water mark is kept per (device, kernel)
+// under a mutex and only ever grows: graph nodes captured earlier keep their
+// (larger) launch sizes valid when a later launch of the same kernel needs less.
+template <typename K>
+inline void ensure_dynamic_smem(K kernel, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> high;
+  if (smem <= 48 * 1024) return;
+  int dev = 0;
+  KB_CUDA_CHECK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& hw = high[{dev, reinterpret_cast<const void*>(kernel)}];
+  if (smem <= hw) return;
+  KB_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  hw = smem;
+}
 
 struct DevLevel2D {
   int n, S, M;

@@ -2117,14 +2117,7 @@ int device_attr(cudaDeviceAttr a) {
 
 template <typename K>
 void set_smem(K kernel, size_t smem) {
-  // dynamic shared memory above 48 KB needs the opt-in.  The attribute only
-  // ever grows: graph nodes captured earlier keep their (larger) launch sizes
-  // valid when a later launch of the same kernel needs less.
-  static std::map<const void*, size_t> high;
-  size_t& hw = high[reinterpret_cast<const void*>(kernel)];
-  if (smem <= hw) return;
-  KB_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  hw = smem;
+  ensure_dynamic_smem(kernel, smem);
 }
 
 void launch_gs_level(const DevHier2D& hd, const DevLevel2D& lv, double* u, const double* b, int sweeps,

@@ -19,8 +19,6 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
-#include <map>
-#include <mutex>
 #include <string>
 
 #include "dev3d.hpp"
@@ -1938,12 +1936,7 @@ void launch3_apply(const DevLevel3D& lv, bool mass, const double* x, double* y, 
   init_constants();
   if (apply_streams(lv)) {
     const size_t smem = (kAsSlots + 240 + kAsSlots * static_cast<size_t>(plane_stride(lv.n))) * 8;
-    static size_t smem_set = 0;  // only ever grows (graph nodes captured earlier stay launchable)
-    if (smem > smem_set) {
-      KB_CUDA_CHECK(cudaFuncSetAttribute(k3_apply_stream, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem)));
-      smem_set = smem;
-    }
+    ensure_dynamic_smem(k3_apply_stream, smem);
     k3_apply_stream<<<lv.M, kAsThreads, smem, st>>>(lv, mass ? 1 : 0, x, y, b, mode);
     check3("k3_apply_stream");
     if (lv.ng > 0) {
@@ -1969,17 +1962,7 @@ template <int NT, int US, int BS>
 void launch_gs_planes(const DevLevel3D& lv, double* u, const double* b, cudaStream_t st) {
   const int steps = 4 * (lv.n - 3);
   const int smem = 8 * (US + BS) + 8 * ((steps + 4) >> 2 << 1) + (US + BS) * plane_stride(lv.n) * 8;
-  static std::mutex mu;
-  static std::map<int, int> high;  // per device: largest opt-in so far
-  {
-    std::lock_guard<std::mutex> lock(mu);
-    int dev = 0;
-    KB_CUDA_CHECK(cudaGetDevice(&dev));
-    if (smem > 48 * 1024 && high[dev] < smem) {
-      KB_CUDA_CHECK(cudaFuncSetAttribute(k3_gs_planes<NT, US, BS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      high[dev] = smem;
-    }
-  }
+  ensure_dynamic_smem(k3_gs_planes<NT, US, BS>, static_cast<size_t>(smem));
   k3_gs_planes<NT, US, BS><<<lv.M, NT, smem, st>>>(lv, u, b);
   check3("k3_gs_planes");
 }
@@ -2121,11 +2104,7 @@ void launch3_cg0(const DevLevel3D& lv0, double* u, const double* b, double* scra
   const int compact = compact_bytes > 0 && base + compact_bytes + 64 <= 220 * 1024 ? 1 : 0;
   const int nmem4 = !compact && lv0.cg_members4 > 0 && base + lv0.cg_members4 * 8.0 <= 200 * 1024 ? lv0.cg_members4 : 0;
   const size_t smem = base + (compact ? compact_bytes + 64 : static_cast<size_t>(nmem4) * 8);
-  static size_t cg0_high = 0;  // only ever grows (graph nodes captured earlier stay launchable)
-  if (smem > cg0_high) {
-    KB_CUDA_CHECK(cudaFuncSetAttribute(k3_cg0, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    cg0_high = smem;
-  }
+  ensure_dynamic_smem(k3_cg0, smem);
   k3_cg0<<<1, 1024, smem, st>>>(lv0, u, b, prm, status, nmem4, compact);
   check3("k3_cg0");
 }
@@ -2136,12 +2115,7 @@ void launch3_estimate(const DevLevel3D& lv, const double* uL, const double* wb, 
   const bool cells = estimate_cells();
   if (!cells && apply_streams(lv)) {
     const size_t smem = (240 + 6 * static_cast<size_t>(plane_stride(lv.n))) * 8;
-    static size_t smem_set = 0;  // only ever grows (graph nodes captured earlier stay launchable)
-    if (smem > smem_set) {
-      KB_CUDA_CHECK(cudaFuncSetAttribute(k3_estimate_stream, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem)));
-      smem_set = smem;
-    }
+    ensure_dynamic_smem(k3_estimate_stream, smem);
     k3_estimate_stream<<<lv.M, kEsThreads, smem, st>>>(lv, uL, wb, wc, sums);
     check3("k3_estimate_stream");
     return;

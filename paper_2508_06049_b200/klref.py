@@ -17,6 +17,8 @@ import os
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
 
+import time
+
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -272,6 +274,65 @@ class MacroMesh:
             parts = next(it).split()
             elements.append([idmap[int(v)] for v in parts[1:2 + dim]])
         return MacroMesh(np.array(coords, dtype=np.float64), np.array(elements, dtype=np.int32), dim)
+
+    def boundary_vertices(self) -> np.ndarray:
+        """Per vertex: on the domain boundary (a facet used by exactly one element),
+        the flag column of the mesh format (proj/src/mesh_io.cpp:121-127)."""
+        from collections import Counter
+        d = self.dim
+        cnt = Counter()
+        for el in self.elements:
+            for skip in range(d + 1):
+                cnt[tuple(sorted(int(v) for t, v in enumerate(el) if t != skip))] += 1
+        flag = np.zeros(len(self.coords), dtype=bool)
+        for facet, c in cnt.items():
+            if c == 1:
+                flag[list(facet)] = True
+        return flag
+
+    def write(self, path: str) -> None:
+        """write_mesh of the reference (proj/src/mesh_io.cpp:104-143): header, the
+        referenced vertices renumbered compactly in ascending id order with %.17g
+        coordinates and the boundary flag, the elements in slot order."""
+        used = sorted({int(v) for el in self.elements for v in el})
+        new = {old: k for k, old in enumerate(used)}
+        bnd = self.boundary_vertices()
+        with open(path, "w") as fh:
+            fh.write("# written " + time.strftime("%Y-%m-%d %H:%M:%S", time.gmtime()) + " UTC\n")
+            fh.write(f"dim {self.dim}\n")
+            fh.write(f"vertices {len(used)}\n")
+            for old in used:
+                xs = " ".join("%.17g" % float(c) for c in self.coords[old][: self.dim])
+                fh.write(f"{new[old]} {xs} {1 if bnd[old] else 0}\n")
+            fh.write(f"elements {len(self.elements)}\n")
+            for e, el in enumerate(self.elements):
+                fh.write(str(e) + " " + " ".join(str(new[int(v)]) for v in el) + "\n")
+
+
+def write_marks(path: str, ids) -> None:
+    """Marks file in the format read_marks_file accepts (proj/src/mesh_io.cpp:145-163):
+    element positions of the written mesh, whitespace separated, '#' comments."""
+    with open(path, "w") as fh:
+        fh.write("# marked elements (positions in the mesh file)\n")
+        fh.write(" ".join(str(int(i)) for i in sorted(set(int(i) for i in ids))) + "\n")
+
+
+def read_marks(path: str, num_elements: int) -> np.ndarray:
+    """read_marks_file (proj/src/mesh_io.cpp:145-163): sorted unique ids, range-checked."""
+    ids = []
+    try:
+        fh = open(path)
+    except OSError as e:
+        raise IoError(f"cannot open marks file: {path}") from e
+    with fh:
+        for ln in fh:
+            ln = ln.split("#", 1)[0]
+            for tok in ln.split():
+                v = int(tok)
+                if v < 0 or v >= num_elements:
+                    raise IoError(f"mark id out of range: {v}")
+                ids.append(v)
+    return np.array(sorted(set(ids)), dtype=np.int64)
 
 
 class _Handle:
