@@ -1974,11 +1974,13 @@ void launch3_gs_interior(const DevLevel3D& lv, double* u, const double* b, cudaS
     k3_gs_planes_global<<<lv.M, kT, 0, st>>>(lv, u, b);
     check3("k3_gs_planes_global");
   } else if (lv.n == 64) {
-    launch_gs_planes<512, 4, 2>(lv, u, b, st);
+    launch_gs_planes<512, 4, 2>(lv, u, b, st);  // 103 KB: two CTAs per SM
   } else if (lv.n == 32) {
-    launch_gs_planes<128, 8, 4>(lv, u, b, st);
+    // CTAs per SM matter more than the prefetch depth here (27 KB, eight CTAs
+    // per SM: 0.44 ms per 2 sweeps on 3072 macros; 54 KB with 8 + 4 slots: 0.62 ms)
+    launch_gs_planes<128, 4, 2>(lv, u, b, st);
   } else {
-    launch_gs_planes<32, 8, 4>(lv, u, b, st);
+    launch_gs_planes<32, 4, 2>(lv, u, b, st);
   }
 }
 
