@@ -697,12 +697,50 @@ static void set_bnd(const o3h* h, int l, int prob, const double* par, double* u,
   }
 }
 
-/* level-0 CG (cg_level0 order, proj/src/multigrid.cpp:198-229) */
+/* Level-0 operator on the macro-vertex values, assembled: row g adds, over
+ * the group's members in slot order, their partial stencils (centre first,
+ * then the directions inside the macro); coefficients of one column are added
+ * in that order, the columns keep their first-appearance order; y_g is the
+ * sequential sum over the row, written to every copy. */
+static void apply0(const o3h* h, const double* x, double* y) {
+  const o3lev* lv = &h->lv[0];
+  const int n = lv->n, S = lv->S;
+  for (int g = 0; g < lv->ng; ++g) {
+    const int b = lv->gptr[g], e = lv->gptr[g + 1];
+    int* col = malloc(sizeof(int) * 15 * (size_t)(e - b));
+    double* val = malloc(sizeof(double) * 15 * (size_t)(e - b));
+    int nc = 0;
+    for (int q = b; q < e; ++q) {
+      const int s = lv->mslot[q], i = lv->mi[q], j = lv->mj[q], k = lv->mk[q];
+      const double* ps = lv->psK + 240 * (size_t)s + 15 * sig_of(n, i, j, k);
+      for (int d = 0; d < 15; ++d) {
+        const int a = i + DIR[d][0], bb = j + DIR[d][1], c = k + DIR[d][2];
+        if (!inl(n, a, bb, c)) continue;
+        const int gc = lv->gid[(size_t)s * S + lat3(n, a, bb, c)];
+        int t = 0;
+        while (t < nc && col[t] != gc) ++t;
+        if (t == nc) { col[nc] = gc; val[nc] = ps[d]; ++nc; }
+        else val[t] = val[t] + ps[d];
+      }
+    }
+    double v = 0.0;
+    for (int t = 0; t < nc; ++t) {
+      const int gb = lv->gptr[col[t]];
+      const double xv = x[(size_t)lv->mslot[gb] * S + lv->midx[gb]];
+      v = t == 0 ? val[0] * xv : v + val[t] * xv;
+    }
+    for (int q = b; q < e; ++q) y[(size_t)lv->mslot[q] * S + lv->midx[q]] = v;
+    free(col); free(val);
+  }
+}
+
+/* level-0 CG (cg_level0 order, proj/src/multigrid.cpp:198-229) on the assembled operator */
 int o3_cg0(const o3h* h, double* u, const double* b, double rel, double absf, int maxit, int* iters) {
   const o3lev* lv = &h->lv[0];
   const size_t N = (size_t)h->M * lv->S;
   double *r = malloc(8 * N), *p = malloc(8 * N), *ap = malloc(8 * N), *bz = malloc(8 * N);
-  o3_residual(h, 0, u, b, r);
+  apply0(h, u, r);
+  for (size_t q = 0; q < N; ++q) r[q] = (lv->flag[q] & 2) ? 0.0 : b[q] - r[q];
   memcpy(p, r, 8 * N);
   for (size_t q = 0; q < N; ++q) bz[q] = (lv->flag[q] & 2) ? 0.0 : b[q];
   double rr = o3_dot(h, 0, r, r);
@@ -711,7 +749,7 @@ int o3_cg0(const o3h* h, double* u, const double* b, double rel, double absf, in
   int it = 0, st = 0;
   while (sqrt(rr) > tol) {
     if (++it > maxit) { st = 1; break; }
-    o3_apply(h, 0, 0, p, ap);
+    apply0(h, p, ap);
     for (size_t q = 0; q < N; ++q)
       if (lv->flag[q] & 2) ap[q] = 0.0;
     const double pap = o3_dot(h, 0, p, ap);

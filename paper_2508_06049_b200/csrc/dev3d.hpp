@@ -49,20 +49,12 @@ struct DevLevel3D {
   const int* own_dot;          // group owner copy offsets (dot order)
   const double* psK;           // boundary partial stencils: 16 signatures x 15 per macro
   const double* psM;
-  // level-0 CG on the unique macro-vertex values (level 0 only): per group a
-  // member range, per member a term range of (coefficient, vertex) pairs
-  const int* cg_gmem;          // ng + 1
-  const int* cg_mterm;         // members + 1
-  const double* cg_coef;
-  const int* cg_vid;
-  int cg_members4;             // member count when every member has exactly 4 terms, else 0
-  // compact form of the 4-term program (cg_members4 > 0): the distinct
-  // coefficient rows (4 doubles each, bitwise-deduplicated), per member its row
-  // and its 4 vertex ids (16 bit); staged in shared memory by k3_cg0
-  const double* cg_rows;
-  const unsigned short* cg_mrow;
-  const unsigned short* cg_mvid;  // 4 per member
-  int cg_nrows;                   // 0: not available
+  // level-0 CG on the unique macro-vertex values (level 0 only): the assembled
+  // operator rows (row g = group g = macro vertex g; columns are vertex ids)
+  const int* cg_rowptr;        // ng + 1
+  const unsigned short* cg_col;
+  const double* cg_val;
+  int cg_nnz;
   // sharded levels (solver3d_shard.cpp): a member with mem_slot < 0 lives on
   // another shard; its contribution (partial row or copy value, as the
   // operation needs) is ghost[~mem_slot], received by the exchange before the

@@ -1240,97 +1240,19 @@ __global__ void __launch_bounds__(kT) k3_pack(DevLevel3D lv, int mode, const dou
 }
 
 // ---------------------------------------------------------------- level-0 CG (one CTA)
-// cg_level0 (proj/src/multigrid.cpp:198-229 sequence) on the unique
-// macro-vertex values held in shared memory; operator rows from the level-0
-// program (the members' partial stencils in slot order, the same arithmetic
-// as the copy-based apply), inner products in chunks of 32 terms then over
-// the chunk sums (the 3-d dot order, oracle o3_dot).
-__device__ void cg0_apply(const DevLevel3D& lv, const double* x, double* y, const double* b,
-                          const unsigned char* dom, int residual) {
-  for (int g = threadIdx.x; g < lv.ng; g += blockDim.x) {
-    const int m0 = lv.cg_gmem[g], m1 = lv.cg_gmem[g + 1];
-    double v = 0.0;
-    for (int q = m0; q < m1; ++q) {
-      const int t0 = lv.cg_mterm[q], t1 = lv.cg_mterm[q + 1];
-      double acc = lv.cg_coef[t0] * x[lv.cg_vid[t0]];
-      for (int t = t0 + 1; t < t1; ++t) acc = acc + lv.cg_coef[t] * x[lv.cg_vid[t]];
-      v = (m1 - m0 == 1) ? acc : v + acc;
-    }
-    y[g] = dom[g] ? 0.0 : (residual ? b[g] - v : v);
-  }
-}
-
-// Same operator, member-parallel (every level-0 member has exactly 4 terms):
-// the members' partial rows into mp[] (the loads of 4 members in flight per
-// thread), then per group the member sum in slot order from shared memory.
-__device__ void cg0_apply4(const DevLevel3D& lv, const double* x, double* y, const double* b,
-                           const unsigned char* dom, int residual, double* mp, int nmem) {
-  const double2* cf = reinterpret_cast<const double2*>(lv.cg_coef);
-  const int4* vi = reinterpret_cast<const int4*>(lv.cg_vid);
-  constexpr int U = 4;
-  for (int q0 = threadIdx.x; q0 < nmem; q0 += U * blockDim.x) {
-    double2 c[U][2];
-    int4 v[U];
-#pragma unroll
-    for (int a = 0; a < U; ++a) {
-      const int q = min(q0 + a * static_cast<int>(blockDim.x), nmem - 1);
-      c[a][0] = __ldg(cf + 2 * q);
-      c[a][1] = __ldg(cf + 2 * q + 1);
-      v[a] = __ldg(vi + q);
-    }
-#pragma unroll
-    for (int a = 0; a < U; ++a) {
-      const int q = q0 + a * static_cast<int>(blockDim.x);
-      double acc = c[a][0].x * x[v[a].x];
-      acc = acc + c[a][0].y * x[v[a].y];
-      acc = acc + c[a][1].x * x[v[a].z];
-      acc = acc + c[a][1].y * x[v[a].w];
-      if (q < nmem) mp[q] = acc;
-    }
-  }
-  __syncthreads();
-  for (int g = threadIdx.x; g < lv.ng; g += blockDim.x) {
-    const int m0 = lv.cg_gmem[g], m1 = lv.cg_gmem[g + 1];
-    double v = 0.0;
-    for (int q = m0; q < m1; ++q) v = (m1 - m0 == 1) ? mp[q] : v + mp[q];
-    y[g] = dom[g] ? 0.0 : (residual ? b[g] - v : v);
-  }
-}
-
-// Same operator from the compact program: the distinct coefficient rows and the
-// member row ids in shared memory, the member vertex ids (8 bytes per member)
-// from L2; member partials in parallel into mp[] (4 members in flight per
-// thread), then per group the member sum in slot order from shared memory (the
-// order and arithmetic of cg0_apply).
-__device__ void cg0_apply_compact(int ng, int nm, const int* gmem, const double* rows, const unsigned short* mrow,
-                                  const ushort4* __restrict__ mvid, const double* x, double* y, const double* b,
-                                  const unsigned char* dom, int residual, double* mp) {
-  constexpr int U = 4;
-  for (int q0 = threadIdx.x; q0 < nm; q0 += U * blockDim.x) {
-    ushort4 v[U];
-    int rw[U];
-#pragma unroll
-    for (int a = 0; a < U; ++a) {
-      const int q = min(q0 + a * static_cast<int>(blockDim.x), nm - 1);
-      v[a] = __ldg(mvid + q);
-      rw[a] = mrow[q];
-    }
-#pragma unroll
-    for (int a = 0; a < U; ++a) {
-      const int q = q0 + a * static_cast<int>(blockDim.x);
-      const double* c = rows + 4 * rw[a];
-      double acc = c[0] * x[v[a].x];
-      acc = acc + c[1] * x[v[a].y];
-      acc = acc + c[2] * x[v[a].z];
-      acc = acc + c[3] * x[v[a].w];
-      if (q < nm) mp[q] = acc;
-    }
-  }
-  __syncthreads();
+// CG on the unique macro-vertex values in shared memory (cg_level0's loop,
+// proj/src/multigrid.cpp:198-229).  The level-0 operator is assembled (round 2
+// specification, oracle apply0): row g adds, over the group's members in slot
+// order, their partial stencils (centre first, then the directions inside the
+// macro), coefficients of one column added in that order, columns in
+// first-appearance order; y_g is the sequential sum over the row.  One thread
+// per row; the rows sit in shared memory when they fit.
+__device__ void cg0_apply_csr(int ng, const int* rp, const unsigned short* col, const double* val, const double* x,
+                              double* y, const double* b, const unsigned char* dom, int residual) {
   for (int g = threadIdx.x; g < ng; g += blockDim.x) {
-    const int m0 = gmem[g], m1 = gmem[g + 1];
-    double v = 0.0;
-    for (int q = m0; q < m1; ++q) v = (m1 - m0 == 1) ? mp[q] : v + mp[q];
+    const int p0 = rp[g], p1 = rp[g + 1];
+    double v = val[p0] * x[col[p0]];
+    for (int t = p0 + 1; t < p1; ++t) v = v + val[t] * x[col[t]];
     y[g] = dom[g] ? 0.0 : (residual ? b[g] - v : v);
   }
 }
@@ -1370,7 +1292,7 @@ __device__ double cg0_dot(int ng, const double* a, const double* b, const unsign
 }
 
 __global__ void __launch_bounds__(1024) k3_cg0(DevLevel3D lv, double* uc, const double* bc, CgParams prm,
-                                               DevStatus* status, int nmem4, int compact) {
+                                               DevStatus* status, int staged) {
   extern __shared__ double sm[];
   const int ng = lv.ng;
   double* u = sm;
@@ -1380,28 +1302,24 @@ __global__ void __launch_bounds__(1024) k3_cg0(DevLevel3D lv, double* uc, const 
   double* ap = p + ng;
   double* prod = ap + ng;  // dot-product terms
   double* chunks = prod + ng;
-  double* mp = chunks + (ng + 31) / 32;  // nmem4 member partials (member-parallel operator)
-  // compact program (compact != 0, nmem4 == 0): member partials, rows, member rows, group ranges
-  const int nm = compact ? lv.cg_members4 : 0;
-  double* cmp = mp;
-  double* crow = cmp + nm;
-  unsigned short* cmrow = reinterpret_cast<unsigned short*>(crow + (compact ? 4 * lv.cg_nrows : 0));
-  int* cgm = reinterpret_cast<int*>(cmrow + ((nm + 1) & ~1));
-  unsigned char* dom = compact ? reinterpret_cast<unsigned char*>(cgm + ng + 1)
-                               : reinterpret_cast<unsigned char*>(mp + nmem4);
-  const ushort4* cvid = reinterpret_cast<const ushort4*>(lv.cg_mvid);
-  if (compact) {
-    for (int t = threadIdx.x; t < 4 * lv.cg_nrows; t += blockDim.x) crow[t] = lv.cg_rows[t];
-    for (int t = threadIdx.x; t < nm; t += blockDim.x) cmrow[t] = lv.cg_mrow[t];
-    for (int t = threadIdx.x; t <= ng; t += blockDim.x) cgm[t] = lv.cg_gmem[t];
+  // staged != 0: the assembled rows in shared memory behind the vectors
+  const int nnz = lv.cg_nnz;
+  double* sval = chunks + (ng + 31) / 32;
+  int* srp = reinterpret_cast<int*>(sval + (staged ? nnz : 0));
+  unsigned short* scol = reinterpret_cast<unsigned short*>(srp + (staged ? ng + 1 : 0));
+  unsigned char* dom = reinterpret_cast<unsigned char*>(scol + (staged ? ((nnz + 3) & ~3) : 0));
+  if (staged) {
+    for (int t = threadIdx.x; t < nnz; t += blockDim.x) {
+      sval[t] = lv.cg_val[t];
+      scol[t] = lv.cg_col[t];
+    }
+    for (int t = threadIdx.x; t <= ng; t += blockDim.x) srp[t] = lv.cg_rowptr[t];
   }
+  const int* rp = staged ? srp : lv.cg_rowptr;
+  const unsigned short* col = staged ? scol : lv.cg_col;
+  const double* val = staged ? sval : lv.cg_val;
   auto cg0_op = [&](const double* x, double* y, const double* bb, int residual) {
-    if (compact)
-      cg0_apply_compact(ng, nm, cgm, crow, cmrow, cvid, x, y, bb, dom, residual, cmp);
-    else if (nmem4 > 0)
-      cg0_apply4(lv, x, y, bb, dom, residual, mp, nmem4);
-    else
-      cg0_apply(lv, x, y, bb, dom, residual);
+    cg0_apply_csr(ng, rp, col, val, x, y, bb, dom, residual);
   };
   for (int g = threadIdx.x; g < ng; g += blockDim.x) {
     u[g] = uc[lv.own_dot[g]];
@@ -1633,13 +1551,17 @@ __global__ void __launch_bounds__(kEsThreads, 2) k3_estimate_stream(DevLevel3D l
   const int n = lv.n, S = lv.S, m = blockIdx.x, tid = threadIdx.x;
   const int stride = plane_stride(n);
   double* ps = reinterpret_cast<double*>(es_smem);  // 16 signatures x 15
-  double* rb = ps + 240;                             // e_b ring, 3 slots
-  double* rc = rb + 3 * stride;                      // e_c ring, 3 slots
+  double* rb = ps + 240;                             // e_b ring, 2 slots (planes k, k + 1)
+  double* rc = rb + 2 * stride;                      // e_c ring, 2 slots
   const size_t mo = static_cast<size_t>(m) * S;
-  for (int t = tid; t < 240; t += kEsThreads) ps[t] = __ldg(lv.psM + 240 * static_cast<size_t>(m) + t);
+  for (int t = tid; t < 240; t += kEsThreads)
+    ps[t] = __ldg(lv.psM + 240 * static_cast<size_t>(m) + t) * (t % 15 == 0 ? 1.0 : 2.0);
+  // e^T M e over the macro's (symmetric) assembled mass matrix as the diagonal
+  // plus twice the forward half: the odd directions are the lexicographically
+  // positive ones (planes k and k + 1 only), their coefficients doubled here
   double s[15];
 #pragma unroll
-  for (int d = 0; d < 15; ++d) s[d] = __ldg(lv.stM + 15 * static_cast<size_t>(m) + d);
+  for (int d = 0; d < 15; ++d) s[d] = __ldg(lv.stM + 15 * static_cast<size_t>(m) + d) * (d == 0 ? 1.0 : 2.0);
   double lu[kEsPer], lb[kEsPer], lc[kEsPer];
   auto load = [&](int k) {  // plane k of uL, wb, wc into registers
     if (k > n) return;
@@ -1657,7 +1579,7 @@ __global__ void __launch_bounds__(kEsThreads, 2) k3_estimate_stream(DevLevel3D l
   };
   auto store = [&](int k) {  // e of plane k into its ring slot
     if (k > n) return;
-    const int len = (n - k + 1) * (n - k + 2) / 2, sl = (k % 3) * stride;
+    const int len = (n - k + 1) * (n - k + 2) / 2, sl = (k & 1) * stride;
 #pragma unroll
     for (int t = 0; t < kEsPer; ++t) {
       const int q = tid + t * kEsThreads;
@@ -1678,7 +1600,7 @@ __global__ void __launch_bounds__(kEsThreads, 2) k3_estimate_stream(DevLevel3D l
     const int m2 = n - k;
     int base[3];
 #pragma unroll
-    for (int d = 0; d < 3; ++d) base[d] = (((k - 1 + d) % 3 + 3) % 3) * stride;
+    for (int d = 0; d < 3; ++d) base[d] = ((k - 1 + d) & 1) * stride;  // base[0] (plane k - 1) is not read
     if (k >= 1 && m2 >= 3) {
       const int mi = m2 - 3, ni = (mi + 1) * (mi + 2) / 2;
       for (int e = tid; e < ni; e += kEsThreads) {
@@ -1692,12 +1614,11 @@ __global__ void __launch_bounds__(kEsThreads, 2) k3_estimate_stream(DevLevel3D l
         ra[2] = ra[0] - (m2 + 2 - j);
         ra[5] = base[2] + r0 - j;
         ra[3] = ra[5] - (m2 + 1 - j);
-        ra[6] = base[0] + r0 + j;
-        ra[4] = ra[6] + (m2 + 2 - j);
+        ra[6] = ra[4] = 0;
         const double eb0 = rb[ra[0] + i], ec0 = rc[ra[0] + i];
         double mb = s[0] * eb0, mc = s[0] * ec0;
 #pragma unroll
-        for (int d = 1; d < 15; ++d) {
+        for (int d = 1; d < 15; d += 2) {
           const int a = ra[dir_row(d)] + i + dir_di(d);
           mb = mb + s[d] * rb[a];
           mc = mc + s[d] * rc[a];
@@ -1730,7 +1651,7 @@ __global__ void __launch_bounds__(kEsThreads, 2) k3_estimate_stream(DevLevel3D l
       const double eb0 = rb[c0], ec0 = rc[c0];
       double mb = cf[0] * eb0, mc = cf[0] * ec0;
 #pragma unroll
-      for (int d = 1; d < 15; ++d) {
+      for (int d = 1; d < 15; d += 2) {
         const bool ok = (sig & dir_bad(d)) == 0;
         const int a = ok ? ra[dir_row(d)] + i + dir_di(d) : c0;
         const double tb = mb + cf[d] * rb[a], tc = mc + cf[d] * rc[a];
@@ -2096,18 +2017,14 @@ void launch3_cg0(const DevLevel3D& lv0, double* u, const double* b, double* scra
   init_constants();
   const size_t base = (6 * static_cast<size_t>(lv0.ng) + (lv0.ng + 31) / 32) * sizeof(double) + lv0.ng + 16;
   if (base > 200 * 1024) fail(KB_STRUCTURAL, "coarse mesh too large for the level-0 CG (more than ~4800 vertices)");
-  // compact program staged in shared memory when it fits (no per-iteration L2
-  // traffic for the operator), else the member-parallel operator when the
-  // member partials fit next to the vectors, else the plain one
-  const size_t compact_bytes =
-      lv0.cg_nrows > 0 ? 8 * static_cast<size_t>(lv0.cg_members4) + 32 * static_cast<size_t>(lv0.cg_nrows) +
-                             2 * static_cast<size_t>((lv0.cg_members4 + 1) & ~1) + 4 * static_cast<size_t>(lv0.ng + 1)
-                       : 0;
-  const int compact = compact_bytes > 0 && base + compact_bytes + 64 <= 220 * 1024 ? 1 : 0;
-  const int nmem4 = !compact && lv0.cg_members4 > 0 && base + lv0.cg_members4 * 8.0 <= 200 * 1024 ? lv0.cg_members4 : 0;
-  const size_t smem = base + (compact ? compact_bytes + 64 : static_cast<size_t>(nmem4) * 8);
+  if (!lv0.cg_rowptr) fail(KB_INTERNAL, "level-0 operator rows missing");
+  // the assembled rows staged in shared memory when they fit (no per-iteration L2 traffic)
+  const size_t rows_bytes = 8 * static_cast<size_t>(lv0.cg_nnz) + 4 * static_cast<size_t>(lv0.ng + 1) +
+                            2 * static_cast<size_t>((lv0.cg_nnz + 3) & ~3);
+  const int staged = base + rows_bytes + 64 <= 220 * 1024 ? 1 : 0;
+  const size_t smem = base + (staged ? rows_bytes + 64 : 0);
   ensure_dynamic_smem(k3_cg0, smem);
-  k3_cg0<<<1, 1024, smem, st>>>(lv0, u, b, prm, status, nmem4, compact);
+  k3_cg0<<<1, 1024, smem, st>>>(lv0, u, b, prm, status, staged);
   check3("k3_cg0");
 }
 
@@ -2116,7 +2033,7 @@ void launch3_estimate(const DevLevel3D& lv, const double* uL, const double* wb, 
   init_constants();
   const bool cells = estimate_cells();
   if (!cells && apply_streams(lv)) {
-    const size_t smem = (240 + 6 * static_cast<size_t>(plane_stride(lv.n))) * 8;
+    const size_t smem = (240 + 4 * static_cast<size_t>(plane_stride(lv.n))) * 8;
     ensure_dynamic_smem(k3_estimate_stream, smem);
     k3_estimate_stream<<<lv.M, kEsThreads, smem, st>>>(lv, uL, wb, wc, sums);
     check3("k3_estimate_stream");

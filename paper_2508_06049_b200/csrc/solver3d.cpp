@@ -211,42 +211,33 @@ std::unique_ptr<DeviceHierarchy3D> DeviceHierarchy3D::create(const Mesh3D& mesh,
     dl.psK = d->arena.upload(lv.psK);
     dl.psM = d->arena.upload(lv.psM);
     if (l == 0) {
-      dl.cg_gmem = d->arena.upload(cg_gmem);
-      dl.cg_mterm = d->arena.upload(cg_mterm);
-      dl.cg_coef = d->arena.upload(cg_coef);
-      dl.cg_vid = d->arena.upload(cg_vid);
-      bool four = true;
-      for (size_t q = 0; q + 1 < cg_mterm.size(); ++q) four = four && cg_mterm[q + 1] - cg_mterm[q] == 4;
-      dl.cg_members4 = four ? static_cast<int>(cg_mterm.size()) - 1 : 0;
-      // compact program: distinct coefficient rows + 16-bit member records
-      if (four) {
-        std::map<std::array<std::uint64_t, 4>, int> rows;
-        std::vector<double> row_vals;
-        std::vector<unsigned short> mrow, mvid;
-        bool ok = true;
-        for (int q = 0; q < dl.cg_members4 && ok; ++q) {
-          std::array<std::uint64_t, 4> key{};
-          std::memcpy(key.data(), &cg_coef[4 * static_cast<size_t>(q)], 32);
-          auto it = rows.find(key);
-          if (it == rows.end()) {
-            it = rows.emplace(key, static_cast<int>(rows.size())).first;
-            row_vals.insert(row_vals.end(), &cg_coef[4 * static_cast<size_t>(q)], &cg_coef[4 * static_cast<size_t>(q)] + 4);
+      // assembled level-0 operator: row g adds the members' partial stencils in
+      // slot order (terms centre first), coefficients of one column added in
+      // that order, columns in first-appearance order (oracle apply0)
+      std::vector<int> rowptr(1, 0);
+      std::vector<unsigned short> col;
+      std::vector<double> val;
+      for (size_t g = 0; g + 1 < cg_gmem.size(); ++g) {
+        const size_t start = col.size();
+        for (int q = cg_gmem[g]; q < cg_gmem[g + 1]; ++q)
+          for (int t = cg_mterm[q]; t < cg_mterm[q + 1]; ++t) {
+            const int v = cg_vid[t];
+            if (v < 0 || v >= 65536) fail(KB_STRUCTURAL, "coarse mesh too large for the level-0 CG (vertex id >= 65536)");
+            size_t pos = start;
+            while (pos < col.size() && col[pos] != v) ++pos;
+            if (pos == col.size()) {
+              col.push_back(static_cast<unsigned short>(v));
+              val.push_back(cg_coef[t]);
+            } else {
+              val[pos] = val[pos] + cg_coef[t];
+            }
           }
-          ok = it->second < 4096;
-          mrow.push_back(static_cast<unsigned short>(it->second));
-          for (int t = 0; t < 4; ++t) {
-            const int v = cg_vid[4 * static_cast<size_t>(q) + t];
-            ok = ok && v >= 0 && v < 65536;
-            mvid.push_back(static_cast<unsigned short>(v));
-          }
-        }
-        if (ok) {
-          dl.cg_rows = d->arena.upload(row_vals);
-          dl.cg_mrow = d->arena.upload(mrow);
-          dl.cg_mvid = d->arena.upload(mvid);
-          dl.cg_nrows = static_cast<int>(rows.size());
-        }
+        rowptr.push_back(static_cast<int>(col.size()));
       }
+      dl.cg_rowptr = d->arena.upload(rowptr);
+      dl.cg_col = d->arena.upload(col);
+      dl.cg_val = d->arena.upload(val);
+      dl.cg_nnz = static_cast<int>(col.size());
     }
     d->lev.push_back(dl);
   }
