@@ -920,7 +920,7 @@ __global__ void __launch_bounds__(NT, MINB) k3_gs_sweeps(DevLevel3D lv, double* 
 // read once and u written once per sweep.  The nodes of a step come from the
 // level's step lists (entry = in-plane index | j << 16), one per thread.
 template <int NT, int US, int BS>
-__global__ void __launch_bounds__(NT) k3_gs_planes(DevLevel3D lv, double* u, const double* __restrict__ b) {
+__global__ void __launch_bounds__(NT, 1024 / NT) k3_gs_planes(DevLevel3D lv, double* u, const double* __restrict__ b) {
   // US u slots (plane k in slot k % US, US - 2 planes ahead), BS b slots (plane
   // k in slot (k - 1) % BS, BS - 1 planes ahead); one mbarrier per slot
   extern __shared__ __align__(128) unsigned long long gp_smem[];
@@ -969,10 +969,10 @@ __global__ void __launch_bounds__(NT) k3_gs_planes(DevLevel3D lv, double* u, con
     for (int k = 0; k <= US - 2; ++k) issue_u(k);
     for (int k = 1; k <= BS - 1; ++k) issue_b(k);
   }
-  if (tid == 32)
+  if (tid == 0) {
     for (int k = US - 1; k < US - 1 + PF; ++k) l2_prefetch(um, k);
-  if (tid == 64)
     for (int k = BS; k < BS + PF; ++k) l2_prefetch(bm, k);
+  }
   double s[15];
 #pragma unroll
   for (int d = 1; d < 15; ++d) s[d] = __ldg(lv.stK + 15 * m + d);
@@ -980,18 +980,31 @@ __global__ void __launch_bounds__(NT) k3_gs_planes(DevLevel3D lv, double* u, con
   const double inv_c = __ldg(lv.inv_c + m);
   for (int t = tid; t <= steps; t += NT) sp[t] = __ldg(lv.pat_ptr + t);
   __syncthreads();
-  // this thread's entries of the next three steps are loaded ahead (L2 latency)
-  auto entry = [&](int st) {
-    return st < steps && tid < sp[st + 1] - sp[st] ? __ldg(lv.pat_node + sp[st] + tid) : 0;
-  };
-  int e1 = entry(0), e2 = entry(1), e3 = entry(2);
+  // step starts in a rolling register window w0..w4 = sp[st .. st + 4]; this
+  // thread's entries of the next three steps are loaded ahead (L2 latency)
+  auto spc = [&](int t) { return sp[min(t, steps)]; };
+  int w0 = spc(0), w1 = spc(1), w2 = spc(2), w3 = spc(3), w4 = spc(4);
+  auto entry = [&](int lo, int hi) { return tid < hi - lo ? __ldg(lv.pat_node + lo + tid) : 0; };
+  int e1 = entry(w0, w1), e2 = entry(w1, w2), e3 = entry(w2, w3);
+  const int warp = tid >> 5;
   for (int k = 1; k <= n - 3; ++k) {
+    // The steps shrink with k: a warp beyond the plane's largest step has no
+    // node left in this or any later plane and leaves; the others meet at a
+    // named barrier sized for the warps that remain.
+    int need;
+    {
+      const int st = 4 * (k - 1);
+      const int big = max(max(w1 - w0, w2 - w1), max(w3 - w2, w4 - w3));
+      need = min(NT / 32, (big + 31) >> 5);
+      (void)st;
+    }
+    if (warp >= need) break;
     if (tid == 0) {
       issue_u(k + US - 2);  // its slot held plane k - 2
       issue_b(k + BS - 1);  // its slot held plane k - 1
+      l2_prefetch(um, k + US - 2 + PF);
+      l2_prefetch(bm, k + BS - 1 + PF);
     }
-    if (tid == 32) l2_prefetch(um, k + US - 2 + PF);
-    if (tid == 64) l2_prefetch(bm, k + BS - 1 + PF);
     if (k == 1) {
       p3_mbar_wait(bar_s, 0);
       p3_mbar_wait(bar_s + 8u, 0);
@@ -1006,9 +1019,10 @@ __global__ void __launch_bounds__(NT) k3_gs_planes(DevLevel3D lv, double* u, con
         ring_b + ((k - 1) % BS) * stride + static_cast<int>((reinterpret_cast<size_t>(bm + gp) >> 3) & 1);
 #pragma unroll 1
     for (int q = 0; q < 4; ++q) {
-      const int st = 4 * (k - 1) + q, p0 = sp[st], cnt = sp[st + 1] - p0;
+      const int st = 4 * (k - 1) + q, p0 = w0, cnt = w1 - w0;
       int ent = e1;
-      e1 = e2, e2 = e3, e3 = entry(st + 3);
+      e1 = e2, e2 = e3, e3 = entry(w3, w4);
+      w0 = w1, w1 = w2, w2 = w3, w3 = w4, w4 = spc(st + 5);
       for (int e = tid; e < cnt; e += NT) {
         if (e != tid) ent = __ldg(lv.pat_node + p0 + e);
         const int c = ent & 0xffff, j = ent >> 16;
@@ -1018,11 +1032,10 @@ __global__ void __launch_bounds__(NT) k3_gs_planes(DevLevel3D lv, double* u, con
         ring_u[b0 + c] = v;
         um[gp + c] = v;
       }
-      __syncthreads();
+      asm volatile("bar.sync 1, %0;" ::"r"(32 * need) : "memory");
     }
   }
 }
-
 // The same order straight on global memory (n > 64): one CTA per macro, rows
 // to warps, block barriers between the classes.
 __global__ void __launch_bounds__(kT) k3_gs_planes_global(DevLevel3D lv, double* u, const double* __restrict__ b) {
