@@ -361,9 +361,9 @@ __global__ void __launch_bounds__(kT) k3_apply_groups_warp(DevLevel3D lv, int ma
 //                   write to every copy.
 // Same operations and orders as k3_apply / partial_row (bit-identical).
 constexpr int kAsSlots = 4;
-constexpr int kAsThreads = 256;
 constexpr int kAsPF = 6;  // L2 prefetch distance (planes) ahead of the TMA stream
 
+template <int kAsThreads>
 __global__ void __launch_bounds__(kAsThreads) k3_apply_stream(DevLevel3D lv, int mass, const double* __restrict__ x,
                                                               double* y, const double* __restrict__ b, int mode) {
   extern __shared__ __align__(128) unsigned long long as_smem[];
@@ -1870,8 +1870,22 @@ void launch3_apply(const DevLevel3D& lv, bool mass, const double* x, double* y, 
   init_constants();
   if (apply_streams(lv)) {
     const size_t smem = (kAsSlots + 240 + kAsSlots * static_cast<size_t>(plane_stride(lv.n))) * 8;
-    ensure_dynamic_smem(k3_apply_stream, smem);
-    k3_apply_stream<<<lv.M, kAsThreads, smem, st>>>(lv, mass ? 1 : 0, x, y, b, mode);
+    // threads per macro by plane size: the per-plane barrier and TMA wait cost
+    // less with fewer warps and more CTAs per SM on the small planes (residual on
+    // 3072 macros: n = 32 0.51 -> 0.36 ms with 128 threads, n = 16 0.22 -> 0.13 ms
+    // and n = 8 0.12 -> 0.08 ms with 64; n = 64 keeps 256)
+    static const int nt_exp = getenv("KB_AS_NT") ? atoi(getenv("KB_AS_NT")) : 0;
+    const int nt = nt_exp ? nt_exp : (lv.n >= 64 ? 256 : lv.n >= 32 ? 128 : 64);
+    if (nt == 64) {
+      ensure_dynamic_smem(k3_apply_stream<64>, smem);
+      k3_apply_stream<64><<<lv.M, 64, smem, st>>>(lv, mass ? 1 : 0, x, y, b, mode);
+    } else if (nt == 128) {
+      ensure_dynamic_smem(k3_apply_stream<128>, smem);
+      k3_apply_stream<128><<<lv.M, 128, smem, st>>>(lv, mass ? 1 : 0, x, y, b, mode);
+    } else {
+      ensure_dynamic_smem(k3_apply_stream<256>, smem);
+      k3_apply_stream<256><<<lv.M, 256, smem, st>>>(lv, mass ? 1 : 0, x, y, b, mode);
+    }
     check3("k3_apply_stream");
     if (lv.ng > 0) {
       k3_apply_groups<<<blocks_for(lv.ng), kT, 0, st>>>(lv, y, b, mode);
