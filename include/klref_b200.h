@@ -116,6 +116,10 @@ const char* klref_last_error(void);
 double klref_last_error_residual(void); /* SolverError::last_residual */
 int klref_last_error_level(void);       /* ResourceError::level */
 int klref_abi_version(void);
+/* Creates the CUDA context of the current device (no reference counterpart:
+ * a cold process pays it on the first hierarchy build otherwise); KLREF_ERR_CUDA
+ * without a device. */
+int klref_device_init(void);
 
 /* ---- coarse mesh ------------------------------------------------------ */
 /* Conforming macro mesh in slot order (MacroMesh::create,

@@ -127,6 +127,9 @@ const char* klref_last_error(void) { return g_msg.c_str(); }
 double klref_last_error_residual(void) { return g_residual; }
 int klref_last_error_level(void) { return g_level; }
 int klref_abi_version(void) { return 1; }
+int klref_device_init(void) {
+  return guarded([&] { KB_CUDA_CHECK(cudaFree(nullptr)); });
+}
 
 int klref_mesh_create(int dim, int num_vertices, const double* coords, int num_elements, const int* corners,
                       klref_mesh* out) {

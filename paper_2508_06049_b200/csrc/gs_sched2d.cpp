@@ -128,7 +128,7 @@ void build_one(const Hierarchy2D& h, Level2D& lv, int sweeps, GsSched2D& out) {
 }  // namespace
 
 void Hierarchy2D::build_gs_schedules() {
-  for (int l = 1; l <= L; ++l) {
+  parallel_levels(1, L, [&](int l) {
     Level2D& lv = levels[l];
     const int n = lv.n, S = lv.S;
     const int NG = static_cast<int>(lv.grp_ptr.size()) - 1;
@@ -137,7 +137,7 @@ void Hierarchy2D::build_gs_schedules() {
     const std::size_t interior = copies - static_cast<std::size_t>(M) * 3 * n;
     const std::size_t nu = NG + interior;
     const std::size_t table = 16 * (nu + 1) + 8 * 26 * static_cast<std::size_t>(M) + 16 * NG;
-    if (table > kSchedTableBytes) continue;
+    if (table > kSchedTableBytes) return;
     lv.sc_nu = static_cast<int>(nu);
     lv.sc_copy_cell.assign(copies, -1);
     lv.sc_cell_copy.assign(nu, -1);
@@ -179,7 +179,7 @@ void Hierarchy2D::build_gs_schedules() {
     if (getenv("KB_SCHED_DEBUG"))
       std::fprintf(stderr, "gs schedule M=%d l=%d nu=%zu: 1 sweep %d levels (width %d, block %d words), 2 sweeps %d levels\n",
                    M, l, nu, lv.sched[0].levels, lv.sched[0].max_width, lv.sched[0].max_block_words, lv.sched[1].levels);
-  }
+  });
 }
 
 }  // namespace kb

@@ -2,6 +2,9 @@
 #include "hier2d.hpp"
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -276,6 +279,7 @@ void Hierarchy2D::node_coordinates(int slot, int l, int i, int j, double& x, dou
 }
 
 Hierarchy2D Hierarchy2D::build(const Mesh2D& mesh, int max_level) {
+  const auto tb = std::chrono::steady_clock::now();
   if (max_level < 0) fail(KB_STRUCTURAL, "hierarchy level must be nonnegative");
   if (max_level > 9) fail(KB_STRUCTURAL, "2-d wavefront smoother supports levels <= 9");
   Hierarchy2D h;
@@ -397,9 +401,10 @@ Hierarchy2D Hierarchy2D::build(const Mesh2D& mesh, int max_level) {
     throw e;
   }
 
-  // Derived tables.
-  for (int l = 0; l <= max_level; ++l) {
+  // Derived tables: the levels are independent, one host thread each.
+  auto derive = [&](int l) {
     Level2D& lvl = h.levels[l];
+    const auto tl0 = std::chrono::steady_clock::now();
     const int n = lvl.n, S = lvl.S;
     lvl.node_gid.assign(static_cast<std::size_t>(M) * S, -1);
     lvl.node_flags.assign(static_cast<std::size_t>(M) * S, 4);  // interior: owner
@@ -467,7 +472,7 @@ Hierarchy2D Hierarchy2D::build(const Mesh2D& mesh, int max_level) {
         for (int t = 1; t <= n - 1; ++t) lvl.dot_order.push_back(static_cast<int>(base + edge_lattice_index(n, le, t)));
       }
     }
-    if (l == 0) continue;
+    if (l == 0) return;
 
     // Wavefront Gauss-Seidel tables.
     lvl.bnode.assign(static_cast<std::size_t>(M) * 3 * n, BNode{});
@@ -573,10 +578,25 @@ Hierarchy2D Hierarchy2D::build(const Mesh2D& mesh, int max_level) {
       lvl.ghost_ptr.push_back(static_cast<int>(lvl.ghost_off.size()));
       lvl.max_ghosts = std::max(lvl.max_ghosts, static_cast<int>(ghosts.size()));
     }
+    const auto tp0 = std::chrono::steady_clock::now();
     build_programs(lvl, M);
-  }
+    if (getenv("KB_BUILD_TRACE"))
+      fprintf(stderr, "  level %d: tables %.1f ms, programs %.1f ms (prog %zu KB, rec %zu, bnode %zu)\n", l,
+              1e3 * std::chrono::duration<double>(tp0 - tl0).count(),
+              1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - tp0).count(),
+              lvl.prog.size() * sizeof(lvl.prog[0]) / 1024, lvl.rec.size(), lvl.bnode.size());
+  };
+  parallel_levels(0, max_level, derive);
+  const bool trace = getenv("KB_BUILD_TRACE") != nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
   h.build_gs_schedules();
+  const auto t1 = std::chrono::steady_clock::now();
   h.build_pipe_tables();
+  const auto t2 = std::chrono::steady_clock::now();
+  if (trace)
+    fprintf(stderr, "hierarchy build: tables+programs %.1f ms, gs schedules %.1f ms, pipe tables %.1f ms\n",
+            1e3 * std::chrono::duration<double>(t0 - tb).count(), 1e3 * std::chrono::duration<double>(t1 - t0).count(),
+            1e3 * std::chrono::duration<double>(t2 - t1).count());
   return h;
 }
 

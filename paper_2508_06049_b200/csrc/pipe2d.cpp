@@ -8,7 +8,6 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
-#include <map>
 
 #include "hier2d.hpp"
 
@@ -38,9 +37,33 @@ void build_level(const Hierarchy2D& h, Level2D& lv) {
   struct Reader {
     int m, th;
   };
-  std::vector<long long> w_serial(copies, 0);
-  std::vector<int> w_m(copies, -1), w_t(copies, 0);
-  std::vector<std::vector<Reader>> readers(copies);
+  // the per-location state is kept for the tracked locations only (a few per
+  // cent of the copies): loc_id maps a copy offset to its compact index
+  std::vector<int> loc_id(copies, -1);
+  int ntracked = 0;
+  for (std::size_t L = 0; L < copies; ++L)
+    if (tracked[L]) loc_id[L] = ntracked++;
+  std::vector<long long> w_serial_c(ntracked, 0);
+  std::vector<int> w_m_c(ntracked, -1), w_t_c(ntracked, 0);
+  std::vector<std::vector<Reader>> readers_c(ntracked);
+  struct LocView {  // indexable by copy offset (tracked locations only)
+    std::vector<int>& id;
+    std::vector<long long>& serial;
+    long long& operator[](std::size_t L) { return serial[id[L]]; }
+  };
+  LocView w_serial{loc_id, w_serial_c};
+  struct IntView {
+    std::vector<int>& id;
+    std::vector<int>& v;
+    int& operator[](std::size_t L) { return v[id[L]]; }
+  };
+  IntView w_m{loc_id, w_m_c}, w_t{loc_id, w_t_c};
+  struct ReadersView {
+    std::vector<int>& id;
+    std::vector<std::vector<Reader>>& v;
+    std::vector<Reader>& operator[](std::size_t L) { return v[id[L]]; }
+  };
+  ReadersView readers{loc_id, readers_c};
   // initial loads: every macro reads its lattice and its ghosts before its step
   // 0; semantically at (sweep 0, m), so only later writers wait for them
   auto initial_loads = [&](int m) {
@@ -62,9 +85,12 @@ void build_level(const Hierarchy2D& h, Level2D& lv) {
   for (int m = 0; m < M; ++m) know_g[m].assign(lv.ghost_ptr[m + 1] - lv.ghost_ptr[m], 0);
   long long serial = 0;
 
+  // per step: requirements (macro, progress) and fetches (destination, source),
+  // fixed capacity kPipeLanes each (more is not supported by the kernel: the
+  // macro-DAG smoother runs then); counts keep counting past the capacity
   struct StepRec {
-    std::map<int, int> req;  // macro -> progress
-    std::vector<std::pair<int, int>> fetch;
+    int nreq = 0, nfetch = 0;
+    std::pair<int, int> req[kPipeLanes], fetch[kPipeLanes];
   };
   std::vector<StepRec> recs(static_cast<std::size_t>(M) * 2 * T);
   auto bpos_of = [&](int i, int j) { return bpos(n, i, j); };
@@ -81,13 +107,20 @@ void build_level(const Hierarchy2D& h, Level2D& lv) {
         const int tau = s * T + t;
         auto need = [&](int m2, int p) {
           if (m2 == m) return;
-          auto it = R.req.find(m2);
-          if (it == R.req.end() || it->second < p) R.req[m2] = p;
+          const int have = std::min(R.nreq, kPipeLanes);
+          for (int e = 0; e < have; ++e)
+            if (R.req[e].first == m2) {
+              if (R.req[e].second < p) R.req[e].second = p;
+              return;
+            }
+          if (R.nreq < kPipeLanes) R.req[R.nreq] = {m2, p};
+          ++R.nreq;
         };
         auto first_use = [&](std::size_t L, int dst, long long& know) {
           if (w_serial[L] == know) return;
           if (w_m[L] >= 0) need(w_m[L], w_t[L] + 2);
-          R.fetch.push_back({dst, static_cast<int>(L)});
+          if (R.nfetch < kPipeLanes) R.fetch[R.nfetch] = {dst, static_cast<int>(L)};
+          ++R.nfetch;
           readers[L].push_back({m, tau + 2});
           know = w_serial[L];
         };
@@ -114,12 +147,24 @@ void build_level(const Hierarchy2D& h, Level2D& lv) {
         };
         // the relaxations of wavefront step t: reads first (no node reads a
         // node of its own step), then writes
-        std::vector<std::pair<int, int>> nodes;
-        for (int j = 0; j <= n; ++j) {
+        // only lattice-boundary nodes and their inner neighbours (i, j or
+        // n - i - j equal to 1) read or write tracked locations: the rows
+        // j = 0, 1, the columns i = 0, 1 and the diagonals i + j = n, n - 1 of
+        // the wavefront i + 2 j = t, in ascending j like the full wavefront
+        int cand[6] = {0, 1, t / 2, (t - 1) / 2, t - n, t - n + 1}, nc = 0;
+        if (t & 1) cand[2] = -1; else cand[3] = -1;
+        std::sort(cand, cand + 6);
+        std::pair<int, int> nodes[6];
+        for (int c = 0; c < 6; ++c) {
+          const int j = cand[c];
+          if (j < 0 || j > n || (c > 0 && cand[c - 1] == j)) continue;
           const int i = t - 2 * j;
-          if (i >= 0 && i <= n - j) nodes.push_back({i, j});
+          if (i < 0 || i > n - j) continue;
+          if (!(is_bnd(i, j) || i == 1 || j == 1 || i + j == n - 1)) continue;
+          nodes[nc++] = {i, j};
         }
-        for (auto [i, j] : nodes) {
+        for (int c = 0; c < nc; ++c) {
+          const int i = nodes[c].first, j = nodes[c].second;
           if (!is_bnd(i, j)) {
             for (int d = 0; d < 6; ++d) read_lattice(i + kDij2[d][0], j + kDij2[d][1]);
             continue;
@@ -140,7 +185,8 @@ void build_level(const Hierarchy2D& h, Level2D& lv) {
             }
           }
         }
-        for (auto [i, j] : nodes) {
+        for (int c = 0; c < nc; ++c) {
+          const int i = nodes[c].first, j = nodes[c].second;
           if (is_bnd(i, j)) {
             const int bp = bpos_of(i, j);
             const int g = lv.node_gid[static_cast<std::size_t>(m) * S + lattice_index(n, i, j)];
@@ -156,9 +202,10 @@ void build_level(const Hierarchy2D& h, Level2D& lv) {
     }
   PipeTables2D& P = lv.pipe;
   P = PipeTables2D{};
-  for (const StepRec& R : recs) {
-    P.maxreq = std::max(P.maxreq, static_cast<int>(R.req.size()));
-    P.maxfetch = std::max(P.maxfetch, static_cast<int>(R.fetch.size()));
+  for (StepRec& R : recs) {
+    P.maxreq = std::max(P.maxreq, R.nreq);
+    P.maxfetch = std::max(P.maxfetch, R.nfetch);
+    std::sort(R.req, R.req + std::min(R.nreq, kPipeLanes));
   }
   if (P.maxreq > kPipeLanes || P.maxfetch > kPipeLanes) {  // not supported: the macro-DAG smoother runs
     if (getenv("KB_PIPE_DEBUG"))
@@ -171,13 +218,11 @@ void build_level(const Hierarchy2D& h, Level2D& lv) {
   for (std::size_t r = 0; r < recs.size(); ++r) {
     std::int32_t* w = &P.rec[r * P.rec_words];
     for (int k = 0; k < kPipeLanes; ++k) w[4 * k] = -1, w[4 * k + 2] = -1;
-    int k = 0;
-    for (const auto& [m2, p] : recs[r].req) {
-      w[4 * k] = m2;
-      w[4 * k + 1] = p;
-      ++k;
+    for (int k = 0; k < recs[r].nreq; ++k) {
+      w[4 * k] = recs[r].req[k].first;
+      w[4 * k + 1] = recs[r].req[k].second;
     }
-    for (std::size_t f = 0; f < recs[r].fetch.size(); ++f) {
+    for (int f = 0; f < recs[r].nfetch; ++f) {
       w[4 * f + 2] = recs[r].fetch[f].second;
       w[4 * f + 3] = recs[r].fetch[f].first;
     }
@@ -185,7 +230,7 @@ void build_level(const Hierarchy2D& h, Level2D& lv) {
   P.ok = true;
   if (getenv("KB_PIPE_DEBUG")) {
     long long nr = 0, nf = 0;
-    for (const StepRec& R : recs) nr += R.req.size(), nf += R.fetch.size();
+    for (const StepRec& R : recs) nr += R.nreq, nf += R.nfetch;
     std::fprintf(stderr, "pipe tables M=%d n=%d: maxreq %d maxfetch %d, total req %lld fetch %lld (%.2f / %.2f per step)\n", M, n,
                  P.maxreq, P.maxfetch, nr, nf, double(nr) / recs.size(), double(nf) / recs.size());
     // critical path of the two sweeps under a unit model: a step costs c, a
@@ -200,7 +245,9 @@ void build_level(const Hierarchy2D& h, Level2D& lv) {
             const std::size_t e = static_cast<std::size_t>(m) * 2 * T + tau;
             double start = tau > 0 ? F[e - 1] : 0.0;
             int hp = tau > 0 ? hops[e - 1] : 0;
-            for (const auto& [m2, p] : recs[(static_cast<std::size_t>(m) * 2 + sw) * T + t].req) {
+            const StepRec& RR = recs[(static_cast<std::size_t>(m) * 2 + sw) * T + t];
+            for (int qq = 0; qq < RR.nreq; ++qq) {
+              const int m2 = RR.req[qq].first, p = RR.req[qq].second;
               const std::size_t e2 = static_cast<std::size_t>(m2) * 2 * T + (p - 2);
               if (F[e2] + h > start) start = F[e2] + h, hp = hops[e2] + 1;
             }
@@ -217,11 +264,11 @@ void build_level(const Hierarchy2D& h, Level2D& lv) {
 }  // namespace
 
 void Hierarchy2D::build_pipe_tables() {
-  for (int l = 1; l <= L; ++l) {
+  parallel_levels(1, L, [&](int l) {
     Level2D& lv = levels[l];
-    if (lv.n < min_pipe_n() || lv.sc_nu > 0 || lv.n > 128) continue;
+    if (lv.n < min_pipe_n() || lv.sc_nu > 0 || lv.n > 128) return;
     build_level(*this, lv);
-  }
+  });
 }
 
 }  // namespace kb

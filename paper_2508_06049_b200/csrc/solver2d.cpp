@@ -2,20 +2,68 @@
 #include "solver2d.hpp"
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 
 namespace kb {
 
 // ------------------------------------------------------------------ arena
+// The arenas come from the device's default stream-ordered memory pool with
+// the release threshold lifted, so an AMR loop that rebuilds hierarchy and
+// solver per step reuses the freed blocks instead of paying cudaMalloc /
+// cudaFree (2 - 40 ms per 100 MB arena, measured) every time.  The allocation
+// is made usable from every stream by synchronising the allocating (legacy
+// default) stream; the free is preceded by a device synchronise, like cudaFree.
+namespace {
+bool arena_pool_ready() {
+  static const bool ok = [] {
+    const char* e = getenv("KB_ARENA_POOL");
+    if (e && e[0] == '0') return false;
+    int dev = 0, supported = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return false;
+    if (cudaDeviceGetAttribute(&supported, cudaDevAttrMemoryPoolsSupported, dev) != cudaSuccess || !supported) {
+      cudaGetLastError();
+      return false;
+    }
+    cudaMemPool_t pool = nullptr;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    unsigned long long keep = ~0ull;
+    if (cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return true;
+  }();
+  return ok;
+}
+}  // namespace
+
 DeviceArena::~DeviceArena() {
-  if (base_) cudaFree(base_);
+  if (!base_) return;
+  if (pooled_) {
+    cudaDeviceSynchronize();
+    cudaFreeAsync(base_, nullptr);
+  } else {
+    cudaFree(base_);
+  }
 }
 
 void DeviceArena::reserve(size_t bytes) {
   if (base_) fail(KB_INTERNAL, "arena already reserved");
   cap_ = bytes + 256;
-  const cudaError_t e = cudaMalloc(&base_, cap_);
+  cudaError_t e;
+  if (cap_ <= (size_t(1) << 30) && arena_pool_ready()) {  // large arenas: plain cudaMalloc (nothing retained)
+    e = cudaMallocAsync(reinterpret_cast<void**>(&base_), cap_, nullptr);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(nullptr);
+    pooled_ = e == cudaSuccess;
+  } else {
+    e = cudaMalloc(&base_, cap_);
+  }
   if (e != cudaSuccess) {
     base_ = nullptr;
     Error err(KB_RESOURCE, std::string("device allocation failed: ") + cudaGetErrorString(e));
@@ -43,7 +91,9 @@ size_t vbytes(const std::vector<T>& v) {
 // ------------------------------------------------------------------ hierarchy upload
 std::unique_ptr<DeviceHierarchy2D> DeviceHierarchy2D::create(const Mesh2D& mesh, int max_level) {
   auto d = std::make_unique<DeviceHierarchy2D>();
+  const auto tc0 = std::chrono::steady_clock::now();
   d->host = Hierarchy2D::build(mesh, max_level);
+  const auto tc1 = std::chrono::steady_clock::now();
   const Hierarchy2D& h = d->host;
   const int M = h.M;
   std::vector<std::vector<int>> mem_off(h.L + 1), mem_ij(h.L + 1);
@@ -116,7 +166,9 @@ std::unique_ptr<DeviceHierarchy2D> DeviceHierarchy2D::create(const Mesh2D& mesh,
     }
     bytes += vbytes(cg_mem_ptr) + vbytes(cg_mem_dof) + vbytes(cg_copy_ptr) + vbytes(cg_copy) + vbytes(cg_mem_coef);
   }
+  const auto tc2 = std::chrono::steady_clock::now();
   d->arena.reserve(bytes + 4096);
+  const auto tc3 = std::chrono::steady_clock::now();
   d->dh.M = M;
   d->dh.L = h.L;
   d->dh.nb_lo_ptr = d->arena.upload(h.nb_lo_ptr);
@@ -191,6 +243,11 @@ std::unique_ptr<DeviceHierarchy2D> DeviceHierarchy2D::create(const Mesh2D& mesh,
     }
     d->lev.push_back(dl);
   }
+  if (getenv("KB_BUILD_TRACE")) {
+    auto ms = [](auto a, auto b) { return 1e3 * std::chrono::duration<double>(b - a).count(); };
+    fprintf(stderr, "device hierarchy: host build %.1f ms, host tables %.1f ms, arena %.1f ms (%zu MB), upload %.1f ms\n",
+            ms(tc0, tc1), ms(tc1, tc2), ms(tc2, tc3), bytes >> 20, ms(tc3, std::chrono::steady_clock::now()));
+  }
   return d;
 }
 
@@ -261,7 +318,9 @@ Solver2D::Solver2D(std::shared_ptr<DeviceHierarchy2D> h, Problem2D p, SolverConf
   bytes += round256(3 * lsize(0) * 8) + round256(2 * M * 8) + round256(lsize(L_) * 8) +
            round256(lsize(std::max(L_ - 1, 0)) * 8) + round256(64 * 8) + round256(8) +
            round256(sizeof(DevStatus)) + round256((M + 3) / 4 * 16);
+  const auto ts0 = std::chrono::steady_clock::now();
   arena_.reserve(bytes);
+  const auto ts1 = std::chrono::steady_clock::now();
   u_.assign(L_ + 1, nullptr);
   b_.assign(L_ + 1, nullptr);
   w_.assign(L_ + 1, nullptr);
@@ -303,9 +362,25 @@ Solver2D::Solver2D(std::shared_ptr<DeviceHierarchy2D> h, Problem2D p, SolverConf
     if (src_kind_ == SRC_TABLE) ftab_count_[l] = fsize(l);
     stage_count_ += gbnd_count_[l] + ftab_count_[l];
   }
-  KB_CUDA_CHECK(cudaMallocHost(&stage_, stage_count_ * sizeof(double)));
+  const auto ts2 = std::chrono::steady_clock::now();
+  // small staging buffers are pinned; a large source table (tens of MB) goes
+  // through pageable memory (pinning it costs more than the staged copy saves)
+  stage_pinned_ = stage_count_ * sizeof(double) <= (8u << 20);
+  if (stage_pinned_) {
+    KB_CUDA_CHECK(cudaMallocHost(&stage_, stage_count_ * sizeof(double)));
+  } else {
+    stage_ = static_cast<double*>(std::malloc(stage_count_ * sizeof(double)));
+    if (!stage_) fail(KB_RESOURCE, "host allocation of the problem tables failed");
+  }
+  const auto ts3 = std::chrono::steady_clock::now();
   load_problem(prob_);
   KB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+  if (getenv("KB_BUILD_TRACE")) {
+    auto ms = [](auto a, auto b) { return 1e3 * std::chrono::duration<double>(b - a).count(); };
+    fprintf(stderr, "solver: arena %.1f ms (%zu MB), misc %.1f ms, pinned stage %.1f ms (%zu MB), tabulate + copy %.1f ms\n",
+            ms(ts0, ts1), bytes >> 20, ms(ts1, ts2), ms(ts2, ts3), (stage_count_ * 8) >> 20,
+            ms(ts3, std::chrono::steady_clock::now()));
+  }
   KB_CUDA_CHECK(cudaMemset(status_, 0, sizeof(DevStatus)));
 }
 
@@ -315,7 +390,10 @@ Solver2D::~Solver2D() {
   if (own_stream_) cudaStreamDestroy(own_stream_);
   if (status_host_) cudaFreeHost(status_host_);
   if (sums_host_) cudaFreeHost(sums_host_);
-  if (stage_) cudaFreeHost(stage_);
+  if (stage_) {
+    if (stage_pinned_) cudaFreeHost(stage_);
+    else std::free(stage_);
+  }
 }
 
 void Solver2D::tabulate(const Problem2D& p) {
@@ -330,7 +408,9 @@ void Solver2D::tabulate(const Problem2D& p) {
     const int n = lv.n;
     double* g = dst;
     std::fill(g, g + gbnd_count_[l], 0.0);
-    for (int s = 0; s < M; ++s) {
+    // the problem's callbacks are evaluated macro-parallel on host threads (pure
+    // functions of (x, y) like the reference's problems; KB_HOST_THREADS=0: in order)
+    parallel_for(M, [&](int s) {
       auto visit = [&](int i, int j) {
         if (!hh.on_domain_boundary(s, l, i, j)) return;
         const int gid = hh.boundary_group(s, l, i, j);
@@ -342,7 +422,7 @@ void Solver2D::tabulate(const Problem2D& p) {
       for (int i = 0; i <= n; ++i) visit(i, 0);
       for (int j = 1; j <= n; ++j) visit(0, j);
       for (int j = 1; j <= n - 1; ++j) visit(n - j, j);
-    }
+    });
     dst += gbnd_count_[l];
     if (ftab_count_[l]) {
       // f at the cell edge midpoints through the RHS map (proj/src/fem.cpp:183-194)
@@ -350,7 +430,7 @@ void Solver2D::tabulate(const Problem2D& p) {
       const int SF = lattice_size(n2);
       double* f = dst;
       std::fill(f, f + ftab_count_[l], 0.0);
-      for (int s = 0; s < M; ++s) {
+      parallel_for(M, [&](int s) {
         const auto& v = hh.mesh.tri[s];
         const double c0x = hh.mesh.x[v[0]], c0y = hh.mesh.y[v[0]];
         const double ux = (hh.mesh.x[v[1]] - c0x) / n, uy = (hh.mesh.y[v[1]] - c0y) / n;
@@ -362,7 +442,7 @@ void Solver2D::tabulate(const Problem2D& p) {
             f[static_cast<size_t>(s) * SF + lattice_index(n2, I, J)] =
                 p.source(c0x + hi * ux + hj * wx, c0y + hi * uy + hj * wy);
           }
-      }
+      });
       dst += ftab_count_[l];
     }
   }

@@ -40,6 +40,7 @@ class DeviceArena {
  private:
   char* base_ = nullptr;
   size_t cap_ = 0, used_ = 0;
+  bool pooled_ = false;  // from the stream-ordered pool (cudaMallocAsync)
 };
 
 struct DeviceHierarchy2D {
@@ -180,6 +181,7 @@ class Solver2D {
   cudaStream_t own_stream_ = nullptr;
   // pinned staging of the problem tables (Dirichlet g per level, f table per level)
   double* stage_ = nullptr;
+  bool stage_pinned_ = true;
   std::size_t stage_count_ = 0;
   std::vector<std::size_t> gbnd_count_, ftab_count_;
   // profiling probes

@@ -110,6 +110,7 @@ SIGNATURES = {
     "klref_last_error": (C.c_char_p, []),
     "klref_last_error_residual": (_D, []),
     "klref_last_error_level": (_I, []),
+    "klref_device_init": (_I, []),
     "klref_abi_version": (_I, []),
     "klref_mesh_create": (_I, [_I, _I, _PD, _I, _PI, _PP]),
     "klref_mesh_destroy": (None, [_P]),
