@@ -1,6 +1,11 @@
 // Shared host-side definitions of the klref-b200 library.
 #pragma once
 
+#include <algorithm>
+#include <cstdlib>
+#include <exception>
+#include <thread>
+#include <vector>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -33,6 +38,67 @@ struct Error : std::runtime_error {
 // (proj/include/klref/hhg.hpp:13-14).
 inline int lattice_index(int n, int i, int j) { return j * (n + 1) - (j * (j - 1)) / 2 + i; }
 inline int lattice_size(int n) { return (n + 1) * (n + 2) / 2; }
+
+// fn(l) for l = lo..hi, one host thread per level (the levels' tables are
+// independent); the first exception is rethrown on the caller's thread.
+// KB_HOST_THREADS=0 runs them in order on the caller's thread.
+template <typename F>
+inline void parallel_levels(int lo, int hi, F fn) {
+  static const bool serial = [] {
+    const char* e = getenv("KB_HOST_THREADS");
+    return e && e[0] == '0';
+  }();
+  if (serial || hi <= lo) {
+    for (int l = lo; l <= hi; ++l) fn(l);
+    return;
+  }
+  std::vector<std::thread> th;
+  std::vector<std::exception_ptr> err(static_cast<std::size_t>(hi - lo + 1));
+  for (int l = hi; l >= lo; --l)  // largest level first
+    th.emplace_back([&, l] {
+      try {
+        fn(l);
+      } catch (...) {
+        err[static_cast<std::size_t>(l - lo)] = std::current_exception();
+      }
+    });
+  for (auto& t : th) t.join();
+  for (auto& e : err)
+    if (e) std::rethrow_exception(e);
+}
+
+// fn(i) for i = 0..count-1 on up to 16 host threads (contiguous chunks); the
+// first exception is rethrown on the caller's thread.  KB_HOST_THREADS=0 runs
+// the loop on the caller's thread.
+template <typename F>
+inline void parallel_for(int count, F fn) {
+  static const int nthreads = [] {
+    const char* e = getenv("KB_HOST_THREADS");
+    if (e) return std::max(1, atoi(e));
+    const unsigned hw = std::thread::hardware_concurrency();
+    return static_cast<int>(std::min(16u, std::max(1u, hw)));
+  }();
+  const int T = std::min(nthreads, count);
+  if (T <= 1) {
+    for (int i = 0; i < count; ++i) fn(i);
+    return;
+  }
+  std::vector<std::thread> th;
+  std::vector<std::exception_ptr> err(static_cast<std::size_t>(T));
+  for (int t = 0; t < T; ++t)
+    th.emplace_back([&, t] {
+      try {
+        const int lo = static_cast<int>(static_cast<long long>(count) * t / T);
+        const int hi = static_cast<int>(static_cast<long long>(count) * (t + 1) / T);
+        for (int i = lo; i < hi; ++i) fn(i);
+      } catch (...) {
+        err[static_cast<std::size_t>(t)] = std::current_exception();
+      }
+    });
+  for (auto& t : th) t.join();
+  for (auto& e : err)
+    if (e) std::rethrow_exception(e);
+}
 
 }  // namespace kb
 

@@ -139,6 +139,34 @@ Hierarchy3D Hierarchy3D::build(const Mesh3D& mesh, int max_level) {
       ebnd.insert({f[1], f[2]});
     }
 
+  // per tet: ids / boundary flags of its 6 edges (by local vertex pair) and 4
+  // faces (by the local vertex they miss), so the per-node loops below do no
+  // map look-ups
+  std::vector<std::array<int, 16>> tet_edge(M);
+  std::vector<std::array<std::uint8_t, 16>> tet_edge_bnd(M);
+  std::vector<std::array<int, 4>> tet_face(M), tet_face_use(M);
+  for (int s = 0; s < M; ++s) {
+    const auto& t = mesh.tet[s];
+    tet_edge[s].fill(-1);
+    tet_edge_bnd[s].fill(0);
+    for (int a = 0; a < 4; ++a)
+      for (int b = 0; b < 4; ++b) {
+        if (a == b) continue;
+        const auto key = std::make_pair(std::min(t[a], t[b]), std::max(t[a], t[b]));
+        tet_edge[s][4 * a + b] = edge_id.at(key);
+        tet_edge_bnd[s][4 * a + b] = ebnd.count(key) > 0;
+      }
+    for (int o = 0; o < 4; ++o) {
+      std::array<int, 3> f{};
+      int q = 0;
+      for (int a = 0; a < 4; ++a)
+        if (a != o) f[q++] = t[a];
+      std::sort(f.begin(), f.end());
+      tet_face[s][o] = face_id.at(f);
+      tet_face_use[s][o] = face_use[tet_face[s][o]];
+    }
+  }
+
   // vertex colouring in Z_2^m: grid parity when the vertices sit on a uniform
   // axis-aligned grid (Kuhn meshes: 8 colours), else greedy by ascending id
   std::vector<int> vcol(NV, 0);
@@ -216,7 +244,8 @@ Hierarchy3D Hierarchy3D::build(const Mesh3D& mesh, int max_level) {
   h.colors = ncol;
 
   try {
-    for (int l = 0; l <= max_level; ++l) {
+    h.levels.resize(static_cast<std::size_t>(max_level) + 1);
+    parallel_levels(0, max_level, [&](int l) {  // the levels are independent: one host thread each
       Level3D lv;
       const int n = 1 << l;
       lv.n = n;
@@ -226,21 +255,21 @@ Hierarchy3D Hierarchy3D::build(const Mesh3D& mesh, int max_level) {
       const long long per_face = n >= 3 ? static_cast<long long>(n - 1) * (n - 2) / 2 : 0;
       const long long nG = NV + static_cast<long long>(nE) * (n - 1) + nF * per_face;
       // group layout: vertices, edges (t = weight on the higher-id end), faces (lattice of size n-3)
-      auto gid_of = [&](const int* vid, const int* w) -> long long {
-        int sup[4], sw[4], cnt = 0;
+      auto gid_of = [&](int s, const int* vid, const int* w) -> long long {
+        int loc[4], sw[4], cnt = 0;
         for (int q = 0; q < 4; ++q)
           if (w[q] > 0) {
-            sup[cnt] = vid[q];
+            loc[cnt] = q;
             sw[cnt] = w[q];
             ++cnt;
           }
         for (int a = 0; a < cnt; ++a)  // sort the support by vertex id
           for (int b = a + 1; b < cnt; ++b)
-            if (sup[b] < sup[a]) std::swap(sup[a], sup[b]), std::swap(sw[a], sw[b]);
-        if (cnt == 1) return sup[0];
-        if (cnt == 2) return NV + static_cast<long long>(edge_id.at({sup[0], sup[1]})) * (n - 1) + (sw[1] - 1);
+            if (vid[loc[b]] < vid[loc[a]]) std::swap(loc[a], loc[b]), std::swap(sw[a], sw[b]);
+        if (cnt == 1) return vid[loc[0]];
+        if (cnt == 2) return NV + static_cast<long long>(tet_edge[s][4 * loc[0] + loc[1]]) * (n - 1) + (sw[1] - 1);
         return NV + static_cast<long long>(nE) * (n - 1) +
-               static_cast<long long>(face_id.at({sup[0], sup[1], sup[2]})) * per_face +
+               static_cast<long long>(tet_face[s][6 - loc[0] - loc[1] - loc[2]]) * per_face +
                lattice_index(n - 3, sw[1] - 1, sw[2] - 1);
       };
       auto gcolor = [&](const int* vid, const int* w) {
@@ -261,7 +290,7 @@ Hierarchy3D Hierarchy3D::build(const Mesh3D& mesh, int max_level) {
             for (int i = 0; i <= n - k - j; ++i) {
               const int w[4] = {n - i - j - k, i, j, k};
               if (w[0] > 0 && i > 0 && j > 0 && k > 0) continue;
-              const int g = static_cast<int>(gid_of(vid, w));
+              const int g = static_cast<int>(gid_of(s, vid, w));
               node_g[static_cast<size_t>(s) * S + lattice_index3(n, i, j, k)] = g;
               ++cnt[g + 1];
             }
@@ -295,19 +324,16 @@ Hierarchy3D Hierarchy3D::build(const Mesh3D& mesh, int max_level) {
               lv.mem_idx[fill[g]] = lattice_index3(n, i, j, k);
               ++fill[g];
               // domain boundary: the node's support lies in a boundary face
-              int sup[4], c = 0;
+              int loc[4], c = 0;
               for (int q = 0; q < 4; ++q)
-                if (w[q] > 0) sup[c++] = vid[q];
-              for (int a = 0; a < c; ++a)  // sort the support (<= 3 ids)
-                for (int b2 = a + 1; b2 < c; ++b2)
-                  if (sup[b2] < sup[a]) std::swap(sup[a], sup[b2]);
+                if (w[q] > 0) loc[c++] = q;
               bool dom;
               if (c == 1)
-                dom = vbnd[sup[0]];
+                dom = vbnd[vid[loc[0]]];
               else if (c == 2)
-                dom = ebnd.count({sup[0], sup[1]}) > 0;
+                dom = tet_edge_bnd[s][4 * loc[0] + loc[1]] != 0;
               else
-                dom = face_use[face_id.at({sup[0], sup[1], sup[2]})] == 1;
+                dom = tet_face_use[s][6 - loc[0] - loc[1] - loc[2]] == 1;
               lv.grp_domain[g] = dom;
               lv.grp_color[g] = gcolor(vid, w);
               lv.node_flags[off] = static_cast<std::uint8_t>(1 | (dom ? 2 : 0) | (owner ? 4 : 0));
@@ -434,11 +460,11 @@ Hierarchy3D Hierarchy3D::build(const Mesh3D& mesh, int max_level) {
         std::vector<int> f2(lv.color_grp_ptr.begin(), lv.color_grp_ptr.end() - 1);
         for (long long g = 0; g < nG; ++g) lv.color_grp[f2[lv.grp_color[g]]++] = static_cast<int>(g);
       }
-      h.levels.push_back(std::move(lv));
-    }
+      h.levels[static_cast<std::size_t>(l)] = std::move(lv);
+    });
   } catch (const std::bad_alloc&) {
     Error e(KB_RESOURCE, "out of memory while building a 3-d hierarchy level");
-    e.level = static_cast<int>(h.levels.size());
+    e.level = max_level;
     throw e;
   }
   return h;
