@@ -1861,6 +1861,14 @@ bool estimate_cells() {
   return cells == 1;
 }
 
+// threads of a (macro, k-plane) block: the average plane of a level-n lattice
+// holds (n + 1)(n + 2) / 6 nodes (experiment: KB_PLANE_NT)
+int plane_threads(int n) {
+  static const int forced = getenv("KB_PLANE_NT") ? atoi(getenv("KB_PLANE_NT")) : 0;
+  if (forced) return forced;
+  return n >= 64 ? 256 : n >= 32 ? 128 : 64;
+}
+
 int blocks_for(long long count) { return static_cast<int>(std::max(1ll, (count + kT - 1) / kT)); }
 
 }  // namespace
@@ -1994,14 +2002,14 @@ int launch3_gs_count(const DevLevel3D& lv, int sweeps) {
 void launch3_prolong(const DevLevel3D& coarse, const DevLevel3D& fine, const double* c, double* f, int mode,
                      cudaStream_t st) {
   init_constants();
-  k3_prolong<<<fine.M * (fine.n + 1), kT, 0, st>>>(coarse, fine, c, f, mode);
+  k3_prolong<<<fine.M * (fine.n + 1), plane_threads(fine.n), 0, st>>>(coarse, fine, c, f, mode);
   check3("k3_prolong");
 }
 
 void launch3_restrict(const DevLevel3D& fine, const DevLevel3D& coarse, const double* rf, double* rc,
                       int zero_domain, cudaStream_t st) {
   init_constants();
-  k3_restrict<<<coarse.M * (coarse.n + 1), kT, 0, st>>>(fine, coarse, rf, rc);
+  k3_restrict<<<coarse.M * (coarse.n + 1), plane_threads(coarse.n), 0, st>>>(fine, coarse, rf, rc);
   check3("k3_restrict");
   launch3_sync_zero(coarse, rc, 1, zero_domain, st);
 }
@@ -2009,7 +2017,7 @@ void launch3_restrict(const DevLevel3D& fine, const DevLevel3D& coarse, const do
 void launch3_restrict_only(const DevLevel3D& fine, const DevLevel3D& coarse, const double* rf, double* rc,
                            cudaStream_t st) {
   init_constants();
-  k3_restrict<<<coarse.M * (coarse.n + 1), kT, 0, st>>>(fine, coarse, rf, rc);
+  k3_restrict<<<coarse.M * (coarse.n + 1), plane_threads(coarse.n), 0, st>>>(fine, coarse, rf, rc);
   check3("k3_restrict");
 }
 
