@@ -69,16 +69,17 @@ inline void parallel_levels(int lo, int hi, F fn) {
 
 // fn(i) for i = 0..count-1 on up to 16 host threads (contiguous chunks); the
 // first exception is rethrown on the caller's thread.  KB_HOST_THREADS=0 runs
-// the loop on the caller's thread.
+// the loop on the caller's thread, as does worth_threads = false (small loops:
+// spawning the threads costs more than they save).
 template <typename F>
-inline void parallel_for(int count, F fn) {
+inline void parallel_for(int count, F fn, bool worth_threads = true) {
   static const int nthreads = [] {
     const char* e = getenv("KB_HOST_THREADS");
     if (e) return std::max(1, atoi(e));
     const unsigned hw = std::thread::hardware_concurrency();
     return static_cast<int>(std::min(16u, std::max(1u, hw)));
   }();
-  const int T = std::min(nthreads, count);
+  const int T = worth_threads ? std::min(nthreads, count) : 1;
   if (T <= 1) {
     for (int i = 0; i < count; ++i) fn(i);
     return;

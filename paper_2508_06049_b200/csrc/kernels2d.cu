@@ -22,6 +22,14 @@
 
 #include "dev2d.hpp"
 
+// Measurement traces (per-step clock stamps, printf timelines) are compiled in
+// only with -DKB_GS_TRACE (Makefile NVDEFS); production kernels carry none.
+#ifdef KB_GS_TRACE
+#define KB_TRACING(x) (x)
+#else
+#define KB_TRACING(x) false
+#endif
+
 namespace kb {
 namespace {
 
@@ -1423,9 +1431,9 @@ __global__ void __launch_bounds__(kSchedMaxThreads, 1) k_gs_sched(DevLevel2D lv,
   const int tmax = (slot_bytes - 64) / 32;  // header loads stay inside the slot
   for (int g = 0; g < total; ++g) {
     const int slot = g & (K - 1);  // K is a power of two
-    if (trace && tid == 0 && g < 512) g_sched_trace[0][g] = clock64();
+    if (KB_TRACING(trace) && tid == 0 && g < 512) g_sched_trace[0][g] = clock64();
     mbar_wait(mbar_s + 8u * slot, static_cast<unsigned>((g >> kshift) & 1));
-    if (trace && tid == 0 && g < 512) g_sched_trace[1][g] = clock64();
+    if (KB_TRACING(trace) && tid == 0 && g < 512) g_sched_trace[1][g] = clock64();
     const unsigned blk = ring_s + static_cast<unsigned>(slot) * slot_bytes;
     // warp-uniform trip count: every lane reaches the member-sum shuffles; the
     // first header is loaded together with the count (slot 0 exists in every block)
@@ -1441,7 +1449,7 @@ __global__ void __launch_bounds__(kSchedMaxThreads, 1) k_gs_sched(DevLevel2D lv,
       const bool interior = h0.y >= 0;
       const int nm = (!act || interior) ? 0 : h0.w;  // group members (-1: domain boundary)
       const double B = ld_s64(sb_s + 8u * (act ? cell : 0));
-      if (trace && tid == 0 && g < 512) g_sched_trace[3][g] = clock64() + (cell == -12345 ? 1 : 0);
+      if (KB_TRACING(trace) && tid == 0 && g < 512) g_sched_trace[3][g] = clock64() + (cell == -12345 ? 1 : 0);
       double o = 0.0;
       if (q < nm) {
         // member q's partial_row (proj/src/fem.cpp:138-172 cell order, coefficients inline)
@@ -1461,7 +1469,7 @@ __global__ void __launch_bounds__(kSchedMaxThreads, 1) k_gs_sched(DevLevel2D lv,
 #pragma unroll
         for (int c = 0; c < 3; ++c) o = o + (k[2 * c] * x[2 * c] + k[2 * c + 1] * x[2 * c + 1]);
       }
-      if (trace && tid == 0 && g < 512) g_sched_trace[4][g] = clock64() + (o == 12345.0 ? 1 : 0);
+      if (KB_TRACING(trace) && tid == 0 && g < 512) g_sched_trace[4][g] = clock64() + (o == 12345.0 ? 1 : 0);
       // members summed in ascending slot; lanes beyond a group's members hold
       // +0.0, the bound is warp-uniform (the whole warp shuffles, converged)
       double ov[SG];
@@ -1470,7 +1478,7 @@ __global__ void __launch_bounds__(kSchedMaxThreads, 1) k_gs_sched(DevLevel2D lv,
       double off = 0.0;
 #pragma unroll
       for (int r = 0; r < SG; ++r) off = off + ov[r];
-      if (trace && tid == 0 && g < 512) g_sched_trace[5][g] = clock64() + (off == 12345.0 ? 1 : 0) + (nm << 20);
+      if (KB_TRACING(trace) && tid == 0 && g < 512) g_sched_trace[5][g] = clock64() + (off == 12345.0 ? 1 : 0) + (nm << 20);
       if (act && q == 0) {
         double res;
         if (interior) {
@@ -1506,7 +1514,7 @@ __global__ void __launch_bounds__(kSchedMaxThreads, 1) k_gs_sched(DevLevel2D lv,
         st_s64(su_s + 8u * cell, res);
       }
     }
-    if (trace && tid == 0 && g < 512) g_sched_trace[2][g] = clock64();
+    if (KB_TRACING(trace) && tid == 0 && g < 512) g_sched_trace[2][g] = clock64();
     __syncthreads();
     if (tid == producer && g + K < total) {
       const int lvl = (g + K) % levels;
@@ -1517,7 +1525,7 @@ __global__ void __launch_bounds__(kSchedMaxThreads, 1) k_gs_sched(DevLevel2D lv,
   }
   const size_t copies = static_cast<size_t>(M) * lv.S;
   for (size_t k = tid; k < copies; k += nthreads) u[k] = su[lv.sc_copy_cell[k]];
-  if (trace && tid == 0) {
+  if (KB_TRACING(trace) && tid == 0) {
     for (int g = 0; g < total && g < 40; ++g)
       printf("level %d: wait %lld hdr %lld member %lld sum %lld final %lld barrier+issue %lld nm %lld\n", g,
              g_sched_trace[1][g] - g_sched_trace[0][g], g_sched_trace[3][g] - g_sched_trace[1][g],
@@ -1699,14 +1707,14 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
           const int* pm = progress + e.x;
           int v;
           long long spins = 0;
-          if (trace & 1) ++n_wait, t_wait -= clock64();
+          if (KB_TRACING(trace & 1)) ++n_wait, t_wait -= clock64();
           while ((v = ld_acquire(pm)) < e.y) {
             if (++spins == (1ll << 24)) {  // a broken table would deadlock: fail loudly instead
               printf("k_gs_pipe: macro %d step %d waits for macro %d progress %d (has %d)\n", m, sl, e.x, e.y, v);
               __trap();
             }
           }
-          if (trace & 1) t_wait += clock64();
+          if (KB_TRACING(trace & 1)) t_wait += clock64();
           known[e.x & (kPipeKnown - 1)] = make_int2(e.x, v);
         }
       }
@@ -1726,7 +1734,7 @@ __global__ void __launch_bounds__(384, 1) k_gs_pipe(DevLevel2D lv, double* u, co
       PTR(11, st);
     }
     cp_async_wait<0>();
-    if ((trace & 1) && lane == 0 && (m % 20 == 0 || m == gridDim.x - 1))
+    if (KB_TRACING(trace & 1) && lane == 0 && (m % 20 == 0 || m == gridDim.x - 1))
       printf("pipe macro %d: steps %d, prefetch waits %d, cycles waiting %lld of %lld\n", m, total, n_wait, t_wait,
              clock64() - t_start);
   } else if (warp == Wc) {

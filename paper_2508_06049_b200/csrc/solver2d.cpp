@@ -422,7 +422,7 @@ void Solver2D::tabulate(const Problem2D& p) {
       for (int i = 0; i <= n; ++i) visit(i, 0);
       for (int j = 1; j <= n; ++j) visit(0, j);
       for (int j = 1; j <= n - 1; ++j) visit(n - j, j);
-    });
+    }, gbnd_count_[l] >= 20000);
     dst += gbnd_count_[l];
     if (ftab_count_[l]) {
       // f at the cell edge midpoints through the RHS map (proj/src/fem.cpp:183-194)
@@ -442,7 +442,7 @@ void Solver2D::tabulate(const Problem2D& p) {
             f[static_cast<size_t>(s) * SF + lattice_index(n2, I, J)] =
                 p.source(c0x + hi * ux + hj * wx, c0y + hi * uy + hj * wy);
           }
-      });
+      }, ftab_count_[l] >= 20000);
       dst += ftab_count_[l];
     }
   }
