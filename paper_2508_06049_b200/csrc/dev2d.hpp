@@ -132,7 +132,7 @@ struct DevStatus {
 void launch_apply(const DevLevel2D& lv, const double* K, const double* x, double* y, const double* b,
                   int mode, cudaStream_t st);
 void launch_restrict(const DevLevel2D& fine, const DevLevel2D& coarse, const double* r, double* rc,
-                     int zero_boundary, cudaStream_t st);
+                     int zero_boundary, cudaStream_t st, double* zero_out = nullptr);
 void launch_prolong(const DevLevel2D& coarse, const DevLevel2D& fine, const double* c, double* f,
                     double* next, const double* gbnd, int mode, cudaStream_t st);
 void launch_set_boundary(const DevLevel2D& lv, double* f, const double* gbnd, int zero_rest,

@@ -245,10 +245,11 @@ __device__ __forceinline__ double gather_restrict(const double* __restrict__ f,
 }
 
 __global__ void k_restrict(DevLevel2D fine, DevLevel2D coarse, const double* __restrict__ r, double* rc,
-                           int zero_boundary) {
+                           int zero_boundary, double* zero_out) {
   const int total = coarse.M * coarse.S;
   const int Sc = coarse.S, Sf = fine.S, nc = coarse.n, nf = fine.n;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < total; k += gridDim.x * blockDim.x) {
+    if (zero_out) zero_out[k] = 0.0;  // the V-cycle's zero initial guess on the coarse level (one launch less)
     const int slot = k / Sc;
     int I, J;
     decode(nc, k - slot * Sc, I, J);
@@ -2065,9 +2066,9 @@ void launch_apply(const DevLevel2D& lv, const double* K, const double* x, double
 }
 
 void launch_restrict(const DevLevel2D& fine, const DevLevel2D& coarse, const double* r, double* rc,
-                     int zero_boundary, cudaStream_t st) {
+                     int zero_boundary, cudaStream_t st, double* zero_out) {
   k_restrict<<<grid_for(static_cast<long long>(coarse.M) * coarse.S), kThreads, 0, st>>>(fine, coarse, r, rc,
-                                                                                         zero_boundary);
+                                                                                         zero_boundary, zero_out);
   check_launch("k_restrict");
 }
 

@@ -569,10 +569,9 @@ void Solver2D::vcycle(int l, double* u, const double* b) {
   }
   launch_apply(lev[l], lev[l].kstiff, u, r_[l], b, APPLY_RESIDUAL, stream_);
   mark(KK_RESIDUAL, 24.0 * dofs(l));
-  launch_restrict(lev[l], lev[l - 1], r_[l], vb_[l - 1], 1, stream_);
-  mark(KK_RESTRICT, 8.0 * dofs(l) + 8.0 * dofs(l - 1));
-  KB_CUDA_CHECK(cudaMemsetAsync(vu_[l - 1], 0, level_size(l - 1) * 8, stream_));
-  mark(KK_OTHER, 8.0 * dofs(l - 1), 0);  // memset, not a kernel
+  // the restriction also writes the coarse level's zero initial guess (no memset node)
+  launch_restrict(lev[l], lev[l - 1], r_[l], vb_[l - 1], 1, stream_, vu_[l - 1]);
+  mark(KK_RESTRICT, 8.0 * dofs(l) + 16.0 * dofs(l - 1));
   vcycle(l - 1, vu_[l - 1], vb_[l - 1]);
   launch_prolong(lev[l - 1], lev[l], vu_[l - 1], u, nullptr, nullptr, PROLONG_ADD, stream_);
   mark(KK_PROLONG, 16.0 * dofs(l) + 8.0 * dofs(l - 1));
