@@ -82,7 +82,7 @@ void launch3_prolong(const DevLevel3D& coarse, const DevLevel3D& fine, const dou
 // restriction of an owner-masked fine vector (A3_RES_OWNER residual), then
 // coarse additive sync; zero_domain: coarse domain-boundary copies 0
 void launch3_restrict(const DevLevel3D& fine, const DevLevel3D& coarse, const double* rf, double* rc,
-                      int zero_domain, cudaStream_t st);
+                      int zero_domain, cudaStream_t st, double* zero_out = nullptr);
 // the restriction alone over coarse.M macros (no sync; sharded levels)
 void launch3_restrict_only(const DevLevel3D& fine, const DevLevel3D& coarse, const double* rf, double* rc,
                            cudaStream_t st);

@@ -1102,7 +1102,7 @@ __global__ void __launch_bounds__(kT) k3_prolong(DevLevel3D cv, DevLevel3D fv, c
 // value at (2i, 2j, 2k) and half of each fine neighbour along the 14
 // directions, in direction order (the oracle's order)
 __global__ void __launch_bounds__(kT) k3_restrict(DevLevel3D fv, DevLevel3D cv, const double* __restrict__ rf,
-                                                  double* rc) {
+                                                  double* rc, double* zero_out) {
   const int nf = fv.n, nc = cv.n;
   const int m = blockIdx.x / (nc + 1), k = blockIdx.x - m * (nc + 1);
   const int m2 = nc - k;
@@ -1138,6 +1138,7 @@ __global__ void __launch_bounds__(kT) k3_restrict(DevLevel3D fv, DevLevel3D cv, 
       acc = acc + (d == 0 ? v : 0.5 * v);
     }
     rc[static_cast<size_t>(m) * cv.S + base + q] = acc;
+    if (zero_out) zero_out[static_cast<size_t>(m) * cv.S + base + q] = 0.0;  // the coarse zero initial guess
   }
 }
 
@@ -2007,9 +2008,9 @@ void launch3_prolong(const DevLevel3D& coarse, const DevLevel3D& fine, const dou
 }
 
 void launch3_restrict(const DevLevel3D& fine, const DevLevel3D& coarse, const double* rf, double* rc,
-                      int zero_domain, cudaStream_t st) {
+                      int zero_domain, cudaStream_t st, double* zero_out) {
   init_constants();
-  k3_restrict<<<coarse.M * (coarse.n + 1), plane_threads(coarse.n), 0, st>>>(fine, coarse, rf, rc);
+  k3_restrict<<<coarse.M * (coarse.n + 1), plane_threads(coarse.n), 0, st>>>(fine, coarse, rf, rc, zero_out);
   check3("k3_restrict");
   launch3_sync_zero(coarse, rc, 1, zero_domain, st);
 }
@@ -2017,7 +2018,7 @@ void launch3_restrict(const DevLevel3D& fine, const DevLevel3D& coarse, const do
 void launch3_restrict_only(const DevLevel3D& fine, const DevLevel3D& coarse, const double* rf, double* rc,
                            cudaStream_t st) {
   init_constants();
-  k3_restrict<<<coarse.M * (coarse.n + 1), plane_threads(coarse.n), 0, st>>>(fine, coarse, rf, rc);
+  k3_restrict<<<coarse.M * (coarse.n + 1), plane_threads(coarse.n), 0, st>>>(fine, coarse, rf, rc, nullptr);
   check3("k3_restrict");
 }
 

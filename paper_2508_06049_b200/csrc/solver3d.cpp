@@ -575,10 +575,9 @@ void Solver3D::vcycle(int l, double* u, const double* b) {
   }
   launch3_apply(lev[l], false, u, r_[l], b, A3_RES_OWNER, stream_);
   mark(KK_RESIDUAL, 24.0 * dofs(l), launch3_apply_count(lev[l]));
-  launch3_restrict(lev[l], lev[l - 1], r_[l], vb_[l - 1], 1, stream_);
-  mark(KK_RESTRICT, 8.0 * dofs(l) + 8.0 * dofs(l - 1), 2);
-  KB_CUDA_CHECK(cudaMemsetAsync(vu_[l - 1], 0, level_size(l - 1) * 8, stream_));
-  mark(KK_OTHER, 8.0 * dofs(l - 1), 0);
+  // the restriction also writes the coarse level's zero initial guess (no memset node)
+  launch3_restrict(lev[l], lev[l - 1], r_[l], vb_[l - 1], 1, stream_, vu_[l - 1]);
+  mark(KK_RESTRICT, 8.0 * dofs(l) + 16.0 * dofs(l - 1), 2);
   vcycle(l - 1, vu_[l - 1], vb_[l - 1]);
   launch3_prolong(lev[l - 1], lev[l], vu_[l - 1], u, P3_ADD, stream_);
   mark(KK_PROLONG, 16.0 * dofs(l) + 8.0 * dofs(l - 1));
