@@ -383,6 +383,7 @@ class GridHierarchy(_Handle):
         _check(fn(m.ptr, max_level, C.byref(out)))
         h = GridHierarchy(out.value)
         h.mesh = m
+        h.dim = int(mesh.dim)
         return h
 
     def _int(self, fn, *args):
@@ -425,9 +426,12 @@ class GridHierarchy(_Handle):
         return ptr, mem
 
     def element_matrices(self, l, kind=STIFFNESS):
+        """OperatorP1::matrices / stencil: 2-d (M, 18) up + down matrices and the
+        (M, 7) stencil; 3-d (M, 96) six micro-tet types of 4 x 4 and the (M, 15) stencil."""
         M = self.num_macros()
-        mats = np.zeros((M, 18))
-        st = np.zeros((M, 7))
+        three = getattr(self, "dim", 2) == 3
+        mats = np.zeros((M, 96 if three else 18))
+        st = np.zeros((M, 15 if three else 7))
         _check(lib().klref_hierarchy_element_matrices(self.ptr, l, kind, _dptr(mats), _dptr(st)))
         return mats, st
 

@@ -130,3 +130,42 @@ def _has_device():
         return rt.cuInit(0) == 0 and rt.cuDeviceGetCount(ctypes.byref(n)) == 0 and n.value > 0
     except OSError:
         return False
+
+
+def test_threaded_host_build_equals_serial():
+    """The per-level host tables are built on one thread per level (common.hpp
+    parallel_levels); KB_HOST_THREADS=0 builds them in order.  Both must give the
+    same groups and element matrices (2-d and 3-d)."""
+    import hashlib
+    import subprocess
+    import sys
+
+    code = r'''
+import hashlib, os, sys
+sys.path.insert(0, os.environ["KB_REPO"])
+import numpy as np
+from paper_2508_06049_b200 import klref as K
+from paper_2508_06049_b200.meshes import kuhn_cube
+hsh = hashlib.sha256()
+for mesh, L in ((K.MacroMesh.read(os.path.join(os.environ["KB_REPO"], "tests", "golden", "cfg2_k3.mesh")), 5), (kuhn_cube(2), 3)):
+    h = K.GridHierarchy.build(mesh, L, device=False)
+    for l in range(L + 1):
+        ptr, mem = h.groups(l)
+        hsh.update(np.ascontiguousarray(ptr).tobytes()); hsh.update(np.ascontiguousarray(mem).tobytes())
+        mats, st = h.element_matrices(l, K.STIFFNESS)
+        hsh.update(np.ascontiguousarray(mats).tobytes()); hsh.update(np.ascontiguousarray(st).tobytes())
+        hsh.update(str(h.dof_count(l)).encode())
+print(hsh.hexdigest())
+'''
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = []
+    for threads in ("0", None):
+        env = dict(os.environ, KB_REPO=repo)
+        if threads is not None:
+            env["KB_HOST_THREADS"] = threads
+        else:
+            env.pop("KB_HOST_THREADS", None)
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-500:]
+        out.append(r.stdout.strip())
+    assert out[0] == out[1] and len(out[0]) == 64
