@@ -2212,8 +2212,11 @@ void launch_gs(const DevHier2D& hd, const DevLevel2D& lv, double* u, const doubl
     if (smem > 0) {
       static int trace = getenv("KB_SCHED_TRACE") ? 1 : 0;
       const int SG = lv.sc_max_members[si] <= 4 ? 4 : lv.sc_max_members[si] <= 8 ? 8 : lv.sc_max_members[si] <= 16 ? 16 : 32;
+      // at most 512 threads: wider levels take a second pass, every level's block
+      // barrier is cheaper (cfg2 k = 5, level 3: 277 -> 264 us per 2-sweep call)
+      static const int cap = getenv("KB_SCHED_THREADS") ? atoi(getenv("KB_SCHED_THREADS")) : 512;
       const int threads = static_cast<int>(
-          std::min<long long>(kSchedMaxThreads, std::max<long long>(64, ((static_cast<long long>(lv.sc_max_width[si]) * SG + 31) / 32) * 32)));
+          std::min<long long>(cap, std::max<long long>(64, ((static_cast<long long>(lv.sc_max_width[si]) * SG + 31) / 32) * 32)));
       auto go = [&](auto kern) {
         set_smem(kern, smem);
         kern<<<1, threads, smem, st>>>(lv, u, b, si, reps, K, slot, trace);
