@@ -137,7 +137,9 @@ void Hierarchy2D::build_gs_schedules() {
     const std::size_t interior = copies - static_cast<std::size_t>(M) * 3 * n;
     const std::size_t nu = NG + interior;
     const std::size_t table = 16 * (nu + 1) + 8 * 26 * static_cast<std::size_t>(M) + 16 * NG;
-    if (table > kSchedTableBytes) return;
+    static const std::size_t table_max =
+        getenv("KB_SCHED_TABLE_KB") ? static_cast<std::size_t>(atoi(getenv("KB_SCHED_TABLE_KB"))) * 1024 : kSchedTableBytes;
+    if (table > table_max) return;
     lv.sc_nu = static_cast<int>(nu);
     lv.sc_copy_cell.assign(copies, -1);
     lv.sc_cell_copy.assign(nu, -1);

@@ -72,7 +72,7 @@ struct BNode {
 constexpr int kProgLaneWords = 16;                        // 128 bytes
 constexpr int kProgStepWords = 6 * kProgLaneWords;        // 3 node types x 2 members
 // shared-memory budget of the static schedule's resident tables (u, b, macro and group tables)
-constexpr std::size_t kSchedTableBytes = 160 * 1024;
+constexpr std::size_t kSchedTableBytes = 80 * 1024;  // end of round 2: above it the pipelined smoother is faster (sweep in DESIGN.md)
 constexpr int kSchedMemberWords = 20;
 
 // Exact-order Gauss-Seidel of a small level as a static schedule

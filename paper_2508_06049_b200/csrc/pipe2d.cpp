@@ -20,7 +20,7 @@ int min_pipe_n() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("KB_GS_PIPE_MIN_N");
-    v = e ? atoi(e) : 16;
+    v = e ? atoi(e) : 8;
   }
   return v;
 }
