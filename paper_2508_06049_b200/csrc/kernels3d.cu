@@ -1834,6 +1834,15 @@ bool gs_split() {
   return v == 1;
 }
 
+// largest n whose smoother runs whole (boundary colours and interior steps) in
+// one cooperative launch; above it the sweeps alternate the cooperative
+// boundary kernel with the plane-stream interior (experiment: KB_GS3_WHOLE_N)
+int gs_whole_n() {
+  // n = 16 split: 0.214 -> 0.174 ms per 2 sweeps on 384 macros, 0.335 -> 0.323 ms on 3072; n = 8 split is slower on 3072
+  static const int v = getenv("KB_GS3_WHOLE_N") ? atoi(getenv("KB_GS3_WHOLE_N")) : 8;
+  return std::min(v, 16);
+}
+
 // KB_GS3_PHASES (measurement only): 1 boundary phase, 2 interior phase, 3 both
 int gs_phases() {
   static int v = -1;
@@ -1970,7 +1979,7 @@ void launch3_gs(const DevLevel3D& lv, double* u, const double* b, int sweeps, cu
   if (const char* e = getenv("KB_GS3_G")) group = std::max(1, atoi(e));
   // levels with step lists (n <= 16) run whole in one launch; larger levels
   // alternate the boundary colours (cooperative) with the plane-stream interior
-  const bool whole = lv.n <= 16;
+  const bool whole = lv.n <= gs_whole_n();
   const int calls = whole ? 1 : sweeps;
   for (int s = 0; s < calls; ++s) {
     cudaLaunchConfig_t cfg{};
@@ -1997,7 +2006,7 @@ int launch3_gs_count(const DevLevel3D& lv, int sweeps) {
   if (sweeps <= 0) return 0;
   const int interior = lv.n >= 4 ? 1 : 0;
   if (gs_split()) return sweeps * (lv.colors + interior);
-  return lv.n <= 16 ? 1 : sweeps * (1 + interior);
+  return lv.n <= gs_whole_n() ? 1 : sweeps * (1 + interior);
 }
 
 void launch3_prolong(const DevLevel3D& coarse, const DevLevel3D& fine, const double* c, double* f, int mode,
