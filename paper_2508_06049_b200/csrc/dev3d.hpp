@@ -25,6 +25,7 @@ struct DevLevel3D {
   const int* color_grp_ptr;    // boundary groups by colour
   const int* color_grp;         // per colour: wide groups (> 4 members) first
   const int* color_wide_end;    // per colour: end of its wide groups in color_grp
+  int max_color_groups;         // largest colour (groups): sizes the cooperative smoother's grid
   // flat records of the groups at their position t in color_grp: header
   // (diagonal lo, hi, members | domain << 16, first member in wide_mem) and, for
   // narrow groups (<= 4 members), four member slots (macro slot, i | j << 10 |

@@ -1970,8 +1970,16 @@ void launch3_gs(const DevLevel3D& lv, double* u, const double* b, int sweeps, cu
     KB_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k3_gs_sweeps<256, 3>, 256, 0));
     if (occ < 1) fail(KB_CUDA, "k3_gs_sweeps cannot be resident");
   }
+  // grid by the largest colour phase: lanes of its groups / 256, in whole
+  // multiples of the SM count, at least one CTA per SM (fewer CTAs: cheaper grid
+  // barriers; 384 macros at n = 8: 0.141 -> 0.110 ms per 2 sweeps with 148 CTAs)
   int grid = occ * sms;
-  if (lv.n <= 4) grid = std::min(grid, sms);  // tiny levels: one CTA per SM (cheaper grid barriers)
+  if (lv.max_color_groups > 0) {
+    const long long lanes = static_cast<long long>(lv.max_color_groups) * (lv.n <= 8 ? 4 : 2);
+    const int want = static_cast<int>((lanes + 255) / 256);
+    grid = std::min(grid, std::max(sms, (want + sms - 1) / sms * sms));
+  }
+  if (lv.n <= 4) grid = std::min(grid, sms);  // tiny levels: one CTA per SM
   if (const char* e = getenv("KB_GS3_GRID")) grid = std::max(1, std::min(grid, atoi(e)));
   int active = grid;
   if (const char* e = getenv("KB_GS3_ACTIVE")) active = std::max(1, std::min(grid, atoi(e)));

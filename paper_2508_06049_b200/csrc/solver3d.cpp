@@ -162,6 +162,9 @@ std::unique_ptr<DeviceHierarchy3D> DeviceHierarchy3D::create(const Mesh3D& mesh,
       }
       dl.color_grp = d->arena.upload(cg);
       dl.color_wide_end = d->arena.upload(wide_end);
+      dl.max_color_groups = 0;
+      for (int c = 0; c < h.colors; ++c)
+        dl.max_color_groups = std::max(dl.max_color_groups, lv.color_grp_ptr[c + 1] - lv.color_grp_ptr[c]);
       // flat records of the groups at their colour-list position
       std::vector<int4> hdr(cg.size(), make_int4(0, 0, 0, 0));
       std::vector<int2> mem(4 * cg.size(), make_int2(-1, 0)), wide;

@@ -93,6 +93,7 @@ ShardedSolver3D::ShardedSolver3D(std::shared_ptr<DeviceHierarchy3D> h, Problem3D
         dl.color_grp = sh.tables.upload(s.color_grp);
         dl.color_wide_end = sh.tables.upload(s.color_wide_end);
         dl.nar_hdr = nullptr;  // shard tables: the chained group tables
+        dl.max_color_groups = 0;
         dl.nar_mem = nullptr;
         dl.wide_mem = nullptr;
         // per-macro tables of the full hierarchy, from this shard's first slot
